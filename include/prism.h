@@ -1,0 +1,174 @@
+/*
+ * prism.h — C ABI of the B200-native PRISM Newton–Schulz library (libprism.so).
+ *
+ * PRISM (arXiv 2601.22137, /root/reference/PAPER.md = "P:<line>") computes
+ * matrix functions by a Newton–Schulz iteration whose top polynomial
+ * coefficient alpha_k is refitted every step from a Gaussian-sketched residual
+ * (eq. (4); Appendix A.1).  This library runs that
+ * iteration for batches of matrices on one sm_100a GPU:
+ *   prism_polar          polar factor U V^T of A = U S V^T (Table 1
+ *                        rows P:252-254) — Muon orthogonalisation;
+ *   prism_sqrt_invsqrt   A^{1/2} and A^{-1/2} of SPD A (Theorem 3
+ *                        P:273-275) — Shampoo preconditioners.
+ *
+ * Conventions (all entry points):
+ *   - Matrices are dense, row-major, addressed by a device pointer and a
+ *     leading dimension in ELEMENTS.  Element type follows the precision:
+ *     PRISM_BF16 -> __nv_bfloat16 (2 bytes); PRISM_FP32 / PRISM_TF32 -> float.
+ *   - Arrays of per-matrix pointers / sizes (A, lda, m, n, ...) are HOST arrays
+ *     of length `batch`; the pointers they hold are DEVICE pointers.
+ *   - Ownership: the caller owns every device buffer (inputs, outputs, report,
+ *     workspace).  The library never allocates device memory; the handle owns
+ *     only host-side pinned staging and cached plans.
+ *   - Asynchrony: work is enqueued on `stream` (a cudaStream_t, may be NULL for
+ *     the legacy default stream) and the call returns without synchronising.
+ *     Outputs and the report are valid after the caller synchronises the stream.
+ *   - The workspace must not be used by anything else until the stream has
+ *     finished the call; it holds the solver state and the per-call tables.
+ *   - Errors: argument errors are detected on the host before any launch and
+ *     return a non-zero prism_status; prism_last_error() describes the last
+ *     failure of the calling thread.  No C++ exception crosses the ABI.
+ *     Numerical outcomes are per-matrix report status values, not call errors.
+ *   - Thread safety: a handle may be used by one host thread at a time.
+ */
+#ifndef PRISM_H_
+#define PRISM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PRISM_VERSION_MAJOR 0
+#define PRISM_VERSION_MINOR 1
+
+typedef struct prism_handle_s* prism_handle;
+
+typedef enum {
+  PRISM_OK = 0,
+  PRISM_ERR_INVALID_ARG = 1, /* null pointer, bad size/option, workspace too small */
+  PRISM_ERR_UNSUPPORTED = 2, /* valid but not supported (e.g. sketch_size > 8, fit exact on device) */
+  PRISM_ERR_CUDA = 3,        /* a CUDA runtime/driver call failed */
+  PRISM_ERR_INTERNAL = 4
+} prism_status;
+
+typedef enum {
+  PRISM_BF16 = 0, /* bf16 storage, bf16 tcgen05 MMA (kind::f16), fp32 accumulate */
+  PRISM_FP32 = 1, /* fp32 storage, 3xTF32 tcgen05 MMA (hi*hi + hi*lo + lo*hi), fp32 accumulate */
+  PRISM_TF32 = 2  /* fp32 storage, 1xTF32 tcgen05 MMA */
+} prism_precision;
+
+typedef enum {
+  PRISM_FIT_SKETCHED = 0, /* alpha_k from the sketched quartic, eq. (4) */
+  PRISM_FIT_TAYLOR = 1    /* alpha_k = Taylor coefficient: classical Newton–Schulz */
+} prism_fit;
+
+typedef enum {
+  PRISM_CONVERGED = 0,  /* ||I - G_k||_F <= tol * sqrt(s) before an update */
+  PRISM_MAX_ITERS = 1,  /* max_iters updates applied without converging */
+  PRISM_DIVERGED = 2,   /* ||R_k||_F increased 5 times in a row (R12) */
+  PRISM_NONFINITE = 3,  /* NaN / Inf residual */
+  PRISM_ZERO_INPUT = 4  /* ||A||_F = 0: output is zero */
+} prism_solve_status;
+
+typedef struct {
+  int degree;          /* 3 ("PRISM-3", d=1: g = I + aR) or 5 ("PRISM-5", d=2: g = I + R/2 + aR^2) */
+  int max_iters;       /* >= 1: maximum number of updates */
+  int sketch_size;     /* p, rows of the Gaussian sketch S_k, 1 <= p <= 8 ("as small as 5"); default 8 */
+  double tol;          /* > 0: stop before the update when ||R_k||_F <= tol * sqrt(s) (R12) */
+  uint64_t seed;       /* Philox key; S_k depends only on (seed, matrix id, k) (R8) */
+  int precision;       /* prism_precision */
+  int fit;             /* prism_fit */
+  int warmup_iters;    /* alpha_k = u for k < warmup_iters; 0 for the paper's eq. (4) everywhere */
+  double alpha_lo;     /* interval [l, u] for alpha; NaN -> paper default */
+  double alpha_hi;     /*   [1/2, 1] for degree 3, [3/8, 29/20] for degree 5 */
+} prism_options;
+
+/* Per-matrix results, DEVICE pointers (any may be NULL), written on `stream`. */
+typedef struct {
+  int32_t* iters;      /* [batch] updates applied */
+  float* resid;        /* [batch] final ||R||_F / sqrt(s) */
+  int32_t* status;     /* [batch] prism_solve_status */
+  double* alphas;      /* [batch * max_iters] alpha_k history (row b, column k), or NULL */
+  float* resid_hist;   /* [batch * (max_iters + 1)] ||R_k||_F / sqrt(s), or NULL */
+} prism_report;
+
+/* Fill `o` with defaults: degree 5, max_iters 30, p 8, tol 1e-6, seed 42, BF16, sketched, no warmup. */
+void prism_default_options(prism_options* o);
+
+prism_status prism_create(prism_handle* h);
+prism_status prism_destroy(prism_handle h);
+/* Message for the last failing call made by this thread (never NULL). */
+const char* prism_last_error(void);
+/* Number of exported entry points and their names (for ABI checks). */
+int prism_abi_version(void);
+
+/*
+ * Polar factor.  For matrix i of the batch: A_i is m[i] x n[i] (row-major, lda[i]),
+ * Q_i receives U V^T with the same shape (ldq[i]; Q may alias A).  Wide inputs
+ * (m < n) are handled as A^T (P:456 assumes m >= n; R14).
+ * matrix_ids: optional HOST array of global matrix indices used as the sketch
+ * stream id (so a batch split across GPUs draws the same S_k); NULL -> 0..batch-1.
+ * Workspace: at least prism_polar_workspace(...) bytes of device memory, 256-B aligned.
+ */
+size_t prism_polar_workspace(prism_handle h, int batch, const int64_t* m, const int64_t* n,
+                             const prism_options* o);
+prism_status prism_polar(prism_handle h, int batch, const int64_t* m, const int64_t* n,
+                         const void* const* A, const int64_t* lda, void* const* Q, const int64_t* ldq,
+                         const int64_t* matrix_ids, const prism_options* o, const prism_report* rep,
+                         void* workspace, size_t ws_bytes, void* stream);
+
+/*
+ * Coupled square root / inverse square root of SPD n[i] x n[i] matrices
+ * (symmetry is the caller's contract; a non-SPD input shows up as a
+ * DIVERGED / NONFINITE / MAX_ITERS status).  Asqrt / Ainvsqrt: either array,
+ * or any entry, may be NULL.  Output leading dimension ld_out[i].
+ */
+size_t prism_sqrt_workspace(prism_handle h, int batch, const int64_t* n, const prism_options* o);
+prism_status prism_sqrt_invsqrt(prism_handle h, int batch, const int64_t* n, const void* const* A,
+                                const int64_t* lda, void* const* Asqrt, void* const* Ainvsqrt,
+                                const int64_t* ld_out, const int64_t* matrix_ids, const prism_options* o,
+                                const prism_report* rep, void* workspace, size_t ws_bytes, void* stream);
+
+/*
+ * LPT partition: assign `batch` matrices with costs cost[i]
+ * (e.g. F_min x expected iterations) to `ranks` ranks, largest first to the
+ * least-loaded rank, ties by lower index / lower rank.  Writes owner[i] in
+ * [0, ranks).  Deterministic: every rank computes the same plan.  Host only.
+ */
+prism_status prism_lpt_partition(int batch, const double* cost, int ranks, int32_t* owner);
+
+/* Per-iteration F_min (symmetric products counted once) of a polar solve. */
+double prism_polar_flops_per_iter(int64_t m, int64_t n, int degree, int sketch_size);
+/* Dense-GEMM flop count per sqrt iteration (general products). */
+double prism_sqrt_flops_per_iter(int64_t n, int degree, int sketch_size);
+
+/* ---- test hooks (exercised by tests/test_gpu_*.py) ---------------------------- */
+
+/*
+ * One grouped tcgen05 GEMM problem: out = epilogue(A * B) with A (M x K, row-major,
+ * lda) and B either K-major (b_mn = 0: B stored N x K, ldb, i.e. out = A B^T) or
+ * MN-major (b_mn = 1: B stored K x N).  mode: 0 RESID (I - D, with per-tile
+ * sum of squares into norm_part[tiles_m*tiles_n] and diag(D) into gdiag),
+ * 1 POLY (c1*C + alpha*D), 2 APPLY (C + (scale_by_alpha ? alpha : 1)*D), 3 STORE.
+ * sym: triangle schedule + mirrored stores (requires M == N).  FP32 precision
+ * (3xTF32) takes the lo planes A_lo, B_lo, C_lo, out_lo (hi planes pre-truncated).
+ * alpha_dev: device double.  Leading dimensions must be multiples of 16 bytes.
+ */
+prism_status prism_debug_gemm(prism_handle h, int precision, int b_mn, int mode, int sym, int M, int N, int K,
+                              const void* A, const void* A_lo, int64_t lda, const void* B, const void* B_lo,
+                              int64_t ldb, const void* C, const void* C_lo, int64_t ldc, void* out,
+                              void* out_lo, int64_t ldo, const double* alpha_dev, float c1, int scale_by_alpha,
+                              float* norm_part, float* gdiag, void* workspace, size_t ws_bytes, void* stream);
+/* S_k for (seed, matrix id b, iteration k): p x s floats into S_dev (R8). */
+prism_status prism_debug_sketch(uint64_t seed, int64_t b, int k, int p, int s, float* S_dev, void* stream);
+/* Device quartic argmin on [lo, hi] (R15/R16): n problems, c_dev[5*n] -> alpha_dev[n]. */
+prism_status prism_debug_argmin(int n, const double* c_dev, double lo, double hi, double a_taylor,
+                                double* alpha_dev, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PRISM_H_ */

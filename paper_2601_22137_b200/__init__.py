@@ -1,12 +1,14 @@
 """paper_2601_22137_b200 — B200-native PRISM Newton–Schulz (arXiv 2601.22137).
 
-Thin Python binding over the C-ABI library ``libprism.so`` (include/prism.h).
-The library is loaded lazily; every compute entry point fails loudly if it is
-missing (there is no CPU fallback).
+Thin Python binding over the C-ABI library ``_lib/libprism.so``
+(``include/prism.h``).  The library is loaded lazily; every compute entry
+point raises if it is missing (there is no CPU fallback).
 """
 
 from .binding import (  # noqa: F401
-    PrismError, Options, lib, polar, sqrt_invsqrt, PRECISION, FIT, STATUS,
+    FIT, PRECISION, STATUS, Handle, PrismError, default_handle, lib, lpt_partition, make_options, polar,
+    polar_flops_per_iter, sqrt_flops_per_iter, sqrt_invsqrt,
 )
 
-__all__ = ["PrismError", "Options", "lib", "polar", "sqrt_invsqrt", "PRECISION", "FIT", "STATUS"]
+__all__ = ["FIT", "PRECISION", "STATUS", "Handle", "PrismError", "default_handle", "lib", "lpt_partition",
+           "make_options", "polar", "polar_flops_per_iter", "sqrt_flops_per_iter", "sqrt_invsqrt"]

@@ -1,5 +1,297 @@
-"""placeholder; replaced by the ctypes binding."""
+"""ctypes binding of libprism.so (include/prism.h).
+
+Argument marshalling only: torch is used for device memory (outputs,
+workspace, report buffers) and streams; every step of the PRISM iteration
+runs in the library's CUDA kernels.  If the library is missing the calls
+raise — there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libprism.so")
+
+PRECISION = {"bf16": 0, "fp32": 1, "tf32": 2}
+FIT = {"sketched": 0, "taylor": 1}
+STATUS = {0: "converged", 1: "max_iters", 2: "diverged", 3: "nonfinite", 4: "zero_input"}
+
+c_i64p = ctypes.POINTER(ctypes.c_int64)
+
+
 class PrismError(RuntimeError):
     pass
-Options = lib = polar = sqrt_invsqrt = None
-PRECISION = FIT = STATUS = {}
+
+
+class Options(ctypes.Structure):
+    _fields_ = [
+        ("degree", ctypes.c_int),
+        ("max_iters", ctypes.c_int),
+        ("sketch_size", ctypes.c_int),
+        ("tol", ctypes.c_double),
+        ("seed", ctypes.c_uint64),
+        ("precision", ctypes.c_int),
+        ("fit", ctypes.c_int),
+        ("warmup_iters", ctypes.c_int),
+        ("alpha_lo", ctypes.c_double),
+        ("alpha_hi", ctypes.c_double),
+    ]
+
+
+class Report(ctypes.Structure):
+    _fields_ = [
+        ("iters", ctypes.c_void_p),
+        ("resid", ctypes.c_void_p),
+        ("status", ctypes.c_void_p),
+        ("alphas", ctypes.c_void_p),
+        ("resid_hist", ctypes.c_void_p),
+    ]
+
+
+EXPORTS = [
+    "prism_default_options", "prism_create", "prism_destroy", "prism_last_error", "prism_abi_version",
+    "prism_polar_workspace", "prism_polar", "prism_sqrt_workspace", "prism_sqrt_invsqrt",
+    "prism_lpt_partition", "prism_polar_flops_per_iter", "prism_sqrt_flops_per_iter",
+    "prism_debug_gemm", "prism_debug_sketch", "prism_debug_argmin",
+]
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib():
+    """Load libprism.so once and declare the C signatures."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise PrismError(f"{LIB_PATH} not built (run `python build.py`); no CPU fallback exists")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i32, i64, dbl, u64, sz = (ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double,
+                                      ctypes.c_uint64, ctypes.c_size_t)
+        L.prism_default_options.argtypes = [ctypes.POINTER(Options)]
+        L.prism_default_options.restype = None
+        L.prism_create.argtypes = [ctypes.POINTER(vp)]
+        L.prism_destroy.argtypes = [vp]
+        L.prism_last_error.restype = ctypes.c_char_p
+        L.prism_abi_version.restype = i32
+        L.prism_polar_workspace.argtypes = [vp, i32, c_i64p, c_i64p, ctypes.POINTER(Options)]
+        L.prism_polar_workspace.restype = sz
+        L.prism_polar.argtypes = [vp, i32, c_i64p, c_i64p, ctypes.POINTER(vp), c_i64p, ctypes.POINTER(vp), c_i64p,
+                                  c_i64p, ctypes.POINTER(Options), ctypes.POINTER(Report), vp, sz, vp]
+        L.prism_sqrt_workspace.argtypes = [vp, i32, c_i64p, ctypes.POINTER(Options)]
+        L.prism_sqrt_workspace.restype = sz
+        L.prism_sqrt_invsqrt.argtypes = [vp, i32, c_i64p, ctypes.POINTER(vp), c_i64p, ctypes.POINTER(vp),
+                                         ctypes.POINTER(vp), c_i64p, c_i64p, ctypes.POINTER(Options),
+                                         ctypes.POINTER(Report), vp, sz, vp]
+        L.prism_lpt_partition.argtypes = [i32, ctypes.POINTER(dbl), i32, ctypes.POINTER(ctypes.c_int32)]
+        L.prism_polar_flops_per_iter.argtypes = [i64, i64, i32, i32]
+        L.prism_polar_flops_per_iter.restype = dbl
+        L.prism_sqrt_flops_per_iter.argtypes = [i64, i32, i32]
+        L.prism_sqrt_flops_per_iter.restype = dbl
+        L.prism_debug_gemm.argtypes = [vp, i32, i32, i32, i32, i32, i32, i32, vp, vp, i64, vp, vp, i64, vp, vp, i64,
+                                       vp, vp, i64, vp, ctypes.c_float, i32, vp, vp, vp, sz, vp]
+        L.prism_debug_sketch.argtypes = [u64, i64, i32, i32, i32, vp, vp]
+        L.prism_debug_argmin.argtypes = [i32, vp, dbl, dbl, dbl, vp, vp]
+        for name in ("prism_create", "prism_destroy", "prism_polar", "prism_sqrt_invsqrt", "prism_lpt_partition",
+                     "prism_debug_gemm", "prism_debug_sketch", "prism_debug_argmin"):
+            getattr(L, name).restype = i32
+        _lib = L
+        return L
+
+
+def check(status: int, what: str):
+    if status != 0:
+        msg = lib().prism_last_error().decode(errors="replace")
+        raise PrismError(f"{what} failed (status {status}): {msg}")
+
+
+def _i64(vals):
+    return (ctypes.c_int64 * len(vals))(*[int(v) for v in vals])
+
+
+def _ptrs(ts):
+    return (ctypes.c_void_p * len(ts))(*[(t.data_ptr() if t is not None else None) for t in ts])
+
+
+class Handle:
+    """A prism_handle plus a reusable device workspace (per device)."""
+
+    def __init__(self):
+        h = ctypes.c_void_p()
+        check(lib().prism_create(ctypes.byref(h)), "prism_create")
+        self.h = h
+        self._ws = {}
+
+    def __del__(self):
+        try:
+            if self.h and _lib is not None:
+                _lib.prism_destroy(self.h)
+        except Exception:
+            pass
+
+    def workspace(self, nbytes: int, device):
+        import torch
+        key = str(device)
+        ws = self._ws.get(key)
+        if ws is None or ws.numel() < nbytes:
+            ws = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
+            self._ws[key] = ws
+        return ws
+
+
+_default = None
+
+
+def default_handle() -> Handle:
+    global _default
+    if _default is None:
+        _default = Handle()
+    return _default
+
+
+def make_options(degree=5, max_iters=30, sketch_size=8, tol=1e-6, seed=42, precision="bf16", fit="sketched",
+                 warmup_iters=0, alpha_lo=None, alpha_hi=None) -> Options:
+    o = Options()
+    lib().prism_default_options(ctypes.byref(o))
+    o.degree = int(degree)
+    o.max_iters = int(max_iters)
+    o.sketch_size = int(sketch_size)
+    o.tol = float(tol)
+    o.seed = int(seed) & 0xFFFFFFFFFFFFFFFF
+    o.precision = PRECISION[precision] if isinstance(precision, str) else int(precision)
+    o.fit = FIT[fit] if isinstance(fit, str) else int(fit)
+    o.warmup_iters = int(warmup_iters)
+    o.alpha_lo = math.nan if alpha_lo is None else float(alpha_lo)
+    o.alpha_hi = math.nan if alpha_hi is None else float(alpha_hi)
+    return o
+
+
+def _precision_of(t, precision):
+    import torch
+    if precision is not None:
+        return precision
+    return "bf16" if t.dtype == torch.bfloat16 else "fp32"
+
+
+def _check_dtype(ts, precision):
+    import torch
+    want = torch.bfloat16 if precision == "bf16" else torch.float32
+    for t in ts:
+        if t.dtype != want or not t.is_cuda or t.dim() != 2 or t.stride(1) != 1:
+            raise PrismError(f"inputs must be 2-D CUDA {want} tensors with unit column stride")
+
+
+def _report_buffers(batch, max_iters, device):
+    import torch
+    return {
+        "iters": torch.zeros(batch, dtype=torch.int32, device=device),
+        "resid": torch.zeros(batch, dtype=torch.float32, device=device),
+        "status": torch.full((batch,), -1, dtype=torch.int32, device=device),
+        "alphas": torch.full((batch, max_iters), float("nan"), dtype=torch.float64, device=device),
+        "resid_hist": torch.full((batch, max_iters + 1), float("nan"), dtype=torch.float32, device=device),
+    }
+
+
+def _report_struct(rb):
+    r = Report()
+    r.iters = rb["iters"].data_ptr()
+    r.resid = rb["resid"].data_ptr()
+    r.status = rb["status"].data_ptr()
+    r.alphas = rb["alphas"].data_ptr()
+    r.resid_hist = rb["resid_hist"].data_ptr()
+    return r
+
+
+def polar(mats, degree=5, max_iters=30, sketch_size=8, tol=1e-6, seed=42, precision=None, fit="sketched",
+          warmup_iters=0, alpha_lo=None, alpha_hi=None, out=None, matrix_ids=None, stream=None, handle=None):
+    """Polar factors of a batch of CUDA matrices via prism_polar.
+
+    Returns (outputs, report) where report holds device tensors iters, resid,
+    status, alphas [batch, max_iters], resid_hist [batch, max_iters+1].
+    Asynchronous on `stream` (default: torch's current stream).
+    """
+    import torch
+    mats = list(mats)
+    if not mats:
+        return [], {}
+    precision = _precision_of(mats[0], precision)
+    _check_dtype(mats, precision)
+    dev = mats[0].device
+    h = handle or default_handle()
+    o = make_options(degree, max_iters, sketch_size, tol, seed, precision, fit, warmup_iters, alpha_lo, alpha_hi)
+    B = len(mats)
+    m = _i64([t.shape[0] for t in mats])
+    n = _i64([t.shape[1] for t in mats])
+    if out is None:
+        out = [torch.empty_like(t) for t in mats]
+    _check_dtype(out, precision)
+    need = lib().prism_polar_workspace(h.h, B, m, n, ctypes.byref(o))
+    if need == 0:
+        raise PrismError("prism_polar_workspace rejected the arguments: " + lib().prism_last_error().decode())
+    ws = h.workspace(need, dev)
+    rb = _report_buffers(B, max_iters, dev)
+    rep = _report_struct(rb)
+    ids = _i64(matrix_ids) if matrix_ids is not None else None
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    check(lib().prism_polar(h.h, B, m, n, _ptrs(mats), _i64([t.stride(0) for t in mats]), _ptrs(out),
+                            _i64([t.stride(0) for t in out]), ids, ctypes.byref(o), ctypes.byref(rep),
+                            ws.data_ptr(), ws.numel(), ctypes.c_void_p(st.cuda_stream)), "prism_polar")
+    return out, rb
+
+
+def sqrt_invsqrt(mats, degree=5, max_iters=30, sketch_size=8, tol=1e-6, seed=42, precision=None, fit="sketched",
+                 warmup_iters=0, alpha_lo=None, alpha_hi=None, want_sqrt=True, want_invsqrt=True, matrix_ids=None,
+                 stream=None, handle=None):
+    """A^{1/2}, A^{-1/2} of a batch of SPD CUDA matrices via prism_sqrt_invsqrt."""
+    import torch
+    mats = list(mats)
+    if not mats:
+        return [], [], {}
+    precision = _precision_of(mats[0], precision)
+    _check_dtype(mats, precision)
+    dev = mats[0].device
+    h = handle or default_handle()
+    o = make_options(degree, max_iters, sketch_size, tol, seed, precision, fit, warmup_iters, alpha_lo, alpha_hi)
+    B = len(mats)
+    n = _i64([t.shape[0] for t in mats])
+    sq = [torch.empty_like(t) for t in mats] if want_sqrt else None
+    isq = [torch.empty_like(t) for t in mats] if want_invsqrt else None
+    ld_out = _i64([t.shape[1] for t in mats])
+    need = lib().prism_sqrt_workspace(h.h, B, n, ctypes.byref(o))
+    if need == 0:
+        raise PrismError("prism_sqrt_workspace rejected the arguments: " + lib().prism_last_error().decode())
+    ws = h.workspace(need, dev)
+    rb = _report_buffers(B, max_iters, dev)
+    rep = _report_struct(rb)
+    ids = _i64(matrix_ids) if matrix_ids is not None else None
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    check(lib().prism_sqrt_invsqrt(h.h, B, n, _ptrs(mats), _i64([t.stride(0) for t in mats]),
+                                   _ptrs(sq) if sq else None, _ptrs(isq) if isq else None, ld_out, ids,
+                                   ctypes.byref(o), ctypes.byref(rep), ws.data_ptr(), ws.numel(),
+                                   ctypes.c_void_p(st.cuda_stream)), "prism_sqrt_invsqrt")
+    return sq, isq, rb
+
+
+def lpt_partition(costs, ranks: int):
+    """Deterministic LPT assignment (prism_lpt_partition): owner rank per matrix."""
+    B = len(costs)
+    c = (ctypes.c_double * B)(*[float(x) for x in costs])
+    own = (ctypes.c_int32 * B)()
+    check(lib().prism_lpt_partition(B, c, int(ranks), own), "prism_lpt_partition")
+    return list(own)
+
+
+def polar_flops_per_iter(m, n, degree=5, sketch_size=8) -> float:
+    return float(lib().prism_polar_flops_per_iter(int(m), int(n), int(degree), int(sketch_size)))
+
+
+def sqrt_flops_per_iter(n, degree=5, sketch_size=8) -> float:
+    return float(lib().prism_sqrt_flops_per_iter(int(n), int(degree), int(sketch_size)))

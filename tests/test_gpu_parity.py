@@ -1,0 +1,167 @@
+"""End-to-end parity of the CUDA path (through the C ABI) with the fp64 oracle.
+
+Bounds (BASELINE.json north_star, refined per input class in SURVEY §8(c)):
+relative Frobenius error <= 1e-5 in FP32 (3xTF32) mode and <= 2e-2 in BF16
+mode, iteration count to tolerance within +-1.  Inputs are the exact values
+stored in the device dtype, read back as fp64 for the oracle.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2601_22137_b200 as P
+from oracle import prism
+from paper_2601_22137_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+DT = {"bf16": torch.bfloat16, "fp32": torch.float32, "tf32": torch.float32}
+
+
+def _dev(A, prec):
+    t = torch.tensor(A).to(DT[prec]).cuda()
+    return t, t.double().cpu().numpy()
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def _polar_pair(A, prec, deg, tol, max_iters=30, seed=42, warmup=0, fit="sketched"):
+    At, Aq = _dev(A, prec)
+    Q, rep = P.polar([At], degree=deg, max_iters=max_iters, tol=tol, seed=seed, precision=prec,
+                     warmup_iters=warmup, fit=fit)
+    torch.cuda.synchronize()
+    Qo, ro = prism.polar(Aq, d=1 if deg == 3 else 2, p=8, tol=tol, max_iters=max_iters, seed=seed,
+                         warmup=warmup, fit=fit)
+    return Q[0].double().cpu().numpy(), {k: v[0].cpu().numpy() for k, v in rep.items()}, Qo, ro
+
+
+@pytest.mark.parametrize("shape", [(256, 128), (128, 256), (300, 200), (1000, 700), (520, 520)])
+@pytest.mark.parametrize("deg", [3, 5])
+def test_polar_fp32_parity(shape, deg):
+    A = W.gaussian(*shape, seed=shape[0] + deg)
+    Q, rep, Qo, ro = _polar_pair(A, "fp32", deg, tol=1e-5)
+    assert int(rep["status"]) == prism.CONVERGED and ro.status == prism.CONVERGED
+    assert abs(int(rep["iters"]) - ro.iters) <= 1
+    assert _rel(Q, Qo) <= 1e-5
+    n = min(len(ro.alphas), int(rep["iters"]))
+    assert np.max(np.abs(rep["alphas"][:n] - np.array(ro.alphas[:n]))) <= 1e-3
+
+
+@pytest.mark.parametrize("kind", ["htmp", "logspaced"])
+def test_polar_fp32_parity_spectra(kind):
+    A = W.htmp(600, 384, 0.5, seed=3) if kind == "htmp" else W.logspaced(600, 384, 1e-3, seed=3)
+    Q, rep, Qo, ro = _polar_pair(A, "fp32", 5, tol=1e-5, max_iters=40)
+    assert abs(int(rep["iters"]) - ro.iters) <= 1
+    assert _rel(Q, Qo) <= (1e-5 if kind == "htmp" else 5e-5)   # SURVEY §8(c) log-uniform row
+
+
+@pytest.mark.parametrize("shape,deg", [((768, 768), 5), ((3072, 768), 5), ((768, 2304), 3), ((768, 3072), 5)])
+def test_polar_bf16_parity_gpt2_shapes(shape, deg):
+    A = W.gaussian(*shape, seed=7)
+    Q, rep, Qo, ro = _polar_pair(A, "bf16", deg, tol=3e-2)
+    assert int(rep["status"]) == prism.CONVERGED
+    assert abs(int(rep["iters"]) - ro.iters) <= 1
+    assert _rel(Q, Qo) <= 2e-2
+
+
+def test_polar_tf32_parity():
+    A = W.gaussian(300, 200, seed=5)
+    Q, rep, Qo, ro = _polar_pair(A, "tf32", 5, tol=1e-2)
+    assert abs(int(rep["iters"]) - ro.iters) <= 1
+    assert _rel(Q, Qo) <= 5e-3
+
+
+def test_polar_taylor_and_warmup_modes():
+    A = W.gaussian(200, 136, seed=9)
+    Q, rep, Qo, ro = _polar_pair(A, "fp32", 5, tol=1e-5, fit="taylor")
+    assert int(rep["iters"]) == ro.iters and _rel(Q, Qo) <= 1e-5
+    assert np.all(rep["alphas"][: ro.iters] == 0.375)
+    Q, rep, Qo, ro = _polar_pair(A, "fp32", 3, tol=1e-5, warmup=3)
+    assert np.all(rep["alphas"][:3] == 1.0) and abs(int(rep["iters"]) - ro.iters) <= 1
+    assert _rel(Q, Qo) <= 1e-5
+
+
+def test_polar_equal_sigma_closed_form():
+    # A = c Q: R_k = l_k I, closed-form trajectory (tests/test_oracle_prism.py); d=2, s=256 -> 5 iterations
+    A = W.equal_sigma(512, 256, 2.5, seed=4)
+    Q, rep, Qo, ro = _polar_pair(A, "fp32", 5, tol=1e-6)
+    assert int(rep["iters"]) == ro.iters
+    assert _rel(Q, A / 2.5) <= 1e-5
+
+
+@pytest.mark.parametrize("n,kappa,deg", [(256, 1e2, 5), (200, 1e2, 3), (640, 1e2, 5), (384, 1e4, 5)])
+def test_sqrt_fp32_parity(n, kappa, deg):
+    A = W.spd_logspaced(n, kappa, seed=n)
+    At, Aq = _dev(A, "fp32")
+    tol = 1e-5 if kappa <= 1e2 else 3e-5
+    X, Y, rep = P.sqrt_invsqrt([At], degree=deg, max_iters=40, tol=tol, seed=42, precision="fp32")
+    torch.cuda.synchronize()
+    Xo, Yo, ro = prism.sqrt_invsqrt(Aq, d=1 if deg == 3 else 2, p=8, tol=tol, max_iters=40, seed=42)
+    assert int(rep["status"][0]) == prism.CONVERGED
+    assert abs(int(rep["iters"][0]) - ro.iters) <= 1
+    assert _rel(X[0].double().cpu().numpy(), Xo) <= 1e-5
+    # inverse root: cond(A^{-1/2}) ~ kappa^{1/2} amplifies; SURVEY §8(c) rows
+    assert _rel(Y[0].double().cpu().numpy(), Yo) <= (3e-5 if kappa <= 1e2 else 3e-4)
+
+
+def test_batch_mixed_shapes_equals_single_solves():
+    shapes = [(300, 200), (128, 256), (256, 256), (520, 136)]
+    mats = [torch.tensor(W.gaussian(m, n, seed=i)).float().cuda() for i, (m, n) in enumerate(shapes)]
+    Qb, rb = P.polar(mats, degree=5, tol=1e-5, precision="fp32")
+    torch.cuda.synchronize()
+    for i, t in enumerate(mats):
+        Qs, rs = P.polar([t], degree=5, tol=1e-5, precision="fp32", matrix_ids=[i])
+        torch.cuda.synchronize()
+        assert torch.equal(Qs[0], Qb[i])                      # same kernels, same sketch stream -> same bits
+        assert int(rs["iters"][0]) == int(rb["iters"][i])
+        Qo, ro = prism.polar(t.double().cpu().numpy(), d=2, p=8, tol=1e-5, seed=42, b=i)
+        assert _rel(Qb[i].double().cpu().numpy(), Qo) <= 1e-5
+
+
+def test_edge_cases():
+    # zero input, single column, p = s, max_iters stop, NaN input
+    z = torch.zeros(64, 32, device="cuda")
+    one = torch.tensor(W.gaussian(40, 1, seed=1)).float().cuda()
+    small = torch.tensor(W.gaussian(16, 8, seed=2)).float().cuda()
+    nan = torch.tensor(W.gaussian(48, 24, seed=3)).float().cuda()
+    nan[3, 5] = float("nan")
+    Q, rep = P.polar([z, small, nan], degree=5, tol=1e-5, precision="fp32", sketch_size=8)
+    Q1, rep1 = P.polar([one], degree=5, tol=1e-5, precision="fp32", sketch_size=1)
+    torch.cuda.synchronize()
+    st = rep["status"].cpu().tolist()
+    assert st[0] == prism.ZERO_INPUT and torch.all(Q[0] == 0)
+    assert st[1] == prism.CONVERGED
+    assert st[2] == prism.NONFINITE
+    assert int(rep1["status"][0]) == prism.CONVERGED
+    v = one.double().cpu().numpy()
+    assert _rel(Q1[0].double().cpu().numpy(), v / np.linalg.norm(v)) <= 1e-6
+    Qo, ro = prism.polar(small.double().cpu().numpy(), d=2, p=8, tol=1e-5, seed=42, b=1)
+    assert _rel(Q[1].double().cpu().numpy(), Qo) <= 1e-5
+    A = torch.tensor(W.logspaced(96, 64, 1e-4, seed=4)).float().cuda()
+    Q, rep = P.polar([A], degree=5, tol=1e-9, max_iters=3, precision="fp32")
+    torch.cuda.synchronize()
+    assert int(rep["status"][0]) == prism.MAX_ITERS and int(rep["iters"][0]) == 3
+
+
+def test_gpt2_batch_full_size_sampled():
+    """configs[1] at full size in the bench's launch configuration: 48 BF16
+    matrices in one call; 4 sampled matrices (one per shape) vs the oracle,
+    all 48 checked by the polar property ||Q^T Q - I|| (any size)."""
+    shapes = W.gpt2_small_shapes()
+    mats_np = W.muon_batch(shapes, seed=1, kind="gaussian")
+    mats = [torch.tensor(a).to(torch.bfloat16).cuda() for a in mats_np]
+    Q, rep = P.polar(mats, degree=5, max_iters=20, tol=3e-2, seed=42, precision="bf16")
+    torch.cuda.synchronize()
+    assert torch.all(rep["status"] == prism.CONVERGED)
+    for i in range(48):
+        q = Q[i].double()
+        G = q.T @ q if q.shape[0] >= q.shape[1] else q @ q.T
+        s = G.shape[0]
+        assert float(torch.linalg.norm(G - torch.eye(s, device=G.device, dtype=G.dtype))) / s ** 0.5 <= 0.06
+    for i in (0, 1, 2, 3):
+        Qo, ro = prism.polar(mats[i].double().cpu().numpy(), d=2, p=8, tol=3e-2, max_iters=20, seed=42, b=i)
+        assert abs(int(rep["iters"][i]) - ro.iters) <= 1
+        assert _rel(Q[i].double().cpu().numpy(), Qo) <= 2e-2
