@@ -1,0 +1,385 @@
+"""bench.py — PRISM Newton–Schulz on B200 (BASELINE.json metric/configs).
+
+A "step" is one call of the whole hot path over one batch: normalise, then
+per iteration residual GEMM -> sketch chain -> alpha solve -> square GEMM ->
+apply GEMM, until every matrix converged, then write-back.  Default workload
+(N=1) is BASELINE.json configs[1]: the Muon step of GPT-2 small, 48 BF16
+layer gradients 768x{768,2304,3072} / 3072x768, PRISM-5 polar.
+
+Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl prism|reference]
+                        [--workload gpt2|square4096|gpt1b|shampoo]
+Multi-GPU: launched by torch.distributed.run, one rank per GPU; each rank
+solves its own batch (independent matrices, no data-path collective), so the
+scaling is weak.  Prints one JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PRISM solves/sec and TFLOP/s vs B200 BF16 peak; iterations to tolerance"
+
+
+# ---------------------------------------------------------------- workloads
+def workload(name: str, rank: int):
+    from paper_2601_22137_b200 import workloads as W
+    if name == "gpt2":
+        shapes = W.gpt2_small_shapes()
+        mats = W.muon_batch(shapes, seed=1 + rank, kind="mixed")
+        opts = dict(degree=5, max_iters=20, tol=3e-2, sketch_size=8, seed=42, precision="bf16")
+        desc = ("GPT-2 small Muon step (BASELINE.json configs[1]): 48 BF16 gradient matrices, 12 x "
+                "{768x2304, 768x768, 768x3072, 3072x768}; half Gaussian (MP), half HTMP-like kappa=0.5; "
+                "PRISM-5 polar, p=8, tol 3e-2, max_iters 20")
+        return "gpt2-small-muon-step", shapes, mats, opts, desc, "polar"
+    if name == "square4096":
+        shapes = [(4096, 4096)]
+        mats = [W.gaussian(4096, 4096, seed=4096 + rank)]
+        opts = dict(degree=5, max_iters=25, tol=3e-2, sketch_size=8, seed=42, precision="bf16")
+        desc = "single 4096x4096 Gaussian BF16 polar (north_star 60%-of-peak target shape), PRISM-5, p=8, tol 3e-2"
+        return "polar-4096-square", shapes, mats, opts, desc, "polar"
+    if name == "gpt1b":
+        shapes = W.gpt_1b_shapes()
+        mats = W.muon_batch(shapes, seed=1 + rank, kind="gaussian")
+        opts = dict(degree=5, max_iters=20, tol=3e-2, sketch_size=8, seed=42, precision="bf16")
+        desc = ("1.2B-param GPT Muon step (configs[4] batch, one GPU): 96 BF16 matrices 24 x "
+                "{2048x6144, 2048^2, 2048x8192, 8192x2048}, Gaussian, PRISM-5, tol 3e-2")
+        return "gpt-1b-muon-step", shapes, mats, opts, desc, "polar"
+    if name == "shampoo":
+        shapes = [(1024, 1024)] * 8 + [(2048, 2048)] * 4 + [(4096, 4096)] * 2
+        mats = [W.spd_logspaced(m, 1e2, seed=100 * rank + i) for i, (m, _) in enumerate(shapes)]
+        opts = dict(degree=5, max_iters=30, tol=1e-5, sketch_size=8, seed=42, precision="fp32")
+        desc = ("Shampoo step (configs[2]): 8x1024 + 4x2048 + 2x4096 SPD blocks, lambda log-spaced, kappa=1e2, "
+                "FP32 (3xTF32) coupled sqrt/inv-sqrt, PRISM-5, tol 1e-5")
+        return "shampoo-sqrt-step", shapes, mats, opts, desc, "sqrt"
+    raise SystemExit(f"unknown workload {name}")
+
+
+# ---------------------------------------------------------------- helpers
+def read_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return d, "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, \
+            "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def flush_l2(buf):
+    buf.add_(1)   # 256 MiB write > 126 MB L2
+
+
+def cpu_oracle_solve(A, kind, opts, b):
+    from oracle import prism
+    d = 1 if opts["degree"] == 3 else 2
+    if kind == "polar":
+        return prism.polar(A, d=d, p=opts["sketch_size"], tol=opts["tol"], max_iters=opts["max_iters"],
+                           seed=opts["seed"], b=b)[1]
+    return prism.sqrt_invsqrt(A, d=d, p=opts["sketch_size"], tol=opts["tol"], max_iters=opts["max_iters"],
+                              seed=opts["seed"], b=b)[2]
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max([int(i.get("num_threads", 1)) for i in threadpool_info()] + [1])
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def stored_inputs(mats, dtype_name):
+    """Inputs rounded to the device dtype, as fp64 numpy (what the oracle reads)."""
+    import torch
+    dt = torch.bfloat16 if dtype_name == "bf16" else torch.float32
+    return [torch.tensor(a).to(dt).double().numpy() for a in mats]
+
+
+# ---------------------------------------------------------------- reference arm (the oracle)
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    name, shapes, mats, opts, desc, kind = workload(args.workload, 0)
+    A = stored_inputs(mats, opts["precision"])
+    order = sorted(range(len(A)), key=lambda i: A[i].size)   # bounded sample: smallest matrices first
+    for w in range(args.warmup):
+        cpu_oracle_solve(A[order[w % len(A)]], kind, opts, order[w % len(A)])
+    times = []
+    for s in range(args.steps):
+        i = order[s % len(A)]
+        t0 = time.perf_counter()
+        cpu_oracle_solve(A[i], kind, opts, i)
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    value = args.steps / total
+    cores = blas_threads()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded), inputs rounded to the device dtype",
+        "config": {"workload": name, "description": desc,
+                   "reference": "fp64 numpy oracle (oracle/prism.py) on host cores; one matrix per step"},
+        "cpu_baseline": {"value": value, "unit": "solves/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{args.steps} single-matrix solves of the workload, smallest first"},
+        "e2e": {"value": value, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="prism", choices=["prism", "reference"])
+    ap.add_argument("--workload", default="gpt2", choices=["gpt2", "square4096", "gpt1b", "shampoo"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)   # timing rule: >= 3 warm-up steps
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2601_22137_b200 as P
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    name, shapes, mats_np, opts, desc, kind = workload(args.workload, rank)
+    dt = torch.bfloat16 if opts["precision"] == "bf16" else torch.float32
+    host = [torch.tensor(a).to(dt).pin_memory() for a in mats_np]
+    mats = [h.to(dev) for h in host]
+    B = len(mats)
+    h = P.Handle()
+    ids = list(range(B))
+    stream = torch.cuda.current_stream(dev)
+
+    def solve(inputs, out=None):
+        if kind == "polar":
+            return P.polar(inputs, out=out, matrix_ids=ids, handle=h, **opts)
+        return P.sqrt_invsqrt(inputs, matrix_ids=ids, handle=h, **opts)
+
+    outs = [torch.empty_like(m) for m in mats] if kind == "polar" else None
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    for _ in range(args.warmup):
+        solve(mats, outs)
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, L2 flushed before each (outside the events)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    rep = None
+    for s in range(args.steps):
+        flush_l2(flush)
+        ev[s][0].record(stream)
+        res = solve(mats, outs)
+        ev[s][1].record(stream)
+        rep = res[-1]
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = sum(a.elapsed_time(b) for a, b in ev)
+    launches_per_step = h.launch_count()
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.barrier()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ms_step = ms_max / args.steps
+    value = world * B * args.steps / (ms_max / 1e3)
+
+    iters = rep["iters"].cpu().tolist()
+    status = rep["status"].cpu().tolist()
+    if kind == "polar":
+        f_iter = [P.polar_flops_per_iter(m, n, opts["degree"], opts["sketch_size"]) for (m, n) in shapes]
+    else:
+        f_iter = [P.sqrt_flops_per_iter(m, opts["degree"], opts["sketch_size"]) for (m, _) in shapes]
+    flops_step = sum(f * k for f, k in zip(f_iter, iters))
+    tflops = world * flops_step * args.steps / (ms_max / 1e3) / 1e12
+
+    # ---- e2e: pinned host inputs -> device -> solve -> host, all inside the timed region
+    host_out = [torch.empty_like(x).pin_memory() for x in host]
+    dev_in = [torch.empty_like(m) for m in mats]
+    e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    for s in range(args.steps):
+        flush_l2(flush)
+        e_ev[s][0].record(stream)
+        for d_, h_ in zip(dev_in, host):
+            d_.copy_(h_, non_blocking=True)
+        res = solve(dev_in, outs)
+        src = outs if kind == "polar" else res[0]
+        for h_, d_ in zip(host_out, src):
+            h_.copy_(d_, non_blocking=True)
+        e_ev[s][1].record(stream)
+    torch.cuda.synchronize()
+    e_ms = sum(a.elapsed_time(b) for a, b in e_ev)
+    te = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e_value = world * B * args.steps / (float(te.item()) / 1e3)
+    nbytes = sum(x.numel() * x.element_size() for x in host)
+
+    # ---- per-kernel device timing (separate pass; CUDA events on the launching stream)
+    h.profile(True)
+    h.profile_read(reset=True)
+    for s in range(args.steps):
+        flush_l2(flush)
+        solve(mats, outs)
+    torch.cuda.synchronize()
+    prof = h.profile_read(reset=True)
+    h.profile(False)
+    peaks, peak_src = read_peaks()
+    peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1400.0)))
+    if opts["precision"] != "bf16":
+        peak = peak / 2.0 / 3.0   # tf32 = bf16 / 2 (nominal ratio), 3 MMAs per product in 3xTF32
+    if kind == "polar":
+        apply_flops = sum(2.0 * max(m, n) * min(m, n) ** 2 * k for (m, n), k in zip(shapes, iters)) * args.steps
+        gram_flops = sum(max(m, n) * min(m, n) * (min(m, n) + 1) * (k + 1) for (m, n), k in zip(shapes, iters)) * args.steps
+        sq_flops = sum(min(m, n) ** 2 * (min(m, n) + 1) * k for (m, n), k in zip(shapes, iters)) * args.steps
+    else:
+        apply_flops = sum(4.0 * m ** 3 * k for (m, _), k in zip(shapes, iters)) * args.steps
+        gram_flops = sum(2.0 * m ** 3 * (k + 1) for (m, _), k in zip(shapes, iters)) * args.steps
+        sq_flops = sum(2.0 * m ** 3 * k for (m, _), k in zip(shapes, iters)) * args.steps
+    apply_ms = prof["apply"]["ms"]
+    achieved = apply_flops / (apply_ms / 1e3) / 1e12 if apply_ms > 0 else None
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"traffic_{name}.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("apply_dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    kernel_tflops = {k: (f / (prof[k]["ms"] / 1e3) / 1e12 if prof[k]["ms"] > 0 else None)
+                     for k, f in (("gram", gram_flops), ("square", sq_flops), ("apply", apply_flops))}
+    prof_total = sum(v["ms"] for v in prof.values())
+    shares = {k: (v["ms"] / prof_total if prof_total > 0 else None) for k, v in prof.items()}
+
+    # ---- CPU baseline: the oracle on a bounded sample (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        A = stored_inputs(mats_np, opts["precision"])
+        seen, sample = set(), []
+        for i, shp in enumerate(shapes):
+            if shp not in seen:
+                seen.add(shp)
+                sample.append(i)
+        t0 = time.perf_counter()
+        for i in sample:
+            cpu_oracle_solve(A[i], kind, opts, i)
+        sec = time.perf_counter() - t0
+        cpu = {"value": len(sample) / sec, "unit": "solves/s", "cores": blas_threads(), "kind": "oracle",
+               "sample": f"{len(sample)} of {B} matrices (one per distinct shape), fp64 numpy oracle, {sec:.2f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": opts["precision"],
+            "data": "synthetic: seeded matrices shaped like the paper's workloads (no datasets)",
+            "config": {"workload": name, "description": desc, "matrices_per_gpu": B, "solver": kind,
+                       "degree": opts["degree"], "sketch_size": opts["sketch_size"], "tol": opts["tol"],
+                       "max_iters": opts["max_iters"], "precision": opts["precision"],
+                       "l2": "flushed (256 MiB write) before every timed step, outside the events",
+                       "parallelism": f"independent batch per GPU x{world}"},
+            "tflops": tflops, "tflops_unit": "F_min (symmetric products once) per second",
+            "frac_of_peak_sustained": tflops / peak if peak else None,
+            "iterations": {"mean": sum(iters) / B, "max": max(iters), "min": min(iters),
+                           "histogram": {str(k): iters.count(k) for k in sorted(set(iters))}},
+            "status_converged": sum(1 for x in status if x == 0),
+            "clocks": clk,
+            "e2e": {"value": e_value, "unit": "solves/s", "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes},
+            "gpu_launches": launches_per_step * args.steps,
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "kernel": "prism_gemm_kernel apply (X + X.P), tcgen05",
+                         "peak_source": peak_src + (" bf16 sustained" if opts["precision"] == "bf16"
+                                                    else " bf16 sustained / 2 (tf32) / 3 (3xTF32)")},
+            "kernels": {"tflops": kernel_tflops, "time_share": shares,
+                        "ms_per_step": {k: v["ms"] / args.steps for k, v in prof.items()}},
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

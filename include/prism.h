@@ -145,6 +145,20 @@ double prism_polar_flops_per_iter(int64_t m, int64_t n, int degree, int sketch_s
 /* Dense-GEMM flop count per sqrt iteration (general products). */
 double prism_sqrt_flops_per_iter(int64_t n, int degree, int sketch_size);
 
+/* ---- measurement (bench.py) ---------------------------------------------------- */
+
+/* Kernel launches issued by the most recent prism_polar / prism_sqrt_invsqrt on h. */
+int64_t prism_launch_count(prism_handle h);
+/*
+ * Per-kernel-kind device timing.  When enabled, every launch group is bracketed
+ * with CUDA events on the caller's stream (kinds: 0 residual GEMM, 1 square GEMM,
+ * 2 apply GEMM, 3 sketch + chain, 4 alpha solve, 5 normalise/finalise).
+ * prism_profile_read synchronises those events and returns the accumulated
+ * milliseconds and launch counts per kind since the last reset (arrays of 6).
+ */
+prism_status prism_profile_enable(prism_handle h, int enable);
+prism_status prism_profile_read(prism_handle h, double* ms, int64_t* launches, int reset);
+
 /* ---- test hooks (exercised by tests/test_gpu_*.py) ---------------------------- */
 
 /*

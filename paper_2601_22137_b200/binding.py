@@ -56,6 +56,7 @@ EXPORTS = [
     "prism_default_options", "prism_create", "prism_destroy", "prism_last_error", "prism_abi_version",
     "prism_polar_workspace", "prism_polar", "prism_sqrt_workspace", "prism_sqrt_invsqrt",
     "prism_lpt_partition", "prism_polar_flops_per_iter", "prism_sqrt_flops_per_iter",
+    "prism_launch_count", "prism_profile_enable", "prism_profile_read",
     "prism_debug_gemm", "prism_debug_sketch", "prism_debug_argmin",
 ]
 
@@ -98,10 +99,15 @@ def lib():
         L.prism_sqrt_flops_per_iter.restype = dbl
         L.prism_debug_gemm.argtypes = [vp, i32, i32, i32, i32, i32, i32, i32, vp, vp, i64, vp, vp, i64, vp, vp, i64,
                                        vp, vp, i64, vp, ctypes.c_float, i32, vp, vp, vp, sz, vp]
+        L.prism_launch_count.argtypes = [vp]
+        L.prism_launch_count.restype = i64
+        L.prism_profile_enable.argtypes = [vp, i32]
+        L.prism_profile_read.argtypes = [vp, ctypes.POINTER(dbl), ctypes.POINTER(i64), i32]
         L.prism_debug_sketch.argtypes = [u64, i64, i32, i32, i32, vp, vp]
         L.prism_debug_argmin.argtypes = [i32, vp, dbl, dbl, dbl, vp, vp]
         for name in ("prism_create", "prism_destroy", "prism_polar", "prism_sqrt_invsqrt", "prism_lpt_partition",
-                     "prism_debug_gemm", "prism_debug_sketch", "prism_debug_argmin"):
+                     "prism_debug_gemm", "prism_debug_sketch", "prism_debug_argmin",
+                     "prism_profile_enable", "prism_profile_read"):
             getattr(L, name).restype = i32
         _lib = L
         return L
@@ -136,6 +142,21 @@ class Handle:
                 _lib.prism_destroy(self.h)
         except Exception:
             pass
+
+    KINDS = ("gram", "square", "apply", "sketch_chain", "alpha", "norm_final")
+
+    def launch_count(self) -> int:
+        """Kernel launches issued by the last solve on this handle."""
+        return int(lib().prism_launch_count(self.h))
+
+    def profile(self, enable: bool):
+        check(lib().prism_profile_enable(self.h, 1 if enable else 0), "prism_profile_enable")
+
+    def profile_read(self, reset: bool = True) -> dict:
+        ms = (ctypes.c_double * 6)()
+        nl = (ctypes.c_int64 * 6)()
+        check(lib().prism_profile_read(self.h, ms, nl, 1 if reset else 0), "prism_profile_read")
+        return {k: {"ms": ms[i], "launches": nl[i]} for i, k in enumerate(self.KINDS)}
 
     def workspace(self, nbytes: int, device):
         import torch

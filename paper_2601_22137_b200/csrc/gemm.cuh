@@ -1,9 +1,10 @@
 // Persistent, warp-specialised, grouped tcgen05 GEMM for the PRISM iteration.
 //
 // One launch runs a list of tiles drawn from many independent problems (the
-// matrices of a Muon/Shampoo batch): D = A·B with
-//   A  : M x K, K-major (row-major A), fed by TMA with 128-B swizzle
-//   B  : K-major (B stored N x K, i.e. A·Bᵀ) or MN-major (B stored K x N)
+// matrices of a Muon/Shampoo batch): D = A·B with operands
+// fed by TMA with 128-B swizzle, each either K-major (A stored M x K / B stored
+// N x K) or MN-major (A stored K x M / B stored K x N) — a per-problem runtime
+// choice, so XᵀX of a tall row-major X needs no transpose.
 //   D  : fp32 accumulator in TMEM (two accumulator buffers, so the epilogue
 //        of tile t overlaps the MMAs of tile t+1)
 // and a fused epilogue that forms the PRISM quantity directly:
@@ -27,7 +28,14 @@
 
 namespace prism {
 
-enum EpiMode : int { EPI_RESID = 0, EPI_POLY = 1, EPI_APPLY = 2, EPI_STORE = 3 };
+enum EpiMode : int { EPI_RESID = 0, EPI_POLY = 1, EPI_APPLY = 2, EPI_STORE = 3, EPI_CHAIN = 4 };
+
+// Sketch-chain pass codes (EPI_CHAIN).  The thin GEMM computes
+// D = R · [W_hi | W_lo] (N = 2w) and the epilogue forms out = D_hi + D_lo, then
+//   d=2: P1 K1 -> Q (diag trick) -> next [K1|Q];  P2 [K2|L1] keep K2 -> next [K2|L1];
+//        P3 [K3|L2] keep K3,L2 -> next L2;  P4 L3 keep -> next L3;  P5 L4 -> <Va,Vb>
+//   d=1: P1 K1 keep -> next Q;  P2 L1 keep -> next L1;  P3 L2 -> <Va,Vb>
+enum ChainPassCode : int { CH2_P1 = 0, CH2_P2, CH2_P3, CH2_P4, CH2_P5, CH1_P1, CH1_P2, CH1_P3 };
 
 struct GemmProblem {
   const CUtensorMap* tmA;
@@ -45,47 +53,64 @@ struct GemmProblem {
   int M, N, K;
   int mode, sym, matrix, scale_by_alpha, tiles_n;
   float c1;
-  int pad_;
+  int pass;              // EPI_CHAIN pass code
+  int a_mn, b_mn;        // operand major-ness: 0 K-major, 1 MN-major
+  // EPI_CHAIN operands (row i of R = row i of the output)
+  const float* S;        // [p][ldS] sketch (fp32)
+  const void* Rg;        // R (for R_ii), compute dtype (+ R_lo in 3xTF32)
+  const void* Rg_lo;
+  void* Wn;              // next pass B operand: [2w'][ldS] hi rows then lo rows, compute dtype
+  float* keep;           // [4][M][p] fp32 kept chain columns
+  double* chain_part;    // [tiles_m][6] per-tile <Va,Vb> partials
+  long long ldS, ldr;
+  int p;
+  int pad2_;
 };
 
 struct GemmLaunch {
-  const GemmProblem* probs;
-  const uint32_t* tiles;   // (problem << 20) | (tm << 10) | tn
-  const int* done;         // per matrix (stride done_stride ints): 1 = stopped, skip its tiles
+  const GemmProblem* probs;      // problem table (even iterations)
+  const GemmProblem* probs_odd;  // problem table for odd iterations (ping-pong buffers) or null
+  const uint32_t* tiles;         // (problem << 20) | (tm << 10) | tn
+  const int* done;               // per matrix (stride done_stride ints): 1 = stopped, skip its tiles
+  const int* iter;               // device iteration counter k (or null): run only if iter_lo <= k < iter_hi
   int done_stride;
   int ntiles;
+  int iter_lo, iter_hi;
 };
 
-template <int KIND_, bool SPLIT_, bool BMN_>
+template <int KIND_, bool SPLIT_, int BN_ = 0>
 struct GemmCfg {
   static constexpr int KIND = KIND_;
   static constexpr bool SPLIT = SPLIT_;
-  static constexpr bool BMN = BMN_;
   static constexpr int ESZ = KIND == 0 ? 2 : 4;
   static constexpr int BM = 128;
-  static constexpr int BN = KIND == 0 ? 256 : 128;
+  static constexpr int BN = BN_ ? BN_ : (KIND == 0 ? 256 : 128);
+  // thin chain GEMM (BN = 32): B already carries [W_hi | W_lo], so 3xTF32 needs
+  // only A_lo · B besides A · B (no B_lo plane)
+  static constexpr bool LOB = SPLIT && BN != 32;
   static constexpr int BK = 128 / ESZ;          // one 128-B swizzle row of K
   static constexpr int UK = 32 / ESZ;           // K per tcgen05.mma (32 bytes)
   static constexpr int A_BYTES = BM * BK * ESZ;
   static constexpr int B_BYTES = BN * BK * ESZ;
-  static constexpr int NOPS = SPLIT ? 2 : 1;
-  static constexpr int STAGE_BYTES = NOPS * (A_BYTES + B_BYTES);
+  static constexpr int STAGE_BYTES = (SPLIT ? 2 * A_BYTES : A_BYTES) + (LOB ? 2 * B_BYTES : B_BYTES);
   static constexpr int STAGES_RAW = (192 * 1024) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int TMEM_COLS = 2 * BN;
-  static constexpr int B_ATOMS = BN * ESZ / 128;  // MN-major: 128-B wide boxes along N
-  static constexpr int B_ATOM_BYTES = BK * 128;
-  // MN-major B: bf16 uses the 128-B swizzle (8-row K groups, SBO 1024); tf32 must use
+  static constexpr int AE = 128 / ESZ;           // elements per 128-B atom along MN (MN-major)
+  static constexpr int ATOM_BYTES = BK * 128;    // one MN-major atom column: BK rows of 128 B
+  // MN-major: bf16 uses the 128-B swizzle (8-row K groups, SBO 1024); tf32 must use
   // the 128-B/32-B-atom swizzle (layout type 1, 4-row K groups, SBO 512).
-  static constexpr uint32_t BMN_LAYOUT = KIND == 0 ? 2u : 1u;
-  static constexpr uint32_t BMN_SBO = KIND == 0 ? 1024u : 512u;
-  static constexpr uint32_t IDESC = idesc_make(KIND == 0 ? 1u : 2u, BMN ? 1u : 0u, BM, BN);
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr uint32_t MN_LAYOUT = KIND == 0 ? 2u : 1u;
+  static constexpr uint32_t MN_SBO = KIND == 0 ? 1024u : 512u;
+  static constexpr uint32_t IDESC = idesc_make(KIND == 0 ? 1u : 2u, 0u, BM, BN);
+  static constexpr int TB_BYTES = 4 * 32 * 33 * 4;   // per-epilogue-warp 32x33 fp32 transpose buffers
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 512 /*barriers, scratch*/ + TB_BYTES;
   static constexpr int THREADS = 192;
   // k-blocks per TMEM accumulation chunk: tf32 partials are promoted to fp32
   // registers every k-block (3xTF32, K = 32: 12 MMAs per chunk) or every 4
   // (1xTF32); bf16 keeps one accumulator per tile (products exact, 2^-9 output).
   static constexpr int PROMO_KB = KIND == 0 ? (1 << 30) : (SPLIT ? 1 : 4);
+  static constexpr int TMEM_ALLOC = TMEM_COLS < 32 ? 32 : TMEM_COLS;
 };
 
 // ---------------------------------------------------------------- epilogue helpers
@@ -186,23 +211,28 @@ __device__ __forceinline__ void store_row32(void* out, void* out_lo, long long o
   }
 }
 
-// Fused epilogue for one 32-column row segment [j0, j0+32) of output row i,
-// given the fp32 accumulator values d[] of D = A·B.
+// Fused epilogue for one 32 x 32 block: rows i0 + lane (one row per lane of an
+// epilogue warp), columns [j0, j0 + 32), given the fp32 accumulators d[] of
+// D = A·B and (POLY / APPLY) the prefetched row segment c[] of C.  Called by all
+// 32 lanes of the warp (warp-collective: the symmetric mirror goes through a
+// per-warp 32 x 33 shared-memory transpose tb so that both the direct and the
+// mirrored stores are 16-byte vectors).
 template <class Cfg>
-__device__ __forceinline__ void epi_segment(const GemmProblem& P, int mode, bool sym, int i, int j0, float coefA,
-                                            float coefC, const float (&d)[32], float& sumsq) {
-  if (i >= P.M || j0 >= P.N) return;
-  if (sym && j0 + 31 < i) return;           // whole segment below the diagonal
+__device__ __forceinline__ void epi_segment(const GemmProblem& P, int mode, bool sym, int i0, int lane, int j0,
+                                            float coefA, float coefC, const float (&d)[32], const float (&c)[32],
+                                            float* tb, float& sumsq) {
+  if (i0 >= P.M || j0 >= P.N) return;            // warp-uniform
+  if (sym && j0 + 31 < i0) return;               // block strictly below the diagonal
+  const int i = i0 + lane;
+  const bool row_ok = i < P.M;
   float v[32];
   if (mode == EPI_POLY || mode == EPI_APPLY) {
-    float c[32];
-    load_row32<Cfg::KIND, Cfg::SPLIT>(P.C, P.C_lo, P.ldc, i, j0, P.N, c);
 #pragma unroll
     for (int u = 0; u < 32; ++u) v[u] = coefC * c[u] + coefA * d[u];
   } else if (mode == EPI_RESID) {
 #pragma unroll
     for (int u = 0; u < 32; ++u) v[u] = ((j0 + u == i) ? 1.f : 0.f) - d[u];
-    if (P.gdiag && i >= j0 && i < j0 + 32) {
+    if (P.gdiag && row_ok && i >= j0 && i < j0 + 32) {
 #pragma unroll
       for (int u = 0; u < 32; ++u)
         if (j0 + u == i) P.gdiag[i] = d[u];
@@ -212,41 +242,190 @@ __device__ __forceinline__ void epi_segment(const GemmProblem& P, int mode, bool
     for (int u = 0; u < 32; ++u) v[u] = d[u];
   }
   const long long off = (long long)i * P.ldo + j0;
+  const bool full_n = j0 + 32 <= P.N;
   if (!sym) {
-    if (j0 + 32 <= P.N) {
+    if (row_ok) {
+      if (full_n) {
+        store_row32<Cfg::KIND, Cfg::SPLIT>(P.out, P.out_lo, off, v);
+        if (mode == EPI_RESID) {
+#pragma unroll
+          for (int u = 0; u < 32; ++u) sumsq = fmaf(v[u], v[u], sumsq);
+        }
+      } else {
+        for (int u = 0; u < 32; ++u)
+          if (j0 + u < P.N) {
+            store_elem<Cfg::KIND, Cfg::SPLIT>(P.out, P.out_lo, off + u, v[u]);
+            if (mode == EPI_RESID) sumsq = fmaf(v[u], v[u], sumsq);
+          }
+      }
+    }
+    return;
+  }
+  // symmetric: upper triangle (j >= i) written directly, (j > i) mirrored to (j, i)
+  const bool diag = j0 < i0 + 32;                // 32-aligned blocks: the diagonal block
+  if (row_ok) {
+    if (!diag && full_n) {
       store_row32<Cfg::KIND, Cfg::SPLIT>(P.out, P.out_lo, off, v);
       if (mode == EPI_RESID) {
 #pragma unroll
-        for (int u = 0; u < 32; ++u) sumsq += v[u] * v[u];
+        for (int u = 0; u < 32; ++u) sumsq = fmaf(2.f * v[u], v[u], sumsq);
       }
     } else {
-      for (int u = 0; u < 32; ++u)
-        if (j0 + u < P.N) {
-          store_elem<Cfg::KIND, Cfg::SPLIT>(P.out, P.out_lo, off + u, v[u]);
-          if (mode == EPI_RESID) sumsq += v[u] * v[u];
-        }
-    }
-  } else {
-    // upper triangle (j >= i) written directly, (j > i) mirrored to (j, i)
-    if (j0 >= i && j0 + 32 <= P.N) {
-      store_row32<Cfg::KIND, Cfg::SPLIT>(P.out, P.out_lo, off, v);
-    } else {
+#pragma unroll
       for (int u = 0; u < 32; ++u) {
         const int j = j0 + u;
-        if (j >= i && j < P.N) store_elem<Cfg::KIND, Cfg::SPLIT>(P.out, P.out_lo, off + u, v[u]);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < 32; ++u) {
-      const int j = j0 + u;
-      if (j > i && j < P.N) {
-        store_elem<Cfg::KIND, Cfg::SPLIT>(P.out, P.out_lo, (long long)j * P.ldo + i, v[u]);
-        if (mode == EPI_RESID) sumsq += 2.f * v[u] * v[u];
-      } else if (j == i && mode == EPI_RESID) {
-        sumsq += v[u] * v[u];
+        if (j >= i && j < P.N) {
+          store_elem<Cfg::KIND, Cfg::SPLIT>(P.out, P.out_lo, off + u, v[u]);
+          if (mode == EPI_RESID) sumsq = fmaf(j > i ? 2.f * v[u] : v[u], v[u], sumsq);
+        }
       }
     }
   }
+  // mirror through shared memory: lane l takes column j = j0 + l, rows i0 .. i0+31
+#pragma unroll
+  for (int u = 0; u < 32; ++u) tb[lane * 33 + u] = v[u];
+  __syncwarp();
+  const int j = j0 + lane;
+  if (j < P.N) {
+    float w[32];
+#pragma unroll
+    for (int u = 0; u < 32; ++u) w[u] = tb[u * 33 + lane];
+    const long long moff = (long long)j * P.ldo + i0;
+    if (!diag && i0 + 32 <= P.M) {
+      store_row32<Cfg::KIND, Cfg::SPLIT>(P.out, P.out_lo, moff, w);
+    } else {
+#pragma unroll
+      for (int u = 0; u < 32; ++u)
+        if (i0 + u < j && i0 + u < P.M) store_elem<Cfg::KIND, Cfg::SPLIT>(P.out, P.out_lo, moff + u, w[u]);
+    }
+  }
+  __syncwarp();
+}
+
+// Sketch-chain epilogue (thin GEMM, BN = 32): d[c] + d[w + c] = (R W)[i][c].
+template <class Cfg>
+__device__ __forceinline__ void store_w(const GemmProblem& P, int c, int wn, int i, float v) {
+  // next-pass B operand, hi row c and lo row wn + c (K-major: [2w'][ldS])
+  if constexpr (Cfg::KIND == 0) {
+    const __nv_bfloat16 h = __float2bfloat16_rn(v);
+    static_cast<__nv_bfloat16*>(P.Wn)[(long long)c * P.ldS + i] = h;
+    static_cast<__nv_bfloat16*>(P.Wn)[(long long)(wn + c) * P.ldS + i] = __float2bfloat16_rn(v - __bfloat162float(h));
+  } else {
+    const float h = tf32_trunc(v);
+    static_cast<float*>(P.Wn)[(long long)c * P.ldS + i] = h;
+    static_cast<float*>(P.Wn)[(long long)(wn + c) * P.ldS + i] = v - h;
+  }
+}
+
+template <class Cfg>
+__device__ __forceinline__ void epi_chain(const GemmProblem& P, int i, int tm, const float (&d)[32], double* dred,
+                                          int q, int lane, int et) {
+  const int p = P.p;
+  const int w = P.N / 2;          // columns of this pass's output
+  const bool valid = i < P.M;
+  double g[6] = {0, 0, 0, 0, 0, 0};
+  float o[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) o[c] = (c < w) ? d[c] + d[w + c] : 0.f;
+  float* keep = P.keep;
+  const long long M = P.M;
+  auto K = [&](int slot, int c) -> float& { return keep[((long long)slot * M + i) * p + c]; };
+  if (valid) {
+    switch (P.pass) {
+      case CH2_P1:
+      case CH1_P1: {
+        float rii;
+        if constexpr (Cfg::KIND == 0) rii = __bfloat162float(static_cast<const __nv_bfloat16*>(P.Rg)[(long long)i * P.ldr + i]);
+        else rii = static_cast<const float*>(P.Rg)[(long long)i * P.ldr + i] +
+                   (P.Rg_lo ? static_cast<const float*>(P.Rg_lo)[(long long)i * P.ldr + i] : 0.f);
+        const float gii = P.gdiag[i];
+        for (int c = 0; c < p; ++c) {
+          const float sc = P.S[(long long)c * P.ldS + i];
+          const float qv = gii * sc - (o[c] - rii * sc);   // Q = G S^T, G_ii exact (fp32 from the Gram)
+          if (P.pass == CH2_P1) {
+            store_w<Cfg>(P, c, 2 * p, i, o[c]);
+            store_w<Cfg>(P, p + c, 2 * p, i, qv);
+          } else {
+            K(0, c) = o[c];
+            store_w<Cfg>(P, c, p, i, qv);
+          }
+        }
+        break;
+      }
+      case CH2_P2:
+        for (int c = 0; c < p; ++c) {
+          K(0, c) = o[c];
+          store_w<Cfg>(P, c, 2 * p, i, o[c]);
+          store_w<Cfg>(P, p + c, 2 * p, i, o[p + c]);
+        }
+        break;
+      case CH2_P3:
+        for (int c = 0; c < p; ++c) {
+          K(1, c) = o[c];
+          K(2, c) = o[p + c];
+          store_w<Cfg>(P, c, p, i, o[p + c]);
+        }
+        break;
+      case CH2_P4:
+      case CH1_P2:
+        for (int c = 0; c < p; ++c) {
+          K(P.pass == CH2_P4 ? 3 : 1, c) = o[c];
+          store_w<Cfg>(P, c, p, i, o[c]);
+        }
+        break;
+      default:  // CH2_P5 / CH1_P3: inner products <Va, Vb> (fp64 products of widened factors)
+        for (int c = 0; c < p; ++c) {
+          double v0, v1, v2;
+          if (P.pass == CH2_P5) {
+            v0 = 0.25 * (3.0 * (double)K(0, c) + (double)K(1, c));   // 1/4 (3 K2 + K3)
+            v1 = -((double)K(3, c) + 2.0 * (double)K(2, c));         // -(L3 + 2 L2)
+            v2 = -(double)o[c];                                      // -L4
+          } else {
+            v0 = (double)K(0, c);                                    // K1
+            v1 = -2.0 * (double)K(1, c);                             // -2 L1
+            v2 = -(double)o[c];                                      // -L2
+          }
+          g[0] += v0 * v0; g[1] += v0 * v1; g[2] += v0 * v2;
+          g[3] += v1 * v1; g[4] += v1 * v2; g[5] += v2 * v2;
+        }
+        break;
+    }
+  }
+  if (P.pass == CH2_P5 || P.pass == CH1_P3) {
+#pragma unroll
+    for (int j = 0; j < 6; ++j) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) g[j] += __shfl_xor_sync(0xffffffffu, g[j], off);
+    }
+    if (lane == 0)
+#pragma unroll
+      for (int j = 0; j < 6; ++j) dred[q * 6 + j] = g[j];
+    named_bar_sync(1, 128);
+    if (et == 0)
+#pragma unroll
+      for (int j = 0; j < 6; ++j)
+        P.chain_part[tm * 6 + j] = (dred[0 * 6 + j] + dred[1 * 6 + j]) + (dred[2 * 6 + j] + dred[3 * 6 + j]);
+    named_bar_sync(1, 128);
+  }
+}
+
+// TMA load of one operand tile (rows = BM or BN along MN, BK along K) into smem.
+template <class Cfg>
+__device__ __forceinline__ void load_operand(uint8_t* dst, const CUtensorMap* map, uint64_t* bar, int mn0, int k0,
+                                             int rows, int mn_major) {
+  if (mn_major) {
+    for (int q = 0; q < rows / Cfg::AE; ++q)
+      tma_load_2d(dst + q * Cfg::ATOM_BYTES, map, bar, mn0 + q * Cfg::AE, k0);
+  } else {
+    tma_load_2d(dst, map, bar, k0, mn0);
+  }
+}
+
+// UMMA smem descriptor of the k-th K-step (UK elements) of an operand tile.
+template <class Cfg>
+__device__ __forceinline__ uint64_t operand_desc(uint32_t base, int k, int mn_major) {
+  return mn_major ? sdesc_rt(base + k * Cfg::UK * 128, Cfg::ATOM_BYTES, Cfg::MN_SBO, Cfg::MN_LAYOUT)
+                  : sdesc_rt(base + k * 32, 16, 1024, 2u);
 }
 
 // ---------------------------------------------------------------- the kernel
@@ -265,9 +444,18 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
   uint64_t* tempty = tfull + 2;                // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   float* red = reinterpret_cast<float*>(tmem_slot + 4);   // [4] epilogue reduction scratch
+  double* dred = reinterpret_cast<double*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES + 256);   // [4][6]
+  float* tbuf = reinterpret_cast<float*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES + 512);     // [4][32*33]
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  // device-side loop control (CUDA-graph WHILE body): uniform early exit / parity select
+  const GemmProblem* __restrict__ probs = L.probs;
+  if (L.iter) {
+    const int k = *L.iter;
+    if (k < L.iter_lo || k >= L.iter_hi) return;
+    if (L.probs_odd && (k & 1)) probs = L.probs_odd;
+  }
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {
@@ -280,7 +468,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
     }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  if (warp == 1) tmem_alloc(tmem_slot, Cfg::TMEM_ALLOC);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -293,7 +481,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < L.ntiles; t += gridDim.x) {
         const uint32_t code = L.tiles[t];
-        const GemmProblem& P = L.probs[code >> 20];
+        const GemmProblem& P = probs[code >> 20];
         if (L.done && L.done[P.matrix * L.done_stride]) continue;
         const int tm = (code >> 10) & 1023, tn = code & 1023;
         const int nkb = (P.K + Cfg::BK - 1) / Cfg::BK;
@@ -302,27 +490,14 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
           uint8_t* sA = stage_base + stage * Cfg::STAGE_BYTES;
           uint8_t* sB = sA + Cfg::A_BYTES;
           mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
-          tma_load_2d(sA, P.tmA, &full[stage], kb * Cfg::BK, tm * Cfg::BM);
-          if constexpr (Cfg::BMN) {
-#pragma unroll
-            for (int q = 0; q < Cfg::B_ATOMS; ++q)
-              tma_load_2d(sB + q * Cfg::B_ATOM_BYTES, P.tmB, &full[stage], tn * Cfg::BN + q * (128 / Cfg::ESZ),
-                          kb * Cfg::BK);
-          } else {
-            tma_load_2d(sB, P.tmB, &full[stage], kb * Cfg::BK, tn * Cfg::BN);
-          }
+          load_operand<Cfg>(sA, P.tmA, &full[stage], tm * Cfg::BM, kb * Cfg::BK, Cfg::BM, P.a_mn);
+          load_operand<Cfg>(sB, P.tmB, &full[stage], tn * Cfg::BN, kb * Cfg::BK, Cfg::BN, P.b_mn);
           if constexpr (Cfg::SPLIT) {
             uint8_t* sA2 = sB + Cfg::B_BYTES;
             uint8_t* sB2 = sA2 + Cfg::A_BYTES;
-            tma_load_2d(sA2, P.tmA_lo, &full[stage], kb * Cfg::BK, tm * Cfg::BM);
-            if constexpr (Cfg::BMN) {
-#pragma unroll
-              for (int q = 0; q < Cfg::B_ATOMS; ++q)
-                tma_load_2d(sB2 + q * Cfg::B_ATOM_BYTES, P.tmB_lo, &full[stage],
-                            tn * Cfg::BN + q * (128 / Cfg::ESZ), kb * Cfg::BK);
-            } else {
-              tma_load_2d(sB2, P.tmB_lo, &full[stage], kb * Cfg::BK, tn * Cfg::BN);
-            }
+            load_operand<Cfg>(sA2, P.tmA_lo, &full[stage], tm * Cfg::BM, kb * Cfg::BK, Cfg::BM, P.a_mn);
+            if constexpr (Cfg::LOB)
+              load_operand<Cfg>(sB2, P.tmB_lo, &full[stage], tn * Cfg::BN, kb * Cfg::BK, Cfg::BN, P.b_mn);
           }
           if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
         }
@@ -337,7 +512,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
       uint32_t acc_phase = 0;
       for (int t = blockIdx.x; t < L.ntiles; t += gridDim.x) {
         const uint32_t code = L.tiles[t];
-        const GemmProblem& P = L.probs[code >> 20];
+        const GemmProblem& P = probs[code >> 20];
         if (L.done && L.done[P.matrix * L.done_stride]) continue;
         const int nkb = (P.K + Cfg::BK - 1) / Cfg::BK;
         // tf32: one TMEM accumulation chunk per PROMO_KB k-blocks, promoted to fp32
@@ -352,22 +527,18 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
             tc_fence_after();
             const uint32_t aA = smem_u32(stage_base + stage * Cfg::STAGE_BYTES);
             const uint32_t aB = aA + Cfg::A_BYTES;
+            const uint32_t idesc = Cfg::IDESC | ((uint32_t)P.a_mn << 15) | ((uint32_t)P.b_mn << 16);
 #pragma unroll
             for (int k = 0; k < Cfg::BK / Cfg::UK; ++k) {
-              const uint64_t da = sdesc_sw128(aA + k * 32, 16, 1024);
-              const uint64_t db =
-                  Cfg::BMN ? sdesc_sw128<Cfg::BMN_LAYOUT>(aB + k * Cfg::UK * 128, Cfg::B_ATOM_BYTES, Cfg::BMN_SBO)
-                           : sdesc_sw128(aB + k * 32, 16, 1024);
-              umma<Cfg::KIND>(dt, da, db, Cfg::IDESC, (kb != kb0 || k != 0) ? 1u : 0u);
+              const uint64_t da = operand_desc<Cfg>(aA, k, P.a_mn);
+              const uint64_t db = operand_desc<Cfg>(aB, k, P.b_mn);
+              umma<Cfg::KIND>(dt, da, db, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
               if constexpr (Cfg::SPLIT) {
                 const uint32_t aA2 = aB + Cfg::B_BYTES;
                 const uint32_t aB2 = aA2 + Cfg::A_BYTES;
-                const uint64_t da2 = sdesc_sw128(aA2 + k * 32, 16, 1024);
-                const uint64_t db2 =
-                    Cfg::BMN ? sdesc_sw128<Cfg::BMN_LAYOUT>(aB2 + k * Cfg::UK * 128, Cfg::B_ATOM_BYTES, Cfg::BMN_SBO)
-                             : sdesc_sw128(aB2 + k * 32, 16, 1024);
-                umma<Cfg::KIND>(dt, da, db2, Cfg::IDESC, 1u);   // A_hi · B_lo
-                umma<Cfg::KIND>(dt, da2, db, Cfg::IDESC, 1u);   // A_lo · B_hi
+                const uint64_t da2 = operand_desc<Cfg>(aA2, k, P.a_mn);
+                if constexpr (Cfg::LOB) umma<Cfg::KIND>(dt, da, operand_desc<Cfg>(aB2, k, P.b_mn), idesc, 1u);   // A_hi · B_lo
+                umma<Cfg::KIND>(dt, da2, db, idesc, 1u);                                                          // A_lo · B_hi
               }
             }
             umma_commit(&empty[stage]);     // smem slot free once these MMAs retire
@@ -386,7 +557,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < L.ntiles; t += gridDim.x) {
       const uint32_t code = L.tiles[t];
-      const GemmProblem& P = L.probs[code >> 20];
+      const GemmProblem& P = probs[code >> 20];
       if (L.done && L.done[P.matrix * L.done_stride]) continue;
       const int tm = (code >> 10) & 1023, tn = code & 1023;
       const int mode = P.mode;
@@ -397,8 +568,17 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
       if (mode == EPI_APPLY && P.scale_by_alpha) coefA = static_cast<float>(*P.alpha);
       float sumsq = 0.f;
 
+      float* tb = tbuf + q * 32 * 33;
+      const int i0 = tm * Cfg::BM + q * 32;
+      const bool needC = (mode == EPI_POLY || mode == EPI_APPLY);
       if constexpr (Cfg::PROMO_KB >= (1 << 20)) {
-        // bf16: one TMEM accumulator per tile, consumed 32 columns at a time
+        // bf16: one TMEM accumulator per tile, consumed 32 columns at a time; the C row
+        // segment of chunk ch+1 is fetched while chunk ch is processed
+        float cbuf[32];
+#pragma unroll
+        for (int u = 0; u < 32; ++u) cbuf[u] = 0.f;
+        if (needC && i < P.M && tn * Cfg::BN < P.N)
+          load_row32<Cfg::KIND, Cfg::SPLIT>(P.C, P.C_lo, P.ldc, i, tn * Cfg::BN, P.N, cbuf);
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
         const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * Cfg::BN;
@@ -411,7 +591,19 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
           float d[32];
 #pragma unroll
           for (int u = 0; u < 32; ++u) d[u] = __uint_as_float(r[u]);
-          epi_segment<Cfg>(P, mode, sym, i, tn * Cfg::BN + ch * 32, coefA, coefC, d, sumsq);
+          if constexpr (Cfg::BN == 32) {
+            epi_chain<Cfg>(P, i, tm, d, dred, q, lane, et);
+          } else {
+            float cnext[32];
+#pragma unroll
+            for (int u = 0; u < 32; ++u) cnext[u] = 0.f;
+            const int jn = tn * Cfg::BN + (ch + 1) * 32;
+            if (needC && ch + 1 < Cfg::BN / 32 && i < P.M && jn < P.N)
+              load_row32<Cfg::KIND, Cfg::SPLIT>(P.C, P.C_lo, P.ldc, i, jn, P.N, cnext);
+            epi_segment<Cfg>(P, mode, sym, i0, lane, tn * Cfg::BN + ch * 32, coefA, coefC, d, cbuf, tb, sumsq);
+#pragma unroll
+            for (int u = 0; u < 32; ++u) cbuf[u] = cnext[u];
+          }
         }
         tc_fence_before();
         mbar_arrive(&tempty[acc]);
@@ -441,8 +633,18 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
           if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
 #pragma unroll
-        for (int ch = 0; ch < Cfg::BN / 32; ++ch)
-          epi_segment<Cfg>(P, mode, sym, i, tn * Cfg::BN + ch * 32, coefA, coefC, d[ch], sumsq);
+        for (int ch = 0; ch < Cfg::BN / 32; ++ch) {
+          if constexpr (Cfg::BN == 32) {
+            epi_chain<Cfg>(P, i, tm, d[ch], dred, q, lane, et);
+          } else {
+            float c[32];
+#pragma unroll
+            for (int u = 0; u < 32; ++u) c[u] = 0.f;
+            const int j0 = tn * Cfg::BN + ch * 32;
+            if (needC && i < P.M && j0 < P.N) load_row32<Cfg::KIND, Cfg::SPLIT>(P.C, P.C_lo, P.ldc, i, j0, P.N, c);
+            epi_segment<Cfg>(P, mode, sym, i0, lane, j0, coefA, coefC, d[ch], c, tb, sumsq);
+          }
+        }
       }
 
       if (mode == EPI_RESID && P.norm_part) {
@@ -461,7 +663,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+    tmem_dealloc(tmem_base, Cfg::TMEM_ALLOC);
   }
 }
 

@@ -40,25 +40,36 @@ struct MatDesc {
   float* norm_part;    // Gram per-tile partials
   int tiles_m, tiles_n, sym;
   int pad_;
-  float* S;            // [p x s] sketch
-  float* chain;        // chain buffers: 5 blocks of [s x 2p]
+  float* S;            // [p x ldS] sketch S_k (fp32)
+  void* W[2];          // chain B operands [4p x ldS] (compute dtype), hi rows then lo rows
+  float* keep;         // [4][s][p] kept chain columns (fp32)
+  double* chain_part;  // [tiles_m][6] per-tile <Va,Vb>
+  long long ldS;
+  int chain_tiles;
+  int pad2_;
 };
 
 struct SolveParams {
   MatDesc* mats;
   MatState* st;
-  double* alpha_hist;   // [batch * max_iters] or null (user)
-  float* resid_hist;    // [batch * (max_iters+1)] or null (user)
-  int32_t* rep_iters;   // user report (device) or null
+  int* iter;            // device iteration counter k (workspace)
+  double* alpha_hist;   // [batch * max_iters] (workspace; copied to the user's report)
+  float* resid_hist;    // [batch * (max_iters+1)] (workspace)
+  int32_t* rep_iters;   // user report (device) or null — only used by k_report
   float* rep_resid;
   int32_t* rep_status;
+  double* rep_alphas;
+  float* rep_resid_hist;
   double* fro_part;     // [batch * kFroParts]
+  const int* tile_off;  // [batch + 1] prefix of 64x64 layout tiles (normalise: Xt; finalise: output)
+  const int* out_tile_off;
+  int n_tiles, n_out_tiles;
   int batch, p, d, max_iters, warmup, fit, precision, kind_sqrt;
   double tol, alo, ahi, ataylor;
   unsigned long long seed;
 };
 
-constexpr int kFroParts = 32;
+constexpr int kFroParts = 256;   // row-strided partial sums per matrix (fixed order)
 
 // ----------------------------------------------------------------- helpers
 __device__ __forceinline__ float load_val(const void* base, long long idx, int prec_bf16) {
@@ -87,20 +98,59 @@ __device__ __forceinline__ T block_sum(T v, T* scratch) {
 }
 
 // ----------------------------------------------------------------- a1: ||A||_F partials
-// grid (kFroParts, batch), 256 threads; block j handles rows r = j, j+kFroParts, ...
+// grid (kFroParts, batch), 256 threads; block j handles rows r = j, j + kFroParts, ...
+// with 16-byte vector loads when the row layout allows it.
 __global__ void __launch_bounds__(256) k_fro_partials(SolveParams P) {
   __shared__ double scratch[8];
   const MatDesc& D = P.mats[blockIdx.y];
   const int bf16 = P.precision == 0;
+  const int esz = bf16 ? 2 : 4, vec = 16 / esz;
+  const bool vok = ((D.lda * esz) % 16 == 0) && ((reinterpret_cast<uintptr_t>(D.A) & 15) == 0);
   double acc = 0.0;
   for (int r = blockIdx.x; r < D.m; r += kFroParts) {
-    for (int c = threadIdx.x; c < D.n; c += 256) {
-      double x = (double)load_val(D.A, (long long)r * D.lda + c, bf16);
+    const char* row = static_cast<const char*>(D.A) + (long long)r * D.lda * esz;
+    const int nv = vok ? D.n / vec : 0;
+    for (int c = threadIdx.x; c < nv; c += 256) {
+      const uint4 w = __ldg(reinterpret_cast<const uint4*>(row) + c);
+      if (bf16) {
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(h[e]);
+          acc += (double)f.x * f.x + (double)f.y * f.y;
+        }
+      } else {
+        const float* f = reinterpret_cast<const float*>(&w);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc += (double)f[e] * f[e];
+      }
+    }
+    for (int c = nv * vec + threadIdx.x; c < D.n; c += 256) {
+      const double x = (double)load_val(D.A, (long long)r * D.lda + c, bf16);
       acc += x * x;
     }
   }
   acc = block_sum<double, 256>(acc, scratch);
   if (threadIdx.x == 0) P.fro_part[blockIdx.y * kFroParts + blockIdx.x] = acc;
+}
+
+// c = ||A||_F per matrix from the row-strided partials (fixed-order tree); one block per matrix
+__global__ void __launch_bounds__(256) k_fro_final(SolveParams P) {
+  __shared__ double scratch[8];
+  const int b = blockIdx.x;
+  double v = (threadIdx.x < kFroParts) ? P.fro_part[b * kFroParts + threadIdx.x] : 0.0;
+  v = block_sum<double, 256>(v, scratch);
+  if (threadIdx.x == 0) P.st[b].c = sqrt(v);
+}
+
+// block -> (matrix, tile) over a batch-wide flat tile list (prefix array off[batch + 1])
+__device__ __forceinline__ int find_matrix(const int* off, int batch, int t) {
+  int lo = 0, hi = batch - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (off[mid] <= t) lo = mid; else hi = mid - 1;
+  }
+  return lo;
 }
 
 __device__ __forceinline__ void store_x(void* hi, void* lo, long long idx, float v, int precision) {
@@ -115,48 +165,107 @@ __device__ __forceinline__ void store_x(void* hi, void* lo, long long idx, float
   }
 }
 
-// a1: X_0 = A / ||A||_F in the compute layout (polar: Xt = s x L), Y_0 = I (sqrt),
-// state init.  grid (ceil(cols/32), ceil(rows/32), batch) over the *output* Xt,
-// 32x8 threads with a smem transpose for the tall case.
-__global__ void __launch_bounds__(256) k_normalize(SolveParams P) {
-  __shared__ float tile[32][33];
-  const int b = blockIdx.z;
-  const MatDesc& D = P.mats[b];
-  // every block recomputes c from the fixed-order partials (deterministic)
-  double ss = 0.0;
-  for (int j = 0; j < kFroParts; ++j) ss += P.fro_part[b * kFroParts + j];
-  const double c = sqrt(ss);
-  const float inv = c > 0.0 ? (float)(1.0 / c) : 0.f;
-  const int bf16 = P.precision == 0;
-  const int rows = P.kind_sqrt ? D.n : D.s;   // rows of Xt
-  const int cols = P.kind_sqrt ? D.n : D.L;
-  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
-  if (r0 >= rows || c0 >= cols) return;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  if (D.trans) {
-    // Xt[r][c] = A[c][r]: read A rows c0.. (coalesced over r), transpose through smem
-    for (int k = ty; k < 32; k += 8) {
-      const int ar = c0 + k, ac = r0 + tx;
-      tile[k][tx] = (ar < D.m && ac < D.n) ? load_val(D.A, (long long)ar * D.lda + ac, bf16) : 0.f;
-    }
-    __syncthreads();
-    for (int k = ty; k < 32; k += 8) {
-      const int xr = r0 + k, xc = c0 + tx;
-      if (xr < rows && xc < cols) store_x(D.X[0], D.X_lo[0], (long long)xr * D.ldx + xc, tile[tx][k] * inv, P.precision);
-    }
-  } else {
-    for (int k = ty; k < 32; k += 8) {
-      const int xr = r0 + k, xc = c0 + tx;
-      if (xr < rows && xc < cols) {
-        float v = load_val(D.A, (long long)xr * D.lda + xc, bf16) * inv;
-        store_x(D.X[0], D.X_lo[0], (long long)xr * D.ldx + xc, v, P.precision);
-        if (P.kind_sqrt) store_x(D.Y[0], D.Y_lo[0], (long long)xr * D.ldx + xc, xr == xc ? 1.f : 0.f, P.precision);
+// Layout tiles (normalise / finalise): 32 rows x 32 16-byte vectors, one block
+// (256 threads, 4 vectors each, a warp = one 512-B row segment) per tile over a
+// batch-wide flat list.  X keeps A's row-major layout, so both are scaled copies.
+template <int PREC>   // 0 bf16, 1 fp32 hi+lo (3xTF32 split), 2 fp32
+struct Vec {
+  static constexpr int ESZ = PREC == 0 ? 2 : 4;
+  static constexpr int VE = 16 / ESZ;
+  float v[VE];
+  __device__ __forceinline__ void load(const void* base, const void* lo, long long idx, int n_valid, bool vec) {
+    if (PREC == 0) {
+      const __nv_bfloat16* p = static_cast<const __nv_bfloat16*>(base) + idx;
+      if (vec) {
+        const uint4 w = __ldg(reinterpret_cast<const uint4*>(p));
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) { const float2 f = __bfloat1622float2(h[e]); v[2 * e] = f.x; v[2 * e + 1] = f.y; }
+      } else {
+#pragma unroll
+        for (int e = 0; e < VE; ++e) v[e] = e < n_valid ? __bfloat162float(p[e]) : 0.f;
+      }
+    } else {
+      const float* p = static_cast<const float*>(base) + idx;
+      const float* q = (PREC == 1 && lo) ? static_cast<const float*>(lo) + idx : nullptr;
+      if (vec) {
+        const float4 w = __ldg(reinterpret_cast<const float4*>(p));
+        v[0] = w.x; v[1] = w.y; v[2] = w.z; v[3] = w.w;
+        if (q) { const float4 l = __ldg(reinterpret_cast<const float4*>(q)); v[0] += l.x; v[1] += l.y; v[2] += l.z; v[3] += l.w; }
+      } else {
+#pragma unroll
+        for (int e = 0; e < VE; ++e) v[e] = e < n_valid ? p[e] + (q ? q[e] : 0.f) : 0.f;
       }
     }
   }
-  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+  // store v * scale; split (PREC 1) writes tf32-truncated hi and the remainder to lo
+  __device__ __forceinline__ void store(void* base, void* lo, long long idx, int n_valid, bool vec, float scale,
+                                        bool split) const {
+    if (PREC == 0) {
+      __nv_bfloat16* p = static_cast<__nv_bfloat16*>(base) + idx;
+      if (vec) {
+        uint4 w;
+        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&w);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(v[2 * e] * scale, v[2 * e + 1] * scale);
+        *reinterpret_cast<uint4*>(p) = w;
+      } else {
+#pragma unroll
+        for (int e = 0; e < VE; ++e) if (e < n_valid) p[e] = __float2bfloat16_rn(v[e] * scale);
+      }
+    } else {
+      float* p = static_cast<float*>(base) + idx;
+      float* q = split ? static_cast<float*>(lo) + idx : nullptr;
+      float o[VE], h[VE];
+#pragma unroll
+      for (int e = 0; e < VE; ++e) {
+        o[e] = v[e] * scale;
+        h[e] = split ? __uint_as_float(__float_as_uint(o[e]) & 0xFFFFE000u) : o[e];
+      }
+      if (vec) {
+        *reinterpret_cast<float4*>(p) = make_float4(h[0], h[1], h[2], h[3]);
+        if (q) *reinterpret_cast<float4*>(q) = make_float4(o[0] - h[0], o[1] - h[1], o[2] - h[2], o[3] - h[3]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < VE; ++e)
+          if (e < n_valid) { p[e] = h[e]; if (q) q[e] = o[e] - h[e]; }
+      }
+    }
+  }
+};
+
+// a1: X_0 = A / ||A||_F (same row-major layout), Y_0 = I (sqrt), state init.
+template <int PREC>
+__global__ void __launch_bounds__(256) k_normalize(SolveParams P) {
+  using V = Vec<PREC>;
+  const int t = blockIdx.x;
+  const int b = find_matrix(P.tile_off, P.batch, t);
+  const MatDesc& D = P.mats[b];
+  const double c = P.st[b].c;   // written by k_fro_final
+  const float inv = c > 0.0 ? (float)(1.0 / c) : 0.f;
+  const int TW = 32 * V::VE;
+  const int tcn = (D.n + TW - 1) / TW;
+  const int lt = t - P.tile_off[b];
+  const int r0 = (lt / tcn) * 32, c0 = (lt % tcn) * TW;
+  const bool src_vec = ((D.lda * V::ESZ) % 16 == 0) && ((reinterpret_cast<uintptr_t>(D.A) & 15) == 0);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int slot = threadIdx.x + 256 * j;
+    const int r = r0 + slot / 32, col = c0 + (slot % 32) * V::VE;
+    if (r >= D.m || col >= D.n) continue;
+    const int nv = min(V::VE, D.n - col);
+    V x;
+    x.load(D.A, nullptr, (long long)r * D.lda + col, nv, src_vec && nv == V::VE);
+    x.store(D.X[0], D.X_lo[0], (long long)r * D.ldx + col, nv, nv == V::VE, inv, PREC == 1);
+    if (P.kind_sqrt) {
+#pragma unroll
+      for (int e = 0; e < V::VE; ++e) x.v[e] = (col + e == r) ? 1.f : 0.f;
+      x.store(D.Y[0], D.Y_lo[0], (long long)r * D.ldx + col, nv, nv == V::VE, 1.f, PREC == 1);
+    }
+  }
+  if (lt == 0 && threadIdx.x == 0) {
+    if (b == 0) *P.iter = 0;
     MatState& S = P.st[b];
-    S.c = c;
     S.alpha = P.ataylor;
     S.r_prev = INFINITY;
     S.resid = 0.f;
@@ -248,133 +357,57 @@ __device__ void portable_sincos_2pi(unsigned long long K, double* so, double* co
   }
 }
 
-// S_k (p x s, fp32) for every active matrix.  grid (ceil(p*s/2/256), batch).
-__global__ void __launch_bounds__(256) k_sketch(SolveParams P, int k) {
-  const int b = blockIdx.y;
-  const MatDesc& D = P.mats[b];
-  if (P.st[b].done) return;
-  const int s = D.s;
-  const long long total = (long long)P.p * s;
-  const long long e = (long long)blockIdx.x * 256 + threadIdx.x;   // pair index
-  if (2 * e >= total) return;
-  uint32_t ctr[4] = {(uint32_t)e, (uint32_t)k, (uint32_t)D.sketch_id, 0x534B4348u};
-  philox10(ctr, (uint32_t)(P.seed & 0xFFFFFFFFull), (uint32_t)(P.seed >> 32));
+__device__ __forceinline__ void sketch_pair(unsigned long long seed, uint32_t k, uint32_t b, uint32_t e, double* z0,
+                                            double* z1) {
+  uint32_t ctr[4] = {e, k, b, 0x534B4348u};
+  philox10(ctr, (uint32_t)(seed & 0xFFFFFFFFull), (uint32_t)(seed >> 32));
   const unsigned long long K1 = ((unsigned long long)(ctr[0] >> 5) << 26) + (ctr[1] >> 6);
   const unsigned long long K2 = ((unsigned long long)(ctr[2] >> 5) << 26) + (ctr[3] >> 6);
   const double u1 = dmul((double)(K1 + 1ull), 0x1p-53);   // (0, 1], exact
   const double rad = __dsqrt_rn(dmul(-2.0, portable_log(u1)));
   double sn, cs;
   portable_sincos_2pi(K2, &sn, &cs);
-  D.S[2 * e] = __double2float_rn(dmul(rad, cs));
-  if (2 * e + 1 < total) D.S[2 * e + 1] = __double2float_rn(dmul(rad, sn));
+  *z0 = dmul(rad, cs);   // even element: cos
+  *z1 = dmul(rad, sn);   // odd element: sin
 }
 
-// ----------------------------------------------------------------- a4: sketch chain
-// OUT[i][c] = sum_j R[i][j] * IN[j][c], c < w (<= 16), fp32 accumulate.
-// IN is staged per j-chunk into smem as [c][j] from one of the sources:
-enum ChainSrc : int { SRC_S = 0, SRC_K1Q = 1, SRC_Q = 2, SRC_BUF = 3 };
-struct ChainPass {
-  int src, w, in_off, in_ld;   // SRC_BUF: IN[j][c] = in[j*in_ld + in_off + c]
-  int in_blk, out_blk;         // chain block indices (each [s x 2p] floats)
-};
-constexpr int kChainRows = 32;     // rows per block (4 per warp)
-constexpr int kChainJC = 256;      // j-chunk
+__device__ __forceinline__ void store_split(void* W, long long idx_hi, long long idx_lo, float v, int bf16) {
+  if (bf16) {
+    const __nv_bfloat16 h = __float2bfloat16_rn(v);
+    static_cast<__nv_bfloat16*>(W)[idx_hi] = h;
+    static_cast<__nv_bfloat16*>(W)[idx_lo] = __float2bfloat16_rn(v - __bfloat162float(h));
+  } else {
+    const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+    static_cast<float*>(W)[idx_hi] = h;
+    static_cast<float*>(W)[idx_lo] = v - h;
+  }
+}
 
-template <int BF16>
-__global__ void __launch_bounds__(256) k_chain(SolveParams P, ChainPass C) {
-  __shared__ float sIn[16][kChainJC + 2];
+// S_k (p x s, fp32) for every active matrix, and the first chain operand
+// W[0] = [S_hi ; S_lo] (compute dtype).  grid (ceil(p*s/2/256), batch).
+__device__ __forceinline__ bool fit_at(const SolveParams& P, int k) {
+  return P.fit == 0 && k < P.max_iters && k >= P.warmup;
+}
+
+__global__ void __launch_bounds__(256) k_sketch(SolveParams P) {
   const int b = blockIdx.y;
   const MatDesc& D = P.mats[b];
-  if (P.st[b].done) return;
-  const int s = D.s, p = P.p, w = C.w;
-  const int row0 = blockIdx.x * kChainRows;
-  if (row0 >= s) return;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const size_t blk = (size_t)s * 2 * p;
-  const float* in = D.chain + C.in_blk * blk;
-  float* out = D.chain + C.out_blk * blk;
-  float acc[4][16];
-#pragma unroll
-  for (int r = 0; r < 4; ++r)
-#pragma unroll
-    for (int c = 0; c < 16; ++c) acc[r][c] = 0.f;
-
-  for (int j0 = 0; j0 < s; j0 += kChainJC) {
-    __syncthreads();
-    // stage IN[j0 .. j0+JC) into sIn[c][jj]
-    for (int idx = threadIdx.x; idx < w * kChainJC; idx += 256) {
-      const int c = idx / kChainJC, jj = idx - c * kChainJC, j = j0 + jj;
-      float v = 0.f;
-      if (j < s) {
-        if (C.src == SRC_S) {
-          v = D.S[(size_t)c * s + j];
-        } else if (C.src == SRC_BUF) {
-          v = in[(size_t)j * C.in_ld + C.in_off + c];
-        } else {
-          // K1 = R S^T (chain block in_blk, [s][p]); Q = G S^T with G_jj exact in fp32:
-          // Q_j = G_jj S_j - (K1_j - R_jj S_j)   (off-diagonal part of -R S^T)
-          const int cc = (C.src == SRC_K1Q && c < p) ? c : (C.src == SRC_K1Q ? c - p : c);
-          const float k1 = in[(size_t)j * p + cc];
-          if (C.src == SRC_K1Q && c < p) {
-            v = k1;
-          } else {
-            const float sj = D.S[(size_t)cc * s + j];
-            float rjj;
-            if (BF16) rjj = __bfloat162float(static_cast<const __nv_bfloat16*>(D.R)[(size_t)j * D.ldr + j]);
-            else rjj = static_cast<const float*>(D.R)[(size_t)j * D.ldr + j] +
-                       (D.R_lo ? static_cast<const float*>(D.R_lo)[(size_t)j * D.ldr + j] : 0.f);
-            v = D.gdiag[j] * sj - (k1 - rjj * sj);
-          }
-        }
-      }
-      sIn[c][jj] = v;
-    }
-    __syncthreads();
-    // each warp: 4 rows; lanes over j pairs
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int i = row0 + warp * 4 + r;
-      if (i >= s) break;
-      for (int jj = 2 * lane; jj < kChainJC; jj += 64) {
-        const int j = j0 + jj;
-        if (j >= s) break;
-        float r0, r1;
-        if (BF16) {
-          const __nv_bfloat16* rp = static_cast<const __nv_bfloat16*>(D.R) + (size_t)i * D.ldr + j;
-          if (j + 1 < s) {
-            float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(rp));
-            r0 = f.x; r1 = f.y;
-          } else {
-            r0 = __bfloat162float(rp[0]); r1 = 0.f;
-          }
-        } else {
-          const float* rp = static_cast<const float*>(D.R) + (size_t)i * D.ldr + j;
-          const float* rl = D.R_lo ? static_cast<const float*>(D.R_lo) + (size_t)i * D.ldr + j : nullptr;
-          r0 = rp[0] + (rl ? rl[0] : 0.f);
-          r1 = (j + 1 < s) ? rp[1] + (rl ? rl[1] : 0.f) : 0.f;
-        }
-#pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          if (c < w) {
-            const float2 x = *reinterpret_cast<const float2*>(&sIn[c][jj]);
-            acc[r][c] = fmaf(r0, x.x, acc[r][c]);
-            acc[r][c] = fmaf(r1, x.y, acc[r][c]);
-          }
-        }
-      }
-    }
-  }
-  // reduce over lanes (fixed tree) and store
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const int i = row0 + warp * 4 + r;
-#pragma unroll
-    for (int c = 0; c < 16; ++c) {
-      float v = acc[r][c];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0 && c < w && i < s) out[(size_t)i * w + c] = v;
-    }
+  const int k = *P.iter;
+  if (!fit_at(P, k) || P.st[b].done) return;
+  const int s = D.s, p = P.p;
+  const long long total = (long long)p * s;
+  const long long e = (long long)blockIdx.x * 256 + threadIdx.x;   // pair index
+  if (2 * e >= total) return;
+  double z[2];
+  sketch_pair(P.seed, (uint32_t)k, (uint32_t)D.sketch_id, (uint32_t)e, &z[0], &z[1]);
+  const int bf16 = P.precision == 0;
+  for (int t = 0; t < 2; ++t) {
+    const long long q = 2 * e + t;
+    if (q >= total) break;
+    const int row = (int)(q / s), col = (int)(q - (long long)row * s);
+    const float v = __double2float_rn(z[t]);
+    D.S[(long long)row * D.ldS + col] = v;
+    store_split(D.W[0], (long long)row * D.ldS + col, (long long)(p + row) * D.ldS + col, v, bf16);
   }
 }
 
@@ -455,9 +488,11 @@ __device__ double argmin_quartic(const double c[5], double lo, double hi, double
 
 // One block (256 threads) per matrix: residual norm, stop test (R12), and
 // alpha_k from the factored sketched loss m(a) = ||V0 + a V1 + a^2 V2||^2.
-__global__ void __launch_bounds__(256) k_alpha(SolveParams P, int k, int do_fit) {
+__global__ void __launch_bounds__(256) k_alpha(SolveParams P) {
   __shared__ double scratch[8];
   __shared__ int s_stop;
+  const int k = *P.iter;
+  const int do_fit = fit_at(P, k) ? 1 : 0;
   const int b = blockIdx.x;
   const MatDesc& D = P.mats[b];
   MatState& S = P.st[b];
@@ -475,7 +510,7 @@ __global__ void __launch_bounds__(256) k_alpha(SolveParams P, int k, int do_fit)
   const double r2 = block_sum<double, 256>(part, scratch);
   const double r = sqrt(r2);
   if (threadIdx.x == 0) {
-    if (P.resid_hist) P.resid_hist[(size_t)b * (P.max_iters + 1) + k] = (float)(r / sqrt((double)s));
+    P.resid_hist[(size_t)b * (P.max_iters + 1) + k] = (float)(r / sqrt((double)s));
     int stop = 0, status = 1;
     if (!isfinite(r)) { stop = 1; status = 3; }
     else if (r <= P.tol * sqrt((double)s)) { stop = 1; status = 0; }
@@ -501,101 +536,97 @@ __global__ void __launch_bounds__(256) k_alpha(SolveParams P, int k, int do_fit)
   if (!do_fit) {
     a = (k < P.warmup) ? P.ahi : P.ataylor;
   } else {
-    // V vectors from the chain blocks (factored form R17)
-    const int p = P.p;
-    const size_t blk = (size_t)s * 2 * p;
-    const float* ch = D.chain;
+    // <Va, Vb> from the chain GEMM's per-tile partials (fixed order, R17)
     double g00 = 0, g01 = 0, g02 = 0, g11 = 0, g12 = 0, g22 = 0;
-    for (int e = threadIdx.x; e < s * p; e += 256) {
-      const int i = e / p, c = e - i * p;
-      double v0, v1, v2;
-      if (P.d == 1) {
-        // blk0 = K1 [s][p]; blk1 = L1 [s][p]; blk2 = L2 [s][p]
-        v0 = (double)ch[0 * blk + (size_t)i * p + c];
-        v1 = -2.0 * (double)ch[1 * blk + (size_t)i * p + c];
-        v2 = -(double)ch[2 * blk + (size_t)i * p + c];
-      } else {
-        // blk1 = [K2 | L1] [s][2p]; blk2 = [K3 | L2] [s][2p]; blk3 = L3 [s][p]; blk4 = L4 [s][p]
-        const double K2 = ch[1 * blk + (size_t)i * 2 * p + c];
-        const double K3 = ch[2 * blk + (size_t)i * 2 * p + c];
-        const double L2 = ch[2 * blk + (size_t)i * 2 * p + p + c];
-        const double L3 = ch[3 * blk + (size_t)i * p + c];
-        const double L4 = ch[4 * blk + (size_t)i * p + c];
-        v0 = 0.25 * (3.0 * K2 + K3);
-        v1 = -(L3 + 2.0 * L2);
-        v2 = -L4;
-      }
-      g00 += v0 * v0; g01 += v0 * v1; g02 += v0 * v2;
-      g11 += v1 * v1; g12 += v1 * v2; g22 += v2 * v2;
+    for (int t = 0; t < D.chain_tiles; ++t) {
+      const double* cp = D.chain_part + 6 * t;
+      g00 += cp[0]; g01 += cp[1]; g02 += cp[2]; g11 += cp[3]; g12 += cp[4]; g22 += cp[5];
     }
-    g00 = block_sum<double, 256>(g00, scratch);
-    g01 = block_sum<double, 256>(g01, scratch);
-    g02 = block_sum<double, 256>(g02, scratch);
-    g11 = block_sum<double, 256>(g11, scratch);
-    g12 = block_sum<double, 256>(g12, scratch);
-    g22 = block_sum<double, 256>(g22, scratch);
     double c[5] = {g00, 2.0 * g01, g11 + 2.0 * g02, 2.0 * g12, g22};
     a = (k < P.warmup) ? P.ahi : argmin_quartic(c, P.alo, P.ahi, P.ataylor);
   }
   if (threadIdx.x == 0) {
     S.alpha = a;
-    if (P.alpha_hist) P.alpha_hist[(size_t)b * P.max_iters + k] = a;
+    P.alpha_hist[(size_t)b * P.max_iters + k] = a;
   }
 }
 
 // ----------------------------------------------------------------- a7: outputs
-// Polar: Q = Xt^T (tall) or Xt (wide); sqrt: A^{1/2} = sqrt(c) X, A^{-1/2} = Y/sqrt(c).
+// a7: polar Q = X_final; sqrt A^{1/2} = sqrt(c) X, A^{-1/2} = Y / sqrt(c) (cast to the user dtype).
+template <int PREC>
 __global__ void __launch_bounds__(256) k_finalize(SolveParams P) {
-  __shared__ float tile[32][33];
-  const int b = blockIdx.z;
+  using V = Vec<PREC>;
+  using VO = Vec<PREC == 0 ? 0 : 2>;   // user output: bf16 or plain fp32
+  const int t = blockIdx.x;
+  const int b = find_matrix(P.out_tile_off, P.batch, t);
   const MatDesc& D = P.mats[b];
   const MatState& S = P.st[b];
   const int par = S.iters & 1;
-  const int bf16 = P.precision == 0;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;   // over the *output* (m x n)
-  auto ld = [&](const void* hi, const void* lo, long long idx) -> float {
-    float v = load_val(hi, idx, bf16);
-    if (P.precision == 1 && lo) v += static_cast<const float*>(lo)[idx];
-    return v;
-  };
-  auto st = [&](void* q, long long idx, float v) {
-    if (bf16) static_cast<__nv_bfloat16*>(q)[idx] = __float2bfloat16_rn(v);
-    else static_cast<float*>(q)[idx] = v;
-  };
-  if (r0 >= D.m || c0 >= D.n) return;
-  if (P.kind_sqrt) {
-    const float fs = (float)sqrt(S.c);
-    const float fi = S.c > 0.0 ? (float)(1.0 / sqrt(S.c)) : 0.f;
-    for (int k = ty; k < 32; k += 8) {
-      const int r = r0 + k, c = c0 + tx;
-      if (r < D.m && c < D.n) {
-        const long long xi = (long long)r * D.ldx + c;
-        if (D.Q) st(D.Q, (long long)r * D.ldq + c, S.c > 0.0 ? fs * ld(D.X[par], D.X_lo[par], xi) : 0.f);
-        if (D.Q2) st(D.Q2, (long long)r * D.ldq + c, fi * ld(D.Y[par], D.Y_lo[par], xi));
-      }
+  const int TW = 32 * V::VE;
+  const int tcn = (D.n + TW - 1) / TW;
+  const int lt = t - P.out_tile_off[b];
+  const int r0 = (lt / tcn) * 32, c0 = (lt % tcn) * TW;
+  const float fs = P.kind_sqrt ? (float)sqrt(S.c) : 1.f;
+  const float fi = (P.kind_sqrt && S.c > 0.0) ? (float)(1.0 / sqrt(S.c)) : 0.f;
+  const bool q_vec = ((D.ldq * V::ESZ) % 16 == 0);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int slot = threadIdx.x + 256 * j;
+    const int r = r0 + slot / 32, col = c0 + (slot % 32) * V::VE;
+    if (r >= D.m || col >= D.n) continue;
+    const int nv = min(V::VE, D.n - col);
+    const long long xi = (long long)r * D.ldx + col, qi = (long long)r * D.ldq + col;
+    if (D.Q) {
+      V x;
+      x.load(D.X[par], D.X_lo[par], xi, nv, nv == V::VE);
+      VO o;
+#pragma unroll
+      for (int e = 0; e < V::VE; ++e) o.v[e] = x.v[e];
+      const bool vq = q_vec && nv == V::VE && ((reinterpret_cast<uintptr_t>(D.Q) & 15) == 0);
+      o.store(D.Q, nullptr, qi, nv, vq, (P.kind_sqrt && S.c > 0.0) ? fs : (P.kind_sqrt ? 0.f : 1.f), false);
     }
-  } else if (D.trans) {
-    // Q[r][c] = Xt[c][r]
-    for (int k = ty; k < 32; k += 8) {
-      const int xr = c0 + k, xc = r0 + tx;
-      tile[k][tx] = (xr < D.n && xc < D.m) ? ld(D.X[par], D.X_lo[par], (long long)xr * D.ldx + xc) : 0.f;
-    }
-    __syncthreads();
-    for (int k = ty; k < 32; k += 8) {
-      const int r = r0 + k, c = c0 + tx;
-      if (r < D.m && c < D.n) st(D.Q, (long long)r * D.ldq + c, tile[tx][k]);
-    }
-  } else {
-    for (int k = ty; k < 32; k += 8) {
-      const int r = r0 + k, c = c0 + tx;
-      if (r < D.m && c < D.n) st(D.Q, (long long)r * D.ldq + c, ld(D.X[par], D.X_lo[par], (long long)r * D.ldx + c));
+    if (P.kind_sqrt && D.Q2) {
+      V y;
+      y.load(D.Y[par], D.Y_lo[par], xi, nv, nv == V::VE);
+      VO o;
+#pragma unroll
+      for (int e = 0; e < V::VE; ++e) o.v[e] = y.v[e];
+      const bool vq = q_vec && nv == V::VE && ((reinterpret_cast<uintptr_t>(D.Q2) & 15) == 0);
+      o.store(D.Q2, nullptr, qi, nv, vq, fi, false);
     }
   }
-  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
-    if (P.rep_iters) P.rep_iters[b] = S.iters;
-    if (P.rep_resid) P.rep_resid[b] = S.resid;
-    if (P.rep_status) P.rep_status[b] = S.status;
+}
+
+// End of one loop iteration: k <- k + 1; keep looping while any matrix is active.
+// (In the CUDA-graph path this sets the WHILE node's condition on the device.)
+__global__ void k_advance(SolveParams P, cudaGraphConditionalHandle handle, int use_handle, int* all_done_out) {
+  __shared__ int active;
+  if (threadIdx.x == 0) active = 0;
+  __syncthreads();
+  int a = 0;
+  for (int b = threadIdx.x; b < P.batch; b += blockDim.x) a |= !P.st[b].done;
+  if (a) atomicOr(&active, 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *P.iter = *P.iter + 1;
+    if (all_done_out) *all_done_out = active ? 0 : 1;
+    if (use_handle) cudaGraphSetConditional(handle, active ? 1u : 0u);
+  }
+}
+
+// Copy the solve's report (state + histories kept in the workspace) to the caller's buffers.
+__global__ void k_report(SolveParams P) {
+  const int nh = P.max_iters, nr = P.max_iters + 1;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.batch * nr; i += gridDim.x * blockDim.x) {
+    const int b = i / nr, k = i - b * nr;
+    const int it = P.st[b].iters;
+    if (P.rep_resid_hist) P.rep_resid_hist[i] = (k <= it) ? P.resid_hist[i] : __int_as_float(0x7fc00000);
+    if (P.rep_alphas && k < nh) P.rep_alphas[(size_t)b * nh + k] = (k < it) ? P.alpha_hist[(size_t)b * nh + k] : __longlong_as_double(0x7ff8000000000000ll);
+    if (k == 0) {
+      if (P.rep_iters) P.rep_iters[b] = it;
+      if (P.rep_resid) P.rep_resid[b] = P.st[b].resid;
+      if (P.rep_status) P.rep_status[b] = P.st[b].status;
+    }
   }
 }
 

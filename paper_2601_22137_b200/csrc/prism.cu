@@ -52,7 +52,9 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-enum OpKind { OP_A = 0, OP_BK = 1, OP_BMN = 2 };
+// OP_A: K-major A tile (box BK x 128); OP_BK: K-major B tile (box BK x BN);
+// OP_MN: MN-major operand (box 128-B x BK), A or B.
+enum OpKind { OP_A = 0, OP_BK = 1, OP_MN = 2 };
 
 struct MapSpec {
   const void* ptr;
@@ -75,7 +77,7 @@ bool encode_map(CUtensorMap* out, const MapSpec& s) {
   cuuint32_t es[2] = {1, 1};
   CUresult r = fn(out, s.esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
                   const_cast<void*>(s.ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  (s.kind == OP_BMN && s.esz == 4) ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                  (s.kind == OP_MN && s.esz == 4) ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
@@ -109,12 +111,16 @@ cudaError_t launch_gemm_cfg(const GemmLaunch& L, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_gemm(int precision, bool bmn, const GemmLaunch& L, cudaStream_t st) {
-  if (precision == PRISM_BF16)
-    return bmn ? launch_gemm_cfg<GemmCfg<0, false, true>>(L, st) : launch_gemm_cfg<GemmCfg<0, false, false>>(L, st);
-  if (precision == PRISM_FP32)
-    return bmn ? launch_gemm_cfg<GemmCfg<1, true, true>>(L, st) : launch_gemm_cfg<GemmCfg<1, true, false>>(L, st);
-  return bmn ? launch_gemm_cfg<GemmCfg<1, false, true>>(L, st) : launch_gemm_cfg<GemmCfg<1, false, false>>(L, st);
+cudaError_t launch_chain(int precision, const GemmLaunch& L, cudaStream_t st) {
+  if (precision == PRISM_BF16) return launch_gemm_cfg<GemmCfg<0, false, 32>>(L, st);
+  if (precision == PRISM_FP32) return launch_gemm_cfg<GemmCfg<1, true, 32>>(L, st);
+  return launch_gemm_cfg<GemmCfg<1, false, 32>>(L, st);
+}
+
+cudaError_t launch_gemm(int precision, const GemmLaunch& L, cudaStream_t st) {
+  if (precision == PRISM_BF16) return launch_gemm_cfg<GemmCfg<0, false>>(L, st);
+  if (precision == PRISM_FP32) return launch_gemm_cfg<GemmCfg<1, true>>(L, st);
+  return launch_gemm_cfg<GemmCfg<1, false>>(L, st);
 }
 
 int tile_bn(int precision) { return precision == PRISM_BF16 ? 256 : 128; }
@@ -140,12 +146,20 @@ struct PinnedDeleter {
 };
 
 struct Plan {
+  ~Plan() {
+    if (exec) cudaGraphExecDestroy(exec);
+  }
+  cudaGraphExec_t exec = nullptr;   // CUDA graph: WHILE(any matrix active) { one iteration }
+  int* d_iter = nullptr;            // device iteration counter
+  int* d_all_done = nullptr;
+  int per_iter_launches = 0;
   std::vector<long long> key;
   size_t ws_need = 0;
   size_t meta_off = 0, meta_bytes = 0;
   std::unique_ptr<uint8_t, PinnedDeleter> blob;
   SolveParams params{};
-  LaunchDesc gram[2], square, apply[2];
+  LaunchDesc gram[2], square, apply[2], chain[5];
+  int n_chain = 0;
   bool has_square = false;
   int max_s = 0, max_rows = 0, max_cols = 0, max_m = 0, max_n = 0;
 };
@@ -216,6 +230,9 @@ prism_status build_plan(const Request& r, Plan& P) {
   // state region
   MatState* d_st = reinterpret_cast<MatState*>(bump.take(sizeof(MatState) * B));
   double* d_fro = reinterpret_cast<double*>(bump.take(sizeof(double) * B * kFroParts));
+  int* d_iter = reinterpret_cast<int*>(bump.take(2 * sizeof(int)));
+  double* d_ahist = reinterpret_cast<double*>(bump.take(sizeof(double) * B * o.max_iters));
+  float* d_rhist = reinterpret_cast<float*>(bump.take(sizeof(float) * B * (o.max_iters + 1)));
 
   std::vector<MatDesc> mats(B);
   std::vector<MapSpec> maps;
@@ -237,14 +254,15 @@ prism_status build_plan(const Request& r, Plan& P) {
     D.ldq = r.ldq[i];
     D.m = m;
     D.n = n;
-    if (r.sqrt_kind) { D.s = n; D.L = n; D.trans = 0; }
-    else { D.s = std::min(m, n); D.L = std::max(m, n); D.trans = (m >= n) ? 1 : 0; }
+    if (r.sqrt_kind) { D.s = n; D.L = n; }
+    else { D.s = std::min(m, n); D.L = std::max(m, n); }
+    D.trans = 0;   // X keeps A's row-major layout (no transposes; MN-major operands instead)
     D.sketch_id = r.ids ? (int)r.ids[i] : i;
     const int s = D.s, L = D.L;
-    const long long ldx = (long long)align_up(L, 64), ldr = (long long)align_up(s, 64);
+    const long long ldx = (long long)align_up(n, 64), ldr = (long long)align_up(s, 64);
     D.ldx = ldx;
     D.ldr = ldr;
-    const size_t xbytes = (size_t)s * ldx * esz, rbytes = (size_t)s * ldr * esz;
+    const size_t xbytes = (size_t)m * ldx * esz, rbytes = (size_t)s * ldr * esz;
     for (int t = 0; t < 2; ++t) {
       D.X[t] = bump.take(xbytes);
       D.X_lo[t] = split ? bump.take(xbytes) : nullptr;
@@ -262,14 +280,20 @@ prism_status build_plan(const Request& r, Plan& P) {
     D.tiles_n = (s + BN - 1) / BN;
     D.sym = r.sqrt_kind ? 0 : 1;
     D.norm_part = reinterpret_cast<float*>(bump.take(sizeof(float) * D.tiles_m * D.tiles_n));
-    D.S = reinterpret_cast<float*>(bump.take(sizeof(float) * p * s));
-    D.chain = reinterpret_cast<float*>(bump.take(sizeof(float) * 5 * (size_t)s * 2 * p));
+    const long long ldS = (long long)align_up(s, 64);
+    D.ldS = ldS;
+    D.S = reinterpret_cast<float*>(bump.take(sizeof(float) * p * ldS));
+    D.W[0] = bump.take((size_t)esz * 4 * p * ldS);
+    D.W[1] = bump.take((size_t)esz * 4 * p * ldS);
+    D.keep = reinterpret_cast<float*>(bump.take(sizeof(float) * 4 * (size_t)s * p));
+    D.chain_tiles = D.tiles_m;
+    D.chain_part = reinterpret_cast<double*>(bump.take(sizeof(double) * 6 * D.tiles_m));
     P.max_s = std::max(P.max_s, s);
     P.max_rows = std::max(P.max_rows, s);
     P.max_cols = std::max(P.max_cols, L);
     P.max_m = std::max(P.max_m, m);
     P.max_n = std::max(P.max_n, n);
-    if (L / BN >= 1023 || s / 128 >= 1023)
+    if (L / BN >= 1023 || L / 128 >= 1023)
       return fail(PRISM_ERR_UNSUPPORTED, "matrix too large for the tile encoding");
 
     const double* alpha_ptr = &d_st[i].alpha;
@@ -284,22 +308,38 @@ prism_status build_plan(const Request& r, Plan& P) {
       return h;
     };
     if (!r.sqrt_kind) {
-      // polar, compute layout Xt (s x L): G = Xt Xt^T, P = R/2 + a R^2, Xt' = Xt + P Xt
+      // polar: X keeps A's row-major layout (m x n).  Tall (m >= n): G = X^T X with both
+      // operands MN-major, X' = X + X P (A = X K-major, B = P K-major by symmetry).
+      // Wide (m < n): G = X X^T (both K-major), X' = X + P X (B = X MN-major).
+      const bool tall = m >= n;
       for (int t = 0; t < 2; ++t) {
         HostProblem g = mk(s, s, L, EPI_RESID, 1, D.R, D.R_lo, ldr, nullptr, nullptr, 0);
         g.p.norm_part = D.norm_part;
         g.p.gdiag = D.gdiag;
-        g.mapA = add_map(D.X[t], s, L, ldx, OP_A);
-        g.mapB = add_map(D.X[t], s, L, ldx, OP_BK);
-        if (split) { g.mapA_lo = add_map(D.X_lo[t], s, L, ldx, OP_A); g.mapB_lo = add_map(D.X_lo[t], s, L, ldx, OP_BK); }
+        if (tall) {
+          g.p.a_mn = g.p.b_mn = 1;
+          g.mapA = g.mapB = add_map(D.X[t], m, n, ldx, OP_MN);
+          if (split) g.mapA_lo = g.mapB_lo = add_map(D.X_lo[t], m, n, ldx, OP_MN);
+        } else {
+          g.mapA = add_map(D.X[t], m, n, ldx, OP_A);
+          g.mapB = add_map(D.X[t], m, n, ldx, OP_BK);
+          if (split) { g.mapA_lo = add_map(D.X_lo[t], m, n, ldx, OP_A); g.mapB_lo = add_map(D.X_lo[t], m, n, ldx, OP_BK); }
+        }
         P.gram[t].probs.push_back(g);
         const void* Pa = d == 2 ? Pm : D.R;
         const void* Pa_lo = d == 2 ? Pm_lo : D.R_lo;
-        HostProblem a = mk(s, L, s, EPI_APPLY, 0, D.X[1 - t], D.X_lo[1 - t], ldx, D.X[t], D.X_lo[t], ldx);
+        HostProblem a = mk(m, n, s, EPI_APPLY, 0, D.X[1 - t], D.X_lo[1 - t], ldx, D.X[t], D.X_lo[t], ldx);
         a.p.scale_by_alpha = d == 1;
-        a.mapA = add_map(Pa, s, s, ldr, OP_A);
-        a.mapB = add_map(D.X[t], s, L, ldx, OP_BMN);
-        if (split) { a.mapA_lo = add_map(Pa_lo, s, s, ldr, OP_A); a.mapB_lo = add_map(D.X_lo[t], s, L, ldx, OP_BMN); }
+        if (tall) {
+          a.mapA = add_map(D.X[t], m, n, ldx, OP_A);
+          a.mapB = add_map(Pa, s, s, ldr, OP_BK);
+          if (split) { a.mapA_lo = add_map(D.X_lo[t], m, n, ldx, OP_A); a.mapB_lo = add_map(Pa_lo, s, s, ldr, OP_BK); }
+        } else {
+          a.p.b_mn = 1;
+          a.mapA = add_map(Pa, s, s, ldr, OP_A);
+          a.mapB = add_map(D.X[t], m, n, ldx, OP_MN);
+          if (split) { a.mapA_lo = add_map(Pa_lo, s, s, ldr, OP_A); a.mapB_lo = add_map(D.X_lo[t], m, n, ldx, OP_MN); }
+        }
         P.apply[t].probs.push_back(a);
       }
       if (d == 2) {
@@ -317,39 +357,72 @@ prism_status build_plan(const Request& r, Plan& P) {
         HostProblem g = mk(nn, nn, nn, EPI_RESID, 0, D.R, D.R_lo, ldr, nullptr, nullptr, 0);
         g.p.norm_part = D.norm_part;
         g.p.gdiag = D.gdiag;
+        g.p.b_mn = 1;
         g.mapA = add_map(D.Y[t], nn, nn, ldx, OP_A);
-        g.mapB = add_map(D.X[t], nn, nn, ldx, OP_BMN);
-        if (split) { g.mapA_lo = add_map(D.Y_lo[t], nn, nn, ldx, OP_A); g.mapB_lo = add_map(D.X_lo[t], nn, nn, ldx, OP_BMN); }
+        g.mapB = add_map(D.X[t], nn, nn, ldx, OP_MN);
+        if (split) { g.mapA_lo = add_map(D.Y_lo[t], nn, nn, ldx, OP_A); g.mapB_lo = add_map(D.X_lo[t], nn, nn, ldx, OP_MN); }
         P.gram[t].probs.push_back(g);
         const void* Pa = d == 2 ? Pm : D.R;
         const void* Pa_lo = d == 2 ? Pm_lo : D.R_lo;
         HostProblem ax = mk(nn, nn, nn, EPI_APPLY, 0, D.X[1 - t], D.X_lo[1 - t], ldx, D.X[t], D.X_lo[t], ldx);
         ax.p.scale_by_alpha = d == 1;
+        ax.p.b_mn = 1;
         ax.mapA = add_map(D.X[t], nn, nn, ldx, OP_A);
-        ax.mapB = add_map(Pa, nn, nn, ldr, OP_BMN);
-        if (split) { ax.mapA_lo = add_map(D.X_lo[t], nn, nn, ldx, OP_A); ax.mapB_lo = add_map(Pa_lo, nn, nn, ldr, OP_BMN); }
+        ax.mapB = add_map(Pa, nn, nn, ldr, OP_MN);
+        if (split) { ax.mapA_lo = add_map(D.X_lo[t], nn, nn, ldx, OP_A); ax.mapB_lo = add_map(Pa_lo, nn, nn, ldr, OP_MN); }
         P.apply[t].probs.push_back(ax);
         HostProblem ay = mk(nn, nn, nn, EPI_APPLY, 0, D.Y[1 - t], D.Y_lo[1 - t], ldx, D.Y[t], D.Y_lo[t], ldx);
         ay.p.scale_by_alpha = d == 1;
+        ay.p.b_mn = 1;
         ay.mapA = add_map(Pa, nn, nn, ldr, OP_A);
-        ay.mapB = add_map(D.Y[t], nn, nn, ldx, OP_BMN);
-        if (split) { ay.mapA_lo = add_map(Pa_lo, nn, nn, ldr, OP_A); ay.mapB_lo = add_map(D.Y_lo[t], nn, nn, ldx, OP_BMN); }
+        ay.mapB = add_map(D.Y[t], nn, nn, ldx, OP_MN);
+        if (split) { ay.mapA_lo = add_map(Pa_lo, nn, nn, ldr, OP_A); ay.mapB_lo = add_map(D.Y_lo[t], nn, nn, ldx, OP_MN); }
         P.apply[t].probs.push_back(ay);
       }
       if (d == 2) {
         HostProblem q = mk(nn, nn, nn, EPI_POLY, 0, Pm, Pm_lo, ldr, D.R, D.R_lo, ldr);
         q.p.c1 = 0.5f;
+        q.p.b_mn = 1;
         q.mapA = add_map(D.R, nn, nn, ldr, OP_A);
-        q.mapB = add_map(D.R, nn, nn, ldr, OP_BMN);
-        if (split) { q.mapA_lo = add_map(D.R_lo, nn, nn, ldr, OP_A); q.mapB_lo = add_map(D.R_lo, nn, nn, ldr, OP_BMN); }
+        q.mapB = add_map(D.R, nn, nn, ldr, OP_MN);
+        if (split) { q.mapA_lo = add_map(D.R_lo, nn, nn, ldr, OP_A); q.mapB_lo = add_map(D.R_lo, nn, nn, ldr, OP_MN); }
         P.square.probs.push_back(q);
+      }
+    }
+    // sketch chain (thin tcgen05 GEMMs): pass j reads W[j%2], writes W[(j+1)%2]
+    {
+      static const int codes2[5] = {CH2_P1, CH2_P2, CH2_P3, CH2_P4, CH2_P5};
+      static const int codes1[3] = {CH1_P1, CH1_P2, CH1_P3};
+      static const int nin2[5] = {2, 4, 4, 2, 2};   // rows of B (= 2 x input width) in units of p
+      static const int nin1[3] = {2, 2, 2};
+      const int npass = d == 2 ? 5 : 3;
+      for (int j = 0; j < npass; ++j) {
+        const int N = (d == 2 ? nin2[j] : nin1[j]) * p;
+        HostProblem c = mk(s, N, s, EPI_CHAIN, 0, nullptr, nullptr, 0, nullptr, nullptr, 0);
+        c.p.pass = d == 2 ? codes2[j] : codes1[j];
+        c.p.S = D.S;
+        c.p.Rg = D.R;
+        c.p.Rg_lo = D.R_lo;
+        c.p.gdiag = D.gdiag;
+        c.p.Wn = D.W[(j + 1) % 2];
+        c.p.keep = D.keep;
+        c.p.chain_part = D.chain_part;
+        c.p.ldS = D.ldS;
+        c.p.ldr = ldr;
+        c.p.p = p;
+        c.p.tiles_n = 1;
+        c.mapA = add_map(D.R, s, s, ldr, OP_A);
+        if (split) c.mapA_lo = add_map(D.R_lo, s, s, ldr, OP_A);
+        maps.push_back(MapSpec{D.W[j % 2], N, s, D.ldS, esz, OP_BK, 32, BK});
+        c.mapB = (int)maps.size();
+        P.chain[j].probs.push_back(c);
       }
     }
   }
   P.has_square = (d == 2);
+  P.n_chain = (d == 2) ? 5 : 3;
   // tile lists (problem index within its launch)
-  auto finish = [&](LaunchDesc& L, bool bmn) {
-    L.bmn = bmn;
+  auto finish = [&](LaunchDesc& L, bool) {
     L.tiles.clear();
     for (int j = 0; j < (int)L.probs.size(); ++j)
       add_tiles(L, j, L.probs[j].p.M, L.probs[j].p.N, BN, L.probs[j].p.sym != 0);
@@ -361,14 +434,34 @@ prism_status build_plan(const Request& r, Plan& P) {
     finish(P.apply[t], true);
   }
   if (P.has_square) finish(P.square, !polar_k);
+  for (int j = 0; j < P.n_chain; ++j) {
+    LaunchDesc& L = P.chain[j];
+    L.tiles.clear();
+    for (int q = 0; q < (int)L.probs.size(); ++q) add_tiles(L, q, L.probs[q].p.M, L.probs[q].p.N, 32, false);
+    sort_tiles_by_cost(L);
+  }
   if ((int)P.apply[0].probs.size() >= 4096) return fail(PRISM_ERR_UNSUPPORTED, "batch too large (max 2047 sqrt / 4095 polar)");
 
-  // meta region (serialised blob): [mats][problems...][tiles...][maps]
+  // flat 64x64 tile prefixes for the layout kernels (normalise over Xt, finalise over the output)
+  std::vector<int> toff(B + 1, 0), ooff(B + 1, 0);
+  for (int i = 0; i < B; ++i) {
+    const MatDesc& D = mats[i];
+    const int tw = 32 * (16 / esz);   // layout tile: 32 rows x 32 16-byte vectors
+    toff[i + 1] = toff[i] + ((D.m + 31) / 32) * ((D.n + tw - 1) / tw);
+    ooff[i + 1] = toff[i + 1];
+  }
+  // meta region (serialised blob): [mats][tile prefixes][problems...][tiles...][maps]
   P.meta_off = align_up(bump.off, 1024);
   size_t off = 0;
   const size_t mats_off = off;
   off += sizeof(MatDesc) * B;
-  LaunchDesc* all[5] = {&P.gram[0], &P.gram[1], &P.apply[0], &P.apply[1], &P.square};
+  off = align_up(off, 128);
+  const size_t toff_off = off;
+  off += sizeof(int) * (B + 1);
+  const size_t ooff_off = off;
+  off += sizeof(int) * (B + 1);
+  LaunchDesc* all[10] = {&P.gram[0], &P.gram[1], &P.apply[0], &P.apply[1], &P.square,
+                         &P.chain[0], &P.chain[1], &P.chain[2], &P.chain[3], &P.chain[4]};
   for (LaunchDesc* L : all) {
     off = align_up(off, 128);
     L->probs_off = off;
@@ -392,6 +485,8 @@ prism_status build_plan(const Request& r, Plan& P) {
   P.blob.reset(blob);
   std::memset(blob, 0, P.meta_bytes);
   std::memcpy(blob + mats_off, mats.data(), sizeof(MatDesc) * B);
+  std::memcpy(blob + toff_off, toff.data(), sizeof(int) * (B + 1));
+  std::memcpy(blob + ooff_off, ooff.data(), sizeof(int) * (B + 1));
   CUtensorMap* hmaps = reinterpret_cast<CUtensorMap*>(blob + maps_off);
   for (size_t j = 0; j < maps.size(); ++j)
     if (!encode_map(&hmaps[j], maps[j])) return fail(PRISM_ERR_CUDA, "cuTensorMapEncodeTiled failed");
@@ -415,7 +510,16 @@ prism_status build_plan(const Request& r, Plan& P) {
   SolveParams& S = P.params;
   std::memset(&S, 0, sizeof(S));
   S.mats = reinterpret_cast<MatDesc*>(meta_dev + mats_off);
+  S.tile_off = reinterpret_cast<const int*>(meta_dev + toff_off);
+  S.out_tile_off = reinterpret_cast<const int*>(meta_dev + ooff_off);
+  S.n_tiles = toff[B];
+  S.n_out_tiles = ooff[B];
   S.st = d_st;
+  S.iter = d_iter;
+  S.alpha_hist = d_ahist;
+  S.resid_hist = d_rhist;
+  P.d_iter = d_iter;
+  P.d_all_done = d_iter + 1;
   S.fro_part = d_fro;
   S.batch = B;
   S.p = p;
@@ -433,15 +537,32 @@ prism_status build_plan(const Request& r, Plan& P) {
   return PRISM_OK;
 }
 
-GemmLaunch make_launch(const Plan& P, const LaunchDesc& L, char* ws) {
-  GemmLaunch g;
+GemmLaunch make_launch(const Plan& P, const LaunchDesc& L, const LaunchDesc* odd, char* ws, int lo, int hi) {
+  GemmLaunch g{};
   char* meta = ws + P.meta_off;
   g.probs = reinterpret_cast<const GemmProblem*>(meta + L.probs_off);
+  g.probs_odd = odd ? reinterpret_cast<const GemmProblem*>(meta + odd->probs_off) : nullptr;
   g.tiles = reinterpret_cast<const uint32_t*>(meta + L.tiles_off);
   g.done = &P.params.st[0].done;
   g.done_stride = sizeof(MatState) / sizeof(int);
   g.ntiles = (int)L.tiles.size();
+  g.iter = P.params.iter;
+  g.iter_lo = lo;
+  g.iter_hi = hi;
   return g;
+}
+
+// Make every kernel's large-smem attribute current before any graph capture.
+void ensure_attrs() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  GemmLaunch z{};
+  z.ntiles = 0;
+  for (int prec = 0; prec < 3; ++prec) {
+    launch_gemm(prec, z, 0);
+    launch_chain(prec, z, 0);
+  }
 }
 
 prism_status validate(const Request& r) {
@@ -475,8 +596,59 @@ prism_status validate(const Request& r) {
 }  // namespace
 
 // ====================================================================== handle
+constexpr int kKinds = 6;
 struct prism_handle_s {
   std::list<std::unique_ptr<Plan>> plans;   // most recent first
+  long long launches = 0;                   // launches of the last solve
+  bool profiling = false;
+  std::vector<cudaEvent_t> pool;            // reusable events
+  size_t pool_used = 0;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> marks;   // (kind, (start, stop))
+  std::vector<long long> mark_launches;
+  double acc_ms[kKinds] = {0};
+  long long acc_launches[kKinds] = {0};
+  cudaStream_t cap = nullptr;               // private stream for graph capture
+  int* last_iter = nullptr;                 // device iteration counter of the last solve
+  int last_fixed = 0, last_per_iter = 0;
+  int* h_flag = nullptr;                    // pinned host flag (profiling path)
+  ~prism_handle_s() {
+    plans.clear();
+    for (cudaEvent_t e : pool) cudaEventDestroy(e);
+    if (cap) cudaStreamDestroy(cap);
+    if (h_flag) cudaFreeHost(h_flag);
+  }
+  cudaEvent_t next_event() {
+    if (pool_used == pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      pool.push_back(e);
+    }
+    return pool[pool_used++];
+  }
+};
+
+// Scoped timing of one launch group (no-op unless profiling is enabled).
+struct KindTimer {
+  prism_handle_s* h;
+  cudaStream_t st;
+  int kind;
+  long long nl;
+  cudaEvent_t a = nullptr;
+  KindTimer(prism_handle_s* h_, cudaStream_t st_, int kind_, long long nl_) : h(h_), st(st_), kind(kind_), nl(nl_) {
+    h->launches += nl;
+    if (h->profiling) {
+      a = h->next_event();
+      cudaEventRecord(a, st);
+    }
+  }
+  ~KindTimer() {
+    if (h->profiling) {
+      cudaEvent_t b = h->next_event();
+      cudaEventRecord(b, st);
+      h->marks.push_back({kind, {a, b}});
+      h->mark_launches.push_back(nl);
+    }
+  }
 };
 
 static std::vector<long long> make_key(const Request& r) {
@@ -540,54 +712,113 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
   if (ws_bytes < P->ws_need) return fail(PRISM_ERR_INVALID_ARG, "workspace too small");
 
   PRISM_CK(cudaMemcpyAsync(r.ws + P->meta_off, P->blob.get(), P->meta_bytes, cudaMemcpyHostToDevice, st));
-  SolveParams S = P->params;
-  S.alpha_hist = rep ? rep->alphas : nullptr;
-  S.resid_hist = rep ? rep->resid_hist : nullptr;
+  SolveParams S = P->params;   // report pointers are only read by k_report (outside the graph)
   S.rep_iters = rep ? rep->iters : nullptr;
   S.rep_resid = rep ? rep->resid : nullptr;
   S.rep_status = rep ? rep->status : nullptr;
+  S.rep_alphas = rep ? rep->alphas : nullptr;
+  S.rep_resid_hist = rep ? rep->resid_hist : nullptr;
   const int B = r.batch;
   const int prec = r.o.precision;
 
-  k_fro_partials<<<dim3(kFroParts, B), 256, 0, st>>>(S);
-  k_normalize<<<dim3((P->max_cols + 31) / 32, (P->max_rows + 31) / 32, B), 256, 0, st>>>(S);
+  h->launches = 0;
+  {
+    KindTimer t(h, st, 5, 3);
+    k_fro_partials<<<dim3(kFroParts, B), 256, 0, st>>>(S);
+    k_fro_final<<<B, 256, 0, st>>>(S);
+    if (prec == PRISM_BF16) k_normalize<0><<<S.n_tiles, 256, 0, st>>>(S);
+    else if (prec == PRISM_FP32) k_normalize<1><<<S.n_tiles, 256, 0, st>>>(S);
+    else k_normalize<2><<<S.n_tiles, 256, 0, st>>>(S);
+  }
   PRISM_CK(cudaGetLastError());
-  const GemmLaunch g_gram[2] = {make_launch(*P, P->gram[0], r.ws), make_launch(*P, P->gram[1], r.ws)};
-  const GemmLaunch g_apply[2] = {make_launch(*P, P->apply[0], r.ws), make_launch(*P, P->apply[1], r.ws)};
-  const GemmLaunch g_sq = make_launch(*P, P->square, r.ws);
+  const int M = r.o.max_iters;
+  const GemmLaunch g_gram = make_launch(*P, P->gram[0], &P->gram[1], r.ws, 0, M + 1);
+  const GemmLaunch g_apply = make_launch(*P, P->apply[0], &P->apply[1], r.ws, 0, M);
+  const GemmLaunch g_sq = make_launch(*P, P->square, nullptr, r.ws, 0, M);
+  GemmLaunch g_chain[5];
+  for (int j = 0; j < P->n_chain; ++j) g_chain[j] = make_launch(*P, P->chain[j], nullptr, r.ws, r.o.warmup_iters, M);
+  const bool sketched = r.o.fit == PRISM_FIT_SKETCHED;
   const int p = S.p;
-  const dim3 chain_grid((P->max_s + kChainRows - 1) / kChainRows, B);
-  for (int k = 0; k <= r.o.max_iters; ++k) {
-    const int par = k & 1;
-    PRISM_CK(launch_gemm(prec, P->gram[par].bmn, g_gram[par], st));
-    const bool fit = r.o.fit == PRISM_FIT_SKETCHED && k < r.o.max_iters && k >= r.o.warmup_iters;
-    if (fit) {
-      k_sketch<<<dim3((p * P->max_s / 2 + 256) / 256, B), 256, 0, st>>>(S, k);
-      auto chain = [&](int src, int w, int in_blk, int in_ld, int in_off, int out_blk) {
-        ChainPass c{src, w, in_off, in_ld, in_blk, out_blk};
-        if (prec == PRISM_BF16) k_chain<1><<<chain_grid, 256, 0, st>>>(S, c);
-        else k_chain<0><<<chain_grid, 256, 0, st>>>(S, c);
-      };
-      if (S.d == 2) {
-        chain(SRC_S, p, 0, 0, 0, 0);             // K1 = R S^T
-        chain(SRC_K1Q, 2 * p, 0, p, 0, 1);       // [K2 | L1] = R [K1 | Q]
-        chain(SRC_BUF, 2 * p, 1, 2 * p, 0, 2);   // [K3 | L2] = R [K2 | L1]
-        chain(SRC_BUF, p, 2, 2 * p, p, 3);       // L3 = R L2
-        chain(SRC_BUF, p, 3, p, 0, 4);           // L4 = R L3
-      } else {
-        chain(SRC_S, p, 0, 0, 0, 0);             // K1 = R S^T
-        chain(SRC_Q, p, 0, p, 0, 1);             // L1 = R Q
-        chain(SRC_BUF, p, 1, p, 0, 2);           // L2 = R L1
-      }
+  // one iteration k (k read on the device): R_k, stop test, S_k, chain, alpha_k, P, X_{k+1}
+  auto body = [&](cudaStream_t s2, cudaGraphConditionalHandle ch, int use_handle, bool timed) -> prism_status {
+    {
+      KindTimer t(h, s2, 0, timed ? 1 : 0);
+      PRISM_CK(launch_gemm(prec, g_gram, s2));
     }
-    k_alpha<<<B, 256, 0, st>>>(S, k, fit ? 1 : 0);
+    if (sketched) {
+      KindTimer t(h, s2, 3, timed ? 1 + P->n_chain : 0);
+      k_sketch<<<dim3((p * P->max_s / 2 + 256) / 256, B), 256, 0, s2>>>(S);
+      for (int j = 0; j < P->n_chain; ++j) PRISM_CK(launch_chain(prec, g_chain[j], s2));
+    }
+    {
+      KindTimer t(h, s2, 4, timed ? 1 : 0);
+      k_alpha<<<B, 256, 0, s2>>>(S);
+    }
+    if (P->has_square) {
+      KindTimer t(h, s2, 1, timed ? 1 : 0);
+      PRISM_CK(launch_gemm(prec, g_sq, s2));
+    }
+    {
+      KindTimer t(h, s2, 2, timed ? 1 : 0);
+      PRISM_CK(launch_gemm(prec, g_apply, s2));
+    }
+    k_advance<<<1, 256, 0, s2>>>(S, ch, use_handle, P->d_all_done);
     PRISM_CK(cudaGetLastError());
-    if (k < r.o.max_iters) {
-      if (P->has_square) PRISM_CK(launch_gemm(prec, P->square.bmn, g_sq, st));
-      PRISM_CK(launch_gemm(prec, P->apply[par].bmn, g_apply[par], st));
+    return PRISM_OK;
+  };
+  P->per_iter_launches = 3 + (sketched ? 1 + P->n_chain : 0) + (P->has_square ? 1 : 0) + 1;
+  if (!h->profiling) {
+    if (!P->exec) {
+      // build the device-driven loop once per plan: WHILE(any active) { body }
+      ensure_attrs();
+      if (!h->cap) PRISM_CK(cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking));
+      cudaGraph_t g;
+      PRISM_CK(cudaGraphCreate(&g, 0));
+      cudaGraphConditionalHandle ch;
+      PRISM_CK(cudaGraphConditionalHandleCreate(&ch, g, 1, cudaGraphCondAssignDefault));
+      alignas(cudaGraphNodeParams) unsigned char cp_buf[sizeof(cudaGraphNodeParams)] = {};
+      cudaGraphNodeParams& cp = *reinterpret_cast<cudaGraphNodeParams*>(cp_buf);
+      cp.type = cudaGraphNodeTypeConditional;
+      cp.conditional.handle = ch;
+      cp.conditional.type = cudaGraphCondTypeWhile;
+      cp.conditional.size = 1;
+      cudaGraphNode_t cn;
+      PRISM_CK(cudaGraphAddNode(&cn, g, nullptr, 0, &cp));
+      cudaGraph_t bodyg = cp.conditional.phGraph_out[0];
+      PRISM_CK(cudaStreamBeginCaptureToGraph(h->cap, bodyg, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+      const long long saved = h->launches;
+      prism_status bs = body(h->cap, ch, 1, false);
+      h->launches = saved;
+      cudaGraph_t got;
+      cudaError_t ec = cudaStreamEndCapture(h->cap, &got);
+      if (bs) { cudaGraphDestroy(g); return bs; }
+      if (ec != cudaSuccess) { cudaGraphDestroy(g); return fail(PRISM_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ec)); }
+      cudaError_t ei = cudaGraphInstantiate(&P->exec, g, 0);
+      cudaGraphDestroy(g);
+      if (ei != cudaSuccess) { P->exec = nullptr; return fail(PRISM_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ei)); }
+    }
+    PRISM_CK(cudaGraphLaunch(P->exec, st));
+  } else {
+    // profiling: direct launches bracketed by events, host-side exit once all matrices stopped
+    if (!h->h_flag) PRISM_CK(cudaMallocHost(&h->h_flag, sizeof(int)));
+    for (int k = 0; k <= M; ++k) {
+      prism_status bs = body(st, 0, 0, true);
+      if (bs) return bs;
+      PRISM_CK(cudaMemcpyAsync(h->h_flag, P->d_all_done, sizeof(int), cudaMemcpyDeviceToHost, st));
+      PRISM_CK(cudaStreamSynchronize(st));
+      if (*h->h_flag) break;
     }
   }
-  k_finalize<<<dim3((P->max_n + 31) / 32, (P->max_m + 31) / 32, B), 256, 0, st>>>(S);
+  {
+    KindTimer t(h, st, 5, 1);
+    if (prec == PRISM_BF16) k_finalize<0><<<S.n_out_tiles, 256, 0, st>>>(S);
+    else if (prec == PRISM_FP32) k_finalize<1><<<S.n_out_tiles, 256, 0, st>>>(S);
+    else k_finalize<2><<<S.n_out_tiles, 256, 0, st>>>(S);
+  }
+  if (rep) k_report<<<std::max(1, std::min(64, (B * (M + 1) + 255) / 256)), 256, 0, st>>>(S);
+  h->last_iter = P->d_iter;
+  h->last_fixed = 4 + (rep ? 1 : 0);
+  h->last_per_iter = P->per_iter_launches;
   PRISM_CK(cudaGetLastError());
   return PRISM_OK;
 }
@@ -598,16 +829,10 @@ __global__ void k_sketch_debug(unsigned long long seed, int b, int k, int p, int
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long total = (long long)p * s;
   if (2 * e >= total) return;
-  uint32_t ctr[4] = {(uint32_t)e, (uint32_t)k, (uint32_t)b, 0x534B4348u};
-  philox10(ctr, (uint32_t)(seed & 0xFFFFFFFFull), (uint32_t)(seed >> 32));
-  const unsigned long long K1 = ((unsigned long long)(ctr[0] >> 5) << 26) + (ctr[1] >> 6);
-  const unsigned long long K2 = ((unsigned long long)(ctr[2] >> 5) << 26) + (ctr[3] >> 6);
-  const double u1 = dmul((double)(K1 + 1ull), 0x1p-53);
-  const double rad = __dsqrt_rn(dmul(-2.0, portable_log(u1)));
-  double sn, cs;
-  portable_sincos_2pi(K2, &sn, &cs);
-  S[2 * e] = __double2float_rn(dmul(rad, cs));
-  if (2 * e + 1 < total) S[2 * e + 1] = __double2float_rn(dmul(rad, sn));
+  double z0, z1;
+  sketch_pair(seed, (uint32_t)k, (uint32_t)b, (uint32_t)e, &z0, &z1);
+  S[2 * e] = __double2float_rn(z0);
+  if (2 * e + 1 < total) S[2 * e + 1] = __double2float_rn(z1);
 }
 __global__ void k_argmin_debug(int n, const double* c, double lo, double hi, double aT, double* out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -703,6 +928,43 @@ prism_status prism_sqrt_invsqrt(prism_handle h, int batch, const int64_t* n, con
   }
 }
 
+int64_t prism_launch_count(prism_handle h) {
+  // fixed launches + per-iteration launches x iterations executed (reads the device
+  // counter of the last solve: synchronises the device)
+  if (!h) return -1;
+  if (!h->last_iter) return 0;
+  int k = 0;
+  if (cudaMemcpy(&k, h->last_iter, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  return (int64_t)h->last_fixed + (int64_t)h->last_per_iter * k;
+}
+
+prism_status prism_profile_enable(prism_handle h, int enable) {
+  if (!h) return fail(PRISM_ERR_INVALID_ARG, "null handle");
+  h->profiling = enable != 0;
+  return PRISM_OK;
+}
+
+prism_status prism_profile_read(prism_handle h, double* ms, int64_t* launches, int reset) {
+  if (!h) return fail(PRISM_ERR_INVALID_ARG, "null handle");
+  for (size_t j = 0; j < h->marks.size(); ++j) {
+    const auto& m = h->marks[j];
+    PRISM_CK(cudaEventSynchronize(m.second.second));
+    float t = 0.f;
+    PRISM_CK(cudaEventElapsedTime(&t, m.second.first, m.second.second));
+    h->acc_ms[m.first] += t;
+    h->acc_launches[m.first] += h->mark_launches[j];
+  }
+  h->marks.clear();
+  h->mark_launches.clear();
+  h->pool_used = 0;
+  for (int k = 0; k < kKinds; ++k) {
+    if (ms) ms[k] = h->acc_ms[k];
+    if (launches) launches[k] = h->acc_launches[k];
+    if (reset) { h->acc_ms[k] = 0; h->acc_launches[k] = 0; }
+  }
+  return PRISM_OK;
+}
+
 prism_status prism_lpt_partition(int batch, const double* cost, int ranks, int32_t* owner) {
   if (batch < 0 || ranks < 1 || (batch > 0 && (!cost || !owner))) return fail(PRISM_ERR_INVALID_ARG, "bad LPT args");
   std::vector<int> order(batch);
@@ -764,7 +1026,7 @@ prism_status prism_debug_gemm(prism_handle h, int precision, int b_mn, int mode,
   std::memset(hb, 0, need);
   char* wsd = static_cast<char*>(workspace);
   CUtensorMap* hm = reinterpret_cast<CUtensorMap*>(hb);
-  const OpKind bk = b_mn ? OP_BMN : OP_BK;
+  const OpKind bk = b_mn ? OP_MN : OP_BK;
   const int brows = b_mn ? K : N, bcols = b_mn ? N : K;
   if (!encode_map(&hm[0], MapSpec{A, M, K, lda, esz, OP_A, BN, BK}) ||
       !encode_map(&hm[1], MapSpec{B, brows, bcols, ldb, esz, bk, BN, BK}))
@@ -783,6 +1045,7 @@ prism_status prism_debug_gemm(prism_handle h, int precision, int b_mn, int mode,
   gp->ldo = ldo; gp->ldc = ldc; gp->M = M; gp->N = N; gp->K = K;
   gp->mode = mode; gp->sym = sym; gp->matrix = 0; gp->scale_by_alpha = scale_by_alpha;
   gp->tiles_n = (N + BN - 1) / BN; gp->c1 = c1;
+  gp->a_mn = 0; gp->b_mn = b_mn ? 1 : 0;
   LaunchDesc L;
   HostProblem hp;
   hp.p = *gp;
@@ -791,13 +1054,13 @@ prism_status prism_debug_gemm(prism_handle h, int precision, int b_mn, int mode,
   const size_t tiles_off = 4 * sizeof(CUtensorMap) + align_up(sizeof(GemmProblem), 128);
   std::memcpy(hb + tiles_off, L.tiles.data(), 4 * L.tiles.size());
   PRISM_CK(cudaMemcpyAsync(wsd, hb, need, cudaMemcpyHostToDevice, static_cast<cudaStream_t>(stream)));
-  GemmLaunch g;
+  GemmLaunch g{};
   g.probs = reinterpret_cast<const GemmProblem*>(wsd + 4 * sizeof(CUtensorMap));
   g.tiles = reinterpret_cast<const uint32_t*>(wsd + tiles_off);
   g.done = nullptr;
   g.done_stride = 0;
   g.ntiles = (int)L.tiles.size();
-  PRISM_CK(launch_gemm(precision, b_mn != 0, g, static_cast<cudaStream_t>(stream)));
+  PRISM_CK(launch_gemm(precision, g, static_cast<cudaStream_t>(stream)));
   PRISM_CK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
   return PRISM_OK;
 }

@@ -145,6 +145,16 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr, uint32_t lbo, ui
   return d;
 }
 
+__device__ __forceinline__ uint64_t sdesc_rt(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(layout) << 61;
+  return d;
+}
+
 // Instruction descriptor (kind::f16 / kind::tf32, fp32 accumulate, dense).
 //   [4,6) D format (1 = f32); [7,10) A format; [10,13) B format (bf16 = 1, tf32 = 2);
 //   [15] A major (0 = K); [16] B major (1 = MN); [17,23) N >> 3; [24,29) M >> 4.
