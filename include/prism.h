@@ -140,6 +140,26 @@ prism_status prism_sqrt_invsqrt(prism_handle h, int batch, const int64_t* n, con
  */
 prism_status prism_lpt_partition(int batch, const double* cost, int ranks, int32_t* owner);
 
+/*
+ * Row-block split of ONE tall polar problem across ranks (C4: 8192^2 over
+ * 2/4/8 GPUs).  Rank r holds rows [row0, row0 + rows) of the global m x n matrix A.
+ * Per iteration k the caller all-reduces (sums) the n x n fp32 partial Gram G = X_r^T X_r
+ * between prism_rowblock_gram and prism_rowblock_update (e.g. NCCL all_reduce on `stream`);
+ * every rank then forms the identical R = I - G, sketch S_k (matrix id 0), alpha_k and
+ * P, and updates its own rows X_r <- X_r g_d(R; alpha_k).  Sequence:
+ *   begin (writes the local sum of squares to fro2_local[0]) -> all-reduce fro2 ->
+ *   for k = 0..max_iters: gram(k) -> all-reduce G -> update(k) -> stop when *all_done;
+ *   end (writes Q_rows and the report).  One row-block solve per host thread at a time.
+ * G: n x n fp32 device buffer (ld n); all_done: device int32 (1 once converged / stopped).
+ */
+size_t prism_rowblock_workspace(prism_handle h, int64_t rows, int64_t n, const prism_options* o);
+prism_status prism_rowblock_begin(prism_handle h, int64_t rows, int64_t n, const void* A_rows, int64_t lda,
+                                  void* Q_rows, int64_t ldq, float* G, double* fro2_local, const prism_options* o,
+                                  void* workspace, size_t ws_bytes, void* stream);
+prism_status prism_rowblock_gram(prism_handle h, int k, const double* fro2_global, void* stream);
+prism_status prism_rowblock_update(prism_handle h, int k, const float* G, int32_t* all_done, void* stream);
+prism_status prism_rowblock_end(prism_handle h, const prism_report* rep, void* stream);
+
 /* Per-iteration F_min (symmetric products counted once) of a polar solve. */
 double prism_polar_flops_per_iter(int64_t m, int64_t n, int degree, int sketch_size);
 /* Dense-GEMM flop count per sqrt iteration (general products). */

@@ -57,6 +57,8 @@ EXPORTS = [
     "prism_polar_workspace", "prism_polar", "prism_sqrt_workspace", "prism_sqrt_invsqrt",
     "prism_lpt_partition", "prism_polar_flops_per_iter", "prism_sqrt_flops_per_iter",
     "prism_launch_count", "prism_profile_enable", "prism_profile_read",
+    "prism_rowblock_workspace", "prism_rowblock_begin", "prism_rowblock_gram", "prism_rowblock_update",
+    "prism_rowblock_end",
     "prism_debug_gemm", "prism_debug_sketch", "prism_debug_argmin",
 ]
 
@@ -103,11 +105,18 @@ def lib():
         L.prism_launch_count.restype = i64
         L.prism_profile_enable.argtypes = [vp, i32]
         L.prism_profile_read.argtypes = [vp, ctypes.POINTER(dbl), ctypes.POINTER(i64), i32]
+        L.prism_rowblock_workspace.argtypes = [vp, i64, i64, ctypes.POINTER(Options)]
+        L.prism_rowblock_workspace.restype = sz
+        L.prism_rowblock_begin.argtypes = [vp, i64, i64, vp, i64, vp, i64, vp, vp, ctypes.POINTER(Options), vp, sz, vp]
+        L.prism_rowblock_gram.argtypes = [vp, i32, vp, vp]
+        L.prism_rowblock_update.argtypes = [vp, i32, vp, vp, vp]
+        L.prism_rowblock_end.argtypes = [vp, ctypes.POINTER(Report), vp]
         L.prism_debug_sketch.argtypes = [u64, i64, i32, i32, i32, vp, vp]
         L.prism_debug_argmin.argtypes = [i32, vp, dbl, dbl, dbl, vp, vp]
         for name in ("prism_create", "prism_destroy", "prism_polar", "prism_sqrt_invsqrt", "prism_lpt_partition",
                      "prism_debug_gemm", "prism_debug_sketch", "prism_debug_argmin",
-                     "prism_profile_enable", "prism_profile_read"):
+                     "prism_profile_enable", "prism_profile_read", "prism_rowblock_begin",
+                     "prism_rowblock_gram", "prism_rowblock_update", "prism_rowblock_end"):
             getattr(L, name).restype = i32
         _lib = L
         return L
@@ -299,6 +308,53 @@ def sqrt_invsqrt(mats, degree=5, max_iters=30, sketch_size=8, tol=1e-6, seed=42,
                                    ctypes.byref(o), ctypes.byref(rep), ws.data_ptr(), ws.numel(),
                                    ctypes.c_void_p(st.cuda_stream)), "prism_sqrt_invsqrt")
     return sq, isq, rb
+
+
+class RowBlockSolver:
+    """C-ABI steps of the row-block split (prism_rowblock_*): marshalling only."""
+
+    def __init__(self, A_rows, degree=5, max_iters=30, sketch_size=8, tol=1e-6, seed=42, precision=None,
+                 fit="sketched", warmup_iters=0, alpha_lo=None, alpha_hi=None, handle=None, stream=None):
+        import torch
+        precision = _precision_of(A_rows, precision)
+        _check_dtype([A_rows], precision)
+        self.A = A_rows
+        self.dev = A_rows.device
+        self.h = handle or Handle()
+        self.o = make_options(degree, max_iters, sketch_size, tol, seed, precision, fit, warmup_iters, alpha_lo,
+                              alpha_hi)
+        self.max_iters = max_iters
+        rows, n = A_rows.shape
+        self.Q = torch.empty_like(A_rows)
+        self.G = torch.empty(n, n, dtype=torch.float32, device=self.dev)
+        self.fro2 = torch.zeros(1, dtype=torch.float64, device=self.dev)
+        self.done = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.rb = _report_buffers(1, max_iters, self.dev)
+        need = lib().prism_rowblock_workspace(self.h.h, rows, n, ctypes.byref(self.o))
+        if need == 0:
+            raise PrismError("prism_rowblock_workspace rejected the arguments: " + lib().prism_last_error().decode())
+        self.ws = self.h.workspace(need, self.dev)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.dev)
+        self._s = ctypes.c_void_p(self.stream.cuda_stream)
+
+    def begin(self):
+        rows, n = self.A.shape
+        check(lib().prism_rowblock_begin(self.h.h, rows, n, self.A.data_ptr(), self.A.stride(0), self.Q.data_ptr(),
+                                         self.Q.stride(0), self.G.data_ptr(), self.fro2.data_ptr(),
+                                         ctypes.byref(self.o), self.ws.data_ptr(), self.ws.numel(), self._s),
+              "prism_rowblock_begin")
+
+    def gram(self, k):
+        check(lib().prism_rowblock_gram(self.h.h, int(k), self.fro2.data_ptr(), self._s), "prism_rowblock_gram")
+
+    def update(self, k):
+        check(lib().prism_rowblock_update(self.h.h, int(k), self.G.data_ptr(), self.done.data_ptr(), self._s),
+              "prism_rowblock_update")
+
+    def end(self):
+        rep = _report_struct(self.rb)
+        check(lib().prism_rowblock_end(self.h.h, ctypes.byref(rep), self._s), "prism_rowblock_end")
+        return self.Q, self.rb
 
 
 def lpt_partition(costs, ranks: int):

@@ -28,7 +28,7 @@
 
 namespace prism {
 
-enum EpiMode : int { EPI_RESID = 0, EPI_POLY = 1, EPI_APPLY = 2, EPI_STORE = 3, EPI_CHAIN = 4 };
+enum EpiMode : int { EPI_RESID = 0, EPI_POLY = 1, EPI_APPLY = 2, EPI_STORE = 3, EPI_CHAIN = 4, EPI_GRAM32 = 5 };
 
 // Sketch-chain pass codes (EPI_CHAIN).  The thin GEMM computes
 // D = R · [W_hi | W_lo] (N = 2w) and the epilogue forms out = D_hi + D_lo, then
@@ -55,6 +55,9 @@ struct GemmProblem {
   float c1;
   int pass;              // EPI_CHAIN pass code
   int a_mn, b_mn;        // operand major-ness: 0 K-major, 1 MN-major
+  int ksplit;            // EPI_CHAIN split-K slices (tile code tn = slice index) or 1
+  float* kpart;          // [ksplit][M][32] split-K partials
+  int* kcnt;             // [tiles_m] arrival counters (self-resetting)
   // EPI_CHAIN operands (row i of R = row i of the output)
   const float* S;        // [p][ldS] sketch (fp32)
   const void* Rg;        // R (for R_ii), compute dtype (+ R_lo in 3xTF32)
@@ -103,9 +106,12 @@ struct GemmCfg {
   static constexpr uint32_t MN_LAYOUT = KIND == 0 ? 2u : 1u;
   static constexpr uint32_t MN_SBO = KIND == 0 ? 1024u : 512u;
   static constexpr uint32_t IDESC = idesc_make(KIND == 0 ? 1u : 2u, 0u, BM, BN);
-  static constexpr int TB_BYTES = 4 * 32 * 33 * 4;   // per-epilogue-warp 32x33 fp32 transpose buffers
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 512 /*barriers, scratch*/ + TB_BYTES;
-  static constexpr int THREADS = 192;
+  static constexpr int EPI_WARPS = 8;   // two per TMEM lane quarter, each owning half the columns
+  static constexpr int NCH = BN / 32;   // 32-column chunks per tile
+  static constexpr int CH_PER = NCH >= 2 ? NCH / 2 : 1;
+  static constexpr int TB_BYTES = EPI_WARPS * 32 * 33 * 4;   // per-epilogue-warp 32x33 fp32 transpose buffers
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers, scratch*/ + TB_BYTES;
+  static constexpr int THREADS = 64 + 32 * EPI_WARPS;
   // k-blocks per TMEM accumulation chunk: tf32 partials are promoted to fp32
   // registers every k-block (3xTF32, K = 32: 12 MMAs per chunk) or every 4
   // (1xTF32); bf16 keeps one accumulator per tile (products exact, 2^-9 output).
@@ -168,6 +174,34 @@ __device__ __forceinline__ void load_row32(const void* base, const void* base_lo
   }
 }
 
+// bf16 C row segment as raw 16-byte words (converted only when used, so the
+// load latency overlaps the previous chunk's work)
+__device__ __forceinline__ void load_raw_bf16(const void* base, long long ld, int i, int j0, int N, uint4 (&w)[4]) {
+  const __nv_bfloat16* p = static_cast<const __nv_bfloat16*>(base) + (long long)i * ld + j0;
+  if (j0 + 32 <= N) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) w[u] = __ldg(reinterpret_cast<const uint4*>(p) + u);
+  } else {
+    __nv_bfloat16 t[32];
+#pragma unroll
+    for (int u = 0; u < 32; ++u) t[u] = (j0 + u < N) ? p[u] : __float2bfloat16_rn(0.f);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) w[u] = reinterpret_cast<const uint4*>(t)[u];
+  }
+}
+__device__ __forceinline__ void decode_bf16(const uint4 (&w)[4], float (&c)[32]) {
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w[u]);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __bfloat1622float2(h[e]);
+      c[u * 8 + 2 * e] = f.x;
+      c[u * 8 + 2 * e + 1] = f.y;
+    }
+  }
+}
+
 template <int KIND, bool SPLIT>
 __device__ __forceinline__ void store_elem(void* out, void* out_lo, long long idx, float v) {
   if constexpr (KIND == 0) {
@@ -211,6 +245,32 @@ __device__ __forceinline__ void store_row32(void* out, void* out_lo, long long o
   }
 }
 
+// Row-block partial Gram (EPI_GRAM32): out = D in plain fp32 whatever the compute
+// dtype (the partial Grams are summed across ranks), symmetric triangle + mirror.
+__device__ __forceinline__ void epi_gram32(const GemmProblem& P, int i0, int lane, int j0, const float (&d)[32],
+                                           float* tb) {
+  if (i0 >= P.M || j0 >= P.N || j0 + 31 < i0) return;   // warp-uniform
+  const int i = i0 + lane;
+  float* out = static_cast<float*>(P.out);
+  if (i < P.M) {
+#pragma unroll
+    for (int u = 0; u < 32; ++u) {
+      const int j = j0 + u;
+      if (j >= i && j < P.N) out[(long long)i * P.ldo + j] = d[u];
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 32; ++u) tb[lane * 33 + u] = d[u];
+  __syncwarp();
+  const int j = j0 + lane;
+  if (j < P.N) {
+#pragma unroll
+    for (int u = 0; u < 32; ++u)
+      if (i0 + u < j && i0 + u < P.M) out[(long long)j * P.ldo + i0 + u] = tb[u * 33 + lane];
+  }
+  __syncwarp();
+}
+
 // Fused epilogue for one 32 x 32 block: rows i0 + lane (one row per lane of an
 // epilogue warp), columns [j0, j0 + 32), given the fp32 accumulators d[] of
 // D = A·B and (POLY / APPLY) the prefetched row segment c[] of C.  Called by all
@@ -221,6 +281,7 @@ template <class Cfg>
 __device__ __forceinline__ void epi_segment(const GemmProblem& P, int mode, bool sym, int i0, int lane, int j0,
                                             float coefA, float coefC, const float (&d)[32], const float (&c)[32],
                                             float* tb, float& sumsq) {
+  if (mode == EPI_GRAM32) { epi_gram32(P, i0, lane, j0, d, tb); return; }
   if (i0 >= P.M || j0 >= P.N) return;            // warp-uniform
   if (sym && j0 + 31 < i0) return;               // block strictly below the diagonal
   const int i = i0 + lane;
@@ -319,10 +380,10 @@ __device__ __forceinline__ void store_w(const GemmProblem& P, int c, int wn, int
 
 template <class Cfg>
 __device__ __forceinline__ void epi_chain(const GemmProblem& P, int i, int tm, const float (&d)[32], double* dred,
-                                          int q, int lane, int et) {
+                                          int e, int lane, int et, bool active) {
   const int p = P.p;
   const int w = P.N / 2;          // columns of this pass's output
-  const bool valid = i < P.M;
+  const bool valid = active && i < P.M;
   double g[6] = {0, 0, 0, 0, 0, 0};
   float o[16];
 #pragma unroll
@@ -399,13 +460,31 @@ __device__ __forceinline__ void epi_chain(const GemmProblem& P, int i, int tm, c
     }
     if (lane == 0)
 #pragma unroll
-      for (int j = 0; j < 6; ++j) dred[q * 6 + j] = g[j];
-    named_bar_sync(1, 128);
+      for (int j = 0; j < 6; ++j) dred[e * 6 + j] = g[j];
+    named_bar_sync(1, 32 * Cfg::EPI_WARPS);
     if (et == 0)
 #pragma unroll
-      for (int j = 0; j < 6; ++j)
-        P.chain_part[tm * 6 + j] = (dred[0 * 6 + j] + dred[1 * 6 + j]) + (dred[2 * 6 + j] + dred[3 * 6 + j]);
-    named_bar_sync(1, 128);
+      for (int j = 0; j < 6; ++j) {
+        double t = 0.0;
+        for (int x = 0; x < Cfg::EPI_WARPS; ++x) t += dred[x * 6 + j];
+        P.chain_part[tm * 6 + j] = t;
+      }
+    named_bar_sync(1, 32 * Cfg::EPI_WARPS);
+  }
+}
+
+// K range of a tile: split-K tiles (chain) carry the slice index in the tn field.
+template <class Cfg>
+__device__ __forceinline__ void tile_krange(const GemmProblem& P, int& tn, int& kb_lo, int& kb_hi) {
+  const int nkb = (P.K + Cfg::BK - 1) / Cfg::BK;
+  if (P.ksplit > 1) {
+    const int ks = tn;
+    tn = 0;
+    kb_lo = ks * nkb / P.ksplit;
+    kb_hi = (ks + 1) * nkb / P.ksplit;
+  } else {
+    kb_lo = 0;
+    kb_hi = nkb;
   }
 }
 
@@ -443,9 +522,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
   uint64_t* tfull = bars + 2 * Cfg::STAGES;    // [2]
   uint64_t* tempty = tfull + 2;                // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  float* red = reinterpret_cast<float*>(tmem_slot + 4);   // [4] epilogue reduction scratch
-  double* dred = reinterpret_cast<double*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES + 256);   // [4][6]
-  float* tbuf = reinterpret_cast<float*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES + 512);     // [4][32*33]
+  float* red = reinterpret_cast<float*>(tmem_slot + 4);   // [8] epilogue reduction scratch
+  int* sflag = reinterpret_cast<int*>(red + 8);           // split-K "last CTA" flag
+  double* dred = reinterpret_cast<double*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES + 256);   // [8][6]
+  float* tbuf = reinterpret_cast<float*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES + 1024);    // [8][32*33]
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -464,7 +544,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
+      mbar_init(&tempty[a], 32 * Cfg::EPI_WARPS);
     }
     fence_mbar_init();
   }
@@ -483,9 +563,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
         const uint32_t code = L.tiles[t];
         const GemmProblem& P = probs[code >> 20];
         if (L.done && L.done[P.matrix * L.done_stride]) continue;
-        const int tm = (code >> 10) & 1023, tn = code & 1023;
-        const int nkb = (P.K + Cfg::BK - 1) / Cfg::BK;
-        for (int kb = 0; kb < nkb; ++kb) {
+        const int tm = (code >> 10) & 1023;
+        int tn = code & 1023, kb_lo, kb_hi;
+        tile_krange<Cfg>(P, tn, kb_lo, kb_hi);
+        for (int kb = kb_lo; kb < kb_hi; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sA = stage_base + stage * Cfg::STAGE_BYTES;
           uint8_t* sB = sA + Cfg::A_BYTES;
@@ -514,11 +595,12 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
         const uint32_t code = L.tiles[t];
         const GemmProblem& P = probs[code >> 20];
         if (L.done && L.done[P.matrix * L.done_stride]) continue;
-        const int nkb = (P.K + Cfg::BK - 1) / Cfg::BK;
+        int tn = code & 1023, kb_lo, kb_hi;
+        tile_krange<Cfg>(P, tn, kb_lo, kb_hi);
         // tf32: one TMEM accumulation chunk per PROMO_KB k-blocks, promoted to fp32
         // registers by the epilogue (bounds the truncation of the MMA accumulator add)
-        for (int kb0 = 0; kb0 < nkb; kb0 += Cfg::PROMO_KB) {
-          const int kb1 = min(nkb, kb0 + Cfg::PROMO_KB);
+        for (int kb0 = kb_lo; kb0 < kb_hi; kb0 += Cfg::PROMO_KB) {
+          const int kb1 = min(kb_hi, kb0 + Cfg::PROMO_KB);
           mbar_wait(&tempty[acc], acc_phase ^ 1);
           tc_fence_after();
           const uint32_t dt = tmem_base + acc * Cfg::BN;
@@ -550,111 +632,163 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
       }
     }
   } else {
-    // ===================== epilogue (warps 2..5) =====================
+    // ===================== epilogue (warps 2..9) =====================
     const int q = warp & 3;                 // TMEM lane quarter this warp may access
-    const int et = threadIdx.x - 64;        // 0..127
+    const int e = warp - 2;                 // 0..7
+    const int h = e >> 2;                   // column half of the tile owned by this warp
+    const int et = threadIdx.x - 64;        // 0..255
+    const int c_begin = h * Cfg::CH_PER;
+    const int c_end = min(Cfg::NCH, c_begin + Cfg::CH_PER);
+    float* tb = tbuf + e * 32 * 33;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < L.ntiles; t += gridDim.x) {
       const uint32_t code = L.tiles[t];
       const GemmProblem& P = probs[code >> 20];
       if (L.done && L.done[P.matrix * L.done_stride]) continue;
-      const int tm = (code >> 10) & 1023, tn = code & 1023;
+      const int tm = (code >> 10) & 1023;
+      int tn = code & 1023, kb_lo, kb_hi;
+      const int ks = tn;
+      tile_krange<Cfg>(P, tn, kb_lo, kb_hi);
       const int mode = P.mode;
       const bool sym = P.sym != 0;
-      const int i = tm * Cfg::BM + q * 32 + lane;   // output row of this thread
+      const int i0 = tm * Cfg::BM + q * 32;
+      const int i = i0 + lane;                     // output row of this thread
       float coefA = 1.f, coefC = 1.f;
       if (mode == EPI_POLY) { coefA = static_cast<float>(*P.alpha); coefC = P.c1; }
       if (mode == EPI_APPLY && P.scale_by_alpha) coefA = static_cast<float>(*P.alpha);
+      const bool needC = (mode == EPI_POLY || mode == EPI_APPLY);
       float sumsq = 0.f;
 
-      float* tb = tbuf + q * 32 * 33;
-      const int i0 = tm * Cfg::BM + q * 32;
-      const bool needC = (mode == EPI_POLY || mode == EPI_APPLY);
-      if constexpr (Cfg::PROMO_KB >= (1 << 20)) {
-        // bf16: one TMEM accumulator per tile, consumed 32 columns at a time; the C row
-        // segment of chunk ch+1 is fetched while chunk ch is processed
-        float cbuf[32];
+      if constexpr (Cfg::BN == 32) {
+        // thin chain GEMM: one 32-column chunk, owned by the h == 0 warps
+        float d[32];
 #pragma unroll
-        for (int u = 0; u < 32; ++u) cbuf[u] = 0.f;
-        if (needC && i < P.M && tn * Cfg::BN < P.N)
-          load_row32<Cfg::KIND, Cfg::SPLIT>(P.C, P.C_lo, P.ldc, i, tn * Cfg::BN, P.N, cbuf);
+        for (int u = 0; u < 32; ++u) d[u] = 0.f;
+        for (int kb0 = kb_lo; kb0 < kb_hi; kb0 += Cfg::PROMO_KB) {
+          mbar_wait(&tfull[acc], acc_phase);
+          tc_fence_after();
+          if (h == 0) {
+            uint32_t r[32];
+            tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * Cfg::BN, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int u = 0; u < 32; ++u) d[u] += __uint_as_float(r[u]);
+          }
+          tc_fence_before();
+          mbar_arrive(&tempty[acc]);
+          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+        if (P.ksplit > 1) {
+          // split-K: publish this slice, the last-arriving CTA of the row tile sums the
+          // slices in fixed order (deterministic) and runs the chain epilogue
+          if (h == 0 && i < P.M) {
+            float4* dst = reinterpret_cast<float4*>(P.kpart + ((long long)ks * P.M + i) * 32);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) dst[u] = make_float4(d[4 * u], d[4 * u + 1], d[4 * u + 2], d[4 * u + 3]);
+          }
+          __threadfence();
+          named_bar_sync(1, 32 * Cfg::EPI_WARPS);
+          if (et == 0) sflag[0] = (atomicAdd(&P.kcnt[tm], 1) == P.ksplit - 1) ? 1 : 0;
+          named_bar_sync(1, 32 * Cfg::EPI_WARPS);
+          if (!sflag[0]) continue;
+          __threadfence();
+          if (h == 0 && i < P.M) {
+#pragma unroll
+            for (int u = 0; u < 32; ++u) d[u] = 0.f;
+            for (int x = 0; x < P.ksplit; ++x) {
+              const float4* src = reinterpret_cast<const float4*>(P.kpart + ((long long)x * P.M + i) * 32);
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const float4 v = __ldcg(src + u);
+                d[4 * u] += v.x; d[4 * u + 1] += v.y; d[4 * u + 2] += v.z; d[4 * u + 3] += v.w;
+              }
+            }
+          }
+          if (et == 0) P.kcnt[tm] = 0;
+        }
+        epi_chain<Cfg>(P, i, tm, d, dred, e, lane, et, h == 0);
+      } else if constexpr (Cfg::KIND == 0) {
+        // bf16: one TMEM accumulator per tile; this warp consumes its 32-column chunks
+        // while the raw C row segment of the next chunk is in flight
+        uint4 craw[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) craw[u] = make_uint4(0, 0, 0, 0);
+        if (needC && i < P.M && tn * Cfg::BN + c_begin * 32 < P.N)
+          load_raw_bf16(P.C, P.ldc, i, tn * Cfg::BN + c_begin * 32, P.N, craw);
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
         const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * Cfg::BN;
 #pragma unroll 1
-        for (int ch = 0; ch < Cfg::BN / 32; ++ch) {
+        for (int ch = c_begin; ch < c_end; ++ch) {
           __syncwarp();
           uint32_t r[32];
           tmem_ld32(tbase + ch * 32, r);
+          uint4 cnext[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) cnext[u] = make_uint4(0, 0, 0, 0);
+          const int jn = tn * Cfg::BN + (ch + 1) * 32;
+          if (needC && ch + 1 < c_end && i < P.M && jn < P.N) load_raw_bf16(P.C, P.ldc, i, jn, P.N, cnext);
           tmem_ld_wait();
-          float d[32];
+          float d[32], c[32];
 #pragma unroll
           for (int u = 0; u < 32; ++u) d[u] = __uint_as_float(r[u]);
-          if constexpr (Cfg::BN == 32) {
-            epi_chain<Cfg>(P, i, tm, d, dred, q, lane, et);
-          } else {
-            float cnext[32];
+          decode_bf16(craw, c);
+          epi_segment<Cfg>(P, mode, sym, i0, lane, tn * Cfg::BN + ch * 32, coefA, coefC, d, c, tb, sumsq);
 #pragma unroll
-            for (int u = 0; u < 32; ++u) cnext[u] = 0.f;
-            const int jn = tn * Cfg::BN + (ch + 1) * 32;
-            if (needC && ch + 1 < Cfg::BN / 32 && i < P.M && jn < P.N)
-              load_row32<Cfg::KIND, Cfg::SPLIT>(P.C, P.C_lo, P.ldc, i, jn, P.N, cnext);
-            epi_segment<Cfg>(P, mode, sym, i0, lane, tn * Cfg::BN + ch * 32, coefA, coefC, d, cbuf, tb, sumsq);
-#pragma unroll
-            for (int u = 0; u < 32; ++u) cbuf[u] = cnext[u];
-          }
+          for (int u = 0; u < 4; ++u) craw[u] = cnext[u];
         }
         tc_fence_before();
         mbar_arrive(&tempty[acc]);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       } else {
         // tf32: sum the K-chunk partials from TMEM in fp32 registers (round-to-nearest)
-        float d[Cfg::BN / 32][32];
+        float d[Cfg::CH_PER][32];
 #pragma unroll
-        for (int ch = 0; ch < Cfg::BN / 32; ++ch)
+        for (int x = 0; x < Cfg::CH_PER; ++x)
 #pragma unroll
-          for (int u = 0; u < 32; ++u) d[ch][u] = 0.f;
+          for (int u = 0; u < 32; ++u) d[x][u] = 0.f;
         const int nkb = (P.K + Cfg::BK - 1) / Cfg::BK;
         for (int kb0 = 0; kb0 < nkb; kb0 += Cfg::PROMO_KB) {
           mbar_wait(&tfull[acc], acc_phase);
           tc_fence_after();
           const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * Cfg::BN;
 #pragma unroll
-          for (int ch = 0; ch < Cfg::BN / 32; ++ch) {
+          for (int x = 0; x < Cfg::CH_PER; ++x) {
             uint32_t r[32];
-            tmem_ld32(tbase + ch * 32, r);
+            tmem_ld32(tbase + (c_begin + x) * 32, r);
             tmem_ld_wait();
 #pragma unroll
-            for (int u = 0; u < 32; ++u) d[ch][u] += __uint_as_float(r[u]);
+            for (int u = 0; u < 32; ++u) d[x][u] += __uint_as_float(r[u]);
           }
           tc_fence_before();
           mbar_arrive(&tempty[acc]);
           if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
 #pragma unroll
-        for (int ch = 0; ch < Cfg::BN / 32; ++ch) {
-          if constexpr (Cfg::BN == 32) {
-            epi_chain<Cfg>(P, i, tm, d[ch], dred, q, lane, et);
-          } else {
-            float c[32];
+        for (int x = 0; x < Cfg::CH_PER; ++x) {
+          float c[32];
 #pragma unroll
-            for (int u = 0; u < 32; ++u) c[u] = 0.f;
-            const int j0 = tn * Cfg::BN + ch * 32;
-            if (needC && i < P.M && j0 < P.N) load_row32<Cfg::KIND, Cfg::SPLIT>(P.C, P.C_lo, P.ldc, i, j0, P.N, c);
-            epi_segment<Cfg>(P, mode, sym, i0, lane, j0, coefA, coefC, d[ch], c, tb, sumsq);
-          }
+          for (int u = 0; u < 32; ++u) c[u] = 0.f;
+          const int j0 = tn * Cfg::BN + (c_begin + x) * 32;
+          if (needC && i < P.M && j0 < P.N) load_row32<Cfg::KIND, Cfg::SPLIT>(P.C, P.C_lo, P.ldc, i, j0, P.N, c);
+          epi_segment<Cfg>(P, mode, sym, i0, lane, j0, coefA, coefC, d[x], c, tb, sumsq);
         }
       }
 
       if (mode == EPI_RESID && P.norm_part) {
-        // deterministic per-tile Σ out²: fixed shuffle tree, then 4 warps in order
+        // deterministic per-tile sum of out^2: fixed shuffle tree, then the 8 warps in order
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) sumsq += __shfl_xor_sync(0xffffffffu, sumsq, o);
-        if (lane == 0) red[q] = sumsq;
-        named_bar_sync(1, 128);
-        if (et == 0) P.norm_part[tm * P.tiles_n + tn] = (red[0] + red[1]) + (red[2] + red[3]);
-        named_bar_sync(1, 128);
+        if (lane == 0) red[e] = sumsq;
+        named_bar_sync(1, 32 * Cfg::EPI_WARPS);
+        if (et == 0) {
+          float tsum = 0.f;
+#pragma unroll
+          for (int x = 0; x < Cfg::EPI_WARPS; ++x) tsum += red[x];
+          P.norm_part[tm * P.tiles_n + tn] = tsum;
+        }
+        named_bar_sync(1, 32 * Cfg::EPI_WARPS);
       }
     }
   }

@@ -44,6 +44,8 @@ struct MatDesc {
   void* W[2];          // chain B operands [4p x ldS] (compute dtype), hi rows then lo rows
   float* keep;         // [4][s][p] kept chain columns (fp32)
   double* chain_part;  // [tiles_m][6] per-tile <Va,Vb>
+  float* kpart;        // [ksplit][s][32] chain split-K partials
+  int* kcnt;           // [tiles_m] chain split-K arrival counters
   long long ldS;
   int chain_tiles;
   int pad2_;
@@ -64,6 +66,8 @@ struct SolveParams {
   const int* tile_off;  // [batch + 1] prefix of 64x64 layout tiles (normalise: Xt; finalise: output)
   const int* out_tile_off;
   int n_tiles, n_out_tiles;
+  double* fro2_out;     // row-block begin: local sum of squares (else null)
+  const double* fro2_in;   // row-block: all-reduced sum of squares (else null)
   int batch, p, d, max_iters, warmup, fit, precision, kind_sqrt;
   double tol, alo, ahi, ataylor;
   unsigned long long seed;
@@ -140,8 +144,47 @@ __global__ void __launch_bounds__(256) k_fro_final(SolveParams P) {
   const int b = blockIdx.x;
   double v = (threadIdx.x < kFroParts) ? P.fro_part[b * kFroParts + threadIdx.x] : 0.0;
   v = block_sum<double, 256>(v, scratch);
-  if (threadIdx.x == 0) P.st[b].c = sqrt(v);
+  if (threadIdx.x == 0) {
+    if (P.fro2_out) P.fro2_out[b] = v;   // row-block: the caller all-reduces it
+    else P.st[b].c = sqrt(v);
+  }
 }
+
+// row-block: c = sqrt(all-reduced sum of squares)
+__global__ void k_set_c(SolveParams P) {
+  if (threadIdx.x == 0) P.st[blockIdx.x].c = sqrt(P.fro2_in[blockIdx.x]);
+}
+
+__global__ void k_set_iter(SolveParams P, int k) {
+  if (threadIdx.x == 0) *P.iter = k;
+}
+
+__device__ __forceinline__ void store_x(void* hi, void* lo, long long idx, float v, int precision);
+
+// row-block: R = I - G from the all-reduced fp32 Gram (n x n, ld n), diag(G), and the
+// per-tile sum of R^2 in the layout the alpha kernel reads (tiles of 128 x bn, sym = 0).
+template <int PREC>
+__global__ void __launch_bounds__(256) k_resid_from_gram(SolveParams P, const float* G, int bn) {
+  __shared__ double scratch[8];
+  const MatDesc& D = P.mats[0];
+  if (P.st[0].done) return;
+  const int n = D.s;
+  const int tm = blockIdx.y, tn = blockIdx.x;
+  double acc = 0.0;
+  for (int e = threadIdx.x; e < 128 * bn; e += 256) {
+    const int i = tm * 128 + e / bn, j = tn * bn + e % bn;
+    if (i >= n || j >= n) continue;
+    const float g = G[(long long)i * n + j];
+    const float r = (i == j ? 1.f : 0.f) - g;
+    store_x(D.R, D.R_lo, (long long)i * D.ldr + j, r, PREC);
+    if (i == j) D.gdiag[i] = g;
+    acc += (double)r * r;
+  }
+  acc = block_sum<double, 256>(acc, scratch);
+  if (threadIdx.x == 0) D.norm_part[tm * D.tiles_n + tn] = (float)acc;
+}
+
+// block -> (matrix, tile) over a batch-wide flat tile list
 
 // block -> (matrix, tile) over a batch-wide flat tile list (prefix array off[batch + 1])
 __device__ __forceinline__ int find_matrix(const int* off, int batch, int t) {
@@ -262,6 +305,9 @@ __global__ void __launch_bounds__(256) k_normalize(SolveParams P) {
       for (int e = 0; e < V::VE; ++e) x.v[e] = (col + e == r) ? 1.f : 0.f;
       x.store(D.Y[0], D.Y_lo[0], (long long)r * D.ldx + col, nv, nv == V::VE, 1.f, PREC == 1);
     }
+  }
+  if (lt == 0) {
+    for (int x = threadIdx.x; x < D.chain_tiles; x += 256) D.kcnt[x] = 0;
   }
   if (lt == 0 && threadIdx.x == 0) {
     if (b == 0) *P.iter = 0;

@@ -158,7 +158,7 @@ struct Plan {
   size_t meta_off = 0, meta_bytes = 0;
   std::unique_ptr<uint8_t, PinnedDeleter> blob;
   SolveParams params{};
-  LaunchDesc gram[2], square, apply[2], chain[5];
+  LaunchDesc gram[2], square, apply[2], chain[5], gram32[2];
   int n_chain = 0;
   bool has_square = false;
   int max_s = 0, max_rows = 0, max_cols = 0, max_m = 0, max_n = 0;
@@ -177,6 +177,8 @@ struct Request {
   const int64_t* ids;
   prism_options o;
   char* ws;   // null: size query only
+  bool rowblock = false;   // row-block member of a split tall matrix: force the tall form, s = n
+  float* G = nullptr;      // row-block: fp32 partial Gram output (n x n, ld n)
 };
 
 void resolve_interval(prism_options& o, double& lo, double& hi, double& aT, int& d) {
@@ -242,6 +244,9 @@ prism_status build_plan(const Request& r, Plan& P) {
   };
 
   P.max_s = P.max_rows = P.max_cols = P.max_m = P.max_n = 0;
+  // chain split-K (deterministic last-CTA reduction, gemm.cuh) is implemented but off:
+  // measured on B200 it lengthened the 4096^2 passes (40 us vs 29 us per pass)
+  const int ksplit = 1;
   for (int i = 0; i < B; ++i) {
     MatDesc& D = mats[i];
     std::memset(&D, 0, sizeof(D));
@@ -255,6 +260,7 @@ prism_status build_plan(const Request& r, Plan& P) {
     D.m = m;
     D.n = n;
     if (r.sqrt_kind) { D.s = n; D.L = n; }
+    else if (r.rowblock) { D.s = n; D.L = m; }
     else { D.s = std::min(m, n); D.L = std::max(m, n); }
     D.trans = 0;   // X keeps A's row-major layout (no transposes; MN-major operands instead)
     D.sketch_id = r.ids ? (int)r.ids[i] : i;
@@ -278,7 +284,7 @@ prism_status build_plan(const Request& r, Plan& P) {
     D.gdiag = reinterpret_cast<float*>(bump.take(sizeof(float) * s));
     D.tiles_m = (s + 127) / 128;
     D.tiles_n = (s + BN - 1) / BN;
-    D.sym = r.sqrt_kind ? 0 : 1;
+    D.sym = (r.sqrt_kind || r.rowblock) ? 0 : 1;
     D.norm_part = reinterpret_cast<float*>(bump.take(sizeof(float) * D.tiles_m * D.tiles_n));
     const long long ldS = (long long)align_up(s, 64);
     D.ldS = ldS;
@@ -288,6 +294,9 @@ prism_status build_plan(const Request& r, Plan& P) {
     D.keep = reinterpret_cast<float*>(bump.take(sizeof(float) * 4 * (size_t)s * p));
     D.chain_tiles = D.tiles_m;
     D.chain_part = reinterpret_cast<double*>(bump.take(sizeof(double) * 6 * D.tiles_m));
+    const int ks_i = std::max(1, std::min(ksplit, s / 64));
+    D.kpart = ks_i > 1 ? reinterpret_cast<float*>(bump.take(sizeof(float) * (size_t)ks_i * s * 32)) : nullptr;
+    D.kcnt = reinterpret_cast<int*>(bump.take(sizeof(int) * D.tiles_m));
     P.max_s = std::max(P.max_s, s);
     P.max_rows = std::max(P.max_rows, s);
     P.max_cols = std::max(P.max_cols, L);
@@ -311,7 +320,7 @@ prism_status build_plan(const Request& r, Plan& P) {
       // polar: X keeps A's row-major layout (m x n).  Tall (m >= n): G = X^T X with both
       // operands MN-major, X' = X + X P (A = X K-major, B = P K-major by symmetry).
       // Wide (m < n): G = X X^T (both K-major), X' = X + P X (B = X MN-major).
-      const bool tall = m >= n;
+      const bool tall = r.rowblock || m >= n;
       for (int t = 0; t < 2; ++t) {
         HostProblem g = mk(s, s, L, EPI_RESID, 1, D.R, D.R_lo, ldr, nullptr, nullptr, 0);
         g.p.norm_part = D.norm_part;
@@ -326,6 +335,17 @@ prism_status build_plan(const Request& r, Plan& P) {
           if (split) { g.mapA_lo = add_map(D.X_lo[t], m, n, ldx, OP_A); g.mapB_lo = add_map(D.X_lo[t], m, n, ldx, OP_BK); }
         }
         P.gram[t].probs.push_back(g);
+        if (r.rowblock) {
+          // partial Gram X_r^T X_r in fp32 into the caller's buffer (summed across ranks)
+          HostProblem g32 = g;
+          g32.p.mode = EPI_GRAM32;
+          g32.p.out = r.G;
+          g32.p.out_lo = nullptr;
+          g32.p.ldo = n;
+          g32.p.norm_part = nullptr;
+          g32.p.gdiag = nullptr;
+          P.gram32[t].probs.push_back(g32);
+        }
         const void* Pa = d == 2 ? Pm : D.R;
         const void* Pa_lo = d == 2 ? Pm_lo : D.R_lo;
         HostProblem a = mk(m, n, s, EPI_APPLY, 0, D.X[1 - t], D.X_lo[1 - t], ldx, D.X[t], D.X_lo[t], ldx);
@@ -411,6 +431,9 @@ prism_status build_plan(const Request& r, Plan& P) {
         c.p.ldr = ldr;
         c.p.p = p;
         c.p.tiles_n = 1;
+        c.p.ksplit = ks_i;
+        c.p.kpart = D.kpart;
+        c.p.kcnt = D.kcnt;
         c.mapA = add_map(D.R, s, s, ldr, OP_A);
         if (split) c.mapA_lo = add_map(D.R_lo, s, s, ldr, OP_A);
         maps.push_back(MapSpec{D.W[j % 2], N, s, D.ldS, esz, OP_BK, 32, BK});
@@ -432,12 +455,18 @@ prism_status build_plan(const Request& r, Plan& P) {
   for (int t = 0; t < 2; ++t) {
     finish(P.gram[t], !polar_k);
     finish(P.apply[t], true);
+    if (r.rowblock) finish(P.gram32[t], false);
   }
   if (P.has_square) finish(P.square, !polar_k);
   for (int j = 0; j < P.n_chain; ++j) {
     LaunchDesc& L = P.chain[j];
     L.tiles.clear();
-    for (int q = 0; q < (int)L.probs.size(); ++q) add_tiles(L, q, L.probs[q].p.M, L.probs[q].p.N, 32, false);
+    for (int q = 0; q < (int)L.probs.size(); ++q) {
+      const GemmProblem& gq = L.probs[q].p;
+      for (int tm = 0; tm < (gq.M + 127) / 128; ++tm)
+        for (int ks = 0; ks < gq.ksplit; ++ks)
+          L.tiles.push_back(((uint32_t)q << 20) | ((uint32_t)tm << 10) | (uint32_t)ks);
+    }
     sort_tiles_by_cost(L);
   }
   if ((int)P.apply[0].probs.size() >= 4096) return fail(PRISM_ERR_UNSUPPORTED, "batch too large (max 2047 sqrt / 4095 polar)");
@@ -460,8 +489,8 @@ prism_status build_plan(const Request& r, Plan& P) {
   off += sizeof(int) * (B + 1);
   const size_t ooff_off = off;
   off += sizeof(int) * (B + 1);
-  LaunchDesc* all[10] = {&P.gram[0], &P.gram[1], &P.apply[0], &P.apply[1], &P.square,
-                         &P.chain[0], &P.chain[1], &P.chain[2], &P.chain[3], &P.chain[4]};
+  LaunchDesc* all[12] = {&P.gram[0], &P.gram[1], &P.apply[0], &P.apply[1], &P.square,
+                         &P.chain[0], &P.chain[1], &P.chain[2], &P.chain[3], &P.chain[4], &P.gram32[0], &P.gram32[1]};
   for (LaunchDesc* L : all) {
     off = align_up(off, 128);
     L->probs_off = off;
@@ -654,6 +683,8 @@ struct KindTimer {
 static std::vector<long long> make_key(const Request& r) {
   std::vector<long long> k;
   k.push_back(r.sqrt_kind);
+  k.push_back(r.rowblock);
+  k.push_back((long long)(uintptr_t)r.G);
   k.push_back(r.batch);
   const prism_options& o = r.o;
   long long tolbits, alo, ahi;
@@ -677,9 +708,8 @@ static std::vector<long long> make_key(const Request& r) {
   return k;
 }
 
-static prism_status run_solve(prism_handle h, const Request& r0, const prism_report* rep, size_t ws_bytes,
-                              cudaStream_t st) {
-  Request r = r0;
+// Plan lookup (LRU keyed by every argument that shapes the tables) or build.
+static prism_status get_plan(prism_handle h, const Request& r, size_t ws_bytes, Plan** out) {
   if (!h) return fail(PRISM_ERR_INVALID_ARG, "null handle");
   prism_status v = validate(r);
   if (v) return v;
@@ -710,6 +740,16 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
     P = h->plans.front().get();
   }
   if (ws_bytes < P->ws_need) return fail(PRISM_ERR_INVALID_ARG, "workspace too small");
+  *out = P;
+  return PRISM_OK;
+}
+
+static prism_status run_solve(prism_handle h, const Request& r0, const prism_report* rep, size_t ws_bytes,
+                              cudaStream_t st) {
+  Request r = r0;
+  Plan* P = nullptr;
+  prism_status gs = get_plan(h, r, ws_bytes, &P);
+  if (gs) return gs;
 
   PRISM_CK(cudaMemcpyAsync(r.ws + P->meta_off, P->blob.get(), P->meta_bytes, cudaMemcpyHostToDevice, st));
   SolveParams S = P->params;   // report pointers are only read by k_report (outside the graph)
@@ -962,6 +1002,125 @@ prism_status prism_profile_read(prism_handle h, double* ms, int64_t* launches, i
     if (launches) launches[k] = h->acc_launches[k];
     if (reset) { h->acc_ms[k] = 0; h->acc_launches[k] = 0; }
   }
+  return PRISM_OK;
+}
+
+// ---------------------------------------------------------------- row-block split
+// State of the handle's current row-block solve (set by prism_rowblock_begin).
+static thread_local struct RowBlockState {
+  Plan* plan = nullptr;
+  char* ws = nullptr;
+  int prec = 0, max_iters = 0, warmup = 0, fit = 0;
+} g_rb;
+
+size_t prism_rowblock_workspace(prism_handle h, int64_t rows, int64_t n, const prism_options* o) {
+  if (!h || !o || rows < 1 || n < 1) return 0;
+  const void* fakeA = reinterpret_cast<const void*>(256);
+  void* fakeQ = reinterpret_cast<void*>(256);
+  int64_t ld = n;
+  Request r{false, 1, &rows, &n, &fakeA, &ld, &fakeQ, nullptr, &ld, nullptr, *o, nullptr};
+  r.rowblock = true;
+  r.G = reinterpret_cast<float*>(256);
+  if (validate(r)) return 0;
+  Plan P;
+  if (build_plan(r, P)) return 0;
+  return P.ws_need;
+}
+
+prism_status prism_rowblock_begin(prism_handle h, int64_t rows, int64_t n, const void* A_rows, int64_t lda,
+                                  void* Q_rows, int64_t ldq, float* G, double* fro2_local, const prism_options* o,
+                                  void* workspace, size_t ws_bytes, void* stream) {
+  try {
+    if (!o || !G || !fro2_local) return fail(PRISM_ERR_INVALID_ARG, "null options / G / fro2 buffer");
+    const void* A = A_rows;
+    void* Q = Q_rows;
+    Request r{false, 1, &rows, &n, &A, &lda, &Q, nullptr, &ldq, nullptr, *o, static_cast<char*>(workspace)};
+    r.rowblock = true;
+    r.G = G;
+    Plan* P = nullptr;
+    prism_status gs = get_plan(h, r, ws_bytes, &P);
+    if (gs) return gs;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    PRISM_CK(cudaMemcpyAsync(r.ws + P->meta_off, P->blob.get(), P->meta_bytes, cudaMemcpyHostToDevice, st));
+    SolveParams S = P->params;
+    S.fro2_out = fro2_local;
+    k_fro_partials<<<dim3(kFroParts, 1), 256, 0, st>>>(S);
+    k_fro_final<<<1, 256, 0, st>>>(S);
+    PRISM_CK(cudaGetLastError());
+    g_rb.plan = P;
+    g_rb.ws = r.ws;
+    g_rb.prec = o->precision;
+    g_rb.max_iters = o->max_iters;
+    g_rb.warmup = o->warmup_iters;
+    g_rb.fit = o->fit;
+    return PRISM_OK;
+  } catch (...) {
+    return fail(PRISM_ERR_INTERNAL, "exception in prism_rowblock_begin");
+  }
+}
+
+prism_status prism_rowblock_gram(prism_handle h, int k, const double* fro2_global, void* stream) {
+  if (!h || !g_rb.plan) return fail(PRISM_ERR_INVALID_ARG, "prism_rowblock_begin not called");
+  Plan* P = g_rb.plan;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  SolveParams S = P->params;
+  if (k == 0) {
+    if (!fro2_global) return fail(PRISM_ERR_INVALID_ARG, "null fro2_global at k = 0");
+    S.fro2_in = fro2_global;
+    k_set_c<<<1, 32, 0, st>>>(S);
+    if (g_rb.prec == PRISM_BF16) k_normalize<0><<<S.n_tiles, 256, 0, st>>>(S);
+    else if (g_rb.prec == PRISM_FP32) k_normalize<1><<<S.n_tiles, 256, 0, st>>>(S);
+    else k_normalize<2><<<S.n_tiles, 256, 0, st>>>(S);
+  }
+  k_set_iter<<<1, 32, 0, st>>>(S, k);
+  GemmLaunch g = make_launch(*P, P->gram32[0], &P->gram32[1], g_rb.ws, 0, g_rb.max_iters + 1);
+  PRISM_CK(launch_gemm(g_rb.prec, g, st));
+  PRISM_CK(cudaGetLastError());
+  return PRISM_OK;
+}
+
+prism_status prism_rowblock_update(prism_handle h, int k, const float* G, int32_t* all_done, void* stream) {
+  if (!h || !g_rb.plan) return fail(PRISM_ERR_INVALID_ARG, "prism_rowblock_begin not called");
+  if (!G) return fail(PRISM_ERR_INVALID_ARG, "null G");
+  Plan* P = g_rb.plan;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  SolveParams S = P->params;
+  const int prec = g_rb.prec, M = g_rb.max_iters;
+  const int bn = tile_bn(prec);
+  const int n = P->max_s;
+  const dim3 rg((n + bn - 1) / bn, (n + 127) / 128);
+  if (prec == PRISM_BF16) k_resid_from_gram<0><<<rg, 256, 0, st>>>(S, G, bn);
+  else if (prec == PRISM_FP32) k_resid_from_gram<1><<<rg, 256, 0, st>>>(S, G, bn);
+  else k_resid_from_gram<2><<<rg, 256, 0, st>>>(S, G, bn);
+  if (g_rb.fit == PRISM_FIT_SKETCHED) {
+    k_sketch<<<dim3((S.p * n / 2 + 256) / 256, 1), 256, 0, st>>>(S);
+    for (int j = 0; j < P->n_chain; ++j)
+      PRISM_CK(launch_chain(prec, make_launch(*P, P->chain[j], nullptr, g_rb.ws, g_rb.warmup, M), st));
+  }
+  k_alpha<<<1, 256, 0, st>>>(S);
+  if (P->has_square) PRISM_CK(launch_gemm(prec, make_launch(*P, P->square, nullptr, g_rb.ws, 0, M), st));
+  PRISM_CK(launch_gemm(prec, make_launch(*P, P->apply[0], &P->apply[1], g_rb.ws, 0, M), st));
+  k_advance<<<1, 256, 0, st>>>(S, 0, 0, all_done ? reinterpret_cast<int*>(all_done) : P->d_all_done);
+  PRISM_CK(cudaGetLastError());
+  return PRISM_OK;
+}
+
+prism_status prism_rowblock_end(prism_handle h, const prism_report* rep, void* stream) {
+  if (!h || !g_rb.plan) return fail(PRISM_ERR_INVALID_ARG, "prism_rowblock_begin not called");
+  Plan* P = g_rb.plan;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  SolveParams S = P->params;
+  S.rep_iters = rep ? rep->iters : nullptr;
+  S.rep_resid = rep ? rep->resid : nullptr;
+  S.rep_status = rep ? rep->status : nullptr;
+  S.rep_alphas = rep ? rep->alphas : nullptr;
+  S.rep_resid_hist = rep ? rep->resid_hist : nullptr;
+  if (g_rb.prec == PRISM_BF16) k_finalize<0><<<S.n_out_tiles, 256, 0, st>>>(S);
+  else if (g_rb.prec == PRISM_FP32) k_finalize<1><<<S.n_out_tiles, 256, 0, st>>>(S);
+  else k_finalize<2><<<S.n_out_tiles, 256, 0, st>>>(S);
+  if (rep) k_report<<<1, 256, 0, st>>>(S);
+  PRISM_CK(cudaGetLastError());
+  g_rb.plan = nullptr;
   return PRISM_OK;
 }
 

@@ -165,3 +165,50 @@ def test_gpt2_batch_full_size_sampled():
         Qo, ro = prism.polar(mats[i].double().cpu().numpy(), d=2, p=8, tol=3e-2, max_iters=20, seed=42, b=i)
         assert abs(int(rep["iters"][i]) - ro.iters) <= 1
         assert _rel(Q[i].double().cpu().numpy(), Qo) <= 2e-2
+
+
+def test_rowblock_two_ranks_emulated_equals_single_solve():
+    """Row-block split (configs[3] path) with 2 ranks emulated by 2 host threads on one
+    GPU: the all-reduce is a host-synchronised sum of the two partial Grams (no kernel
+    waits on another), so the ranks' kernels never depend on each other in flight."""
+    import threading
+    from paper_2601_22137_b200 import dist as PD
+    from paper_2601_22137_b200.binding import RowBlockSolver
+    m, n = 1024, 384
+    A = torch.tensor(W.gaussian(m, n, seed=21)).float().cuda()
+    parts = [A[:640].contiguous(), A[640:].contiguous()]
+    bar = threading.Barrier(2)
+    slot = [None, None]
+    res = [None, None]
+
+    def allreduce_factory(rank):
+        def ar(t):
+            torch.cuda.synchronize()
+            slot[rank] = t.clone()
+            bar.wait()
+            total = slot[0] + slot[1]          # same order on both ranks -> identical bits
+            bar.wait()
+            t.copy_(total)
+            torch.cuda.synchronize()
+        return ar
+
+    def run(rank):
+        st = RowBlockSolver(parts[rank], degree=5, tol=1e-5, max_iters=30, precision="fp32",
+                            stream=torch.cuda.Stream())
+        with torch.cuda.stream(st.stream):
+            res[rank] = PD.polar_rowblock(parts[rank], allreduce=allreduce_factory(rank), steps=st)
+        torch.cuda.synchronize()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    Q = torch.cat([res[0][0], res[1][0]]).double().cpu().numpy()
+    Qs, rs = P.polar([A], degree=5, tol=1e-5, max_iters=30, precision="fp32", matrix_ids=[0])
+    torch.cuda.synchronize()
+    Qo, ro = prism.polar(A.double().cpu().numpy(), d=2, p=8, tol=1e-5, max_iters=30, seed=42, b=0)
+    assert int(res[0][1]["iters"][0]) == int(res[1][1]["iters"][0])
+    assert abs(int(res[0][1]["iters"][0]) - ro.iters) <= 1
+    assert _rel(Q, Qo) <= 1e-5
+    assert _rel(Q, Qs[0].double().cpu().numpy()) <= 1e-5
