@@ -59,7 +59,8 @@ EXPORTS = [
     "prism_launch_count", "prism_profile_enable", "prism_profile_read",
     "prism_rowblock_workspace", "prism_rowblock_begin", "prism_rowblock_gram", "prism_rowblock_update",
     "prism_rowblock_end",
-    "prism_debug_gemm", "prism_debug_sketch", "prism_debug_argmin",
+    "prism_debug_gemm", "prism_debug_sketch", "prism_debug_argmin", "prism_debug_trace",
+    "prism_debug_trace_gemm",
 ]
 
 _lib = None
@@ -113,9 +114,11 @@ def lib():
         L.prism_rowblock_end.argtypes = [vp, ctypes.POINTER(Report), vp]
         L.prism_debug_sketch.argtypes = [u64, i64, i32, i32, i32, vp, vp]
         L.prism_debug_argmin.argtypes = [i32, vp, dbl, dbl, dbl, vp, vp]
+        L.prism_debug_trace.argtypes = [vp]
+        L.prism_debug_trace_gemm.argtypes = [vp, i32]
         for name in ("prism_create", "prism_destroy", "prism_polar", "prism_sqrt_invsqrt", "prism_lpt_partition",
-                     "prism_debug_gemm", "prism_debug_sketch", "prism_debug_argmin",
-                     "prism_profile_enable", "prism_profile_read", "prism_rowblock_begin",
+                     "prism_debug_gemm", "prism_debug_sketch", "prism_debug_argmin", "prism_debug_trace",
+                     "prism_debug_trace_gemm", "prism_profile_enable", "prism_profile_read", "prism_rowblock_begin",
                      "prism_rowblock_gram", "prism_rowblock_update", "prism_rowblock_end"):
             getattr(L, name).restype = i32
         _lib = L

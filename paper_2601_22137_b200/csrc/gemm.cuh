@@ -56,8 +56,6 @@ struct GemmProblem {
   int pass;              // EPI_CHAIN pass code
   int a_mn, b_mn;        // operand major-ness: 0 K-major, 1 MN-major
   int ksplit;            // EPI_CHAIN split-K slices (tile code tn = slice index) or 1
-  float* kpart;          // [ksplit][M][32] split-K partials
-  int* kcnt;             // [tiles_m] arrival counters (self-resetting)
   // EPI_CHAIN operands (row i of R = row i of the output)
   const float* S;        // [p][ldS] sketch (fp32)
   const void* Rg;        // R (for R_ii), compute dtype (+ R_lo in 3xTF32)
@@ -79,24 +77,38 @@ struct GemmLaunch {
   int done_stride;
   int ntiles;
   int iter_lo, iter_hi;
+  int ksplit;                    // chain split-K: cluster size (the CTAs of one row tile), else 1
 };
 
-template <int KIND_, bool SPLIT_, int BN_ = 0>
+template <int KIND_, bool SPLIT_, int BN_ = 0, bool CTA2_ = (BN_ == 0)>
 struct GemmCfg {
   static constexpr int KIND = KIND_;
   static constexpr bool SPLIT = SPLIT_;
+  // CTA pair (cta_group::2): a cluster of 2 CTAs computes a 256 x BN tile; each CTA
+  // loads its 128 rows of A and half of B (BN/2 rows), holds 128 x BN of the
+  // accumulator, and only the even CTA issues the MMAs.  Cuts the L2 -> SMEM operand
+  // traffic per FLOP by a third versus 128 x BN single-CTA tiles.
+  static constexpr bool CTA2 = CTA2_;
+  static constexpr int CG = CTA2 ? 2 : 1;
   static constexpr int ESZ = KIND == 0 ? 2 : 4;
-  static constexpr int BM = 128;
+  static constexpr int BM = 128;                  // rows per CTA
+  static constexpr int TILE_M = BM * CG;          // rows per (pair) tile
   static constexpr int BN = BN_ ? BN_ : (KIND == 0 ? 256 : 128);
+  static constexpr int B_ROWS = BN / CG;          // B rows (along N) loaded per CTA
   // thin chain GEMM (BN = 32): B already carries [W_hi | W_lo], so 3xTF32 needs
   // only A_lo · B besides A · B (no B_lo plane)
   static constexpr bool LOB = SPLIT && BN != 32;
   static constexpr int BK = 128 / ESZ;          // one 128-B swizzle row of K
   static constexpr int UK = 32 / ESZ;           // K per tcgen05.mma (32 bytes)
   static constexpr int A_BYTES = BM * BK * ESZ;
-  static constexpr int B_BYTES = BN * BK * ESZ;
+  static constexpr int B_BYTES = B_ROWS * BK * ESZ;
   static constexpr int STAGE_BYTES = (SPLIT ? 2 * A_BYTES : A_BYTES) + (LOB ? 2 * B_BYTES : B_BYTES);
-  static constexpr int STAGES_RAW = (192 * 1024) / STAGE_BYTES;
+  // chain split-K: the leader CTA of a cluster receives up to 3 fp32 128 x 32 partials
+  // (DSMEM), in the transpose-buffer region (unused by the chain epilogue) and beyond
+  static constexpr int TB_BYTES = 8 * 32 * 33 * 4;   // per-epilogue-warp 32x33 fp32 transpose buffers
+  static constexpr int RED_BYTES = BN == 32 ? 3 * 32 * 128 * 4 : 0;
+  static constexpr int SCRATCH_BYTES = RED_BYTES > TB_BYTES ? RED_BYTES : TB_BYTES;
+  static constexpr int STAGES_RAW = (192 * 1024 - (SCRATCH_BYTES - TB_BYTES)) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int TMEM_COLS = 2 * BN;
   static constexpr int AE = 128 / ESZ;           // elements per 128-B atom along MN (MN-major)
@@ -105,12 +117,11 @@ struct GemmCfg {
   // the 128-B/32-B-atom swizzle (layout type 1, 4-row K groups, SBO 512).
   static constexpr uint32_t MN_LAYOUT = KIND == 0 ? 2u : 1u;
   static constexpr uint32_t MN_SBO = KIND == 0 ? 1024u : 512u;
-  static constexpr uint32_t IDESC = idesc_make(KIND == 0 ? 1u : 2u, 0u, BM, BN);
+  static constexpr uint32_t IDESC = idesc_make(KIND == 0 ? 1u : 2u, 0u, TILE_M, BN);
   static constexpr int EPI_WARPS = 8;   // two per TMEM lane quarter, each owning half the columns
   static constexpr int NCH = BN / 32;   // 32-column chunks per tile
   static constexpr int CH_PER = NCH >= 2 ? NCH / 2 : 1;
-  static constexpr int TB_BYTES = EPI_WARPS * 32 * 33 * 4;   // per-epilogue-warp 32x33 fp32 transpose buffers
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers, scratch*/ + TB_BYTES;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers, scratch*/ + SCRATCH_BYTES;
   static constexpr int THREADS = 64 + 32 * EPI_WARPS;
   // k-blocks per TMEM accumulation chunk: tf32 partials are promoted to fp32
   // registers every k-block (3xTF32, K = 32: 12 MMAs per chunk) or every 4
@@ -200,6 +211,52 @@ __device__ __forceinline__ void decode_bf16(const uint4 (&w)[4], float (&c)[32])
       c[u * 8 + 2 * e + 1] = f.y;
     }
   }
+}
+
+// ---- coalesced 32 x 32 bf16 block moves for an epilogue warp (one row per lane in
+// registers).  A lane-per-row access makes every warp instruction touch 32 lines with
+// 16-B pieces; restaging through the warp's smem buffer (32 rows x 64 B, 16-B chunks
+// XOR-swizzled: conflict-free both ways) lets each instruction move 8 rows x 64 B.
+__device__ __forceinline__ uint32_t stg_off(int row, int ch) { return (uint32_t)(row * 64 + ((ch ^ ((row >> 1) & 3)) << 4)); }
+
+// this lane's row v[32] -> rows [r0, r0 + 32) x cols [c0, c0 + 32) of out (block fully in bounds)
+__device__ __forceinline__ void warp_store_bf16_block(void* out, long long ld, long long r0, long long c0,
+                                                      const float (&v)[32], uint8_t* stg, int lane) {
+#pragma unroll
+  for (int ch = 0; ch < 4; ++ch) {
+    uint4 w;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&w);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(v[ch * 8 + 2 * e], v[ch * 8 + 2 * e + 1]);
+    *reinterpret_cast<uint4*>(stg + stg_off(lane, ch)) = w;
+  }
+  __syncwarp();
+  __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out);
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int row = u * 8 + (lane >> 2), ch = lane & 3;
+    *reinterpret_cast<uint4*>(o + (r0 + row) * ld + c0 + ch * 8) = *reinterpret_cast<const uint4*>(stg + stg_off(row, ch));
+  }
+  __syncwarp();
+}
+// coalesced global read of a 32 x 32 bf16 block (registers, in flight) ...
+__device__ __forceinline__ void warp_load_bf16_block(const void* base, long long ld, long long r0, long long c0,
+                                                     uint4 (&g)[4], int lane) {
+  const __nv_bfloat16* p = static_cast<const __nv_bfloat16*>(base);
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+    g[u] = __ldg(reinterpret_cast<const uint4*>(p + (r0 + u * 8 + (lane >> 2)) * ld + c0 + (lane & 3) * 8));
+}
+// ... then redistributed so that this lane holds its row as 32 floats
+__device__ __forceinline__ void warp_rows_from_block(const uint4 (&g)[4], uint8_t* stg, int lane, float (&c)[32]) {
+#pragma unroll
+  for (int u = 0; u < 4; ++u) *reinterpret_cast<uint4*>(stg + stg_off(u * 8 + (lane >> 2), lane & 3)) = g[u];
+  __syncwarp();
+  uint4 w[4];
+#pragma unroll
+  for (int ch = 0; ch < 4; ++ch) w[ch] = *reinterpret_cast<const uint4*>(stg + stg_off(lane, ch));
+  __syncwarp();
+  decode_bf16(w, c);
 }
 
 template <int KIND, bool SPLIT>
@@ -304,8 +361,16 @@ __device__ __forceinline__ void epi_segment(const GemmProblem& P, int mode, bool
   }
   const long long off = (long long)i * P.ldo + j0;
   const bool full_n = j0 + 32 <= P.N;
+  const bool full_blk = full_n && i0 + 32 <= P.M;   // warp-uniform
+  uint8_t* stg = reinterpret_cast<uint8_t*>(tb);
   if (!sym) {
-    if (row_ok) {
+    if (Cfg::KIND == 0 && full_blk) {
+      warp_store_bf16_block(P.out, P.ldo, i0, j0, v, stg, lane);
+      if (mode == EPI_RESID) {
+#pragma unroll
+        for (int u = 0; u < 32; ++u) sumsq = fmaf(v[u], v[u], sumsq);
+      }
+    } else if (row_ok) {
       if (full_n) {
         store_row32<Cfg::KIND, Cfg::SPLIT>(P.out, P.out_lo, off, v);
         if (mode == EPI_RESID) {
@@ -324,7 +389,13 @@ __device__ __forceinline__ void epi_segment(const GemmProblem& P, int mode, bool
   }
   // symmetric: upper triangle (j >= i) written directly, (j > i) mirrored to (j, i)
   const bool diag = j0 < i0 + 32;                // 32-aligned blocks: the diagonal block
-  if (row_ok) {
+  if (Cfg::KIND == 0 && !diag && full_blk) {
+    warp_store_bf16_block(P.out, P.ldo, i0, j0, v, stg, lane);
+    if (mode == EPI_RESID) {
+#pragma unroll
+      for (int u = 0; u < 32; ++u) sumsq = fmaf(2.f * v[u], v[u], sumsq);
+    }
+  } else if (row_ok) {
     if (!diag && full_n) {
       store_row32<Cfg::KIND, Cfg::SPLIT>(P.out, P.out_lo, off, v);
       if (mode == EPI_RESID) {
@@ -352,7 +423,11 @@ __device__ __forceinline__ void epi_segment(const GemmProblem& P, int mode, bool
 #pragma unroll
     for (int u = 0; u < 32; ++u) w[u] = tb[u * 33 + lane];
     const long long moff = (long long)j * P.ldo + i0;
-    if (!diag && i0 + 32 <= P.M) {
+    if (Cfg::KIND == 0 && !diag && full_blk) {
+      // (whole warp: full_blk implies j < P.N for every lane)
+      __syncwarp();
+      warp_store_bf16_block(P.out, P.ldo, j0, i0, w, stg, lane);
+    } else if (!diag && i0 + 32 <= P.M) {
       store_row32<Cfg::KIND, Cfg::SPLIT>(P.out, P.out_lo, moff, w);
     } else {
 #pragma unroll
@@ -380,79 +455,120 @@ __device__ __forceinline__ void store_w(const GemmProblem& P, int c, int wn, int
 
 template <class Cfg>
 __device__ __forceinline__ void epi_chain(const GemmProblem& P, int i, int tm, const float (&d)[32], double* dred,
-                                          int e, int lane, int et, bool active) {
+                                          int e, int lane, int et, int h) {
+  // Row i of the pass output; the two warps sharing a TMEM lane quarter split the p
+  // sketch rows c (h = 0: c < p/2, h = 1: the rest).  Every load is issued before the
+  // first store (the output and keep buffers would otherwise serialise them).
   const int p = P.p;
   const int w = P.N / 2;          // columns of this pass's output
-  const bool valid = active && i < P.M;
+  const bool valid = i < P.M;
+  const int c0 = h ? (p + 1) / 2 : 0;
+  const int c1 = h ? p : (p + 1) / 2;
   double g[6] = {0, 0, 0, 0, 0, 0};
-  float o[16];
+  // o[c] = d[c] + d[w + c] (hi + lo halves of the pass output); the runtime shifts by w
+  // and p are done by conditional fixed shifts so d / o stay in registers
+  float t[32];
 #pragma unroll
-  for (int c = 0; c < 16; ++c) o[c] = (c < w) ? d[c] + d[w + c] : 0.f;
-  float* keep = P.keep;
-  const long long M = P.M;
-  auto K = [&](int slot, int c) -> float& { return keep[((long long)slot * M + i) * p + c]; };
-  if (valid) {
-    switch (P.pass) {
-      case CH2_P1:
-      case CH1_P1: {
-        float rii;
-        if constexpr (Cfg::KIND == 0) rii = __bfloat162float(static_cast<const __nv_bfloat16*>(P.Rg)[(long long)i * P.ldr + i]);
-        else rii = static_cast<const float*>(P.Rg)[(long long)i * P.ldr + i] +
-                   (P.Rg_lo ? static_cast<const float*>(P.Rg_lo)[(long long)i * P.ldr + i] : 0.f);
-        const float gii = P.gdiag[i];
-        for (int c = 0; c < p; ++c) {
-          const float sc = P.S[(long long)c * P.ldS + i];
-          const float qv = gii * sc - (o[c] - rii * sc);   // Q = G S^T, G_ii exact (fp32 from the Gram)
-          if (P.pass == CH2_P1) {
-            store_w<Cfg>(P, c, 2 * p, i, o[c]);
-            store_w<Cfg>(P, p + c, 2 * p, i, qv);
-          } else {
-            K(0, c) = o[c];
-            store_w<Cfg>(P, c, p, i, qv);
-          }
-        }
-        break;
+  for (int u = 0; u < 32; ++u) t[u] = d[u];
+#pragma unroll
+  for (int bit = 16; bit >= 1; bit >>= 1)
+    if (w & bit) {
+#pragma unroll
+      for (int u = 0; u < 32; ++u) t[u] = (u + bit < 32) ? t[u + bit] : 0.f;
+    }
+  float o[16], op[8];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) o[c] = (c < w) ? d[c] + t[c] : 0.f;
+  {
+    float sh[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) sh[c] = o[c];
+#pragma unroll
+    for (int bit = 8; bit >= 1; bit >>= 1)
+      if (p & bit) {
+#pragma unroll
+        for (int c = 0; c < 16; ++c) sh[c] = (c + bit < 16) ? sh[c + bit] : 0.f;
       }
-      case CH2_P2:
-        for (int c = 0; c < p; ++c) {
-          K(0, c) = o[c];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) op[c] = sh[c];   // op[c] = op[c]
+  }
+  float* __restrict__ keep = P.keep;
+  const long long M = P.M;
+  const int pass = P.pass;
+  if (valid) {
+    if (pass == CH2_P1 || pass == CH1_P1) {
+      float rii;
+      if constexpr (Cfg::KIND == 0) rii = __bfloat162float(static_cast<const __nv_bfloat16*>(P.Rg)[(long long)i * P.ldr + i]);
+      else rii = static_cast<const float*>(P.Rg)[(long long)i * P.ldr + i] +
+                 (P.Rg_lo ? static_cast<const float*>(P.Rg_lo)[(long long)i * P.ldr + i] : 0.f);
+      const float gii = P.gdiag[i];
+      float sc[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) sc[c] = (c >= c0 && c < c1) ? __ldg(P.S + (long long)c * P.ldS + i) : 0.f;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        if (c < c0 || c >= c1) continue;
+        const float qv = gii * sc[c] - (o[c] - rii * sc[c]);   // Q = G S^T, G_ii exact (fp32 from the Gram)
+        if (pass == CH2_P1) {
           store_w<Cfg>(P, c, 2 * p, i, o[c]);
-          store_w<Cfg>(P, p + c, 2 * p, i, o[p + c]);
+          store_w<Cfg>(P, p + c, 2 * p, i, qv);
+        } else {
+          keep[i * p + c] = o[c];
+          store_w<Cfg>(P, c, p, i, qv);
         }
-        break;
-      case CH2_P3:
-        for (int c = 0; c < p; ++c) {
-          K(1, c) = o[c];
-          K(2, c) = o[p + c];
-          store_w<Cfg>(P, c, p, i, o[p + c]);
+      }
+    } else if (pass == CH2_P2) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        if (c < c0 || c >= c1) continue;
+        keep[i * p + c] = o[c];
+        store_w<Cfg>(P, c, 2 * p, i, o[c]);
+        store_w<Cfg>(P, p + c, 2 * p, i, op[c]);
+      }
+    } else if (pass == CH2_P3) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        if (c < c0 || c >= c1) continue;
+        keep[(M + i) * p + c] = o[c];
+        keep[(2 * M + i) * p + c] = op[c];
+        store_w<Cfg>(P, c, p, i, op[c]);
+      }
+    } else if (pass == CH2_P4 || pass == CH1_P2) {
+      const long long slot = pass == CH2_P4 ? 3 : 1;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        if (c < c0 || c >= c1) continue;
+        keep[(slot * M + i) * p + c] = o[c];
+        store_w<Cfg>(P, c, p, i, o[c]);
+      }
+    } else {
+      // CH2_P5 / CH1_P3: inner products <Va, Vb> (fp64 products of widened factors)
+      const int ns = pass == CH2_P5 ? 4 : 2;
+      float kv[4][8];
+#pragma unroll
+      for (int sl = 0; sl < 4; ++sl)
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          kv[sl][c] = (sl < ns && c >= c0 && c < c1) ? __ldcg(keep + ((long long)sl * M + i) * p + c) : 0.f;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        if (c < c0 || c >= c1) continue;
+        double v0, v1, v2;
+        if (pass == CH2_P5) {
+          v0 = 0.25 * (3.0 * (double)kv[0][c] + (double)kv[1][c]);   // 1/4 (3 K2 + K3)
+          v1 = -((double)kv[3][c] + 2.0 * (double)kv[2][c]);         // -(L3 + 2 L2)
+          v2 = -(double)o[c];                                        // -L4
+        } else {
+          v0 = (double)kv[0][c];                                     // K1
+          v1 = -2.0 * (double)kv[1][c];                              // -2 L1
+          v2 = -(double)o[c];                                        // -L2
         }
-        break;
-      case CH2_P4:
-      case CH1_P2:
-        for (int c = 0; c < p; ++c) {
-          K(P.pass == CH2_P4 ? 3 : 1, c) = o[c];
-          store_w<Cfg>(P, c, p, i, o[c]);
-        }
-        break;
-      default:  // CH2_P5 / CH1_P3: inner products <Va, Vb> (fp64 products of widened factors)
-        for (int c = 0; c < p; ++c) {
-          double v0, v1, v2;
-          if (P.pass == CH2_P5) {
-            v0 = 0.25 * (3.0 * (double)K(0, c) + (double)K(1, c));   // 1/4 (3 K2 + K3)
-            v1 = -((double)K(3, c) + 2.0 * (double)K(2, c));         // -(L3 + 2 L2)
-            v2 = -(double)o[c];                                      // -L4
-          } else {
-            v0 = (double)K(0, c);                                    // K1
-            v1 = -2.0 * (double)K(1, c);                             // -2 L1
-            v2 = -(double)o[c];                                      // -L2
-          }
-          g[0] += v0 * v0; g[1] += v0 * v1; g[2] += v0 * v2;
-          g[3] += v1 * v1; g[4] += v1 * v2; g[5] += v2 * v2;
-        }
-        break;
+        g[0] += v0 * v0; g[1] += v0 * v1; g[2] += v0 * v2;
+        g[3] += v1 * v1; g[4] += v1 * v2; g[5] += v2 * v2;
+      }
     }
   }
-  if (P.pass == CH2_P5 || P.pass == CH1_P3) {
+  if (pass == CH2_P5 || pass == CH1_P3) {
 #pragma unroll
     for (int j = 0; j < 6; ++j) {
 #pragma unroll
@@ -477,11 +593,12 @@ __device__ __forceinline__ void epi_chain(const GemmProblem& P, int i, int tm, c
 template <class Cfg>
 __device__ __forceinline__ void tile_krange(const GemmProblem& P, int& tn, int& kb_lo, int& kb_hi) {
   const int nkb = (P.K + Cfg::BK - 1) / Cfg::BK;
-  if (P.ksplit > 1) {
+  if (P.mode == EPI_CHAIN) {
+    // slice ks of P.ksplit; slices past the matrix's own factor (launch cluster larger) are empty
     const int ks = tn;
     tn = 0;
-    kb_lo = ks * nkb / P.ksplit;
-    kb_hi = (ks + 1) * nkb / P.ksplit;
+    kb_lo = ks < P.ksplit ? ks * nkb / P.ksplit : nkb;
+    kb_hi = ks < P.ksplit ? (ks + 1) * nkb / P.ksplit : nkb;
   } else {
     kb_lo = 0;
     kb_hi = nkb;
@@ -490,13 +607,19 @@ __device__ __forceinline__ void tile_krange(const GemmProblem& P, int& tn, int& 
 
 // TMA load of one operand tile (rows = BM or BN along MN, BK along K) into smem.
 template <class Cfg>
+__device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  if constexpr (Cfg::CTA2) tma_load_2d_pair(dst, map, bar, c0, c1);
+  else tma_load_2d(dst, map, bar, c0, c1);
+}
+
+template <class Cfg>
 __device__ __forceinline__ void load_operand(uint8_t* dst, const CUtensorMap* map, uint64_t* bar, int mn0, int k0,
                                              int rows, int mn_major) {
   if (mn_major) {
     for (int q = 0; q < rows / Cfg::AE; ++q)
-      tma_load_2d(dst + q * Cfg::ATOM_BYTES, map, bar, mn0 + q * Cfg::AE, k0);
+      tma2d<Cfg>(dst + q * Cfg::ATOM_BYTES, map, bar, mn0 + q * Cfg::AE, k0);
   } else {
-    tma_load_2d(dst, map, bar, k0, mn0);
+    tma2d<Cfg>(dst, map, bar, k0, mn0);
   }
 }
 
@@ -508,6 +631,17 @@ __device__ __forceinline__ uint64_t operand_desc(uint32_t base, int k, int mn_ma
 }
 
 // ---------------------------------------------------------------- the kernel
+
+// Debug timeline of the thin chain GEMM (prism_debug_trace): per pass and CTA,
+// TRACE_W globaltimer stamps; null (the default) disables every stamp.
+__device__ unsigned long long* g_gemm_trace = nullptr;
+constexpr int TRACE_W = 80;
+// Main-GEMM k-block timeline (prism_debug_trace_gemm): for launches whose first problem has
+// epilogue mode g_trace_mode, each CTA's first tile records [0,64) producer issue (after
+// its empty wait), [64,128) MMA full arrival, [128,192) MMA issue done, per k-block.
+__device__ unsigned long long* g_gemm_trace2 = nullptr;
+__device__ int g_trace_mode = -1;
+constexpr int TRACE2_W = 240;   // + [192 + 4 j ..]: tile j mma start / end, epilogue start / end
 
 template <class Cfg>
 __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __grid_constant__ GemmLaunch L) {
@@ -521,16 +655,31 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
   uint64_t* empty = bars + Cfg::STAGES;        // [STAGES]
   uint64_t* tfull = bars + 2 * Cfg::STAGES;    // [2]
   uint64_t* tempty = tfull + 2;                // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* red_full = tempty + 2;             // chain split-K: partials landed in the leader
+  uint64_t* red_empty = red_full + 1;          // chain split-K: leader consumed this CTA's partial
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(red_empty + 1);
   float* red = reinterpret_cast<float*>(tmem_slot + 4);   // [8] epilogue reduction scratch
-  int* sflag = reinterpret_cast<int*>(red + 8);           // split-K "last CTA" flag
   double* dred = reinterpret_cast<double*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES + 256);   // [8][6]
   float* tbuf = reinterpret_cast<float*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES + 1024);    // [8][32*33]
+  float* redbuf = tbuf;                                                                    // [3][32][128] (chain)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t rank = Cfg::CTA2 ? cluster_ctarank() : 0u;   // CTA within the pair
+  const bool leader = rank == 0;
+  const int cid = Cfg::CTA2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;   // tile-loop index / stride
+  const int ncl = Cfg::CTA2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  // chain split-K: the cluster's CTAs take the K slices 0..ksplit-1 of one row tile
+  // (tiles grouped by row tile, grid a multiple of ksplit, so slice == cluster rank)
+  const int ksplit = (Cfg::BN == 32 && L.ksplit > 1) ? L.ksplit : 1;
+  const uint32_t krank = ksplit > 1 ? cluster_ctarank() : 0u;
   // device-side loop control (CUDA-graph WHILE body): uniform early exit / parity select
   const GemmProblem* __restrict__ probs = L.probs;
+  unsigned long long* trace = nullptr;
+  if (Cfg::BN == 32 && g_gemm_trace) trace = g_gemm_trace + ((size_t)L.probs[0].pass * 1024 + blockIdx.x) * TRACE_W;
+  if (trace && threadIdx.x == 0) trace[0] = globaltimer_ns();
+  unsigned long long* trace2 = nullptr;
+  if (Cfg::BN != 32 && g_gemm_trace2 && L.probs[0].mode == g_trace_mode) trace2 = g_gemm_trace2 + (size_t)blockIdx.x * TRACE2_W;
   if (L.iter) {
     const int k = *L.iter;
     if (k < L.iter_lo || k >= L.iter_hi) return;
@@ -544,54 +693,72 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 32 * Cfg::EPI_WARPS);
+      mbar_init(&tempty[a], Cfg::CG * Cfg::EPI_WARPS);   // one arrival per epilogue warp (of both CTAs)
     }
+    mbar_init(red_full, 1);                      // leader's expect_tx; the slices complete_tx
+    mbar_init(red_empty, Cfg::EPI_WARPS);        // one arrival per leader epilogue warp
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, Cfg::TMEM_ALLOC);
+  if (warp == 1) tmem_alloc<Cfg::CG>(tmem_slot, Cfg::TMEM_ALLOC);
   tc_fence_before();
-  __syncthreads();
+  if (Cfg::CTA2 || ksplit > 1) cluster_sync_all();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (trace && threadIdx.x == 0) trace[1] = globaltimer_ns();
 
   if (warp == 0) {
     // ===================== TMA producer =====================
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < L.ntiles; t += gridDim.x) {
+      for (int t = cid; t < L.ntiles; t += ncl) {
         const uint32_t code = L.tiles[t];
         const GemmProblem& P = probs[code >> 20];
         if (L.done && L.done[P.matrix * L.done_stride]) continue;
         const int tm = (code >> 10) & 1023;
         int tn = code & 1023, kb_lo, kb_hi;
         tile_krange<Cfg>(P, tn, kb_lo, kb_hi);
+        // warm the TMA descriptor cache with this tile's maps (they live in global memory)
+        tma_prefetch(P.tmA);
+        tma_prefetch(P.tmB);
+        if constexpr (Cfg::SPLIT) {
+          tma_prefetch(P.tmA_lo);
+          if constexpr (Cfg::LOB) tma_prefetch(P.tmB_lo);
+        }
+        const int am0 = tm * Cfg::TILE_M + (int)rank * Cfg::BM;      // this CTA's rows of A
+        const int bn0 = tn * Cfg::BN + (int)rank * Cfg::B_ROWS;      // this CTA's half of B
         for (int kb = kb_lo; kb < kb_hi; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sA = stage_base + stage * Cfg::STAGE_BYTES;
           uint8_t* sB = sA + Cfg::A_BYTES;
-          mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
-          load_operand<Cfg>(sA, P.tmA, &full[stage], tm * Cfg::BM, kb * Cfg::BK, Cfg::BM, P.a_mn);
-          load_operand<Cfg>(sB, P.tmB, &full[stage], tn * Cfg::BN, kb * Cfg::BK, Cfg::BN, P.b_mn);
+          // the leader's full barrier counts the bytes of both CTAs of the pair
+          if (leader) mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES * Cfg::CG);
+          load_operand<Cfg>(sA, P.tmA, &full[stage], am0, kb * Cfg::BK, Cfg::BM, P.a_mn);
+          load_operand<Cfg>(sB, P.tmB, &full[stage], bn0, kb * Cfg::BK, Cfg::B_ROWS, P.b_mn);
           if constexpr (Cfg::SPLIT) {
             uint8_t* sA2 = sB + Cfg::B_BYTES;
             uint8_t* sB2 = sA2 + Cfg::A_BYTES;
-            load_operand<Cfg>(sA2, P.tmA_lo, &full[stage], tm * Cfg::BM, kb * Cfg::BK, Cfg::BM, P.a_mn);
+            load_operand<Cfg>(sA2, P.tmA_lo, &full[stage], am0, kb * Cfg::BK, Cfg::BM, P.a_mn);
             if constexpr (Cfg::LOB)
-              load_operand<Cfg>(sB2, P.tmB_lo, &full[stage], tn * Cfg::BN, kb * Cfg::BK, Cfg::BN, P.b_mn);
+              load_operand<Cfg>(sB2, P.tmB_lo, &full[stage], bn0, kb * Cfg::BK, Cfg::B_ROWS, P.b_mn);
           }
+          if (trace && kb == kb_lo) trace[2] = globaltimer_ns();
+          if (trace2 && t == cid && kb < 64) trace2[kb] = globaltimer_ns();
           if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
         }
       }
+      if (trace) trace[3] = globaltimer_ns();
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer =====================
-    if (lane == 0) {
+    // ===================== MMA issuer (leader CTA of the pair) =====================
+    if (lane == 0 && leader) {
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = blockIdx.x; t < L.ntiles; t += gridDim.x) {
+      int tcount = 0;
+      for (int t = cid; t < L.ntiles; t += ncl) {
         const uint32_t code = L.tiles[t];
         const GemmProblem& P = probs[code >> 20];
         if (L.done && L.done[P.matrix * L.done_stride]) continue;
@@ -606,6 +773,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
           const uint32_t dt = tmem_base + acc * Cfg::BN;
           for (int kb = kb0; kb < kb1; ++kb) {
             mbar_wait(&full[stage], phase);
+            if (trace && kb - kb_lo < 64) trace[8 + kb - kb_lo] = globaltimer_ns();
+            if (trace2 && t == cid && kb < 64) trace2[64 + kb] = globaltimer_ns();
+            if (trace2 && kb == kb_lo && tcount < 8) trace2[192 + 4 * tcount] = globaltimer_ns();
             tc_fence_after();
             const uint32_t aA = smem_u32(stage_base + stage * Cfg::STAGE_BYTES);
             const uint32_t aB = aA + Cfg::A_BYTES;
@@ -614,22 +784,26 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
             for (int k = 0; k < Cfg::BK / Cfg::UK; ++k) {
               const uint64_t da = operand_desc<Cfg>(aA, k, P.a_mn);
               const uint64_t db = operand_desc<Cfg>(aB, k, P.b_mn);
-              umma<Cfg::KIND>(dt, da, db, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+              umma<Cfg::KIND, Cfg::CG>(dt, da, db, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
               if constexpr (Cfg::SPLIT) {
                 const uint32_t aA2 = aB + Cfg::B_BYTES;
                 const uint32_t aB2 = aA2 + Cfg::A_BYTES;
                 const uint64_t da2 = operand_desc<Cfg>(aA2, k, P.a_mn);
-                if constexpr (Cfg::LOB) umma<Cfg::KIND>(dt, da, operand_desc<Cfg>(aB2, k, P.b_mn), idesc, 1u);   // A_hi · B_lo
-                umma<Cfg::KIND>(dt, da2, db, idesc, 1u);                                                          // A_lo · B_hi
+                if constexpr (Cfg::LOB) umma<Cfg::KIND, Cfg::CG>(dt, da, operand_desc<Cfg>(aB2, k, P.b_mn), idesc, 1u);   // A_hi · B_lo
+                umma<Cfg::KIND, Cfg::CG>(dt, da2, db, idesc, 1u);                                                          // A_lo · B_hi
               }
             }
-            umma_commit(&empty[stage]);     // smem slot free once these MMAs retire
+            umma_commit<Cfg::CG>(&empty[stage]);     // smem slots (of both CTAs) free once these MMAs retire
+            if (trace2 && t == cid && kb < 64) trace2[128 + kb] = globaltimer_ns();
             if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
           }
-          umma_commit(&tfull[acc]);          // accumulator (chunk) ready for the epilogue
+          umma_commit<Cfg::CG>(&tfull[acc]);          // accumulator (chunk) ready for both epilogues
           if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
+        if (trace2 && tcount < 8) trace2[192 + 4 * tcount + 1] = globaltimer_ns();
+        ++tcount;
       }
+      if (trace) trace[6] = globaltimer_ns();
     }
   } else {
     // ===================== epilogue (warps 2..9) =====================
@@ -642,7 +816,18 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
     float* tb = tbuf + e * 32 * 33;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < L.ntiles; t += gridDim.x) {
+    uint32_t red_phase = 0;
+    int etcount = 0;
+    // accumulator release: one arrival per epilogue warp on the leader's tempty barrier
+    auto release_acc = [&](uint64_t* bar) {
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (Cfg::CTA2 && !leader) mbar_arrive_cluster(bar, 0u);
+        else mbar_arrive(bar);
+      }
+    };
+    for (int t = cid; t < L.ntiles; t += ncl) {
       const uint32_t code = L.tiles[t];
       const GemmProblem& P = probs[code >> 20];
       if (L.done && L.done[P.matrix * L.done_stride]) continue;
@@ -652,7 +837,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
       tile_krange<Cfg>(P, tn, kb_lo, kb_hi);
       const int mode = P.mode;
       const bool sym = P.sym != 0;
-      const int i0 = tm * Cfg::BM + q * 32;
+      const int i0 = tm * Cfg::TILE_M + (int)rank * Cfg::BM + q * 32;
       const int i = i0 + lane;                     // output row of this thread
       float coefA = 1.f, coefC = 1.f;
       if (mode == EPI_POLY) { coefA = static_cast<float>(*P.alpha); coefC = P.c1; }
@@ -661,62 +846,84 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
       float sumsq = 0.f;
 
       if constexpr (Cfg::BN == 32) {
-        // thin chain GEMM: one 32-column chunk, owned by the h == 0 warps
+        // thin chain GEMM: one 32-column chunk, read by both warps of each lane quarter
         float d[32];
 #pragma unroll
         for (int u = 0; u < 32; ++u) d[u] = 0.f;
         for (int kb0 = kb_lo; kb0 < kb_hi; kb0 += Cfg::PROMO_KB) {
           mbar_wait(&tfull[acc], acc_phase);
+          if (trace && et == 0) trace[4] = globaltimer_ns();
           tc_fence_after();
-          if (h == 0) {
-            uint32_t r[32];
-            tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * Cfg::BN, r);
-            tmem_ld_wait();
+          uint32_t r[32];
+          tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * Cfg::BN, r);
+          tmem_ld_wait();
 #pragma unroll
-            for (int u = 0; u < 32; ++u) d[u] += __uint_as_float(r[u]);
-          }
-          tc_fence_before();
-          mbar_arrive(&tempty[acc]);
+          for (int u = 0; u < 32; ++u) d[u] += __uint_as_float(r[u]);
+          release_acc(&tempty[acc]);
           if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
-        if (P.ksplit > 1) {
-          // split-K: publish this slice, the last-arriving CTA of the row tile sums the
-          // slices in fixed order (deterministic) and runs the chain epilogue
-          if (h == 0 && i < P.M) {
-            float4* dst = reinterpret_cast<float4*>(P.kpart + ((long long)ks * P.M + i) * 32);
+        if (ksplit > 1) {
+          // split-K over the cluster: each non-leader st.async's its fp32 128 x 32 partial
+          // into slot (rank-1) of the leader's smem (row-major, 16-B chunks XOR-swizzled by
+          // row: conflict-free), completing bytes on the leader's red_full; the leader sums
+          // the slices in fixed order (deterministic).  red_empty hands the slot back.
+          const int row = q * 32 + lane;
+          if (krank != 0) {
+            mbar_wait(red_empty, red_phase ^ 1);
+            float* slot = redbuf + (krank - 1) * 32 * 128 + row * 32;
 #pragma unroll
-            for (int u = 0; u < 8; ++u) dst[u] = make_float4(d[4 * u], d[4 * u + 1], d[4 * u + 2], d[4 * u + 3]);
+            for (int j = 0; j < 4; ++j) {
+              const int jj = h * 4 + j;   // this warp's half of the 8 chunks
+              float4 v;
+              if (h == 0) v = make_float4(d[4 * j], d[4 * j + 1], d[4 * j + 2], d[4 * j + 3]);
+              else v = make_float4(d[16 + 4 * j], d[17 + 4 * j], d[18 + 4 * j], d[19 + 4 * j]);
+              st_async_v4(slot + ((jj ^ (row & 7)) << 2), red_full, 0u, v);
+            }
+            red_phase ^= 1;
+            if (trace && et == 0) trace[74] = globaltimer_ns();
+            continue;
           }
-          __threadfence();
-          named_bar_sync(1, 32 * Cfg::EPI_WARPS);
-          if (et == 0) sflag[0] = (atomicAdd(&P.kcnt[tm], 1) == P.ksplit - 1) ? 1 : 0;
-          named_bar_sync(1, 32 * Cfg::EPI_WARPS);
-          if (!sflag[0]) continue;
-          __threadfence();
-          if (h == 0 && i < P.M) {
+          if (et == 0) mbar_arrive_expect_tx(red_full, (uint32_t)(ksplit - 1) * 32 * 128 * 4);
+          mbar_wait(red_full, red_phase);
+          if (trace && et == 0) trace[75] = globaltimer_ns();
+          for (int x = 0; x < ksplit - 1; ++x) {
+            const float* slot = redbuf + x * 32 * 128 + row * 32;
 #pragma unroll
-            for (int u = 0; u < 32; ++u) d[u] = 0.f;
-            for (int x = 0; x < P.ksplit; ++x) {
-              const float4* src = reinterpret_cast<const float4*>(P.kpart + ((long long)x * P.M + i) * 32);
-#pragma unroll
-              for (int u = 0; u < 8; ++u) {
-                const float4 v = __ldcg(src + u);
-                d[4 * u] += v.x; d[4 * u + 1] += v.y; d[4 * u + 2] += v.z; d[4 * u + 3] += v.w;
-              }
+            for (int j = 0; j < 8; ++j) {
+              const float4 v = *reinterpret_cast<const float4*>(slot + ((j ^ (row & 7)) << 2));
+              d[4 * j] += v.x; d[4 * j + 1] += v.y; d[4 * j + 2] += v.z; d[4 * j + 3] += v.w;
             }
           }
-          if (et == 0) P.kcnt[tm] = 0;
+          red_phase ^= 1;
         }
-        epi_chain<Cfg>(P, i, tm, d, dred, e, lane, et, h == 0);
+        epi_chain<Cfg>(P, i, tm, d, dred, e, lane, et, h);
+        if (ksplit > 1 && krank == 0) {
+          // slots consumed (their values were summed above): hand them back to the slices
+          __syncwarp();
+          if (lane == 0)
+            for (int x = 1; x < ksplit; ++x) mbar_arrive_release_cluster(red_empty, (uint32_t)x);
+        }
+        if (trace && et == 0) trace[5] = globaltimer_ns();
       } else if constexpr (Cfg::KIND == 0) {
         // bf16: one TMEM accumulator per tile; this warp consumes its 32-column chunks
         // while the raw C row segment of the next chunk is in flight
-        uint4 craw[4];
+        // C blocks: coalesced when the warp's 32 x 32 block is in bounds, else per-row
+        const bool rows_full = i0 + 32 <= P.M;
+        auto c_issue = [&](int j, uint4 (&g)[4]) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) craw[u] = make_uint4(0, 0, 0, 0);
-        if (needC && i < P.M && tn * Cfg::BN + c_begin * 32 < P.N)
-          load_raw_bf16(P.C, P.ldc, i, tn * Cfg::BN + c_begin * 32, P.N, craw);
+          for (int u = 0; u < 4; ++u) g[u] = make_uint4(0, 0, 0, 0);
+          if (!needC || j >= P.N) return;
+          if (rows_full && j + 32 <= P.N) warp_load_bf16_block(P.C, P.ldc, i0, j, g, lane);
+          else if (i < P.M) load_raw_bf16(P.C, P.ldc, i, j, P.N, g);
+        };
+        auto c_finish = [&](int j, const uint4 (&g)[4], float (&c)[32]) {
+          if (needC && rows_full && j + 32 <= P.N) warp_rows_from_block(g, reinterpret_cast<uint8_t*>(tb), lane, c);
+          else decode_bf16(g, c);
+        };
+        uint4 craw[4];
+        c_issue(tn * Cfg::BN + c_begin * 32, craw);
         mbar_wait(&tfull[acc], acc_phase);
+        if (trace2 && et == 0 && leader && etcount < 8) trace2[192 + 4 * etcount + 2] = globaltimer_ns();
         tc_fence_after();
         const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * Cfg::BN;
 #pragma unroll 1
@@ -725,21 +932,24 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
           uint32_t r[32];
           tmem_ld32(tbase + ch * 32, r);
           uint4 cnext[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) cnext[u] = make_uint4(0, 0, 0, 0);
           const int jn = tn * Cfg::BN + (ch + 1) * 32;
-          if (needC && ch + 1 < c_end && i < P.M && jn < P.N) load_raw_bf16(P.C, P.ldc, i, jn, P.N, cnext);
+          if (ch + 1 < c_end) c_issue(jn, cnext);
+          else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) cnext[u] = make_uint4(0, 0, 0, 0);
+          }
           tmem_ld_wait();
+          if (trace2 && et == 0 && leader && etcount == 0 && ch < 8) trace2[224 + 2 * ch] = globaltimer_ns();
           float d[32], c[32];
 #pragma unroll
           for (int u = 0; u < 32; ++u) d[u] = __uint_as_float(r[u]);
-          decode_bf16(craw, c);
+          c_finish(tn * Cfg::BN + ch * 32, craw, c);
           epi_segment<Cfg>(P, mode, sym, i0, lane, tn * Cfg::BN + ch * 32, coefA, coefC, d, c, tb, sumsq);
+          if (trace2 && et == 0 && leader && etcount == 0 && ch < 8) trace2[225 + 2 * ch] = globaltimer_ns();
 #pragma unroll
           for (int u = 0; u < 4; ++u) craw[u] = cnext[u];
         }
-        tc_fence_before();
-        mbar_arrive(&tempty[acc]);
+        release_acc(&tempty[acc]);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       } else {
         // tf32: sum the K-chunk partials from TMEM in fp32 registers (round-to-nearest)
@@ -761,8 +971,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
 #pragma unroll
             for (int u = 0; u < 32; ++u) d[x][u] += __uint_as_float(r[u]);
           }
-          tc_fence_before();
-          mbar_arrive(&tempty[acc]);
+          release_acc(&tempty[acc]);
           if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
 #pragma unroll
@@ -782,22 +991,25 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
         for (int o = 16; o > 0; o >>= 1) sumsq += __shfl_xor_sync(0xffffffffu, sumsq, o);
         if (lane == 0) red[e] = sumsq;
         named_bar_sync(1, 32 * Cfg::EPI_WARPS);
-        if (et == 0) {
+        if (et == 0 && (tm * Cfg::CG + (int)rank) * Cfg::BM < P.M) {
           float tsum = 0.f;
 #pragma unroll
           for (int x = 0; x < Cfg::EPI_WARPS; ++x) tsum += red[x];
-          P.norm_part[tm * P.tiles_n + tn] = tsum;
+          P.norm_part[(tm * Cfg::CG + (int)rank) * P.tiles_n + tn] = tsum;
         }
         named_bar_sync(1, 32 * Cfg::EPI_WARPS);
       }
+      if (trace2 && et == 0 && leader && etcount < 8) trace2[192 + 4 * etcount + 3] = globaltimer_ns();
+      ++etcount;
     }
   }
 
   tc_fence_before();
-  __syncthreads();
+  if (Cfg::CTA2 || ksplit > 1) cluster_sync_all();   // no CTA leaves while a peer may still touch its smem
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, Cfg::TMEM_ALLOC);
+    tmem_dealloc<Cfg::CG>(tmem_base, Cfg::TMEM_ALLOC);
   }
 }
 

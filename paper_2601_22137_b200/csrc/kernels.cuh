@@ -44,8 +44,6 @@ struct MatDesc {
   void* W[2];          // chain B operands [4p x ldS] (compute dtype), hi rows then lo rows
   float* keep;         // [4][s][p] kept chain columns (fp32)
   double* chain_part;  // [tiles_m][6] per-tile <Va,Vb>
-  float* kpart;        // [ksplit][s][32] chain split-K partials
-  int* kcnt;           // [tiles_m] chain split-K arrival counters
   long long ldS;
   int chain_tiles;
   int pad2_;
@@ -305,9 +303,6 @@ __global__ void __launch_bounds__(256) k_normalize(SolveParams P) {
       for (int e = 0; e < V::VE; ++e) x.v[e] = (col + e == r) ? 1.f : 0.f;
       x.store(D.Y[0], D.Y_lo[0], (long long)r * D.ldx + col, nv, nv == V::VE, 1.f, PREC == 1);
     }
-  }
-  if (lt == 0) {
-    for (int x = threadIdx.x; x < D.chain_tiles; x += 256) D.kcnt[x] = 0;
   }
   if (lt == 0 && threadIdx.x == 0) {
     if (b == 0) *P.iter = 0;

@@ -72,7 +72,7 @@ bool encode_map(CUtensorMap* out, const MapSpec& s) {
   cuuint64_t strides[1] = {(cuuint64_t)(s.ld * s.esz)};
   cuuint32_t box[2];
   if (s.kind == OP_A) { box[0] = s.BK; box[1] = 128; }
-  else if (s.kind == OP_BK) { box[0] = s.BK; box[1] = s.BN; }
+  else if (s.kind == OP_BK) { box[0] = s.BK; box[1] = s.BN; }   // BN = rows of B per CTA
   else { box[0] = 128 / s.esz; box[1] = s.BK; }
   cuuint32_t es[2] = {1, 1};
   CUresult r = fn(out, s.esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
@@ -106,9 +106,43 @@ cudaError_t launch_gemm_cfg(const GemmLaunch& L, cudaStream_t st) {
     attr = true;
   }
   if (L.ntiles <= 0) return cudaSuccess;
-  const int grid = std::min(L.ntiles, num_sms());
-  prism_gemm_kernel<Cfg><<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(L);
-  return cudaGetLastError();
+  if constexpr (Cfg::CTA2) {
+    // clusters of 2 CTAs (one CTA pair per tile), persistent over the tile list
+    const int pairs = std::min(L.ntiles, num_sms() / 2);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * pairs);
+    cfg.blockDim = dim3(Cfg::THREADS);
+    cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, prism_gemm_kernel<Cfg>, L);
+  } else if (L.ksplit > 1) {
+    // chain split-K: clusters of ksplit CTAs, one row tile per cluster per round
+    const int grid = std::min(L.ntiles, num_sms() / L.ksplit * L.ksplit);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(Cfg::THREADS);
+    cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = L.ksplit;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, prism_gemm_kernel<Cfg>, L);
+  } else {
+    const int grid = std::min(L.ntiles, num_sms());
+    prism_gemm_kernel<Cfg><<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(L);
+    return cudaGetLastError();
+  }
 }
 
 cudaError_t launch_chain(int precision, const GemmLaunch& L, cudaStream_t st) {
@@ -117,7 +151,24 @@ cudaError_t launch_chain(int precision, const GemmLaunch& L, cudaStream_t st) {
   return launch_gemm_cfg<GemmCfg<1, false, 32>>(L, st);
 }
 
+// Main GEMM variant: CTA pairs (cta_group::2, 256 x BN tiles) by default; PRISM_GEMM_1CTA=1
+// selects single-CTA 128 x BN tiles (A/B comparison knob for profiling).
+static bool use_1cta() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PRISM_GEMM_1CTA");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+int tile_m_main() { return use_1cta() ? 128 : 256; }
+
 cudaError_t launch_gemm(int precision, const GemmLaunch& L, cudaStream_t st) {
+  if (use_1cta()) {
+    if (precision == PRISM_BF16) return launch_gemm_cfg<GemmCfg<0, false, 0, false>>(L, st);
+    if (precision == PRISM_FP32) return launch_gemm_cfg<GemmCfg<1, true, 0, false>>(L, st);
+    return launch_gemm_cfg<GemmCfg<1, false, 0, false>>(L, st);
+  }
   if (precision == PRISM_BF16) return launch_gemm_cfg<GemmCfg<0, false>>(L, st);
   if (precision == PRISM_FP32) return launch_gemm_cfg<GemmCfg<1, true>>(L, st);
   return launch_gemm_cfg<GemmCfg<1, false>>(L, st);
@@ -160,6 +211,7 @@ struct Plan {
   SolveParams params{};
   LaunchDesc gram[2], square, apply[2], chain[5], gram32[2];
   int n_chain = 0;
+  int chain_ksplit = 1;   // cluster size of the chain launches (split-K)
   bool has_square = false;
   int max_s = 0, max_rows = 0, max_cols = 0, max_m = 0, max_n = 0;
 };
@@ -200,14 +252,23 @@ struct Bump {
   }
 };
 
+// Main GEMMs run on CTA pairs: tiles of TILE_M = 256 rows x BN columns.
+int tile_m_main();
+
 void add_tiles(LaunchDesc& L, int prob, int M, int N, int BN, bool sym) {
-  const int tm_n = (M + 127) / 128, tn_n = (N + BN - 1) / BN;
+  const int kTileM = tile_m_main();
+  const int tm_n = (M + kTileM - 1) / kTileM, tn_n = (N + BN - 1) / BN;
   for (int tm = 0; tm < tm_n; ++tm)
     for (int tn = 0; tn < tn_n; ++tn) {
-      if (sym && tn * BN + BN - 1 < tm * 128) continue;
+      if (sym && tn * BN + BN - 1 < tm * kTileM) continue;
       L.tiles.push_back(((uint32_t)prob << 20) | ((uint32_t)tm << 10) | (uint32_t)tn);
     }
 }
+
+// Chain split-K factor of one matrix: a function of its size s alone (never of the
+// batch), so a matrix's bits do not depend on what it is batched with (or on the
+// rank it lands on).  Each slice keeps >= 8 k-blocks.
+int chain_ks(int s) { return std::max(1, std::min(4, s / 512)); }
 
 void sort_tiles_by_cost(LaunchDesc& L) {
   std::stable_sort(L.tiles.begin(), L.tiles.end(), [&](uint32_t a, uint32_t b) {
@@ -239,14 +300,11 @@ prism_status build_plan(const Request& r, Plan& P) {
   std::vector<MatDesc> mats(B);
   std::vector<MapSpec> maps;
   auto add_map = [&](const void* ptr, int rows, int cols, long long ld, OpKind k) -> int {
-    maps.push_back(MapSpec{ptr, rows, cols, ld, esz, k, BN, BK});
+    maps.push_back(MapSpec{ptr, rows, cols, ld, esz, k, tile_m_main() == 256 ? BN / 2 : BN, BK});   // CTA pairs: half of B per CTA
     return (int)maps.size();   // 1-based index
   };
 
   P.max_s = P.max_rows = P.max_cols = P.max_m = P.max_n = 0;
-  // chain split-K (deterministic last-CTA reduction, gemm.cuh) is implemented but off:
-  // measured on B200 it lengthened the 4096^2 passes (40 us vs 29 us per pass)
-  const int ksplit = 1;
   for (int i = 0; i < B; ++i) {
     MatDesc& D = mats[i];
     std::memset(&D, 0, sizeof(D));
@@ -294,9 +352,6 @@ prism_status build_plan(const Request& r, Plan& P) {
     D.keep = reinterpret_cast<float*>(bump.take(sizeof(float) * 4 * (size_t)s * p));
     D.chain_tiles = D.tiles_m;
     D.chain_part = reinterpret_cast<double*>(bump.take(sizeof(double) * 6 * D.tiles_m));
-    const int ks_i = std::max(1, std::min(ksplit, s / 64));
-    D.kpart = ks_i > 1 ? reinterpret_cast<float*>(bump.take(sizeof(float) * (size_t)ks_i * s * 32)) : nullptr;
-    D.kcnt = reinterpret_cast<int*>(bump.take(sizeof(int) * D.tiles_m));
     P.max_s = std::max(P.max_s, s);
     P.max_rows = std::max(P.max_rows, s);
     P.max_cols = std::max(P.max_cols, L);
@@ -431,9 +486,7 @@ prism_status build_plan(const Request& r, Plan& P) {
         c.p.ldr = ldr;
         c.p.p = p;
         c.p.tiles_n = 1;
-        c.p.ksplit = ks_i;
-        c.p.kpart = D.kpart;
-        c.p.kcnt = D.kcnt;
+        c.p.ksplit = chain_ks(s);
         c.mapA = add_map(D.R, s, s, ldr, OP_A);
         if (split) c.mapA_lo = add_map(D.R_lo, s, s, ldr, OP_A);
         maps.push_back(MapSpec{D.W[j % 2], N, s, D.ldS, esz, OP_BK, 32, BK});
@@ -458,13 +511,22 @@ prism_status build_plan(const Request& r, Plan& P) {
     if (r.rowblock) finish(P.gram32[t], false);
   }
   if (P.has_square) finish(P.square, !polar_k);
+  // chain split-K (DSMEM cluster reduction, gemm.cuh): the chain streams R through only
+  // s/128 row tiles per matrix and each SM's TMA pulls ~35 B/cycle, so large matrices
+  // split every row tile over a cluster of CTAs (measured B200, s = 4096: 19.5 us
+  // mainloop with 32 CTAs, 4.7 us with 128)
+  // The launch's cluster size is the largest factor; a matrix with a smaller one leaves
+  // its trailing slices empty (exact zeros in the leader's fixed-order sum).
+  P.chain_ksplit = 1;
+  if (P.n_chain)
+    for (const HostProblem& hp : P.chain[0].probs) P.chain_ksplit = std::max(P.chain_ksplit, hp.p.ksplit);
   for (int j = 0; j < P.n_chain; ++j) {
     LaunchDesc& L = P.chain[j];
     L.tiles.clear();
     for (int q = 0; q < (int)L.probs.size(); ++q) {
       const GemmProblem& gq = L.probs[q].p;
       for (int tm = 0; tm < (gq.M + 127) / 128; ++tm)
-        for (int ks = 0; ks < gq.ksplit; ++ks)
+        for (int ks = 0; ks < P.chain_ksplit; ++ks)
           L.tiles.push_back(((uint32_t)q << 20) | ((uint32_t)tm << 10) | (uint32_t)ks);
     }
     sort_tiles_by_cost(L);
@@ -568,6 +630,7 @@ prism_status build_plan(const Request& r, Plan& P) {
 
 GemmLaunch make_launch(const Plan& P, const LaunchDesc& L, const LaunchDesc* odd, char* ws, int lo, int hi) {
   GemmLaunch g{};
+  g.ksplit = (!L.probs.empty() && L.probs[0].p.mode == EPI_CHAIN) ? P.chain_ksplit : 1;
   char* meta = ws + P.meta_off;
   g.probs = reinterpret_cast<const GemmProblem*>(meta + L.probs_off);
   g.probs_odd = odd ? reinterpret_cast<const GemmProblem*>(meta + odd->probs_off) : nullptr;
@@ -1188,11 +1251,11 @@ prism_status prism_debug_gemm(prism_handle h, int precision, int b_mn, int mode,
   const OpKind bk = b_mn ? OP_MN : OP_BK;
   const int brows = b_mn ? K : N, bcols = b_mn ? N : K;
   if (!encode_map(&hm[0], MapSpec{A, M, K, lda, esz, OP_A, BN, BK}) ||
-      !encode_map(&hm[1], MapSpec{B, brows, bcols, ldb, esz, bk, BN, BK}))
+      !encode_map(&hm[1], MapSpec{B, brows, bcols, ldb, esz, bk, tile_m_main() == 256 ? BN / 2 : BN, BK}))
     return fail(PRISM_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   if (split) {
     if (!encode_map(&hm[2], MapSpec{A_lo, M, K, lda, esz, OP_A, BN, BK}) ||
-        !encode_map(&hm[3], MapSpec{B_lo, brows, bcols, ldb, esz, bk, BN, BK}))
+        !encode_map(&hm[3], MapSpec{B_lo, brows, bcols, ldb, esz, bk, tile_m_main() == 256 ? BN / 2 : BN, BK}))
       return fail(PRISM_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   }
   GemmProblem* gp = reinterpret_cast<GemmProblem*>(hb + 4 * sizeof(CUtensorMap));
@@ -1222,6 +1285,15 @@ prism_status prism_debug_gemm(prism_handle h, int precision, int b_mn, int mode,
   PRISM_CK(launch_gemm(precision, g, static_cast<cudaStream_t>(stream)));
   PRISM_CK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
   return PRISM_OK;
+}
+
+prism_status prism_debug_trace(unsigned long long* buf_dev) {
+  return cudaMemcpyToSymbol(g_gemm_trace, &buf_dev, sizeof(buf_dev)) == cudaSuccess ? PRISM_OK : PRISM_ERR_CUDA;
+}
+
+prism_status prism_debug_trace_gemm(unsigned long long* buf_dev, int mode) {
+  if (cudaMemcpyToSymbol(g_gemm_trace2, &buf_dev, sizeof(buf_dev)) != cudaSuccess) return PRISM_ERR_CUDA;
+  return cudaMemcpyToSymbol(g_trace_mode, &mode, sizeof(mode)) == cudaSuccess ? PRISM_OK : PRISM_ERR_CUDA;
 }
 
 prism_status prism_debug_sketch(uint64_t seed, int64_t b, int k, int p, int s, float* S_dev, void* stream) {
