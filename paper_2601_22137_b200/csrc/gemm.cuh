@@ -28,6 +28,7 @@
 
 namespace prism {
 
+__device__ int g_dbg_flags = 0;   // timing experiments only (prism_debug_trace_gemm): 1 skip mirror stores, 2 skip direct stores
 enum EpiMode : int { EPI_RESID = 0, EPI_POLY = 1, EPI_APPLY = 2, EPI_STORE = 3, EPI_CHAIN = 4, EPI_GRAM32 = 5 };
 
 // Sketch-chain pass codes (EPI_CHAIN).  The thin GEMM computes
@@ -388,54 +389,65 @@ __device__ __forceinline__ void epi_segment(const GemmProblem& P, int mode, bool
     return;
   }
   // symmetric: upper triangle (j >= i) written directly, (j > i) mirrored to (j, i)
-  const bool diag = j0 < i0 + 32;                // 32-aligned blocks: the diagonal block
-  if (Cfg::KIND == 0 && !diag && full_blk) {
-    warp_store_bf16_block(P.out, P.ldo, i0, j0, v, stg, lane);
-    if (mode == EPI_RESID) {
-#pragma unroll
-      for (int u = 0; u < 32; ++u) sumsq = fmaf(2.f * v[u], v[u], sumsq);
-    }
-  } else if (row_ok) {
-    if (!diag && full_n) {
-      store_row32<Cfg::KIND, Cfg::SPLIT>(P.out, P.out_lo, off, v);
-      if (mode == EPI_RESID) {
-#pragma unroll
-        for (int u = 0; u < 32; ++u) sumsq = fmaf(2.f * v[u], v[u], sumsq);
-      }
-    } else {
-#pragma unroll
-      for (int u = 0; u < 32; ++u) {
-        const int j = j0 + u;
-        if (j >= i && j < P.N) {
-          store_elem<Cfg::KIND, Cfg::SPLIT>(P.out, P.out_lo, off + u, v[u]);
-          if (mode == EPI_RESID) sumsq = fmaf(j > i ? 2.f * v[u] : v[u], v[u], sumsq);
-        }
-      }
-    }
-  }
-  // mirror through shared memory: lane l takes column j = j0 + l, rows i0 .. i0+31
+  const bool diag = j0 < i0 + 32;                // 32-aligned blocks: the diagonal block (j0 == i0)
+  const int dbgf = g_dbg_flags;
+  // transpose through shared memory: lane l obtains column j0 + l, rows i0 .. i0+31
 #pragma unroll
   for (int u = 0; u < 32; ++u) tb[lane * 33 + u] = v[u];
   __syncwarp();
-  const int j = j0 + lane;
-  if (j < P.N) {
-    float w[32];
+  float w[32];
 #pragma unroll
-    for (int u = 0; u < 32; ++u) w[u] = tb[u * 33 + lane];
+  for (int u = 0; u < 32; ++u) w[u] = tb[u * 33 + lane];
+  __syncwarp();
+  if (diag) {
+    // whole symmetric block at once: own values on and above the diagonal, transposed
+    // ones below (exact symmetry), written as full rows — no partial-sector stores
+#pragma unroll
+    for (int u = 0; u < 32; ++u) {
+      if (mode == EPI_RESID && u >= lane && j0 + u < P.N && row_ok) sumsq = fmaf(u > lane ? 2.f * v[u] : v[u], v[u], sumsq);
+      v[u] = u >= lane ? v[u] : w[u];
+    }
+    if (Cfg::KIND == 0 && full_blk) {
+      if (!(dbgf & 2)) warp_store_bf16_block(P.out, P.ldo, i0, j0, v, stg, lane);
+    } else if (row_ok) {
+      if (full_n) {
+        store_row32<Cfg::KIND, Cfg::SPLIT>(P.out, P.out_lo, off, v);
+      } else {
+        for (int u = 0; u < 32; ++u)
+          if (j0 + u < P.N) store_elem<Cfg::KIND, Cfg::SPLIT>(P.out, P.out_lo, off + u, v[u]);
+      }
+    }
+    return;
+  }
+  if (Cfg::KIND == 0 && full_blk) {
+    if (!(dbgf & 2)) warp_store_bf16_block(P.out, P.ldo, i0, j0, v, stg, lane);
+  } else if (row_ok) {
+    if (full_n) {
+      store_row32<Cfg::KIND, Cfg::SPLIT>(P.out, P.out_lo, off, v);
+    } else {
+      for (int u = 0; u < 32; ++u)
+        if (j0 + u < P.N) store_elem<Cfg::KIND, Cfg::SPLIT>(P.out, P.out_lo, off + u, v[u]);
+    }
+  }
+  if (mode == EPI_RESID && row_ok) {
+#pragma unroll
+    for (int u = 0; u < 32; ++u)
+      if (j0 + u < P.N) sumsq = fmaf(2.f * v[u], v[u], sumsq);
+  }
+  // mirror: lane l writes row j0 + l, columns i0 .. i0+31 (all below the diagonal)
+  const int j = j0 + lane;
+  if (Cfg::KIND == 0 && full_blk) {
+    if (!(dbgf & 1)) warp_store_bf16_block(P.out, P.ldo, j0, i0, w, stg, lane);
+  } else if (j < P.N) {
     const long long moff = (long long)j * P.ldo + i0;
-    if (Cfg::KIND == 0 && !diag && full_blk) {
-      // (whole warp: full_blk implies j < P.N for every lane)
-      __syncwarp();
-      warp_store_bf16_block(P.out, P.ldo, j0, i0, w, stg, lane);
-    } else if (!diag && i0 + 32 <= P.M) {
+    if (i0 + 32 <= P.M) {
       store_row32<Cfg::KIND, Cfg::SPLIT>(P.out, P.out_lo, moff, w);
     } else {
 #pragma unroll
       for (int u = 0; u < 32; ++u)
-        if (i0 + u < j && i0 + u < P.M) store_elem<Cfg::KIND, Cfg::SPLIT>(P.out, P.out_lo, moff + u, w[u]);
+        if (i0 + u < P.M) store_elem<Cfg::KIND, Cfg::SPLIT>(P.out, P.out_lo, moff + u, w[u]);
     }
   }
-  __syncwarp();
 }
 
 // Sketch-chain epilogue (thin GEMM, BN = 32): d[c] + d[w + c] = (R W)[i][c].
@@ -641,7 +653,7 @@ constexpr int TRACE_W = 80;
 // its empty wait), [64,128) MMA full arrival, [128,192) MMA issue done, per k-block.
 __device__ unsigned long long* g_gemm_trace2 = nullptr;
 __device__ int g_trace_mode = -1;
-constexpr int TRACE2_W = 240;   // + [192 + 4 j ..]: tile j mma start / end, epilogue start / end
+constexpr int TRACE2_W = 376;   // + [248 + 16 e + 4 ch + k]: warp e, chunk ch: ld issue, ld done, C done, stored   // + [192 + 4 j ..]: tile j mma start / end, epilogue start / end
 
 template <class Cfg>
 __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __grid_constant__ GemmLaunch L) {
@@ -929,6 +941,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
 #pragma unroll 1
         for (int ch = c_begin; ch < c_end; ++ch) {
           __syncwarp();
+          const bool tw = trace2 && lane == 0 && leader && etcount == 0 && ch - c_begin < 4;
+          const int tslot = 248 + 16 * e + 4 * (ch - c_begin);
+          if (tw) trace2[tslot] = globaltimer_ns();
           uint32_t r[32];
           tmem_ld32(tbase + ch * 32, r);
           uint4 cnext[4];
@@ -940,12 +955,16 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
           }
           tmem_ld_wait();
           if (trace2 && et == 0 && leader && etcount == 0 && ch < 8) trace2[224 + 2 * ch] = globaltimer_ns();
+          if (tw) trace2[tslot + 1] = globaltimer_ns();
           float d[32], c[32];
 #pragma unroll
           for (int u = 0; u < 32; ++u) d[u] = __uint_as_float(r[u]);
           c_finish(tn * Cfg::BN + ch * 32, craw, c);
+          if (trace2 && et == 0 && leader && etcount == 0 && ch < 8) trace2[240 + ch] = globaltimer_ns();
+          if (tw) trace2[tslot + 2] = globaltimer_ns();
           epi_segment<Cfg>(P, mode, sym, i0, lane, tn * Cfg::BN + ch * 32, coefA, coefC, d, c, tb, sumsq);
           if (trace2 && et == 0 && leader && etcount == 0 && ch < 8) trace2[225 + 2 * ch] = globaltimer_ns();
+          if (tw) trace2[tslot + 3] = globaltimer_ns();
 #pragma unroll
           for (int u = 0; u < 4; ++u) craw[u] = cnext[u];
         }

@@ -1293,7 +1293,9 @@ prism_status prism_debug_trace(unsigned long long* buf_dev) {
 
 prism_status prism_debug_trace_gemm(unsigned long long* buf_dev, int mode) {
   if (cudaMemcpyToSymbol(g_gemm_trace2, &buf_dev, sizeof(buf_dev)) != cudaSuccess) return PRISM_ERR_CUDA;
-  return cudaMemcpyToSymbol(g_trace_mode, &mode, sizeof(mode)) == cudaSuccess ? PRISM_OK : PRISM_ERR_CUDA;
+  const int m = mode < 0 ? -1 : (mode & 0xFF), flags = mode < 0 ? 0 : (mode >> 8);
+  if (cudaMemcpyToSymbol(g_dbg_flags, &flags, sizeof(flags)) != cudaSuccess) return PRISM_ERR_CUDA;
+  return cudaMemcpyToSymbol(g_trace_mode, &m, sizeof(m)) == cudaSuccess ? PRISM_OK : PRISM_ERR_CUDA;
 }
 
 prism_status prism_debug_sketch(uint64_t seed, int64_t b, int k, int p, int s, float* S_dev, void* stream) {
