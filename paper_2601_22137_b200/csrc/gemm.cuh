@@ -685,18 +685,12 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
   // (tiles grouped by row tile, grid a multiple of ksplit, so slice == cluster rank)
   const int ksplit = (Cfg::BN == 32 && L.ksplit > 1) ? L.ksplit : 1;
   const uint32_t krank = ksplit > 1 ? cluster_ctarank() : 0u;
-  // device-side loop control (CUDA-graph WHILE body): uniform early exit / parity select
   const GemmProblem* __restrict__ probs = L.probs;
   unsigned long long* trace = nullptr;
   if (Cfg::BN == 32 && g_gemm_trace) trace = g_gemm_trace + ((size_t)L.probs[0].pass * 1024 + blockIdx.x) * TRACE_W;
   if (trace && threadIdx.x == 0) trace[0] = globaltimer_ns();
   unsigned long long* trace2 = nullptr;
   if (Cfg::BN != 32 && g_gemm_trace2 && L.probs[0].mode == g_trace_mode) trace2 = g_gemm_trace2 + (size_t)blockIdx.x * TRACE2_W;
-  if (L.iter) {
-    const int k = *L.iter;
-    if (k < L.iter_lo || k >= L.iter_hi) return;
-    if (L.probs_odd && (k & 1)) probs = L.probs_odd;
-  }
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {
@@ -719,7 +713,30 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
   const uint32_t tmem_base = *tmem_slot;
   if (trace && threadIdx.x == 0) trace[1] = globaltimer_ns();
 
-  if (warp == 0) {
+  // before the predecessor is done: the tile list, problem tables and tensor maps are
+  // plan constants, so warm them; then wait for the predecessor's results
+  if (threadIdx.x == 0 && cid < L.ntiles) {
+    const uint32_t code = __ldg(L.tiles + cid);
+    tma_prefetch(L.probs[code >> 20].tmA);
+    tma_prefetch(L.probs[code >> 20].tmB);
+    if (L.probs_odd) {
+      tma_prefetch(L.probs_odd[code >> 20].tmA);
+      tma_prefetch(L.probs_odd[code >> 20].tmB);
+    }
+  }
+  griddep_launch();
+  griddep_wait();
+  // device-side loop control (CUDA-graph WHILE body): uniform skip / parity select
+  bool run = true;
+  if (L.iter) {
+    const int k = *L.iter;
+    run = k >= L.iter_lo && k < L.iter_hi;
+    if (L.probs_odd && (k & 1)) probs = L.probs_odd;
+  }
+
+  if (!run) {
+    // this launch is outside its iteration window: nothing to do
+  } else if (warp == 0) {
     // ===================== TMA producer =====================
     if (lane == 0) {
       int stage = 0;

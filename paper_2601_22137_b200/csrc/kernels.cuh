@@ -103,6 +103,8 @@ __device__ __forceinline__ T block_sum(T v, T* scratch) {
 // grid (kFroParts, batch), 256 threads; block j handles rows r = j, j + kFroParts, ...
 // with 16-byte vector loads when the row layout allows it.
 __global__ void __launch_bounds__(256) k_fro_partials(SolveParams P) {
+  griddep_wait();
+  griddep_launch();
   __shared__ double scratch[8];
   const MatDesc& D = P.mats[blockIdx.y];
   const int bf16 = P.precision == 0;
@@ -138,6 +140,8 @@ __global__ void __launch_bounds__(256) k_fro_partials(SolveParams P) {
 
 // c = ||A||_F per matrix from the row-strided partials (fixed-order tree); one block per matrix
 __global__ void __launch_bounds__(256) k_fro_final(SolveParams P) {
+  griddep_wait();
+  griddep_launch();
   __shared__ double scratch[8];
   const int b = blockIdx.x;
   double v = (threadIdx.x < kFroParts) ? P.fro_part[b * kFroParts + threadIdx.x] : 0.0;
@@ -150,10 +154,14 @@ __global__ void __launch_bounds__(256) k_fro_final(SolveParams P) {
 
 // row-block: c = sqrt(all-reduced sum of squares)
 __global__ void k_set_c(SolveParams P) {
+  griddep_wait();
+  griddep_launch();
   if (threadIdx.x == 0) P.st[blockIdx.x].c = sqrt(P.fro2_in[blockIdx.x]);
 }
 
 __global__ void k_set_iter(SolveParams P, int k) {
+  griddep_wait();
+  griddep_launch();
   if (threadIdx.x == 0) *P.iter = k;
 }
 
@@ -163,6 +171,8 @@ __device__ __forceinline__ void store_x(void* hi, void* lo, long long idx, float
 // per-tile sum of R^2 in the layout the alpha kernel reads (tiles of 128 x bn, sym = 0).
 template <int PREC>
 __global__ void __launch_bounds__(256) k_resid_from_gram(SolveParams P, const float* G, int bn) {
+  griddep_wait();
+  griddep_launch();
   __shared__ double scratch[8];
   const MatDesc& D = P.mats[0];
   if (P.st[0].done) return;
@@ -278,6 +288,8 @@ struct Vec {
 // a1: X_0 = A / ||A||_F (same row-major layout), Y_0 = I (sqrt), state init.
 template <int PREC>
 __global__ void __launch_bounds__(256) k_normalize(SolveParams P) {
+  griddep_wait();
+  griddep_launch();
   using V = Vec<PREC>;
   const int t = blockIdx.x;
   const int b = find_matrix(P.tile_off, P.batch, t);
@@ -431,6 +443,8 @@ __device__ __forceinline__ bool fit_at(const SolveParams& P, int k) {
 }
 
 __global__ void __launch_bounds__(256) k_sketch(SolveParams P) {
+  griddep_wait();
+  griddep_launch();
   const int b = blockIdx.y;
   const MatDesc& D = P.mats[b];
   const int k = *P.iter;
@@ -530,6 +544,8 @@ __device__ double argmin_quartic(const double c[5], double lo, double hi, double
 // One block (256 threads) per matrix: residual norm, stop test (R12), and
 // alpha_k from the factored sketched loss m(a) = ||V0 + a V1 + a^2 V2||^2.
 __global__ void __launch_bounds__(256) k_alpha(SolveParams P) {
+  griddep_wait();
+  griddep_launch();
   __shared__ double scratch[8];
   __shared__ int s_stop;
   const int k = *P.iter;
@@ -596,6 +612,8 @@ __global__ void __launch_bounds__(256) k_alpha(SolveParams P) {
 // a7: polar Q = X_final; sqrt A^{1/2} = sqrt(c) X, A^{-1/2} = Y / sqrt(c) (cast to the user dtype).
 template <int PREC>
 __global__ void __launch_bounds__(256) k_finalize(SolveParams P) {
+  griddep_wait();
+  griddep_launch();
   using V = Vec<PREC>;
   using VO = Vec<PREC == 0 ? 0 : 2>;   // user output: bf16 or plain fp32
   const int t = blockIdx.x;
@@ -641,6 +659,8 @@ __global__ void __launch_bounds__(256) k_finalize(SolveParams P) {
 // End of one loop iteration: k <- k + 1; keep looping while any matrix is active.
 // (In the CUDA-graph path this sets the WHILE node's condition on the device.)
 __global__ void k_advance(SolveParams P, cudaGraphConditionalHandle handle, int use_handle, int* all_done_out) {
+  griddep_wait();
+  griddep_launch();
   __shared__ int active;
   if (threadIdx.x == 0) active = 0;
   __syncthreads();
@@ -657,6 +677,8 @@ __global__ void k_advance(SolveParams P, cudaGraphConditionalHandle handle, int 
 
 // Copy the solve's report (state + histories kept in the workspace) to the caller's buffers.
 __global__ void k_report(SolveParams P) {
+  griddep_wait();
+  griddep_launch();
   const int nh = P.max_iters, nr = P.max_iters + 1;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.batch * nr; i += gridDim.x * blockDim.x) {
     const int b = i / nr, k = i - b * nr;

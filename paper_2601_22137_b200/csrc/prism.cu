@@ -96,6 +96,43 @@ int num_sms() {
   return g_num_sms;
 }
 
+// Programmatic dependent launch (PRISM_PDL=0 disables, for A/B timing): every kernel
+// calls griddep_wait() before reading its predecessors' results (ptx.cuh).
+static bool use_pdl() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PRISM_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+// Launch `k` with PDL and (cluster > 1) a 1-D cluster.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, int cluster,
+                     Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  int n = 0;
+  at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[n].val.programmaticStreamSerializationAllowed = use_pdl() ? 1 : 0;
+  ++n;
+  if (cluster > 1) {
+    at[n].id = cudaLaunchAttributeClusterDimension;
+    at[n].val.clusterDim.x = cluster;
+    at[n].val.clusterDim.y = 1;
+    at[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 template <class Cfg>
 cudaError_t launch_gemm_cfg(const GemmLaunch& L, cudaStream_t st) {
   static bool attr = false;
@@ -109,39 +146,14 @@ cudaError_t launch_gemm_cfg(const GemmLaunch& L, cudaStream_t st) {
   if constexpr (Cfg::CTA2) {
     // clusters of 2 CTAs (one CTA pair per tile), persistent over the tile list
     const int pairs = std::min(L.ntiles, num_sms() / 2);
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(2 * pairs);
-    cfg.blockDim = dim3(Cfg::THREADS);
-    cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, prism_gemm_kernel<Cfg>, L);
+    return launch_k(prism_gemm_kernel<Cfg>, dim3(2 * pairs), dim3(Cfg::THREADS), Cfg::SMEM_BYTES, st, 2, L);
   } else if (L.ksplit > 1) {
     // chain split-K: clusters of ksplit CTAs, one row tile per cluster per round
     const int grid = std::min(L.ntiles, num_sms() / L.ksplit * L.ksplit);
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(Cfg::THREADS);
-    cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = L.ksplit;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, prism_gemm_kernel<Cfg>, L);
+    return launch_k(prism_gemm_kernel<Cfg>, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM_BYTES, st, L.ksplit, L);
   } else {
     const int grid = std::min(L.ntiles, num_sms());
-    prism_gemm_kernel<Cfg><<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(L);
-    return cudaGetLastError();
+    return launch_k(prism_gemm_kernel<Cfg>, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM_BYTES, st, 1, L);
   }
 }
 
@@ -827,11 +839,11 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
   h->launches = 0;
   {
     KindTimer t(h, st, 5, 3);
-    k_fro_partials<<<dim3(kFroParts, B), 256, 0, st>>>(S);
-    k_fro_final<<<B, 256, 0, st>>>(S);
-    if (prec == PRISM_BF16) k_normalize<0><<<S.n_tiles, 256, 0, st>>>(S);
-    else if (prec == PRISM_FP32) k_normalize<1><<<S.n_tiles, 256, 0, st>>>(S);
-    else k_normalize<2><<<S.n_tiles, 256, 0, st>>>(S);
+    PRISM_CK(launch_k(k_fro_partials, dim3(dim3(kFroParts, B)), dim3(256), 0, st, 1, S));
+    PRISM_CK(launch_k(k_fro_final, dim3(B), dim3(256), 0, st, 1, S));
+    if (prec == PRISM_BF16) PRISM_CK(launch_k(k_normalize<0>, dim3(S.n_tiles), dim3(256), 0, st, 1, S));
+    else if (prec == PRISM_FP32) PRISM_CK(launch_k(k_normalize<1>, dim3(S.n_tiles), dim3(256), 0, st, 1, S));
+    else PRISM_CK(launch_k(k_normalize<2>, dim3(S.n_tiles), dim3(256), 0, st, 1, S));
   }
   PRISM_CK(cudaGetLastError());
   const int M = r.o.max_iters;
@@ -850,12 +862,12 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
     }
     if (sketched) {
       KindTimer t(h, s2, 3, timed ? 1 + P->n_chain : 0);
-      k_sketch<<<dim3((p * P->max_s / 2 + 256) / 256, B), 256, 0, s2>>>(S);
+      PRISM_CK(launch_k(k_sketch, dim3((p * P->max_s / 2 + 256) / 256, B), dim3(256), 0, s2, 1, S));
       for (int j = 0; j < P->n_chain; ++j) PRISM_CK(launch_chain(prec, g_chain[j], s2));
     }
     {
       KindTimer t(h, s2, 4, timed ? 1 : 0);
-      k_alpha<<<B, 256, 0, s2>>>(S);
+      PRISM_CK(launch_k(k_alpha, dim3(B), dim3(256), 0, s2, 1, S));
     }
     if (P->has_square) {
       KindTimer t(h, s2, 1, timed ? 1 : 0);
@@ -865,7 +877,7 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
       KindTimer t(h, s2, 2, timed ? 1 : 0);
       PRISM_CK(launch_gemm(prec, g_apply, s2));
     }
-    k_advance<<<1, 256, 0, s2>>>(S, ch, use_handle, P->d_all_done);
+    PRISM_CK(launch_k(k_advance, dim3(1), dim3(256), 0, s2, 1, S, ch, use_handle, P->d_all_done));
     PRISM_CK(cudaGetLastError());
     return PRISM_OK;
   };
@@ -914,11 +926,11 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
   }
   {
     KindTimer t(h, st, 5, 1);
-    if (prec == PRISM_BF16) k_finalize<0><<<S.n_out_tiles, 256, 0, st>>>(S);
-    else if (prec == PRISM_FP32) k_finalize<1><<<S.n_out_tiles, 256, 0, st>>>(S);
-    else k_finalize<2><<<S.n_out_tiles, 256, 0, st>>>(S);
+    if (prec == PRISM_BF16) PRISM_CK(launch_k(k_finalize<0>, dim3(S.n_out_tiles), dim3(256), 0, st, 1, S));
+    else if (prec == PRISM_FP32) PRISM_CK(launch_k(k_finalize<1>, dim3(S.n_out_tiles), dim3(256), 0, st, 1, S));
+    else PRISM_CK(launch_k(k_finalize<2>, dim3(S.n_out_tiles), dim3(256), 0, st, 1, S));
   }
-  if (rep) k_report<<<std::max(1, std::min(64, (B * (M + 1) + 255) / 256)), 256, 0, st>>>(S);
+  if (rep) PRISM_CK(launch_k(k_report, dim3(std::max(1, std::min(64, (B * (M + 1) + 255) / 256))), dim3(256), 0, st, 1, S));
   h->last_iter = P->d_iter;
   h->last_fixed = 4 + (rep ? 1 : 0);
   h->last_per_iter = P->per_iter_launches;
@@ -1107,8 +1119,8 @@ prism_status prism_rowblock_begin(prism_handle h, int64_t rows, int64_t n, const
     PRISM_CK(cudaMemcpyAsync(r.ws + P->meta_off, P->blob.get(), P->meta_bytes, cudaMemcpyHostToDevice, st));
     SolveParams S = P->params;
     S.fro2_out = fro2_local;
-    k_fro_partials<<<dim3(kFroParts, 1), 256, 0, st>>>(S);
-    k_fro_final<<<1, 256, 0, st>>>(S);
+    PRISM_CK(launch_k(k_fro_partials, dim3(dim3(kFroParts, 1)), dim3(256), 0, st, 1, S));
+    PRISM_CK(launch_k(k_fro_final, dim3(1), dim3(256), 0, st, 1, S));
     PRISM_CK(cudaGetLastError());
     g_rb.plan = P;
     g_rb.ws = r.ws;
@@ -1130,12 +1142,12 @@ prism_status prism_rowblock_gram(prism_handle h, int k, const double* fro2_globa
   if (k == 0) {
     if (!fro2_global) return fail(PRISM_ERR_INVALID_ARG, "null fro2_global at k = 0");
     S.fro2_in = fro2_global;
-    k_set_c<<<1, 32, 0, st>>>(S);
-    if (g_rb.prec == PRISM_BF16) k_normalize<0><<<S.n_tiles, 256, 0, st>>>(S);
-    else if (g_rb.prec == PRISM_FP32) k_normalize<1><<<S.n_tiles, 256, 0, st>>>(S);
-    else k_normalize<2><<<S.n_tiles, 256, 0, st>>>(S);
+    PRISM_CK(launch_k(k_set_c, dim3(1), dim3(32), 0, st, 1, S));
+    if (g_rb.prec == PRISM_BF16) PRISM_CK(launch_k(k_normalize<0>, dim3(S.n_tiles), dim3(256), 0, st, 1, S));
+    else if (g_rb.prec == PRISM_FP32) PRISM_CK(launch_k(k_normalize<1>, dim3(S.n_tiles), dim3(256), 0, st, 1, S));
+    else PRISM_CK(launch_k(k_normalize<2>, dim3(S.n_tiles), dim3(256), 0, st, 1, S));
   }
-  k_set_iter<<<1, 32, 0, st>>>(S, k);
+  PRISM_CK(launch_k(k_set_iter, dim3(1), dim3(32), 0, st, 1, S, k));
   GemmLaunch g = make_launch(*P, P->gram32[0], &P->gram32[1], g_rb.ws, 0, g_rb.max_iters + 1);
   PRISM_CK(launch_gemm(g_rb.prec, g, st));
   PRISM_CK(cudaGetLastError());
@@ -1152,18 +1164,18 @@ prism_status prism_rowblock_update(prism_handle h, int k, const float* G, int32_
   const int bn = tile_bn(prec);
   const int n = P->max_s;
   const dim3 rg((n + bn - 1) / bn, (n + 127) / 128);
-  if (prec == PRISM_BF16) k_resid_from_gram<0><<<rg, 256, 0, st>>>(S, G, bn);
-  else if (prec == PRISM_FP32) k_resid_from_gram<1><<<rg, 256, 0, st>>>(S, G, bn);
-  else k_resid_from_gram<2><<<rg, 256, 0, st>>>(S, G, bn);
+  if (prec == PRISM_BF16) PRISM_CK(launch_k(k_resid_from_gram<0>, dim3(rg), dim3(256), 0, st, 1, S, G, bn));
+  else if (prec == PRISM_FP32) PRISM_CK(launch_k(k_resid_from_gram<1>, dim3(rg), dim3(256), 0, st, 1, S, G, bn));
+  else PRISM_CK(launch_k(k_resid_from_gram<2>, dim3(rg), dim3(256), 0, st, 1, S, G, bn));
   if (g_rb.fit == PRISM_FIT_SKETCHED) {
-    k_sketch<<<dim3((S.p * n / 2 + 256) / 256, 1), 256, 0, st>>>(S);
+    PRISM_CK(launch_k(k_sketch, dim3((S.p * n / 2 + 256) / 256, 1), dim3(256), 0, st, 1, S));
     for (int j = 0; j < P->n_chain; ++j)
       PRISM_CK(launch_chain(prec, make_launch(*P, P->chain[j], nullptr, g_rb.ws, g_rb.warmup, M), st));
   }
-  k_alpha<<<1, 256, 0, st>>>(S);
+  PRISM_CK(launch_k(k_alpha, dim3(1), dim3(256), 0, st, 1, S));
   if (P->has_square) PRISM_CK(launch_gemm(prec, make_launch(*P, P->square, nullptr, g_rb.ws, 0, M), st));
   PRISM_CK(launch_gemm(prec, make_launch(*P, P->apply[0], &P->apply[1], g_rb.ws, 0, M), st));
-  k_advance<<<1, 256, 0, st>>>(S, 0, 0, all_done ? reinterpret_cast<int*>(all_done) : P->d_all_done);
+  PRISM_CK(launch_k(k_advance, dim3(1), dim3(256), 0, st, 1, S, 0, 0, all_done ? reinterpret_cast<int*>(all_done) : P->d_all_done));
   PRISM_CK(cudaGetLastError());
   return PRISM_OK;
 }
@@ -1178,10 +1190,10 @@ prism_status prism_rowblock_end(prism_handle h, const prism_report* rep, void* s
   S.rep_status = rep ? rep->status : nullptr;
   S.rep_alphas = rep ? rep->alphas : nullptr;
   S.rep_resid_hist = rep ? rep->resid_hist : nullptr;
-  if (g_rb.prec == PRISM_BF16) k_finalize<0><<<S.n_out_tiles, 256, 0, st>>>(S);
-  else if (g_rb.prec == PRISM_FP32) k_finalize<1><<<S.n_out_tiles, 256, 0, st>>>(S);
-  else k_finalize<2><<<S.n_out_tiles, 256, 0, st>>>(S);
-  if (rep) k_report<<<1, 256, 0, st>>>(S);
+  if (g_rb.prec == PRISM_BF16) PRISM_CK(launch_k(k_finalize<0>, dim3(S.n_out_tiles), dim3(256), 0, st, 1, S));
+  else if (g_rb.prec == PRISM_FP32) PRISM_CK(launch_k(k_finalize<1>, dim3(S.n_out_tiles), dim3(256), 0, st, 1, S));
+  else PRISM_CK(launch_k(k_finalize<2>, dim3(S.n_out_tiles), dim3(256), 0, st, 1, S));
+  if (rep) PRISM_CK(launch_k(k_report, dim3(1), dim3(256), 0, st, 1, S));
   PRISM_CK(cudaGetLastError());
   g_rb.plan = nullptr;
   return PRISM_OK;
