@@ -469,13 +469,13 @@ template <class Cfg>
 __device__ __forceinline__ void epi_chain(const GemmProblem& P, int i, int tm, const float (&d)[32], double* dred,
                                           int e, int lane, int et, int h) {
   // Row i of the pass output; the two warps sharing a TMEM lane quarter split the p
-  // sketch rows c (h = 0: c < p/2, h = 1: the rest).  Every load is issued before the
+  // sketch rows c (h = 0: c < p/2, h = 1: the rest; h = 2: all, chaint.cuh).  Every load is issued before the
   // first store (the output and keep buffers would otherwise serialise them).
   const int p = P.p;
   const int w = P.N / 2;          // columns of this pass's output
   const bool valid = i < P.M;
-  const int c0 = h ? (p + 1) / 2 : 0;
-  const int c1 = h ? p : (p + 1) / 2;
+  const int c0 = h == 1 ? (p + 1) / 2 : 0;       // h = 2: one thread per row, every c
+  const int c1 = h == 0 ? (p + 1) / 2 : p;
   double g[6] = {0, 0, 0, 0, 0, 0};
   // o[c] = d[c] + d[w + c] (hi + lo halves of the pass output); the runtime shifts by w
   // and p are done by conditional fixed shifts so d / o stay in registers

@@ -4,6 +4,7 @@
 // for the contract and DESIGN.md for the data layout.
 #include "../../include/prism.h"
 #include "gemm.cuh"
+#include "chaint.cuh"
 #include "kernels.cuh"
 
 #include <algorithm>
@@ -157,6 +158,27 @@ cudaError_t launch_gemm_cfg(const GemmLaunch& L, cudaStream_t st) {
   }
 }
 
+template <class Cfg>
+cudaError_t launch_chaint_cfg(const GemmLaunch& L, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(prism_chaint_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Cfg::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  if (L.ntiles <= 0) return cudaSuccess;
+  const int grid = std::min(L.ntiles, num_sms());
+  return launch_k(prism_chaint_kernel<Cfg>, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM_BYTES, st, 1, L);
+}
+
+// Transposed chain pass (chaint.cuh) for the matrices that do not split K.
+cudaError_t launch_chaint(int precision, const GemmLaunch& L, cudaStream_t st) {
+  if (precision == PRISM_BF16) return launch_chaint_cfg<ChainTCfg<0, false>>(L, st);
+  if (precision == PRISM_FP32) return launch_chaint_cfg<ChainTCfg<1, true>>(L, st);
+  return launch_chaint_cfg<ChainTCfg<1, false>>(L, st);
+}
+
 cudaError_t launch_chain(int precision, const GemmLaunch& L, cudaStream_t st) {
   if (precision == PRISM_BF16) return launch_gemm_cfg<GemmCfg<0, false, 32>>(L, st);
   if (precision == PRISM_FP32) return launch_gemm_cfg<GemmCfg<1, true, 32>>(L, st);
@@ -221,7 +243,7 @@ struct Plan {
   size_t meta_off = 0, meta_bytes = 0;
   std::unique_ptr<uint8_t, PinnedDeleter> blob;
   SolveParams params{};
-  LaunchDesc gram[2], square, apply[2], chain[5], gram32[2];
+  LaunchDesc gram[2], square, apply[2], chain[5], chaint[5], gram32[2];   // chain: N = 32 form; chaint: transposed
   int n_chain = 0;
   int chain_ksplit = 1;   // cluster size of the chain launches (split-K)
   bool has_square = false;
@@ -362,7 +384,10 @@ prism_status build_plan(const Request& r, Plan& P) {
     D.W[0] = bump.take((size_t)esz * 4 * p * ldS);
     D.W[1] = bump.take((size_t)esz * 4 * p * ldS);
     D.keep = reinterpret_cast<float*>(bump.take(sizeof(float) * 4 * (size_t)s * p));
-    D.chain_tiles = D.tiles_m;
+    // chain form: transposed (256-row tiles of R, chaint.cuh) unless the
+    // matrix splits K over a cluster (N = 32 form, 128-row tiles)
+    const bool chain_t = chain_ks(s) == 1;
+    D.chain_tiles = chain_t ? (s + 255) / 256 : D.tiles_m;
     D.chain_part = reinterpret_cast<double*>(bump.take(sizeof(double) * 6 * D.tiles_m));
     P.max_s = std::max(P.max_s, s);
     P.max_rows = std::max(P.max_rows, s);
@@ -499,11 +524,24 @@ prism_status build_plan(const Request& r, Plan& P) {
         c.p.p = p;
         c.p.tiles_n = 1;
         c.p.ksplit = chain_ks(s);
-        c.mapA = add_map(D.R, s, s, ldr, OP_A);
-        if (split) c.mapA_lo = add_map(D.R_lo, s, s, ldr, OP_A);
-        maps.push_back(MapSpec{D.W[j % 2], N, s, D.ldS, esz, OP_BK, 32, BK});
-        c.mapB = (int)maps.size();
-        P.chain[j].probs.push_back(c);
+        if (chain_t) {
+          // A = W (rows c, K-major [c][ldS]; box 32 rows, OOB rows zero), B = R (256-row box)
+          maps.push_back(MapSpec{D.W[j % 2], N, s, D.ldS, esz, OP_BK, 32, BK});
+          c.mapA = (int)maps.size();
+          maps.push_back(MapSpec{D.R, s, s, ldr, esz, OP_BK, 256, BK});
+          c.mapB = (int)maps.size();
+          if (split) {
+            maps.push_back(MapSpec{D.R_lo, s, s, ldr, esz, OP_BK, 256, BK});
+            c.mapB_lo = (int)maps.size();
+          }
+          P.chaint[j].probs.push_back(c);
+        } else {
+          c.mapA = add_map(D.R, s, s, ldr, OP_A);
+          if (split) c.mapA_lo = add_map(D.R_lo, s, s, ldr, OP_A);
+          maps.push_back(MapSpec{D.W[j % 2], N, s, D.ldS, esz, OP_BK, 32, BK});
+          c.mapB = (int)maps.size();
+          P.chain[j].probs.push_back(c);
+        }
       }
     }
   }
@@ -542,6 +580,11 @@ prism_status build_plan(const Request& r, Plan& P) {
           L.tiles.push_back(((uint32_t)q << 20) | ((uint32_t)tm << 10) | (uint32_t)ks);
     }
     sort_tiles_by_cost(L);
+    LaunchDesc& T = P.chaint[j];
+    T.tiles.clear();
+    for (int q = 0; q < (int)T.probs.size(); ++q)
+      for (int tn = 0; tn < (T.probs[q].p.M + 255) / 256; ++tn) T.tiles.push_back(((uint32_t)q << 20) | ((uint32_t)tn << 10));
+    sort_tiles_by_cost(T);
   }
   if ((int)P.apply[0].probs.size() >= 4096) return fail(PRISM_ERR_UNSUPPORTED, "batch too large (max 2047 sqrt / 4095 polar)");
 
@@ -563,8 +606,9 @@ prism_status build_plan(const Request& r, Plan& P) {
   off += sizeof(int) * (B + 1);
   const size_t ooff_off = off;
   off += sizeof(int) * (B + 1);
-  LaunchDesc* all[12] = {&P.gram[0], &P.gram[1], &P.apply[0], &P.apply[1], &P.square,
-                         &P.chain[0], &P.chain[1], &P.chain[2], &P.chain[3], &P.chain[4], &P.gram32[0], &P.gram32[1]};
+  LaunchDesc* all[17] = {&P.gram[0],  &P.gram[1],  &P.apply[0], &P.apply[1], &P.square,    &P.chain[0],
+                         &P.chain[1], &P.chain[2], &P.chain[3], &P.chain[4], &P.chaint[0], &P.chaint[1],
+                         &P.chaint[2], &P.chaint[3], &P.chaint[4], &P.gram32[0], &P.gram32[1]};
   for (LaunchDesc* L : all) {
     off = align_up(off, 128);
     L->probs_off = off;
@@ -666,6 +710,7 @@ void ensure_attrs() {
   for (int prec = 0; prec < 3; ++prec) {
     launch_gemm(prec, z, 0);
     launch_chain(prec, z, 0);
+    launch_chaint(prec, z, 0);
   }
 }
 
@@ -850,8 +895,13 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
   const GemmLaunch g_gram = make_launch(*P, P->gram[0], &P->gram[1], r.ws, 0, M + 1);
   const GemmLaunch g_apply = make_launch(*P, P->apply[0], &P->apply[1], r.ws, 0, M);
   const GemmLaunch g_sq = make_launch(*P, P->square, nullptr, r.ws, 0, M);
-  GemmLaunch g_chain[5];
-  for (int j = 0; j < P->n_chain; ++j) g_chain[j] = make_launch(*P, P->chain[j], nullptr, r.ws, r.o.warmup_iters, M);
+  GemmLaunch g_chain[5], g_chaint[5];
+  int n_chain_launches = 0;
+  for (int j = 0; j < P->n_chain; ++j) {
+    g_chain[j] = make_launch(*P, P->chain[j], nullptr, r.ws, r.o.warmup_iters, M);
+    g_chaint[j] = make_launch(*P, P->chaint[j], nullptr, r.ws, r.o.warmup_iters, M);
+    n_chain_launches += (g_chain[j].ntiles > 0) + (g_chaint[j].ntiles > 0);
+  }
   const bool sketched = r.o.fit == PRISM_FIT_SKETCHED;
   const int p = S.p;
   // one iteration k (k read on the device): R_k, stop test, S_k, chain, alpha_k, P, X_{k+1}
@@ -861,9 +911,12 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
       PRISM_CK(launch_gemm(prec, g_gram, s2));
     }
     if (sketched) {
-      KindTimer t(h, s2, 3, timed ? 1 + P->n_chain : 0);
+      KindTimer t(h, s2, 3, timed ? 1 + n_chain_launches : 0);
       PRISM_CK(launch_k(k_sketch, dim3((p * P->max_s / 2 + 256) / 256, B), dim3(256), 0, s2, 1, S));
-      for (int j = 0; j < P->n_chain; ++j) PRISM_CK(launch_chain(prec, g_chain[j], s2));
+      for (int j = 0; j < P->n_chain; ++j) {
+        PRISM_CK(launch_chaint(prec, g_chaint[j], s2));
+        PRISM_CK(launch_chain(prec, g_chain[j], s2));
+      }
     }
     {
       KindTimer t(h, s2, 4, timed ? 1 : 0);
@@ -881,7 +934,7 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
     PRISM_CK(cudaGetLastError());
     return PRISM_OK;
   };
-  P->per_iter_launches = 3 + (sketched ? 1 + P->n_chain : 0) + (P->has_square ? 1 : 0) + 1;
+  P->per_iter_launches = 3 + (sketched ? 1 + n_chain_launches : 0) + (P->has_square ? 1 : 0) + 1;
   if (!h->profiling) {
     if (!P->exec) {
       // build the device-driven loop once per plan: WHILE(any active) { body }
@@ -1169,8 +1222,10 @@ prism_status prism_rowblock_update(prism_handle h, int k, const float* G, int32_
   else PRISM_CK(launch_k(k_resid_from_gram<2>, dim3(rg), dim3(256), 0, st, 1, S, G, bn));
   if (g_rb.fit == PRISM_FIT_SKETCHED) {
     PRISM_CK(launch_k(k_sketch, dim3((S.p * n / 2 + 256) / 256, 1), dim3(256), 0, st, 1, S));
-    for (int j = 0; j < P->n_chain; ++j)
+    for (int j = 0; j < P->n_chain; ++j) {
+      PRISM_CK(launch_chaint(prec, make_launch(*P, P->chaint[j], nullptr, g_rb.ws, g_rb.warmup, M), st));
       PRISM_CK(launch_chain(prec, make_launch(*P, P->chain[j], nullptr, g_rb.ws, g_rb.warmup, M), st));
+    }
   }
   PRISM_CK(launch_k(k_alpha, dim3(1), dim3(256), 0, st, 1, S));
   if (P->has_square) PRISM_CK(launch_gemm(prec, make_launch(*P, P->square, nullptr, g_rb.ws, 0, M), st));

@@ -121,6 +121,26 @@ def test_batch_mixed_shapes_equals_single_solves():
         assert _rel(Qb[i].double().cpu().numpy(), Qo) <= 1e-5
 
 
+def test_split_chain_parity_and_batch_bits():
+    # s >= 1024 takes the N = 32 chain with K split over a CTA cluster (split factor s/512,
+    # capped at 4); smaller s the transposed chain.  One batch mixes factors 4, 2 and the
+    # transposed form: each matrix must come out bit-identical to its single solve (the
+    # launch cluster is the batch maximum; smaller factors leave empty slices), and the
+    # s = 1024 one within the FP32 bound of the oracle.
+    shapes = [(2048, 2048), (1536, 1024), (300, 200)]
+    mats = [torch.tensor(W.gaussian(m, n, seed=10 + i)).float().cuda() for i, (m, n) in enumerate(shapes)]
+    Qb, rb = P.polar(mats, degree=5, tol=1e-5, precision="fp32")
+    torch.cuda.synchronize()
+    for i, t in enumerate(mats):
+        Qs, rs = P.polar([t], degree=5, tol=1e-5, precision="fp32", matrix_ids=[i])
+        torch.cuda.synchronize()
+        assert torch.equal(Qs[0], Qb[i])
+        assert int(rs["iters"][0]) == int(rb["iters"][i])
+    Qo, ro = prism.polar(mats[1].double().cpu().numpy(), d=2, p=8, tol=1e-5, seed=42, b=1)
+    assert _rel(Qb[1].double().cpu().numpy(), Qo) <= 1e-5
+    assert abs(int(rb["iters"][1]) - ro.iters) <= 1
+
+
 def test_edge_cases():
     # zero input, single column, p = s, max_iters stop, NaN input
     z = torch.zeros(64, 32, device="cuda")
