@@ -205,8 +205,7 @@ prism_status prism_debug_argmin(int n, const double* c_dev, double lo, double hi
  * per-pass, per-CTA globaltimer stamps of every later chain launch; NULL disables. */
 prism_status prism_debug_trace(unsigned long long* buf_dev);
 /* Main-GEMM k-block timeline (diagnostics only): buf_dev = device u64[148 * 192]; launches
- * whose epilogue mode is `mode & 0xFF` (0 residual, 1 poly, 2 apply) record per-CTA stamps;
- * mode >> 8 = timing-experiment flags (1 skip mirror stores, 2 skip direct stores: wrong results). */
+ * whose epilogue mode is `mode` (0 residual, 1 poly, 2 apply) record per-CTA stamps. */
 prism_status prism_debug_trace_gemm(unsigned long long* buf_dev, int mode);
 
 #ifdef __cplusplus

@@ -28,7 +28,6 @@
 
 namespace prism {
 
-__device__ int g_dbg_flags = 0;   // timing experiments only (prism_debug_trace_gemm): 1 skip mirror stores, 2 skip direct stores
 enum EpiMode : int { EPI_RESID = 0, EPI_POLY = 1, EPI_APPLY = 2, EPI_STORE = 3, EPI_CHAIN = 4, EPI_GRAM32 = 5 };
 
 // Sketch-chain pass codes (EPI_CHAIN).  The thin GEMM computes
@@ -81,6 +80,17 @@ struct GemmLaunch {
   int ksplit;                    // chain split-K: cluster size (the CTAs of one row tile), else 1
 };
 
+// The problem fields the tile epilogue needs, held in registers for the tile: read
+// through `const GemmProblem&` they are reloaded from global memory after every store
+// (the compiler cannot rule out aliasing).
+struct EpiArgs {
+  void* out;
+  void* out_lo;
+  float* gdiag;
+  long long ldo;
+  int M, N;
+};
+
 template <int KIND_, bool SPLIT_, int BN_ = 0, bool CTA2_ = (BN_ == 0)>
 struct GemmCfg {
   static constexpr int KIND = KIND_;
@@ -123,7 +133,11 @@ struct GemmCfg {
   static constexpr int NCH = BN / 32;   // 32-column chunks per tile
   static constexpr int CH_PER = NCH >= 2 ? NCH / 2 : 1;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers, scratch*/ + SCRATCH_BYTES;
-  static constexpr int THREADS = 64 + 32 * EPI_WARPS;
+  // warpgroup 0: TMA producer (warp 0), MMA issuer (warp 1), two idle warps — shrunk to
+  // REG_LO registers; warpgroups 1-2: the epilogue warps 4..11, grown to REG_HI
+  // (setmaxnreg: the epilogue keeps accumulator, C and output rows in registers)
+  static constexpr int THREADS = 128 + 32 * EPI_WARPS;
+  static constexpr int REG_LO = 72, REG_HI = 216;   // 128 x 72 + 256 x 216 = 384 x 168 (the launch allocation)
   // k-blocks per TMEM accumulation chunk: tf32 partials are promoted to fp32
   // registers every k-block (3xTF32, K = 32: 12 MMAs per chunk) or every 4
   // (1xTF32); bf16 keeps one accumulator per tile (products exact, 2^-9 output).
@@ -305,7 +319,7 @@ __device__ __forceinline__ void store_row32(void* out, void* out_lo, long long o
 
 // Row-block partial Gram (EPI_GRAM32): out = D in plain fp32 whatever the compute
 // dtype (the partial Grams are summed across ranks), symmetric triangle + mirror.
-__device__ __forceinline__ void epi_gram32(const GemmProblem& P, int i0, int lane, int j0, const float (&d)[32],
+__device__ __forceinline__ void epi_gram32(const EpiArgs& P, int i0, int lane, int j0, const float (&d)[32],
                                            float* tb) {
   if (i0 >= P.M || j0 >= P.N || j0 + 31 < i0) return;   // warp-uniform
   const int i = i0 + lane;
@@ -336,7 +350,7 @@ __device__ __forceinline__ void epi_gram32(const GemmProblem& P, int i0, int lan
 // per-warp 32 x 33 shared-memory transpose tb so that both the direct and the
 // mirrored stores are 16-byte vectors).
 template <class Cfg>
-__device__ __forceinline__ void epi_segment(const GemmProblem& P, int mode, bool sym, int i0, int lane, int j0,
+__device__ __forceinline__ void epi_segment(const EpiArgs& P, int mode, bool sym, int i0, int lane, int j0,
                                             float coefA, float coefC, const float (&d)[32], const float (&c)[32],
                                             float* tb, float& sumsq) {
   if (mode == EPI_GRAM32) { epi_gram32(P, i0, lane, j0, d, tb); return; }
@@ -390,7 +404,6 @@ __device__ __forceinline__ void epi_segment(const GemmProblem& P, int mode, bool
   }
   // symmetric: upper triangle (j >= i) written directly, (j > i) mirrored to (j, i)
   const bool diag = j0 < i0 + 32;                // 32-aligned blocks: the diagonal block (j0 == i0)
-  const int dbgf = g_dbg_flags;
   // transpose through shared memory: lane l obtains column j0 + l, rows i0 .. i0+31
 #pragma unroll
   for (int u = 0; u < 32; ++u) tb[lane * 33 + u] = v[u];
@@ -408,7 +421,7 @@ __device__ __forceinline__ void epi_segment(const GemmProblem& P, int mode, bool
       v[u] = u >= lane ? v[u] : w[u];
     }
     if (Cfg::KIND == 0 && full_blk) {
-      if (!(dbgf & 2)) warp_store_bf16_block(P.out, P.ldo, i0, j0, v, stg, lane);
+      warp_store_bf16_block(P.out, P.ldo, i0, j0, v, stg, lane);
     } else if (row_ok) {
       if (full_n) {
         store_row32<Cfg::KIND, Cfg::SPLIT>(P.out, P.out_lo, off, v);
@@ -420,7 +433,7 @@ __device__ __forceinline__ void epi_segment(const GemmProblem& P, int mode, bool
     return;
   }
   if (Cfg::KIND == 0 && full_blk) {
-    if (!(dbgf & 2)) warp_store_bf16_block(P.out, P.ldo, i0, j0, v, stg, lane);
+    warp_store_bf16_block(P.out, P.ldo, i0, j0, v, stg, lane);
   } else if (row_ok) {
     if (full_n) {
       store_row32<Cfg::KIND, Cfg::SPLIT>(P.out, P.out_lo, off, v);
@@ -437,7 +450,7 @@ __device__ __forceinline__ void epi_segment(const GemmProblem& P, int mode, bool
   // mirror: lane l writes row j0 + l, columns i0 .. i0+31 (all below the diagonal)
   const int j = j0 + lane;
   if (Cfg::KIND == 0 && full_blk) {
-    if (!(dbgf & 1)) warp_store_bf16_block(P.out, P.ldo, j0, i0, w, stg, lane);
+    warp_store_bf16_block(P.out, P.ldo, j0, i0, w, stg, lane);
   } else if (j < P.N) {
     const long long moff = (long long)j * P.ldo + i0;
     if (i0 + 32 <= P.M) {
@@ -734,9 +747,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
     if (L.probs_odd && (k & 1)) probs = L.probs_odd;
   }
 
-  if (!run) {
-    // this launch is outside its iteration window: nothing to do
-  } else if (warp == 0) {
+  if (warp < 4) {
+    setmaxnreg_dec<Cfg::REG_LO>();
+    if (!run) {
+      // this launch is outside its iteration window: nothing to do
+    } else if (warp == 0) {
     // ===================== TMA producer =====================
     if (lane == 0) {
       int stage = 0;
@@ -834,12 +849,15 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
       }
       if (trace) trace[6] = globaltimer_ns();
     }
+    }
   } else {
-    // ===================== epilogue (warps 2..9) =====================
+    setmaxnreg_inc<Cfg::REG_HI>();
+    if (run) {
+    // ===================== epilogue (warps 4..11) =====================
     const int q = warp & 3;                 // TMEM lane quarter this warp may access
-    const int e = warp - 2;                 // 0..7
+    const int e = warp - 4;                 // 0..7
     const int h = e >> 2;                   // column half of the tile owned by this warp
-    const int et = threadIdx.x - 64;        // 0..255
+    const int et = threadIdx.x - 128;       // 0..255
     const int c_begin = h * Cfg::CH_PER;
     const int c_end = min(Cfg::NCH, c_begin + Cfg::CH_PER);
     float* tb = tbuf + e * 32 * 33;
@@ -866,6 +884,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
       tile_krange<Cfg>(P, tn, kb_lo, kb_hi);
       const int mode = P.mode;
       const bool sym = P.sym != 0;
+      const EpiArgs ea{P.out, P.out_lo, P.gdiag, P.ldo, P.M, P.N};
+      const void* const Cp = P.C;
+      const long long ldc = P.ldc;
       const int i0 = tm * Cfg::TILE_M + (int)rank * Cfg::BM + q * 32;
       const int i = i0 + lane;                     // output row of this thread
       float coefA = 1.f, coefC = 1.f;
@@ -937,53 +958,49 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
         // bf16: one TMEM accumulator per tile; this warp consumes its 32-column chunks
         // while the raw C row segment of the next chunk is in flight
         // C blocks: coalesced when the warp's 32 x 32 block is in bounds, else per-row
-        const bool rows_full = i0 + 32 <= P.M;
+        const bool rows_full = i0 + 32 <= ea.M;
         auto c_issue = [&](int j, uint4 (&g)[4]) {
 #pragma unroll
           for (int u = 0; u < 4; ++u) g[u] = make_uint4(0, 0, 0, 0);
-          if (!needC || j >= P.N) return;
-          if (rows_full && j + 32 <= P.N) warp_load_bf16_block(P.C, P.ldc, i0, j, g, lane);
-          else if (i < P.M) load_raw_bf16(P.C, P.ldc, i, j, P.N, g);
+          if (!needC || j >= ea.N) return;
+          if (rows_full && j + 32 <= ea.N) warp_load_bf16_block(Cp, ldc, i0, j, g, lane);
+          else if (i < ea.M) load_raw_bf16(Cp, ldc, i, j, ea.N, g);
         };
         auto c_finish = [&](int j, const uint4 (&g)[4], float (&c)[32]) {
-          if (needC && rows_full && j + 32 <= P.N) warp_rows_from_block(g, reinterpret_cast<uint8_t*>(tb), lane, c);
+          if (needC && rows_full && j + 32 <= ea.N) warp_rows_from_block(g, reinterpret_cast<uint8_t*>(tb), lane, c);
           else decode_bf16(g, c);
         };
-        uint4 craw[4];
-        c_issue(tn * Cfg::BN + c_begin * 32, craw);
+        // software pipeline per warp: C blocks two chunks ahead (slot = chunk parity); the
+        // TMEM load of a chunk overlaps the redistribution of its C block
+        const int jb = tn * Cfg::BN;
+        uint4 cq0[4], cq1[4];
+        c_issue(jb + c_begin * 32, cq0);
+        if (c_begin + 1 < c_end) c_issue(jb + (c_begin + 1) * 32, cq1);
         mbar_wait(&tfull[acc], acc_phase);
         if (trace2 && et == 0 && leader && etcount < 8) trace2[192 + 4 * etcount + 2] = globaltimer_ns();
         tc_fence_after();
         const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * Cfg::BN;
-#pragma unroll 1
-        for (int ch = c_begin; ch < c_end; ++ch) {
-          __syncwarp();
+        auto step = [&](int ch, uint4 (&cs)[4]) {
           const bool tw = trace2 && lane == 0 && leader && etcount == 0 && ch - c_begin < 4;
           const int tslot = 248 + 16 * e + 4 * (ch - c_begin);
-          if (tw) trace2[tslot] = globaltimer_ns();
+          if (tw) trace2[tslot] = clock64();
           uint32_t r[32];
           tmem_ld32(tbase + ch * 32, r);
-          uint4 cnext[4];
-          const int jn = tn * Cfg::BN + (ch + 1) * 32;
-          if (ch + 1 < c_end) c_issue(jn, cnext);
-          else {
-#pragma unroll
-            for (int u = 0; u < 4; ++u) cnext[u] = make_uint4(0, 0, 0, 0);
-          }
-          tmem_ld_wait();
-          if (trace2 && et == 0 && leader && etcount == 0 && ch < 8) trace2[224 + 2 * ch] = globaltimer_ns();
-          if (tw) trace2[tslot + 1] = globaltimer_ns();
           float d[32], c[32];
+          c_finish(jb + ch * 32, cs, c);
+          if (tw) trace2[tslot + 2] = clock64();
+          if (ch + 2 < c_end) c_issue(jb + (ch + 2) * 32, cs);
+          tmem_ld_wait_dep(r);
+          if (tw) trace2[tslot + 1] = clock64();
 #pragma unroll
           for (int u = 0; u < 32; ++u) d[u] = __uint_as_float(r[u]);
-          c_finish(tn * Cfg::BN + ch * 32, craw, c);
-          if (trace2 && et == 0 && leader && etcount == 0 && ch < 8) trace2[240 + ch] = globaltimer_ns();
-          if (tw) trace2[tslot + 2] = globaltimer_ns();
-          epi_segment<Cfg>(P, mode, sym, i0, lane, tn * Cfg::BN + ch * 32, coefA, coefC, d, c, tb, sumsq);
-          if (trace2 && et == 0 && leader && etcount == 0 && ch < 8) trace2[225 + 2 * ch] = globaltimer_ns();
-          if (tw) trace2[tslot + 3] = globaltimer_ns();
-#pragma unroll
-          for (int u = 0; u < 4; ++u) craw[u] = cnext[u];
+          epi_segment<Cfg>(ea, mode, sym, i0, lane, jb + ch * 32, coefA, coefC, d, c, tb, sumsq);
+          if (tw) trace2[tslot + 3] = clock64();
+        };
+#pragma unroll 1
+        for (int ch = c_begin; ch < c_end; ch += 2) {
+          step(ch, cq0);
+          if (ch + 1 < c_end) step(ch + 1, cq1);
         }
         release_acc(&tempty[acc]);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
@@ -1017,7 +1034,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
           for (int u = 0; u < 32; ++u) c[u] = 0.f;
           const int j0 = tn * Cfg::BN + (c_begin + x) * 32;
           if (needC && i < P.M && j0 < P.N) load_row32<Cfg::KIND, Cfg::SPLIT>(P.C, P.C_lo, P.ldc, i, j0, P.N, c);
-          epi_segment<Cfg>(P, mode, sym, i0, lane, j0, coefA, coefC, d[x], c, tb, sumsq);
+          epi_segment<Cfg>(ea, mode, sym, i0, lane, j0, coefA, coefC, d[x], c, tb, sumsq);
         }
       }
 
@@ -1040,6 +1057,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
     }
   }
 
+  }
   tc_fence_before();
   if (Cfg::CTA2 || ksplit > 1) cluster_sync_all();   // no CTA leaves while a peer may still touch its smem
   else __syncthreads();

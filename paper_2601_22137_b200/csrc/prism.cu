@@ -1360,8 +1360,7 @@ prism_status prism_debug_trace(unsigned long long* buf_dev) {
 
 prism_status prism_debug_trace_gemm(unsigned long long* buf_dev, int mode) {
   if (cudaMemcpyToSymbol(g_gemm_trace2, &buf_dev, sizeof(buf_dev)) != cudaSuccess) return PRISM_ERR_CUDA;
-  const int m = mode < 0 ? -1 : (mode & 0xFF), flags = mode < 0 ? 0 : (mode >> 8);
-  if (cudaMemcpyToSymbol(g_dbg_flags, &flags, sizeof(flags)) != cudaSuccess) return PRISM_ERR_CUDA;
+  const int m = mode < 0 ? -1 : (mode & 0xFF);
   return cudaMemcpyToSymbol(g_trace_mode, &m, sizeof(m)) == cudaSuccess ? PRISM_OK : PRISM_ERR_CUDA;
 }
 

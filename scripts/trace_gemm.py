@@ -16,7 +16,6 @@ from paper_2601_22137_b200 import binding as B  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="square4096")
-ap.add_argument("--flags", type=int, default=0, help="timing experiments: 1 skip mirror stores, 2 skip direct stores")
 a = ap.parse_args()
 name, shapes, mats_np, opts, desc, kind = bench.workload(a.workload, 0)
 dt = torch.bfloat16 if opts["precision"] == "bf16" else torch.float32
@@ -27,7 +26,7 @@ run()
 torch.cuda.synchronize()
 for mode, nm in [(0, "gram/resid"), (1, "square/poly"), (2, "apply")]:
     buf = torch.zeros(148 * 376, dtype=torch.int64, device="cuda")
-    B.check(B.lib().prism_debug_trace_gemm(ctypes.c_void_p(buf.data_ptr()), mode | (a.flags << 8)), "trace")
+    B.check(B.lib().prism_debug_trace_gemm(ctypes.c_void_p(buf.data_ptr()), mode), "trace")
     run()
     torch.cuda.synchronize()
     B.check(B.lib().prism_debug_trace_gemm(None, -1), "trace")
@@ -70,8 +69,9 @@ for mode, nm in [(0, "gram/resid"), (1, "square/poly"), (2, "apply")]:
     cfr = np.where(cf > 0, (cf - tz[:, 0, 2][:, None]) / 1e3, np.nan)
     print("   first-tile epilogue chunks, C ready (us after epi start, median):", " ".join(f"{x:5.2f}" for x in np.nanmedian(cfr, 0)))
     W = T[lead, 248:376].reshape(-1, 8, 4, 4)
-    Wr = np.where(W > 0, (W - tz[:, 0, 2][:, None, None, None]) / 1e3, np.nan)
-    print("   per-warp chunks (CTA-median) [ld issue, ld done, C done, stored] us after epi start:")
+    base = W[:, :, 0:1, 0:1]
+    Wr = np.where(W > 0, W - base, np.nan)
+    print("   per-warp chunks (CTA-median) [start, tmem ready, C ready, stored] SM cycles after the warp's first chunk:")
     med = np.nanmedian(Wr, 0)
     for e in range(8):
-        print(f"     warp {e}:", "  ".join("[" + ",".join(f"{x:5.2f}" for x in med[e, c]) + "]" for c in range(4)))
+        print(f"     warp {e}:", "  ".join("[" + ",".join(f"{x:6.0f}" for x in med[e, c]) + "]" for c in range(4)))
