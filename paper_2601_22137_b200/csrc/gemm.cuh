@@ -234,9 +234,8 @@ __device__ __forceinline__ void decode_bf16(const uint4 (&w)[4], float (&c)[32])
 // XOR-swizzled: conflict-free both ways) lets each instruction move 8 rows x 64 B.
 __device__ __forceinline__ uint32_t stg_off(int row, int ch) { return (uint32_t)(row * 64 + ((ch ^ ((row >> 1) & 3)) << 4)); }
 
-// this lane's row v[32] -> rows [r0, r0 + 32) x cols [c0, c0 + 32) of out (block fully in bounds)
-__device__ __forceinline__ void warp_store_bf16_block(void* out, long long ld, long long r0, long long c0,
-                                                      const float (&v)[32], uint8_t* stg, int lane) {
+// this lane's row v[32] as bf16 into the staging block (row `lane`)
+__device__ __forceinline__ void stage_row_bf16(const float (&v)[32], uint8_t* stg, int lane) {
 #pragma unroll
   for (int ch = 0; ch < 4; ++ch) {
     uint4 w;
@@ -245,13 +244,40 @@ __device__ __forceinline__ void warp_store_bf16_block(void* out, long long ld, l
     for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(v[ch * 8 + 2 * e], v[ch * 8 + 2 * e + 1]);
     *reinterpret_cast<uint4*>(stg + stg_off(lane, ch)) = w;
   }
-  __syncwarp();
+}
+// staged block -> rows [r0, r0 + 32) x cols [c0, c0 + 32) of out, 8 rows x 64 B per instruction
+__device__ __forceinline__ void store_staged_bf16(void* out, long long ld, long long r0, long long c0,
+                                                  const uint8_t* stg, int lane) {
   __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out);
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     const int row = u * 8 + (lane >> 2), ch = lane & 3;
     *reinterpret_cast<uint4*>(o + (r0 + row) * ld + c0 + ch * 8) = *reinterpret_cast<const uint4*>(stg + stg_off(row, ch));
   }
+}
+// dst = src^T for a staged 32 x 32 bf16 block: the 16 8x8 tiles are read transposed
+// (ldmatrix .trans) and written to the mirrored tile positions (stmatrix)
+__device__ __forceinline__ void transpose_staged_bf16(const uint8_t* src, uint8_t* dst, int lane) {
+  const int i = lane >> 3, j = lane & 7;   // this lane addresses row j of tile i of the x4 group
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    uint32_t r0, r1, r2, r3;
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(smem_u32(src + stg_off(8 * a + j, i))));
+    // tile (a, b = i) transposed goes to tile position (b, a)
+    asm volatile("stmatrix.sync.aligned.m8n8.x4.shared.b16 [%0], {%1, %2, %3, %4};" ::"r"(
+                     smem_u32(dst + stg_off(8 * i + j, a))),
+                 "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+                 : "memory");
+  }
+}
+// this lane's row v[32] -> rows [r0, r0 + 32) x cols [c0, c0 + 32) of out (block fully in bounds)
+__device__ __forceinline__ void warp_store_bf16_block(void* out, long long ld, long long r0, long long c0,
+                                                      const float (&v)[32], uint8_t* stg, int lane) {
+  stage_row_bf16(v, stg, lane);
+  __syncwarp();
+  store_staged_bf16(out, ld, r0, c0, stg, lane);
   __syncwarp();
 }
 // coalesced global read of a 32 x 32 bf16 block (registers, in flight) ...
@@ -404,6 +430,39 @@ __device__ __forceinline__ void epi_segment(const EpiArgs& P, int mode, bool sym
   }
   // symmetric: upper triangle (j >= i) written directly, (j > i) mirrored to (j, i)
   const bool diag = j0 < i0 + 32;                // 32-aligned blocks: the diagonal block (j0 == i0)
+  if (Cfg::KIND == 0 && full_blk) {
+    // bf16 rows staged once; the mirror is the staged block transposed by 8x8 tiles
+    // (ldmatrix.trans / stmatrix) — same bf16 values, exact symmetry
+    uint8_t* stg2 = stg + 2048;
+    stage_row_bf16(v, stg, lane);
+    __syncwarp();
+    if (!diag) store_staged_bf16(P.out, P.ldo, i0, j0, stg, lane);
+    transpose_staged_bf16(stg, stg2, lane);
+    __syncwarp();
+    if (mode == EPI_RESID) {
+#pragma unroll
+      for (int u = 0; u < 32; ++u)
+        if (!diag || u >= lane) sumsq = fmaf((diag && u == lane) ? v[u] : 2.f * v[u], v[u], sumsq);
+    }
+    if (!diag) {
+      store_staged_bf16(P.out, P.ldo, j0, i0, stg2, lane);
+    } else {
+      // diagonal block: row lane = own values on/above the diagonal, transposed below
+      uint4 wr[4];
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) wr[ch] = *reinterpret_cast<const uint4*>(stg2 + stg_off(lane, ch));
+      float w[32];
+      decode_bf16(wr, w);
+#pragma unroll
+      for (int u = 0; u < 32; ++u) w[u] = u >= lane ? v[u] : w[u];
+      __syncwarp();
+      stage_row_bf16(w, stg, lane);
+      __syncwarp();
+      store_staged_bf16(P.out, P.ldo, i0, j0, stg, lane);
+    }
+    __syncwarp();
+    return;
+  }
   // transpose through shared memory: lane l obtains column j0 + l, rows i0 .. i0+31
 #pragma unroll
   for (int u = 0; u < 32; ++u) tb[lane * 33 + u] = v[u];
