@@ -121,6 +121,21 @@ prism_status prism_polar(prism_handle h, int batch, const int64_t* m, const int6
                          void* workspace, size_t ws_bytes, void* stream);
 
 /*
+ * End-to-end path on HOST buffers.  A[i] / Q[i] are page-locked host memory
+ * (cudaHostAlloc / cudaHostRegister / torch pin_memory), shapes and leading dimensions as
+ * prism_polar.  The call enqueues, on handle-internal streams, the upload into one of two
+ * handle-owned device staging slots, the solve, and the download into Q, then returns;
+ * `stream` is made to wait for the download, so a sync of `stream` (or later work on it)
+ * observes Q.  Successive calls on one handle pipeline: the upload of call k+1 and the
+ * download of call k overlap the solves.  Staging and workspace are device memory owned by
+ * the handle (grown on demand, which synchronises the device).  rep: optional DEVICE
+ * report, written in call order (read it once no later call is in flight).
+ */
+prism_status prism_polar_host(prism_handle h, int batch, const int64_t* m, const int64_t* n, const void* const* A,
+                              const int64_t* lda, void* const* Q, const int64_t* ldq, const int64_t* matrix_ids,
+                              const prism_options* o, const prism_report* rep, void* stream);
+
+/*
  * Coupled square root / inverse square root of SPD n[i] x n[i] matrices
  * (symmetry is the caller's contract; a non-SPD input shows up as a
  * DIVERGED / NONFINITE / MAX_ITERS status).  Asqrt / Ainvsqrt: either array,
@@ -131,6 +146,11 @@ prism_status prism_sqrt_invsqrt(prism_handle h, int batch, const int64_t* n, con
                                 const int64_t* lda, void* const* Asqrt, void* const* Ainvsqrt,
                                 const int64_t* ld_out, const int64_t* matrix_ids, const prism_options* o,
                                 const prism_report* rep, void* workspace, size_t ws_bytes, void* stream);
+/* prism_sqrt_invsqrt on page-locked HOST buffers, pipelined as prism_polar_host. */
+prism_status prism_sqrt_invsqrt_host(prism_handle h, int batch, const int64_t* n, const void* const* A,
+                                     const int64_t* lda, void* const* Asqrt, void* const* Ainvsqrt,
+                                     const int64_t* ld_out, const int64_t* matrix_ids, const prism_options* o,
+                                     const prism_report* rep, void* stream);
 
 /*
  * LPT partition: assign `batch` matrices with costs cost[i]

@@ -55,6 +55,7 @@ class Report(ctypes.Structure):
 EXPORTS = [
     "prism_default_options", "prism_create", "prism_destroy", "prism_last_error", "prism_abi_version",
     "prism_polar_workspace", "prism_polar", "prism_sqrt_workspace", "prism_sqrt_invsqrt",
+    "prism_polar_host", "prism_sqrt_invsqrt_host",
     "prism_lpt_partition", "prism_polar_flops_per_iter", "prism_sqrt_flops_per_iter",
     "prism_launch_count", "prism_profile_enable", "prism_profile_read",
     "prism_rowblock_workspace", "prism_rowblock_begin", "prism_rowblock_gram", "prism_rowblock_update",
@@ -90,6 +91,11 @@ def lib():
         L.prism_polar_workspace.restype = sz
         L.prism_polar.argtypes = [vp, i32, c_i64p, c_i64p, ctypes.POINTER(vp), c_i64p, ctypes.POINTER(vp), c_i64p,
                                   c_i64p, ctypes.POINTER(Options), ctypes.POINTER(Report), vp, sz, vp]
+        L.prism_polar_host.argtypes = [vp, i32, c_i64p, c_i64p, ctypes.POINTER(vp), c_i64p, ctypes.POINTER(vp),
+                                       c_i64p, c_i64p, ctypes.POINTER(Options), ctypes.POINTER(Report), vp]
+        L.prism_sqrt_invsqrt_host.argtypes = [vp, i32, c_i64p, ctypes.POINTER(vp), c_i64p, ctypes.POINTER(vp),
+                                              ctypes.POINTER(vp), c_i64p, c_i64p, ctypes.POINTER(Options),
+                                              ctypes.POINTER(Report), vp]
         L.prism_sqrt_workspace.argtypes = [vp, i32, c_i64p, ctypes.POINTER(Options)]
         L.prism_sqrt_workspace.restype = sz
         L.prism_sqrt_invsqrt.argtypes = [vp, i32, c_i64p, ctypes.POINTER(vp), c_i64p, ctypes.POINTER(vp),
@@ -117,6 +123,7 @@ def lib():
         L.prism_debug_trace.argtypes = [vp]
         L.prism_debug_trace_gemm.argtypes = [vp, i32]
         for name in ("prism_create", "prism_destroy", "prism_polar", "prism_sqrt_invsqrt", "prism_lpt_partition",
+                     "prism_polar_host", "prism_sqrt_invsqrt_host",
                      "prism_debug_gemm", "prism_debug_sketch", "prism_debug_argmin", "prism_debug_trace",
                      "prism_debug_trace_gemm", "prism_profile_enable", "prism_profile_read", "prism_rowblock_begin",
                      "prism_rowblock_gram", "prism_rowblock_update", "prism_rowblock_end"):
@@ -214,12 +221,13 @@ def _precision_of(t, precision):
     return "bf16" if t.dtype == torch.bfloat16 else "fp32"
 
 
-def _check_dtype(ts, precision):
+def _check_dtype(ts, precision, on_host=False):
     import torch
     want = torch.bfloat16 if precision == "bf16" else torch.float32
+    where = "pinned host" if on_host else "CUDA"
     for t in ts:
-        if t.dtype != want or not t.is_cuda or t.dim() != 2 or t.stride(1) != 1:
-            raise PrismError(f"inputs must be 2-D CUDA {want} tensors with unit column stride")
+        if t.dtype != want or t.is_cuda == on_host or t.dim() != 2 or t.stride(1) != 1:
+            raise PrismError(f"inputs must be 2-D {where} {want} tensors with unit column stride")
 
 
 def _report_buffers(batch, max_iters, device):
@@ -278,6 +286,77 @@ def polar(mats, degree=5, max_iters=30, sketch_size=8, tol=1e-6, seed=42, precis
                             _i64([t.stride(0) for t in out]), ids, ctypes.byref(o), ctypes.byref(rep),
                             ws.data_ptr(), ws.numel(), ctypes.c_void_p(st.cuda_stream)), "prism_polar")
     return out, rb
+
+
+def _check_pinned(ts, what):
+    for t in ts:
+        if t.device.type != "cpu" or not t.is_pinned():
+            raise PrismError(f"{what}: host-path tensors must be pinned CPU tensors (tensor.pin_memory())")
+
+
+def polar_host(mats, degree=5, max_iters=30, sketch_size=8, tol=1e-6, seed=42, precision=None, fit="sketched",
+               warmup_iters=0, alpha_lo=None, alpha_hi=None, out=None, matrix_ids=None, stream=None, handle=None,
+               device=None):
+    """Polar factors of pinned HOST matrices via prism_polar_host (end-to-end path).
+
+    Uploads, solves and downloads on the handle's internal streams; returns
+    (outputs, report) immediately — outputs (pinned host tensors) and the device
+    report are valid once `stream` (default: the current stream of `device`)
+    reaches this call.  Successive calls on one handle overlap copies with solves.
+    """
+    import torch
+    mats = list(mats)
+    if not mats:
+        return [], {}
+    _check_pinned(mats, "polar_host")
+    precision = _precision_of(mats[0], precision)
+    _check_dtype(mats, precision, on_host=True)
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    h = handle or default_handle()
+    o = make_options(degree, max_iters, sketch_size, tol, seed, precision, fit, warmup_iters, alpha_lo, alpha_hi)
+    B = len(mats)
+    if out is None:
+        out = [torch.empty_like(t).pin_memory() for t in mats]
+    _check_pinned(out, "polar_host")
+    _check_dtype(out, precision, on_host=True)
+    rb = _report_buffers(B, max_iters, dev)
+    rep = _report_struct(rb)
+    ids = _i64(matrix_ids) if matrix_ids is not None else None
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    check(lib().prism_polar_host(h.h, B, _i64([t.shape[0] for t in mats]), _i64([t.shape[1] for t in mats]),
+                                 _ptrs(mats), _i64([t.stride(0) for t in mats]), _ptrs(out),
+                                 _i64([t.stride(0) for t in out]), ids, ctypes.byref(o), ctypes.byref(rep),
+                                 ctypes.c_void_p(st.cuda_stream)), "prism_polar_host")
+    return out, rb
+
+
+def sqrt_invsqrt_host(mats, degree=5, max_iters=30, sketch_size=8, tol=1e-6, seed=42, precision=None,
+                      fit="sketched", warmup_iters=0, alpha_lo=None, alpha_hi=None, want_sqrt=True,
+                      want_invsqrt=True, matrix_ids=None, stream=None, handle=None, device=None):
+    """A^{1/2}, A^{-1/2} of pinned HOST SPD matrices via prism_sqrt_invsqrt_host."""
+    import torch
+    mats = list(mats)
+    if not mats:
+        return [], [], {}
+    _check_pinned(mats, "sqrt_invsqrt_host")
+    precision = _precision_of(mats[0], precision)
+    _check_dtype(mats, precision, on_host=True)
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    h = handle or default_handle()
+    o = make_options(degree, max_iters, sketch_size, tol, seed, precision, fit, warmup_iters, alpha_lo, alpha_hi)
+    B = len(mats)
+    sq = [torch.empty_like(t).pin_memory() for t in mats] if want_sqrt else None
+    isq = [torch.empty_like(t).pin_memory() for t in mats] if want_invsqrt else None
+    rb = _report_buffers(B, max_iters, dev)
+    rep = _report_struct(rb)
+    ids = _i64(matrix_ids) if matrix_ids is not None else None
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    check(lib().prism_sqrt_invsqrt_host(h.h, B, _i64([t.shape[0] for t in mats]), _ptrs(mats),
+                                        _i64([t.stride(0) for t in mats]), _ptrs(sq) if sq else None,
+                                        _ptrs(isq) if isq else None, _i64([t.shape[1] for t in mats]), ids,
+                                        ctypes.byref(o), ctypes.byref(rep), ctypes.c_void_p(st.cuda_stream)),
+          "prism_sqrt_invsqrt_host")
+    return sq, isq, rb
 
 
 def sqrt_invsqrt(mats, degree=5, max_iters=30, sketch_size=8, tol=1e-6, seed=42, precision=None, fit="sketched",

@@ -8,6 +8,8 @@
 #include "kernels.cuh"
 
 #include <algorithm>
+#include <array>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <list>
@@ -233,7 +235,12 @@ struct PinnedDeleter {
 struct Plan {
   ~Plan() {
     if (exec) cudaGraphExecDestroy(exec);
+    if (meta_dev) cudaFree(meta_dev);
   }
+  // plan constants (matrix descriptors, tile lists, problem tables, tensor maps) in a
+  // device allocation owned by the plan, uploaded once when the plan is built: a per-solve
+  // upload would queue behind unrelated host->device copies on the copy engine
+  char* meta_dev = nullptr;
   cudaGraphExec_t exec = nullptr;   // CUDA graph: WHILE(any matrix active) { one iteration }
   int* d_iter = nullptr;            // device iteration counter
   int* d_all_done = nullptr;
@@ -623,10 +630,11 @@ prism_status build_plan(const Request& r, Plan& P) {
   const size_t maps_off = off;
   off += sizeof(CUtensorMap) * maps.size();
   P.meta_bytes = align_up(off, 256);
-  P.ws_need = P.meta_off + P.meta_bytes;
+  P.ws_need = P.meta_off;
   if (!r.ws) return PRISM_OK;
 
-  char* meta_dev = r.ws + P.meta_off;
+  if (cudaMalloc(&P.meta_dev, P.meta_bytes) != cudaSuccess) return fail(PRISM_ERR_CUDA, "cudaMalloc(plan constants)");
+  char* meta_dev = P.meta_dev;
   uint8_t* blob = nullptr;
   if (cudaMallocHost(&blob, P.meta_bytes) != cudaSuccess) return fail(PRISM_ERR_CUDA, "cudaMallocHost(plan blob)");
   P.blob.reset(blob);
@@ -653,6 +661,9 @@ prism_status build_plan(const Request& r, Plan& P) {
     }
     std::memcpy(blob + L->tiles_off, L->tiles.data(), sizeof(uint32_t) * L->tiles.size());
   }
+
+  if (cudaMemcpy(P.meta_dev, blob, P.meta_bytes, cudaMemcpyHostToDevice) != cudaSuccess)
+    return fail(PRISM_ERR_CUDA, "upload of plan constants");
 
   SolveParams& S = P.params;
   std::memset(&S, 0, sizeof(S));
@@ -687,7 +698,8 @@ prism_status build_plan(const Request& r, Plan& P) {
 GemmLaunch make_launch(const Plan& P, const LaunchDesc& L, const LaunchDesc* odd, char* ws, int lo, int hi) {
   GemmLaunch g{};
   g.ksplit = (!L.probs.empty() && L.probs[0].p.mode == EPI_CHAIN) ? P.chain_ksplit : 1;
-  char* meta = ws + P.meta_off;
+  (void)ws;
+  char* meta = P.meta_dev;
   g.probs = reinterpret_cast<const GemmProblem*>(meta + L.probs_off);
   g.probs_odd = odd ? reinterpret_cast<const GemmProblem*>(meta + odd->probs_off) : nullptr;
   g.tiles = reinterpret_cast<const uint32_t*>(meta + L.tiles_off);
@@ -760,11 +772,38 @@ struct prism_handle_s {
   int* last_iter = nullptr;                 // device iteration counter of the last solve
   int last_fixed = 0, last_per_iter = 0;
   int* h_flag = nullptr;                    // pinned host flag (profiling path)
+  // host-buffer path (prism_polar_host / prism_sqrt_invsqrt_host): two device staging
+  // slots, upload / solve / download on three internal streams, ordered by events, so
+  // call k+1's upload and call k's download overlap the solves
+  struct HostSlot {
+    char* in = nullptr;
+    char* out = nullptr;
+    char* out2 = nullptr;
+    size_t in_bytes = 0, out_bytes = 0;
+    cudaEvent_t ev_h2d = nullptr, ev_comp = nullptr, ev_d2h = nullptr;
+    bool used = false;
+  };
+  HostSlot slots[2];
+  int slot_next = 0;
+  cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
+  char* hws = nullptr;   // workspace of the host-path solves (they run in order on s_comp)
+  size_t hws_bytes = 0;
   ~prism_handle_s() {
     plans.clear();
     for (cudaEvent_t e : pool) cudaEventDestroy(e);
     if (cap) cudaStreamDestroy(cap);
     if (h_flag) cudaFreeHost(h_flag);
+    if (s_in || s_comp || s_out) cudaDeviceSynchronize();
+    for (HostSlot& sl : slots) {
+      if (sl.in) cudaFree(sl.in);
+      if (sl.out) cudaFree(sl.out);
+      if (sl.out2) cudaFree(sl.out2);
+      for (cudaEvent_t e : {sl.ev_h2d, sl.ev_comp, sl.ev_d2h})
+        if (e) cudaEventDestroy(e);
+    }
+    if (hws) cudaFree(hws);
+    for (cudaStream_t x : {s_in, s_comp, s_out})
+      if (x) cudaStreamDestroy(x);
   }
   cudaEvent_t next_event() {
     if (pool_used == pool.size()) {
@@ -871,7 +910,6 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
   prism_status gs = get_plan(h, r, ws_bytes, &P);
   if (gs) return gs;
 
-  PRISM_CK(cudaMemcpyAsync(r.ws + P->meta_off, P->blob.get(), P->meta_bytes, cudaMemcpyHostToDevice, st));
   SolveParams S = P->params;   // report pointers are only read by k_report (outside the graph)
   S.rep_iters = rep ? rep->iters : nullptr;
   S.rep_resid = rep ? rep->resid : nullptr;
@@ -1071,6 +1109,154 @@ prism_status prism_polar(prism_handle h, int batch, const int64_t* m, const int6
   }
 }
 
+// Host <-> device copy of an m x w block (element size esz): one linear copy when both
+// sides are compact (cudaMemcpy2DAsync would move it row by row), else a 2-D copy.
+static cudaError_t copy_block(void* dst, size_t dld, const void* src, size_t sld, size_t w, size_t m, size_t esz,
+                              cudaMemcpyKind kind, cudaStream_t st) {
+  if (dld == w && sld == w) return cudaMemcpyAsync(dst, src, m * w * esz, kind, st);
+  return cudaMemcpy2DAsync(dst, dld * esz, src, sld * esz, w * esz, m, kind, st);
+}
+
+// End-to-end path on host buffers (see prism.h): stage, solve, return, pipelined.
+static prism_status host_solve(prism_handle h, bool sqrt_kind, int batch, const int64_t* m, const int64_t* n,
+                               const void* const* A_host, const int64_t* lda, void* const* O1, void* const* O2,
+                               const int64_t* ldo, const int64_t* ids, const prism_options* o,
+                               const prism_report* rep, cudaStream_t caller) {
+  if (!h || !o) return fail(PRISM_ERR_INVALID_ARG, "null handle / options");
+  if (batch < 1 || !m || !A_host || !lda || !ldo || (!sqrt_kind && (!n || !O1)))
+    return fail(PRISM_ERR_INVALID_ARG, "bad host-path arguments");
+  const size_t esz = (size_t)elem_size(o->precision);
+  // compact device staging (ld = n)
+  std::vector<size_t> off(batch + 1, 0);
+  for (int i = 0; i < batch; ++i) {
+    const int64_t mm = m[i], nn = sqrt_kind ? m[i] : n[i];
+    if (mm < 1 || nn < 1 || lda[i] < nn || ldo[i] < nn) return fail(PRISM_ERR_INVALID_ARG, "bad host-path shape");
+    off[i + 1] = off[i] + align_up((size_t)(mm * nn) * esz, 256);
+  }
+  const size_t bytes = off[batch];
+  if (!h->s_in) {
+    for (cudaStream_t* x : {&h->s_in, &h->s_comp, &h->s_out})
+      PRISM_CK(cudaStreamCreateWithFlags(x, cudaStreamNonBlocking));
+    for (auto& sl : h->slots)
+      for (cudaEvent_t* e : {&sl.ev_h2d, &sl.ev_comp, &sl.ev_d2h})
+        PRISM_CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  }
+  std::vector<int64_t> ldc(batch);
+  std::vector<const void*> din(batch);
+  std::vector<void*> dout(batch), dout2(batch);
+  auto& sl = h->slots[h->slot_next];
+  h->slot_next ^= 1;
+  const bool two = sqrt_kind && O1 && O2;
+  const size_t ws_need = sqrt_kind ? prism_sqrt_workspace(h, batch, m, o) : prism_polar_workspace(h, batch, m, n, o);
+  if (!ws_need) return fail(PRISM_ERR_INVALID_ARG, "workspace query failed");
+  if (sl.in_bytes < bytes || sl.out_bytes < bytes || (two && !sl.out2) || h->hws_bytes < ws_need) {
+    PRISM_CK(cudaDeviceSynchronize());   // growing: nothing of the old buffers may be in flight
+    if (sl.in_bytes < bytes || sl.out_bytes < bytes || (two && !sl.out2)) {
+      if (sl.in) cudaFree(sl.in);
+      if (sl.out) cudaFree(sl.out);
+      if (sl.out2) cudaFree(sl.out2);
+      sl.in = sl.out = sl.out2 = nullptr;
+      PRISM_CK(cudaMalloc(&sl.in, bytes));
+      PRISM_CK(cudaMalloc(&sl.out, bytes));
+      if (sqrt_kind) PRISM_CK(cudaMalloc(&sl.out2, bytes));
+      sl.in_bytes = sl.out_bytes = bytes;
+    }
+    if (h->hws_bytes < ws_need) {
+      if (h->hws) cudaFree(h->hws);
+      h->hws = nullptr;
+      PRISM_CK(cudaMalloc(&h->hws, ws_need));
+      h->hws_bytes = ws_need;
+    }
+  }
+  for (int i = 0; i < batch; ++i) {
+    ldc[i] = sqrt_kind ? m[i] : n[i];
+    din[i] = sl.in + off[i];
+    dout[i] = sl.out + off[i];
+    dout2[i] = sl.out2 ? sl.out2 + off[i] : nullptr;
+  }
+  // optional timeline (PRISM_HOST_TRACE=1): per call, upload / solve / download spans
+  static const bool tr = getenv("PRISM_HOST_TRACE") != nullptr;
+  static std::vector<std::array<cudaEvent_t, 6>> tl;
+  std::array<cudaEvent_t, 6> te{};
+  if (tr) {
+    for (auto& e : te) cudaEventCreate(&e);
+  }
+  // upload (after this slot's previous solve has consumed its inputs)
+  if (sl.used) PRISM_CK(cudaStreamWaitEvent(h->s_in, sl.ev_comp, 0));
+  if (tr) cudaEventRecord(te[0], h->s_in);
+  for (int i = 0; i < batch; ++i)
+    PRISM_CK(copy_block(sl.in + off[i], ldc[i], A_host[i], lda[i], ldc[i], m[i], esz, cudaMemcpyHostToDevice,
+                        h->s_in));
+  if (tr) cudaEventRecord(te[1], h->s_in);
+  PRISM_CK(cudaEventRecord(sl.ev_h2d, h->s_in));
+  // solve (after the upload, and after this slot's previous download has read its outputs)
+  PRISM_CK(cudaStreamWaitEvent(h->s_comp, sl.ev_h2d, 0));
+  if (sl.used) PRISM_CK(cudaStreamWaitEvent(h->s_comp, sl.ev_d2h, 0));
+  if (tr) cudaEventRecord(te[2], h->s_comp);
+  prism_status st;
+  if (sqrt_kind)
+    st = prism_sqrt_invsqrt(h, batch, m, din.data(), ldc.data(), O1 ? dout.data() : nullptr,
+                            O2 ? dout2.data() : nullptr, ldc.data(), ids, o, rep, h->hws, h->hws_bytes, h->s_comp);
+  else
+    st = prism_polar(h, batch, m, n, din.data(), ldc.data(), dout.data(), ldc.data(), ids, o, rep, h->hws,
+                     h->hws_bytes, h->s_comp);
+  if (st) return st;
+  if (tr) cudaEventRecord(te[3], h->s_comp);
+  PRISM_CK(cudaEventRecord(sl.ev_comp, h->s_comp));
+  // download
+  PRISM_CK(cudaStreamWaitEvent(h->s_out, sl.ev_comp, 0));
+  if (tr) cudaEventRecord(te[4], h->s_out);
+  for (int i = 0; i < batch; ++i) {
+    if (O1 && O1[i])
+      PRISM_CK(copy_block(O1[i], ldo[i], sl.out + off[i], ldc[i], ldc[i], m[i], esz, cudaMemcpyDeviceToHost,
+                          h->s_out));
+    if (two && O2[i])
+      PRISM_CK(copy_block(O2[i], ldo[i], sl.out2 + off[i], ldc[i], ldc[i], m[i], esz, cudaMemcpyDeviceToHost,
+                          h->s_out));
+  }
+  if (tr) {
+    cudaEventRecord(te[5], h->s_out);
+    tl.push_back(te);
+    if (tl.size() == 12) {
+      cudaDeviceSynchronize();
+      for (size_t c = 0; c < tl.size(); ++c) {
+        float v[6];
+        for (int k = 0; k < 6; ++k) cudaEventElapsedTime(&v[k], tl[0][0], tl[c][k]);
+        fprintf(stderr, "call %2zu  h2d [%7.2f %7.2f]  solve [%7.2f %7.2f]  d2h [%7.2f %7.2f] ms\n", c, v[0], v[1],
+                v[2], v[3], v[4], v[5]);
+      }
+      tl.clear();
+    }
+  }
+  PRISM_CK(cudaEventRecord(sl.ev_d2h, h->s_out));
+  PRISM_CK(cudaStreamWaitEvent(caller, sl.ev_d2h, 0));
+  sl.used = true;
+  return PRISM_OK;
+}
+
+prism_status prism_polar_host(prism_handle h, int batch, const int64_t* m, const int64_t* n, const void* const* A,
+                              const int64_t* lda, void* const* Q, const int64_t* ldq, const int64_t* matrix_ids,
+                              const prism_options* o, const prism_report* rep, void* stream) {
+  try {
+    return host_solve(h, false, batch, m, n, A, lda, Q, nullptr, ldq, matrix_ids, o, rep,
+                      static_cast<cudaStream_t>(stream));
+  } catch (...) {
+    return fail(PRISM_ERR_INTERNAL, "exception in prism_polar_host");
+  }
+}
+
+prism_status prism_sqrt_invsqrt_host(prism_handle h, int batch, const int64_t* n, const void* const* A,
+                                     const int64_t* lda, void* const* Asqrt, void* const* Ainvsqrt,
+                                     const int64_t* ld_out, const int64_t* matrix_ids, const prism_options* o,
+                                     const prism_report* rep, void* stream) {
+  try {
+    return host_solve(h, true, batch, n, n, A, lda, Asqrt, Ainvsqrt, ld_out, matrix_ids, o, rep,
+                      static_cast<cudaStream_t>(stream));
+  } catch (...) {
+    return fail(PRISM_ERR_INTERNAL, "exception in prism_sqrt_invsqrt_host");
+  }
+}
+
 size_t prism_sqrt_workspace(prism_handle h, int batch, const int64_t* n, const prism_options* o) {
   if (!h || !o || !n || batch < 1) return 0;
   std::vector<const void*> fakeA(batch, reinterpret_cast<const void*>(256));
@@ -1169,8 +1355,7 @@ prism_status prism_rowblock_begin(prism_handle h, int64_t rows, int64_t n, const
     prism_status gs = get_plan(h, r, ws_bytes, &P);
     if (gs) return gs;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    PRISM_CK(cudaMemcpyAsync(r.ws + P->meta_off, P->blob.get(), P->meta_bytes, cudaMemcpyHostToDevice, st));
-    SolveParams S = P->params;
+      SolveParams S = P->params;
     S.fro2_out = fro2_local;
     PRISM_CK(launch_k(k_fro_partials, dim3(dim3(kFroParts, 1)), dim3(256), 0, st, 1, S));
     PRISM_CK(launch_k(k_fro_final, dim3(1), dim3(256), 0, st, 1, S));

@@ -141,6 +141,29 @@ def test_split_chain_parity_and_batch_bits():
     assert abs(int(rb["iters"][1]) - ro.iters) <= 1
 
 
+def test_host_path_pipelined_equals_device_path():
+    # prism_polar_host: three different batches submitted back to back (two staging
+    # slots, so the third reuses the first slot while the pipeline is busy); each result
+    # must be bit-identical to the device-path solve of the same inputs
+    shapes = [(300, 200), (128, 256), (520, 136)]
+    batches = [[torch.tensor(W.gaussian(m, n, seed=100 * c + i)).to(torch.bfloat16).pin_memory()
+                for i, (m, n) in enumerate(shapes)] for c in range(3)]
+    h = P.Handle()
+    outs = [P.polar_host(b, degree=5, tol=3e-2, precision="bf16", handle=h)[0] for b in batches]
+    torch.cuda.synchronize()
+    for b, o in zip(batches, outs):
+        ref, _ = P.polar([t.cuda() for t in b], degree=5, tol=3e-2, precision="bf16")
+        torch.cuda.synchronize()
+        for x, y in zip(o, ref):
+            assert torch.equal(x, y.cpu())
+    A = [torch.tensor(W.spd_logspaced(96, 1e2, seed=7)).float().pin_memory()]
+    sq, isq, _ = P.sqrt_invsqrt_host(A, degree=5, tol=1e-5, precision="fp32", handle=h)
+    torch.cuda.synchronize()
+    rs, ri, _ = P.sqrt_invsqrt([A[0].cuda()], degree=5, tol=1e-5, precision="fp32")
+    torch.cuda.synchronize()
+    assert torch.equal(sq[0], rs[0].cpu()) and torch.equal(isq[0], ri[0].cpu())
+
+
 def test_edge_cases():
     # zero input, single column, p = s, max_iters stop, NaN input
     z = torch.zeros(64, 32, device="cuda")
