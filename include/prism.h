@@ -123,7 +123,7 @@ prism_status prism_polar(prism_handle h, int batch, const int64_t* m, const int6
 /*
  * End-to-end path on HOST buffers.  A[i] / Q[i] are page-locked host memory
  * (cudaHostAlloc / cudaHostRegister / torch pin_memory), shapes and leading dimensions as
- * prism_polar.  The call enqueues, on handle-internal streams, the upload into one of two
+ * prism_polar.  The call enqueues, on handle-internal streams, the upload into one of three
  * handle-owned device staging slots, the solve, and the download into Q, then returns;
  * `stream` is made to wait for the download, so a sync of `stream` (or later work on it)
  * observes Q.  Successive calls on one handle pipeline: the upload of call k+1 and the

@@ -772,7 +772,7 @@ struct prism_handle_s {
   int* last_iter = nullptr;                 // device iteration counter of the last solve
   int last_fixed = 0, last_per_iter = 0;
   int* h_flag = nullptr;                    // pinned host flag (profiling path)
-  // host-buffer path (prism_polar_host / prism_sqrt_invsqrt_host): two device staging
+  // host-buffer path (prism_polar_host / prism_sqrt_invsqrt_host): device staging
   // slots, upload / solve / download on three internal streams, ordered by events, so
   // call k+1's upload and call k's download overlap the solves
   struct HostSlot {
@@ -783,7 +783,8 @@ struct prism_handle_s {
     cudaEvent_t ev_h2d = nullptr, ev_comp = nullptr, ev_d2h = nullptr;
     bool used = false;
   };
-  HostSlot slots[2];
+  static constexpr int kMaxSlots = 4;
+  HostSlot slots[kMaxSlots];
   int slot_next = 0;
   cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
   char* hws = nullptr;   // workspace of the host-path solves (they run in order on s_comp)
@@ -1144,8 +1145,13 @@ static prism_status host_solve(prism_handle h, bool sqrt_kind, int batch, const 
   std::vector<int64_t> ldc(batch);
   std::vector<const void*> din(batch);
   std::vector<void*> dout(batch), dout2(batch);
+  static const int nslots = [] {
+    const char* e = getenv("PRISM_HOST_SLOTS");
+    const int v = e ? atoi(e) : 3;
+    return std::max(2, std::min(prism_handle_s::kMaxSlots, v));
+  }();
   auto& sl = h->slots[h->slot_next];
-  h->slot_next ^= 1;
+  h->slot_next = (h->slot_next + 1) % nslots;
   const bool two = sqrt_kind && O1 && O2;
   const size_t ws_need = sqrt_kind ? prism_sqrt_workspace(h, batch, m, o) : prism_polar_workspace(h, batch, m, n, o);
   if (!ws_need) return fail(PRISM_ERR_INVALID_ARG, "workspace query failed");

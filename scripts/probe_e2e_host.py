@@ -17,7 +17,7 @@ host = [torch.tensor(a).to(dt).pin_memory() for a in mats_np]
 out = [torch.empty_like(x).pin_memory() for x in host]
 h = P.Handle()
 dev = [x.cuda() for x in host]
-for _ in range(2):
+for _ in range(4):   # every staging slot and its plan warmed
     P.polar_host(host, out=out, handle=h, **opts)
     P.polar(dev, handle=h, **opts)
 torch.cuda.synchronize()
