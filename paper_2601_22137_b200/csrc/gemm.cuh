@@ -1029,37 +1029,39 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
           if (needC && rows_full && j + 32 <= ea.N) warp_rows_from_block(g, reinterpret_cast<uint8_t*>(tb), lane, c);
           else decode_bf16(g, c);
         };
-        // software pipeline per warp: C blocks two chunks ahead (slot = chunk parity); the
-        // TMEM load of a chunk overlaps the redistribution of its C block
+        // software pipeline per warp: chunk ch+1's tcgen05.ld (ping-pong registers) and its
+        // C block are in flight while chunk ch is combined and stored
         const int jb = tn * Cfg::BN;
-        uint4 cq0[4], cq1[4];
-        c_issue(jb + c_begin * 32, cq0);
-        if (c_begin + 1 < c_end) c_issue(jb + (c_begin + 1) * 32, cq1);
+        uint4 cq[4];
+        c_issue(jb + c_begin * 32, cq);
         mbar_wait(&tfull[acc], acc_phase);
         if (trace2 && et == 0 && leader && etcount < 8) trace2[192 + 4 * etcount + 2] = globaltimer_ns();
         tc_fence_after();
         const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * Cfg::BN;
-        auto step = [&](int ch, uint4 (&cs)[4]) {
+        uint32_t ra[32], rb[32];
+        tmem_ld32(tbase + c_begin * 32, ra);
+        tmem_ld_wait_dep(ra);
+        auto step = [&](int ch, uint32_t (&rc)[32], uint32_t (&rn)[32]) {
           const bool tw = trace2 && lane == 0 && leader && etcount == 0 && ch - c_begin < 4;
           const int tslot = 248 + 16 * e + 4 * (ch - c_begin);
           if (tw) trace2[tslot] = clock64();
-          uint32_t r[32];
-          tmem_ld32(tbase + ch * 32, r);
+          const bool more = ch + 1 < c_end;
+          if (more) tmem_ld32(tbase + (ch + 1) * 32, rn);
           float d[32], c[32];
-          c_finish(jb + ch * 32, cs, c);
+          c_finish(jb + ch * 32, cq, c);
           if (tw) trace2[tslot + 2] = clock64();
-          if (ch + 2 < c_end) c_issue(jb + (ch + 2) * 32, cs);
-          tmem_ld_wait_dep(r);
-          if (tw) trace2[tslot + 1] = clock64();
+          if (more) c_issue(jb + (ch + 1) * 32, cq);
 #pragma unroll
-          for (int u = 0; u < 32; ++u) d[u] = __uint_as_float(r[u]);
+          for (int u = 0; u < 32; ++u) d[u] = __uint_as_float(rc[u]);
+          if (tw) trace2[tslot + 1] = clock64();
           epi_segment<Cfg>(ea, mode, sym, i0, lane, jb + ch * 32, coefA, coefC, d, c, tb, sumsq);
+          if (more) tmem_ld_wait_dep(rn);
           if (tw) trace2[tslot + 3] = clock64();
         };
 #pragma unroll 1
         for (int ch = c_begin; ch < c_end; ch += 2) {
-          step(ch, cq0);
-          if (ch + 1 < c_end) step(ch + 1, cq1);
+          step(ch, ra, rb);
+          if (ch + 1 < c_end) step(ch + 1, rb, ra);
         }
         release_acc(&tempty[acc]);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
