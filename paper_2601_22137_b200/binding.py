@@ -60,8 +60,8 @@ EXPORTS = [
     "prism_launch_count", "prism_profile_enable", "prism_profile_read",
     "prism_rowblock_workspace", "prism_rowblock_begin", "prism_rowblock_gram", "prism_rowblock_update",
     "prism_rowblock_end",
-    "prism_debug_gemm", "prism_debug_sketch", "prism_debug_argmin", "prism_debug_trace",
-    "prism_debug_trace_gemm",
+    "prism_debug_gemm", "prism_debug_sketch", "prism_debug_argmin",
+    "prism_debug_trace_gemm", "prism_debug_trace_chain",
 ]
 
 _lib = None
@@ -120,12 +120,12 @@ def lib():
         L.prism_rowblock_end.argtypes = [vp, ctypes.POINTER(Report), vp]
         L.prism_debug_sketch.argtypes = [u64, i64, i32, i32, i32, vp, vp]
         L.prism_debug_argmin.argtypes = [i32, vp, dbl, dbl, dbl, vp, vp]
-        L.prism_debug_trace.argtypes = [vp]
         L.prism_debug_trace_gemm.argtypes = [vp, i32]
+        L.prism_debug_trace_chain.argtypes = [vp]
         for name in ("prism_create", "prism_destroy", "prism_polar", "prism_sqrt_invsqrt", "prism_lpt_partition",
                      "prism_polar_host", "prism_sqrt_invsqrt_host",
-                     "prism_debug_gemm", "prism_debug_sketch", "prism_debug_argmin", "prism_debug_trace",
-                     "prism_debug_trace_gemm", "prism_profile_enable", "prism_profile_read", "prism_rowblock_begin",
+                     "prism_debug_gemm", "prism_debug_sketch", "prism_debug_argmin",
+                     "prism_debug_trace_gemm", "prism_debug_trace_chain", "prism_profile_enable", "prism_profile_read", "prism_rowblock_begin",
                      "prism_rowblock_gram", "prism_rowblock_update", "prism_rowblock_end"):
             getattr(L, name).restype = i32
         _lib = L

@@ -1,19 +1,21 @@
-// Transposed sketch-chain pass for matrices that do not split K (PRISM §4.2, the
-// sketched-trace chain of DESIGN.md §4.6): D = W · Rᵀ, i.e. D[c][n] = (R W)[n][c].
+// Sketch-chain pass (PRISM §4.2 — the sketched-trace chain; device form DESIGN.md §4.4,
+// §4.6): D = W · Rᵀ, i.e. D[c][n] = (R W)[n][c], for every matrix of the batch.
 //
 // One tcgen05.mma costs the same ~138 cycles for any N ≤ 256 (measured, scripts/
 // mma_probe.cu), so the thin product R·W (W has 2w ≤ 32 columns) is issued with W as
 // the A operand (M = 128, of which the first 32 rows are the W rows; rows 32..127
 // read the B bytes that follow in smem and give TMEM lanes nobody reads) and 256 rows
-// of R as the B operand (N = 256): half the MMAs of the N = 32 form (gemm.cuh,
-// BN = 32), one 256-row tile of R per CTA.
+// of R as the B operand (N = 256).  Both operands are K-major in their natural
+// layouts: W is stored [c][ldS] (the previous pass's output) and R row-major.
 //
-// Both operands are K-major in their natural layouts: W is stored [c][ldS] (the
-// previous pass's output) and R row-major.  Epilogue: the two warps that may read
-// TMEM lanes 0..31 (warp % 4 == 0) copy D (32 x 256 fp32) to shared memory, then the
-// 256 epilogue threads take one row n of R each and run the same per-row chain
-// epilogue as the N = 32 kernel (epi_chain, gemm.cuh) — identical arithmetic per
-// element, so both kernels produce the same K / L / <Va,Vb> definitions.
+// Large matrices split K over a cluster of C = L.ksplit CTAs (the tile code's low bits
+// carry the slice; a matrix whose own factor P.ksplit is smaller leaves the trailing
+// slices empty, i.e. zeros).  The fp32 partials are combined by a reduce-scatter over
+// distributed shared memory: CTA r owns rows [r·256/C, (r+1)·256/C) of the tile; every
+// CTA st.async's its partial of those rows into the owner's smem (complete_tx on the
+// owner's mbarrier), the owner sums the C slices in fixed order (deterministic) and
+// runs the per-row chain epilogue for its rows.  C = 1: the two warps that may read
+// TMEM lanes 0..31 stage D (32 x 256 fp32) in smem and every epilogue thread takes a row.
 #pragma once
 
 #include "gemm.cuh"
@@ -32,19 +34,34 @@ struct ChainTCfg {
   static constexpr int A_BYTES = WROWS * 128;
   static constexpr int B_BYTES = BN * 128;
   static constexpr int STAGE_BYTES = A_BYTES + (SPLIT ? 2 : 1) * B_BYTES;
-  static constexpr int DSTRIDE = 257;       // D staging row stride (floats): conflict-free both ways
-  static constexpr int DSM_BYTES = 32 * DSTRIDE * 4;
+  // receive / staging buffer: [C sources][32 c][256/C + 4] fp32 (padded rows: conflict-free)
+  static constexpr int recv_bytes(int C) { return C * 32 * (BN / C + 4) * 4; }
+  static constexpr int DSM_BYTES = recv_bytes(4) > recv_bytes(1) ? recv_bytes(4) : recv_bytes(1);
   static constexpr int STAGES_RAW = (227 * 1024 - 2048 - DSM_BYTES) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 6 ? 6 : STAGES_RAW;
   static constexpr int EPI_WARPS = 8;
-  static constexpr int THREADS = 64 + 32 * EPI_WARPS;
-  static constexpr int PROMO_KB = KIND == 0 ? (1 << 30) : (SPLIT ? 1 : 4);
+  // warpgroup 0: TMA producer, MMA issuer, two idle warps (REG_LO registers); warpgroups
+  // 1-2: the epilogue warps 4..11 (REG_HI)
+  static constexpr int THREADS = 128 + 32 * EPI_WARPS;
+  static constexpr int REG_LO = 72, REG_HI = 216;   // 128 x 72 + 256 x 216 = 384 x 168
   static constexpr uint32_t IDESC = idesc_make(KIND == 0 ? 1u : 2u, 0u, 128, BN);
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers*/ + DSM_BYTES;
-  static_assert(STAGES >= 2, "chainT pipeline needs two stages");
+  static_assert(STAGES >= 2, "chain pipeline needs two stages");
 };
 
-template <class Cfg>
+// K-block range of slice `ks` of a matrix split `own` ways (empty past its own factor)
+__device__ __forceinline__ void chain_krange(int K, int BK, int own, int ks, int& lo, int& hi) {
+  const int nkb = (K + BK - 1) / BK;
+  lo = ks < own ? ks * nkb / own : nkb;
+  hi = ks < own ? (ks + 1) * nkb / own : nkb;
+}
+
+// Debug timeline (prism_debug_trace_chain): per pass code and CTA, 16 globaltimer stamps
+// of the launch: 0 entry, 1 setup done, 2 predecessor done, 3 first TMA, 4 last MMA
+// committed, 5 accumulator ready (reader), 6 slices sent, 7 slices received, 8 epilogue done.
+__device__ unsigned long long* g_chain_trace = nullptr;
+
+template <class Cfg, int PASS>
 __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __grid_constant__ GemmLaunch L) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -55,12 +72,22 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
   uint64_t* empty = bars + Cfg::STAGES;
   uint64_t* tfull = bars + 2 * Cfg::STAGES;   // [2]
   uint64_t* tempty = tfull + 2;               // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  double* dred = reinterpret_cast<double*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES + 256);   // [8][6]
-  float* dsm = reinterpret_cast<float*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES + 1024);     // [32][DSTRIDE]
+  uint64_t* recv_full = tempty + 2;           // split: remote slices landed (complete_tx)
+  uint64_t* recv_free = recv_full + 1;        // split: every owner consumed this CTA's slices
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(recv_free + 1);
+  float* dsm = reinterpret_cast<float*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES + 1024);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  unsigned long long* tr = g_chain_trace ? g_chain_trace + ((size_t)L.probs[0].pass * 1024 + blockIdx.x) * 16 : nullptr;
+  if (tr && threadIdx.x == 0) tr[0] = globaltimer_ns();
+  const int C = L.ksplit > 1 ? L.ksplit : 1;           // cluster size (1, 2, 4, 8)
+  const uint32_t krank = C > 1 ? cluster_ctarank() : 0u;
+  const int rows_per = Cfg::BN / C;                    // rows of the tile this CTA finishes
+  const int rstride = rows_per + 4;                    // receive-buffer row stride (floats)
+  // every tile / slice accumulates in TMEM as one chunk (no tf32 promotion chunks): the
+  // same partial whether or not the launch splits K, so a matrix's bits never depend on
+  // the batch; the tf32 accumulation error (~1e-5 relative) is immaterial for alpha
   if (threadIdx.x == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -70,13 +97,17 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 2);   // the two TMEM-reading warps
     }
+    mbar_init(recv_full, 1);                 // own expect_tx arrival; remote bytes complete_tx
+    mbar_init(recv_free, C > 1 ? C - 1 : 1); // one arrival per other owner
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<1>(tmem_slot, 512);
   tc_fence_before();
-  __syncthreads();
+  if (C > 1) cluster_sync_all();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (tr && threadIdx.x == 0) tr[1] = globaltimer_ns();
 
   if (threadIdx.x == 0 && (int)blockIdx.x < L.ntiles) {
     const uint32_t code = __ldg(L.tiles + blockIdx.x);
@@ -85,6 +116,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
   }
   griddep_launch();
   griddep_wait();
+  if (tr && threadIdx.x == 0) tr[2] = globaltimer_ns();
   const GemmProblem* __restrict__ probs = L.probs;
   bool run = true;
   if (L.iter) {
@@ -93,8 +125,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
     if (L.probs_odd && (k & 1)) probs = L.probs_odd;
   }
 
-  if (!run) {
-  } else if (warp == 0) {
+  if (warp < 4) {
+    setmaxnreg_dec<Cfg::REG_LO>();
+    if (!run) {
+    } else if (warp == 0) {
     // ===================== TMA producer =====================
     if (lane == 0) {
       int stage = 0;
@@ -104,8 +138,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
         const GemmProblem& P = probs[code >> 20];
         if (L.done && L.done[P.matrix * L.done_stride]) continue;
         const int n0 = ((code >> 10) & 1023) * Cfg::BN;
-        const int nkb = (P.K + Cfg::BK - 1) / Cfg::BK;
-        for (int kb = 0; kb < nkb; ++kb) {
+        int kb_lo, kb_hi;
+        chain_krange(P.K, Cfg::BK, P.ksplit, (int)(code & 1023), kb_lo, kb_hi);
+        for (int kb = kb_lo; kb < kb_hi; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sA = stage_base + stage * Cfg::STAGE_BYTES;
           uint8_t* sB = sA + Cfg::A_BYTES;
@@ -113,6 +148,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
           tma_load_2d(sA, P.tmA, &full[stage], kb * Cfg::BK, 0);    // W rows 0..31 (OOB rows zero)
           tma_load_2d(sB, P.tmB, &full[stage], kb * Cfg::BK, n0);   // R rows n0 .. n0+255
           if constexpr (Cfg::SPLIT) tma_load_2d(sB + Cfg::B_BYTES, P.tmB_lo, &full[stage], kb * Cfg::BK, n0);
+          if (tr && kb == kb_lo) tr[3] = globaltimer_ns();
           if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -128,9 +164,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
         const uint32_t code = L.tiles[t];
         const GemmProblem& P = probs[code >> 20];
         if (L.done && L.done[P.matrix * L.done_stride]) continue;
-        const int nkb = (P.K + Cfg::BK - 1) / Cfg::BK;
-        for (int kb0 = 0; kb0 < nkb; kb0 += Cfg::PROMO_KB) {
-          const int kb1 = min(nkb, kb0 + Cfg::PROMO_KB);
+        int kb_lo, kb_hi;
+        chain_krange(P.K, Cfg::BK, P.ksplit, (int)(code & 1023), kb_lo, kb_hi);
+        if (kb_lo < kb_hi) {
+          const int kb0 = kb_lo, kb1 = kb_hi;
           mbar_wait(&tempty[acc], acc_phase ^ 1);
           tc_fence_after();
           const uint32_t dt = tmem_base + acc * Cfg::BN;
@@ -151,60 +188,116 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
             if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
           }
           umma_commit<1>(&tfull[acc]);
+          if (tr) tr[4] = globaltimer_ns();
           if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
       }
     }
+    }
   } else {
-    // ===================== epilogue (warps 2..9) =====================
-    const int e = warp - 2;
-    const int et = threadIdx.x - 64;             // 0..255: row n0 + et of R
+    setmaxnreg_inc<Cfg::REG_HI>();
+    if (run) {
+    // ===================== epilogue (warps 4..11) =====================
+    const int e = warp - 4;
+    const int et = threadIdx.x - 128;            // 0..255
     const bool reader = (warp & 3) == 0;         // warps 4 and 8 own TMEM lanes 0..31
     const int h = e >> 2;                        // reader column half
     int acc = 0;
     uint32_t acc_phase = 0;
+    uint32_t rphase = 0;   // split: receive-buffer round parity
     for (int t = blockIdx.x; t < L.ntiles; t += gridDim.x) {
       const uint32_t code = L.tiles[t];
       const GemmProblem& P = probs[code >> 20];
       if (L.done && L.done[P.matrix * L.done_stride]) continue;
       const int tn = (code >> 10) & 1023;
-      const int nkb = (P.K + Cfg::BK - 1) / Cfg::BK;
-      for (int kb0 = 0; kb0 < nkb; kb0 += Cfg::PROMO_KB) {
-        if (reader) {
+      int kb_lo, kb_hi;
+      chain_krange(P.K, Cfg::BK, P.ksplit, (int)(code & 1023), kb_lo, kb_hi);
+      // this thread's row of the pass output, and its operands loaded ahead (chain_prefetch)
+      const bool mine = C == 1 || et < rows_per;   // whole warps (rows_per is a multiple of 32)
+      const int i = !mine ? P.M : tn * Cfg::BN + (C == 1 ? 0 : (int)krank * rows_per) + et;   // P.M: no row
+      const int row0 = tn * Cfg::BN + (C == 1 ? 0 : (int)krank * rows_per) + (et & ~31);
+      const int grp = (mine && row0 < P.M) ? row0 >> 5 : -1;   // this warp's 32-row group
+      ChainPre pre;
+      chain_prefetch<Cfg, PASS>(P, i, 2, pre);
+      // the accumulator (32 x 256, TMEM lanes 0..31) to the owners of its rows: CTA r of
+      // the cluster owns rows [r·rows_per, (r+1)·rows_per); C = 1: all rows stay here
+      const bool have = kb_lo < kb_hi;
+      if (reader) {
+        if (have) {
           mbar_wait(&tfull[acc], acc_phase);
           tc_fence_after();
+        }
+        if (tr && lane == 0 && h == 0) tr[5] = globaltimer_ns();
+        // every owner consumed the previous round's slices: send this round's
+        if (C > 1) mbar_wait(recv_free, rphase ^ 1);
 #pragma unroll 1
-          for (int x = 0; x < 4; ++x) {
-            uint32_t r[32];
-            const int col = h * 128 + x * 32;
+        for (int x = 0; x < 4; ++x) {
+          const int col = h * 128 + x * 32;          // 32 rows n of the tile
+          uint32_t r[32];
+          if (have) {
             tmem_ld32(tmem_base + acc * Cfg::BN + col, r);
             tmem_ld_wait();
-            float* row = dsm + lane * Cfg::DSTRIDE + col;
-            if (kb0 == 0) {
+          } else {
 #pragma unroll
-              for (int u = 0; u < 32; ++u) row[u] = __uint_as_float(r[u]);
-            } else {
-#pragma unroll
-              for (int u = 0; u < 32; ++u) row[u] += __uint_as_float(r[u]);
-            }
+            for (int u = 0; u < 32; ++u) r[u] = 0x80000000u;   // -0.0: x + (-0) == x for every x
           }
+          const uint32_t owner = (uint32_t)(col / rows_per);
+          const int nl = col - (int)owner * rows_per;  // row offset within the owner's range
+          float* dst = dsm + ((size_t)krank * 32 + lane) * rstride + nl;   // source krank's slot
+#pragma unroll
+          for (int u = 0; u < 32; u += 4) {
+            const float4 v = make_float4(__uint_as_float(r[u]), __uint_as_float(r[u + 1]),
+                                         __uint_as_float(r[u + 2]), __uint_as_float(r[u + 3]));
+            if (owner == krank) *reinterpret_cast<float4*>(dst + u) = v;
+            else st_async_v4(dst + u, recv_full, owner, v);
+          }
+        }
+        if (have) {
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[acc]);
         }
-        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        if (tr && lane == 0 && h == 0) tr[6] = globaltimer_ns();
       }
-      named_bar_sync(1, 32 * Cfg::EPI_WARPS);   // D staged
-      float d[32];
+      if (have && ++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if (C > 1 && et == 0) mbar_arrive_expect_tx(recv_full, (uint32_t)(C - 1) * 32 * rows_per * 4);
+      named_bar_sync(1, 32 * Cfg::EPI_WARPS);    // own slice written locally
+      if (C > 1) {
+        mbar_wait(recv_full, rphase);            // the other C-1 slices landed
+        if (tr && et == 0) tr[7] = globaltimer_ns();
+        if (et < rows_per) {
+          // sum the C slices in fixed order (deterministic; -0.0 identity: one real slice
+          // sums to itself exactly) into this thread's column of slot 0; 32 independent
+          // accumulators keep each source's loads in flight together
+          float v[32];
 #pragma unroll
-      for (int c = 0; c < 32; ++c) d[c] = dsm[c * Cfg::DSTRIDE + et];
-      named_bar_sync(1, 32 * Cfg::EPI_WARPS);   // staging free for the next tile
-      epi_chain<Cfg>(P, tn * Cfg::BN + et, tn, d, dred, e, lane, et, 2);
+          for (int c = 0; c < 32; ++c) v[c] = -0.f;
+          for (int src = 0; src < C; ++src) {
+#pragma unroll
+            for (int c = 0; c < 32; ++c) v[c] += dsm[((size_t)src * 32 + c) * rstride + et];
+          }
+#pragma unroll
+          for (int c = 0; c < 32; ++c) dsm[(size_t)c * rstride + et] = v[c];
+        }
+      }
+      if (tr && et == 0) tr[9] = globaltimer_ns();
+      epi_chain<Cfg, PASS>(pre, i, grp, dsm + et, rstride, lane, 2);
+      named_bar_sync(1, 32 * Cfg::EPI_WARPS);    // buffer consumed
+      if (C > 1) {
+        rphase ^= 1;
+        // hand the slots back (gates only a later round's sends: off the critical path)
+        if (et == 32)
+          for (int x = 0; x < C; ++x)
+            if (x != (int)krank) mbar_arrive_release_cluster(recv_free, (uint32_t)x);
+      }
+      if (tr && et == 0) tr[8] = globaltimer_ns();
     }
   }
 
+  }
   tc_fence_before();
-  __syncthreads();
+  if (C > 1) cluster_sync_all();   // no CTA leaves while a peer may still write into its smem
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<1>(tmem_base, 512);

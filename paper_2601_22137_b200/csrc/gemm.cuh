@@ -106,20 +106,14 @@ struct GemmCfg {
   static constexpr int TILE_M = BM * CG;          // rows per (pair) tile
   static constexpr int BN = BN_ ? BN_ : (KIND == 0 ? 256 : 128);
   static constexpr int B_ROWS = BN / CG;          // B rows (along N) loaded per CTA
-  // thin chain GEMM (BN = 32): B already carries [W_hi | W_lo], so 3xTF32 needs
-  // only A_lo · B besides A · B (no B_lo plane)
-  static constexpr bool LOB = SPLIT && BN != 32;
+  static constexpr bool LOB = SPLIT;            // 3xTF32: B carries a lo plane too
   static constexpr int BK = 128 / ESZ;          // one 128-B swizzle row of K
   static constexpr int UK = 32 / ESZ;           // K per tcgen05.mma (32 bytes)
   static constexpr int A_BYTES = BM * BK * ESZ;
   static constexpr int B_BYTES = B_ROWS * BK * ESZ;
   static constexpr int STAGE_BYTES = (SPLIT ? 2 * A_BYTES : A_BYTES) + (LOB ? 2 * B_BYTES : B_BYTES);
-  // chain split-K: the leader CTA of a cluster receives up to 3 fp32 128 x 32 partials
-  // (DSMEM), in the transpose-buffer region (unused by the chain epilogue) and beyond
-  static constexpr int TB_BYTES = 8 * 32 * 33 * 4;   // per-epilogue-warp 32x33 fp32 transpose buffers
-  static constexpr int RED_BYTES = BN == 32 ? 3 * 32 * 128 * 4 : 0;
-  static constexpr int SCRATCH_BYTES = RED_BYTES > TB_BYTES ? RED_BYTES : TB_BYTES;
-  static constexpr int STAGES_RAW = (192 * 1024 - (SCRATCH_BYTES - TB_BYTES)) / STAGE_BYTES;
+  static constexpr int TB_BYTES = 8 * 32 * 33 * 4;   // per-epilogue-warp staging / transpose buffers
+  static constexpr int STAGES_RAW = (192 * 1024) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int TMEM_COLS = 2 * BN;
   static constexpr int AE = 128 / ESZ;           // elements per 128-B atom along MN (MN-major)
@@ -132,7 +126,7 @@ struct GemmCfg {
   static constexpr int EPI_WARPS = 8;   // two per TMEM lane quarter, each owning half the columns
   static constexpr int NCH = BN / 32;   // 32-column chunks per tile
   static constexpr int CH_PER = NCH >= 2 ? NCH / 2 : 1;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers, scratch*/ + SCRATCH_BYTES;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers, scratch*/ + TB_BYTES;
   // warpgroup 0: TMA producer (warp 0), MMA issuer (warp 1), two idle warps — shrunk to
   // REG_LO registers; warpgroups 1-2: the epilogue warps 4..11, grown to REG_HI
   // (setmaxnreg: the epilogue keeps accumulator, C and output rows in registers)
@@ -537,63 +531,78 @@ __device__ __forceinline__ void store_w(const GemmProblem& P, int c, int wn, int
   }
 }
 
-template <class Cfg>
-__device__ __forceinline__ void epi_chain(const GemmProblem& P, int i, int tm, const float (&d)[32], double* dred,
-                                          int e, int lane, int et, int h) {
-  // Row i of the pass output; the two warps sharing a TMEM lane quarter split the p
-  // sketch rows c (h = 0: c < p/2, h = 1: the rest; h = 2: all, chaint.cuh).  Every load is issued before the
-  // first store (the output and keep buffers would otherwise serialise them).
+// Everything the per-row chain epilogue reads besides the accumulator, loaded by
+// chain_prefetch before the accumulator is ready (the loads then overlap the MMAs /
+// the partial exchange; the values are consumed by epi_chain).  P is a local copy:
+// read through a reference every field would be reloaded after each store.
+struct ChainPre {
+  GemmProblem P;
+  float rii, gii;     // pass 1: R_ii and G_ii
+  float v[32];        // pass 1: S[c][i] (c < 8); last pass: kept columns kv[slot][c]
+};
+
+template <class Cfg, int PASS>
+__device__ __forceinline__ void chain_prefetch(const GemmProblem& Pin, int i, int h, ChainPre& pre) {
+  pre.P = Pin;
+  const GemmProblem& P = pre.P;
+  const int p = P.p;
+  const int c0 = h == 1 ? (p + 1) / 2 : 0;
+  const int c1 = h == 0 ? (p + 1) / 2 : p;
+  const bool valid = i < P.M;
+#pragma unroll
+  for (int u = 0; u < 32; ++u) pre.v[u] = 0.f;
+  pre.rii = pre.gii = 0.f;
+  if (!valid) return;
+  if constexpr (PASS == CH2_P1 || PASS == CH1_P1) {
+    if constexpr (Cfg::KIND == 0) pre.rii = __bfloat162float(static_cast<const __nv_bfloat16*>(P.Rg)[(long long)i * P.ldr + i]);
+    else pre.rii = static_cast<const float*>(P.Rg)[(long long)i * P.ldr + i] +
+                   (P.Rg_lo ? static_cast<const float*>(P.Rg_lo)[(long long)i * P.ldr + i] : 0.f);
+    pre.gii = P.gdiag[i];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) pre.v[c] = (c >= c0 && c < c1) ? __ldg(P.S + (long long)c * P.ldS + i) : 0.f;
+  } else if constexpr (PASS == CH2_P5 || PASS == CH1_P3) {
+    const int ns = PASS == CH2_P5 ? 4 : 2;
+    const long long M = P.M;
+#pragma unroll
+    for (int sl = 0; sl < 4; ++sl)
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        pre.v[sl * 8 + c] = (sl < ns && c >= c0 && c < c1) ? __ldcg(P.keep + ((long long)sl * M + i) * p + c) : 0.f;
+  }
+}
+
+template <class Cfg, int PASS>   // one pass code per launch: only its epilogue is compiled in
+__device__ __forceinline__ void epi_chain(const ChainPre& pre, int i, int grp, const float* col, int cs, int lane,
+                                          int h) {
+  const GemmProblem& P = pre.P;
+  // Row i of the pass output: D[c] = col[c * cs] (this thread's column of the staged
+  // accumulator in smem).  The two warps sharing a TMEM lane quarter may split the p
+  // sketch rows c (h = 0: c < p/2, h = 1: the rest; h = 2: all).
   const int p = P.p;
   const int w = P.N / 2;          // columns of this pass's output
   const bool valid = i < P.M;
   const int c0 = h == 1 ? (p + 1) / 2 : 0;       // h = 2: one thread per row, every c
   const int c1 = h == 0 ? (p + 1) / 2 : p;
   double g[6] = {0, 0, 0, 0, 0, 0};
-  // o[c] = d[c] + d[w + c] (hi + lo halves of the pass output); the runtime shifts by w
-  // and p are done by conditional fixed shifts so d / o stay in registers
-  float t[32];
+  // o[c] = D[c] + D[w + c] (hi + lo halves of the pass output), op[c] = o[p + c]
+  float o[8], op[8];
 #pragma unroll
-  for (int u = 0; u < 32; ++u) t[u] = d[u];
-#pragma unroll
-  for (int bit = 16; bit >= 1; bit >>= 1)
-    if (w & bit) {
-#pragma unroll
-      for (int u = 0; u < 32; ++u) t[u] = (u + bit < 32) ? t[u + bit] : 0.f;
-    }
-  float o[16], op[8];
-#pragma unroll
-  for (int c = 0; c < 16; ++c) o[c] = (c < w) ? d[c] + t[c] : 0.f;
-  {
-    float sh[16];
-#pragma unroll
-    for (int c = 0; c < 16; ++c) sh[c] = o[c];
-#pragma unroll
-    for (int bit = 8; bit >= 1; bit >>= 1)
-      if (p & bit) {
-#pragma unroll
-        for (int c = 0; c < 16; ++c) sh[c] = (c + bit < 16) ? sh[c + bit] : 0.f;
-      }
-#pragma unroll
-    for (int c = 0; c < 8; ++c) op[c] = sh[c];   // op[c] = op[c]
+  for (int c = 0; c < 8; ++c) {
+    o[c] = (c < w) ? col[c * cs] + col[(w + c) * cs] : 0.f;
+    op[c] = (p + c < w) ? col[(p + c) * cs] + col[(w + p + c) * cs] : 0.f;
   }
   float* __restrict__ keep = P.keep;
   const long long M = P.M;
-  const int pass = P.pass;
+  constexpr int pass = PASS;
   if (valid) {
-    if (pass == CH2_P1 || pass == CH1_P1) {
-      float rii;
-      if constexpr (Cfg::KIND == 0) rii = __bfloat162float(static_cast<const __nv_bfloat16*>(P.Rg)[(long long)i * P.ldr + i]);
-      else rii = static_cast<const float*>(P.Rg)[(long long)i * P.ldr + i] +
-                 (P.Rg_lo ? static_cast<const float*>(P.Rg_lo)[(long long)i * P.ldr + i] : 0.f);
-      const float gii = P.gdiag[i];
-      float sc[8];
-#pragma unroll
-      for (int c = 0; c < 8; ++c) sc[c] = (c >= c0 && c < c1) ? __ldg(P.S + (long long)c * P.ldS + i) : 0.f;
+    if constexpr (pass == CH2_P1 || pass == CH1_P1) {
+      const float rii = pre.rii, gii = pre.gii;
+      const float* sc = pre.v;
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         if (c < c0 || c >= c1) continue;
         const float qv = gii * sc[c] - (o[c] - rii * sc[c]);   // Q = G S^T, G_ii exact (fp32 from the Gram)
-        if (pass == CH2_P1) {
+        if constexpr (pass == CH2_P1) {
           store_w<Cfg>(P, c, 2 * p, i, o[c]);
           store_w<Cfg>(P, p + c, 2 * p, i, qv);
         } else {
@@ -601,7 +610,7 @@ __device__ __forceinline__ void epi_chain(const GemmProblem& P, int i, int tm, c
           store_w<Cfg>(P, c, p, i, qv);
         }
       }
-    } else if (pass == CH2_P2) {
+    } else if constexpr (pass == CH2_P2) {
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         if (c < c0 || c >= c1) continue;
@@ -609,7 +618,7 @@ __device__ __forceinline__ void epi_chain(const GemmProblem& P, int i, int tm, c
         store_w<Cfg>(P, c, 2 * p, i, o[c]);
         store_w<Cfg>(P, p + c, 2 * p, i, op[c]);
       }
-    } else if (pass == CH2_P3) {
+    } else if constexpr (pass == CH2_P3) {
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         if (c < c0 || c >= c1) continue;
@@ -617,8 +626,8 @@ __device__ __forceinline__ void epi_chain(const GemmProblem& P, int i, int tm, c
         keep[(2 * M + i) * p + c] = op[c];
         store_w<Cfg>(P, c, p, i, op[c]);
       }
-    } else if (pass == CH2_P4 || pass == CH1_P2) {
-      const long long slot = pass == CH2_P4 ? 3 : 1;
+    } else if constexpr (pass == CH2_P4 || pass == CH1_P2) {
+      constexpr long long slot = pass == CH2_P4 ? 3 : 1;
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         if (c < c0 || c >= c1) continue;
@@ -627,18 +636,12 @@ __device__ __forceinline__ void epi_chain(const GemmProblem& P, int i, int tm, c
       }
     } else {
       // CH2_P5 / CH1_P3: inner products <Va, Vb> (fp64 products of widened factors)
-      const int ns = pass == CH2_P5 ? 4 : 2;
-      float kv[4][8];
-#pragma unroll
-      for (int sl = 0; sl < 4; ++sl)
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-          kv[sl][c] = (sl < ns && c >= c0 && c < c1) ? __ldcg(keep + ((long long)sl * M + i) * p + c) : 0.f;
+      const float(&kv)[4][8] = *reinterpret_cast<const float(*)[4][8]>(pre.v);
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         if (c < c0 || c >= c1) continue;
         double v0, v1, v2;
-        if (pass == CH2_P5) {
+        if constexpr (pass == CH2_P5) {
           v0 = 0.25 * (3.0 * (double)kv[0][c] + (double)kv[1][c]);   // 1/4 (3 K2 + K3)
           v1 = -((double)kv[3][c] + 2.0 * (double)kv[2][c]);         // -(L3 + 2 L2)
           v2 = -(double)o[c];                                        // -L4
@@ -652,42 +655,21 @@ __device__ __forceinline__ void epi_chain(const GemmProblem& P, int i, int tm, c
       }
     }
   }
-  if (pass == CH2_P5 || pass == CH1_P3) {
+  if constexpr (pass == CH2_P5 || pass == CH1_P3) {
+    // <Va, Vb> partial of this warp's 32 rows (one aligned row group): a fixed shuffle
+    // tree, written per group — the grouping never depends on the launch (split factor,
+    // batch), so k_alpha's fixed-order sum over groups is reproducible bit for bit
 #pragma unroll
     for (int j = 0; j < 6; ++j) {
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) g[j] += __shfl_xor_sync(0xffffffffu, g[j], off);
     }
-    if (lane == 0)
+    if (lane == 0 && grp >= 0)
 #pragma unroll
-      for (int j = 0; j < 6; ++j) dred[e * 6 + j] = g[j];
-    named_bar_sync(1, 32 * Cfg::EPI_WARPS);
-    if (et == 0)
-#pragma unroll
-      for (int j = 0; j < 6; ++j) {
-        double t = 0.0;
-        for (int x = 0; x < Cfg::EPI_WARPS; ++x) t += dred[x * 6 + j];
-        P.chain_part[tm * 6 + j] = t;
-      }
-    named_bar_sync(1, 32 * Cfg::EPI_WARPS);
+      for (int j = 0; j < 6; ++j) P.chain_part[grp * 6 + j] = g[j];
   }
 }
 
-// K range of a tile: split-K tiles (chain) carry the slice index in the tn field.
-template <class Cfg>
-__device__ __forceinline__ void tile_krange(const GemmProblem& P, int& tn, int& kb_lo, int& kb_hi) {
-  const int nkb = (P.K + Cfg::BK - 1) / Cfg::BK;
-  if (P.mode == EPI_CHAIN) {
-    // slice ks of P.ksplit; slices past the matrix's own factor (launch cluster larger) are empty
-    const int ks = tn;
-    tn = 0;
-    kb_lo = ks < P.ksplit ? ks * nkb / P.ksplit : nkb;
-    kb_hi = ks < P.ksplit ? (ks + 1) * nkb / P.ksplit : nkb;
-  } else {
-    kb_lo = 0;
-    kb_hi = nkb;
-  }
-}
 
 // TMA load of one operand tile (rows = BM or BN along MN, BK along K) into smem.
 template <class Cfg>
@@ -716,10 +698,6 @@ __device__ __forceinline__ uint64_t operand_desc(uint32_t base, int k, int mn_ma
 
 // ---------------------------------------------------------------- the kernel
 
-// Debug timeline of the thin chain GEMM (prism_debug_trace): per pass and CTA,
-// TRACE_W globaltimer stamps; null (the default) disables every stamp.
-__device__ unsigned long long* g_gemm_trace = nullptr;
-constexpr int TRACE_W = 80;
 // Main-GEMM k-block timeline (prism_debug_trace_gemm): for launches whose first problem has
 // epilogue mode g_trace_mode, each CTA's first tile records [0,64) producer issue (after
 // its empty wait), [64,128) MMA full arrival, [128,192) MMA issue done, per k-block.
@@ -739,13 +717,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
   uint64_t* empty = bars + Cfg::STAGES;        // [STAGES]
   uint64_t* tfull = bars + 2 * Cfg::STAGES;    // [2]
   uint64_t* tempty = tfull + 2;                // [2]
-  uint64_t* red_full = tempty + 2;             // chain split-K: partials landed in the leader
-  uint64_t* red_empty = red_full + 1;          // chain split-K: leader consumed this CTA's partial
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(red_empty + 1);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   float* red = reinterpret_cast<float*>(tmem_slot + 4);   // [8] epilogue reduction scratch
-  double* dred = reinterpret_cast<double*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES + 256);   // [8][6]
   float* tbuf = reinterpret_cast<float*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES + 1024);    // [8][32*33]
-  float* redbuf = tbuf;                                                                    // [3][32][128] (chain)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -753,16 +727,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
   const bool leader = rank == 0;
   const int cid = Cfg::CTA2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;   // tile-loop index / stride
   const int ncl = Cfg::CTA2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
-  // chain split-K: the cluster's CTAs take the K slices 0..ksplit-1 of one row tile
-  // (tiles grouped by row tile, grid a multiple of ksplit, so slice == cluster rank)
-  const int ksplit = (Cfg::BN == 32 && L.ksplit > 1) ? L.ksplit : 1;
-  const uint32_t krank = ksplit > 1 ? cluster_ctarank() : 0u;
   const GemmProblem* __restrict__ probs = L.probs;
-  unsigned long long* trace = nullptr;
-  if (Cfg::BN == 32 && g_gemm_trace) trace = g_gemm_trace + ((size_t)L.probs[0].pass * 1024 + blockIdx.x) * TRACE_W;
-  if (trace && threadIdx.x == 0) trace[0] = globaltimer_ns();
   unsigned long long* trace2 = nullptr;
-  if (Cfg::BN != 32 && g_gemm_trace2 && L.probs[0].mode == g_trace_mode) trace2 = g_gemm_trace2 + (size_t)blockIdx.x * TRACE2_W;
+  if (g_gemm_trace2 && L.probs[0].mode == g_trace_mode) trace2 = g_gemm_trace2 + (size_t)blockIdx.x * TRACE2_W;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {
@@ -773,17 +740,14 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], Cfg::CG * Cfg::EPI_WARPS);   // one arrival per epilogue warp (of both CTAs)
     }
-    mbar_init(red_full, 1);                      // leader's expect_tx; the slices complete_tx
-    mbar_init(red_empty, Cfg::EPI_WARPS);        // one arrival per leader epilogue warp
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<Cfg::CG>(tmem_slot, Cfg::TMEM_ALLOC);
   tc_fence_before();
-  if (Cfg::CTA2 || ksplit > 1) cluster_sync_all();
+  if constexpr (Cfg::CTA2) cluster_sync_all();
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  if (trace && threadIdx.x == 0) trace[1] = globaltimer_ns();
 
   // before the predecessor is done: the tile list, problem tables and tensor maps are
   // plan constants, so warm them; then wait for the predecessor's results
@@ -820,8 +784,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
         const GemmProblem& P = probs[code >> 20];
         if (L.done && L.done[P.matrix * L.done_stride]) continue;
         const int tm = (code >> 10) & 1023;
-        int tn = code & 1023, kb_lo, kb_hi;
-        tile_krange<Cfg>(P, tn, kb_lo, kb_hi);
+        const int tn = code & 1023;
+        const int kb_lo = 0, kb_hi = (P.K + Cfg::BK - 1) / Cfg::BK;
         // warm the TMA descriptor cache with this tile's maps (they live in global memory)
         tma_prefetch(P.tmA);
         tma_prefetch(P.tmB);
@@ -846,12 +810,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
             if constexpr (Cfg::LOB)
               load_operand<Cfg>(sB2, P.tmB_lo, &full[stage], bn0, kb * Cfg::BK, Cfg::B_ROWS, P.b_mn);
           }
-          if (trace && kb == kb_lo) trace[2] = globaltimer_ns();
           if (trace2 && t == cid && kb < 64) trace2[kb] = globaltimer_ns();
           if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
         }
       }
-      if (trace) trace[3] = globaltimer_ns();
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (leader CTA of the pair) =====================
@@ -865,8 +827,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
         const uint32_t code = L.tiles[t];
         const GemmProblem& P = probs[code >> 20];
         if (L.done && L.done[P.matrix * L.done_stride]) continue;
-        int tn = code & 1023, kb_lo, kb_hi;
-        tile_krange<Cfg>(P, tn, kb_lo, kb_hi);
+        const int tn = code & 1023;
+        const int kb_lo = 0, kb_hi = (P.K + Cfg::BK - 1) / Cfg::BK;
         // tf32: one TMEM accumulation chunk per PROMO_KB k-blocks, promoted to fp32
         // registers by the epilogue (bounds the truncation of the MMA accumulator add)
         for (int kb0 = kb_lo; kb0 < kb_hi; kb0 += Cfg::PROMO_KB) {
@@ -876,7 +838,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
           const uint32_t dt = tmem_base + acc * Cfg::BN;
           for (int kb = kb0; kb < kb1; ++kb) {
             mbar_wait(&full[stage], phase);
-            if (trace && kb - kb_lo < 64) trace[8 + kb - kb_lo] = globaltimer_ns();
             if (trace2 && t == cid && kb < 64) trace2[64 + kb] = globaltimer_ns();
             if (trace2 && kb == kb_lo && tcount < 8) trace2[192 + 4 * tcount] = globaltimer_ns();
             tc_fence_after();
@@ -906,7 +867,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
         if (trace2 && tcount < 8) trace2[192 + 4 * tcount + 1] = globaltimer_ns();
         ++tcount;
       }
-      if (trace) trace[6] = globaltimer_ns();
     }
     }
   } else {
@@ -922,7 +882,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
     float* tb = tbuf + e * 32 * 33;
     int acc = 0;
     uint32_t acc_phase = 0;
-    uint32_t red_phase = 0;
     int etcount = 0;
     // accumulator release: one arrival per epilogue warp on the leader's tempty barrier
     auto release_acc = [&](uint64_t* bar) {
@@ -938,9 +897,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
       const GemmProblem& P = probs[code >> 20];
       if (L.done && L.done[P.matrix * L.done_stride]) continue;
       const int tm = (code >> 10) & 1023;
-      int tn = code & 1023, kb_lo, kb_hi;
-      const int ks = tn;
-      tile_krange<Cfg>(P, tn, kb_lo, kb_hi);
+      const int tn = code & 1023;
       const int mode = P.mode;
       const bool sym = P.sym != 0;
       const EpiArgs ea{P.out, P.out_lo, P.gdiag, P.ldo, P.M, P.N};
@@ -954,66 +911,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
       const bool needC = (mode == EPI_POLY || mode == EPI_APPLY);
       float sumsq = 0.f;
 
-      if constexpr (Cfg::BN == 32) {
-        // thin chain GEMM: one 32-column chunk, read by both warps of each lane quarter
-        float d[32];
-#pragma unroll
-        for (int u = 0; u < 32; ++u) d[u] = 0.f;
-        for (int kb0 = kb_lo; kb0 < kb_hi; kb0 += Cfg::PROMO_KB) {
-          mbar_wait(&tfull[acc], acc_phase);
-          if (trace && et == 0) trace[4] = globaltimer_ns();
-          tc_fence_after();
-          uint32_t r[32];
-          tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * Cfg::BN, r);
-          tmem_ld_wait();
-#pragma unroll
-          for (int u = 0; u < 32; ++u) d[u] += __uint_as_float(r[u]);
-          release_acc(&tempty[acc]);
-          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-        }
-        if (ksplit > 1) {
-          // split-K over the cluster: each non-leader st.async's its fp32 128 x 32 partial
-          // into slot (rank-1) of the leader's smem (row-major, 16-B chunks XOR-swizzled by
-          // row: conflict-free), completing bytes on the leader's red_full; the leader sums
-          // the slices in fixed order (deterministic).  red_empty hands the slot back.
-          const int row = q * 32 + lane;
-          if (krank != 0) {
-            mbar_wait(red_empty, red_phase ^ 1);
-            float* slot = redbuf + (krank - 1) * 32 * 128 + row * 32;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const int jj = h * 4 + j;   // this warp's half of the 8 chunks
-              float4 v;
-              if (h == 0) v = make_float4(d[4 * j], d[4 * j + 1], d[4 * j + 2], d[4 * j + 3]);
-              else v = make_float4(d[16 + 4 * j], d[17 + 4 * j], d[18 + 4 * j], d[19 + 4 * j]);
-              st_async_v4(slot + ((jj ^ (row & 7)) << 2), red_full, 0u, v);
-            }
-            red_phase ^= 1;
-            if (trace && et == 0) trace[74] = globaltimer_ns();
-            continue;
-          }
-          if (et == 0) mbar_arrive_expect_tx(red_full, (uint32_t)(ksplit - 1) * 32 * 128 * 4);
-          mbar_wait(red_full, red_phase);
-          if (trace && et == 0) trace[75] = globaltimer_ns();
-          for (int x = 0; x < ksplit - 1; ++x) {
-            const float* slot = redbuf + x * 32 * 128 + row * 32;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const float4 v = *reinterpret_cast<const float4*>(slot + ((j ^ (row & 7)) << 2));
-              d[4 * j] += v.x; d[4 * j + 1] += v.y; d[4 * j + 2] += v.z; d[4 * j + 3] += v.w;
-            }
-          }
-          red_phase ^= 1;
-        }
-        epi_chain<Cfg>(P, i, tm, d, dred, e, lane, et, h);
-        if (ksplit > 1 && krank == 0) {
-          // slots consumed (their values were summed above): hand them back to the slices
-          __syncwarp();
-          if (lane == 0)
-            for (int x = 1; x < ksplit; ++x) mbar_arrive_release_cluster(red_empty, (uint32_t)x);
-        }
-        if (trace && et == 0) trace[5] = globaltimer_ns();
-      } else if constexpr (Cfg::KIND == 0) {
+      if constexpr (Cfg::KIND == 0) {
         // bf16: one TMEM accumulator per tile; this warp consumes its 32-column chunks
         // while the raw C row segment of the next chunk is in flight
         // C blocks: coalesced when the warp's 32 x 32 block is in bounds, else per-row
@@ -1120,7 +1018,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
 
   }
   tc_fence_before();
-  if (Cfg::CTA2 || ksplit > 1) cluster_sync_all();   // no CTA leaves while a peer may still touch its smem
+  if constexpr (Cfg::CTA2) cluster_sync_all();   // no CTA leaves while its peer may still touch its smem
   else __syncthreads();
   if (warp == 1) {
     tc_fence_after();

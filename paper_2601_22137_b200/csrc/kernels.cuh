@@ -589,17 +589,25 @@ __global__ void __launch_bounds__(256) k_alpha(SolveParams P) {
   }
   __syncthreads();
   if (s_stop) return;
+  if (threadIdx.x >= 32) return;   // warp 0 fits alpha
   double a;
   if (!do_fit) {
     a = (k < P.warmup) ? P.ahi : P.ataylor;
   } else {
-    // <Va, Vb> from the chain GEMM's per-tile partials (fixed order, R17)
-    double g00 = 0, g01 = 0, g02 = 0, g11 = 0, g12 = 0, g22 = 0;
-    for (int t = 0; t < D.chain_tiles; ++t) {
+    // <Va, Vb> from the chain's per-32-row-group partials (R17): lane l
+    // sums groups l, l+32, ... in order, then a fixed xor tree — reproducible bit for bit
+    double g[6] = {0, 0, 0, 0, 0, 0};
+    for (int t = threadIdx.x; t < D.chain_tiles; t += 32) {
       const double* cp = D.chain_part + 6 * t;
-      g00 += cp[0]; g01 += cp[1]; g02 += cp[2]; g11 += cp[3]; g12 += cp[4]; g22 += cp[5];
+#pragma unroll
+      for (int j = 0; j < 6; ++j) g[j] += cp[j];
     }
-    double c[5] = {g00, 2.0 * g01, g11 + 2.0 * g02, 2.0 * g12, g22};
+#pragma unroll
+    for (int j = 0; j < 6; ++j) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) g[j] += __shfl_xor_sync(0xffffffffu, g[j], o);
+    }
+    double c[5] = {g[0], 2.0 * g[1], g[3] + 2.0 * g[2], 2.0 * g[4], g[5]};
     a = (k < P.warmup) ? P.ahi : argmin_quartic(c, P.alo, P.ahi, P.ataylor);
   }
   if (threadIdx.x == 0) {

@@ -160,32 +160,43 @@ cudaError_t launch_gemm_cfg(const GemmLaunch& L, cudaStream_t st) {
   }
 }
 
-template <class Cfg>
-cudaError_t launch_chaint_cfg(const GemmLaunch& L, cudaStream_t st) {
+template <class Cfg, int PASS>
+cudaError_t launch_chaint_pass(const GemmLaunch& L, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(prism_chaint_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(prism_chaint_kernel<Cfg, PASS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          Cfg::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   if (L.ntiles <= 0) return cudaSuccess;
-  const int grid = std::min(L.ntiles, num_sms());
-  return launch_k(prism_chaint_kernel<Cfg>, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM_BYTES, st, 1, L);
+  const int C = std::max(1, L.ksplit);   // split chains: clusters of C CTAs (reduce-scatter)
+  const int grid = std::min(L.ntiles, num_sms() / C * C);
+  return launch_k(prism_chaint_kernel<Cfg, PASS>, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM_BYTES, st, C, L);
 }
 
-// Transposed chain pass (chaint.cuh) for the matrices that do not split K.
-cudaError_t launch_chaint(int precision, const GemmLaunch& L, cudaStream_t st) {
-  if (precision == PRISM_BF16) return launch_chaint_cfg<ChainTCfg<0, false>>(L, st);
-  if (precision == PRISM_FP32) return launch_chaint_cfg<ChainTCfg<1, true>>(L, st);
-  return launch_chaint_cfg<ChainTCfg<1, false>>(L, st);
+// one kernel per pass code (each carries only its own epilogue: the code of a chain
+// pass runs once per CTA per launch, from a cold instruction cache)
+template <class Cfg>
+cudaError_t launch_chaint_cfg(int pass, const GemmLaunch& L, cudaStream_t st) {
+  switch (pass) {
+    case CH2_P1: return launch_chaint_pass<Cfg, CH2_P1>(L, st);
+    case CH2_P2: return launch_chaint_pass<Cfg, CH2_P2>(L, st);
+    case CH2_P3: return launch_chaint_pass<Cfg, CH2_P3>(L, st);
+    case CH2_P4: return launch_chaint_pass<Cfg, CH2_P4>(L, st);
+    case CH2_P5: return launch_chaint_pass<Cfg, CH2_P5>(L, st);
+    case CH1_P1: return launch_chaint_pass<Cfg, CH1_P1>(L, st);
+    case CH1_P2: return launch_chaint_pass<Cfg, CH1_P2>(L, st);
+    default: return launch_chaint_pass<Cfg, CH1_P3>(L, st);
+  }
 }
 
-cudaError_t launch_chain(int precision, const GemmLaunch& L, cudaStream_t st) {
-  if (precision == PRISM_BF16) return launch_gemm_cfg<GemmCfg<0, false, 32>>(L, st);
-  if (precision == PRISM_FP32) return launch_gemm_cfg<GemmCfg<1, true, 32>>(L, st);
-  return launch_gemm_cfg<GemmCfg<1, false, 32>>(L, st);
+cudaError_t launch_chaint(int precision, int pass, const GemmLaunch& L, cudaStream_t st) {
+  if (precision == PRISM_BF16) return launch_chaint_cfg<ChainTCfg<0, false>>(pass, L, st);
+  if (precision == PRISM_FP32) return launch_chaint_cfg<ChainTCfg<1, true>>(pass, L, st);
+  return launch_chaint_cfg<ChainTCfg<1, false>>(pass, L, st);
 }
+
 
 // Main GEMM variant: CTA pairs (cta_group::2, 256 x BN tiles) by default; PRISM_GEMM_1CTA=1
 // selects single-CTA 128 x BN tiles (A/B comparison knob for profiling).
@@ -250,9 +261,9 @@ struct Plan {
   size_t meta_off = 0, meta_bytes = 0;
   std::unique_ptr<uint8_t, PinnedDeleter> blob;
   SolveParams params{};
-  LaunchDesc gram[2], square, apply[2], chain[5], chaint[5], gram32[2];   // chain: N = 32 form; chaint: transposed
+  LaunchDesc gram[2], square, apply[2], chaint[5], gram32[2];
   int n_chain = 0;
-  int chain_ksplit = 1;   // cluster size of the chain launches (split-K)
+  int chain_ksplit = 1;   // cluster size of the chain launches (split-K; 1, 2 or 4)
   bool has_square = false;
   int max_s = 0, max_rows = 0, max_cols = 0, max_m = 0, max_n = 0;
 };
@@ -306,10 +317,10 @@ void add_tiles(LaunchDesc& L, int prob, int M, int N, int BN, bool sym) {
     }
 }
 
-// Chain split-K factor of one matrix: a function of its size s alone (never of the
-// batch), so a matrix's bits do not depend on what it is batched with (or on the
-// rank it lands on).  Each slice keeps >= 8 k-blocks.
-int chain_ks(int s) { return std::max(1, std::min(4, s / 512)); }
+// Chain split-K factor of one matrix (cluster of CTAs sharing a 256-row tile of R): a
+// function of its size s alone (never of the batch), so a matrix's bits do not depend on
+// what it is batched with (or on the rank it lands on).  Each slice keeps >= 8 k-blocks.
+int chain_ks(int s) { return s < 1024 ? 1 : s < 2048 ? 2 : 4; }   // clusters of 8 do not all co-schedule
 
 void sort_tiles_by_cost(LaunchDesc& L) {
   std::stable_sort(L.tiles.begin(), L.tiles.end(), [&](uint32_t a, uint32_t b) {
@@ -391,11 +402,9 @@ prism_status build_plan(const Request& r, Plan& P) {
     D.W[0] = bump.take((size_t)esz * 4 * p * ldS);
     D.W[1] = bump.take((size_t)esz * 4 * p * ldS);
     D.keep = reinterpret_cast<float*>(bump.take(sizeof(float) * 4 * (size_t)s * p));
-    // chain form: transposed (256-row tiles of R, chaint.cuh) unless the
-    // matrix splits K over a cluster (N = 32 form, 128-row tiles)
-    const bool chain_t = chain_ks(s) == 1;
-    D.chain_tiles = chain_t ? (s + 255) / 256 : D.tiles_m;
-    D.chain_part = reinterpret_cast<double*>(bump.take(sizeof(double) * 6 * D.tiles_m));
+    // <Va,Vb> partials of the chain: one per 32-row group of R (chaint.cuh, epi_chain)
+    D.chain_tiles = (s + 31) / 32;
+    D.chain_part = reinterpret_cast<double*>(bump.take(sizeof(double) * 6 * D.chain_tiles));
     P.max_s = std::max(P.max_s, s);
     P.max_rows = std::max(P.max_rows, s);
     P.max_cols = std::max(P.max_cols, L);
@@ -531,24 +540,16 @@ prism_status build_plan(const Request& r, Plan& P) {
         c.p.p = p;
         c.p.tiles_n = 1;
         c.p.ksplit = chain_ks(s);
-        if (chain_t) {
-          // A = W (rows c, K-major [c][ldS]; box 32 rows, OOB rows zero), B = R (256-row box)
-          maps.push_back(MapSpec{D.W[j % 2], N, s, D.ldS, esz, OP_BK, 32, BK});
-          c.mapA = (int)maps.size();
-          maps.push_back(MapSpec{D.R, s, s, ldr, esz, OP_BK, 256, BK});
-          c.mapB = (int)maps.size();
-          if (split) {
-            maps.push_back(MapSpec{D.R_lo, s, s, ldr, esz, OP_BK, 256, BK});
-            c.mapB_lo = (int)maps.size();
-          }
-          P.chaint[j].probs.push_back(c);
-        } else {
-          c.mapA = add_map(D.R, s, s, ldr, OP_A);
-          if (split) c.mapA_lo = add_map(D.R_lo, s, s, ldr, OP_A);
-          maps.push_back(MapSpec{D.W[j % 2], N, s, D.ldS, esz, OP_BK, 32, BK});
-          c.mapB = (int)maps.size();
-          P.chain[j].probs.push_back(c);
+        // A = W (rows c, K-major [c][ldS]; box 32 rows, OOB rows zero), B = R (256-row box)
+        maps.push_back(MapSpec{D.W[j % 2], N, s, D.ldS, esz, OP_BK, 32, BK});
+        c.mapA = (int)maps.size();
+        maps.push_back(MapSpec{D.R, s, s, ldr, esz, OP_BK, 256, BK});
+        c.mapB = (int)maps.size();
+        if (split) {
+          maps.push_back(MapSpec{D.R_lo, s, s, ldr, esz, OP_BK, 256, BK});
+          c.mapB_lo = (int)maps.size();
         }
+        P.chaint[j].probs.push_back(c);
       }
     }
   }
@@ -568,29 +569,19 @@ prism_status build_plan(const Request& r, Plan& P) {
     if (r.rowblock) finish(P.gram32[t], false);
   }
   if (P.has_square) finish(P.square, !polar_k);
-  // chain split-K (DSMEM cluster reduction, gemm.cuh): the chain streams R through only
-  // s/128 row tiles per matrix and each SM's TMA pulls ~35 B/cycle, so large matrices
-  // split every row tile over a cluster of CTAs (measured B200, s = 4096: 19.5 us
-  // mainloop with 32 CTAs, 4.7 us with 128)
-  // The launch's cluster size is the largest factor; a matrix with a smaller one leaves
-  // its trailing slices empty (exact zeros in the leader's fixed-order sum).
+  // chain tiles (chaint.cuh): 256-row tiles of R, each split over a cluster of C CTAs,
+  // C = the largest factor of the launch's matrices (smaller factors: empty slices).
+  // Tiles of one row tile are contiguous and C-aligned, so slice == cluster rank.
   P.chain_ksplit = 1;
   if (P.n_chain)
-    for (const HostProblem& hp : P.chain[0].probs) P.chain_ksplit = std::max(P.chain_ksplit, hp.p.ksplit);
+    for (const HostProblem& hp : P.chaint[0].probs) P.chain_ksplit = std::max(P.chain_ksplit, hp.p.ksplit);
   for (int j = 0; j < P.n_chain; ++j) {
-    LaunchDesc& L = P.chain[j];
-    L.tiles.clear();
-    for (int q = 0; q < (int)L.probs.size(); ++q) {
-      const GemmProblem& gq = L.probs[q].p;
-      for (int tm = 0; tm < (gq.M + 127) / 128; ++tm)
-        for (int ks = 0; ks < P.chain_ksplit; ++ks)
-          L.tiles.push_back(((uint32_t)q << 20) | ((uint32_t)tm << 10) | (uint32_t)ks);
-    }
-    sort_tiles_by_cost(L);
     LaunchDesc& T = P.chaint[j];
     T.tiles.clear();
     for (int q = 0; q < (int)T.probs.size(); ++q)
-      for (int tn = 0; tn < (T.probs[q].p.M + 255) / 256; ++tn) T.tiles.push_back(((uint32_t)q << 20) | ((uint32_t)tn << 10));
+      for (int tn = 0; tn < (T.probs[q].p.M + 255) / 256; ++tn)
+        for (int ks = 0; ks < P.chain_ksplit; ++ks)
+          T.tiles.push_back(((uint32_t)q << 20) | ((uint32_t)tn << 10) | (uint32_t)ks);
     sort_tiles_by_cost(T);
   }
   if ((int)P.apply[0].probs.size() >= 4096) return fail(PRISM_ERR_UNSUPPORTED, "batch too large (max 2047 sqrt / 4095 polar)");
@@ -613,9 +604,8 @@ prism_status build_plan(const Request& r, Plan& P) {
   off += sizeof(int) * (B + 1);
   const size_t ooff_off = off;
   off += sizeof(int) * (B + 1);
-  LaunchDesc* all[17] = {&P.gram[0],  &P.gram[1],  &P.apply[0], &P.apply[1], &P.square,    &P.chain[0],
-                         &P.chain[1], &P.chain[2], &P.chain[3], &P.chain[4], &P.chaint[0], &P.chaint[1],
-                         &P.chaint[2], &P.chaint[3], &P.chaint[4], &P.gram32[0], &P.gram32[1]};
+  LaunchDesc* all[12] = {&P.gram[0],   &P.gram[1],   &P.apply[0],  &P.apply[1],  &P.square,     &P.chaint[0],
+                         &P.chaint[1], &P.chaint[2], &P.chaint[3], &P.chaint[4], &P.gram32[0], &P.gram32[1]};
   for (LaunchDesc* L : all) {
     off = align_up(off, 128);
     L->probs_off = off;
@@ -695,6 +685,11 @@ prism_status build_plan(const Request& r, Plan& P) {
   return PRISM_OK;
 }
 
+// pass code of chain launch j (all problems of one chain launch share it)
+int chain_pass(const Plan& P, int j) {
+  return P.chaint[j].probs.empty() ? CH2_P1 : P.chaint[j].probs[0].p.pass;
+}
+
 GemmLaunch make_launch(const Plan& P, const LaunchDesc& L, const LaunchDesc* odd, char* ws, int lo, int hi) {
   GemmLaunch g{};
   g.ksplit = (!L.probs.empty() && L.probs[0].p.mode == EPI_CHAIN) ? P.chain_ksplit : 1;
@@ -721,8 +716,7 @@ void ensure_attrs() {
   z.ntiles = 0;
   for (int prec = 0; prec < 3; ++prec) {
     launch_gemm(prec, z, 0);
-    launch_chain(prec, z, 0);
-    launch_chaint(prec, z, 0);
+    for (int pass = CH2_P1; pass <= CH1_P3; ++pass) launch_chaint(prec, pass, z, 0);
   }
 }
 
@@ -934,13 +928,9 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
   const GemmLaunch g_gram = make_launch(*P, P->gram[0], &P->gram[1], r.ws, 0, M + 1);
   const GemmLaunch g_apply = make_launch(*P, P->apply[0], &P->apply[1], r.ws, 0, M);
   const GemmLaunch g_sq = make_launch(*P, P->square, nullptr, r.ws, 0, M);
-  GemmLaunch g_chain[5], g_chaint[5];
-  int n_chain_launches = 0;
-  for (int j = 0; j < P->n_chain; ++j) {
-    g_chain[j] = make_launch(*P, P->chain[j], nullptr, r.ws, r.o.warmup_iters, M);
-    g_chaint[j] = make_launch(*P, P->chaint[j], nullptr, r.ws, r.o.warmup_iters, M);
-    n_chain_launches += (g_chain[j].ntiles > 0) + (g_chaint[j].ntiles > 0);
-  }
+  GemmLaunch g_chaint[5];
+  for (int j = 0; j < P->n_chain; ++j) g_chaint[j] = make_launch(*P, P->chaint[j], nullptr, r.ws, r.o.warmup_iters, M);
+  const int n_chain_launches = P->n_chain;
   const bool sketched = r.o.fit == PRISM_FIT_SKETCHED;
   const int p = S.p;
   // one iteration k (k read on the device): R_k, stop test, S_k, chain, alpha_k, P, X_{k+1}
@@ -952,10 +942,7 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
     if (sketched) {
       KindTimer t(h, s2, 3, timed ? 1 + n_chain_launches : 0);
       PRISM_CK(launch_k(k_sketch, dim3((p * P->max_s / 2 + 256) / 256, B), dim3(256), 0, s2, 1, S));
-      for (int j = 0; j < P->n_chain; ++j) {
-        PRISM_CK(launch_chaint(prec, g_chaint[j], s2));
-        PRISM_CK(launch_chain(prec, g_chain[j], s2));
-      }
+      for (int j = 0; j < P->n_chain; ++j) PRISM_CK(launch_chaint(prec, chain_pass(*P, j), g_chaint[j], s2));
     }
     {
       KindTimer t(h, s2, 4, timed ? 1 : 0);
@@ -1414,8 +1401,8 @@ prism_status prism_rowblock_update(prism_handle h, int k, const float* G, int32_
   if (g_rb.fit == PRISM_FIT_SKETCHED) {
     PRISM_CK(launch_k(k_sketch, dim3((S.p * n / 2 + 256) / 256, 1), dim3(256), 0, st, 1, S));
     for (int j = 0; j < P->n_chain; ++j) {
-      PRISM_CK(launch_chaint(prec, make_launch(*P, P->chaint[j], nullptr, g_rb.ws, g_rb.warmup, M), st));
-      PRISM_CK(launch_chain(prec, make_launch(*P, P->chain[j], nullptr, g_rb.ws, g_rb.warmup, M), st));
+      PRISM_CK(launch_chaint(prec, chain_pass(*P, j), make_launch(*P, P->chaint[j], nullptr, g_rb.ws, g_rb.warmup, M),
+                             st));
     }
   }
   PRISM_CK(launch_k(k_alpha, dim3(1), dim3(256), 0, st, 1, S));
@@ -1545,8 +1532,9 @@ prism_status prism_debug_gemm(prism_handle h, int precision, int b_mn, int mode,
   return PRISM_OK;
 }
 
-prism_status prism_debug_trace(unsigned long long* buf_dev) {
-  return cudaMemcpyToSymbol(g_gemm_trace, &buf_dev, sizeof(buf_dev)) == cudaSuccess ? PRISM_OK : PRISM_ERR_CUDA;
+
+prism_status prism_debug_trace_chain(unsigned long long* buf_dev) {
+  return cudaMemcpyToSymbol(g_chain_trace, &buf_dev, sizeof(buf_dev)) == cudaSuccess ? PRISM_OK : PRISM_ERR_CUDA;
 }
 
 prism_status prism_debug_trace_gemm(unsigned long long* buf_dev, int mode) {

@@ -1,5 +1,4 @@
-"""Per-CTA timeline of the thin chain GEMM passes (prism_debug_trace) for one bench
-workload: entry, setup done, first/last TMA issue, MMA k-block arrivals, epilogue."""
+"""Per-CTA timeline of the chain passes (prism_debug_trace_chain) for one bench workload."""
 import argparse
 import ctypes
 import os
@@ -24,28 +23,23 @@ h = P.Handle()
 run = (lambda: P.polar(mats, handle=h, **opts)) if kind == "polar" else (lambda: P.sqrt_invsqrt(mats, handle=h, **opts))
 run()
 torch.cuda.synchronize()
-buf = torch.zeros(5 * 1024 * 80, dtype=torch.int64, device="cuda")
-B.check(B.lib().prism_debug_trace(ctypes.c_void_p(buf.data_ptr())), "trace")
+buf = torch.zeros(8 * 1024 * 16, dtype=torch.int64, device="cuda")
+B.check(B.lib().prism_debug_trace_chain(ctypes.c_void_p(buf.data_ptr())), "trace")
 run()
 torch.cuda.synchronize()
-B.check(B.lib().prism_debug_trace(None), "trace")
-T = buf.view(5, 1024, 80).cpu().numpy().astype(np.float64)
-for p in range(5):
+B.check(B.lib().prism_debug_trace_chain(None), "trace")
+T = buf.view(8, 1024, 16).cpu().numpy().astype(np.float64)
+names = ["entry", "setup", "pred done", "tma first", "mma done", "acc ready", "sent", "received", "epi done", "epi start"]
+for p in range(8):
     blk = T[p]
     used = blk[:, 0] > 0
     if not used.any():
         continue
     b = blk[used]
     t0 = b[:, 0].min()
-    rel = lambda c: (b[:, c] - t0) / 1000.0
-    print(f"pass {p}: CTAs {used.sum()}  kernel span {(b[:, 5].max() - t0) / 1000:.2f} us")
-    for c, nm in [(0, "entry"), (1, "setup"), (2, "tma first"), (3, "tma last"), (6, "mma done"), (4, "epi tfull"), (5, "epi end"), (74, "part sent"), (75, "part recv")]:
+    print(f"pass code {p}: CTAs {used.sum()}  span {(b[:, :10].max() - t0) / 1e3:.2f} us")
+    for c, nm in enumerate(names):
         sel = b[:, c] > 0
-        if not sel.any():
-            continue
-        v = (b[sel, c] - t0) / 1000.0
-        print(f"   {nm:10s} min {v.min():7.2f} med {np.median(v):7.2f} max {v.max():7.2f}")
-    kb = (b[:, 8:72] - t0) / 1000.0
-    nkb = int((b[0, 8:72] > 0).sum())
-    med = np.median(kb[:, :nkb], axis=0)
-    print("   mma full-arrival (median over CTAs) every 4th kb:", " ".join(f"{x:.2f}" for x in med[::4]))
+        if sel.any():
+            v = (b[sel, c] - t0) / 1e3
+            print(f"   {nm:10s} min {v.min():7.2f} med {np.median(v):7.2f} max {v.max():7.2f}")
