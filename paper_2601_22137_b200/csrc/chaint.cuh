@@ -109,14 +109,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
   const uint32_t tmem_base = *tmem_slot;
   if (tr && threadIdx.x == 0) tr[1] = globaltimer_ns();
 
-  if (threadIdx.x == 0 && (int)blockIdx.x < L.ntiles) {
-    const uint32_t code = __ldg(L.tiles + blockIdx.x);
-    tma_prefetch(L.probs[code >> 20].tmA);
-    tma_prefetch(L.probs[code >> 20].tmB);
-  }
-  griddep_launch();
-  griddep_wait();
-  if (tr && threadIdx.x == 0) tr[2] = globaltimer_ns();
+  // Before the predecessor (the previous pass) completes, everything this launch reads
+  // except W is already final: the iteration counter, the done flags and R were written
+  // at least two launches back, and every kernel of the solve calls launch_dependents only
+  // after its own griddepcontrol.wait (so kernels two launches back have completed).  The
+  // producer therefore stages the R half of its first stages now and adds W after the wait.
   const GemmProblem* __restrict__ probs = L.probs;
   bool run = true;
   if (L.iter) {
@@ -124,6 +121,28 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
     run = k >= L.iter_lo && k < L.iter_hi;
     if (L.probs_odd && (k & 1)) probs = L.probs_odd;
   }
+  int pre_n = 0;   // producer: leading k-blocks of its first tile whose R is in flight
+  if (run && warp == 0 && lane == 0 && (int)blockIdx.x < L.ntiles) {
+    const uint32_t code = L.tiles[blockIdx.x];
+    const GemmProblem& P = probs[code >> 20];
+    tma_prefetch(P.tmA);
+    tma_prefetch(P.tmB);
+    if (!(L.done && L.done[P.matrix * L.done_stride])) {
+      const int n0 = ((code >> 10) & 1023) * Cfg::BN;
+      int kb_lo, kb_hi;
+      chain_krange(P.K, Cfg::BK, P.ksplit, (int)(code & 1023), kb_lo, kb_hi);
+      pre_n = min(Cfg::STAGES, kb_hi - kb_lo);
+      for (int j = 0; j < pre_n; ++j) {
+        uint8_t* sB = stage_base + j * Cfg::STAGE_BYTES + Cfg::A_BYTES;
+        mbar_arrive_expect_tx(&full[j], Cfg::STAGE_BYTES);
+        tma_load_2d(sB, P.tmB, &full[j], (kb_lo + j) * Cfg::BK, n0);
+        if constexpr (Cfg::SPLIT) tma_load_2d(sB + Cfg::B_BYTES, P.tmB_lo, &full[j], (kb_lo + j) * Cfg::BK, n0);
+      }
+    }
+  }
+  griddep_wait();
+  griddep_launch();
+  if (tr && threadIdx.x == 0) tr[2] = globaltimer_ns();
 
   if (warp < 4) {
     setmaxnreg_dec<Cfg::REG_LO>();
@@ -144,10 +163,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sA = stage_base + stage * Cfg::STAGE_BYTES;
           uint8_t* sB = sA + Cfg::A_BYTES;
-          mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+          const bool staged = t == (int)blockIdx.x && kb - kb_lo < pre_n;   // R already in flight
+          if (!staged) mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
           tma_load_2d(sA, P.tmA, &full[stage], kb * Cfg::BK, 0);    // W rows 0..31 (OOB rows zero)
-          tma_load_2d(sB, P.tmB, &full[stage], kb * Cfg::BK, n0);   // R rows n0 .. n0+255
-          if constexpr (Cfg::SPLIT) tma_load_2d(sB + Cfg::B_BYTES, P.tmB_lo, &full[stage], kb * Cfg::BK, n0);
+          if (!staged) {
+            tma_load_2d(sB, P.tmB, &full[stage], kb * Cfg::BK, n0);   // R rows n0 .. n0+255
+            if constexpr (Cfg::SPLIT) tma_load_2d(sB + Cfg::B_BYTES, P.tmB_lo, &full[stage], kb * Cfg::BK, n0);
+          }
           if (tr && kb == kb_lo) tr[3] = globaltimer_ns();
           if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
         }

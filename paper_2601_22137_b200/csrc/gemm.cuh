@@ -760,8 +760,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
       tma_prefetch(L.probs_odd[code >> 20].tmB);
     }
   }
-  griddep_launch();
+  // wait, then let dependents launch: a launch's predecessor-of-predecessor is then always
+  // complete, which the chain kernel relies on for reads before its own wait (chaint.cuh)
   griddep_wait();
+  griddep_launch();
   // device-side loop control (CUDA-graph WHILE body): uniform skip / parity select
   bool run = true;
   if (L.iter) {

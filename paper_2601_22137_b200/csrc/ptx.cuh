@@ -25,7 +25,9 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 // ---------------------------------------------------------------- programmatic dependent launch
 // Every kernel of the solve is launched with programmatic stream serialisation: it may
 // start while its predecessor drains, runs its prologue, and waits here before touching
-// anything a predecessor wrote; launch_dependents lets the successor start early.
+// anything its predecessor wrote; launch_dependents (always issued after the kernel's own
+// wait) lets the successor start early.  Hence when a kernel starts, every launch two or
+// more back has completed: data written there may be read before the wait.
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
