@@ -42,6 +42,8 @@ struct GemmProblem {
   const CUtensorMap* tmB;
   const CUtensorMap* tmA_lo;
   const CUtensorMap* tmB_lo;
+  const CUtensorMap* tmC;   // bf16 epilogue: 32 x 32 blocks of C (TMA load) and of out (TMA store)
+  const CUtensorMap* tmO;
   void* out;
   void* out_lo;
   const void* C;
@@ -112,8 +114,11 @@ struct GemmCfg {
   static constexpr int A_BYTES = BM * BK * ESZ;
   static constexpr int B_BYTES = B_ROWS * BK * ESZ;
   static constexpr int STAGE_BYTES = (SPLIT ? 2 * A_BYTES : A_BYTES) + (LOB ? 2 * B_BYTES : B_BYTES);
-  static constexpr int TB_BYTES = 8 * 32 * 33 * 4;   // per-epilogue-warp staging / transpose buffers
-  static constexpr int STAGES_RAW = (192 * 1024) / STAGE_BYTES;
+  static constexpr int TB_BYTES = 8 * 32 * 33 * 4;   // tf32: per-epilogue-warp staging / transpose buffers
+  // bf16: per epilogue warp two C blocks and two output blocks (32 x 32 bf16, TMA-swizzled)
+  static constexpr int EPI_BYTES = KIND == 0 ? 8 * 4 * 2048 : TB_BYTES;
+  static constexpr int STAGES_RAW =
+      KIND == 0 ? (227 * 1024 - 2048 - EPI_BYTES) / STAGE_BYTES : (192 * 1024) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int TMEM_COLS = 2 * BN;
   static constexpr int AE = 128 / ESZ;           // elements per 128-B atom along MN (MN-major)
@@ -126,7 +131,7 @@ struct GemmCfg {
   static constexpr int EPI_WARPS = 8;   // two per TMEM lane quarter, each owning half the columns
   static constexpr int NCH = BN / 32;   // 32-column chunks per tile
   static constexpr int CH_PER = NCH >= 2 ? NCH / 2 : 1;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers, scratch*/ + TB_BYTES;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers, scratch*/ + EPI_BYTES;
   // warpgroup 0: TMA producer (warp 0), MMA issuer (warp 1), two idle warps — shrunk to
   // REG_LO registers; warpgroups 1-2: the epilogue warps 4..11, grown to REG_HI
   // (setmaxnreg: the epilogue keeps accumulator, C and output rows in registers)
@@ -516,6 +521,89 @@ __device__ __forceinline__ void epi_segment(const EpiArgs& P, int mode, bool sym
   }
 }
 
+// bf16 fused epilogue for one 32 x 32 block through TMA: rows i0 + lane (one row per
+// lane), columns [j0, j0 + 32), accumulators d[] of D = A·B and (POLY / APPLY) the C
+// row c[].  The block is staged as bf16 rows in ob (64-B swizzle = the TMA box layout)
+// and stored by lane 0 (TMA clips rows >= M / columns >= N).  Symmetric outputs: the
+// upper triangle of blocks is computed; an off-diagonal block is also stored transposed
+// (ldmatrix.trans / stmatrix into ob2), a diagonal block is stored whole (own values on /
+// above the diagonal, transposed ones below).  Warp-collective; ob / ob2 must be free.
+template <class Cfg>
+__device__ __forceinline__ void epi_block_tma(const EpiArgs& P, const CUtensorMap* tmO, int mode, bool sym, int i0,
+                                              int lane, int j0, float coefA, float coefC, const float (&d)[32],
+                                              const float (&c)[32], uint8_t* ob, uint8_t* ob2, float& sumsq) {
+  if (sym && j0 + 31 < i0) return;               // block strictly below the diagonal
+  const int i = i0 + lane;
+  const bool row_ok = i < P.M;
+  float v[32];
+  if (mode == EPI_POLY || mode == EPI_APPLY) {
+#pragma unroll
+    for (int u = 0; u < 32; ++u) v[u] = coefC * c[u] + coefA * d[u];
+  } else if (mode == EPI_RESID) {
+#pragma unroll
+    for (int u = 0; u < 32; ++u) v[u] = ((j0 + u == i) ? 1.f : 0.f) - d[u];
+    if (P.gdiag && row_ok && i >= j0 && i < j0 + 32) {
+#pragma unroll
+      for (int u = 0; u < 32; ++u)
+        if (j0 + u == i) P.gdiag[i] = d[u];
+    }
+  } else {
+#pragma unroll
+    for (int u = 0; u < 32; ++u) v[u] = d[u];
+  }
+  const bool diag = sym && j0 < i0 + 32;         // 32-aligned: the diagonal block (j0 == i0)
+  if (mode == EPI_RESID && row_ok) {
+    // ||R||_F^2: every element once (symmetric: each strictly-upper element twice)
+#pragma unroll
+    for (int u = 0; u < 32; ++u) {
+      const int j = j0 + u;
+      if (j < P.N) {
+        if (!sym) sumsq = fmaf(v[u], v[u], sumsq);
+        else if (!diag || u > lane) sumsq = fmaf(2.f * v[u], v[u], sumsq);
+        else if (u == lane) sumsq = fmaf(v[u], v[u], sumsq);
+      }
+    }
+  }
+  stage_row_bf16(v, ob, lane);
+  __syncwarp();
+  if (!sym) {
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_2d(tmO, ob, j0, i0);
+      bulk_commit();
+    }
+    return;
+  }
+  transpose_staged_bf16(ob, ob2, lane);          // ob2 = block^T (same bf16 values)
+  __syncwarp();
+  if (diag) {
+    uint4 wr[4];
+#pragma unroll
+    for (int ch = 0; ch < 4; ++ch) wr[ch] = *reinterpret_cast<const uint4*>(ob2 + stg_off(lane, ch));
+    float w[32];
+    decode_bf16(wr, w);
+#pragma unroll
+    for (int u = 0; u < 32; ++u) w[u] = u >= lane ? v[u] : w[u];
+    __syncwarp();
+    stage_row_bf16(w, ob, lane);
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_2d(tmO, ob, j0, i0);
+      bulk_commit();
+    }
+    return;
+  }
+  fence_proxy_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_2d(tmO, ob, j0, i0);    // the block
+    tma_store_2d(tmO, ob2, i0, j0);   // its mirror
+    bulk_commit();
+  }
+}
+
 // Sketch-chain epilogue (thin GEMM, BN = 32): d[c] + d[w + c] = (R W)[i][c].
 template <class Cfg>
 __device__ __forceinline__ void store_w(const GemmProblem& P, int c, int wn, int i, float v) {
@@ -717,9 +805,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
   uint64_t* empty = bars + Cfg::STAGES;        // [STAGES]
   uint64_t* tfull = bars + 2 * Cfg::STAGES;    // [2]
   uint64_t* tempty = tfull + 2;                // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* cbar = tempty + 2;                 // [16] bf16 epilogue: C block landed (warp e, buffer b)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cbar + 16);
   float* red = reinterpret_cast<float*>(tmem_slot + 4);   // [8] epilogue reduction scratch
-  float* tbuf = reinterpret_cast<float*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES + 1024);    // [8][32*33]
+  float* tbuf = reinterpret_cast<float*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES + 1024);    // [8][32*33] (tf32)
+  uint8_t* ebuf = smem + Cfg::STAGES * Cfg::STAGE_BYTES + 1024;   // bf16: [8 warps][C0, C1, O0, O1] 2 KB each
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -740,6 +830,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], Cfg::CG * Cfg::EPI_WARPS);   // one arrival per epilogue warp (of both CTAs)
     }
+    for (int x = 0; x < 16; ++x) mbar_init(&cbar[x], 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<Cfg::CG>(tmem_slot, Cfg::TMEM_ALLOC);
@@ -884,6 +975,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
     float* tb = tbuf + e * 32 * 33;
     int acc = 0;
     uint32_t acc_phase = 0;
+    uint32_t cph = 0;       // bf16: phase bits of this warp's two C-block barriers
     int etcount = 0;
     // accumulator release: one arrival per epilogue warp on the leader's tempty barrier
     auto release_acc = [&](uint64_t* bar) {
@@ -914,26 +1006,22 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
       float sumsq = 0.f;
 
       if constexpr (Cfg::KIND == 0) {
-        // bf16: one TMEM accumulator per tile; this warp consumes its 32-column chunks
-        // while the raw C row segment of the next chunk is in flight
-        // C blocks: coalesced when the warp's 32 x 32 block is in bounds, else per-row
-        const bool rows_full = i0 + 32 <= ea.M;
-        auto c_issue = [&](int j, uint4 (&g)[4]) {
-#pragma unroll
-          for (int u = 0; u < 4; ++u) g[u] = make_uint4(0, 0, 0, 0);
-          if (!needC || j >= ea.N) return;
-          if (rows_full && j + 32 <= ea.N) warp_load_bf16_block(Cp, ldc, i0, j, g, lane);
-          else if (i < ea.M) load_raw_bf16(Cp, ldc, i, j, ea.N, g);
-        };
-        auto c_finish = [&](int j, const uint4 (&g)[4], float (&c)[32]) {
-          if (needC && rows_full && j + 32 <= ea.N) warp_rows_from_block(g, reinterpret_cast<uint8_t*>(tb), lane, c);
-          else decode_bf16(g, c);
-        };
-        // software pipeline per warp: chunk ch+1's tcgen05.ld (ping-pong registers) and its
-        // C block are in flight while chunk ch is combined and stored
+        // bf16: one TMEM accumulator per tile; per 32-column chunk: C block by TMA (two
+        // chunks ahead, per-warp buffers C0/C1), next chunk's tcgen05.ld in flight
+        // (ping-pong registers), output block staged and TMA-stored (O0/O1 alternate)
+        uint8_t* wb = ebuf + e * 8192;
         const int jb = tn * Cfg::BN;
-        uint4 cq[4];
-        c_issue(jb + c_begin * 32, cq);
+        const CUtensorMap* tmC = P.tmC;
+        const CUtensorMap* tmO = P.tmO;
+        auto c_fetch = [&](int ch) {   // lane 0
+          const int b = (ch - c_begin) & 1;
+          mbar_arrive_expect_tx(&cbar[e * 2 + b], 2048);
+          tma_load_2d(wb + b * 2048, tmC, &cbar[e * 2 + b], jb + ch * 32, i0);
+        };
+        if (needC && lane == 0) {
+          c_fetch(c_begin);
+          if (c_begin + 1 < c_end) c_fetch(c_begin + 1);
+        }
         mbar_wait(&tfull[acc], acc_phase);
         if (trace2 && et == 0 && leader && etcount < 8) trace2[192 + 4 * etcount + 2] = globaltimer_ns();
         tc_fence_after();
@@ -942,21 +1030,40 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
         tmem_ld32(tbase + c_begin * 32, ra);
         tmem_ld_wait_dep(ra);
         auto step = [&](int ch, uint32_t (&rc)[32], uint32_t (&rn)[32]) {
-          const bool tw = trace2 && lane == 0 && leader && etcount == 0 && ch - c_begin < 4;
-          const int tslot = 248 + 16 * e + 4 * (ch - c_begin);
-          if (tw) trace2[tslot] = clock64();
+          const int b = (ch - c_begin) & 1;
           const bool more = ch + 1 < c_end;
           if (more) tmem_ld32(tbase + (ch + 1) * 32, rn);
           float d[32], c[32];
-          c_finish(jb + ch * 32, cq, c);
-          if (tw) trace2[tslot + 2] = clock64();
-          if (more) c_issue(jb + (ch + 1) * 32, cq);
+          if (needC) {
+            mbar_wait(&cbar[e * 2 + b], (cph >> b) & 1u);
+            cph ^= 1u << b;
+            uint4 w[4];
+#pragma unroll
+            for (int x = 0; x < 4; ++x) w[x] = *reinterpret_cast<const uint4*>(wb + b * 2048 + stg_off(lane, x));
+            decode_bf16(w, c);
+            __syncwarp();
+            if (lane == 0 && ch + 2 < c_end) c_fetch(ch + 2);
+          } else {
+#pragma unroll
+            for (int u = 0; u < 32; ++u) c[u] = 0.f;
+          }
 #pragma unroll
           for (int u = 0; u < 32; ++u) d[u] = __uint_as_float(rc[u]);
-          if (tw) trace2[tslot + 1] = clock64();
-          epi_segment<Cfg>(ea, mode, sym, i0, lane, jb + ch * 32, coefA, coefC, d, c, tb, sumsq);
+          // output buffers: non-symmetric blocks alternate O0 / O1 (the previous store may
+          // still be reading the other one); symmetric blocks use both (block + mirror)
+          if (mode == EPI_GRAM32) {
+            // row-block partial Gram: plain fp32 stores (the warp's buffers as transpose scratch)
+            epi_gram32(ea, i0, lane, jb + ch * 32, d, reinterpret_cast<float*>(wb));
+          } else {
+            if (lane == 0) {
+              if (sym) bulk_wait_read<0>();
+              else bulk_wait_read<1>();
+            }
+            __syncwarp();
+            uint8_t* ob = wb + 4096 + (sym ? 0 : b * 2048);
+            epi_block_tma<Cfg>(ea, tmO, mode, sym, i0, lane, jb + ch * 32, coefA, coefC, d, c, ob, wb + 6144, sumsq);
+          }
           if (more) tmem_ld_wait_dep(rn);
-          if (tw) trace2[tslot + 3] = clock64();
         };
 #pragma unroll 1
         for (int ch = c_begin; ch < c_end; ch += 2) {
@@ -1016,6 +1123,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
       if (trace2 && et == 0 && leader && etcount < 8) trace2[192 + 4 * etcount + 3] = globaltimer_ns();
       ++etcount;
     }
+    if (Cfg::KIND == 0 && lane == 0) bulk_wait_all();   // this warp's TMA stores are complete
   }
 
   }

@@ -57,7 +57,7 @@ EncodeTiledFn encode_fn() {
 
 // OP_A: K-major A tile (box BK x 128); OP_BK: K-major B tile (box BK x BN);
 // OP_MN: MN-major operand (box 128-B x BK), A or B.
-enum OpKind { OP_A = 0, OP_BK = 1, OP_MN = 2 };
+enum OpKind { OP_A = 0, OP_BK = 1, OP_MN = 2, OP_EPI = 3 };   // OP_EPI: 32 x 32 epilogue block
 
 struct MapSpec {
   const void* ptr;
@@ -74,13 +74,16 @@ bool encode_map(CUtensorMap* out, const MapSpec& s) {
   cuuint64_t dims[2] = {(cuuint64_t)s.cols, (cuuint64_t)s.rows};
   cuuint64_t strides[1] = {(cuuint64_t)(s.ld * s.esz)};
   cuuint32_t box[2];
-  if (s.kind == OP_A) { box[0] = s.BK; box[1] = 128; }
+  if (s.kind == OP_EPI) { box[0] = 32; box[1] = 32; }
+  else if (s.kind == OP_A) { box[0] = s.BK; box[1] = 128; }
   else if (s.kind == OP_BK) { box[0] = s.BK; box[1] = s.BN; }   // BN = rows of B per CTA
   else { box[0] = 128 / s.esz; box[1] = s.BK; }
   cuuint32_t es[2] = {1, 1};
   CUresult r = fn(out, s.esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
                   const_cast<void*>(s.ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  (s.kind == OP_MN && s.esz == 4) ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                  s.kind == OP_EPI                  ? CU_TENSOR_MAP_SWIZZLE_64B
+                  : (s.kind == OP_MN && s.esz == 4) ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
+                                                    : CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
@@ -229,6 +232,7 @@ int elem_size(int precision) { return precision == PRISM_BF16 ? 2 : 4; }
 struct HostProblem {
   GemmProblem p;      // tm* fields hold map indices (+1; 0 = none) until serialised
   int mapA, mapB, mapA_lo, mapB_lo;
+  int mapC, mapO;     // bf16 epilogue blocks (TMA load of C, TMA store of the output)
 };
 
 struct LaunchDesc {
@@ -422,6 +426,14 @@ prism_status build_plan(const Request& r, Plan& P) {
       h.p.out = out; h.p.out_lo = out_lo; h.p.ldo = ldo; h.p.C = C; h.p.C_lo = C_lo; h.p.ldc = ldc;
       h.p.alpha = alpha_ptr;
       h.p.tiles_n = (N + BN - 1) / BN;
+      if (esz == 2 && (mode == EPI_RESID || mode == EPI_POLY || mode == EPI_APPLY || mode == EPI_STORE)) {
+        maps.push_back(MapSpec{out, M, N, ldo, esz, OP_EPI, 32, 32});
+        h.mapO = (int)maps.size();
+        if (C) {
+          maps.push_back(MapSpec{C, M, N, ldc, esz, OP_EPI, 32, 32});
+          h.mapC = (int)maps.size();
+        }
+      }
       return h;
     };
     if (!r.sqrt_kind) {
@@ -647,6 +659,8 @@ prism_status build_plan(const Request& r, Plan& P) {
       q.tmB = mapptr(L->probs[j].mapB);
       q.tmA_lo = mapptr(L->probs[j].mapA_lo);
       q.tmB_lo = mapptr(L->probs[j].mapB_lo);
+      q.tmC = mapptr(L->probs[j].mapC);
+      q.tmO = mapptr(L->probs[j].mapO);
       gp[j] = q;
     }
     std::memcpy(blob + L->tiles_off, L->tiles.data(), sizeof(uint32_t) * L->tiles.size());
@@ -1478,7 +1492,7 @@ prism_status prism_debug_gemm(prism_handle h, int precision, int b_mn, int mode,
   const int esz = elem_size(precision), BN = tile_bn(precision), BK = tile_bk(precision);
   if ((lda * esz) % 16 || (ldb * esz) % 16 || (ldo * esz) % 16 || (C && (ldc * esz) % 16))
     return fail(PRISM_ERR_INVALID_ARG, "leading dimensions must be 16-B multiples");
-  const size_t need = 4096 + 4 * sizeof(CUtensorMap) + sizeof(GemmProblem) + 4 * ((M + 127) / 128) * ((N + BN - 1) / BN);
+  const size_t need = 4096 + 6 * sizeof(CUtensorMap) + sizeof(GemmProblem) + 4 * ((M + 127) / 128) * ((N + BN - 1) / BN);
   if (ws_bytes < need) return fail(PRISM_ERR_INVALID_ARG, "workspace too small");
   static thread_local std::unique_ptr<uint8_t, PinnedDeleter> blob;
   static thread_local size_t blob_size = 0;
@@ -1503,10 +1517,17 @@ prism_status prism_debug_gemm(prism_handle h, int precision, int b_mn, int mode,
         !encode_map(&hm[3], MapSpec{B_lo, brows, bcols, ldb, esz, bk, tile_m_main() == 256 ? BN / 2 : BN, BK}))
       return fail(PRISM_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   }
-  GemmProblem* gp = reinterpret_cast<GemmProblem*>(hb + 4 * sizeof(CUtensorMap));
+  // bf16 epilogue blocks: TMA store of the output, TMA load of C (maps 4 and 5)
+  if (esz == 2) {
+    if (!encode_map(&hm[4], MapSpec{out, M, N, ldo, esz, OP_EPI, 32, 32}) ||
+        (C && !encode_map(&hm[5], MapSpec{C, M, N, ldc, esz, OP_EPI, 32, 32})))
+      return fail(PRISM_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  }
+  GemmProblem* gp = reinterpret_cast<GemmProblem*>(hb + 6 * sizeof(CUtensorMap));
   const CUtensorMap* dm = reinterpret_cast<const CUtensorMap*>(wsd);
   gp->tmA = dm; gp->tmB = dm + 1;
   gp->tmA_lo = split ? dm + 2 : nullptr; gp->tmB_lo = split ? dm + 3 : nullptr;
+  gp->tmO = esz == 2 ? dm + 4 : nullptr; gp->tmC = (esz == 2 && C) ? dm + 5 : nullptr;
   gp->out = out; gp->out_lo = out_lo; gp->C = C; gp->C_lo = C_lo;
   gp->norm_part = norm_part; gp->gdiag = gdiag; gp->alpha = alpha_dev;
   gp->ldo = ldo; gp->ldc = ldc; gp->M = M; gp->N = N; gp->K = K;
@@ -1518,11 +1539,11 @@ prism_status prism_debug_gemm(prism_handle h, int precision, int b_mn, int mode,
   hp.p = *gp;
   L.probs.push_back(hp);
   add_tiles(L, 0, M, N, BN, sym != 0);
-  const size_t tiles_off = 4 * sizeof(CUtensorMap) + align_up(sizeof(GemmProblem), 128);
+  const size_t tiles_off = 6 * sizeof(CUtensorMap) + align_up(sizeof(GemmProblem), 128);
   std::memcpy(hb + tiles_off, L.tiles.data(), 4 * L.tiles.size());
   PRISM_CK(cudaMemcpyAsync(wsd, hb, need, cudaMemcpyHostToDevice, static_cast<cudaStream_t>(stream)));
   GemmLaunch g{};
-  g.probs = reinterpret_cast<const GemmProblem*>(wsd + 4 * sizeof(CUtensorMap));
+  g.probs = reinterpret_cast<const GemmProblem*>(wsd + 6 * sizeof(CUtensorMap));
   g.tiles = reinterpret_cast<const uint32_t*>(wsd + tiles_off);
   g.done = nullptr;
   g.done_stride = 0;
