@@ -61,6 +61,15 @@ __device__ __forceinline__ void chain_krange(int K, int BK, int own, int ks, int
 // committed, 5 accumulator ready (reader), 6 slices sent, 7 slices received, 8 epilogue done.
 __device__ unsigned long long* g_chain_trace = nullptr;
 
+// Slices of a tile this CTA computes: in a split launch (C > 1) the one at its cluster
+// rank (the tile code's low bits); in a C = 1 launch all P.ksplit slices of the matrix,
+// in order (each accumulated separately and summed in the same order as the split
+// launch's reduce-scatter, so the bits do not depend on C).
+__device__ __forceinline__ void chain_slices(const GemmProblem& P, uint32_t code, int C, int& s_lo, int& s_hi) {
+  s_lo = C > 1 ? (int)(code & 1023) : 0;
+  s_hi = C > 1 ? s_lo + 1 : (P.ksplit > 1 ? P.ksplit : 1);
+}
+
 template <class Cfg, int PASS>
 __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __grid_constant__ GemmLaunch L) {
   extern __shared__ uint8_t smem_raw[];
@@ -129,8 +138,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
     tma_prefetch(P.tmB);
     if (!(L.done && L.done[P.matrix * L.done_stride])) {
       const int n0 = ((code >> 10) & 1023) * Cfg::BN;
-      int kb_lo, kb_hi;
-      chain_krange(P.K, Cfg::BK, P.ksplit, (int)(code & 1023), kb_lo, kb_hi);
+      int s_lo, s_hi, kb_lo, kb_hi, dummy;
+      chain_slices(P, code, C, s_lo, s_hi);
+      chain_krange(P.K, Cfg::BK, P.ksplit, s_lo, kb_lo, dummy);
+      chain_krange(P.K, Cfg::BK, P.ksplit, s_hi - 1, dummy, kb_hi);
       pre_n = min(Cfg::STAGES, kb_hi - kb_lo);
       for (int j = 0; j < pre_n; ++j) {
         uint8_t* sB = stage_base + j * Cfg::STAGE_BYTES + Cfg::A_BYTES;
@@ -157,8 +168,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
         const GemmProblem& P = probs[code >> 20];
         if (L.done && L.done[P.matrix * L.done_stride]) continue;
         const int n0 = ((code >> 10) & 1023) * Cfg::BN;
-        int kb_lo, kb_hi;
-        chain_krange(P.K, Cfg::BK, P.ksplit, (int)(code & 1023), kb_lo, kb_hi);
+        int s_lo, s_hi, kb_lo, kb_hi, dummy;   // the slices' k-blocks are contiguous
+        chain_slices(P, code, C, s_lo, s_hi);
+        chain_krange(P.K, Cfg::BK, P.ksplit, s_lo, kb_lo, dummy);
+        chain_krange(P.K, Cfg::BK, P.ksplit, s_hi - 1, dummy, kb_hi);
         for (int kb = kb_lo; kb < kb_hi; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sA = stage_base + stage * Cfg::STAGE_BYTES;
@@ -186,10 +199,12 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
         const uint32_t code = L.tiles[t];
         const GemmProblem& P = probs[code >> 20];
         if (L.done && L.done[P.matrix * L.done_stride]) continue;
-        int kb_lo, kb_hi;
-        chain_krange(P.K, Cfg::BK, P.ksplit, (int)(code & 1023), kb_lo, kb_hi);
-        if (kb_lo < kb_hi) {
-          const int kb0 = kb_lo, kb1 = kb_hi;
+        int s_lo, s_hi;
+        chain_slices(P, code, C, s_lo, s_hi);
+        for (int sl = s_lo; sl < s_hi; ++sl) {   // one TMEM chunk per slice
+          int kb0, kb1;
+          chain_krange(P.K, Cfg::BK, P.ksplit, sl, kb0, kb1);
+          if (kb0 >= kb1) continue;
           mbar_wait(&tempty[acc], acc_phase ^ 1);
           tc_fence_after();
           const uint32_t dt = tmem_base + acc * Cfg::BN;
@@ -232,8 +247,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
       const GemmProblem& P = probs[code >> 20];
       if (L.done && L.done[P.matrix * L.done_stride]) continue;
       const int tn = (code >> 10) & 1023;
-      int kb_lo, kb_hi;
-      chain_krange(P.K, Cfg::BK, P.ksplit, (int)(code & 1023), kb_lo, kb_hi);
+      int s_lo, s_hi;
+      chain_slices(P, code, C, s_lo, s_hi);
       // this thread's row of the pass output, and its operands loaded ahead (chain_prefetch)
       const bool mine = C == 1 || et < rows_per;   // whole warps (rows_per is a multiple of 32)
       const int i = !mine ? P.M : tn * Cfg::BN + (C == 1 ? 0 : (int)krank * rows_per) + et;   // P.M: no row
@@ -243,6 +258,42 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
       chain_prefetch<Cfg, PASS>(P, i, 2, pre);
       // the accumulator (32 x 256, TMEM lanes 0..31) to the owners of its rows: CTA r of
       // the cluster owns rows [r·rows_per, (r+1)·rows_per); C = 1: all rows stay here
+      if (C == 1) {
+        // every slice here: staged in order (first slice written, later ones added)
+        bool first = true;
+        for (int sl = s_lo; sl < s_hi; ++sl) {
+          int k0, k1;
+          chain_krange(P.K, Cfg::BK, P.ksplit, sl, k0, k1);
+          if (k0 >= k1) continue;
+          if (reader) {
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+#pragma unroll 1
+            for (int x = 0; x < 4; ++x) {
+              const int col = h * 128 + x * 32;
+              uint32_t r[32];
+              tmem_ld32(tmem_base + acc * Cfg::BN + col, r);
+              tmem_ld_wait();
+              float* dst = dsm + (size_t)lane * rstride + col;
+              if (first) {
+#pragma unroll
+                for (int u = 0; u < 32; ++u) dst[u] = __uint_as_float(r[u]);
+              } else {
+#pragma unroll
+                for (int u = 0; u < 32; ++u) dst[u] += __uint_as_float(r[u]);
+              }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+          }
+          first = false;
+          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+        if (tr && reader && lane == 0 && h == 0) tr[5] = globaltimer_ns();
+      } else {
+      int kb_lo, kb_hi;
+      chain_krange(P.K, Cfg::BK, P.ksplit, s_lo, kb_lo, kb_hi);
       const bool have = kb_lo < kb_hi;
       if (reader) {
         if (have) {
@@ -251,7 +302,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
         }
         if (tr && lane == 0 && h == 0) tr[5] = globaltimer_ns();
         // every owner consumed the previous round's slices: send this round's
-        if (C > 1) mbar_wait(recv_free, rphase ^ 1);
+        mbar_wait(recv_free, rphase ^ 1);
 #pragma unroll 1
         for (int x = 0; x < 4; ++x) {
           const int col = h * 128 + x * 32;          // 32 rows n of the tile
@@ -282,6 +333,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
         if (tr && lane == 0 && h == 0) tr[6] = globaltimer_ns();
       }
       if (have && ++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
       if (C > 1 && et == 0) mbar_arrive_expect_tx(recv_full, (uint32_t)(C - 1) * 32 * rows_per * 4);
       named_bar_sync(1, 32 * Cfg::EPI_WARPS);    // own slice written locally
       if (C > 1) {

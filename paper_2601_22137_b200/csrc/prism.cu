@@ -584,9 +584,18 @@ prism_status build_plan(const Request& r, Plan& P) {
   // chain tiles (chaint.cuh): 256-row tiles of R, each split over a cluster of C CTAs,
   // C = the largest factor of the launch's matrices (smaller factors: empty slices).
   // Tiles of one row tile are contiguous and C-aligned, so slice == cluster rank.
+  // A launch whose unsplit row tiles already fill the SMs runs every matrix's slices
+  // in one CTA, in order (same bits, no exchange); otherwise each slice gets a CTA.
   P.chain_ksplit = 1;
-  if (P.n_chain)
-    for (const HostProblem& hp : P.chaint[0].probs) P.chain_ksplit = std::max(P.chain_ksplit, hp.p.ksplit);
+  if (P.n_chain) {
+    long long rows = 0;
+    int kmax = 1;
+    for (const HostProblem& hp : P.chaint[0].probs) {
+      rows += (hp.p.M + 255) / 256;
+      kmax = std::max(kmax, hp.p.ksplit);
+    }
+    P.chain_ksplit = rows >= num_sms() ? 1 : kmax;
+  }
   for (int j = 0; j < P.n_chain; ++j) {
     LaunchDesc& T = P.chaint[j];
     T.tiles.clear();

@@ -141,6 +141,19 @@ def test_split_chain_parity_and_batch_bits():
     assert abs(int(rb["iters"][1]) - ro.iters) <= 1
 
 
+def test_chain_slices_sequential_equals_cluster_split():
+    # A matrix's chain K-slices (s >= 1024) are either spread over a CTA cluster (the
+    # batch has fewer row tiles than SMs) or run in order by one CTA (it has enough):
+    # both sum the slices in the same order, so the results must be bit-identical.
+    big = torch.tensor(W.gaussian(2048, 2048, seed=77)).float().cuda()
+    small = [torch.tensor(W.gaussian(256, 256, seed=100 + i)).float().cuda() for i in range(150)]
+    Qa, ra = P.polar([big], degree=5, tol=1e-5, precision="fp32", matrix_ids=[0])   # 8 tiles: cluster of 4
+    Qb, rb = P.polar([big] + small, degree=5, tol=1e-5, precision="fp32")          # 158 tiles: one CTA
+    torch.cuda.synchronize()
+    assert int(ra["iters"][0]) == int(rb["iters"][0])
+    assert torch.equal(Qa[0], Qb[0])
+
+
 def test_host_path_pipelined_equals_device_path():
     # prism_polar_host: three different batches submitted back to back (two staging
     # slots, so the third reuses the first slot while the pipeline is busy); each result
