@@ -43,3 +43,20 @@ for p in range(8):
         if sel.any():
             v = (b[sel, c] - t0) / 1e3
             print(f"   {nm:10s} min {v.min():7.2f} med {np.median(v):7.2f} max {v.max():7.2f}")
+
+# inter-pass timeline in absolute time: last epilogue of pass j -> release of pass j+1
+print("absolute (us from pass-0 entry): pass, last entry, release (pred done) median, last epi done")
+base = None
+for p in range(8):
+    blk = T[p]
+    used = blk[:, 0] > 0
+    if not used.any():
+        continue
+    b = blk[used]
+    if base is None:
+        base = b[:, 0].min()
+    last_entry = (b[:, 0].max() - base) / 1e3
+    rel = (np.median(b[:, 2]) - base) / 1e3
+    epi = b[:, 8][b[:, 8] > 0]
+    done = (epi.max() - base) / 1e3 if len(epi) else float("nan")
+    print(f"   pass {p}: last entry {last_entry:8.2f}  released {rel:8.2f}  done {done:8.2f}")
