@@ -100,7 +100,7 @@ __device__ __forceinline__ T block_sum(T v, T* scratch) {
 }
 
 // ----------------------------------------------------------------- a1: ||A||_F partials
-// grid (kFroParts, batch), 256 threads; block j handles rows r = j, j + kFroParts, ...
+// grid (kFroParts, batch), 256 threads; block j handles a fixed contiguous share of the matrix
 // with 16-byte vector loads when the row layout allows it.
 __global__ void __launch_bounds__(256) k_fro_partials(SolveParams P) {
   griddep_wait();
@@ -110,29 +110,49 @@ __global__ void __launch_bounds__(256) k_fro_partials(SolveParams P) {
   const int bf16 = P.precision == 0;
   const int esz = bf16 ? 2 : 4, vec = 16 / esz;
   const bool vok = ((D.lda * esz) % 16 == 0) && ((reinterpret_cast<uintptr_t>(D.A) & 15) == 0);
+  const long long nv = vok ? D.n / vec : 0;       // 16-B vectors per row
+  // block j sums a fixed contiguous share of the flattened (row, vector) index space,
+  // four independent 16-B loads in flight per thread (fixed assignment: deterministic)
+  const long long total = (long long)D.m * nv;
+  const long long per = (total + kFroParts - 1) / kFroParts;
+  const long long beg = blockIdx.x * per, end = min(total, beg + per);
+  const char* A = static_cast<const char*>(D.A);
   double acc = 0.0;
-  for (int r = blockIdx.x; r < D.m; r += kFroParts) {
-    const char* row = static_cast<const char*>(D.A) + (long long)r * D.lda * esz;
-    const int nv = vok ? D.n / vec : 0;
-    for (int c = threadIdx.x; c < nv; c += 256) {
-      const uint4 w = __ldg(reinterpret_cast<const uint4*>(row) + c);
+  for (long long base = beg + threadIdx.x; base < end; base += 4 * 256) {
+    uint4 w[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long j = base + (long long)u * 256;
+      w[u] = make_uint4(0, 0, 0, 0);
+      if (j < end) {
+        const long long r = j / nv, c = j - r * nv;
+        w[u] = __ldg(reinterpret_cast<const uint4*>(A + r * D.lda * esz) + c);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
       if (bf16) {
-        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w[u]);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const float2 f = __bfloat1622float2(h[e]);
           acc += (double)f.x * f.x + (double)f.y * f.y;
         }
       } else {
-        const float* f = reinterpret_cast<const float*>(&w);
+        const float* f = reinterpret_cast<const float*>(&w[u]);
 #pragma unroll
         for (int e = 0; e < 4; ++e) acc += (double)f[e] * f[e];
       }
     }
-    for (int c = nv * vec + threadIdx.x; c < D.n; c += 256) {
-      const double x = (double)load_val(D.A, (long long)r * D.lda + c, bf16);
-      acc += x * x;
-    }
+  }
+  // columns past the last whole vector (n % vec, or every column when unaligned)
+  const int c0 = (int)(nv * vec);
+  if (c0 < D.n) {
+    for (int r = blockIdx.x; r < D.m; r += kFroParts)
+      for (int c = c0 + threadIdx.x; c < D.n; c += 256) {
+        const double x = (double)load_val(D.A, (long long)r * D.lda + c, bf16);
+        acc += x * x;
+      }
   }
   acc = block_sum<double, 256>(acc, scratch);
   if (threadIdx.x == 0) P.fro_part[blockIdx.y * kFroParts + blockIdx.x] = acc;
