@@ -14,6 +14,8 @@ Coupled square root (Table 1 rows P:246-250, Theorem 3; R11):
     X_0 = A/||A||_F, Y_0 = I, R_k = I - Y_k X_k
     X_{k+1} = X_k g_d(R_k; a_k),  Y_{k+1} = g_d(R_k; a_k) Y_k
     A^{1/2} ~ sqrt(c) X,  A^{-1/2} ~ Y / sqrt(c)
+Matrix sign (the paper's case study, eq. 2; A^2 symmetric):
+    X_0 = A/||A||_F, R_k = I - X_k^2, X_{k+1} = X_k g_d(R_k; a_k)
 Coefficient a_k (eq. (4)):
     a_k = argmin_{a in [l,u]} || S_k (I - (I-R_k) g_d(R_k;a)^2) ||_F^2
         = argmin m(a),  m(a) = c0 + c1 a + c2 a^2 + c3 a^3 + c4 a^4
@@ -357,3 +359,44 @@ def sqrt_invsqrt(A, d: int = 2, p: int = 8, tol: float = 1e-10, max_iters: int =
     rep.iters = k
     sc = math.sqrt(c)
     return sc * X, Y / sc, rep
+
+
+def sign(A, d: int = 2, p: int = 8, tol: float = 1e-10, max_iters: int = 50,
+         seed: int = 0, b: int = 0, warmup: int = 0, fit: str = FIT_SKETCHED,
+         alpha_lo: float | None = None, alpha_hi: float | None = None):
+    """PRISM Newton–Schulz matrix sign sign(A) = A (A^2)^{-1/2} of a square A in fp64.
+
+    The paper's case study (eq. 2): X_0 = A/||A||_F (R10),
+    R_k = I - X_k^2, X_{k+1} = X_k g_d(R_k; a_k), with the loss of eq. (4) fitted on
+    R_k exactly as for polar / sqrt ("identical formulas; only R differs").  A^2
+    symmetric is the paper's standing assumption: then R_k is symmetric for all
+    k (P:194).  Returns (S, Report).
+    """
+    A = np.asarray(A, dtype=np.float64)
+    n = A.shape[0]
+    lo, hi, aT = interval(d)
+    lo = lo if alpha_lo is None else alpha_lo
+    hi = hi if alpha_hi is None else alpha_hi
+    rep = Report()
+    c = math.sqrt(float(np.sum(A * A)))
+    if c == 0.0:
+        rep.status = ZERO_INPUT
+        return np.zeros_like(A), rep
+    X = A / c                                  # X_0 = A/||A||_F (P:145)
+    I = np.eye(n)
+    incr = 0
+    r_prev = math.inf
+    k = 0
+    while True:
+        R = I - X @ X                          # R_k = I - X_k^2 (eq. 2, P:190)
+        r = float(np.linalg.norm(R, "fro"))
+        stop, incr = _status_update(rep, k, r, r_prev, n, tol, max_iters, incr)
+        r_prev = r
+        if stop:
+            break
+        a = _choose_alpha(k, R, d, fit, p, seed, b, n, warmup, lo, hi, aT, rep)
+        rep.alphas.append(a)
+        X = X @ g_matrix(R, a, d)              # X_{k+1} = X_k g_d(R_k; a_k)
+        k += 1
+    rep.iters = k
+    return X, rep

@@ -371,3 +371,69 @@ def test_sqrt_iterates_commute():
     for iters in (1, 2, 4):
         X, Y, _ = prism.sqrt_invsqrt(A, d=2, tol=1e-300, max_iters=iters)
         assert np.linalg.norm(X @ Y - Y @ X) <= 1e-12 * np.linalg.norm(X) * np.linalg.norm(Y)
+
+
+# ---------------------------------------------------------------- matrix sign
+def _sym_indefinite(n, seed, lo=1e-3):
+    """Q diag(lam) Q^T with |lam| log-spaced in [lo, 1] and alternating signs."""
+    rng = np.random.default_rng(seed)
+    Q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    lam = np.logspace(0, np.log10(lo), n) * np.where(np.arange(n) % 2 == 0, 1.0, -1.0)
+    return (Q * lam[None, :]) @ Q.T
+
+
+@pytest.mark.parametrize("d", [1, 2])
+def test_sign_vs_eigh(d):
+    # sign(A) = V sign(Lambda) V^T for symmetric A (definition P:145 with A^2 = A^T A)
+    A = _sym_indefinite(40, seed=d)
+    lam, V = np.linalg.eigh(A)
+    ref = (V * np.sign(lam)[None, :]) @ V.T
+    S, rep = prism.sign(A, d=d, p=8, tol=1e-12, max_iters=80)
+    assert rep.status == prism.CONVERGED
+    assert np.linalg.norm(S - ref) / np.linalg.norm(ref) <= 1e-10
+
+
+def test_sign_taylor_mode_is_classical_newton_schulz():
+    # textbook Newton-Schulz for the sign (Higham 2008, eq. 5.22): X (3I - X^2) / 2
+    A = _sym_indefinite(16, seed=3, lo=0.05)
+    X = A / np.linalg.norm(A)
+    for _ in range(3):
+        X = 0.5 * X @ (3 * np.eye(16) - X @ X)
+    S, rep = prism.sign(A, d=1, fit="taylor", max_iters=3, tol=1e-300)
+    assert rep.iters == 3 and np.allclose(S, X, atol=1e-14)
+
+
+def test_sign_theorem1_bound_d1_exact():
+    # Theorem 1 (P:197-199): d = 1, exact fit on [1/2, 1]: ||I - X_k^2||_2 <= ||I - A^2||_2^(2^(k-2))
+    for seed in range(4):
+        A = _sym_indefinite(30, seed=10 + seed, lo=10.0 ** -(seed + 1))
+        X0 = A / np.linalg.norm(A)
+        r0 = np.linalg.norm(np.eye(30) - X0 @ X0, 2)
+        for k in range(2, 40):
+            S, rep = prism.sign(A, d=1, fit="exact", tol=1e-300, max_iters=k)
+            rk = np.linalg.norm(np.eye(30) - S @ S, 2)
+            assert rk <= r0 ** (2.0 ** (k - 2)) + 1e-13
+            if rk < 1e-13:
+                break
+
+
+def test_sign_block_matrix_gives_square_roots():
+    # P:273-283: for X_0 = [[0, A], [I, 0]] (A SPD; X_0^2 symmetric),
+    # sign(X_0) = [[0, A^{1/2}], [A^{-1/2}, 0]]
+    n = 12
+    A = W.spd_logspaced(n, 1e2, seed=4)
+    Z = np.zeros((n, n))
+    X0 = np.block([[Z, A], [np.eye(n), Z]])
+    S, rep = prism.sign(X0, d=2, p=8, tol=1e-12, max_iters=80)
+    lam, V = np.linalg.eigh(A)
+    sq = (V * np.sqrt(lam)[None, :]) @ V.T
+    isq = (V / np.sqrt(lam)[None, :]) @ V.T
+    assert rep.status == prism.CONVERGED
+    assert np.abs(S[:n, :n]).max() < 1e-10 and np.abs(S[n:, n:]).max() < 1e-10
+    assert np.linalg.norm(S[:n, n:] - sq) / np.linalg.norm(sq) <= 1e-9
+    assert np.linalg.norm(S[n:, :n] - isq) / np.linalg.norm(isq) <= 1e-9
+
+
+def test_sign_zero_input():
+    S, rep = prism.sign(np.zeros((8, 8)))
+    assert rep.status == prism.ZERO_INPUT and not S.any()
