@@ -146,6 +146,18 @@ prism_status prism_sqrt_invsqrt(prism_handle h, int batch, const int64_t* n, con
                                 const int64_t* lda, void* const* Asqrt, void* const* Ainvsqrt,
                                 const int64_t* ld_out, const int64_t* matrix_ids, const prism_options* o,
                                 const prism_report* rep, void* workspace, size_t ws_bytes, void* stream);
+/*
+ * Matrix sign sign(A) = A (A^2)^{-1/2} of square n[i] x n[i] matrices (the paper's case
+ * study): X_0 = A/||A||_F, R_k = I - X_k^2, X_{k+1} = X_k g_d(R_k; a_k) with
+ * the same sketched fit.  A^2 symmetric is the paper's standing assumption;
+ * otherwise convergence is not guaranteed (status).  S[i] receives sign(A_i) (ld lds[i];
+ * may alias A).  Other arguments as prism_polar.
+ */
+size_t prism_sign_workspace(prism_handle h, int batch, const int64_t* n, const prism_options* o);
+prism_status prism_sign(prism_handle h, int batch, const int64_t* n, const void* const* A, const int64_t* lda,
+                        void* const* S, const int64_t* lds, const int64_t* matrix_ids, const prism_options* o,
+                        const prism_report* rep, void* workspace, size_t ws_bytes, void* stream);
+
 /* prism_sqrt_invsqrt on page-locked HOST buffers, pipelined as prism_polar_host. */
 prism_status prism_sqrt_invsqrt_host(prism_handle h, int batch, const int64_t* n, const void* const* A,
                                      const int64_t* lda, void* const* Asqrt, void* const* Ainvsqrt,

@@ -287,6 +287,7 @@ struct Request {
   char* ws;   // null: size query only
   bool rowblock = false;   // row-block member of a split tall matrix: force the tall form, s = n
   float* G = nullptr;      // row-block: fp32 partial Gram output (n x n, ld n)
+  bool sign_kind = false;  // matrix sign: square path, R = I - X^2, X only (output in Q)
 };
 
 void resolve_interval(prism_options& o, double& lo, double& hi, double& aT, int& d) {
@@ -398,7 +399,7 @@ prism_status build_plan(const Request& r, Plan& P) {
     D.gdiag = reinterpret_cast<float*>(bump.take(sizeof(float) * s));
     D.tiles_m = (s + 127) / 128;
     D.tiles_n = (s + BN - 1) / BN;
-    D.sym = (r.sqrt_kind || r.rowblock) ? 0 : 1;
+    D.sym = (r.sqrt_kind || r.sign_kind || r.rowblock) ? 0 : 1;
     D.norm_part = reinterpret_cast<float*>(bump.take(sizeof(float) * D.tiles_m * D.tiles_n));
     const long long ldS = (long long)align_up(s, 64);
     D.ldS = ldS;
@@ -436,7 +437,7 @@ prism_status build_plan(const Request& r, Plan& P) {
       }
       return h;
     };
-    if (!r.sqrt_kind) {
+    if (!r.sqrt_kind && !r.sign_kind) {
       // polar: X keeps A's row-major layout (m x n).  Tall (m >= n): G = X^T X with both
       // operands MN-major, X' = X + X P (A = X K-major, B = P K-major by symmetry).
       // Wide (m < n): G = X X^T (both K-major), X' = X + P X (B = X MN-major).
@@ -492,15 +493,18 @@ prism_status build_plan(const Request& r, Plan& P) {
       }
     } else {
       // sqrt: G = Y X, P = R/2 + a R^2, X' = X + X P, Y' = Y + P Y (Theorem-3 ordering, R11)
+      // sign: G = X X, X' = X + X P (R general: no symmetric kernels)
       const int nn = s;
       for (int t = 0; t < 2; ++t) {
         HostProblem g = mk(nn, nn, nn, EPI_RESID, 0, D.R, D.R_lo, ldr, nullptr, nullptr, 0);
         g.p.norm_part = D.norm_part;
         g.p.gdiag = D.gdiag;
         g.p.b_mn = 1;
-        g.mapA = add_map(D.Y[t], nn, nn, ldx, OP_A);
+        void* const GA = r.sign_kind ? D.X[t] : D.Y[t];
+        void* const GA_lo = r.sign_kind ? D.X_lo[t] : D.Y_lo[t];
+        g.mapA = add_map(GA, nn, nn, ldx, OP_A);
         g.mapB = add_map(D.X[t], nn, nn, ldx, OP_MN);
-        if (split) { g.mapA_lo = add_map(D.Y_lo[t], nn, nn, ldx, OP_A); g.mapB_lo = add_map(D.X_lo[t], nn, nn, ldx, OP_MN); }
+        if (split) { g.mapA_lo = add_map(GA_lo, nn, nn, ldx, OP_A); g.mapB_lo = add_map(D.X_lo[t], nn, nn, ldx, OP_MN); }
         P.gram[t].probs.push_back(g);
         const void* Pa = d == 2 ? Pm : D.R;
         const void* Pa_lo = d == 2 ? Pm_lo : D.R_lo;
@@ -511,6 +515,7 @@ prism_status build_plan(const Request& r, Plan& P) {
         ax.mapB = add_map(Pa, nn, nn, ldr, OP_MN);
         if (split) { ax.mapA_lo = add_map(D.X_lo[t], nn, nn, ldx, OP_A); ax.mapB_lo = add_map(Pa_lo, nn, nn, ldr, OP_MN); }
         P.apply[t].probs.push_back(ax);
+        if (r.sign_kind) continue;
         HostProblem ay = mk(nn, nn, nn, EPI_APPLY, 0, D.Y[1 - t], D.Y_lo[1 - t], ldx, D.Y[t], D.Y_lo[t], ldx);
         ay.p.scale_by_alpha = d == 1;
         ay.p.b_mn = 1;
@@ -860,6 +865,7 @@ struct KindTimer {
 static std::vector<long long> make_key(const Request& r) {
   std::vector<long long> k;
   k.push_back(r.sqrt_kind);
+  k.push_back(r.sign_kind);
   k.push_back(r.rowblock);
   k.push_back((long long)(uintptr_t)r.G);
   k.push_back(r.batch);
@@ -1295,6 +1301,32 @@ prism_status prism_sqrt_invsqrt(prism_handle h, int batch, const int64_t* n, con
     return run_solve(h, r, rep, ws_bytes, static_cast<cudaStream_t>(stream));
   } catch (...) {
     return fail(PRISM_ERR_INTERNAL, "exception in prism_sqrt_invsqrt");
+  }
+}
+
+size_t prism_sign_workspace(prism_handle h, int batch, const int64_t* n, const prism_options* o) {
+  if (!h || !o || !n || batch < 1) return 0;
+  std::vector<const void*> fakeA(batch, reinterpret_cast<const void*>(256));
+  std::vector<void*> fakeQ(batch, reinterpret_cast<void*>(256));
+  std::vector<int64_t> ld(n, n + batch);
+  Request r{false, batch, n, n, fakeA.data(), ld.data(), fakeQ.data(), nullptr, ld.data(), nullptr, *o, nullptr};
+  r.sign_kind = true;
+  if (validate(r)) return 0;
+  Plan P;
+  if (build_plan(r, P)) return 0;
+  return P.ws_need;
+}
+
+prism_status prism_sign(prism_handle h, int batch, const int64_t* n, const void* const* A, const int64_t* lda,
+                        void* const* S, const int64_t* lds, const int64_t* matrix_ids, const prism_options* o,
+                        const prism_report* rep, void* workspace, size_t ws_bytes, void* stream) {
+  try {
+    if (!o) return fail(PRISM_ERR_INVALID_ARG, "null options");
+    Request r{false, batch, n, n, A, lda, S, nullptr, lds, matrix_ids, *o, static_cast<char*>(workspace)};
+    r.sign_kind = true;
+    return run_solve(h, r, rep, ws_bytes, static_cast<cudaStream_t>(stream));
+  } catch (...) {
+    return fail(PRISM_ERR_INTERNAL, "exception in prism_sign");
   }
 }
 

@@ -17,6 +17,9 @@ Recipes (DESIGN.md §"Input recipe"):
 * ``spd_logspaced`` Q diag(lambda) Q^T, lambda_i = kappa^{-i/(n-1)} (Shampoo
                     blocks with condition number kappa; P:1298 analogue).
 * ``wishart``       G^T G / rows, G Gaussian rows x n.
+* ``sym_indefinite`` Q diag(lambda) Q^T, |lambda_i| log-spaced in [lo, 1] with
+                    alternating signs: symmetric indefinite inputs of the
+                    matrix-sign case study (A^2 symmetric).
 * GPT-2 small / 1B-model Muon batches (BASELINE.json configs[1], [4]).
 """
 
@@ -89,6 +92,13 @@ def equal_sigma(m: int, n: int, c: float, seed: int) -> np.ndarray:
 
 def spd_logspaced(n: int, kappa: float, seed: int) -> np.ndarray:
     lam = kappa ** (-np.arange(n) / max(n - 1, 1))
+    Q = haar(n, n, seed)
+    A = (Q * lam[None, :]) @ Q.T
+    return 0.5 * (A + A.T)
+
+
+def sym_indefinite(n: int, lo: float, seed: int) -> np.ndarray:
+    lam = np.logspace(0.0, np.log10(lo), n) * np.where(np.arange(n) % 2 == 0, 1.0, -1.0)
     Q = haar(n, n, seed)
     A = (Q * lam[None, :]) @ Q.T
     return 0.5 * (A + A.T)
