@@ -62,6 +62,13 @@ def workload(name: str, rank: int):
         desc = ("Shampoo step (configs[2]): 8x1024 + 4x2048 + 2x4096 SPD blocks, lambda log-spaced, kappa=1e2, "
                 "FP32 (3xTF32) coupled sqrt/inv-sqrt, PRISM-5, tol 1e-5")
         return "shampoo-sqrt-step", shapes, mats, opts, desc, "sqrt"
+    if name == "sign4096":
+        shapes = [(4096, 4096)]
+        mats = [W.sym_indefinite(4096, 1e-2, seed=4096 + rank)]
+        opts = dict(degree=5, max_iters=25, tol=3e-2, sketch_size=8, seed=42, precision="bf16")
+        desc = ("single 4096x4096 symmetric indefinite BF16 matrix sign (case study P:145-199; |lambda| "
+                "log-spaced in [1e-2, 1], alternating signs), PRISM-5, p=8, tol 3e-2")
+        return "sign-4096", shapes, mats, opts, desc, "sign"
     raise SystemExit(f"unknown workload {name}")
 
 
@@ -145,6 +152,9 @@ def cpu_oracle_solve(A, kind, opts, b):
     if kind == "polar":
         return prism.polar(A, d=d, p=opts["sketch_size"], tol=opts["tol"], max_iters=opts["max_iters"],
                            seed=opts["seed"], b=b)[1]
+    if kind == "sign":
+        return prism.sign(A, d=d, p=opts["sketch_size"], tol=opts["tol"], max_iters=opts["max_iters"],
+                          seed=opts["seed"], b=b)[1]
     return prism.sqrt_invsqrt(A, d=d, p=opts["sketch_size"], tol=opts["tol"], max_iters=opts["max_iters"],
                               seed=opts["seed"], b=b)[2]
 
@@ -212,7 +222,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="prism", choices=["prism", "reference"])
-    ap.add_argument("--workload", default="gpt2", choices=["gpt2", "square4096", "gpt1b", "shampoo"])
+    ap.add_argument("--workload", default="gpt2", choices=["gpt2", "square4096", "gpt1b", "shampoo", "sign4096"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)   # timing rule: >= 3 warm-up steps
@@ -244,9 +254,11 @@ def main():
     def solve(inputs, out=None):
         if kind == "polar":
             return P.polar(inputs, out=out, matrix_ids=ids, handle=h, **opts)
+        if kind == "sign":
+            return P.sign(inputs, out=out, matrix_ids=ids, handle=h, **opts)
         return P.sqrt_invsqrt(inputs, matrix_ids=ids, handle=h, **opts)
 
-    outs = [torch.empty_like(m) for m in mats] if kind == "polar" else None
+    outs = [torch.empty_like(m) for m in mats] if kind in ("polar", "sign") else None
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     clocks = ClockSampler(local)
     clocks.start()                      # sampled from the timed region to the end of the GPU passes
@@ -282,6 +294,10 @@ def main():
     status = rep["status"].cpu().tolist()
     if kind == "polar":
         f_iter = [P.polar_flops_per_iter(m, n, opts["degree"], opts["sketch_size"]) for (m, n) in shapes]
+    elif kind == "sign":
+        # general (non-symmetric-kernel) products: X.X, R.R (d = 2), X.P, plus the sketch
+        f_iter = [4.0 * m ** 3 + ((2.0 * m ** 3 + 14.0 * m * m * opts["sketch_size"]) if opts["degree"] == 5
+                                  else 6.0 * m * m * opts["sketch_size"]) for (m, _) in shapes]
     else:
         f_iter = [P.sqrt_flops_per_iter(m, opts["degree"], opts["sketch_size"]) for (m, _) in shapes]
     flops_step = sum(f * k for f, k in zip(f_iter, iters))
@@ -297,6 +313,8 @@ def main():
     def solve_host():
         if kind == "polar":
             return P.polar_host(host, out=host_out, matrix_ids=ids, handle=h, **opts)
+        if kind == "sign":
+            return P.sign_host(host, out=host_out, matrix_ids=ids, handle=h, **opts)
         return P.sqrt_invsqrt_host(host, matrix_ids=ids, handle=h, want_sqrt=False, **opts)[1:]
 
     for _ in range(4):   # warm: every staging slot's buffers and plan
@@ -334,6 +352,10 @@ def main():
         apply_flops = sum(2.0 * max(m, n) * min(m, n) ** 2 * k for (m, n), k in zip(shapes, iters)) * args.steps
         gram_flops = sum(max(m, n) * min(m, n) * (min(m, n) + 1) * (k + 1) for (m, n), k in zip(shapes, iters)) * args.steps
         sq_flops = sum(min(m, n) ** 2 * (min(m, n) + 1) * k for (m, n), k in zip(shapes, iters)) * args.steps
+    elif kind == "sign":
+        apply_flops = sum(2.0 * m ** 3 * k for (m, _), k in zip(shapes, iters)) * args.steps
+        gram_flops = sum(2.0 * m ** 3 * (k + 1) for (m, _), k in zip(shapes, iters)) * args.steps
+        sq_flops = sum(2.0 * m ** 3 * k for (m, _), k in zip(shapes, iters)) * args.steps
     else:
         apply_flops = sum(4.0 * m ** 3 * k for (m, _), k in zip(shapes, iters)) * args.steps
         gram_flops = sum(2.0 * m ** 3 * (k + 1) for (m, _), k in zip(shapes, iters)) * args.steps
@@ -379,7 +401,7 @@ def main():
                        "max_iters": opts["max_iters"], "precision": opts["precision"],
                        "l2": "flushed (256 MiB write) before every timed step, outside the events",
                        "parallelism": f"independent batch per GPU x{world}",
-                       "e2e_path": "prism_polar_host / prism_sqrt_invsqrt_host: pinned host inputs uploaded and "
+                       "e2e_path": "prism_polar_host / prism_sqrt_invsqrt_host / prism_sign_host: pinned host inputs uploaded and "
                                    "results downloaded every step; steps pipelined (copies overlap solves)"},
             "tflops": tflops, "tflops_unit": "F_min (symmetric products once) per second",
             "frac_of_peak_sustained": tflops / peak if peak else None,

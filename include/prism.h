@@ -158,6 +158,11 @@ prism_status prism_sign(prism_handle h, int batch, const int64_t* n, const void*
                         void* const* S, const int64_t* lds, const int64_t* matrix_ids, const prism_options* o,
                         const prism_report* rep, void* workspace, size_t ws_bytes, void* stream);
 
+/* prism_sign on page-locked HOST buffers, pipelined as prism_polar_host. */
+prism_status prism_sign_host(prism_handle h, int batch, const int64_t* n, const void* const* A, const int64_t* lda,
+                             void* const* S, const int64_t* lds, const int64_t* matrix_ids, const prism_options* o,
+                             const prism_report* rep, void* stream);
+
 /* prism_sqrt_invsqrt on page-locked HOST buffers, pipelined as prism_polar_host. */
 prism_status prism_sqrt_invsqrt_host(prism_handle h, int batch, const int64_t* n, const void* const* A,
                                      const int64_t* lda, void* const* Asqrt, void* const* Ainvsqrt,

@@ -1135,18 +1135,20 @@ static cudaError_t copy_block(void* dst, size_t dld, const void* src, size_t sld
 }
 
 // End-to-end path on host buffers (see prism.h): stage, solve, return, pipelined.
-static prism_status host_solve(prism_handle h, bool sqrt_kind, int batch, const int64_t* m, const int64_t* n,
+// kind: 0 polar, 1 sqrt / inverse sqrt, 2 sign (square inputs for 1 and 2)
+static prism_status host_solve(prism_handle h, int kind, int batch, const int64_t* m, const int64_t* n,
                                const void* const* A_host, const int64_t* lda, void* const* O1, void* const* O2,
                                const int64_t* ldo, const int64_t* ids, const prism_options* o,
                                const prism_report* rep, cudaStream_t caller) {
   if (!h || !o) return fail(PRISM_ERR_INVALID_ARG, "null handle / options");
-  if (batch < 1 || !m || !A_host || !lda || !ldo || (!sqrt_kind && (!n || !O1)))
+  const bool sqrt_kind = kind == 1, square = kind != 0;
+  if (batch < 1 || !m || !A_host || !lda || !ldo || (kind == 0 && !n) || (!sqrt_kind && !O1))
     return fail(PRISM_ERR_INVALID_ARG, "bad host-path arguments");
   const size_t esz = (size_t)elem_size(o->precision);
   // compact device staging (ld = n)
   std::vector<size_t> off(batch + 1, 0);
   for (int i = 0; i < batch; ++i) {
-    const int64_t mm = m[i], nn = sqrt_kind ? m[i] : n[i];
+    const int64_t mm = m[i], nn = square ? m[i] : n[i];
     if (mm < 1 || nn < 1 || lda[i] < nn || ldo[i] < nn) return fail(PRISM_ERR_INVALID_ARG, "bad host-path shape");
     off[i + 1] = off[i] + align_up((size_t)(mm * nn) * esz, 256);
   }
@@ -1169,7 +1171,9 @@ static prism_status host_solve(prism_handle h, bool sqrt_kind, int batch, const 
   auto& sl = h->slots[h->slot_next];
   h->slot_next = (h->slot_next + 1) % nslots;
   const bool two = sqrt_kind && O1 && O2;
-  const size_t ws_need = sqrt_kind ? prism_sqrt_workspace(h, batch, m, o) : prism_polar_workspace(h, batch, m, n, o);
+  const size_t ws_need = sqrt_kind ? prism_sqrt_workspace(h, batch, m, o)
+                         : kind == 2 ? prism_sign_workspace(h, batch, m, o)
+                                     : prism_polar_workspace(h, batch, m, n, o);
   if (!ws_need) return fail(PRISM_ERR_INVALID_ARG, "workspace query failed");
   if (sl.in_bytes < bytes || sl.out_bytes < bytes || (two && !sl.out2) || h->hws_bytes < ws_need) {
     PRISM_CK(cudaDeviceSynchronize());   // growing: nothing of the old buffers may be in flight
@@ -1191,7 +1195,7 @@ static prism_status host_solve(prism_handle h, bool sqrt_kind, int batch, const 
     }
   }
   for (int i = 0; i < batch; ++i) {
-    ldc[i] = sqrt_kind ? m[i] : n[i];
+    ldc[i] = square ? m[i] : n[i];
     din[i] = sl.in + off[i];
     dout[i] = sl.out + off[i];
     dout2[i] = sl.out2 ? sl.out2 + off[i] : nullptr;
@@ -1219,6 +1223,9 @@ static prism_status host_solve(prism_handle h, bool sqrt_kind, int batch, const 
   if (sqrt_kind)
     st = prism_sqrt_invsqrt(h, batch, m, din.data(), ldc.data(), O1 ? dout.data() : nullptr,
                             O2 ? dout2.data() : nullptr, ldc.data(), ids, o, rep, h->hws, h->hws_bytes, h->s_comp);
+  else if (kind == 2)
+    st = prism_sign(h, batch, m, din.data(), ldc.data(), dout.data(), ldc.data(), ids, o, rep, h->hws, h->hws_bytes,
+                    h->s_comp);
   else
     st = prism_polar(h, batch, m, n, din.data(), ldc.data(), dout.data(), ldc.data(), ids, o, rep, h->hws,
                      h->hws_bytes, h->s_comp);
@@ -1260,7 +1267,7 @@ prism_status prism_polar_host(prism_handle h, int batch, const int64_t* m, const
                               const int64_t* lda, void* const* Q, const int64_t* ldq, const int64_t* matrix_ids,
                               const prism_options* o, const prism_report* rep, void* stream) {
   try {
-    return host_solve(h, false, batch, m, n, A, lda, Q, nullptr, ldq, matrix_ids, o, rep,
+    return host_solve(h, 0, batch, m, n, A, lda, Q, nullptr, ldq, matrix_ids, o, rep,
                       static_cast<cudaStream_t>(stream));
   } catch (...) {
     return fail(PRISM_ERR_INTERNAL, "exception in prism_polar_host");
@@ -1272,10 +1279,21 @@ prism_status prism_sqrt_invsqrt_host(prism_handle h, int batch, const int64_t* n
                                      const int64_t* ld_out, const int64_t* matrix_ids, const prism_options* o,
                                      const prism_report* rep, void* stream) {
   try {
-    return host_solve(h, true, batch, n, n, A, lda, Asqrt, Ainvsqrt, ld_out, matrix_ids, o, rep,
+    return host_solve(h, 1, batch, n, n, A, lda, Asqrt, Ainvsqrt, ld_out, matrix_ids, o, rep,
                       static_cast<cudaStream_t>(stream));
   } catch (...) {
     return fail(PRISM_ERR_INTERNAL, "exception in prism_sqrt_invsqrt_host");
+  }
+}
+
+prism_status prism_sign_host(prism_handle h, int batch, const int64_t* n, const void* const* A, const int64_t* lda,
+                             void* const* S, const int64_t* lds, const int64_t* matrix_ids, const prism_options* o,
+                             const prism_report* rep, void* stream) {
+  try {
+    return host_solve(h, 2, batch, n, n, A, lda, S, nullptr, lds, matrix_ids, o, rep,
+                      static_cast<cudaStream_t>(stream));
+  } catch (...) {
+    return fail(PRISM_ERR_INTERNAL, "exception in prism_sign_host");
   }
 }
 

@@ -83,3 +83,16 @@ def test_sign_zero_input():
     torch.cuda.synchronize()
     assert int(rep["status"][0]) == prism.ZERO_INPUT
     assert not torch.any(S[0])
+
+
+def test_sign_host_path_equals_device_path():
+    sizes = [128, 700]
+    dev = [torch.tensor(W.sym_indefinite(s, 5e-2, seed=300 + s)).to(torch.bfloat16).cuda() for s in sizes]
+    host = [d.cpu().pin_memory() for d in dev]
+    S, rep = P.sign(dev, tol=3e-2, max_iters=30, seed=42, precision="bf16")
+    for _ in range(3):   # pipelined successive calls over the staging slots
+        Sh, reph = P.sign_host(host, tol=3e-2, max_iters=30, seed=42, precision="bf16")
+    torch.cuda.synchronize()
+    for a, b in zip(S, Sh):
+        assert torch.equal(a.cpu(), b)
+    assert torch.equal(rep["iters"], reph["iters"])
