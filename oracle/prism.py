@@ -16,6 +16,11 @@ Coupled square root (Table 1 rows P:246-250, Theorem 3; R11):
     A^{1/2} ~ sqrt(c) X,  A^{-1/2} ~ Y / sqrt(c)
 Matrix sign (the paper's case study, eq. 2; A^2 symmetric):
     X_0 = A/||A||_F, R_k = I - X_k^2, X_{k+1} = X_k g_d(R_k; a_k)
+Coupled inverse Newton A^{-1/q} (Appendix A.3; q = the paper's p):
+    c = (2||A||_F/(q+1))^{1/q}, X_0 = I/c, M_0 = A/c^q, R_k = I - M_k
+    X_{k+1} = X_k (I + a_k R_k),  M_{k+1} = (I + a_k R_k)^q M_k
+    loss of degree 2q, argmin analytic for q <= 2, companion-matrix
+    roots of m' for q >= 3; interval [1/(2q), 2/q] (R22).
 Coefficient a_k (eq. (4)):
     a_k = argmin_{a in [l,u]} || S_k (I - (I-R_k) g_d(R_k;a)^2) ||_F^2
         = argmin m(a),  m(a) = c0 + c1 a + c2 a^2 + c3 a^3 + c4 a^4
@@ -397,6 +402,149 @@ def sign(A, d: int = 2, p: int = 8, tol: float = 1e-10, max_iters: int = 50,
         a = _choose_alpha(k, R, d, fit, p, seed, b, n, warmup, lo, hi, aT, rep)
         rep.alphas.append(a)
         X = X @ g_matrix(R, a, d)              # X_{k+1} = X_k g_d(R_k; a_k)
+        k += 1
+    rep.iters = k
+    return X, rep
+
+
+# --------------------------------------------------------------------------
+# Coupled inverse Newton for A^{-1/p} (Appendix A.3)
+# --------------------------------------------------------------------------
+# The root order is called q here (the paper's p) because p already
+# names the sketch size (the paper's m; R6).
+
+def inv_root_interval(q: int) -> tuple[float, float, float]:
+    """(l, u, a_Taylor) for the inverse q-th root: [1/(2q), 2/q], Taylor 1/q.
+
+    The paper defines a_k with a constraint a in [l, u] but never states
+    the interval (R22).  Taylor: f_1(xi) = 1 + xi/q.  The bracket [a_T/2,
+    2 a_T] mirrors d=1's [1/2, 1] around its Taylor 1/2; with M_0's
+    spectrum in (0, (q+1)/2] it keeps 1 + a xi > 0.
+    """
+    if q < 1:
+        raise ValueError("q >= 1")
+    return 0.5 / q, 2.0 / q, 1.0 / q
+
+
+def inv_root_loss_coeffs(t: np.ndarray, q: int) -> np.ndarray:
+    """c_0..c_{2q} of m(a) = ||S (R + sum_{i=1}^q C(q,i) a^i (R^{i+1} - R^i))||_F^2.
+
+    P:562-566 (loss), expanded for symmetric R: the bracket is
+    sum_i a^i B_i with B_0 = R, B_i = C(q,i)(R^{i+1} - R^i) (polynomials in R),
+    so m(a) = sum_{i,j} a^{i+j} tr(S B_i B_j S^T) and each product is a
+    combination of t_j = tr(S R^j S^T), j = 2..2q+2.  P:570-590 print the
+    result for q = 1, 2 (pinned against it in the tests).
+    """
+    # B_i as coefficient vectors over powers of R (index = power)
+    B = []
+    b0 = np.zeros(q + 2)
+    b0[1] = 1.0
+    B.append(b0)
+    for i in range(1, q + 1):
+        bi = np.zeros(q + 2)
+        bi[i + 1] += math.comb(q, i)
+        bi[i] -= math.comb(q, i)
+        B.append(bi)
+    c = np.zeros(2 * q + 1)
+    for i in range(q + 1):
+        for j in range(q + 1):
+            prod = np.convolve(B[i], B[j])          # B_i B_j as powers of R
+            c[i + j] += float(np.dot(prod, t[: prod.size]))
+    return c
+
+
+def argmin_poly(c: np.ndarray, lo: float, hi: float, alpha_taylor: float) -> float:
+    """argmin_{a in [lo, hi]} of m(a) = sum_i c_i a^i (degree 2q).
+
+    Degree <= 4 (q <= 2, "analytically", P:591): argmin_quartic.  Degree > 4
+    (q >= 3): the real roots of m'(a) = 0 as eigenvalues of its companion
+    matrix (numpy.roots), then m at {lo, hi} and the roots inside,
+    smallest m wins (ties -> smaller a); degenerate loss -> Taylor (R15).
+    """
+    c = np.asarray(c, dtype=np.float64)
+    if c.size <= 5:
+        return argmin_quartic(np.concatenate([c, np.zeros(5 - c.size)]), lo, hi, alpha_taylor)
+    scale = float(np.max(np.abs(c[1:])))
+    if not np.isfinite(scale):
+        return alpha_taylor
+    if scale == 0.0 or scale <= 1e-14 * abs(float(c[0])):
+        return alpha_taylor
+    d = c / scale
+    deriv = np.array([i * d[i] for i in range(1, d.size)])          # m' coefficients, ascending
+    nz = np.nonzero(np.abs(deriv) > 1e-12 * np.max(np.abs(deriv)))[0]
+    deriv = deriv[: nz[-1] + 1]
+    roots = np.roots(deriv[::-1]) if deriv.size > 1 else np.array([])
+
+    def m(a):  # c0 dropped: argmin-invariant
+        return float(np.polyval(d[:0:-1], a) * a)
+
+    cands = [lo, hi]
+    for r in roots:
+        if abs(r.imag) <= 1e-9 * (1.0 + abs(r.real)) and lo <= r.real <= hi:
+            cands.append(float(r.real))
+    cands.sort()
+    best, best_m = cands[0], m(cands[0])
+    for a in cands[1:]:
+        ma = m(a)
+        if ma < best_m:
+            best, best_m = a, ma
+    return best
+
+
+def inv_root(A, q: int = 4, p: int = 8, tol: float = 1e-10, max_iters: int = 50,
+             seed: int = 0, b: int = 0, warmup: int = 0, fit: str = FIT_SKETCHED,
+             alpha_lo: float | None = None, alpha_hi: float | None = None):
+    """PRISM coupled inverse Newton A^{-1/q} of an SPD A in fp64.
+
+        c = (2 ||A||_F / (q+1))^{1/q},  X_0 = I/c,  M_0 = A/c^q      (P:551-553)
+        R_k = I - M_k
+        X_{k+1} = X_k (I + a_k R_k),  M_{k+1} = (I + a_k R_k)^q M_k
+        a_k = argmin_{[l,u]} ||S_k (R_k + sum_i C(q,i) a^i (R_k^{i+1} - R_k^i))||_F^2
+
+    Stop test, sketch and statuses as polar (R8, R12); Taylor a = 1/q is the
+    classical coupled inverse Newton.  Returns (X, Report).
+    """
+    A = np.asarray(A, dtype=np.float64)
+    n = A.shape[0]
+    lo, hi, aT = inv_root_interval(q)
+    lo = lo if alpha_lo is None else alpha_lo
+    hi = hi if alpha_hi is None else alpha_hi
+    rep = Report()
+    nrm = math.sqrt(float(np.sum(A * A)))
+    if nrm == 0.0:
+        rep.status = ZERO_INPUT
+        return np.zeros_like(A), rep
+    cq = 2.0 * nrm / (q + 1)                   # c^q (P:553)
+    c = cq ** (1.0 / q)
+    I = np.eye(n)
+    X = I / c                                  # X_0 = I/c
+    M = A / cq                                 # M_0 = A/c^q
+    incr = 0
+    r_prev = math.inf
+    k = 0
+    while True:
+        R = I - M                              # R_k = I - M_k (P:556)
+        r = float(np.linalg.norm(R, "fro"))
+        stop, incr = _status_update(rep, k, r, r_prev, n, tol, max_iters, incr)
+        r_prev = r
+        if stop:
+            break
+        if k < warmup:
+            a = hi
+        elif fit == FIT_TAYLOR:
+            a = aT
+        else:
+            if fit == FIT_EXACT:
+                t = exact_traces(R, 2 * q + 2)
+            else:
+                t = sketched_traces(R, gaussian_sketch(seed, b, k, p, n), 2 * q + 2)
+            cf = inv_root_loss_coeffs(t, q)
+            rep.coeffs.append(cf)
+            a = argmin_poly(cf, lo, hi, aT)
+        rep.alphas.append(a)
+        G = I + a * R                          # I + a_k R_k
+        X = X @ G                              # X_{k+1} = X_k (I + a_k R_k)
+        M = np.linalg.matrix_power(G, q) @ M   # M_{k+1} = (I + a_k R_k)^q M_k
         k += 1
     rep.iters = k
     return X, rep
