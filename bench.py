@@ -69,6 +69,13 @@ def workload(name: str, rank: int):
         desc = ("single 4096x4096 symmetric indefinite BF16 matrix sign (case study P:145-199; |lambda| "
                 "log-spaced in [1e-2, 1], alternating signs), PRISM-5, p=8, tol 3e-2")
         return "sign-4096", shapes, mats, opts, desc, "sign"
+    if name == "invroot":
+        shapes = [(1024, 1024)] * 8 + [(2048, 2048)] * 4 + [(4096, 4096)] * 2
+        mats = [W.spd_logspaced(m, 1e2, seed=100 * rank + i) for i, (m, _) in enumerate(shapes)]
+        opts = dict(q=4, max_iters=30, tol=1e-5, sketch_size=8, seed=42, precision="fp32")
+        desc = ("Shampoo step with the classic inverse 4th root (configs[2] blocks: 8x1024 + 4x2048 + 2x4096 SPD, "
+                "kappa=1e2, FP32 3xTF32): PRISM coupled inverse Newton A^{-1/4} (P:549-566), tol 1e-5")
+        return "shampoo-invroot4-step", shapes, mats, opts, desc, "inv_root"
     raise SystemExit(f"unknown workload {name}")
 
 
@@ -148,13 +155,16 @@ def flush_l2(buf):
 
 def cpu_oracle_solve(A, kind, opts, b):
     from oracle import prism
-    d = 1 if opts["degree"] == 3 else 2
+    d = 1 if opts.get("degree", 5) == 3 else 2
     if kind == "polar":
         return prism.polar(A, d=d, p=opts["sketch_size"], tol=opts["tol"], max_iters=opts["max_iters"],
                            seed=opts["seed"], b=b)[1]
     if kind == "sign":
         return prism.sign(A, d=d, p=opts["sketch_size"], tol=opts["tol"], max_iters=opts["max_iters"],
                           seed=opts["seed"], b=b)[1]
+    if kind == "inv_root":
+        return prism.inv_root(A, q=opts["q"], p=opts["sketch_size"], tol=opts["tol"], max_iters=opts["max_iters"],
+                              seed=opts["seed"], b=b)[1]
     return prism.sqrt_invsqrt(A, d=d, p=opts["sketch_size"], tol=opts["tol"], max_iters=opts["max_iters"],
                               seed=opts["seed"], b=b)[2]
 
@@ -222,7 +232,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="prism", choices=["prism", "reference"])
-    ap.add_argument("--workload", default="gpt2", choices=["gpt2", "square4096", "gpt1b", "shampoo", "sign4096"])
+    ap.add_argument("--workload", default="gpt2", choices=["gpt2", "square4096", "gpt1b", "shampoo", "sign4096", "invroot"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)   # timing rule: >= 3 warm-up steps
@@ -256,9 +266,11 @@ def main():
             return P.polar(inputs, out=out, matrix_ids=ids, handle=h, **opts)
         if kind == "sign":
             return P.sign(inputs, out=out, matrix_ids=ids, handle=h, **opts)
+        if kind == "inv_root":
+            return P.inv_root(inputs, out=out, matrix_ids=ids, handle=h, **opts)
         return P.sqrt_invsqrt(inputs, matrix_ids=ids, handle=h, **opts)
 
-    outs = [torch.empty_like(m) for m in mats] if kind in ("polar", "sign") else None
+    outs = [torch.empty_like(m) for m in mats] if kind in ("polar", "sign", "inv_root") else None
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     clocks = ClockSampler(local)
     clocks.start()                      # sampled from the timed region to the end of the GPU passes
@@ -294,6 +306,11 @@ def main():
     status = rep["status"].cpu().tolist()
     if kind == "polar":
         f_iter = [P.polar_flops_per_iter(m, n, opts["degree"], opts["sketch_size"]) for (m, n) in shapes]
+    elif kind == "inv_root":
+        # X + aX.R, M + P_q.M, the POLY products of P_q (1 for q = 2, 2 for q = 3, 4), chain
+        npoly = {1: 0, 2: 1, 3: 2, 4: 2}[opts["q"]]
+        f_iter = [(4.0 + 2.0 * npoly) * m ** 3 + 2.0 * (opts["q"] + 1) * m * m * opts["sketch_size"]
+                  for (m, _) in shapes]
     elif kind == "sign":
         # general (non-symmetric-kernel) products: X.X, R.R (d = 2), X.P, plus the sketch
         f_iter = [4.0 * m ** 3 + ((2.0 * m ** 3 + 14.0 * m * m * opts["sketch_size"]) if opts["degree"] == 5
@@ -315,6 +332,8 @@ def main():
             return P.polar_host(host, out=host_out, matrix_ids=ids, handle=h, **opts)
         if kind == "sign":
             return P.sign_host(host, out=host_out, matrix_ids=ids, handle=h, **opts)
+        if kind == "inv_root":
+            return P.inv_root_host(host, out=host_out, matrix_ids=ids, handle=h, **opts)
         return P.sqrt_invsqrt_host(host, matrix_ids=ids, handle=h, want_sqrt=False, **opts)[1:]
 
     for _ in range(4):   # warm: every staging slot's buffers and plan
@@ -352,6 +371,11 @@ def main():
         apply_flops = sum(2.0 * max(m, n) * min(m, n) ** 2 * k for (m, n), k in zip(shapes, iters)) * args.steps
         gram_flops = sum(max(m, n) * min(m, n) * (min(m, n) + 1) * (k + 1) for (m, n), k in zip(shapes, iters)) * args.steps
         sq_flops = sum(min(m, n) ** 2 * (min(m, n) + 1) * k for (m, n), k in zip(shapes, iters)) * args.steps
+    elif kind == "inv_root":
+        npoly = {1: 0, 2: 1, 3: 2, 4: 2}[opts["q"]]
+        apply_flops = sum(4.0 * m ** 3 * k for (m, _), k in zip(shapes, iters)) * args.steps
+        gram_flops = 0.0   # R = I - M is elementwise (k_resid_inv)
+        sq_flops = sum(2.0 * npoly * m ** 3 * k for (m, _), k in zip(shapes, iters)) * args.steps
     elif kind == "sign":
         apply_flops = sum(2.0 * m ** 3 * k for (m, _), k in zip(shapes, iters)) * args.steps
         gram_flops = sum(2.0 * m ** 3 * (k + 1) for (m, _), k in zip(shapes, iters)) * args.steps
@@ -397,11 +421,11 @@ def main():
             "vs_baseline": None, "dtype": opts["precision"],
             "data": "synthetic: seeded matrices shaped like the paper's workloads (no datasets)",
             "config": {"workload": name, "description": desc, "matrices_per_gpu": B, "solver": kind,
-                       "degree": opts["degree"], "sketch_size": opts["sketch_size"], "tol": opts["tol"],
+                       "degree": opts.get("degree"), "q": opts.get("q"), "sketch_size": opts["sketch_size"], "tol": opts["tol"],
                        "max_iters": opts["max_iters"], "precision": opts["precision"],
                        "l2": "flushed (256 MiB write) before every timed step, outside the events",
                        "parallelism": f"independent batch per GPU x{world}",
-                       "e2e_path": "prism_polar_host / prism_sqrt_invsqrt_host / prism_sign_host: pinned host inputs uploaded and "
+                       "e2e_path": "prism_*_host (the kind's host-buffer entry point): pinned host inputs uploaded and "
                                    "results downloaded every step; steps pipelined (copies overlap solves)"},
             "tflops": tflops, "tflops_unit": "F_min (symmetric products once) per second",
             "frac_of_peak_sustained": tflops / peak if peak else None,

@@ -158,6 +158,27 @@ prism_status prism_sign(prism_handle h, int batch, const int64_t* n, const void*
                         void* const* S, const int64_t* lds, const int64_t* matrix_ids, const prism_options* o,
                         const prism_report* rep, void* workspace, size_t ws_bytes, void* stream);
 
+/*
+ * Inverse q-th root A^{-1/q} of SPD n[i] x n[i] matrices by the PRISM-accelerated
+ * coupled inverse Newton iteration (Appendix A.3; the paper's p is q here):
+ *   c = (2||A||_F/(q+1))^{1/q},  X_0 = I/c,  M_0 = A/c^q,  R_k = I - M_k,
+ *   X_{k+1} = X_k (I + a_k R_k),  M_{k+1} = (I + a_k R_k)^q M_k,
+ *   a_k = argmin over [1/(2q), 2/q] (overridable by alpha_lo/hi) of the sketched
+ *   degree-2q loss ||S_k (R_k + sum_i C(q,i) a^i (R_k^{i+1} - R_k^i))||_F^2.
+ * q in 1..4 (PRISM_ERR_UNSUPPORTED otherwise); options.degree is ignored (the method is
+ * first order); fit SKETCHED or TAYLOR (a = 1/q: the classical coupled inverse Newton).
+ * X[i] receives A_i^{-1/q} (ld ldx[i]; may alias A).  Other arguments as prism_polar.
+ */
+size_t prism_inv_root_workspace(prism_handle h, int batch, const int64_t* n, int q, const prism_options* o);
+prism_status prism_inv_root(prism_handle h, int batch, const int64_t* n, int q, const void* const* A,
+                            const int64_t* lda, void* const* X, const int64_t* ldx, const int64_t* matrix_ids,
+                            const prism_options* o, const prism_report* rep, void* workspace, size_t ws_bytes,
+                            void* stream);
+/* prism_inv_root on page-locked HOST buffers, pipelined as prism_polar_host. */
+prism_status prism_inv_root_host(prism_handle h, int batch, const int64_t* n, int q, const void* const* A,
+                                 const int64_t* lda, void* const* X, const int64_t* ldx, const int64_t* matrix_ids,
+                                 const prism_options* o, const prism_report* rep, void* stream);
+
 /* prism_sign on page-locked HOST buffers, pipelined as prism_polar_host. */
 prism_status prism_sign_host(prism_handle h, int batch, const int64_t* n, const void* const* A, const int64_t* lda,
                              void* const* S, const int64_t* lds, const int64_t* matrix_ids, const prism_options* o,
@@ -238,7 +259,7 @@ prism_status prism_debug_sketch(uint64_t seed, int64_t b, int k, int p, int s, f
 /* Device quartic argmin on [lo, hi] (R15/R16): n problems, c_dev[5*n] -> alpha_dev[n]. */
 prism_status prism_debug_argmin(int n, const double* c_dev, double lo, double hi, double a_taylor,
                                 double* alpha_dev, void* stream);
-/* Chain-pass timeline (diagnostics only): buf_dev = device u64[8 * 1024 * 16] receiving
+/* Chain-pass timeline (diagnostics only): buf_dev = device u64[13 * 1024 * 16] (one block per pass code) receiving
  * per-pass-code, per-CTA globaltimer stamps of later chain launches; NULL disables. */
 prism_status prism_debug_trace_chain(unsigned long long* buf_dev);
 /* Main-GEMM k-block timeline (diagnostics only): buf_dev = device u64[148 * 192]; launches

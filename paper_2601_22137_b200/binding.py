@@ -56,6 +56,7 @@ EXPORTS = [
     "prism_default_options", "prism_create", "prism_destroy", "prism_last_error", "prism_abi_version",
     "prism_polar_workspace", "prism_polar", "prism_sqrt_workspace", "prism_sqrt_invsqrt",
     "prism_polar_host", "prism_sqrt_invsqrt_host", "prism_sign_workspace", "prism_sign", "prism_sign_host",
+    "prism_inv_root_workspace", "prism_inv_root", "prism_inv_root_host",
     "prism_lpt_partition", "prism_polar_flops_per_iter", "prism_sqrt_flops_per_iter",
     "prism_launch_count", "prism_profile_enable", "prism_profile_read",
     "prism_rowblock_workspace", "prism_rowblock_begin", "prism_rowblock_gram", "prism_rowblock_update",
@@ -107,6 +108,12 @@ def lib():
                                  ctypes.POINTER(Options), ctypes.POINTER(Report), vp, sz, vp]
         L.prism_sign_host.argtypes = [vp, i32, c_i64p, ctypes.POINTER(vp), c_i64p, ctypes.POINTER(vp), c_i64p,
                                       c_i64p, ctypes.POINTER(Options), ctypes.POINTER(Report), vp]
+        L.prism_inv_root_workspace.argtypes = [vp, i32, c_i64p, i32, ctypes.POINTER(Options)]
+        L.prism_inv_root_workspace.restype = sz
+        L.prism_inv_root.argtypes = [vp, i32, c_i64p, i32, ctypes.POINTER(vp), c_i64p, ctypes.POINTER(vp), c_i64p,
+                                     c_i64p, ctypes.POINTER(Options), ctypes.POINTER(Report), vp, sz, vp]
+        L.prism_inv_root_host.argtypes = [vp, i32, c_i64p, i32, ctypes.POINTER(vp), c_i64p, ctypes.POINTER(vp),
+                                          c_i64p, c_i64p, ctypes.POINTER(Options), ctypes.POINTER(Report), vp]
         L.prism_lpt_partition.argtypes = [i32, ctypes.POINTER(dbl), i32, ctypes.POINTER(ctypes.c_int32)]
         L.prism_polar_flops_per_iter.argtypes = [i64, i64, i32, i32]
         L.prism_polar_flops_per_iter.restype = dbl
@@ -129,7 +136,7 @@ def lib():
         L.prism_debug_trace_gemm.argtypes = [vp, i32]
         L.prism_debug_trace_chain.argtypes = [vp]
         for name in ("prism_create", "prism_destroy", "prism_polar", "prism_sqrt_invsqrt", "prism_lpt_partition",
-                     "prism_polar_host", "prism_sqrt_invsqrt_host", "prism_sign", "prism_sign_host",
+                     "prism_polar_host", "prism_sqrt_invsqrt_host", "prism_sign", "prism_sign_host", "prism_inv_root", "prism_inv_root_host",
                      "prism_debug_gemm", "prism_debug_sketch", "prism_debug_argmin",
                      "prism_debug_trace_gemm", "prism_debug_trace_chain", "prism_profile_enable", "prism_profile_read", "prism_rowblock_begin",
                      "prism_rowblock_gram", "prism_rowblock_update", "prism_rowblock_end"):
@@ -459,6 +466,71 @@ def sign_host(mats, degree=5, max_iters=30, sketch_size=8, tol=1e-6, seed=42, pr
                                 _i64([t.stride(0) for t in mats]), _ptrs(out), _i64([t.stride(0) for t in out]), ids,
                                 ctypes.byref(o), ctypes.byref(rep), ctypes.c_void_p(st.cuda_stream)),
           "prism_sign_host")
+    return out, rb
+
+
+def inv_root(mats, q=4, max_iters=30, sketch_size=8, tol=1e-6, seed=42, precision=None, fit="sketched",
+             warmup_iters=0, alpha_lo=None, alpha_hi=None, out=None, matrix_ids=None, stream=None, handle=None):
+    """A^{-1/q} of a batch of SPD CUDA matrices via prism_inv_root (coupled inverse
+    Newton, P:549-566; q in 1..4)."""
+    import torch
+    mats = list(mats)
+    if not mats:
+        return [], {}
+    precision = _precision_of(mats[0], precision)
+    _check_dtype(mats, precision)
+    for t in mats:
+        if t.shape[0] != t.shape[1]:
+            raise PrismError("inv_root: matrices must be square")
+    dev = mats[0].device
+    h = handle or default_handle()
+    o = make_options(5, max_iters, sketch_size, tol, seed, precision, fit, warmup_iters, alpha_lo, alpha_hi)
+    B = len(mats)
+    n = _i64([t.shape[0] for t in mats])
+    if out is None:
+        out = [torch.empty_like(t) for t in mats]
+    _check_dtype(out, precision)
+    need = lib().prism_inv_root_workspace(h.h, B, n, int(q), ctypes.byref(o))
+    if need == 0:
+        raise PrismError("prism_inv_root_workspace rejected the arguments: " + lib().prism_last_error().decode())
+    ws = h.workspace(need, dev)
+    rb = _report_buffers(B, max_iters, dev)
+    rep = _report_struct(rb)
+    ids = _i64(matrix_ids) if matrix_ids is not None else None
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    check(lib().prism_inv_root(h.h, B, n, int(q), _ptrs(mats), _i64([t.stride(0) for t in mats]), _ptrs(out),
+                               _i64([t.stride(0) for t in out]), ids, ctypes.byref(o), ctypes.byref(rep),
+                               ws.data_ptr(), ws.numel(), ctypes.c_void_p(st.cuda_stream)), "prism_inv_root")
+    return out, rb
+
+
+def inv_root_host(mats, q=4, max_iters=30, sketch_size=8, tol=1e-6, seed=42, precision=None, fit="sketched",
+                  warmup_iters=0, alpha_lo=None, alpha_hi=None, out=None, matrix_ids=None, stream=None,
+                  handle=None, device=None):
+    """A^{-1/q} of pinned HOST SPD matrices via prism_inv_root_host (as polar_host)."""
+    import torch
+    mats = list(mats)
+    if not mats:
+        return [], {}
+    _check_pinned(mats, "inv_root_host")
+    precision = _precision_of(mats[0], precision)
+    _check_dtype(mats, precision, on_host=True)
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    h = handle or default_handle()
+    o = make_options(5, max_iters, sketch_size, tol, seed, precision, fit, warmup_iters, alpha_lo, alpha_hi)
+    B = len(mats)
+    if out is None:
+        out = [torch.empty_like(t).pin_memory() for t in mats]
+    _check_pinned(out, "inv_root_host")
+    _check_dtype(out, precision, on_host=True)
+    rb = _report_buffers(B, max_iters, dev)
+    rep = _report_struct(rb)
+    ids = _i64(matrix_ids) if matrix_ids is not None else None
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    check(lib().prism_inv_root_host(h.h, B, _i64([t.shape[0] for t in mats]), int(q), _ptrs(mats),
+                                    _i64([t.stride(0) for t in mats]), _ptrs(out), _i64([t.stride(0) for t in out]),
+                                    ids, ctypes.byref(o), ctypes.byref(rep), ctypes.c_void_p(st.cuda_stream)),
+          "prism_inv_root_host")
     return out, rb
 
 

@@ -12,6 +12,8 @@
 //                                 fp32 diag(D) (= diag G, for the sketch)
 //   POLY   out = c1·C + α·D       (P = ½R + αR², d=2)
 //   APPLY  out = C + s·D          (X ← X + X·P, or X + α·X·R for d=1)
+//          (general form of both: out = κ_C α^{e_C}·C + κ_A α^{e_A}·D, which also
+//          builds the inverse-Newton polynomials (I + αR)^q − I)
 //   STORE  out = D                (tests)
 // `sym` schedules only tiles touching the upper triangle and mirrors the
 // stores, so XᵀX and R·R cost half a dense GEMM and R, P are exactly symmetric.
@@ -35,7 +37,23 @@ enum EpiMode : int { EPI_RESID = 0, EPI_POLY = 1, EPI_APPLY = 2, EPI_STORE = 3, 
 //   d=2: P1 K1 -> Q (diag trick) -> next [K1|Q];  P2 [K2|L1] keep K2 -> next [K2|L1];
 //        P3 [K3|L2] keep K3,L2 -> next L2;  P4 L3 keep -> next L3;  P5 L4 -> <Va,Vb>
 //   d=1: P1 K1 keep -> next Q;  P2 L1 keep -> next L1;  P3 L2 -> <Va,Vb>
-enum ChainPassCode : int { CH2_P1 = 0, CH2_P2, CH2_P3, CH2_P4, CH2_P5, CH1_P1, CH1_P2, CH1_P3 };
+//   inverse Newton, root q: CH1_P1 (K1 = R S^T keep, next Q = M S^T),
+//        then Z_j = R Z_{j-1}: CH1_P2 (slot 1), CHI_K2 (slot 2), CH2_P4 (slot 3) for
+//        j < q, and CHI_L<q> for j = q: <V_i, V_j>, V_0 = K1, V_i = -C(q,i) Z_i
+enum ChainPassCode : int { CH2_P1 = 0, CH2_P2, CH2_P3, CH2_P4, CH2_P5, CH1_P1, CH1_P2, CH1_P3,
+                           CHI_K2, CHI_L1, CHI_L2, CHI_L3, CHI_L4, CH_NCODES };
+constexpr int kChainG = 15;   // doubles per 32-row group in chain_part (<V_i,V_j>, i <= j <= 4)
+__host__ __device__ constexpr bool chain_is_last(int pass) {
+  return pass == CH2_P5 || pass == CH1_P3 || (pass >= CHI_L1 && pass <= CHI_L4);
+}
+// kept slots the last pass reads
+__host__ __device__ constexpr int chain_last_slots(int pass) {
+  return pass == CH2_P5 ? 4 : pass == CH1_P3 ? 2 : pass - CHI_L1 + 1;
+}
+// <Va,Vb> values the last pass writes
+__host__ __device__ constexpr int chain_ng(int pass) {
+  return (pass >= CHI_L1 && pass <= CHI_L4) ? (pass - CHI_L1 + 2) * (pass - CHI_L1 + 3) / 2 : 6;
+}
 
 struct GemmProblem {
   const CUtensorMap* tmA;
@@ -54,7 +72,9 @@ struct GemmProblem {
   long long ldo, ldc;    // leading dimensions (elements)
   int M, N, K;
   int mode, sym, matrix, scale_by_alpha, tiles_n;
-  float c1;
+  float c1;              // POLY / APPLY: out = c1 α^eC · C + kA α^eA · D
+  float kA;
+  int eA, eC;
   int pass;              // EPI_CHAIN pass code
   int a_mn, b_mn;        // operand major-ness: 0 K-major, 1 MN-major
   int ksplit;            // EPI_CHAIN split-K slices (tile code tn = slice index) or 1
@@ -64,7 +84,7 @@ struct GemmProblem {
   const void* Rg_lo;
   void* Wn;              // next pass B operand: [2w'][ldS] hi rows then lo rows, compute dtype
   float* keep;           // [4][M][p] fp32 kept chain columns
-  double* chain_part;    // [tiles_m][6] per-tile <Va,Vb> partials
+  double* chain_part;    // [row groups][kChainG] per-group <Va,Vb> partials
   long long ldS, ldr;
   int p;
   int pad2_;
@@ -648,8 +668,8 @@ __device__ __forceinline__ void chain_prefetch(const GemmProblem& Pin, int i, in
     pre.gii = P.gdiag[i];
 #pragma unroll
     for (int c = 0; c < 8; ++c) pre.v[c] = (c >= c0 && c < c1) ? __ldg(P.S + (long long)c * P.ldS + i) : 0.f;
-  } else if constexpr (PASS == CH2_P5 || PASS == CH1_P3) {
-    const int ns = PASS == CH2_P5 ? 4 : 2;
+  } else if constexpr (chain_is_last(PASS)) {
+    const int ns = chain_last_slots(PASS);
     const long long M = P.M;
 #pragma unroll
     for (int sl = 0; sl < 4; ++sl)
@@ -671,7 +691,10 @@ __device__ __forceinline__ void epi_chain(const ChainPre& pre, int i, int grp, c
   const bool valid = i < P.M;
   const int c0 = h == 1 ? (p + 1) / 2 : 0;       // h = 2: one thread per row, every c
   const int c1 = h == 0 ? (p + 1) / 2 : p;
-  double g[6] = {0, 0, 0, 0, 0, 0};
+  constexpr int NG = chain_ng(PASS);
+  double g[NG];
+#pragma unroll
+  for (int j = 0; j < NG; ++j) g[j] = 0.0;
   // o[c] = D[c] + D[w + c] (hi + lo halves of the pass output), op[c] = o[p + c]
   float o[8], op[8];
 #pragma unroll
@@ -714,13 +737,35 @@ __device__ __forceinline__ void epi_chain(const ChainPre& pre, int i, int grp, c
         keep[(2 * M + i) * p + c] = op[c];
         store_w<Cfg>(P, c, p, i, op[c]);
       }
-    } else if constexpr (pass == CH2_P4 || pass == CH1_P2) {
-      constexpr long long slot = pass == CH2_P4 ? 3 : 1;
+    } else if constexpr (pass == CH2_P4 || pass == CH1_P2 || pass == CHI_K2) {
+      constexpr long long slot = pass == CH2_P4 ? 3 : pass == CHI_K2 ? 2 : 1;
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         if (c < c0 || c >= c1) continue;
         keep[(slot * M + i) * p + c] = o[c];
         store_w<Cfg>(P, c, p, i, o[c]);
+      }
+    } else if constexpr (pass >= CHI_L1) {
+      // inverse Newton: m(a) = ||sum_i a^i V_i||^2, V_0 = K1, V_i = -C(q,i) Z_i (Z_q = this
+      // pass's output); <V_i, V_j> for i <= j in row-major upper-triangle order
+      constexpr int q = pass - CHI_L1 + 1;
+      const float(&kv)[4][8] = *reinterpret_cast<const float(*)[4][8]>(pre.v);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        if (c < c0 || c >= c1) continue;
+        double v[q + 1];
+        v[0] = (double)kv[0][c];
+#pragma unroll
+        for (int j = 1; j < q; ++j) {
+          const double bin = (q == 4 && j == 2) ? 6.0 : (double)q;   // C(q, j), 1 <= j < q <= 4
+          v[j] = -bin * (double)kv[j][c];
+        }
+        v[q] = -(double)o[c];
+        int idx = 0;
+#pragma unroll
+        for (int a = 0; a <= q; ++a)
+#pragma unroll
+          for (int b = a; b <= q; ++b) g[idx++] += v[a] * v[b];
       }
     } else {
       // CH2_P5 / CH1_P3: inner products <Va, Vb> (fp64 products of widened factors)
@@ -743,18 +788,18 @@ __device__ __forceinline__ void epi_chain(const ChainPre& pre, int i, int grp, c
       }
     }
   }
-  if constexpr (pass == CH2_P5 || pass == CH1_P3) {
+  if constexpr (chain_is_last(pass)) {
     // <Va, Vb> partial of this warp's 32 rows (one aligned row group): a fixed shuffle
     // tree, written per group — the grouping never depends on the launch (split factor,
     // batch), so k_alpha's fixed-order sum over groups is reproducible bit for bit
 #pragma unroll
-    for (int j = 0; j < 6; ++j) {
+    for (int j = 0; j < NG; ++j) {
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) g[j] += __shfl_xor_sync(0xffffffffu, g[j], off);
     }
     if (lane == 0 && grp >= 0)
 #pragma unroll
-      for (int j = 0; j < 6; ++j) P.chain_part[grp * 6 + j] = g[j];
+      for (int j = 0; j < NG; ++j) P.chain_part[grp * kChainG + j] = g[j];
   }
 }
 
@@ -1000,8 +1045,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
       const int i0 = tm * Cfg::TILE_M + (int)rank * Cfg::BM + q * 32;
       const int i = i0 + lane;                     // output row of this thread
       float coefA = 1.f, coefC = 1.f;
-      if (mode == EPI_POLY) { coefA = static_cast<float>(*P.alpha); coefC = P.c1; }
-      if (mode == EPI_APPLY && P.scale_by_alpha) coefA = static_cast<float>(*P.alpha);
+      if (mode == EPI_POLY || mode == EPI_APPLY) {
+        const double al = (P.eA | P.eC) ? *P.alpha : 1.0;
+        const double pa = P.eA == 0 ? 1.0 : P.eA == 1 ? al : P.eA == 2 ? al * al : al * al * al;
+        const double pc = P.eC == 0 ? 1.0 : P.eC == 1 ? al : P.eC == 2 ? al * al : al * al * al;
+        coefA = static_cast<float>((double)P.kA * pa);
+        coefC = static_cast<float>((double)P.c1 * pc);
+      }
       const bool needC = (mode == EPI_POLY || mode == EPI_APPLY);
       float sumsq = 0.f;
 

@@ -5,6 +5,7 @@
 // are bit-reproducible run to run.
 #pragma once
 #include "ptx.cuh"
+#include "gemm.cuh"   // kChainG (chain_part layout)
 
 namespace prism {
 
@@ -67,6 +68,7 @@ struct SolveParams {
   double* fro2_out;     // row-block begin: local sum of squares (else null)
   const double* fro2_in;   // row-block: all-reduced sum of squares (else null)
   int batch, p, d, max_iters, warmup, fit, precision, kind_sqrt;
+  int inv_q;            // coupled inverse Newton root order (0: polar / sqrt / sign)
   double tol, alo, ahi, ataylor;
   unsigned long long seed;
 };
@@ -306,6 +308,7 @@ struct Vec {
 };
 
 // a1: X_0 = A / ||A||_F (same row-major layout), Y_0 = I (sqrt), state init.
+// Inverse Newton: X_0 = I/c, M_0 = A/c^q (M in Y), c^q = 2||A||_F/(q+1).
 template <int PREC>
 __global__ void __launch_bounds__(256) k_normalize(SolveParams P) {
   griddep_wait();
@@ -329,6 +332,16 @@ __global__ void __launch_bounds__(256) k_normalize(SolveParams P) {
     const int nv = min(V::VE, D.n - col);
     V x;
     x.load(D.A, nullptr, (long long)r * D.lda + col, nv, src_vec && nv == V::VE);
+    if (P.inv_q) {
+      const double cq = 2.0 * c / (P.inv_q + 1);
+      x.store(D.Y[0], D.Y_lo[0], (long long)r * D.ldx + col, nv, nv == V::VE, c > 0.0 ? (float)(1.0 / cq) : 0.f,
+              PREC == 1);
+#pragma unroll
+      for (int e = 0; e < V::VE; ++e) x.v[e] = (col + e == r) ? 1.f : 0.f;
+      x.store(D.X[0], D.X_lo[0], (long long)r * D.ldx + col, nv, nv == V::VE,
+              c > 0.0 ? (float)pow(cq, -1.0 / P.inv_q) : 0.f, PREC == 1);
+      continue;
+    }
     x.store(D.X[0], D.X_lo[0], (long long)r * D.ldx + col, nv, nv == V::VE, inv, PREC == 1);
     if (P.kind_sqrt) {
 #pragma unroll
@@ -347,6 +360,45 @@ __global__ void __launch_bounds__(256) k_normalize(SolveParams P) {
     S.done = (c == 0.0) ? 1 : 0;
     S.status = (c == 0.0) ? 4 : 1;   // ZERO_INPUT / MAX_ITERS until decided
   }
+}
+
+// Inverse Newton residual R_k = I - M_k, elementwise: R (compute dtype), fp32
+// diag(M) (for Q = M S^T in the chain, as diag(G) for the other kinds) and per-tile
+// sum of R^2 in the Gram epilogue's tile layout (128 x bn tiles, read by k_alpha).
+// grid (tiles_n, tiles_m, batch) of the largest matrix; M_k is Y[k & 1].
+template <int PREC>
+__global__ void __launch_bounds__(256) k_resid_inv(SolveParams P, int bn) {
+  griddep_wait();
+  griddep_launch();
+  __shared__ double scratch[8];
+  using V = Vec<PREC>;
+  const int b = blockIdx.z;
+  const MatDesc& D = P.mats[b];
+  if (P.st[b].done) return;
+  const int tm = blockIdx.y, tn = blockIdx.x;
+  if (tm >= D.tiles_m || tn >= D.tiles_n) return;
+  const int n = D.s;
+  const int par = *P.iter & 1;
+  const int vpr = bn / V::VE;   // vectors per tile row
+  double acc = 0.0;
+  for (int e = threadIdx.x; e < 128 * vpr; e += 256) {
+    const int i = tm * 128 + e / vpr, j = tn * bn + (e % vpr) * V::VE;
+    if (i >= n || j >= n) continue;
+    const int nv = min(V::VE, n - j);
+    V x;
+    x.load(D.Y[par], D.Y_lo[par], (long long)i * D.ldx + j, nv, nv == V::VE);
+#pragma unroll
+    for (int u = 0; u < V::VE; ++u) {
+      const float mv = x.v[u];
+      const float rv = (j + u == i ? 1.f : 0.f) - mv;
+      if (j + u == i) D.gdiag[i] = mv;
+      x.v[u] = u < nv ? rv : 0.f;
+      acc += (double)x.v[u] * x.v[u];
+    }
+    x.store(D.R, D.R_lo, (long long)i * D.ldr + j, nv, nv == V::VE, 1.f, PREC == 1);
+  }
+  acc = block_sum<double, 256>(acc, scratch);
+  if (threadIdx.x == 0) D.norm_part[tm * D.tiles_n + tn] = (float)acc;
 }
 
 // ----------------------------------------------------------------- a4: Philox sketch
@@ -561,6 +613,56 @@ __device__ double argmin_quartic(const double c[5], double lo, double hi, double
   return best;
 }
 
+// argmin_{a in [lo, hi]} of m(a) = sum_{i<=deg} c_i a^i for deg > 4 (inverse Newton q >= 3,
+// R23), one warp: [lo, hi] cut into 32 cells; a cell whose ends have m' < 0 <= m' holds a
+// local minimum, located by bisection of m'; candidates {lo, hi} U those minima, smallest m
+// wins (ties -> smaller a); degenerate loss -> Taylor.  Every lane returns the result.
+__device__ double argmin_poly_warp(const double* c, int deg, double lo, double hi, double aT) {
+  const int lane = threadIdx.x & 31;
+  double scale = 0.0;
+  for (int i = 1; i <= deg; ++i) scale = fmax(scale, fabs(c[i]));
+  if (!isfinite(scale)) return aT;
+  if (scale == 0.0 || scale <= 1e-14 * fabs(c[0])) return aT;
+  double d[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) d[i] = i <= deg ? c[i] / scale : 0.0;
+  auto m = [&](double a) {   // c0 dropped: argmin-invariant
+    double v = 0.0;
+#pragma unroll
+    for (int i = 8; i >= 1; --i) v = (v + d[i]) * a;
+    return v;
+  };
+  auto mp = [&](double a) {
+    double v = 0.0;
+#pragma unroll
+    for (int i = 8; i >= 1; --i) v = v * a + i * d[i];
+    return v;
+  };
+  const double a0 = lo + (hi - lo) * lane / 32.0;
+  const double a1 = lane == 31 ? hi : lo + (hi - lo) * (lane + 1) / 32.0;
+  double best = lane == 0 ? lo : INFINITY, bm = lane == 0 ? m(lo) : INFINITY;
+  if (lane == 31) {
+    const double mh = m(hi);
+    if (mh < bm) { best = hi; bm = mh; }
+  }
+  if (mp(a0) < 0.0 && mp(a1) >= 0.0) {
+    double x0 = a0, x1 = a1;
+    for (int it = 0; it < 64; ++it) {
+      const double xm = 0.5 * (x0 + x1);
+      if (xm <= x0 || xm >= x1) break;
+      if (mp(xm) < 0.0) x0 = xm; else x1 = xm;
+    }
+    const double mr = m(x1);
+    if (mr < bm || (mr == bm && x1 < best)) { best = x1; bm = mr; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o), om = __shfl_xor_sync(0xffffffffu, bm, o);
+    if (om < bm || (om == bm && ob < best)) { best = ob; bm = om; }
+  }
+  return best;
+}
+
 // One block (256 threads) per matrix: residual norm, stop test (R12), and
 // alpha_k from the factored sketched loss m(a) = ||V0 + a V1 + a^2 V2||^2.
 __global__ void __launch_bounds__(256) k_alpha(SolveParams P) {
@@ -616,19 +718,35 @@ __global__ void __launch_bounds__(256) k_alpha(SolveParams P) {
   } else {
     // <Va, Vb> from the chain's per-32-row-group partials (R17): lane l
     // sums groups l, l+32, ... in order, then a fixed xor tree — reproducible bit for bit
-    double g[6] = {0, 0, 0, 0, 0, 0};
-    for (int t = threadIdx.x; t < D.chain_tiles; t += 32) {
-      const double* cp = D.chain_part + 6 * t;
+    const int q = P.inv_q;
+    const int ng = q ? (q + 1) * (q + 2) / 2 : 6;
+    double g[kChainG];
 #pragma unroll
-      for (int j = 0; j < 6; ++j) g[j] += cp[j];
+    for (int j = 0; j < kChainG; ++j) g[j] = 0.0;
+    for (int t = threadIdx.x; t < D.chain_tiles; t += 32) {
+      const double* cp = D.chain_part + kChainG * t;
+#pragma unroll
+      for (int j = 0; j < kChainG; ++j)
+        if (j < ng) g[j] += cp[j];
     }
 #pragma unroll
-    for (int j = 0; j < 6; ++j) {
+    for (int j = 0; j < kChainG; ++j) {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) g[j] += __shfl_xor_sync(0xffffffffu, g[j], o);
     }
-    double c[5] = {g[0], 2.0 * g[1], g[3] + 2.0 * g[2], 2.0 * g[4], g[5]};
-    a = (k < P.warmup) ? P.ahi : argmin_quartic(c, P.alo, P.ahi, P.ataylor);
+    if (q) {
+      // inverse Newton: m(a) = ||sum_i a^i V_i||^2 -> c_{i+j} += (2 - [i == j]) <V_i, V_j>
+      double c[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+      int idx = 0;
+      for (int i = 0; i <= q; ++i)
+        for (int j = i; j <= q; ++j) c[i + j] += (i == j ? 1.0 : 2.0) * g[idx++];
+      if (k < P.warmup) a = P.ahi;
+      else if (q <= 2) a = argmin_quartic(c, P.alo, P.ahi, P.ataylor);   // degree <= 4: analytic
+      else a = argmin_poly_warp(c, 2 * q, P.alo, P.ahi, P.ataylor);
+    } else {
+      double c[5] = {g[0], 2.0 * g[1], g[3] + 2.0 * g[2], 2.0 * g[4], g[5]};
+      a = (k < P.warmup) ? P.ahi : argmin_quartic(c, P.alo, P.ahi, P.ataylor);
+    }
   }
   if (threadIdx.x == 0) {
     S.alpha = a;

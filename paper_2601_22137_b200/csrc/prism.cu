@@ -190,7 +190,12 @@ cudaError_t launch_chaint_cfg(int pass, const GemmLaunch& L, cudaStream_t st) {
     case CH2_P5: return launch_chaint_pass<Cfg, CH2_P5>(L, st);
     case CH1_P1: return launch_chaint_pass<Cfg, CH1_P1>(L, st);
     case CH1_P2: return launch_chaint_pass<Cfg, CH1_P2>(L, st);
-    default: return launch_chaint_pass<Cfg, CH1_P3>(L, st);
+    case CH1_P3: return launch_chaint_pass<Cfg, CH1_P3>(L, st);
+    case CHI_K2: return launch_chaint_pass<Cfg, CHI_K2>(L, st);
+    case CHI_L1: return launch_chaint_pass<Cfg, CHI_L1>(L, st);
+    case CHI_L2: return launch_chaint_pass<Cfg, CHI_L2>(L, st);
+    case CHI_L3: return launch_chaint_pass<Cfg, CHI_L3>(L, st);
+    default: return launch_chaint_pass<Cfg, CHI_L4>(L, st);
   }
 }
 
@@ -265,10 +270,11 @@ struct Plan {
   size_t meta_off = 0, meta_bytes = 0;
   std::unique_ptr<uint8_t, PinnedDeleter> blob;
   SolveParams params{};
-  LaunchDesc gram[2], square, apply[2], chaint[5], gram32[2];
+  LaunchDesc gram[2], square, square2, apply[2], chaint[5], gram32[2];
   int n_chain = 0;
   int chain_ksplit = 1;   // cluster size of the chain launches (split-K; 1, 2 or 4)
-  bool has_square = false;
+  bool has_square = false, has_square2 = false;
+  int inv_q = 0;                    // inverse Newton root order (0: other kinds)
   int max_s = 0, max_rows = 0, max_cols = 0, max_m = 0, max_n = 0;
 };
 
@@ -288,12 +294,19 @@ struct Request {
   bool rowblock = false;   // row-block member of a split tall matrix: force the tall form, s = n
   float* G = nullptr;      // row-block: fp32 partial Gram output (n x n, ld n)
   bool sign_kind = false;  // matrix sign: square path, R = I - X^2, X only (output in Q)
+  int inv_q = 0;           // coupled inverse Newton A^{-1/q}: X in X[], M in Y[], R = I - M (output in Q)
 };
 
-void resolve_interval(prism_options& o, double& lo, double& hi, double& aT, int& d) {
+void resolve_interval(prism_options& o, double& lo, double& hi, double& aT, int& d, int inv_q = 0) {
   d = (o.degree == 3) ? 1 : 2;
-  const double dlo = d == 1 ? 0.5 : 0.375, dhi = d == 1 ? 1.0 : 1.45;
+  double dlo = d == 1 ? 0.5 : 0.375, dhi = d == 1 ? 1.0 : 1.45;
   aT = d == 1 ? 0.5 : 0.375;   // Taylor coefficient of xi^d in (1-xi)^{-1/2}
+  if (inv_q) {                 // inverse Newton (first order): [1/(2q), 2/q], Taylor 1/q (R22)
+    d = 1;
+    dlo = 0.5 / inv_q;
+    dhi = 2.0 / inv_q;
+    aT = 1.0 / inv_q;
+  }
   lo = std::isnan(o.alpha_lo) ? dlo : o.alpha_lo;
   hi = std::isnan(o.alpha_hi) ? dhi : o.alpha_hi;
 }
@@ -338,8 +351,9 @@ prism_status build_plan(const Request& r, Plan& P) {
   prism_options o = r.o;
   double lo, hi, aT;
   int d;
-  resolve_interval(o, lo, hi, aT, d);
+  resolve_interval(o, lo, hi, aT, d, r.inv_q);
   const int prec = o.precision;
+  const int iq = r.inv_q;
   const int esz = elem_size(prec);
   const bool split = prec == PRISM_FP32;
   const int BN = tile_bn(prec), BK = tile_bk(prec);
@@ -387,19 +401,21 @@ prism_status build_plan(const Request& r, Plan& P) {
     for (int t = 0; t < 2; ++t) {
       D.X[t] = bump.take(xbytes);
       D.X_lo[t] = split ? bump.take(xbytes) : nullptr;
-      if (r.sqrt_kind) {
+      if (r.sqrt_kind || iq) {
         D.Y[t] = bump.take(xbytes);
         D.Y_lo[t] = split ? bump.take(xbytes) : nullptr;
       }
     }
     D.R = bump.take(rbytes);
     D.R_lo = split ? bump.take(rbytes) : nullptr;
-    void* Pm = (d == 2) ? bump.take(rbytes) : nullptr;
-    void* Pm_lo = (d == 2 && split) ? bump.take(rbytes) : nullptr;
+    void* Pm = (iq ? iq >= 2 : d == 2) ? bump.take(rbytes) : nullptr;
+    void* Pm_lo = (Pm && split) ? bump.take(rbytes) : nullptr;
+    void* Pm2 = iq >= 3 ? bump.take(rbytes) : nullptr;
+    void* Pm2_lo = (Pm2 && split) ? bump.take(rbytes) : nullptr;
     D.gdiag = reinterpret_cast<float*>(bump.take(sizeof(float) * s));
     D.tiles_m = (s + 127) / 128;
     D.tiles_n = (s + BN - 1) / BN;
-    D.sym = (r.sqrt_kind || r.sign_kind || r.rowblock) ? 0 : 1;
+    D.sym = (r.sqrt_kind || r.sign_kind || iq || r.rowblock) ? 0 : 1;
     D.norm_part = reinterpret_cast<float*>(bump.take(sizeof(float) * D.tiles_m * D.tiles_n));
     const long long ldS = (long long)align_up(s, 64);
     D.ldS = ldS;
@@ -409,7 +425,7 @@ prism_status build_plan(const Request& r, Plan& P) {
     D.keep = reinterpret_cast<float*>(bump.take(sizeof(float) * 4 * (size_t)s * p));
     // <Va,Vb> partials of the chain: one per 32-row group of R (chaint.cuh, epi_chain)
     D.chain_tiles = (s + 31) / 32;
-    D.chain_part = reinterpret_cast<double*>(bump.take(sizeof(double) * 6 * D.chain_tiles));
+    D.chain_part = reinterpret_cast<double*>(bump.take(sizeof(double) * kChainG * D.chain_tiles));
     P.max_s = std::max(P.max_s, s);
     P.max_rows = std::max(P.max_rows, s);
     P.max_cols = std::max(P.max_cols, L);
@@ -427,6 +443,9 @@ prism_status build_plan(const Request& r, Plan& P) {
       h.p.out = out; h.p.out_lo = out_lo; h.p.ldo = ldo; h.p.C = C; h.p.C_lo = C_lo; h.p.ldc = ldc;
       h.p.alpha = alpha_ptr;
       h.p.tiles_n = (N + BN - 1) / BN;
+      h.p.c1 = 1.f;                          // out = c1 a^eC C + kA a^eA D
+      h.p.kA = 1.f;
+      h.p.eA = mode == EPI_POLY ? 1 : 0;
       if (esz == 2 && (mode == EPI_RESID || mode == EPI_POLY || mode == EPI_APPLY || mode == EPI_STORE)) {
         maps.push_back(MapSpec{out, M, N, ldo, esz, OP_EPI, 32, 32});
         h.mapO = (int)maps.size();
@@ -437,7 +456,55 @@ prism_status build_plan(const Request& r, Plan& P) {
       }
       return h;
     };
-    if (!r.sqrt_kind && !r.sign_kind) {
+    if (iq) {
+      // coupled inverse Newton: R = I - M (elementwise, k_resid_inv),
+      // X' = X + a X R, M' = (I + a R)^q M = M + P_q M with P_q = (I + a R)^q - I:
+      //   q = 1: P_1 = a R (in the apply epilogue)
+      //   q = 2: P_2 = 2a R + a^2 R.R
+      //   q = 3: T = 3a R + a^2 R.R, P_3 = 3a R + a R.T   (Horner)
+      //   q = 4: P_2 as above, P_4 = 2 P_2 + P_2.P_2      (squaring)
+      const int nn = s;
+      auto poly = [&](void* out, void* out_lo, const void* C, const void* C_lo, const void* Aop, const void* Aop_lo,
+                      const void* Bop, const void* Bop_lo, float kC, int eC, float kA, int eA) {
+        HostProblem q = mk(nn, nn, nn, EPI_POLY, 0, out, out_lo, ldr, C, C_lo, ldr);
+        q.p.c1 = kC; q.p.eC = eC; q.p.kA = kA; q.p.eA = eA;
+        q.p.b_mn = 1;
+        q.mapA = add_map(Aop, nn, nn, ldr, OP_A);
+        q.mapB = add_map(Bop, nn, nn, ldr, OP_MN);
+        if (split) { q.mapA_lo = add_map(Aop_lo, nn, nn, ldr, OP_A); q.mapB_lo = add_map(Bop_lo, nn, nn, ldr, OP_MN); }
+        return q;
+      };
+      const void* Pq = D.R;
+      const void* Pq_lo = D.R_lo;
+      if (iq == 2) {
+        P.square.probs.push_back(poly(Pm, Pm_lo, D.R, D.R_lo, D.R, D.R_lo, D.R, D.R_lo, 2.f, 1, 1.f, 2));
+        Pq = Pm; Pq_lo = Pm_lo;
+      } else if (iq == 3) {
+        P.square.probs.push_back(poly(Pm, Pm_lo, D.R, D.R_lo, D.R, D.R_lo, D.R, D.R_lo, 3.f, 1, 1.f, 2));
+        P.square2.probs.push_back(poly(Pm2, Pm2_lo, D.R, D.R_lo, D.R, D.R_lo, Pm, Pm_lo, 3.f, 1, 1.f, 1));
+        Pq = Pm2; Pq_lo = Pm2_lo;
+      } else if (iq == 4) {
+        P.square.probs.push_back(poly(Pm, Pm_lo, D.R, D.R_lo, D.R, D.R_lo, D.R, D.R_lo, 2.f, 1, 1.f, 2));
+        P.square2.probs.push_back(poly(Pm2, Pm2_lo, Pm, Pm_lo, Pm, Pm_lo, Pm, Pm_lo, 2.f, 0, 1.f, 0));
+        Pq = Pm2; Pq_lo = Pm2_lo;
+      }
+      for (int t = 0; t < 2; ++t) {
+        HostProblem ax = mk(nn, nn, nn, EPI_APPLY, 0, D.X[1 - t], D.X_lo[1 - t], ldx, D.X[t], D.X_lo[t], ldx);
+        ax.p.scale_by_alpha = ax.p.eA = 1;                     // X + a X R
+        ax.p.b_mn = 1;
+        ax.mapA = add_map(D.X[t], nn, nn, ldx, OP_A);
+        ax.mapB = add_map(D.R, nn, nn, ldr, OP_MN);
+        if (split) { ax.mapA_lo = add_map(D.X_lo[t], nn, nn, ldx, OP_A); ax.mapB_lo = add_map(D.R_lo, nn, nn, ldr, OP_MN); }
+        P.apply[t].probs.push_back(ax);
+        HostProblem am = mk(nn, nn, nn, EPI_APPLY, 0, D.Y[1 - t], D.Y_lo[1 - t], ldx, D.Y[t], D.Y_lo[t], ldx);
+        am.p.scale_by_alpha = am.p.eA = iq == 1;               // M + P_q M
+        am.p.b_mn = 1;
+        am.mapA = add_map(Pq, nn, nn, ldr, OP_A);
+        am.mapB = add_map(D.Y[t], nn, nn, ldx, OP_MN);
+        if (split) { am.mapA_lo = add_map(Pq_lo, nn, nn, ldr, OP_A); am.mapB_lo = add_map(D.Y_lo[t], nn, nn, ldx, OP_MN); }
+        P.apply[t].probs.push_back(am);
+      }
+    } else if (!r.sqrt_kind && !r.sign_kind) {
       // polar: X keeps A's row-major layout (m x n).  Tall (m >= n): G = X^T X with both
       // operands MN-major, X' = X + X P (A = X K-major, B = P K-major by symmetry).
       // Wide (m < n): G = X X^T (both K-major), X' = X + P X (B = X MN-major).
@@ -470,7 +537,7 @@ prism_status build_plan(const Request& r, Plan& P) {
         const void* Pa = d == 2 ? Pm : D.R;
         const void* Pa_lo = d == 2 ? Pm_lo : D.R_lo;
         HostProblem a = mk(m, n, s, EPI_APPLY, 0, D.X[1 - t], D.X_lo[1 - t], ldx, D.X[t], D.X_lo[t], ldx);
-        a.p.scale_by_alpha = d == 1;
+        a.p.scale_by_alpha = a.p.eA = d == 1;
         if (tall) {
           a.mapA = add_map(D.X[t], m, n, ldx, OP_A);
           a.mapB = add_map(Pa, s, s, ldr, OP_BK);
@@ -509,7 +576,7 @@ prism_status build_plan(const Request& r, Plan& P) {
         const void* Pa = d == 2 ? Pm : D.R;
         const void* Pa_lo = d == 2 ? Pm_lo : D.R_lo;
         HostProblem ax = mk(nn, nn, nn, EPI_APPLY, 0, D.X[1 - t], D.X_lo[1 - t], ldx, D.X[t], D.X_lo[t], ldx);
-        ax.p.scale_by_alpha = d == 1;
+        ax.p.scale_by_alpha = ax.p.eA = d == 1;
         ax.p.b_mn = 1;
         ax.mapA = add_map(D.X[t], nn, nn, ldx, OP_A);
         ax.mapB = add_map(Pa, nn, nn, ldr, OP_MN);
@@ -517,7 +584,7 @@ prism_status build_plan(const Request& r, Plan& P) {
         P.apply[t].probs.push_back(ax);
         if (r.sign_kind) continue;
         HostProblem ay = mk(nn, nn, nn, EPI_APPLY, 0, D.Y[1 - t], D.Y_lo[1 - t], ldx, D.Y[t], D.Y_lo[t], ldx);
-        ay.p.scale_by_alpha = d == 1;
+        ay.p.scale_by_alpha = ay.p.eA = d == 1;
         ay.p.b_mn = 1;
         ay.mapA = add_map(Pa, nn, nn, ldr, OP_A);
         ay.mapB = add_map(D.Y[t], nn, nn, ldx, OP_MN);
@@ -540,11 +607,13 @@ prism_status build_plan(const Request& r, Plan& P) {
       static const int codes1[3] = {CH1_P1, CH1_P2, CH1_P3};
       static const int nin2[5] = {2, 4, 4, 2, 2};   // rows of B (= 2 x input width) in units of p
       static const int nin1[3] = {2, 2, 2};
-      const int npass = d == 2 ? 5 : 3;
+      static const int codesi[4][5] = {{CH1_P1, CHI_L1}, {CH1_P1, CH1_P2, CHI_L2}, {CH1_P1, CH1_P2, CHI_K2, CHI_L3},
+                                       {CH1_P1, CH1_P2, CHI_K2, CH2_P4, CHI_L4}};
+      const int npass = iq ? iq + 1 : d == 2 ? 5 : 3;
       for (int j = 0; j < npass; ++j) {
-        const int N = (d == 2 ? nin2[j] : nin1[j]) * p;
+        const int N = (iq ? 2 : d == 2 ? nin2[j] : nin1[j]) * p;
         HostProblem c = mk(s, N, s, EPI_CHAIN, 0, nullptr, nullptr, 0, nullptr, nullptr, 0);
-        c.p.pass = d == 2 ? codes2[j] : codes1[j];
+        c.p.pass = iq ? codesi[iq - 1][j] : d == 2 ? codes2[j] : codes1[j];
         c.p.S = D.S;
         c.p.Rg = D.R;
         c.p.Rg_lo = D.R_lo;
@@ -570,8 +639,10 @@ prism_status build_plan(const Request& r, Plan& P) {
       }
     }
   }
-  P.has_square = (d == 2);
-  P.n_chain = (d == 2) ? 5 : 3;
+  P.inv_q = iq;
+  P.has_square = iq ? iq >= 2 : d == 2;
+  P.has_square2 = iq >= 3;
+  P.n_chain = iq ? iq + 1 : (d == 2) ? 5 : 3;
   // tile lists (problem index within its launch)
   auto finish = [&](LaunchDesc& L, bool) {
     L.tiles.clear();
@@ -586,6 +657,7 @@ prism_status build_plan(const Request& r, Plan& P) {
     if (r.rowblock) finish(P.gram32[t], false);
   }
   if (P.has_square) finish(P.square, !polar_k);
+  if (P.has_square2) finish(P.square2, !polar_k);
   // chain tiles (chaint.cuh): 256-row tiles of R, each split over a cluster of C CTAs,
   // C = the largest factor of the launch's matrices (smaller factors: empty slices).
   // Tiles of one row tile are contiguous and C-aligned, so slice == cluster rank.
@@ -630,8 +702,9 @@ prism_status build_plan(const Request& r, Plan& P) {
   off += sizeof(int) * (B + 1);
   const size_t ooff_off = off;
   off += sizeof(int) * (B + 1);
-  LaunchDesc* all[12] = {&P.gram[0],   &P.gram[1],   &P.apply[0],  &P.apply[1],  &P.square,     &P.chaint[0],
-                         &P.chaint[1], &P.chaint[2], &P.chaint[3], &P.chaint[4], &P.gram32[0], &P.gram32[1]};
+  LaunchDesc* all[13] = {&P.gram[0],   &P.gram[1],   &P.apply[0],  &P.apply[1],  &P.square,     &P.chaint[0],
+                         &P.chaint[1], &P.chaint[2], &P.chaint[3], &P.chaint[4], &P.gram32[0], &P.gram32[1],
+                         &P.square2};
   for (LaunchDesc* L : all) {
     off = align_up(off, 128);
     L->probs_off = off;
@@ -705,6 +778,7 @@ prism_status build_plan(const Request& r, Plan& P) {
   S.fit = o.fit;
   S.precision = prec;
   S.kind_sqrt = r.sqrt_kind ? 1 : 0;
+  S.inv_q = iq;
   S.tol = o.tol;
   S.alo = lo;
   S.ahi = hi;
@@ -744,7 +818,7 @@ void ensure_attrs() {
   z.ntiles = 0;
   for (int prec = 0; prec < 3; ++prec) {
     launch_gemm(prec, z, 0);
-    for (int pass = CH2_P1; pass <= CH1_P3; ++pass) launch_chaint(prec, pass, z, 0);
+    for (int pass = CH2_P1; pass < CH_NCODES; ++pass) launch_chaint(prec, pass, z, 0);
   }
 }
 
@@ -754,6 +828,7 @@ prism_status validate(const Request& r) {
   if (!r.m || !r.lda || !r.A || (!r.sqrt_kind && (!r.n || !r.Q || !r.ldq)))
     return fail(PRISM_ERR_INVALID_ARG, "null size/pointer array");
   if (o.degree != 3 && o.degree != 5) return fail(PRISM_ERR_INVALID_ARG, "degree must be 3 or 5");
+  if (r.inv_q < 0 || r.inv_q > 4) return fail(PRISM_ERR_UNSUPPORTED, "inverse root order q must be 1..4");
   if (o.max_iters < 1 || o.max_iters > 10000) return fail(PRISM_ERR_INVALID_ARG, "max_iters out of range");
   if (!(o.tol > 0.0)) return fail(PRISM_ERR_INVALID_ARG, "tol must be > 0");
   if (o.precision < 0 || o.precision > 2) return fail(PRISM_ERR_INVALID_ARG, "bad precision");
@@ -866,6 +941,7 @@ static std::vector<long long> make_key(const Request& r) {
   std::vector<long long> k;
   k.push_back(r.sqrt_kind);
   k.push_back(r.sign_kind);
+  k.push_back(r.inv_q);
   k.push_back(r.rowblock);
   k.push_back((long long)(uintptr_t)r.G);
   k.push_back(r.batch);
@@ -957,6 +1033,12 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
   const GemmLaunch g_gram = make_launch(*P, P->gram[0], &P->gram[1], r.ws, 0, M + 1);
   const GemmLaunch g_apply = make_launch(*P, P->apply[0], &P->apply[1], r.ws, 0, M);
   const GemmLaunch g_sq = make_launch(*P, P->square, nullptr, r.ws, 0, M);
+  const GemmLaunch g_sq2 = make_launch(*P, P->square2, nullptr, r.ws, 0, M);
+  int rtm = 1, rtn = 1;   // inverse Newton: tile grid of the residual kernel (largest matrix)
+  if (P->inv_q) {
+    rtm = (P->max_s + 127) / 128;
+    rtn = (P->max_s + tile_bn(prec) - 1) / tile_bn(prec);
+  }
   GemmLaunch g_chaint[5];
   for (int j = 0; j < P->n_chain; ++j) g_chaint[j] = make_launch(*P, P->chaint[j], nullptr, r.ws, r.o.warmup_iters, M);
   const int n_chain_launches = P->n_chain;
@@ -966,7 +1048,14 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
   auto body = [&](cudaStream_t s2, cudaGraphConditionalHandle ch, int use_handle, bool timed) -> prism_status {
     {
       KindTimer t(h, s2, 0, timed ? 1 : 0);
-      PRISM_CK(launch_gemm(prec, g_gram, s2));
+      if (P->inv_q) {
+        const dim3 grid(rtn, rtm, B);
+        if (prec == PRISM_BF16) PRISM_CK(launch_k(k_resid_inv<0>, grid, dim3(256), 0, s2, 1, S, tile_bn(prec)));
+        else if (prec == PRISM_FP32) PRISM_CK(launch_k(k_resid_inv<1>, grid, dim3(256), 0, s2, 1, S, tile_bn(prec)));
+        else PRISM_CK(launch_k(k_resid_inv<2>, grid, dim3(256), 0, s2, 1, S, tile_bn(prec)));
+      } else {
+        PRISM_CK(launch_gemm(prec, g_gram, s2));
+      }
     }
     if (sketched) {
       KindTimer t(h, s2, 3, timed ? 1 + n_chain_launches : 0);
@@ -978,8 +1067,9 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
       PRISM_CK(launch_k(k_alpha, dim3(B), dim3(256), 0, s2, 1, S));
     }
     if (P->has_square) {
-      KindTimer t(h, s2, 1, timed ? 1 : 0);
+      KindTimer t(h, s2, 1, timed ? (P->has_square2 ? 2 : 1) : 0);
       PRISM_CK(launch_gemm(prec, g_sq, s2));
+      if (P->has_square2) PRISM_CK(launch_gemm(prec, g_sq2, s2));
     }
     {
       KindTimer t(h, s2, 2, timed ? 1 : 0);
@@ -989,7 +1079,8 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
     PRISM_CK(cudaGetLastError());
     return PRISM_OK;
   };
-  P->per_iter_launches = 3 + (sketched ? 1 + n_chain_launches : 0) + (P->has_square ? 1 : 0) + 1;
+  P->per_iter_launches = 3 + (sketched ? 1 + n_chain_launches : 0) + (P->has_square ? 1 : 0) +
+                         (P->has_square2 ? 1 : 0) + 1;
   if (!h->profiling) {
     if (!P->exec) {
       // build the device-driven loop once per plan: WHILE(any active) { body }
@@ -1135,8 +1226,8 @@ static cudaError_t copy_block(void* dst, size_t dld, const void* src, size_t sld
 }
 
 // End-to-end path on host buffers (see prism.h): stage, solve, return, pipelined.
-// kind: 0 polar, 1 sqrt / inverse sqrt, 2 sign (square inputs for 1 and 2)
-static prism_status host_solve(prism_handle h, int kind, int batch, const int64_t* m, const int64_t* n,
+// kind: 0 polar, 1 sqrt / inverse sqrt, 2 sign, 3 inverse q-th root (square inputs for 1-3)
+static prism_status host_solve(prism_handle h, int kind, int inv_q, int batch, const int64_t* m, const int64_t* n,
                                const void* const* A_host, const int64_t* lda, void* const* O1, void* const* O2,
                                const int64_t* ldo, const int64_t* ids, const prism_options* o,
                                const prism_report* rep, cudaStream_t caller) {
@@ -1173,6 +1264,7 @@ static prism_status host_solve(prism_handle h, int kind, int batch, const int64_
   const bool two = sqrt_kind && O1 && O2;
   const size_t ws_need = sqrt_kind ? prism_sqrt_workspace(h, batch, m, o)
                          : kind == 2 ? prism_sign_workspace(h, batch, m, o)
+                         : kind == 3 ? prism_inv_root_workspace(h, batch, m, inv_q, o)
                                      : prism_polar_workspace(h, batch, m, n, o);
   if (!ws_need) return fail(PRISM_ERR_INVALID_ARG, "workspace query failed");
   if (sl.in_bytes < bytes || sl.out_bytes < bytes || (two && !sl.out2) || h->hws_bytes < ws_need) {
@@ -1223,6 +1315,9 @@ static prism_status host_solve(prism_handle h, int kind, int batch, const int64_
   if (sqrt_kind)
     st = prism_sqrt_invsqrt(h, batch, m, din.data(), ldc.data(), O1 ? dout.data() : nullptr,
                             O2 ? dout2.data() : nullptr, ldc.data(), ids, o, rep, h->hws, h->hws_bytes, h->s_comp);
+  else if (kind == 3)
+    st = prism_inv_root(h, batch, m, inv_q, din.data(), ldc.data(), dout.data(), ldc.data(), ids, o, rep, h->hws,
+                        h->hws_bytes, h->s_comp);
   else if (kind == 2)
     st = prism_sign(h, batch, m, din.data(), ldc.data(), dout.data(), ldc.data(), ids, o, rep, h->hws, h->hws_bytes,
                     h->s_comp);
@@ -1267,7 +1362,7 @@ prism_status prism_polar_host(prism_handle h, int batch, const int64_t* m, const
                               const int64_t* lda, void* const* Q, const int64_t* ldq, const int64_t* matrix_ids,
                               const prism_options* o, const prism_report* rep, void* stream) {
   try {
-    return host_solve(h, 0, batch, m, n, A, lda, Q, nullptr, ldq, matrix_ids, o, rep,
+    return host_solve(h, 0, 0, batch, m, n, A, lda, Q, nullptr, ldq, matrix_ids, o, rep,
                       static_cast<cudaStream_t>(stream));
   } catch (...) {
     return fail(PRISM_ERR_INTERNAL, "exception in prism_polar_host");
@@ -1279,7 +1374,7 @@ prism_status prism_sqrt_invsqrt_host(prism_handle h, int batch, const int64_t* n
                                      const int64_t* ld_out, const int64_t* matrix_ids, const prism_options* o,
                                      const prism_report* rep, void* stream) {
   try {
-    return host_solve(h, 1, batch, n, n, A, lda, Asqrt, Ainvsqrt, ld_out, matrix_ids, o, rep,
+    return host_solve(h, 1, 0, batch, n, n, A, lda, Asqrt, Ainvsqrt, ld_out, matrix_ids, o, rep,
                       static_cast<cudaStream_t>(stream));
   } catch (...) {
     return fail(PRISM_ERR_INTERNAL, "exception in prism_sqrt_invsqrt_host");
@@ -1290,10 +1385,50 @@ prism_status prism_sign_host(prism_handle h, int batch, const int64_t* n, const 
                              void* const* S, const int64_t* lds, const int64_t* matrix_ids, const prism_options* o,
                              const prism_report* rep, void* stream) {
   try {
-    return host_solve(h, 2, batch, n, n, A, lda, S, nullptr, lds, matrix_ids, o, rep,
+    return host_solve(h, 2, 0, batch, n, n, A, lda, S, nullptr, lds, matrix_ids, o, rep,
                       static_cast<cudaStream_t>(stream));
   } catch (...) {
     return fail(PRISM_ERR_INTERNAL, "exception in prism_sign_host");
+  }
+}
+
+size_t prism_inv_root_workspace(prism_handle h, int batch, const int64_t* n, int q, const prism_options* o) {
+  if (!h || !o || !n || batch < 1) return 0;
+  std::vector<const void*> fakeA(batch, reinterpret_cast<const void*>(256));
+  std::vector<void*> fakeQ(batch, reinterpret_cast<void*>(256));
+  std::vector<int64_t> ld(n, n + batch);
+  Request r{false, batch, n, n, fakeA.data(), ld.data(), fakeQ.data(), nullptr, ld.data(), nullptr, *o, nullptr};
+  r.inv_q = q;
+  if (q < 1 || validate(r)) return 0;
+  Plan P;
+  if (build_plan(r, P)) return 0;
+  return P.ws_need;
+}
+
+prism_status prism_inv_root(prism_handle h, int batch, const int64_t* n, int q, const void* const* A,
+                            const int64_t* lda, void* const* X, const int64_t* ldx, const int64_t* matrix_ids,
+                            const prism_options* o, const prism_report* rep, void* workspace, size_t ws_bytes,
+                            void* stream) {
+  try {
+    if (!o) return fail(PRISM_ERR_INVALID_ARG, "null options");
+    if (q < 1) return fail(PRISM_ERR_INVALID_ARG, "q must be >= 1");
+    Request r{false, batch, n, n, A, lda, X, nullptr, ldx, matrix_ids, *o, static_cast<char*>(workspace)};
+    r.inv_q = q;
+    return run_solve(h, r, rep, ws_bytes, static_cast<cudaStream_t>(stream));
+  } catch (...) {
+    return fail(PRISM_ERR_INTERNAL, "exception in prism_inv_root");
+  }
+}
+
+prism_status prism_inv_root_host(prism_handle h, int batch, const int64_t* n, int q, const void* const* A,
+                                 const int64_t* lda, void* const* X, const int64_t* ldx, const int64_t* matrix_ids,
+                                 const prism_options* o, const prism_report* rep, void* stream) {
+  try {
+    if (q < 1) return fail(PRISM_ERR_INVALID_ARG, "q must be >= 1");
+    return host_solve(h, 3, q, batch, n, n, A, lda, X, nullptr, ldx, matrix_ids, o, rep,
+                      static_cast<cudaStream_t>(stream));
+  } catch (...) {
+    return fail(PRISM_ERR_INTERNAL, "exception in prism_inv_root_host");
   }
 }
 
@@ -1591,7 +1726,11 @@ prism_status prism_debug_gemm(prism_handle h, int precision, int b_mn, int mode,
   gp->norm_part = norm_part; gp->gdiag = gdiag; gp->alpha = alpha_dev;
   gp->ldo = ldo; gp->ldc = ldc; gp->M = M; gp->N = N; gp->K = K;
   gp->mode = mode; gp->sym = sym; gp->matrix = 0; gp->scale_by_alpha = scale_by_alpha;
-  gp->tiles_n = (N + BN - 1) / BN; gp->c1 = c1;
+  gp->tiles_n = (N + BN - 1) / BN;
+  gp->c1 = mode == EPI_POLY ? c1 : 1.f;
+  gp->kA = 1.f;
+  gp->eA = (mode == EPI_POLY || scale_by_alpha) ? 1 : 0;
+  gp->eC = 0;
   gp->a_mn = 0; gp->b_mn = b_mn ? 1 : 0;
   LaunchDesc L;
   HostProblem hp;
