@@ -21,6 +21,9 @@ Coupled inverse Newton A^{-1/q} (Appendix A.3; q = the paper's p):
     X_{k+1} = X_k (I + a_k R_k),  M_{k+1} = (I + a_k R_k)^q M_k
     loss of degree 2q, argmin analytic for q <= 2, companion-matrix
     roots of m' for q >= 3; interval [1/(2q), 2/q] (R22).
+Chebyshev inverse A^{-1} (Appendix A.4):
+    A' = A/||A||_F, X_0 = A'^T, R_k = I - A' X_k, X_{k+1} = X_k (I + R_k + a_k R_k^2),
+    a_k = argmin_{[1/2,2]} ||S_k (R_k^2 - a (R_k^2 - R_k^3))||_F^2 (quadratic; R25, R26).
 Coefficient a_k (eq. (4)):
     a_k = argmin_{a in [l,u]} || S_k (I - (I-R_k) g_d(R_k;a)^2) ||_F^2
         = argmin m(a),  m(a) = c0 + c1 a + c2 a^2 + c3 a^3 + c4 a^4
@@ -548,3 +551,75 @@ def inv_root(A, q: int = 4, p: int = 8, tol: float = 1e-10, max_iters: int = 50,
         k += 1
     rep.iters = k
     return X, rep
+
+
+# --------------------------------------------------------------------------
+# PRISM Chebyshev iteration for A^{-1} (Appendix A.4)
+# --------------------------------------------------------------------------
+
+def chebyshev_interval() -> tuple[float, float, float]:
+    """(l, u, a_Taylor) = (1/2, 2, 1): [1/2, 2]; f_2's xi^2 coefficient 1."""
+    return 0.5, 2.0, 1.0
+
+
+def chebyshev_loss_coeffs(R: np.ndarray, S: np.ndarray | None) -> np.ndarray:
+    """(c0, c1, c2) of m(a) = ||S (R^2 - a (R^2 - R^3))||_F^2, S = I if None.
+
+    Written from the definition for a general (non-symmetric) R, as the section allows
+    (P:598): U = S R^2, V = S (R^2 - R^3) = U - U R, m(a) = ||U - a V||^2.  For symmetric
+    R it equals the printed trace form c1 = -2 t4 + 2 t5, c2 = t4 - 2 t5 + t6 (P:622-627;
+    pinned in the tests) (R26).
+    """
+    U = R @ R if S is None else (S.astype(np.float64) @ R) @ R
+    V = U - U @ R
+    return np.array([float(np.sum(U * U)), -2.0 * float(np.sum(U * V)), float(np.sum(V * V))])
+
+
+def chebyshev_inverse(A, p: int = 8, tol: float = 1e-10, max_iters: int = 50, seed: int = 0, b: int = 0,
+                      warmup: int = 0, fit: str = FIT_SKETCHED, alpha_lo: float | None = None,
+                      alpha_hi: float | None = None):
+    """PRISM-accelerated Chebyshev iteration for A^{-1} of a square full-rank A in fp64.
+
+        c = ||A||_F, A' = A/c (||A'||_2 <= 1, P:598),  X_0 = A'^T           (P:611, R25)
+        R_k = I - A' X_k,  X_{k+1} = X_k (I + R_k + a_k R_k^2)
+        a_k = argmin_{[1/2, 2]} ||S_k (R_k^2 - a (R_k^2 - R_k^3))||_F^2     (P:617-629)
+        A^{-1} = A'^{-1} / c.
+    Stop test, sketch and statuses as polar (R8, R12).  Returns (Ainv, Report).
+    """
+    A = np.asarray(A, dtype=np.float64)
+    n = A.shape[0]
+    lo, hi, aT = chebyshev_interval()
+    lo = lo if alpha_lo is None else alpha_lo
+    hi = hi if alpha_hi is None else alpha_hi
+    rep = Report()
+    c = math.sqrt(float(np.sum(A * A)))
+    if c == 0.0:
+        rep.status = ZERO_INPUT
+        return np.zeros_like(A), rep
+    An = A / c
+    X = An.T.copy()                            # X_0 = A^T (of the normalised A)
+    I = np.eye(n)
+    incr = 0
+    r_prev = math.inf
+    k = 0
+    while True:
+        R = I - An @ X                         # R_k = I - A X_k
+        r = float(np.linalg.norm(R, "fro"))
+        stop, incr = _status_update(rep, k, r, r_prev, n, tol, max_iters, incr)
+        r_prev = r
+        if stop:
+            break
+        if k < warmup:
+            a = hi
+        elif fit == FIT_TAYLOR:
+            a = aT
+        else:
+            S = None if fit == FIT_EXACT else gaussian_sketch(seed, b, k, p, n)
+            cf = chebyshev_loss_coeffs(R, S)
+            rep.coeffs.append(cf)
+            a = argmin_quartic(np.concatenate([cf, [0.0, 0.0]]), lo, hi, aT)   # closed form (P:628)
+        rep.alphas.append(a)
+        X = X @ (I + R + a * (R @ R))          # X_{k+1} = X_k (I + R_k + a_k R_k^2)
+        k += 1
+    rep.iters = k
+    return X / c, rep
