@@ -179,6 +179,27 @@ prism_status prism_inv_root_host(prism_handle h, int batch, const int64_t* n, in
                                  const int64_t* lda, void* const* X, const int64_t* ldx, const int64_t* matrix_ids,
                                  const prism_options* o, const prism_report* rep, void* stream);
 
+/*
+ * Inverse A^{-1} of square full-rank n[i] x n[i] matrices (general, not necessarily
+ * symmetric) by the PRISM-accelerated Chebyshev iteration (Appendix A.4):
+ *   A' = A/||A||_F,  X_0 = A'^T,  R_k = I - A' X_k,  X_{k+1} = X_k (I + R_k + a_k R_k^2),
+ *   a_k = argmin over [1/2, 2] (overridable) of ||S_k (R_k^2 - a (R_k^2 - R_k^3))||_F^2
+ *   (closed form), A^{-1} = X / ||A||_F.  options.degree is ignored; fit SKETCHED or
+ * TAYLOR (a = 1: the classical Chebyshev iteration).  X[i] receives A_i^{-1} (ld ldx[i];
+ * may alias A: the iteration reads its own copy of A' in the workspace).  Other
+ * arguments as prism_polar.
+ */
+size_t prism_chebyshev_inverse_workspace(prism_handle h, int batch, const int64_t* n, const prism_options* o);
+prism_status prism_chebyshev_inverse(prism_handle h, int batch, const int64_t* n, const void* const* A,
+                                     const int64_t* lda, void* const* X, const int64_t* ldx,
+                                     const int64_t* matrix_ids, const prism_options* o, const prism_report* rep,
+                                     void* workspace, size_t ws_bytes, void* stream);
+/* prism_chebyshev_inverse on page-locked HOST buffers, pipelined as prism_polar_host. */
+prism_status prism_chebyshev_inverse_host(prism_handle h, int batch, const int64_t* n, const void* const* A,
+                                          const int64_t* lda, void* const* X, const int64_t* ldx,
+                                          const int64_t* matrix_ids, const prism_options* o,
+                                          const prism_report* rep, void* stream);
+
 /* prism_sign on page-locked HOST buffers, pipelined as prism_polar_host. */
 prism_status prism_sign_host(prism_handle h, int batch, const int64_t* n, const void* const* A, const int64_t* lda,
                              void* const* S, const int64_t* lds, const int64_t* matrix_ids, const prism_options* o,
@@ -259,7 +280,7 @@ prism_status prism_debug_sketch(uint64_t seed, int64_t b, int k, int p, int s, f
 /* Device quartic argmin on [lo, hi] (R15/R16): n problems, c_dev[5*n] -> alpha_dev[n]. */
 prism_status prism_debug_argmin(int n, const double* c_dev, double lo, double hi, double a_taylor,
                                 double* alpha_dev, void* stream);
-/* Chain-pass timeline (diagnostics only): buf_dev = device u64[13 * 1024 * 16] (one block per pass code) receiving
+/* Chain-pass timeline (diagnostics only): buf_dev = device u64[16 * 1024 * 16] (one block per pass code) receiving
  * per-pass-code, per-CTA globaltimer stamps of later chain launches; NULL disables. */
 prism_status prism_debug_trace_chain(unsigned long long* buf_dev);
 /* Main-GEMM k-block timeline (diagnostics only): buf_dev = device u64[148 * 192]; launches

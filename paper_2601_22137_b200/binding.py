@@ -57,6 +57,8 @@ EXPORTS = [
     "prism_polar_workspace", "prism_polar", "prism_sqrt_workspace", "prism_sqrt_invsqrt",
     "prism_polar_host", "prism_sqrt_invsqrt_host", "prism_sign_workspace", "prism_sign", "prism_sign_host",
     "prism_inv_root_workspace", "prism_inv_root", "prism_inv_root_host",
+                     "prism_chebyshev_inverse", "prism_chebyshev_inverse_host",
+    "prism_chebyshev_inverse_workspace", "prism_chebyshev_inverse", "prism_chebyshev_inverse_host",
     "prism_lpt_partition", "prism_polar_flops_per_iter", "prism_sqrt_flops_per_iter",
     "prism_launch_count", "prism_profile_enable", "prism_profile_read",
     "prism_rowblock_workspace", "prism_rowblock_begin", "prism_rowblock_gram", "prism_rowblock_update",
@@ -114,6 +116,13 @@ def lib():
                                      c_i64p, ctypes.POINTER(Options), ctypes.POINTER(Report), vp, sz, vp]
         L.prism_inv_root_host.argtypes = [vp, i32, c_i64p, i32, ctypes.POINTER(vp), c_i64p, ctypes.POINTER(vp),
                                           c_i64p, c_i64p, ctypes.POINTER(Options), ctypes.POINTER(Report), vp]
+        L.prism_chebyshev_inverse_workspace.argtypes = [vp, i32, c_i64p, ctypes.POINTER(Options)]
+        L.prism_chebyshev_inverse_workspace.restype = sz
+        L.prism_chebyshev_inverse.argtypes = [vp, i32, c_i64p, ctypes.POINTER(vp), c_i64p, ctypes.POINTER(vp), c_i64p,
+                                              c_i64p, ctypes.POINTER(Options), ctypes.POINTER(Report), vp, sz, vp]
+        L.prism_chebyshev_inverse_host.argtypes = [vp, i32, c_i64p, ctypes.POINTER(vp), c_i64p, ctypes.POINTER(vp),
+                                                   c_i64p, c_i64p, ctypes.POINTER(Options), ctypes.POINTER(Report),
+                                                   vp]
         L.prism_lpt_partition.argtypes = [i32, ctypes.POINTER(dbl), i32, ctypes.POINTER(ctypes.c_int32)]
         L.prism_polar_flops_per_iter.argtypes = [i64, i64, i32, i32]
         L.prism_polar_flops_per_iter.restype = dbl
@@ -531,6 +540,79 @@ def inv_root_host(mats, q=4, max_iters=30, sketch_size=8, tol=1e-6, seed=42, pre
                                     _i64([t.stride(0) for t in mats]), _ptrs(out), _i64([t.stride(0) for t in out]),
                                     ids, ctypes.byref(o), ctypes.byref(rep), ctypes.c_void_p(st.cuda_stream)),
           "prism_inv_root_host")
+    return out, rb
+
+
+def _square_solve(fn_ws, fn, name, mats, q, max_iters, sketch_size, tol, seed, precision, fit, warmup_iters,
+                  alpha_lo, alpha_hi, out, matrix_ids, stream, handle):
+    import torch
+    mats = list(mats)
+    if not mats:
+        return [], {}
+    precision = _precision_of(mats[0], precision)
+    _check_dtype(mats, precision)
+    for t in mats:
+        if t.shape[0] != t.shape[1]:
+            raise PrismError(f"{name}: matrices must be square")
+    dev = mats[0].device
+    h = handle or default_handle()
+    o = make_options(5, max_iters, sketch_size, tol, seed, precision, fit, warmup_iters, alpha_lo, alpha_hi)
+    B = len(mats)
+    n = _i64([t.shape[0] for t in mats])
+    if out is None:
+        out = [torch.empty_like(t) for t in mats]
+    _check_dtype(out, precision)
+    need = fn_ws(h.h, B, n, ctypes.byref(o))
+    if need == 0:
+        raise PrismError(f"{name} workspace query rejected the arguments: " + lib().prism_last_error().decode())
+    ws = h.workspace(need, dev)
+    rb = _report_buffers(B, max_iters, dev)
+    rep = _report_struct(rb)
+    ids = _i64(matrix_ids) if matrix_ids is not None else None
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    check(fn(h.h, B, n, _ptrs(mats), _i64([t.stride(0) for t in mats]), _ptrs(out), _i64([t.stride(0) for t in out]),
+             ids, ctypes.byref(o), ctypes.byref(rep), ws.data_ptr(), ws.numel(), ctypes.c_void_p(st.cuda_stream)),
+          name)
+    return out, rb
+
+
+def chebyshev_inverse(mats, max_iters=40, sketch_size=8, tol=1e-6, seed=42, precision=None, fit="sketched",
+                      warmup_iters=0, alpha_lo=None, alpha_hi=None, out=None, matrix_ids=None, stream=None,
+                      handle=None):
+    """A^{-1} of a batch of square CUDA matrices via prism_chebyshev_inverse."""
+    return _square_solve(lib().prism_chebyshev_inverse_workspace, lib().prism_chebyshev_inverse,
+                         "prism_chebyshev_inverse", mats, 0, max_iters, sketch_size, tol, seed, precision, fit,
+                         warmup_iters, alpha_lo, alpha_hi, out, matrix_ids, stream, handle)
+
+
+def chebyshev_inverse_host(mats, max_iters=40, sketch_size=8, tol=1e-6, seed=42, precision=None, fit="sketched",
+                           warmup_iters=0, alpha_lo=None, alpha_hi=None, out=None, matrix_ids=None, stream=None,
+                           handle=None, device=None):
+    """A^{-1} of pinned HOST square matrices via prism_chebyshev_inverse_host (as polar_host)."""
+    import torch
+    mats = list(mats)
+    if not mats:
+        return [], {}
+    _check_pinned(mats, "chebyshev_inverse_host")
+    precision = _precision_of(mats[0], precision)
+    _check_dtype(mats, precision, on_host=True)
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    h = handle or default_handle()
+    o = make_options(5, max_iters, sketch_size, tol, seed, precision, fit, warmup_iters, alpha_lo, alpha_hi)
+    B = len(mats)
+    if out is None:
+        out = [torch.empty_like(t).pin_memory() for t in mats]
+    _check_pinned(out, "chebyshev_inverse_host")
+    _check_dtype(out, precision, on_host=True)
+    rb = _report_buffers(B, max_iters, dev)
+    rep = _report_struct(rb)
+    ids = _i64(matrix_ids) if matrix_ids is not None else None
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    check(lib().prism_chebyshev_inverse_host(h.h, B, _i64([t.shape[0] for t in mats]), _ptrs(mats),
+                                             _i64([t.stride(0) for t in mats]), _ptrs(out),
+                                             _i64([t.stride(0) for t in out]), ids, ctypes.byref(o),
+                                             ctypes.byref(rep), ctypes.c_void_p(st.cuda_stream)),
+          "prism_chebyshev_inverse_host")
     return out, rb
 
 

@@ -40,19 +40,22 @@ enum EpiMode : int { EPI_RESID = 0, EPI_POLY = 1, EPI_APPLY = 2, EPI_STORE = 3, 
 //   inverse Newton, root q: CH1_P1 (K1 = R S^T keep, next Q = M S^T),
 //        then Z_j = R Z_{j-1}: CH1_P2 (slot 1), CHI_K2 (slot 2), CH2_P4 (slot 3) for
 //        j < q, and CHI_L<q> for j = q: <V_i, V_j>, V_0 = K1, V_i = -C(q,i) Z_i
+//   Chebyshev inverse (R stored transposed, so a pass gives the rows of W R):
+//        CHC_P1 S R -> next;  CHC_P2 S R^2 keep -> next;  CHC_P3 S R^3: U = S R^2,
+//        V = U - S R^3, <U,U>, <U,V>, <V,V>
 enum ChainPassCode : int { CH2_P1 = 0, CH2_P2, CH2_P3, CH2_P4, CH2_P5, CH1_P1, CH1_P2, CH1_P3,
-                           CHI_K2, CHI_L1, CHI_L2, CHI_L3, CHI_L4, CH_NCODES };
+                           CHI_K2, CHI_L1, CHI_L2, CHI_L3, CHI_L4, CHC_P1, CHC_P2, CHC_P3, CH_NCODES };
 constexpr int kChainG = 15;   // doubles per 32-row group in chain_part (<V_i,V_j>, i <= j <= 4)
 __host__ __device__ constexpr bool chain_is_last(int pass) {
-  return pass == CH2_P5 || pass == CH1_P3 || (pass >= CHI_L1 && pass <= CHI_L4);
+  return pass == CH2_P5 || pass == CH1_P3 || pass == CHC_P3 || (pass >= CHI_L1 && pass <= CHI_L4);
 }
 // kept slots the last pass reads
 __host__ __device__ constexpr int chain_last_slots(int pass) {
-  return pass == CH2_P5 ? 4 : pass == CH1_P3 ? 2 : pass - CHI_L1 + 1;
+  return pass == CH2_P5 ? 4 : pass == CH1_P3 ? 2 : pass == CHC_P3 ? 1 : pass - CHI_L1 + 1;
 }
 // <Va,Vb> values the last pass writes
 __host__ __device__ constexpr int chain_ng(int pass) {
-  return (pass >= CHI_L1 && pass <= CHI_L4) ? (pass - CHI_L1 + 2) * (pass - CHI_L1 + 3) / 2 : 6;
+  return (pass >= CHI_L1 && pass <= CHI_L4) ? (pass - CHI_L1 + 2) * (pass - CHI_L1 + 3) / 2 : pass == CHC_P3 ? 3 : 6;
 }
 
 struct GemmProblem {
@@ -745,7 +748,23 @@ __device__ __forceinline__ void epi_chain(const ChainPre& pre, int i, int grp, c
         keep[(slot * M + i) * p + c] = o[c];
         store_w<Cfg>(P, c, p, i, o[c]);
       }
-    } else if constexpr (pass >= CHI_L1) {
+    } else if constexpr (pass == CHC_P1 || pass == CHC_P2) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        if (c < c0 || c >= c1) continue;
+        if constexpr (pass == CHC_P2) keep[i * p + c] = o[c];
+        store_w<Cfg>(P, c, p, i, o[c]);
+      }
+    } else if constexpr (pass == CHC_P3) {
+      const float(&kv)[4][8] = *reinterpret_cast<const float(*)[4][8]>(pre.v);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        if (c < c0 || c >= c1) continue;
+        const double u = (double)kv[0][c];
+        const double v = u - (double)o[c];
+        g[0] += u * u; g[1] += u * v; g[2] += v * v;
+      }
+    } else if constexpr (pass >= CHI_L1 && pass <= CHI_L4) {
       // inverse Newton: m(a) = ||sum_i a^i V_i||^2, V_0 = K1, V_i = -C(q,i) Z_i (Z_q = this
       // pass's output); <V_i, V_j> for i <= j in row-major upper-triangle order
       constexpr int q = pass - CHI_L1 + 1;

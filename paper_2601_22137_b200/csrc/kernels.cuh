@@ -69,6 +69,7 @@ struct SolveParams {
   const double* fro2_in;   // row-block: all-reduced sum of squares (else null)
   int batch, p, d, max_iters, warmup, fit, precision, kind_sqrt;
   int inv_q;            // coupled inverse Newton root order (0: polar / sqrt / sign)
+  int kind_cheb;        // Chebyshev inverse (A' in Y[0], X_0 = A'^T, output X / c)
   double tol, alo, ahi, ataylor;
   unsigned long long seed;
 };
@@ -332,6 +333,14 @@ __global__ void __launch_bounds__(256) k_normalize(SolveParams P) {
     const int nv = min(V::VE, D.n - col);
     V x;
     x.load(D.A, nullptr, (long long)r * D.lda + col, nv, src_vec && nv == V::VE);
+    if (P.kind_cheb) {
+      // A' = A/c (row-major, Y[0]) and X_0 = A'^T: transposed scalar stores
+      x.store(D.Y[0], D.Y_lo[0], (long long)r * D.ldx + col, nv, nv == V::VE, inv, PREC == 1);
+#pragma unroll
+      for (int e = 0; e < V::VE; ++e)
+        if (e < nv) store_x(D.X[0], D.X_lo[0], (long long)(col + e) * D.ldx + r, x.v[e] * inv, PREC);
+      continue;
+    }
     if (P.inv_q) {
       const double cq = 2.0 * c / (P.inv_q + 1);
       x.store(D.Y[0], D.Y_lo[0], (long long)r * D.ldx + col, nv, nv == V::VE, c > 0.0 ? (float)(1.0 / cq) : 0.f,
@@ -719,7 +728,7 @@ __global__ void __launch_bounds__(256) k_alpha(SolveParams P) {
     // <Va, Vb> from the chain's per-32-row-group partials (R17): lane l
     // sums groups l, l+32, ... in order, then a fixed xor tree — reproducible bit for bit
     const int q = P.inv_q;
-    const int ng = q ? (q + 1) * (q + 2) / 2 : 6;
+    const int ng = q ? (q + 1) * (q + 2) / 2 : P.kind_cheb ? 3 : 6;
     double g[kChainG];
 #pragma unroll
     for (int j = 0; j < kChainG; ++j) g[j] = 0.0;
@@ -734,7 +743,11 @@ __global__ void __launch_bounds__(256) k_alpha(SolveParams P) {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) g[j] += __shfl_xor_sync(0xffffffffu, g[j], o);
     }
-    if (q) {
+    if (P.kind_cheb) {
+      // Chebyshev: m(a) = ||U - a V||^2 (R26), closed form on [1/2, 2]
+      double c[5] = {g[0], -2.0 * g[1], g[2], 0.0, 0.0};
+      a = (k < P.warmup) ? P.ahi : argmin_quartic(c, P.alo, P.ahi, P.ataylor);
+    } else if (q) {
       // inverse Newton: m(a) = ||sum_i a^i V_i||^2 -> c_{i+j} += (2 - [i == j]) <V_i, V_j>
       double c[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
       int idx = 0;
@@ -788,7 +801,9 @@ __global__ void __launch_bounds__(256) k_finalize(SolveParams P) {
 #pragma unroll
       for (int e = 0; e < V::VE; ++e) o.v[e] = x.v[e];
       const bool vq = q_vec && nv == V::VE && ((reinterpret_cast<uintptr_t>(D.Q) & 15) == 0);
-      o.store(D.Q, nullptr, qi, nv, vq, (P.kind_sqrt && S.c > 0.0) ? fs : (P.kind_sqrt ? 0.f : 1.f), false);
+      const float sq = P.kind_cheb ? (S.c > 0.0 ? (float)(1.0 / S.c) : 0.f)
+                                   : (P.kind_sqrt && S.c > 0.0) ? fs : (P.kind_sqrt ? 0.f : 1.f);
+      o.store(D.Q, nullptr, qi, nv, vq, sq, false);
     }
     if (P.kind_sqrt && D.Q2) {
       V y;

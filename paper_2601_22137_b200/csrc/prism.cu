@@ -195,7 +195,10 @@ cudaError_t launch_chaint_cfg(int pass, const GemmLaunch& L, cudaStream_t st) {
     case CHI_L1: return launch_chaint_pass<Cfg, CHI_L1>(L, st);
     case CHI_L2: return launch_chaint_pass<Cfg, CHI_L2>(L, st);
     case CHI_L3: return launch_chaint_pass<Cfg, CHI_L3>(L, st);
-    default: return launch_chaint_pass<Cfg, CHI_L4>(L, st);
+    case CHI_L4: return launch_chaint_pass<Cfg, CHI_L4>(L, st);
+    case CHC_P1: return launch_chaint_pass<Cfg, CHC_P1>(L, st);
+    case CHC_P2: return launch_chaint_pass<Cfg, CHC_P2>(L, st);
+    default: return launch_chaint_pass<Cfg, CHC_P3>(L, st);
   }
 }
 
@@ -295,9 +298,11 @@ struct Request {
   float* G = nullptr;      // row-block: fp32 partial Gram output (n x n, ld n)
   bool sign_kind = false;  // matrix sign: square path, R = I - X^2, X only (output in Q)
   int inv_q = 0;           // coupled inverse Newton A^{-1/q}: X in X[], M in Y[], R = I - M (output in Q)
+  bool cheb_kind = false;  // Chebyshev inverse: A' = A/c in Y[0], R stored transposed, output X / c in Q
 };
 
-void resolve_interval(prism_options& o, double& lo, double& hi, double& aT, int& d, int inv_q = 0) {
+void resolve_interval(prism_options& o, double& lo, double& hi, double& aT, int& d, int inv_q = 0,
+                      bool cheb = false) {
   d = (o.degree == 3) ? 1 : 2;
   double dlo = d == 1 ? 0.5 : 0.375, dhi = d == 1 ? 1.0 : 1.45;
   aT = d == 1 ? 0.5 : 0.375;   // Taylor coefficient of xi^d in (1-xi)^{-1/2}
@@ -306,6 +311,12 @@ void resolve_interval(prism_options& o, double& lo, double& hi, double& aT, int&
     dlo = 0.5 / inv_q;
     dhi = 2.0 / inv_q;
     aT = 1.0 / inv_q;
+  }
+  if (cheb) {                  // Chebyshev: [1/2, 2], Taylor 1 (f_2 = 1 + xi + xi^2)
+    d = 2;
+    dlo = 0.5;
+    dhi = 2.0;
+    aT = 1.0;
   }
   lo = std::isnan(o.alpha_lo) ? dlo : o.alpha_lo;
   hi = std::isnan(o.alpha_hi) ? dhi : o.alpha_hi;
@@ -351,7 +362,8 @@ prism_status build_plan(const Request& r, Plan& P) {
   prism_options o = r.o;
   double lo, hi, aT;
   int d;
-  resolve_interval(o, lo, hi, aT, d, r.inv_q);
+  resolve_interval(o, lo, hi, aT, d, r.inv_q, r.cheb_kind);
+  const bool cheb = r.cheb_kind;
   const int prec = o.precision;
   const int iq = r.inv_q;
   const int esz = elem_size(prec);
@@ -401,21 +413,21 @@ prism_status build_plan(const Request& r, Plan& P) {
     for (int t = 0; t < 2; ++t) {
       D.X[t] = bump.take(xbytes);
       D.X_lo[t] = split ? bump.take(xbytes) : nullptr;
-      if (r.sqrt_kind || iq) {
+      if (r.sqrt_kind || iq || (cheb && t == 0)) {
         D.Y[t] = bump.take(xbytes);
         D.Y_lo[t] = split ? bump.take(xbytes) : nullptr;
       }
     }
     D.R = bump.take(rbytes);
     D.R_lo = split ? bump.take(rbytes) : nullptr;
-    void* Pm = (iq ? iq >= 2 : d == 2) ? bump.take(rbytes) : nullptr;
+    void* Pm = (iq ? iq >= 2 : d == 2) ? bump.take(rbytes) : nullptr;   // Chebyshev: d = 2 (P^T)
     void* Pm_lo = (Pm && split) ? bump.take(rbytes) : nullptr;
     void* Pm2 = iq >= 3 ? bump.take(rbytes) : nullptr;
     void* Pm2_lo = (Pm2 && split) ? bump.take(rbytes) : nullptr;
     D.gdiag = reinterpret_cast<float*>(bump.take(sizeof(float) * s));
     D.tiles_m = (s + 127) / 128;
     D.tiles_n = (s + BN - 1) / BN;
-    D.sym = (r.sqrt_kind || r.sign_kind || iq || r.rowblock) ? 0 : 1;
+    D.sym = (r.sqrt_kind || r.sign_kind || iq || cheb || r.rowblock) ? 0 : 1;
     D.norm_part = reinterpret_cast<float*>(bump.take(sizeof(float) * D.tiles_m * D.tiles_n));
     const long long ldS = (long long)align_up(s, 64);
     D.ldS = ldS;
@@ -456,7 +468,32 @@ prism_status build_plan(const Request& r, Plan& P) {
       }
       return h;
     };
-    if (iq) {
+    if (cheb) {
+      // Chebyshev with R^T stored: R^T = I - X^T A'^T (A = X MN-major, B = A'
+      // K-major), P^T = R^T + a R^T R^T, X' = X + X P (B = P^T K-major)
+      const int nn = s;
+      for (int t = 0; t < 2; ++t) {
+        HostProblem g = mk(nn, nn, nn, EPI_RESID, 0, D.R, D.R_lo, ldr, nullptr, nullptr, 0);
+        g.p.norm_part = D.norm_part;
+        g.p.gdiag = D.gdiag;
+        g.p.a_mn = 1;
+        g.mapA = add_map(D.X[t], nn, nn, ldx, OP_MN);
+        g.mapB = add_map(D.Y[0], nn, nn, ldx, OP_BK);
+        if (split) { g.mapA_lo = add_map(D.X_lo[t], nn, nn, ldx, OP_MN); g.mapB_lo = add_map(D.Y_lo[0], nn, nn, ldx, OP_BK); }
+        P.gram[t].probs.push_back(g);
+        HostProblem ax = mk(nn, nn, nn, EPI_APPLY, 0, D.X[1 - t], D.X_lo[1 - t], ldx, D.X[t], D.X_lo[t], ldx);
+        ax.mapA = add_map(D.X[t], nn, nn, ldx, OP_A);
+        ax.mapB = add_map(Pm, nn, nn, ldr, OP_BK);
+        if (split) { ax.mapA_lo = add_map(D.X_lo[t], nn, nn, ldx, OP_A); ax.mapB_lo = add_map(Pm_lo, nn, nn, ldr, OP_BK); }
+        P.apply[t].probs.push_back(ax);
+      }
+      HostProblem q = mk(nn, nn, nn, EPI_POLY, 0, Pm, Pm_lo, ldr, D.R, D.R_lo, ldr);   // c1 = 1, a^1
+      q.p.b_mn = 1;
+      q.mapA = add_map(D.R, nn, nn, ldr, OP_A);
+      q.mapB = add_map(D.R, nn, nn, ldr, OP_MN);
+      if (split) { q.mapA_lo = add_map(D.R_lo, nn, nn, ldr, OP_A); q.mapB_lo = add_map(D.R_lo, nn, nn, ldr, OP_MN); }
+      P.square.probs.push_back(q);
+    } else if (iq) {
       // coupled inverse Newton: R = I - M (elementwise, k_resid_inv),
       // X' = X + a X R, M' = (I + a R)^q M = M + P_q M with P_q = (I + a R)^q - I:
       //   q = 1: P_1 = a R (in the apply epilogue)
@@ -609,11 +646,12 @@ prism_status build_plan(const Request& r, Plan& P) {
       static const int nin1[3] = {2, 2, 2};
       static const int codesi[4][5] = {{CH1_P1, CHI_L1}, {CH1_P1, CH1_P2, CHI_L2}, {CH1_P1, CH1_P2, CHI_K2, CHI_L3},
                                        {CH1_P1, CH1_P2, CHI_K2, CH2_P4, CHI_L4}};
-      const int npass = iq ? iq + 1 : d == 2 ? 5 : 3;
+      static const int codesc[3] = {CHC_P1, CHC_P2, CHC_P3};
+      const int npass = cheb ? 3 : iq ? iq + 1 : d == 2 ? 5 : 3;
       for (int j = 0; j < npass; ++j) {
-        const int N = (iq ? 2 : d == 2 ? nin2[j] : nin1[j]) * p;
+        const int N = ((iq || cheb) ? 2 : d == 2 ? nin2[j] : nin1[j]) * p;
         HostProblem c = mk(s, N, s, EPI_CHAIN, 0, nullptr, nullptr, 0, nullptr, nullptr, 0);
-        c.p.pass = iq ? codesi[iq - 1][j] : d == 2 ? codes2[j] : codes1[j];
+        c.p.pass = cheb ? codesc[j] : iq ? codesi[iq - 1][j] : d == 2 ? codes2[j] : codes1[j];
         c.p.S = D.S;
         c.p.Rg = D.R;
         c.p.Rg_lo = D.R_lo;
@@ -642,7 +680,7 @@ prism_status build_plan(const Request& r, Plan& P) {
   P.inv_q = iq;
   P.has_square = iq ? iq >= 2 : d == 2;
   P.has_square2 = iq >= 3;
-  P.n_chain = iq ? iq + 1 : (d == 2) ? 5 : 3;
+  P.n_chain = cheb ? 3 : iq ? iq + 1 : (d == 2) ? 5 : 3;
   // tile lists (problem index within its launch)
   auto finish = [&](LaunchDesc& L, bool) {
     L.tiles.clear();
@@ -779,6 +817,7 @@ prism_status build_plan(const Request& r, Plan& P) {
   S.precision = prec;
   S.kind_sqrt = r.sqrt_kind ? 1 : 0;
   S.inv_q = iq;
+  S.kind_cheb = cheb ? 1 : 0;
   S.tol = o.tol;
   S.alo = lo;
   S.ahi = hi;
@@ -942,6 +981,7 @@ static std::vector<long long> make_key(const Request& r) {
   k.push_back(r.sqrt_kind);
   k.push_back(r.sign_kind);
   k.push_back(r.inv_q);
+  k.push_back(r.cheb_kind);
   k.push_back(r.rowblock);
   k.push_back((long long)(uintptr_t)r.G);
   k.push_back(r.batch);
@@ -1226,7 +1266,8 @@ static cudaError_t copy_block(void* dst, size_t dld, const void* src, size_t sld
 }
 
 // End-to-end path on host buffers (see prism.h): stage, solve, return, pipelined.
-// kind: 0 polar, 1 sqrt / inverse sqrt, 2 sign, 3 inverse q-th root (square inputs for 1-3)
+// kind: 0 polar, 1 sqrt / inverse sqrt, 2 sign, 3 inverse q-th root, 4 Chebyshev inverse
+// (square inputs for 1-4)
 static prism_status host_solve(prism_handle h, int kind, int inv_q, int batch, const int64_t* m, const int64_t* n,
                                const void* const* A_host, const int64_t* lda, void* const* O1, void* const* O2,
                                const int64_t* ldo, const int64_t* ids, const prism_options* o,
@@ -1265,6 +1306,7 @@ static prism_status host_solve(prism_handle h, int kind, int inv_q, int batch, c
   const size_t ws_need = sqrt_kind ? prism_sqrt_workspace(h, batch, m, o)
                          : kind == 2 ? prism_sign_workspace(h, batch, m, o)
                          : kind == 3 ? prism_inv_root_workspace(h, batch, m, inv_q, o)
+                         : kind == 4 ? prism_chebyshev_inverse_workspace(h, batch, m, o)
                                      : prism_polar_workspace(h, batch, m, n, o);
   if (!ws_need) return fail(PRISM_ERR_INVALID_ARG, "workspace query failed");
   if (sl.in_bytes < bytes || sl.out_bytes < bytes || (two && !sl.out2) || h->hws_bytes < ws_need) {
@@ -1315,6 +1357,9 @@ static prism_status host_solve(prism_handle h, int kind, int inv_q, int batch, c
   if (sqrt_kind)
     st = prism_sqrt_invsqrt(h, batch, m, din.data(), ldc.data(), O1 ? dout.data() : nullptr,
                             O2 ? dout2.data() : nullptr, ldc.data(), ids, o, rep, h->hws, h->hws_bytes, h->s_comp);
+  else if (kind == 4)
+    st = prism_chebyshev_inverse(h, batch, m, din.data(), ldc.data(), dout.data(), ldc.data(), ids, o, rep, h->hws,
+                                 h->hws_bytes, h->s_comp);
   else if (kind == 3)
     st = prism_inv_root(h, batch, m, inv_q, din.data(), ldc.data(), dout.data(), ldc.data(), ids, o, rep, h->hws,
                         h->hws_bytes, h->s_comp);
@@ -1429,6 +1474,45 @@ prism_status prism_inv_root_host(prism_handle h, int batch, const int64_t* n, in
                       static_cast<cudaStream_t>(stream));
   } catch (...) {
     return fail(PRISM_ERR_INTERNAL, "exception in prism_inv_root_host");
+  }
+}
+
+size_t prism_chebyshev_inverse_workspace(prism_handle h, int batch, const int64_t* n, const prism_options* o) {
+  if (!h || !o || !n || batch < 1) return 0;
+  std::vector<const void*> fakeA(batch, reinterpret_cast<const void*>(256));
+  std::vector<void*> fakeQ(batch, reinterpret_cast<void*>(256));
+  std::vector<int64_t> ld(n, n + batch);
+  Request r{false, batch, n, n, fakeA.data(), ld.data(), fakeQ.data(), nullptr, ld.data(), nullptr, *o, nullptr};
+  r.cheb_kind = true;
+  if (validate(r)) return 0;
+  Plan P;
+  if (build_plan(r, P)) return 0;
+  return P.ws_need;
+}
+
+prism_status prism_chebyshev_inverse(prism_handle h, int batch, const int64_t* n, const void* const* A,
+                                     const int64_t* lda, void* const* X, const int64_t* ldx,
+                                     const int64_t* matrix_ids, const prism_options* o, const prism_report* rep,
+                                     void* workspace, size_t ws_bytes, void* stream) {
+  try {
+    if (!o) return fail(PRISM_ERR_INVALID_ARG, "null options");
+    Request r{false, batch, n, n, A, lda, X, nullptr, ldx, matrix_ids, *o, static_cast<char*>(workspace)};
+    r.cheb_kind = true;
+    return run_solve(h, r, rep, ws_bytes, static_cast<cudaStream_t>(stream));
+  } catch (...) {
+    return fail(PRISM_ERR_INTERNAL, "exception in prism_chebyshev_inverse");
+  }
+}
+
+prism_status prism_chebyshev_inverse_host(prism_handle h, int batch, const int64_t* n, const void* const* A,
+                                          const int64_t* lda, void* const* X, const int64_t* ldx,
+                                          const int64_t* matrix_ids, const prism_options* o,
+                                          const prism_report* rep, void* stream) {
+  try {
+    return host_solve(h, 4, 0, batch, n, n, A, lda, X, nullptr, ldx, matrix_ids, o, rep,
+                      static_cast<cudaStream_t>(stream));
+  } catch (...) {
+    return fail(PRISM_ERR_INTERNAL, "exception in prism_chebyshev_inverse_host");
   }
 }
 

@@ -23,7 +23,7 @@ h = P.Handle()
 run = (lambda: P.polar(mats, handle=h, **opts)) if kind == "polar" else (lambda: P.sqrt_invsqrt(mats, handle=h, **opts))
 run()
 torch.cuda.synchronize()
-buf = torch.zeros(13 * 1024 * 16, dtype=torch.int64, device="cuda")
+buf = torch.zeros(16 * 1024 * 16, dtype=torch.int64, device="cuda")
 B.check(B.lib().prism_debug_trace_chain(ctypes.c_void_p(buf.data_ptr())), "trace")
 run()
 torch.cuda.synchronize()

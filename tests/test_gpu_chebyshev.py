@@ -1,0 +1,94 @@
+"""PRISM Chebyshev inverse (Appendix A.4) through the C-ABI
+prism_chebyshev_inverse against the fp64 oracle `oracle.prism.chebyshev_inverse` on the
+same seeded general (non-symmetric) inputs: FP32 <= 1e-5, BF16 <= 2e-2, iterations +-1."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2601_22137_b200 as P
+from oracle import prism
+from paper_2601_22137_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def _run(A, prec, tol, max_iters=40, fit="sketched"):
+    dt = torch.bfloat16 if prec == "bf16" else torch.float32
+    At = torch.tensor(A).to(dt).cuda()
+    X, rep = P.chebyshev_inverse([At], tol=tol, max_iters=max_iters, seed=42, precision=prec, fit=fit)
+    torch.cuda.synchronize()
+    Xo, ro = prism.chebyshev_inverse(At.double().cpu().numpy(), p=8, tol=tol, max_iters=max_iters, seed=42, fit=fit)
+    return X[0].double().cpu().numpy(), rep, Xo, ro
+
+
+@pytest.mark.parametrize("n", [40, 200, 517])
+@pytest.mark.parametrize("fit", ["sketched", "taylor"])
+def test_chebyshev_fp32_parity(n, fit):
+    A = W.logspaced(n, n, 0.1, seed=n + 1)          # general A, kappa = 10
+    X, rep, Xo, ro = _run(A, "fp32", 1e-5, fit=fit)
+    assert int(rep["status"][0]) == prism.CONVERGED and ro.status == prism.CONVERGED
+    assert abs(int(rep["iters"][0]) - ro.iters) <= 1
+    assert _rel(X, Xo) <= 1e-5
+
+
+@pytest.mark.parametrize("n", [256, 1024, 2048])
+def test_chebyshev_bf16_parity(n):
+    A = W.logspaced(n, n, 0.1, seed=3 * n)
+    X, rep, Xo, ro = _run(A, "bf16", 3e-2, max_iters=30)
+    assert int(rep["status"][0]) == prism.CONVERGED
+    assert abs(int(rep["iters"][0]) - ro.iters) <= 1
+    assert _rel(X, Xo) <= 2e-2
+
+
+def test_chebyshev_gaussian_fp32_vs_inverse():
+    A = W.gaussian(128, 128, seed=11)
+    At = torch.tensor(A).float().cuda()
+    X, rep = P.chebyshev_inverse([At], tol=1e-5, max_iters=80, precision="fp32")
+    torch.cuda.synchronize()
+    a = At.double().cpu().numpy()
+    assert int(rep["status"][0]) == prism.CONVERGED
+    # A^{-1} in fp32 arithmetic: forward error ~ kappa(A) u (R24)
+    kappa = np.linalg.cond(a)
+    assert _rel(X[0].double().cpu().numpy(), np.linalg.inv(a)) <= max(1e-5, 2e-7 * kappa)
+
+
+def test_chebyshev_batch_mixed_sizes_and_in_place():
+    sizes = [64, 300, 1024, 33]
+    mats = [torch.tensor(W.logspaced(s, s, 0.2, seed=400 + s)).float().cuda() for s in sizes]
+    X, rep = P.chebyshev_inverse(mats, tol=1e-5, max_iters=40, seed=42, precision="fp32", matrix_ids=range(4))
+    torch.cuda.synchronize()
+    for i, a in enumerate(mats):
+        Xo, ro = prism.chebyshev_inverse(a.double().cpu().numpy(), p=8, tol=1e-5, max_iters=40, seed=42, b=i)
+        assert int(rep["status"][i]) == prism.CONVERGED
+        assert abs(int(rep["iters"][i]) - ro.iters) <= 1
+        assert _rel(X[i].double().cpu().numpy(), Xo) <= 1e-5
+    one = mats[2].clone()
+    X1, _ = P.chebyshev_inverse([one], tol=1e-5, max_iters=40, seed=42, precision="fp32", matrix_ids=[2], out=[one])
+    torch.cuda.synchronize()
+    assert torch.equal(X1[0], X[2])
+
+
+def test_chebyshev_host_path_equals_device_path():
+    sizes = [128, 700]
+    dev = [torch.tensor(W.logspaced(s, s, 0.2, seed=500 + s)).to(torch.bfloat16).cuda() for s in sizes]
+    host = [d.cpu().pin_memory() for d in dev]
+    X, rep = P.chebyshev_inverse(dev, tol=3e-2, max_iters=30, seed=42, precision="bf16")
+    for _ in range(3):
+        Xh, reph = P.chebyshev_inverse_host(host, tol=3e-2, max_iters=30, seed=42, precision="bf16")
+    torch.cuda.synchronize()
+    for a, b in zip(X, Xh):
+        assert torch.equal(a.cpu(), b)
+    assert torch.equal(rep["iters"], reph["iters"])
+
+
+def test_chebyshev_zero_input():
+    Z = torch.zeros(64, 64, device="cuda")
+    X, rep = P.chebyshev_inverse([Z], precision="fp32")
+    torch.cuda.synchronize()
+    assert int(rep["status"][0]) == prism.ZERO_INPUT
+    assert not torch.any(X[0])
