@@ -76,6 +76,13 @@ def workload(name: str, rank: int):
         desc = ("Shampoo step with the classic inverse 4th root (configs[2] blocks: 8x1024 + 4x2048 + 2x4096 SPD, "
                 "kappa=1e2, FP32 3xTF32): PRISM coupled inverse Newton A^{-1/4} (P:549-566), tol 1e-5")
         return "shampoo-invroot4-step", shapes, mats, opts, desc, "inv_root"
+    if name == "cheb4096":
+        shapes = [(4096, 4096)]
+        mats = [W.logspaced(4096, 4096, 0.1, seed=4096 + rank)]
+        opts = dict(max_iters=30, tol=3e-2, sketch_size=8, seed=42, precision="bf16")
+        desc = ("single 4096x4096 general (non-symmetric) BF16 matrix, sigma log-spaced in [0.1, 1]: PRISM "
+                "Chebyshev inverse (P:596-629), p=8, tol 3e-2")
+        return "chebyshev-inverse-4096", shapes, mats, opts, desc, "chebyshev"
     raise SystemExit(f"unknown workload {name}")
 
 
@@ -162,6 +169,9 @@ def cpu_oracle_solve(A, kind, opts, b):
     if kind == "sign":
         return prism.sign(A, d=d, p=opts["sketch_size"], tol=opts["tol"], max_iters=opts["max_iters"],
                           seed=opts["seed"], b=b)[1]
+    if kind == "chebyshev":
+        return prism.chebyshev_inverse(A, p=opts["sketch_size"], tol=opts["tol"], max_iters=opts["max_iters"],
+                                       seed=opts["seed"], b=b)[1]
     if kind == "inv_root":
         return prism.inv_root(A, q=opts["q"], p=opts["sketch_size"], tol=opts["tol"], max_iters=opts["max_iters"],
                               seed=opts["seed"], b=b)[1]
@@ -232,7 +242,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="prism", choices=["prism", "reference"])
-    ap.add_argument("--workload", default="gpt2", choices=["gpt2", "square4096", "gpt1b", "shampoo", "sign4096", "invroot"])
+    ap.add_argument("--workload", default="gpt2", choices=["gpt2", "square4096", "gpt1b", "shampoo", "sign4096", "invroot", "cheb4096"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)   # timing rule: >= 3 warm-up steps
@@ -268,9 +278,11 @@ def main():
             return P.sign(inputs, out=out, matrix_ids=ids, handle=h, **opts)
         if kind == "inv_root":
             return P.inv_root(inputs, out=out, matrix_ids=ids, handle=h, **opts)
+        if kind == "chebyshev":
+            return P.chebyshev_inverse(inputs, out=out, matrix_ids=ids, handle=h, **opts)
         return P.sqrt_invsqrt(inputs, matrix_ids=ids, handle=h, **opts)
 
-    outs = [torch.empty_like(m) for m in mats] if kind in ("polar", "sign", "inv_root") else None
+    outs = [torch.empty_like(m) for m in mats] if kind in ("polar", "sign", "inv_root", "chebyshev") else None
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     clocks = ClockSampler(local)
     clocks.start()                      # sampled from the timed region to the end of the GPU passes
@@ -306,6 +318,9 @@ def main():
     status = rep["status"].cpu().tolist()
     if kind == "polar":
         f_iter = [P.polar_flops_per_iter(m, n, opts["degree"], opts["sketch_size"]) for (m, n) in shapes]
+    elif kind == "chebyshev":
+        # A'X (residual), R.R, X.P (general products) + 3 chain passes
+        f_iter = [6.0 * m ** 3 + 6.0 * m * m * opts["sketch_size"] for (m, _) in shapes]
     elif kind == "inv_root":
         # X + aX.R, M + P_q.M, the POLY products of P_q (1 for q = 2, 2 for q = 3, 4), chain
         npoly = {1: 0, 2: 1, 3: 2, 4: 2}[opts["q"]]
@@ -332,6 +347,8 @@ def main():
             return P.polar_host(host, out=host_out, matrix_ids=ids, handle=h, **opts)
         if kind == "sign":
             return P.sign_host(host, out=host_out, matrix_ids=ids, handle=h, **opts)
+        if kind == "chebyshev":
+            return P.chebyshev_inverse_host(host, out=host_out, matrix_ids=ids, handle=h, **opts)
         if kind == "inv_root":
             return P.inv_root_host(host, out=host_out, matrix_ids=ids, handle=h, **opts)
         return P.sqrt_invsqrt_host(host, matrix_ids=ids, handle=h, want_sqrt=False, **opts)[1:]
@@ -371,6 +388,10 @@ def main():
         apply_flops = sum(2.0 * max(m, n) * min(m, n) ** 2 * k for (m, n), k in zip(shapes, iters)) * args.steps
         gram_flops = sum(max(m, n) * min(m, n) * (min(m, n) + 1) * (k + 1) for (m, n), k in zip(shapes, iters)) * args.steps
         sq_flops = sum(min(m, n) ** 2 * (min(m, n) + 1) * k for (m, n), k in zip(shapes, iters)) * args.steps
+    elif kind == "chebyshev":
+        apply_flops = sum(2.0 * m ** 3 * k for (m, _), k in zip(shapes, iters)) * args.steps
+        gram_flops = sum(2.0 * m ** 3 * (k + 1) for (m, _), k in zip(shapes, iters)) * args.steps
+        sq_flops = sum(2.0 * m ** 3 * k for (m, _), k in zip(shapes, iters)) * args.steps
     elif kind == "inv_root":
         npoly = {1: 0, 2: 1, 3: 2, 4: 2}[opts["q"]]
         apply_flops = sum(4.0 * m ** 3 * k for (m, _), k in zip(shapes, iters)) * args.steps
