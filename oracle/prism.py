@@ -24,6 +24,10 @@ Coupled inverse Newton A^{-1/q} (Appendix A.3; q = the paper's p):
 Chebyshev inverse A^{-1} (Appendix A.4):
     A' = A/||A||_F, X_0 = A'^T, R_k = I - A' X_k, X_{k+1} = X_k (I + R_k + a_k R_k^2),
     a_k = argmin_{[1/2,2]} ||S_k (R_k^2 - a (R_k^2 - R_k^3))||_F^2 (quadratic; R25, R26).
+DB Newton, product form (Appendix A.2), SPD A:
+    M_0 = X_0 = A, Y_0 = I, M_{k+1} = 2a(1-a)I + (1-a)^2 M_k + a^2 M_k^{-1},
+    X_{k+1} = (1-a)X_k + a X_k M_k^{-1}, Y likewise; a = unconstrained argmin of the
+    exact quartic ||I - M_{k+1}||_F^2 (trace form, no sketch; R27, R28).
 Coefficient a_k (eq. (4)):
     a_k = argmin_{a in [l,u]} || S_k (I - (I-R_k) g_d(R_k;a)^2) ||_F^2
         = argmin m(a),  m(a) = c0 + c1 a + c2 a^2 + c3 a^3 + c4 a^4
@@ -623,3 +627,112 @@ def chebyshev_inverse(A, p: int = 8, tol: float = 1e-10, max_iters: int = 50, se
         k += 1
     rep.iters = k
     return X / c, rep
+
+
+# --------------------------------------------------------------------------
+# PRISM DB Newton, product form, for A^{1/2}, A^{-1/2} (Appendix A.2; f3)
+# --------------------------------------------------------------------------
+
+def db_newton_coeffs(M: np.ndarray, Minv: np.ndarray) -> np.ndarray:
+    """(c0..c4) of m(a) = ||I - M_{k+1}(a)||_F^2 for symmetric M.
+
+    c1..c4 are the paper's trace forms; traces of squares are sums of squared entries
+    (P:521).  c0 (not printed) = ||I - M||_F^2 (the a = 0 value).
+    """
+    n = M.shape[0]
+    tM, tMi = float(np.trace(M)), float(np.trace(Minv))
+    tM2, tMi2 = float(np.sum(M * M)), float(np.sum(Minv * Minv))
+    c0 = n - 2 * tM + tM2
+    c1 = -4 * n + 8 * tM - 4 * tM2
+    c2 = 10 * n - 14 * tM + 6 * tM2 - 2 * tMi
+    c3 = -12 * n + 12 * tM - 4 * tM2 + 4 * tMi
+    c4 = 6 * n - 4 * tM + tM2 - 4 * tMi + tMi2
+    return np.array([c0, c1, c2, c3, c4])
+
+
+def argmin_quartic_free(c: np.ndarray, alpha_default: float) -> float:
+    """Unconstrained argmin over the reals of m(a) = sum c_i a^i (no interval).
+
+    The global minimum of a quartic with c4 > 0 is at a real root of the cubic m'(a) = 0
+    (P:213); candidates = those roots (two Newton polishes, as argmin_quartic), smallest
+    m wins (ties -> smaller a).  c4 <= 0 or a degenerate loss -> the default (1/2, the
+    classical DB Newton step) (R27).
+    """
+    c = np.asarray(c, dtype=np.float64)
+    scale = float(np.max(np.abs(c[1:])))
+    if not np.isfinite(scale) or scale == 0.0 or scale <= 1e-14 * abs(float(c[0])) or c[4] <= 0.0:
+        return alpha_default
+    d1, d2, d3, d4 = (float(x) / scale for x in c[1:])
+
+    def mprime(a):
+        return ((4.0 * d4 * a + 3.0 * d3) * a + 2.0 * d2) * a + d1
+
+    def msecond(a):
+        return (12.0 * d4 * a + 6.0 * d3) * a + 2.0 * d2
+
+    def m(a):
+        return (((d4 * a + d3) * a + d2) * a + d1) * a
+
+    cands = []
+    for r in _real_roots_cubic(4.0 * d4, 3.0 * d3, 2.0 * d2, d1):
+        for _ in range(2):
+            m2 = msecond(r)
+            if m2 != 0.0:
+                nr = r - mprime(r) / m2
+                if math.isfinite(nr):
+                    r = nr
+        if math.isfinite(r):
+            cands.append(r)
+    if not cands:
+        return alpha_default
+    cands.sort()
+    best, best_m = cands[0], m(cands[0])
+    for a in cands[1:]:
+        ma = m(a)
+        if ma < best_m:
+            best, best_m = a, ma
+    return best
+
+
+def db_newton(A, tol: float = 1e-10, max_iters: int = 50, fit: str = FIT_EXACT):
+    """PRISM DB Newton, product form, for an SPD A in fp64.
+
+        M_0 = A, X_0 = A, Y_0 = I
+        M_{k+1} = 2a(1-a) I + (1-a)^2 M_k + a^2 M_k^{-1}
+        X_{k+1} = (1-a) X_k + a X_k M_k^{-1},  Y_{k+1} = (1-a) Y_k + a Y_k M_k^{-1}
+        a_k = argmin_a ||I - M_{k+1}||_F^2 (exact, unsketched, unconstrained; P:507-523)
+    fit="taylor" keeps a = 1/2 (Cheng et al.'s product form).  Residual R_k =
+    I - M_k; stop test and statuses as polar (R12, R28).  Returns (X ~ A^{1/2},
+    Y ~ A^{-1/2}, Report).  No sketch: the coefficients are O(n^2) traces.
+    """
+    A = np.asarray(A, dtype=np.float64)
+    n = A.shape[0]
+    rep = Report()
+    if not np.any(A):
+        rep.status = ZERO_INPUT
+        return np.zeros_like(A), np.zeros_like(A), rep
+    I = np.eye(n)
+    M, X, Y = A.copy(), A.copy(), I.copy()
+    incr = 0
+    r_prev = math.inf
+    k = 0
+    while True:
+        r = float(np.linalg.norm(I - M, "fro"))     # residual I - M_k (M_k = X_k Y_k -> I)
+        stop, incr = _status_update(rep, k, r, r_prev, n, tol, max_iters, incr)
+        r_prev = r
+        if stop:
+            break
+        Minv = np.linalg.inv(M)
+        if fit == FIT_TAYLOR:
+            a = 0.5
+        else:
+            cf = db_newton_coeffs(M, Minv)
+            rep.coeffs.append(cf)
+            a = argmin_quartic_free(cf, 0.5)
+        rep.alphas.append(a)
+        X = (1 - a) * X + a * (X @ Minv)
+        Y = (1 - a) * Y + a * (Y @ Minv)
+        M = 2 * a * (1 - a) * I + (1 - a) ** 2 * M + a * a * Minv
+        k += 1
+    rep.iters = k
+    return X, Y, rep
