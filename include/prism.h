@@ -200,6 +200,29 @@ prism_status prism_chebyshev_inverse_host(prism_handle h, int batch, const int64
                                           const int64_t* matrix_ids, const prism_options* o,
                                           const prism_report* rep, void* stream);
 
+/*
+ * A^{1/2} and A^{-1/2} of SPD n[i] x n[i] matrices by PRISM-accelerated DB Newton in
+ * product form (Appendix A.2):
+ *   M_0 = X_0 = A, Y_0 = I,  M_{k+1} = 2a(1-a) I + (1-a)^2 M_k + a^2 M_k^{-1},
+ *   X_{k+1} = (1-a) X_k + a X_k M_k^{-1},  Y_{k+1} = (1-a) Y_k + a Y_k M_k^{-1},
+ *   a_k = argmin over the reals of the exact quartic ||I - M_{k+1}||_F^2 (no sketch,
+ *   no interval); fit TAYLOR keeps a = 1/2 (the classical product form).
+ * Stops when ||I - M_k||_F <= tol sqrt(n).  M_k^{-1} is computed on the device by a
+ * blocked Gauss-Jordan sweep (128-blocks, tcgen05 GEMMs).  precision must be
+ * PRISM_FP32 (PRISM_ERR_UNSUPPORTED otherwise); options.degree / sketch_size unused.
+ * Asqrt / Ainvsqrt as prism_sqrt_invsqrt (either may be NULL; unscaled).
+ */
+size_t prism_db_newton_workspace(prism_handle h, int batch, const int64_t* n, const prism_options* o);
+prism_status prism_db_newton(prism_handle h, int batch, const int64_t* n, const void* const* A, const int64_t* lda,
+                             void* const* Asqrt, void* const* Ainvsqrt, const int64_t* ld_out,
+                             const int64_t* matrix_ids, const prism_options* o, const prism_report* rep,
+                             void* workspace, size_t ws_bytes, void* stream);
+/* prism_db_newton on page-locked HOST buffers, pipelined as prism_polar_host. */
+prism_status prism_db_newton_host(prism_handle h, int batch, const int64_t* n, const void* const* A,
+                                  const int64_t* lda, void* const* Asqrt, void* const* Ainvsqrt,
+                                  const int64_t* ld_out, const int64_t* matrix_ids, const prism_options* o,
+                                  const prism_report* rep, void* stream);
+
 /* prism_sign on page-locked HOST buffers, pipelined as prism_polar_host. */
 prism_status prism_sign_host(prism_handle h, int batch, const int64_t* n, const void* const* A, const int64_t* lda,
                              void* const* S, const int64_t* lds, const int64_t* matrix_ids, const prism_options* o,

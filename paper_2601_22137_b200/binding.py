@@ -57,8 +57,10 @@ EXPORTS = [
     "prism_polar_workspace", "prism_polar", "prism_sqrt_workspace", "prism_sqrt_invsqrt",
     "prism_polar_host", "prism_sqrt_invsqrt_host", "prism_sign_workspace", "prism_sign", "prism_sign_host",
     "prism_inv_root_workspace", "prism_inv_root", "prism_inv_root_host",
-                     "prism_chebyshev_inverse", "prism_chebyshev_inverse_host",
+                     "prism_chebyshev_inverse", "prism_chebyshev_inverse_host", "prism_db_newton",
+                     "prism_db_newton_host",
     "prism_chebyshev_inverse_workspace", "prism_chebyshev_inverse", "prism_chebyshev_inverse_host",
+    "prism_db_newton_workspace", "prism_db_newton", "prism_db_newton_host",
     "prism_lpt_partition", "prism_polar_flops_per_iter", "prism_sqrt_flops_per_iter",
     "prism_launch_count", "prism_profile_enable", "prism_profile_read",
     "prism_rowblock_workspace", "prism_rowblock_begin", "prism_rowblock_gram", "prism_rowblock_update",
@@ -123,6 +125,14 @@ def lib():
         L.prism_chebyshev_inverse_host.argtypes = [vp, i32, c_i64p, ctypes.POINTER(vp), c_i64p, ctypes.POINTER(vp),
                                                    c_i64p, c_i64p, ctypes.POINTER(Options), ctypes.POINTER(Report),
                                                    vp]
+        L.prism_db_newton_workspace.argtypes = [vp, i32, c_i64p, ctypes.POINTER(Options)]
+        L.prism_db_newton_workspace.restype = sz
+        L.prism_db_newton.argtypes = [vp, i32, c_i64p, ctypes.POINTER(vp), c_i64p, ctypes.POINTER(vp),
+                                      ctypes.POINTER(vp), c_i64p, c_i64p, ctypes.POINTER(Options),
+                                      ctypes.POINTER(Report), vp, sz, vp]
+        L.prism_db_newton_host.argtypes = [vp, i32, c_i64p, ctypes.POINTER(vp), c_i64p, ctypes.POINTER(vp),
+                                           ctypes.POINTER(vp), c_i64p, c_i64p, ctypes.POINTER(Options),
+                                           ctypes.POINTER(Report), vp]
         L.prism_lpt_partition.argtypes = [i32, ctypes.POINTER(dbl), i32, ctypes.POINTER(ctypes.c_int32)]
         L.prism_polar_flops_per_iter.argtypes = [i64, i64, i32, i32]
         L.prism_polar_flops_per_iter.restype = dbl
@@ -614,6 +624,65 @@ def chebyshev_inverse_host(mats, max_iters=40, sketch_size=8, tol=1e-6, seed=42,
                                              ctypes.byref(rep), ctypes.c_void_p(st.cuda_stream)),
           "prism_chebyshev_inverse_host")
     return out, rb
+
+
+def db_newton(mats, max_iters=30, tol=1e-6, precision="fp32", fit="sketched", warmup_iters=0, want_sqrt=True,
+              want_invsqrt=True, matrix_ids=None, stream=None, handle=None):
+    """A^{1/2}, A^{-1/2} of a batch of SPD CUDA fp32 matrices via prism_db_newton (PRISM DB
+    Newton, product form; the fit is exact and unsketched)."""
+    import torch
+    mats = list(mats)
+    if not mats:
+        return [], [], {}
+    _check_dtype(mats, precision)
+    dev = mats[0].device
+    h = handle or default_handle()
+    o = make_options(5, max_iters, 8, tol, 42, precision, fit, warmup_iters)
+    B = len(mats)
+    n = _i64([t.shape[0] for t in mats])
+    sq = [torch.empty_like(t) for t in mats] if want_sqrt else None
+    isq = [torch.empty_like(t) for t in mats] if want_invsqrt else None
+    ld_out = _i64([t.shape[1] for t in mats])
+    need = lib().prism_db_newton_workspace(h.h, B, n, ctypes.byref(o))
+    if need == 0:
+        raise PrismError("prism_db_newton_workspace rejected the arguments: " + lib().prism_last_error().decode())
+    ws = h.workspace(need, dev)
+    rb = _report_buffers(B, max_iters, dev)
+    rep = _report_struct(rb)
+    ids = _i64(matrix_ids) if matrix_ids is not None else None
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    check(lib().prism_db_newton(h.h, B, n, _ptrs(mats), _i64([t.stride(0) for t in mats]),
+                                _ptrs(sq) if sq else None, _ptrs(isq) if isq else None, ld_out, ids,
+                                ctypes.byref(o), ctypes.byref(rep), ws.data_ptr(), ws.numel(),
+                                ctypes.c_void_p(st.cuda_stream)), "prism_db_newton")
+    return sq, isq, rb
+
+
+def db_newton_host(mats, max_iters=30, tol=1e-6, precision="fp32", fit="sketched", warmup_iters=0, want_sqrt=True,
+                   want_invsqrt=True, matrix_ids=None, stream=None, handle=None, device=None):
+    """A^{1/2}, A^{-1/2} of pinned HOST SPD fp32 matrices via prism_db_newton_host."""
+    import torch
+    mats = list(mats)
+    if not mats:
+        return [], [], {}
+    _check_pinned(mats, "db_newton_host")
+    _check_dtype(mats, precision, on_host=True)
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    h = handle or default_handle()
+    o = make_options(5, max_iters, 8, tol, 42, precision, fit, warmup_iters)
+    B = len(mats)
+    sq = [torch.empty_like(t).pin_memory() for t in mats] if want_sqrt else None
+    isq = [torch.empty_like(t).pin_memory() for t in mats] if want_invsqrt else None
+    rb = _report_buffers(B, max_iters, dev)
+    rep = _report_struct(rb)
+    ids = _i64(matrix_ids) if matrix_ids is not None else None
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    check(lib().prism_db_newton_host(h.h, B, _i64([t.shape[0] for t in mats]), _ptrs(mats),
+                                     _i64([t.stride(0) for t in mats]), _ptrs(sq) if sq else None,
+                                     _ptrs(isq) if isq else None, _i64([t.shape[1] for t in mats]), ids,
+                                     ctypes.byref(o), ctypes.byref(rep), ctypes.c_void_p(st.cuda_stream)),
+          "prism_db_newton_host")
+    return sq, isq, rb
 
 
 class RowBlockSolver:

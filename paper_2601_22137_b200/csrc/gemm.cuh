@@ -12,8 +12,9 @@
 //                                 fp32 diag(D) (= diag G, for the sketch)
 //   POLY   out = c1·C + α·D       (P = ½R + αR², d=2)
 //   APPLY  out = C + s·D          (X ← X + X·P, or X + α·X·R for d=1)
-//          (general form of both: out = κ_C α^{e_C}·C + κ_A α^{e_A}·D, which also
-//          builds the inverse-Newton polynomials (I + αR)^q − I)
+//          (general form of both: out = (κ_C α^{e_C} + λ_C)·C + (κ_A α^{e_A} + λ_A)·D,
+//          which also builds the inverse-Newton polynomials (I + αR)^q − I, P:560-561,
+//          the DB Newton updates (1−α)X + αX·M⁻¹, and its Schur sweeps)
 //   STORE  out = D                (tests)
 // `sym` schedules only tiles touching the upper triangle and mirrors the
 // stores, so XᵀX and R·R cost half a dense GEMM and R, P are exactly symmetric.
@@ -75,9 +76,10 @@ struct GemmProblem {
   long long ldo, ldc;    // leading dimensions (elements)
   int M, N, K;
   int mode, sym, matrix, scale_by_alpha, tiles_n;
-  float c1;              // POLY / APPLY: out = c1 α^eC · C + kA α^eA · D
+  float c1;              // POLY / APPLY: out = (c1 α^eC + lC) · C + (kA α^eA + lA) · D
   float kA;
   int eA, eC;
+  float lA, lC;
   int pass;              // EPI_CHAIN pass code
   int a_mn, b_mn;        // operand major-ness: 0 K-major, 1 MN-major
   int ksplit;            // EPI_CHAIN split-K slices (tile code tn = slice index) or 1
@@ -1068,8 +1070,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
         const double al = (P.eA | P.eC) ? *P.alpha : 1.0;
         const double pa = P.eA == 0 ? 1.0 : P.eA == 1 ? al : P.eA == 2 ? al * al : al * al * al;
         const double pc = P.eC == 0 ? 1.0 : P.eC == 1 ? al : P.eC == 2 ? al * al : al * al * al;
-        coefA = static_cast<float>((double)P.kA * pa);
-        coefC = static_cast<float>((double)P.c1 * pc);
+        coefA = static_cast<float>((double)P.kA * pa + (double)P.lA);
+        coefC = static_cast<float>((double)P.c1 * pc + (double)P.lC);
       }
       const bool needC = (mode == EPI_POLY || mode == EPI_APPLY);
       float sumsq = 0.f;

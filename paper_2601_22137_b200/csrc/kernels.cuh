@@ -48,6 +48,14 @@ struct MatDesc {
   long long ldS;
   int chain_tiles;
   int pad2_;
+  // DB Newton (fp32 3xTF32 only): M_k (plain fp32, ld ldx), Gauss-Jordan sweep temporaries
+  // (E = row block of W, T = D E, D = pivot inverse; hi + lo planes), W = R / R_lo,
+  // per-tile (<E1,E1>, <E1,E2>, <E2,E2>) for the alpha fit
+  float* Mst;
+  void* E; void* E_lo;
+  void* T; void* T_lo;
+  void* Dp; void* Dp_lo;
+  double* dbpart;
 };
 
 struct SolveParams {
@@ -70,6 +78,7 @@ struct SolveParams {
   int batch, p, d, max_iters, warmup, fit, precision, kind_sqrt;
   int inv_q;            // coupled inverse Newton root order (0: polar / sqrt / sign)
   int kind_cheb;        // Chebyshev inverse (A' in Y[0], X_0 = A'^T, output X / c)
+  int kind_db;          // DB Newton (M_k in Mst, W = R: M_k then -M_k^{-1}; output X, Y unscaled)
   double tol, alo, ahi, ataylor;
   unsigned long long seed;
 };
@@ -333,6 +342,17 @@ __global__ void __launch_bounds__(256) k_normalize(SolveParams P) {
     const int nv = min(V::VE, D.n - col);
     V x;
     x.load(D.A, nullptr, (long long)r * D.lda + col, nv, src_vec && nv == V::VE);
+    if (P.kind_db) {
+      // DB Newton: X_0 = M_0 = A, Y_0 = I (no scaling, R28)
+      x.store(D.X[0], D.X_lo[0], (long long)r * D.ldx + col, nv, nv == V::VE, 1.f, PREC == 1);
+#pragma unroll
+      for (int e = 0; e < V::VE; ++e)
+        if (e < nv) D.Mst[(long long)r * D.ldx + col + e] = x.v[e];
+#pragma unroll
+      for (int e = 0; e < V::VE; ++e) x.v[e] = (col + e == r) ? 1.f : 0.f;
+      x.store(D.Y[0], D.Y_lo[0], (long long)r * D.ldx + col, nv, nv == V::VE, 1.f, PREC == 1);
+      continue;
+    }
     if (P.kind_cheb) {
       // A' = A/c (row-major, Y[0]) and X_0 = A'^T: transposed scalar stores
       x.store(D.Y[0], D.Y_lo[0], (long long)r * D.ldx + col, nv, nv == V::VE, inv, PREC == 1);
@@ -408,6 +428,180 @@ __global__ void __launch_bounds__(256) k_resid_inv(SolveParams P, int bn) {
   }
   acc = block_sum<double, 256>(acc, scratch);
   if (threadIdx.x == 0) D.norm_part[tm * D.tiles_n + tn] = (float)acc;
+}
+
+// ----------------------------------------------------------------- DB Newton (f3)
+// fp32 hi + lo (3xTF32 split) element access
+__device__ __forceinline__ float ld_split(const void* hi, const void* lo, long long idx) {
+  return static_cast<const float*>(hi)[idx] + static_cast<const float*>(lo)[idx];
+}
+
+// Iteration start: W = M_k (split, the matrix the sweep inverts in place) and the per-tile
+// ||I - M_k||^2 (residual of P:505; M_k = X_k Y_k -> I) in the Gram tile layout.
+// grid (tiles_n, tiles_m, batch), 128 x bn tiles.
+__global__ void __launch_bounds__(256) k_db_begin(SolveParams P, int bn) {
+  griddep_wait();
+  griddep_launch();
+  __shared__ double scratch[8];
+  const int b = blockIdx.z;
+  const MatDesc& D = P.mats[b];
+  if (P.st[b].done) return;
+  const int tm = blockIdx.y, tn = blockIdx.x;
+  if (tm >= D.tiles_m || tn >= D.tiles_n) return;
+  const int n = D.s;
+  double acc = 0.0;
+  for (int e = threadIdx.x; e < 128 * bn; e += 256) {
+    const int i = tm * 128 + e / bn, j = tn * bn + e % bn;
+    if (i >= n || j >= n) continue;
+    const float m = D.Mst[(long long)i * D.ldx + j];
+    store_x(D.R, D.R_lo, (long long)i * D.ldr + j, m, 1);
+    const double r = (i == j ? 1.0 : 0.0) - (double)m;
+    acc += r * r;
+  }
+  acc = block_sum<double, 256>(acc, scratch);
+  if (threadIdx.x == 0) D.norm_part[tm * D.tiles_n + tn] = (float)acc;
+}
+
+constexpr int kGJ = 128;          // Gauss-Jordan block
+constexpr int kGJCopy = 32;       // CTAs copying the row block per matrix
+
+// Sweep step j, part 1: CTA 0 inverts the pivot block W_JJ (J = [128j, 128j + bj)) by
+// in-place Gauss-Jordan in shared memory (SPD: no pivoting) into D; CTAs 1.. copy the row
+// block E = W_J* (bj x n).  grid (1 + kGJCopy, batch), 512 threads, dynamic smem 66 KB.
+__global__ void __launch_bounds__(512) k_gj_pivot(SolveParams P, int j) {
+  griddep_wait();
+  griddep_launch();
+  extern __shared__ float gsm[];
+  const int b = blockIdx.y;
+  const MatDesc& D = P.mats[b];
+  if (P.st[b].done) return;
+  const int n = D.s, J0 = kGJ * j;
+  if (J0 >= n) return;
+  const int bj = min(kGJ, n - J0);
+  if (blockIdx.x == 0) {
+    float(*a)[kGJ + 1] = reinterpret_cast<float(*)[kGJ + 1]>(gsm);
+    float* rowp = gsm + kGJ * (kGJ + 1);
+    float* colf = rowp + kGJ;
+    for (int e = threadIdx.x; e < kGJ * kGJ; e += 512) {
+      const int r = e / kGJ, c = e % kGJ;
+      a[r][c] = (r < bj && c < bj) ? ld_split(D.R, D.R_lo, (long long)(J0 + r) * D.ldr + J0 + c) : (r == c ? 1.f : 0.f);
+    }
+    __syncthreads();
+    for (int p = 0; p < bj; ++p) {
+      if (threadIdx.x < kGJ) {
+        rowp[threadIdx.x] = a[p][threadIdx.x];
+        colf[threadIdx.x] = a[threadIdx.x][p];
+      }
+      __syncthreads();
+      const float inv = 1.f / rowp[p];
+      for (int e = threadIdx.x; e < kGJ * kGJ; e += 512) {
+        const int i = e / kGJ, c = e % kGJ;
+        if (i == p) a[i][c] = (c == p) ? inv : rowp[c] * inv;
+        else a[i][c] = (c == p) ? -colf[i] * inv : a[i][c] - colf[i] * (rowp[c] * inv);
+      }
+      __syncthreads();
+    }
+    for (int e = threadIdx.x; e < kGJ * kGJ; e += 512) {
+      const int r = e / kGJ, c = e % kGJ;
+      store_x(D.Dp, D.Dp_lo, (long long)r * kGJ + c, (r < bj && c < bj) ? a[r][c] : 0.f, 1);
+    }
+  } else {
+    const long long total = (long long)bj * n;
+    const long long per = (total + kGJCopy - 1) / kGJCopy;
+    const long long beg = (blockIdx.x - 1) * per, end = min(total, beg + per);
+    for (long long e = beg + threadIdx.x; e < end; e += 512) {
+      const int r = (int)(e / n), c = (int)(e - (long long)r * n);
+      const long long src = (long long)(J0 + r) * D.ldr + c, dst = (long long)r * D.ldx + c;
+      static_cast<float*>(D.E)[dst] = static_cast<const float*>(D.R)[src];
+      static_cast<float*>(D.E_lo)[dst] = static_cast<const float*>(D.R_lo)[src];
+    }
+  }
+}
+
+// Sweep step j, part 4 (after T = D E and W -= E^T T): row block J of W <- T, column block
+// J <- T^T, W_JJ <- -D.  After every step, W = -M^{-1} (sweep convention).  grid
+// (ceil(n_max / 128), batch) 128-column strips, 256 threads, dynamic smem 66 KB.
+__global__ void __launch_bounds__(256) k_gj_fix(SolveParams P, int j) {
+  griddep_wait();
+  griddep_launch();
+  extern __shared__ float gsm[];
+  const int b = blockIdx.y;
+  const MatDesc& D = P.mats[b];
+  if (P.st[b].done) return;
+  const int n = D.s, J0 = kGJ * j;
+  if (J0 >= n) return;
+  const int bj = min(kGJ, n - J0);
+  const int c0 = kGJ * blockIdx.x;
+  if (c0 >= n) return;
+  const int w = min(kGJ, n - c0);
+  if (c0 == J0) {
+    for (int e = threadIdx.x; e < bj * bj; e += 256) {
+      const int r = e / bj, c = e % bj;
+      store_x(D.R, D.R_lo, (long long)(J0 + r) * D.ldr + J0 + c, -ld_split(D.Dp, D.Dp_lo, (long long)r * kGJ + c), 1);
+    }
+    return;
+  }
+  float(*t)[kGJ + 1] = reinterpret_cast<float(*)[kGJ + 1]>(gsm);
+  for (int e = threadIdx.x; e < bj * w; e += 256) {
+    const int r = e / w, c = e % w;
+    const float v = ld_split(D.T, D.T_lo, (long long)r * D.ldx + c0 + c);
+    t[r][c] = v;
+    store_x(D.R, D.R_lo, (long long)(J0 + r) * D.ldr + c0 + c, v, 1);   // row block
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < bj * w; e += 256) {
+    const int c = e / bj, r = e % bj;
+    store_x(D.R, D.R_lo, (long long)(c0 + c) * D.ldr + J0 + r, t[r][c], 1);   // column block
+  }
+}
+
+// <E1,E1>, <E1,E2>, <E2,E2> per tile, E1 = I - M^{-1} = I + W, E2 = I - M (fp64; R27).
+__global__ void __launch_bounds__(256) k_db_reduce(SolveParams P, int bn) {
+  griddep_wait();
+  griddep_launch();
+  __shared__ double scratch[8];
+  const int b = blockIdx.z;
+  const MatDesc& D = P.mats[b];
+  if (P.st[b].done) return;
+  const int tm = blockIdx.y, tn = blockIdx.x;
+  if (tm >= D.tiles_m || tn >= D.tiles_n) return;
+  const int n = D.s;
+  double s11 = 0.0, s12 = 0.0, s22 = 0.0;
+  for (int e = threadIdx.x; e < 128 * bn; e += 256) {
+    const int i = tm * 128 + e / bn, j = tn * bn + e % bn;
+    if (i >= n || j >= n) continue;
+    const double d = (i == j) ? 1.0 : 0.0;
+    const double e2 = d - (double)D.Mst[(long long)i * D.ldx + j];
+    const double e1 = d + (double)ld_split(D.R, D.R_lo, (long long)i * D.ldr + j);
+    s11 += e1 * e1; s12 += e1 * e2; s22 += e2 * e2;
+  }
+  s11 = block_sum<double, 256>(s11, scratch);
+  s12 = block_sum<double, 256>(s12, scratch);
+  s22 = block_sum<double, 256>(s22, scratch);
+  if (threadIdx.x == 0) {
+    double* o = D.dbpart + 3 * (tm * D.tiles_n + tn);
+    o[0] = s11; o[1] = s12; o[2] = s22;
+  }
+}
+
+// M_{k+1} = 2a(1-a) I + (1-a)^2 M_k + a^2 M_k^{-1}  (W = -M_k^{-1})
+__global__ void __launch_bounds__(256) k_db_update(SolveParams P, int bn) {
+  griddep_wait();
+  griddep_launch();
+  const int b = blockIdx.z;
+  const MatDesc& D = P.mats[b];
+  if (P.st[b].done) return;
+  const int tm = blockIdx.y, tn = blockIdx.x;
+  if (tm >= D.tiles_m || tn >= D.tiles_n) return;
+  const int n = D.s;
+  const double a = P.st[b].alpha;
+  const float c0 = (float)(2.0 * a * (1.0 - a)), c1 = (float)((1.0 - a) * (1.0 - a)), c2 = (float)(a * a);
+  for (int e = threadIdx.x; e < 128 * bn; e += 256) {
+    const int i = tm * 128 + e / bn, j = tn * bn + e % bn;
+    if (i >= n || j >= n) continue;
+    float* m = D.Mst + (long long)i * D.ldx + j;
+    *m = (i == j ? c0 : 0.f) + c1 * *m - c2 * ld_split(D.R, D.R_lo, (long long)i * D.ldr + j);
+  }
 }
 
 // ----------------------------------------------------------------- a4: Philox sketch
@@ -672,6 +866,39 @@ __device__ double argmin_poly_warp(const double* c, int deg, double lo, double h
   return best;
 }
 
+// Unconstrained argmin of the quartic (DB Newton, R27): the real roots of m' (two Newton
+// polishes), smallest m (ties -> smaller a); c4 <= 0 or degenerate -> a_default.
+__device__ double argmin_quartic_free(const double c[5], double a_default) {
+  const double scale = fmax(fmax(fabs(c[1]), fabs(c[2])), fmax(fabs(c[3]), fabs(c[4])));
+  if (!isfinite(scale) || scale == 0.0 || scale <= 1e-14 * fabs(c[0]) || !(c[4] > 0.0)) return a_default;
+  const double d1 = c[1] / scale, d2 = c[2] / scale, d3 = c[3] / scale, d4 = c[4] / scale;
+  double roots[3];
+  const int nr = real_roots_cubic(4.0 * d4, 3.0 * d3, 2.0 * d2, d1, roots);
+  double best = a_default, bm = INFINITY;
+  double cand[3];
+  int nc = 0;
+  for (int i = 0; i < nr; ++i) {
+    double r = roots[i];
+    for (int it = 0; it < 2; ++it) {
+      const double m2 = (12.0 * d4 * r + 6.0 * d3) * r + 2.0 * d2;
+      if (m2 != 0.0) {
+        const double m1 = ((4.0 * d4 * r + 3.0 * d3) * r + 2.0 * d2) * r + d1;
+        const double nr2 = r - m1 / m2;
+        if (isfinite(nr2)) r = nr2;
+      }
+    }
+    if (isfinite(r)) cand[nc++] = r;
+  }
+  for (int i = 1; i < nc; ++i)
+    for (int j = i; j > 0 && cand[j] < cand[j - 1]; --j) { double t = cand[j]; cand[j] = cand[j - 1]; cand[j - 1] = t; }
+  for (int i = 0; i < nc; ++i) {
+    const double a = cand[i];
+    const double ma = (((d4 * a + d3) * a + d2) * a + d1) * a;
+    if (ma < bm) { best = a; bm = ma; }
+  }
+  return best;
+}
+
 // One block (256 threads) per matrix: residual norm, stop test (R12), and
 // alpha_k from the factored sketched loss m(a) = ||V0 + a V1 + a^2 V2||^2.
 __global__ void __launch_bounds__(256) k_alpha(SolveParams P) {
@@ -680,7 +907,7 @@ __global__ void __launch_bounds__(256) k_alpha(SolveParams P) {
   __shared__ double scratch[8];
   __shared__ int s_stop;
   const int k = *P.iter;
-  const int do_fit = fit_at(P, k) ? 1 : 0;
+  const int do_fit = P.kind_db ? (P.fit != 1 && k < P.max_iters && k >= P.warmup) : (fit_at(P, k) ? 1 : 0);
   const int b = blockIdx.x;
   const MatDesc& D = P.mats[b];
   MatState& S = P.st[b];
@@ -727,6 +954,27 @@ __global__ void __launch_bounds__(256) k_alpha(SolveParams P) {
   } else {
     // <Va, Vb> from the chain's per-32-row-group partials (R17): lane l
     // sums groups l, l+32, ... in order, then a fixed xor tree — reproducible bit for bit
+    if (P.kind_db) {
+      // <E1,E1>, <E1,E2>, <E2,E2> over the tiles (fixed order) -> the exact quartic
+      // m(a) = a^4 <E1,E1> + 2 a^2 (1-a)^2 <E1,E2> + (1-a)^4 <E2,E2>  (R27)
+      double s3[3] = {0.0, 0.0, 0.0};
+      const int nt = D.tiles_m * D.tiles_n;
+      for (int t = threadIdx.x; t < nt; t += 32)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) s3[j] += D.dbpart[3 * t + j];
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s3[j] += __shfl_xor_sync(0xffffffffu, s3[j], o);
+      const double A1 = s3[0], B1 = s3[1], C1 = s3[2];
+      const double c[5] = {C1, -4.0 * C1, 2.0 * B1 + 6.0 * C1, -4.0 * B1 - 4.0 * C1, A1 + 2.0 * B1 + C1};
+      a = argmin_quartic_free(c, P.ataylor);
+      if (threadIdx.x == 0) {
+        S.alpha = a;
+        P.alpha_hist[(size_t)b * P.max_iters + k] = a;
+      }
+      return;
+    }
     const int q = P.inv_q;
     const int ng = q ? (q + 1) * (q + 2) / 2 : P.kind_cheb ? 3 : 6;
     double g[kChainG];
@@ -801,18 +1049,18 @@ __global__ void __launch_bounds__(256) k_finalize(SolveParams P) {
 #pragma unroll
       for (int e = 0; e < V::VE; ++e) o.v[e] = x.v[e];
       const bool vq = q_vec && nv == V::VE && ((reinterpret_cast<uintptr_t>(D.Q) & 15) == 0);
-      const float sq = P.kind_cheb ? (S.c > 0.0 ? (float)(1.0 / S.c) : 0.f)
+      const float sq = P.kind_db ? 1.f : P.kind_cheb ? (S.c > 0.0 ? (float)(1.0 / S.c) : 0.f)
                                    : (P.kind_sqrt && S.c > 0.0) ? fs : (P.kind_sqrt ? 0.f : 1.f);
       o.store(D.Q, nullptr, qi, nv, vq, sq, false);
     }
-    if (P.kind_sqrt && D.Q2) {
+    if ((P.kind_sqrt || P.kind_db) && D.Q2) {
       V y;
       y.load(D.Y[par], D.Y_lo[par], xi, nv, nv == V::VE);
       VO o;
 #pragma unroll
       for (int e = 0; e < V::VE; ++e) o.v[e] = y.v[e];
       const bool vq = q_vec && nv == V::VE && ((reinterpret_cast<uintptr_t>(D.Q2) & 15) == 0);
-      o.store(D.Q2, nullptr, qi, nv, vq, fi, false);
+      o.store(D.Q2, nullptr, qi, nv, vq, P.kind_db ? 1.f : fi, false);
     }
   }
 }

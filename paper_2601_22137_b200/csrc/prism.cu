@@ -274,6 +274,9 @@ struct Plan {
   std::unique_ptr<uint8_t, PinnedDeleter> blob;
   SolveParams params{};
   LaunchDesc gram[2], square, square2, apply[2], chaint[5], gram32[2];
+  std::vector<LaunchDesc> gjT, gjS;   // DB Newton sweep steps: T = D E, W -= E^T T
+  bool db = false;
+  int db_steps = 0;
   int n_chain = 0;
   int chain_ksplit = 1;   // cluster size of the chain launches (split-K; 1, 2 or 4)
   bool has_square = false, has_square2 = false;
@@ -299,10 +302,11 @@ struct Request {
   bool sign_kind = false;  // matrix sign: square path, R = I - X^2, X only (output in Q)
   int inv_q = 0;           // coupled inverse Newton A^{-1/q}: X in X[], M in Y[], R = I - M (output in Q)
   bool cheb_kind = false;  // Chebyshev inverse: A' = A/c in Y[0], R stored transposed, output X / c in Q
+  bool db_kind = false;    // DB Newton product form (sqrt path shapes; FP32 only; outputs in Q, Q2)
 };
 
 void resolve_interval(prism_options& o, double& lo, double& hi, double& aT, int& d, int inv_q = 0,
-                      bool cheb = false) {
+                      bool cheb = false, bool db = false) {
   d = (o.degree == 3) ? 1 : 2;
   double dlo = d == 1 ? 0.5 : 0.375, dhi = d == 1 ? 1.0 : 1.45;
   aT = d == 1 ? 0.5 : 0.375;   // Taylor coefficient of xi^d in (1-xi)^{-1/2}
@@ -317,6 +321,10 @@ void resolve_interval(prism_options& o, double& lo, double& hi, double& aT, int&
     dlo = 0.5;
     dhi = 2.0;
     aT = 1.0;
+  }
+  if (db) {                    // DB Newton: unconstrained; classical step 1/2
+    d = 1;
+    dlo = dhi = aT = 0.5;
   }
   lo = std::isnan(o.alpha_lo) ? dlo : o.alpha_lo;
   hi = std::isnan(o.alpha_hi) ? dhi : o.alpha_hi;
@@ -362,8 +370,10 @@ prism_status build_plan(const Request& r, Plan& P) {
   prism_options o = r.o;
   double lo, hi, aT;
   int d;
-  resolve_interval(o, lo, hi, aT, d, r.inv_q, r.cheb_kind);
+  resolve_interval(o, lo, hi, aT, d, r.inv_q, r.cheb_kind, r.db_kind);
   const bool cheb = r.cheb_kind;
+  const bool db = r.db_kind;
+  int db_steps = 0;
   const int prec = o.precision;
   const int iq = r.inv_q;
   const int esz = elem_size(prec);
@@ -392,7 +402,7 @@ prism_status build_plan(const Request& r, Plan& P) {
     MatDesc& D = mats[i];
     std::memset(&D, 0, sizeof(D));
     const int m = (int)r.m[i];
-    const int n = r.sqrt_kind ? (int)r.m[i] : (int)r.n[i];
+    const int n = (r.sqrt_kind || db) ? (int)r.m[i] : (int)r.n[i];
     D.A = r.A[i];
     D.Q = r.Q ? r.Q[i] : nullptr;
     D.Q2 = r.Q2 ? r.Q2[i] : nullptr;
@@ -400,7 +410,7 @@ prism_status build_plan(const Request& r, Plan& P) {
     D.ldq = r.ldq[i];
     D.m = m;
     D.n = n;
-    if (r.sqrt_kind) { D.s = n; D.L = n; }
+    if (r.sqrt_kind || db) { D.s = n; D.L = n; }
     else if (r.rowblock) { D.s = n; D.L = m; }
     else { D.s = std::min(m, n); D.L = std::max(m, n); }
     D.trans = 0;   // X keeps A's row-major layout (no transposes; MN-major operands instead)
@@ -413,21 +423,21 @@ prism_status build_plan(const Request& r, Plan& P) {
     for (int t = 0; t < 2; ++t) {
       D.X[t] = bump.take(xbytes);
       D.X_lo[t] = split ? bump.take(xbytes) : nullptr;
-      if (r.sqrt_kind || iq || (cheb && t == 0)) {
+      if (r.sqrt_kind || iq || db || (cheb && t == 0)) {
         D.Y[t] = bump.take(xbytes);
         D.Y_lo[t] = split ? bump.take(xbytes) : nullptr;
       }
     }
     D.R = bump.take(rbytes);
     D.R_lo = split ? bump.take(rbytes) : nullptr;
-    void* Pm = (iq ? iq >= 2 : d == 2) ? bump.take(rbytes) : nullptr;   // Chebyshev: d = 2 (P^T)
+    void* Pm = (iq ? iq >= 2 : (d == 2 && !db)) ? bump.take(rbytes) : nullptr;   // Chebyshev: d = 2 (P^T)
     void* Pm_lo = (Pm && split) ? bump.take(rbytes) : nullptr;
     void* Pm2 = iq >= 3 ? bump.take(rbytes) : nullptr;
     void* Pm2_lo = (Pm2 && split) ? bump.take(rbytes) : nullptr;
     D.gdiag = reinterpret_cast<float*>(bump.take(sizeof(float) * s));
     D.tiles_m = (s + 127) / 128;
     D.tiles_n = (s + BN - 1) / BN;
-    D.sym = (r.sqrt_kind || r.sign_kind || iq || cheb || r.rowblock) ? 0 : 1;
+    D.sym = (r.sqrt_kind || r.sign_kind || iq || cheb || db || r.rowblock) ? 0 : 1;
     D.norm_part = reinterpret_cast<float*>(bump.take(sizeof(float) * D.tiles_m * D.tiles_n));
     const long long ldS = (long long)align_up(s, 64);
     D.ldS = ldS;
@@ -468,7 +478,55 @@ prism_status build_plan(const Request& r, Plan& P) {
       }
       return h;
     };
-    if (cheb) {
+    if (db) {
+      // DB Newton: W (= R) is swept in place into -M^{-1} by blocked
+      // Gauss-Jordan (R28), then X' = (1-a) X - a X W, Y' = (1-a) Y - a Y W
+      const int nn = s;
+      const size_t ebytes = (size_t)kGJ * ldx * esz;
+      D.Mst = reinterpret_cast<float*>(bump.take((size_t)nn * ldx * sizeof(float)));
+      D.E = bump.take(ebytes);
+      D.E_lo = bump.take(ebytes);
+      D.T = bump.take(ebytes);
+      D.T_lo = bump.take(ebytes);
+      D.Dp = bump.take((size_t)kGJ * kGJ * esz);
+      D.Dp_lo = bump.take((size_t)kGJ * kGJ * esz);
+      D.dbpart = reinterpret_cast<double*>(bump.take(sizeof(double) * 3 * D.tiles_m * D.tiles_n));
+      const int nb = (nn + kGJ - 1) / kGJ;
+      db_steps = std::max(db_steps, nb);
+      if ((int)P.gjT.size() < nb) { P.gjT.resize(nb); P.gjS.resize(nb); }
+      for (int j = 0; j < nb; ++j) {
+        const int bj = std::min(kGJ, nn - kGJ * j);
+        HostProblem tp = mk(bj, nn, bj, EPI_STORE, 0, D.T, D.T_lo, ldx, nullptr, nullptr, 0);   // T = D E
+        tp.p.b_mn = 1;
+        tp.mapA = add_map(D.Dp, bj, bj, kGJ, OP_A);
+        tp.mapA_lo = add_map(D.Dp_lo, bj, bj, kGJ, OP_A);
+        tp.mapB = add_map(D.E, bj, nn, ldx, OP_MN);
+        tp.mapB_lo = add_map(D.E_lo, bj, nn, ldx, OP_MN);
+        P.gjT[j].probs.push_back(tp);
+        HostProblem sp = mk(nn, nn, bj, EPI_POLY, 1, D.R, D.R_lo, ldr, D.R, D.R_lo, ldr);       // W -= E^T T
+        sp.p.c1 = 1.f; sp.p.eC = 0; sp.p.kA = -1.f; sp.p.eA = 0;
+        sp.p.a_mn = sp.p.b_mn = 1;
+        sp.mapA = add_map(D.E, bj, nn, ldx, OP_MN);
+        sp.mapA_lo = add_map(D.E_lo, bj, nn, ldx, OP_MN);
+        sp.mapB = add_map(D.T, bj, nn, ldx, OP_MN);
+        sp.mapB_lo = add_map(D.T_lo, bj, nn, ldx, OP_MN);
+        P.gjS[j].probs.push_back(sp);
+      }
+      for (int t = 0; t < 2; ++t) {
+        for (int y = 0; y < 2; ++y) {
+          void* const* Z = y ? D.Y : D.X;
+          void* const* Zl = y ? D.Y_lo : D.X_lo;
+          HostProblem u = mk(nn, nn, nn, EPI_APPLY, 0, Z[1 - t], Zl[1 - t], ldx, Z[t], Zl[t], ldx);
+          u.p.c1 = -1.f; u.p.eC = 1; u.p.lC = 1.f;    // (1 - a) Z
+          u.p.kA = -1.f; u.p.eA = 1;                   // - a Z W = a Z M^{-1}
+          u.mapA = add_map(Z[t], nn, nn, ldx, OP_A);
+          u.mapB = add_map(D.R, nn, nn, ldr, OP_BK);   // W symmetric: rows of W
+          u.mapA_lo = add_map(Zl[t], nn, nn, ldx, OP_A);
+          u.mapB_lo = add_map(D.R_lo, nn, nn, ldr, OP_BK);
+          P.apply[t].probs.push_back(u);
+        }
+      }
+    } else if (cheb) {
       // Chebyshev with R^T stored: R^T = I - X^T A'^T (A = X MN-major, B = A'
       // K-major), P^T = R^T + a R^T R^T, X' = X + X P (B = P^T K-major)
       const int nn = s;
@@ -639,7 +697,7 @@ prism_status build_plan(const Request& r, Plan& P) {
       }
     }
     // sketch chain (thin tcgen05 GEMMs): pass j reads W[j%2], writes W[(j+1)%2]
-    {
+    if (!db) {
       static const int codes2[5] = {CH2_P1, CH2_P2, CH2_P3, CH2_P4, CH2_P5};
       static const int codes1[3] = {CH1_P1, CH1_P2, CH1_P3};
       static const int nin2[5] = {2, 4, 4, 2, 2};   // rows of B (= 2 x input width) in units of p
@@ -680,7 +738,10 @@ prism_status build_plan(const Request& r, Plan& P) {
   P.inv_q = iq;
   P.has_square = iq ? iq >= 2 : d == 2;
   P.has_square2 = iq >= 3;
-  P.n_chain = cheb ? 3 : iq ? iq + 1 : (d == 2) ? 5 : 3;
+  P.n_chain = db ? 0 : cheb ? 3 : iq ? iq + 1 : (d == 2) ? 5 : 3;
+  if (db) P.has_square = false;
+  P.db = db;
+  P.db_steps = db_steps;
   // tile lists (problem index within its launch)
   auto finish = [&](LaunchDesc& L, bool) {
     L.tiles.clear();
@@ -696,6 +757,8 @@ prism_status build_plan(const Request& r, Plan& P) {
   }
   if (P.has_square) finish(P.square, !polar_k);
   if (P.has_square2) finish(P.square2, !polar_k);
+  for (LaunchDesc& L : P.gjT) finish(L, false);
+  for (LaunchDesc& L : P.gjS) finish(L, false);
   // chain tiles (chaint.cuh): 256-row tiles of R, each split over a cluster of C CTAs,
   // C = the largest factor of the launch's matrices (smaller factors: empty slices).
   // Tiles of one row tile are contiguous and C-aligned, so slice == cluster rank.
@@ -740,9 +803,11 @@ prism_status build_plan(const Request& r, Plan& P) {
   off += sizeof(int) * (B + 1);
   const size_t ooff_off = off;
   off += sizeof(int) * (B + 1);
-  LaunchDesc* all[13] = {&P.gram[0],   &P.gram[1],   &P.apply[0],  &P.apply[1],  &P.square,     &P.chaint[0],
-                         &P.chaint[1], &P.chaint[2], &P.chaint[3], &P.chaint[4], &P.gram32[0], &P.gram32[1],
-                         &P.square2};
+  std::vector<LaunchDesc*> all = {&P.gram[0],   &P.gram[1],   &P.apply[0],  &P.apply[1],  &P.square,
+                                  &P.chaint[0], &P.chaint[1], &P.chaint[2], &P.chaint[3], &P.chaint[4],
+                                  &P.gram32[0], &P.gram32[1], &P.square2};
+  for (LaunchDesc& L : P.gjT) all.push_back(&L);
+  for (LaunchDesc& L : P.gjS) all.push_back(&L);
   for (LaunchDesc* L : all) {
     off = align_up(off, 128);
     L->probs_off = off;
@@ -818,6 +883,7 @@ prism_status build_plan(const Request& r, Plan& P) {
   S.kind_sqrt = r.sqrt_kind ? 1 : 0;
   S.inv_q = iq;
   S.kind_cheb = cheb ? 1 : 0;
+  S.kind_db = db ? 1 : 0;
   S.tol = o.tol;
   S.alo = lo;
   S.ahi = hi;
@@ -848,11 +914,15 @@ GemmLaunch make_launch(const Plan& P, const LaunchDesc& L, const LaunchDesc* odd
   return g;
 }
 
+constexpr int kGJSmem = (kGJ * (kGJ + 1) + 2 * kGJ) * 4;   // Gauss-Jordan pivot / fix-up tiles
+
 // Make every kernel's large-smem attribute current before any graph capture.
 void ensure_attrs() {
   static bool done = false;
   if (done) return;
   done = true;
+  cudaFuncSetAttribute(k_gj_pivot, cudaFuncAttributeMaxDynamicSharedMemorySize, kGJSmem);
+  cudaFuncSetAttribute(k_gj_fix, cudaFuncAttributeMaxDynamicSharedMemorySize, kGJSmem);
   GemmLaunch z{};
   z.ntiles = 0;
   for (int prec = 0; prec < 3; ++prec) {
@@ -864,10 +934,12 @@ void ensure_attrs() {
 prism_status validate(const Request& r) {
   const prism_options& o = r.o;
   if (r.batch < 1) return fail(PRISM_ERR_INVALID_ARG, "batch must be >= 1");
-  if (!r.m || !r.lda || !r.A || (!r.sqrt_kind && (!r.n || !r.Q || !r.ldq)))
+  if (!r.m || !r.lda || !r.A || (!r.sqrt_kind && !r.db_kind && (!r.n || !r.Q || !r.ldq)))
     return fail(PRISM_ERR_INVALID_ARG, "null size/pointer array");
   if (o.degree != 3 && o.degree != 5) return fail(PRISM_ERR_INVALID_ARG, "degree must be 3 or 5");
   if (r.inv_q < 0 || r.inv_q > 4) return fail(PRISM_ERR_UNSUPPORTED, "inverse root order q must be 1..4");
+  if (r.db_kind && o.precision != PRISM_FP32)
+    return fail(PRISM_ERR_UNSUPPORTED, "DB Newton needs precision FP32 (its M^{-1} sweep is not run in bf16/tf32)");
   if (o.max_iters < 1 || o.max_iters > 10000) return fail(PRISM_ERR_INVALID_ARG, "max_iters out of range");
   if (!(o.tol > 0.0)) return fail(PRISM_ERR_INVALID_ARG, "tol must be > 0");
   if (o.precision < 0 || o.precision > 2) return fail(PRISM_ERR_INVALID_ARG, "bad precision");
@@ -878,11 +950,11 @@ prism_status validate(const Request& r) {
   if (o.warmup_iters < 0) return fail(PRISM_ERR_INVALID_ARG, "warmup_iters must be >= 0");
   const int esz = elem_size(o.precision);
   for (int i = 0; i < r.batch; ++i) {
-    const int64_t m = r.m[i], n = r.sqrt_kind ? r.m[i] : r.n[i];
+    const int64_t m = r.m[i], n = (r.sqrt_kind || r.db_kind) ? r.m[i] : r.n[i];
     if (m < 1 || n < 1 || m > (1 << 20) || n > (1 << 20)) return fail(PRISM_ERR_INVALID_ARG, "bad matrix size");
     if (!r.A[i]) return fail(PRISM_ERR_INVALID_ARG, "null input matrix");
     if (r.lda[i] < n) return fail(PRISM_ERR_INVALID_ARG, "lda < n");
-    if (!r.sqrt_kind && !r.Q[i]) return fail(PRISM_ERR_INVALID_ARG, "null output matrix");
+    if (!r.sqrt_kind && !r.db_kind && !r.Q[i]) return fail(PRISM_ERR_INVALID_ARG, "null output matrix");
     if ((r.Q || r.Q2) && r.ldq[i] < n) return fail(PRISM_ERR_INVALID_ARG, "ldq < n");
     if (std::min(m, n) < o.sketch_size) return fail(PRISM_ERR_INVALID_ARG, "sketch_size > min(m, n)");
     if (reinterpret_cast<uintptr_t>(r.A[i]) % esz) return fail(PRISM_ERR_INVALID_ARG, "misaligned input");
@@ -982,6 +1054,7 @@ static std::vector<long long> make_key(const Request& r) {
   k.push_back(r.sign_kind);
   k.push_back(r.inv_q);
   k.push_back(r.cheb_kind);
+  k.push_back(r.db_kind);
   k.push_back(r.rowblock);
   k.push_back((long long)(uintptr_t)r.G);
   k.push_back(r.batch);
@@ -996,7 +1069,7 @@ static std::vector<long long> make_key(const Request& r) {
   k.push_back((long long)(uintptr_t)r.ws);
   for (int i = 0; i < r.batch; ++i) {
     k.push_back(r.m[i]);
-    k.push_back(r.sqrt_kind ? r.m[i] : r.n[i]);
+    k.push_back((r.sqrt_kind || r.db_kind) ? r.m[i] : r.n[i]);
     k.push_back(r.lda[i]);
     k.push_back(r.ldq ? r.ldq[i] : 0);
     k.push_back((long long)(uintptr_t)r.A[i]);
@@ -1074,8 +1147,13 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
   const GemmLaunch g_apply = make_launch(*P, P->apply[0], &P->apply[1], r.ws, 0, M);
   const GemmLaunch g_sq = make_launch(*P, P->square, nullptr, r.ws, 0, M);
   const GemmLaunch g_sq2 = make_launch(*P, P->square2, nullptr, r.ws, 0, M);
-  int rtm = 1, rtn = 1;   // inverse Newton: tile grid of the residual kernel (largest matrix)
-  if (P->inv_q) {
+  std::vector<GemmLaunch> g_gjT, g_gjS;
+  for (int j = 0; j < P->db_steps; ++j) {
+    g_gjT.push_back(make_launch(*P, P->gjT[j], nullptr, r.ws, 0, M));
+    g_gjS.push_back(make_launch(*P, P->gjS[j], nullptr, r.ws, 0, M));
+  }
+  int rtm = 1, rtn = 1;   // inverse Newton / DB Newton: tile grid of the elementwise kernels (largest matrix)
+  if (P->inv_q || P->db) {
     rtm = (P->max_s + 127) / 128;
     rtn = (P->max_s + tile_bn(prec) - 1) / tile_bn(prec);
   }
@@ -1086,6 +1164,41 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
   const int p = S.p;
   // one iteration k (k read on the device): R_k, stop test, S_k, chain, alpha_k, P, X_{k+1}
   auto body = [&](cudaStream_t s2, cudaGraphConditionalHandle ch, int use_handle, bool timed) -> prism_status {
+    if (P->db) {
+      // DB Newton: W = M_k, sweep W -> -M_k^{-1}, fit a, X/Y GEMMs, M update
+      const dim3 eg(rtn, rtm, B);
+      const int bn = tile_bn(prec);
+      {
+        KindTimer t(h, s2, 0, timed ? 1 : 0);
+        PRISM_CK(launch_k(k_db_begin, eg, dim3(256), 0, s2, 1, S, bn));
+      }
+      {
+        KindTimer t(h, s2, 1, timed ? 4 * P->db_steps : 0);
+        const int strips = (P->max_s + kGJ - 1) / kGJ;
+        for (int j = 0; j < P->db_steps; ++j) {
+          PRISM_CK(launch_k(k_gj_pivot, dim3(1 + kGJCopy, B), dim3(512), kGJSmem, s2, 1, S, j));
+          PRISM_CK(launch_gemm(prec, g_gjT[j], s2));
+          PRISM_CK(launch_gemm(prec, g_gjS[j], s2));
+          PRISM_CK(launch_k(k_gj_fix, dim3(strips, B), dim3(256), kGJSmem, s2, 1, S, j));
+        }
+      }
+      {
+        KindTimer t(h, s2, 3, timed ? 1 : 0);
+        PRISM_CK(launch_k(k_db_reduce, eg, dim3(256), 0, s2, 1, S, bn));
+      }
+      {
+        KindTimer t(h, s2, 4, timed ? 1 : 0);
+        PRISM_CK(launch_k(k_alpha, dim3(B), dim3(256), 0, s2, 1, S));
+      }
+      {
+        KindTimer t(h, s2, 2, timed ? 2 : 0);
+        PRISM_CK(launch_gemm(prec, g_apply, s2));
+        PRISM_CK(launch_k(k_db_update, eg, dim3(256), 0, s2, 1, S, bn));
+      }
+      PRISM_CK(launch_k(k_advance, dim3(1), dim3(256), 0, s2, 1, S, ch, use_handle, P->d_all_done));
+      PRISM_CK(cudaGetLastError());
+      return PRISM_OK;
+    }
     {
       KindTimer t(h, s2, 0, timed ? 1 : 0);
       if (P->inv_q) {
@@ -1119,8 +1232,9 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
     PRISM_CK(cudaGetLastError());
     return PRISM_OK;
   };
-  P->per_iter_launches = 3 + (sketched ? 1 + n_chain_launches : 0) + (P->has_square ? 1 : 0) +
-                         (P->has_square2 ? 1 : 0) + 1;
+  P->per_iter_launches = P->db ? 6 + 4 * P->db_steps
+                                : 3 + (sketched ? 1 + n_chain_launches : 0) + (P->has_square ? 1 : 0) +
+                                      (P->has_square2 ? 1 : 0) + 1;
   if (!h->profiling) {
     if (!P->exec) {
       // build the device-driven loop once per plan: WHILE(any active) { body }
@@ -1266,14 +1380,14 @@ static cudaError_t copy_block(void* dst, size_t dld, const void* src, size_t sld
 }
 
 // End-to-end path on host buffers (see prism.h): stage, solve, return, pipelined.
-// kind: 0 polar, 1 sqrt / inverse sqrt, 2 sign, 3 inverse q-th root, 4 Chebyshev inverse
-// (square inputs for 1-4)
+// kind: 0 polar, 1 sqrt / inverse sqrt, 2 sign, 3 inverse q-th root, 4 Chebyshev inverse,
+// 5 DB Newton sqrt / inverse sqrt (square inputs for 1-5)
 static prism_status host_solve(prism_handle h, int kind, int inv_q, int batch, const int64_t* m, const int64_t* n,
                                const void* const* A_host, const int64_t* lda, void* const* O1, void* const* O2,
                                const int64_t* ldo, const int64_t* ids, const prism_options* o,
                                const prism_report* rep, cudaStream_t caller) {
   if (!h || !o) return fail(PRISM_ERR_INVALID_ARG, "null handle / options");
-  const bool sqrt_kind = kind == 1, square = kind != 0;
+  const bool sqrt_kind = kind == 1 || kind == 5, square = kind != 0;
   if (batch < 1 || !m || !A_host || !lda || !ldo || (kind == 0 && !n) || (!sqrt_kind && !O1))
     return fail(PRISM_ERR_INVALID_ARG, "bad host-path arguments");
   const size_t esz = (size_t)elem_size(o->precision);
@@ -1303,7 +1417,8 @@ static prism_status host_solve(prism_handle h, int kind, int inv_q, int batch, c
   auto& sl = h->slots[h->slot_next];
   h->slot_next = (h->slot_next + 1) % nslots;
   const bool two = sqrt_kind && O1 && O2;
-  const size_t ws_need = sqrt_kind ? prism_sqrt_workspace(h, batch, m, o)
+  const size_t ws_need = kind == 5 ? prism_db_newton_workspace(h, batch, m, o)
+                         : sqrt_kind ? prism_sqrt_workspace(h, batch, m, o)
                          : kind == 2 ? prism_sign_workspace(h, batch, m, o)
                          : kind == 3 ? prism_inv_root_workspace(h, batch, m, inv_q, o)
                          : kind == 4 ? prism_chebyshev_inverse_workspace(h, batch, m, o)
@@ -1354,7 +1469,10 @@ static prism_status host_solve(prism_handle h, int kind, int inv_q, int batch, c
   if (sl.used) PRISM_CK(cudaStreamWaitEvent(h->s_comp, sl.ev_d2h, 0));
   if (tr) cudaEventRecord(te[2], h->s_comp);
   prism_status st;
-  if (sqrt_kind)
+  if (kind == 5)
+    st = prism_db_newton(h, batch, m, din.data(), ldc.data(), O1 ? dout.data() : nullptr, O2 ? dout2.data() : nullptr,
+                         ldc.data(), ids, o, rep, h->hws, h->hws_bytes, h->s_comp);
+  else if (sqrt_kind)
     st = prism_sqrt_invsqrt(h, batch, m, din.data(), ldc.data(), O1 ? dout.data() : nullptr,
                             O2 ? dout2.data() : nullptr, ldc.data(), ids, o, rep, h->hws, h->hws_bytes, h->s_comp);
   else if (kind == 4)
@@ -1513,6 +1631,44 @@ prism_status prism_chebyshev_inverse_host(prism_handle h, int batch, const int64
                       static_cast<cudaStream_t>(stream));
   } catch (...) {
     return fail(PRISM_ERR_INTERNAL, "exception in prism_chebyshev_inverse_host");
+  }
+}
+
+size_t prism_db_newton_workspace(prism_handle h, int batch, const int64_t* n, const prism_options* o) {
+  if (!h || !o || !n || batch < 1) return 0;
+  std::vector<const void*> fakeA(batch, reinterpret_cast<const void*>(256));
+  std::vector<int64_t> ld(n, n + batch);
+  Request r{false, batch, n, n, fakeA.data(), ld.data(), nullptr, nullptr, ld.data(), nullptr, *o, nullptr};
+  r.db_kind = true;
+  if (validate(r)) return 0;
+  Plan P;
+  if (build_plan(r, P)) return 0;
+  return P.ws_need;
+}
+
+prism_status prism_db_newton(prism_handle h, int batch, const int64_t* n, const void* const* A, const int64_t* lda,
+                             void* const* Asqrt, void* const* Ainvsqrt, const int64_t* ld_out,
+                             const int64_t* matrix_ids, const prism_options* o, const prism_report* rep,
+                             void* workspace, size_t ws_bytes, void* stream) {
+  try {
+    if (!o) return fail(PRISM_ERR_INVALID_ARG, "null options");
+    Request r{false, batch, n, n, A, lda, Asqrt, Ainvsqrt, ld_out, matrix_ids, *o, static_cast<char*>(workspace)};
+    r.db_kind = true;
+    return run_solve(h, r, rep, ws_bytes, static_cast<cudaStream_t>(stream));
+  } catch (...) {
+    return fail(PRISM_ERR_INTERNAL, "exception in prism_db_newton");
+  }
+}
+
+prism_status prism_db_newton_host(prism_handle h, int batch, const int64_t* n, const void* const* A,
+                                  const int64_t* lda, void* const* Asqrt, void* const* Ainvsqrt,
+                                  const int64_t* ld_out, const int64_t* matrix_ids, const prism_options* o,
+                                  const prism_report* rep, void* stream) {
+  try {
+    return host_solve(h, 5, 0, batch, n, n, A, lda, Asqrt, Ainvsqrt, ld_out, matrix_ids, o, rep,
+                      static_cast<cudaStream_t>(stream));
+  } catch (...) {
+    return fail(PRISM_ERR_INTERNAL, "exception in prism_db_newton_host");
   }
 }
 
@@ -1815,6 +1971,7 @@ prism_status prism_debug_gemm(prism_handle h, int precision, int b_mn, int mode,
   gp->kA = 1.f;
   gp->eA = (mode == EPI_POLY || scale_by_alpha) ? 1 : 0;
   gp->eC = 0;
+  gp->lA = gp->lC = 0.f;
   gp->a_mn = 0; gp->b_mn = b_mn ? 1 : 0;
   LaunchDesc L;
   HostProblem hp;
