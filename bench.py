@@ -83,6 +83,13 @@ def workload(name: str, rank: int):
         desc = ("single 4096x4096 general (non-symmetric) BF16 matrix, sigma log-spaced in [0.1, 1]: PRISM "
                 "Chebyshev inverse (P:596-629), p=8, tol 3e-2")
         return "chebyshev-inverse-4096", shapes, mats, opts, desc, "chebyshev"
+    if name == "dbnewton":
+        shapes = [(1024, 1024)] * 8 + [(2048, 2048)] * 4 + [(4096, 4096)] * 2
+        mats = [W.spd_logspaced(m, 1e2, seed=100 * rank + i) for i, (m, _) in enumerate(shapes)]
+        opts = dict(max_iters=30, tol=1e-5, sketch_size=8, precision="fp32")
+        desc = ("Shampoo step (configs[2] blocks: 8x1024 + 4x2048 + 2x4096 SPD, kappa=1e2, FP32 3xTF32): PRISM "
+                "DB Newton product form A^{1/2}, A^{-1/2} (P:499-523; exact unsketched fit), tol 1e-5")
+        return "shampoo-dbnewton-step", shapes, mats, opts, desc, "db_newton"
     raise SystemExit(f"unknown workload {name}")
 
 
@@ -98,62 +105,97 @@ def read_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons during the timed region (B200_PROFILING.md)."""
+    """SM clocks and throttle reasons sampled DURING the timed region (B200_PROFILING.md
+    clocks line).  NVML polled every 10 ms from a thread (the timed region of a short run
+    lasts only tens of ms, too short for nvidia-smi's 200 ms loop); nvidia-smi fallback."""
 
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake_slowdown", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
         self.index = index
+        self.samples = []          # (time, sm_mhz, set(reasons))
+        self.max_mhz = None
+        self.t0 = 0.0
+        self.stop_ev = threading.Event()
         self.proc = None
-        self.lines = []
+        self.source = None
 
     def start(self):
         try:
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+            masks = [(nm, getattr(N, attr)) for nm, attr in self.REASONS if hasattr(N, attr)]
+
+            def poll():
+                while not self.stop_ev.is_set():
+                    try:
+                        mhz = float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
+                        r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.samples.append((time.time(), mhz, {nm for nm, m in masks if r & m}))
+                    except Exception:
+                        pass
+                    self.stop_ev.wait(0.01)
+            self.t = threading.Thread(target=poll, daemon=True)
+            self.t.start()
+            self.source = "nvml 10 ms"
+            return
+        except Exception:
+            pass
+        try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read_smi, daemon=True)
             self.t.start()
+            self.source = "nvidia-smi 100 ms"
         except Exception:
             self.proc = None
 
-    def _read(self):
+    def _read_smi(self):
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in self.proc.stdout:
-            self.lines.append((time.time(), line.strip()))
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                mhz = float(f[0])
+                self.max_mhz = float(f[1])
+            except ValueError:
+                continue
+            self.samples.append((time.time(), mhz, {nm for nm, v in zip(names, f[4:8]) if v.lower() == "active"}))
 
     def mark(self):
         """Start of the timed region: samples from here on are reported."""
         self.t0 = time.time()
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        t0 = getattr(self, "t0", 0.0)
-        for ts, ln in self.lines:
-            if ts < t0:
-                continue
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 8:
-                continue
+        self.stop_ev.set()
+        if self.proc is not None:
+            self.proc.terminate()
             try:
-                sm.append(float(f[0]))
-                mx = float(f[1])
-            except ValueError:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.source is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
+        time.sleep(0.02)
+        sm, reasons = [], set()
+        for ts, mhz, rs in list(self.samples):
+            if ts < self.t0:
                 continue
-            for nm, v in zip(names, f[4:8]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+            sm.append(mhz)
+            reasons |= rs
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples": len(sm), "source": self.source}
 
 
 def flush_l2(buf):
@@ -172,6 +214,8 @@ def cpu_oracle_solve(A, kind, opts, b):
     if kind == "chebyshev":
         return prism.chebyshev_inverse(A, p=opts["sketch_size"], tol=opts["tol"], max_iters=opts["max_iters"],
                                        seed=opts["seed"], b=b)[1]
+    if kind == "db_newton":
+        return prism.db_newton(A, tol=opts["tol"], max_iters=opts["max_iters"])[2]
     if kind == "inv_root":
         return prism.inv_root(A, q=opts["q"], p=opts["sketch_size"], tol=opts["tol"], max_iters=opts["max_iters"],
                               seed=opts["seed"], b=b)[1]
@@ -242,7 +286,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="prism", choices=["prism", "reference"])
-    ap.add_argument("--workload", default="gpt2", choices=["gpt2", "square4096", "gpt1b", "shampoo", "sign4096", "invroot", "cheb4096"])
+    ap.add_argument("--workload", default="gpt2", choices=["gpt2", "square4096", "gpt1b", "shampoo", "sign4096", "invroot", "cheb4096",
+                                                             "dbnewton"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)   # timing rule: >= 3 warm-up steps
@@ -280,8 +325,11 @@ def main():
             return P.inv_root(inputs, out=out, matrix_ids=ids, handle=h, **opts)
         if kind == "chebyshev":
             return P.chebyshev_inverse(inputs, out=out, matrix_ids=ids, handle=h, **opts)
+        if kind == "db_newton":
+            return P.db_newton(inputs, matrix_ids=ids, handle=h, **dbo)
         return P.sqrt_invsqrt(inputs, matrix_ids=ids, handle=h, **opts)
 
+    dbo = {k: v for k, v in opts.items() if k != "sketch_size"}
     outs = [torch.empty_like(m) for m in mats] if kind in ("polar", "sign", "inv_root", "chebyshev") else None
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     clocks = ClockSampler(local)
@@ -326,6 +374,9 @@ def main():
         npoly = {1: 0, 2: 1, 3: 2, 4: 2}[opts["q"]]
         f_iter = [(4.0 + 2.0 * npoly) * m ** 3 + 2.0 * (opts["q"] + 1) * m * m * opts["sketch_size"]
                   for (m, _) in shapes]
+    elif kind == "db_newton":
+        # Gauss-Jordan sweep M -> -M^{-1} (2 n^3), X.W and Y.W (4 n^3)
+        f_iter = [6.0 * m ** 3 for (m, _) in shapes]
     elif kind == "sign":
         # general (non-symmetric-kernel) products: X.X, R.R (d = 2), X.P, plus the sketch
         f_iter = [4.0 * m ** 3 + ((2.0 * m ** 3 + 14.0 * m * m * opts["sketch_size"]) if opts["degree"] == 5
@@ -351,6 +402,8 @@ def main():
             return P.chebyshev_inverse_host(host, out=host_out, matrix_ids=ids, handle=h, **opts)
         if kind == "inv_root":
             return P.inv_root_host(host, out=host_out, matrix_ids=ids, handle=h, **opts)
+        if kind == "db_newton":
+            return P.db_newton_host(host, matrix_ids=ids, handle=h, want_sqrt=False, **dbo)[1:]
         return P.sqrt_invsqrt_host(host, matrix_ids=ids, handle=h, want_sqrt=False, **opts)[1:]
 
     for _ in range(4):   # warm: every staging slot's buffers and plan
@@ -397,6 +450,10 @@ def main():
         apply_flops = sum(4.0 * m ** 3 * k for (m, _), k in zip(shapes, iters)) * args.steps
         gram_flops = 0.0   # R = I - M is elementwise (k_resid_inv)
         sq_flops = sum(2.0 * npoly * m ** 3 * k for (m, _), k in zip(shapes, iters)) * args.steps
+    elif kind == "db_newton":
+        apply_flops = sum(4.0 * m ** 3 * k for (m, _), k in zip(shapes, iters)) * args.steps
+        gram_flops = 0.0   # M_k copied / residual formed elementwise (k_db_begin)
+        sq_flops = sum(2.0 * m ** 3 * k for (m, _), k in zip(shapes, iters)) * args.steps   # GJ sweep
     elif kind == "sign":
         apply_flops = sum(2.0 * m ** 3 * k for (m, _), k in zip(shapes, iters)) * args.steps
         gram_flops = sum(2.0 * m ** 3 * (k + 1) for (m, _), k in zip(shapes, iters)) * args.steps
@@ -429,11 +486,17 @@ def main():
                 seen.add(shp)
                 sample.append(i)
         t0 = time.perf_counter()
-        for i in sample:
-            cpu_oracle_solve(A[i], kind, opts, i)
+        done = 0
+        while True:          # whole passes over the one-per-shape sample, ~10 s of CPU work
+            for i in sample:
+                cpu_oracle_solve(A[i], kind, opts, i)
+            done += 1
+            if time.perf_counter() - t0 >= 10.0:
+                break
         sec = time.perf_counter() - t0
-        cpu = {"value": len(sample) / sec, "unit": "solves/s", "cores": blas_threads(), "kind": "oracle",
-               "sample": f"{len(sample)} of {B} matrices (one per distinct shape), fp64 numpy oracle, {sec:.2f} s"}
+        cpu = {"value": done * len(sample) / sec, "unit": "solves/s", "cores": blas_threads(), "kind": "oracle",
+               "sample": f"{done} pass(es) x {len(sample)} of {B} matrices (one per distinct shape), "
+                         f"fp64 numpy oracle, {sec:.2f} s"}
 
     if rank == 0:
         line = {

@@ -479,31 +479,51 @@ __global__ void __launch_bounds__(512) k_gj_pivot(SolveParams P, int j) {
   if (J0 >= n) return;
   const int bj = min(kGJ, n - J0);
   if (blockIdx.x == 0) {
-    float(*a)[kGJ + 1] = reinterpret_cast<float(*)[kGJ + 1]>(gsm);
-    float* rowp = gsm + kGJ * (kGJ + 1);
-    float* colf = rowp + kGJ;
-    for (int e = threadIdx.x; e < kGJ * kGJ; e += 512) {
-      const int r = e / kGJ, c = e % kGJ;
-      a[r][c] = (r < bj && c < bj) ? ld_split(D.R, D.R_lo, (long long)(J0 + r) * D.ldr + J0 + c) : (r == c ? 1.f : 0.f);
+    // Thread t owns column c = t % 128 of rows [32 g, 32 g + 32), g = t / 128, in registers;
+    // step p broadcasts row p and column p through double-buffered shared vectors (one
+    // barrier per step).  Padding outside bj is the identity (untouched by steps p < bj).
+    float* rowp = gsm;                 // [2][kGJ]
+    float* colf = gsm + 2 * kGJ;       // [2][kGJ]
+    const int c = threadIdx.x & (kGJ - 1), g = threadIdx.x >> 7;
+    float a[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const int r = 32 * g + i;
+      a[i] = (r < bj && c < bj) ? ld_split(D.R, D.R_lo, (long long)(J0 + r) * D.ldr + J0 + c) : (r == c ? 1.f : 0.f);
     }
-    __syncthreads();
-    for (int p = 0; p < bj; ++p) {
-      if (threadIdx.x < kGJ) {
-        rowp[threadIdx.x] = a[p][threadIdx.x];
-        colf[threadIdx.x] = a[threadIdx.x][p];
+#pragma unroll 1
+    for (int pb = 0; pb < 4; ++pb) {
+#pragma unroll
+      for (int pi = 0; pi < 32; ++pi) {
+        const int p = 32 * pb + pi;
+        if (p < bj) {
+          const int buf = (p & 1) * kGJ;
+          if (g == pb) rowp[buf + c] = a[pi];
+          if (c == p) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4)
+              *reinterpret_cast<float4*>(colf + buf + 32 * g + i) = make_float4(a[i], a[i + 1], a[i + 2], a[i + 3]);
+          }
+          __syncthreads();
+          const float inv = 1.f / rowp[buf + p];
+          const float rp = rowp[buf + c] * inv;
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            const float4 cf4 = *reinterpret_cast<const float4*>(colf + buf + 32 * g + i);
+            const float cf[4] = {cf4.x, cf4.y, cf4.z, cf4.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              if (g == pb && i + u == pi) a[i + u] = (c == p) ? inv : rp;
+              else a[i + u] = (c == p) ? -cf[u] * inv : a[i + u] - cf[u] * rp;
+            }
+          }
+        }
       }
-      __syncthreads();
-      const float inv = 1.f / rowp[p];
-      for (int e = threadIdx.x; e < kGJ * kGJ; e += 512) {
-        const int i = e / kGJ, c = e % kGJ;
-        if (i == p) a[i][c] = (c == p) ? inv : rowp[c] * inv;
-        else a[i][c] = (c == p) ? -colf[i] * inv : a[i][c] - colf[i] * (rowp[c] * inv);
-      }
-      __syncthreads();
     }
-    for (int e = threadIdx.x; e < kGJ * kGJ; e += 512) {
-      const int r = e / kGJ, c = e % kGJ;
-      store_x(D.Dp, D.Dp_lo, (long long)r * kGJ + c, (r < bj && c < bj) ? a[r][c] : 0.f, 1);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const int r = 32 * g + i;
+      store_x(D.Dp, D.Dp_lo, (long long)r * kGJ + c, (r < bj && c < bj) ? a[i] : 0.f, 1);
     }
   } else {
     const long long total = (long long)bj * n;

@@ -1235,10 +1235,10 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
   P->per_iter_launches = P->db ? 6 + 4 * P->db_steps
                                 : 3 + (sketched ? 1 + n_chain_launches : 0) + (P->has_square ? 1 : 0) +
                                       (P->has_square2 ? 1 : 0) + 1;
+  ensure_attrs();   // large-smem attributes: before the graph capture and the direct launches
   if (!h->profiling) {
     if (!P->exec) {
       // build the device-driven loop once per plan: WHILE(any active) { body }
-      ensure_attrs();
       if (!h->cap) PRISM_CK(cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking));
       cudaGraph_t g;
       PRISM_CK(cudaGraphCreate(&g, 0));

@@ -25,6 +25,14 @@ if a.direct:
 for _ in range(a.solves):
     if kind == "polar":
         Q, rep = P.polar(mats, handle=h, **opts)
+    elif kind == "sign":
+        Q, rep = P.sign(mats, handle=h, **opts)
+    elif kind == "inv_root":
+        Q, rep = P.inv_root(mats, handle=h, **opts)
+    elif kind == "chebyshev":
+        Q, rep = P.chebyshev_inverse(mats, handle=h, **opts)
+    elif kind == "db_newton":
+        X, Y, rep = P.db_newton(mats, handle=h, **{k: v for k, v in opts.items() if k != "sketch_size"})
     else:
         X, Y, rep = P.sqrt_invsqrt(mats, handle=h, **opts)
 torch.cuda.synchronize()
