@@ -72,7 +72,8 @@ struct SolveParams {
   double* fro_part;     // [batch * kFroParts]
   const int* tile_off;  // [batch + 1] prefix of 64x64 layout tiles (normalise: Xt; finalise: output)
   const int* out_tile_off;
-  int n_tiles, n_out_tiles;
+  const int* fro_off;   // [batch + 1] prefix of the per-matrix ||A||_F partial counts (fro_parts)
+  int n_tiles, n_out_tiles, n_fro_blocks;
   double* fro2_out;     // row-block begin: local sum of squares (else null)
   const double* fro2_in;   // row-block: all-reduced sum of squares (else null)
   int batch, p, d, max_iters, warmup, fit, precision, kind_sqrt;
@@ -83,7 +84,12 @@ struct SolveParams {
   unsigned long long seed;
 };
 
-constexpr int kFroParts = 256;   // row-strided partial sums per matrix (fixed order)
+constexpr int kFroParts = 256;   // max ||A||_F partials per matrix (fixed order)
+// partials of an m x n matrix: one per 32 K elements, 1 .. kFroParts (size-only rule)
+__host__ __device__ inline int fro_parts(long long m, long long n) {
+  const long long q = (m * n + 32767) / 32768;
+  return (int)(q < 1 ? 1 : q > kFroParts ? kFroParts : q);
+}
 
 // ----------------------------------------------------------------- helpers
 __device__ __forceinline__ float load_val(const void* base, long long idx, int prec_bf16) {
@@ -111,23 +117,36 @@ __device__ __forceinline__ T block_sum(T v, T* scratch) {
   return t;
 }
 
+// matrix owning flat block t of a per-matrix prefix table off[0..batch]
+__device__ __forceinline__ int find_matrix(const int* off, int batch, int t) {
+  int lo = 0, hi = batch - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (off[mid] <= t) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
 // ----------------------------------------------------------------- a1: ||A||_F partials
-// grid (kFroParts, batch), 256 threads; block j handles a fixed contiguous share of the matrix
-// with 16-byte vector loads when the row layout allows it.
+// One block per partial; a matrix gets fro_parts(m, n) blocks (a function of its size only,
+// so its bits do not depend on the batch), listed by the prefix P.fro_off.  Block j sums a
+// fixed contiguous share of the matrix with 16-byte vector loads when the layout allows it.
 __global__ void __launch_bounds__(256) k_fro_partials(SolveParams P) {
   griddep_wait();
   griddep_launch();
   __shared__ double scratch[8];
-  const MatDesc& D = P.mats[blockIdx.y];
+  const int b = find_matrix(P.fro_off, P.batch, blockIdx.x);
+  const int jp = blockIdx.x - P.fro_off[b], parts = P.fro_off[b + 1] - P.fro_off[b];
+  const MatDesc& D = P.mats[b];
   const int bf16 = P.precision == 0;
   const int esz = bf16 ? 2 : 4, vec = 16 / esz;
   const bool vok = ((D.lda * esz) % 16 == 0) && ((reinterpret_cast<uintptr_t>(D.A) & 15) == 0);
   const long long nv = vok ? D.n / vec : 0;       // 16-B vectors per row
-  // block j sums a fixed contiguous share of the flattened (row, vector) index space,
+  // block jp sums a fixed contiguous share of the flattened (row, vector) index space,
   // four independent 16-B loads in flight per thread (fixed assignment: deterministic)
   const long long total = (long long)D.m * nv;
-  const long long per = (total + kFroParts - 1) / kFroParts;
-  const long long beg = blockIdx.x * per, end = min(total, beg + per);
+  const long long per = (total + parts - 1) / parts;
+  const long long beg = jp * per, end = min(total, beg + per);
   const char* A = static_cast<const char*>(D.A);
   double acc = 0.0;
   for (long long base = beg + threadIdx.x; base < end; base += 4 * 256) {
@@ -160,23 +179,24 @@ __global__ void __launch_bounds__(256) k_fro_partials(SolveParams P) {
   // columns past the last whole vector (n % vec, or every column when unaligned)
   const int c0 = (int)(nv * vec);
   if (c0 < D.n) {
-    for (int r = blockIdx.x; r < D.m; r += kFroParts)
+    for (int r = jp; r < D.m; r += parts)
       for (int c = c0 + threadIdx.x; c < D.n; c += 256) {
         const double x = (double)load_val(D.A, (long long)r * D.lda + c, bf16);
         acc += x * x;
       }
   }
   acc = block_sum<double, 256>(acc, scratch);
-  if (threadIdx.x == 0) P.fro_part[blockIdx.y * kFroParts + blockIdx.x] = acc;
+  if (threadIdx.x == 0) P.fro_part[b * kFroParts + jp] = acc;
 }
 
-// c = ||A||_F per matrix from the row-strided partials (fixed-order tree); one block per matrix
+// c = ||A||_F per matrix from its partials (fixed-order tree); one block per matrix
 __global__ void __launch_bounds__(256) k_fro_final(SolveParams P) {
   griddep_wait();
   griddep_launch();
   __shared__ double scratch[8];
   const int b = blockIdx.x;
-  double v = (threadIdx.x < kFroParts) ? P.fro_part[b * kFroParts + threadIdx.x] : 0.0;
+  const int parts = P.fro_off[b + 1] - P.fro_off[b];
+  double v = (threadIdx.x < parts) ? P.fro_part[b * kFroParts + threadIdx.x] : 0.0;
   v = block_sum<double, 256>(v, scratch);
   if (threadIdx.x == 0) {
     if (P.fro2_out) P.fro2_out[b] = v;   // row-block: the caller all-reduces it
@@ -222,18 +242,6 @@ __global__ void __launch_bounds__(256) k_resid_from_gram(SolveParams P, const fl
   }
   acc = block_sum<double, 256>(acc, scratch);
   if (threadIdx.x == 0) D.norm_part[tm * D.tiles_n + tn] = (float)acc;
-}
-
-// block -> (matrix, tile) over a batch-wide flat tile list
-
-// block -> (matrix, tile) over a batch-wide flat tile list (prefix array off[batch + 1])
-__device__ __forceinline__ int find_matrix(const int* off, int batch, int t) {
-  int lo = 0, hi = batch - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (off[mid] <= t) lo = mid; else hi = mid - 1;
-  }
-  return lo;
 }
 
 __device__ __forceinline__ void store_x(void* hi, void* lo, long long idx, float v, int precision) {

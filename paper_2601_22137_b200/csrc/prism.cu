@@ -357,7 +357,10 @@ void add_tiles(LaunchDesc& L, int prob, int M, int N, int BN, bool sym) {
 // Chain split-K factor of one matrix (cluster of CTAs sharing a 256-row tile of R): a
 // function of its size s alone (never of the batch), so a matrix's bits do not depend on
 // what it is batched with (or on the rank it lands on).  Each slice keeps >= 8 k-blocks.
-int chain_ks(int s) { return s < 1024 ? 1 : s < 2048 ? 2 : 4; }   // clusters of 8 do not all co-schedule
+int chain_ks(int s) {   // clusters of 8 do not all co-schedule
+  static const int small = [] { const char* e = getenv("PRISM_CHAIN_KS_SMALL"); return e ? atoi(e) : 1; }();
+  return s < 1024 ? small : s < 2048 ? 2 : 4;
+}
 
 void sort_tiles_by_cost(LaunchDesc& L) {
   std::stable_sort(L.tiles.begin(), L.tiles.end(), [&](uint32_t a, uint32_t b) {
@@ -786,9 +789,10 @@ prism_status build_plan(const Request& r, Plan& P) {
   if ((int)P.apply[0].probs.size() >= 4096) return fail(PRISM_ERR_UNSUPPORTED, "batch too large (max 2047 sqrt / 4095 polar)");
 
   // flat 64x64 tile prefixes for the layout kernels (normalise over Xt, finalise over the output)
-  std::vector<int> toff(B + 1, 0), ooff(B + 1, 0);
+  std::vector<int> toff(B + 1, 0), ooff(B + 1, 0), foff(B + 1, 0);
   for (int i = 0; i < B; ++i) {
     const MatDesc& D = mats[i];
+    foff[i + 1] = foff[i] + fro_parts(D.m, D.n);
     const int tw = 32 * (16 / esz);   // layout tile: 32 rows x 32 16-byte vectors
     toff[i + 1] = toff[i] + ((D.m + 31) / 32) * ((D.n + tw - 1) / tw);
     ooff[i + 1] = toff[i + 1];
@@ -802,6 +806,8 @@ prism_status build_plan(const Request& r, Plan& P) {
   const size_t toff_off = off;
   off += sizeof(int) * (B + 1);
   const size_t ooff_off = off;
+  off += sizeof(int) * (B + 1);
+  const size_t foff_off = off;
   off += sizeof(int) * (B + 1);
   std::vector<LaunchDesc*> all = {&P.gram[0],   &P.gram[1],   &P.apply[0],  &P.apply[1],  &P.square,
                                   &P.chaint[0], &P.chaint[1], &P.chaint[2], &P.chaint[3], &P.chaint[4],
@@ -834,6 +840,7 @@ prism_status build_plan(const Request& r, Plan& P) {
   std::memcpy(blob + mats_off, mats.data(), sizeof(MatDesc) * B);
   std::memcpy(blob + toff_off, toff.data(), sizeof(int) * (B + 1));
   std::memcpy(blob + ooff_off, ooff.data(), sizeof(int) * (B + 1));
+  std::memcpy(blob + foff_off, foff.data(), sizeof(int) * (B + 1));
   CUtensorMap* hmaps = reinterpret_cast<CUtensorMap*>(blob + maps_off);
   for (size_t j = 0; j < maps.size(); ++j)
     if (!encode_map(&hmaps[j], maps[j])) return fail(PRISM_ERR_CUDA, "cuTensorMapEncodeTiled failed");
@@ -864,6 +871,8 @@ prism_status build_plan(const Request& r, Plan& P) {
   S.mats = reinterpret_cast<MatDesc*>(meta_dev + mats_off);
   S.tile_off = reinterpret_cast<const int*>(meta_dev + toff_off);
   S.out_tile_off = reinterpret_cast<const int*>(meta_dev + ooff_off);
+  S.fro_off = reinterpret_cast<const int*>(meta_dev + foff_off);
+  S.n_fro_blocks = foff[B];
   S.n_tiles = toff[B];
   S.n_out_tiles = ooff[B];
   S.st = d_st;
@@ -1135,7 +1144,7 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
   h->launches = 0;
   {
     KindTimer t(h, st, 5, 3);
-    PRISM_CK(launch_k(k_fro_partials, dim3(dim3(kFroParts, B)), dim3(256), 0, st, 1, S));
+    PRISM_CK(launch_k(k_fro_partials, dim3(S.n_fro_blocks), dim3(256), 0, st, 1, S));
     PRISM_CK(launch_k(k_fro_final, dim3(B), dim3(256), 0, st, 1, S));
     if (prec == PRISM_BF16) PRISM_CK(launch_k(k_normalize<0>, dim3(S.n_tiles), dim3(256), 0, st, 1, S));
     else if (prec == PRISM_FP32) PRISM_CK(launch_k(k_normalize<1>, dim3(S.n_tiles), dim3(256), 0, st, 1, S));
@@ -1798,7 +1807,7 @@ prism_status prism_rowblock_begin(prism_handle h, int64_t rows, int64_t n, const
     cudaStream_t st = static_cast<cudaStream_t>(stream);
       SolveParams S = P->params;
     S.fro2_out = fro2_local;
-    PRISM_CK(launch_k(k_fro_partials, dim3(dim3(kFroParts, 1)), dim3(256), 0, st, 1, S));
+    PRISM_CK(launch_k(k_fro_partials, dim3(S.n_fro_blocks), dim3(256), 0, st, 1, S));
     PRISM_CK(launch_k(k_fro_final, dim3(1), dim3(256), 0, st, 1, S));
     PRISM_CK(cudaGetLastError());
     g_rb.plan = P;

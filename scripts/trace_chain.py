@@ -15,8 +15,11 @@ from paper_2601_22137_b200 import binding as B  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="square4096")
+ap.add_argument("--max-iters", type=int, default=0, help="cap the solve (all matrices still active in the traced pass)")
 a = ap.parse_args()
 name, shapes, mats_np, opts, desc, kind = bench.workload(a.workload, 0)
+if a.max_iters:
+    opts["max_iters"] = a.max_iters
 dt = torch.bfloat16 if opts["precision"] == "bf16" else torch.float32
 mats = [torch.tensor(m).to(dt).cuda() for m in mats_np]
 h = P.Handle()
@@ -28,9 +31,9 @@ B.check(B.lib().prism_debug_trace_chain(ctypes.c_void_p(buf.data_ptr())), "trace
 run()
 torch.cuda.synchronize()
 B.check(B.lib().prism_debug_trace_chain(None), "trace")
-T = buf.view(8, 1024, 16).cpu().numpy().astype(np.float64)
+T = buf.view(16, 1024, 16).cpu().numpy().astype(np.float64)
 names = ["entry", "setup", "pred done", "tma first", "mma done", "acc ready", "sent", "received", "epi done", "epi start"]
-for p in range(8):
+for p in range(16):
     blk = T[p]
     used = blk[:, 0] > 0
     if not used.any():
@@ -47,7 +50,7 @@ for p in range(8):
 # inter-pass timeline in absolute time: last epilogue of pass j -> release of pass j+1
 print("absolute (us from pass-0 entry): pass, last entry, release (pred done) median, last epi done")
 base = None
-for p in range(8):
+for p in range(16):
     blk = T[p]
     used = blk[:, 0] > 0
     if not used.any():
