@@ -487,16 +487,20 @@ def main():
                 sample.append(i)
         t0 = time.perf_counter()
         done = 0
+        oracle_iters = {}
         while True:          # whole passes over the one-per-shape sample, ~10 s of CPU work
             for i in sample:
-                cpu_oracle_solve(A[i], kind, opts, i)
+                oracle_iters[i] = int(cpu_oracle_solve(A[i], kind, opts, i).iters)
             done += 1
             if time.perf_counter() - t0 >= 10.0:
                 break
         sec = time.perf_counter() - t0
         cpu = {"value": done * len(sample) / sec, "unit": "solves/s", "cores": blas_threads(), "kind": "oracle",
                "sample": f"{done} pass(es) x {len(sample)} of {B} matrices (one per distinct shape), "
-                         f"fp64 numpy oracle, {sec:.2f} s"}
+                         f"fp64 numpy oracle, {sec:.2f} s",
+               # iterations to tolerance, device vs the fp64 oracle on the same stored inputs
+               "iters_vs_oracle": {"matrix": sample, "device": [int(iters[i]) for i in sample],
+                                   "oracle": [oracle_iters[i] for i in sample]}}
 
     if rank == 0:
         line = {

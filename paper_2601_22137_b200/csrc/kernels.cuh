@@ -471,12 +471,18 @@ __global__ void __launch_bounds__(256) k_db_begin(SolveParams P, int bn) {
 }
 
 constexpr int kGJ = 128;          // Gauss-Jordan block
-constexpr int kGJCopy = 32;       // CTAs copying the row block per matrix
+constexpr int kGJCopy = 64;       // CTAs copying the row block per matrix
 
 // Sweep step j, part 1: CTA 0 inverts the pivot block W_JJ (J = [128j, 128j + bj)) by
-// in-place Gauss-Jordan in shared memory (SPD: no pivoting) into D; CTAs 1.. copy the row
-// block E = W_J* (bj x n).  grid (1 + kGJCopy, batch), 512 threads, dynamic smem 66 KB.
-__global__ void __launch_bounds__(512) k_gj_pivot(SolveParams P, int j) {
+// Gauss-Jordan (SPD: no pivoting) into D; CTAs 1.. copy the row block E = W_J* (bj x n).
+// grid (1 + kGJCopy, batch), 128 threads.
+// Pivot CTA: thread c owns column c, all 128 rows in registers, kept in rotated order so
+// that the pivot row of every step is register 0: step p reads column p (thread p's
+// registers, broadcast through a double-buffered shared vector, one barrier per step),
+// updates rows 1..127 into registers 0..126 and writes the new pivot row into register
+// 127 — after bj steps row r sits in register (r - bj) mod 128.  Padding outside bj is
+// the identity (untouched by steps p < bj).
+__global__ void __launch_bounds__(kGJ) k_gj_pivot(SolveParams P, int j) {
   griddep_wait();
   griddep_launch();
   extern __shared__ float gsm[];
@@ -487,61 +493,70 @@ __global__ void __launch_bounds__(512) k_gj_pivot(SolveParams P, int j) {
   if (J0 >= n) return;
   const int bj = min(kGJ, n - J0);
   if (blockIdx.x == 0) {
-    // Thread t owns column c = t % 128 of rows [32 g, 32 g + 32), g = t / 128, in registers;
-    // step p broadcasts row p and column p through double-buffered shared vectors (one
-    // barrier per step).  Padding outside bj is the identity (untouched by steps p < bj).
-    float* rowp = gsm;                 // [2][kGJ]
-    float* colf = gsm + 2 * kGJ;       // [2][kGJ]
-    const int c = threadIdx.x & (kGJ - 1), g = threadIdx.x >> 7;
-    float a[32];
+    float* colf = gsm;   // [2][kGJ]
+    const int c = threadIdx.x;
+    float a[kGJ];
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const int r = 32 * g + i;
-      a[i] = (r < bj && c < bj) ? ld_split(D.R, D.R_lo, (long long)(J0 + r) * D.ldr + J0 + c) : (r == c ? 1.f : 0.f);
-    }
+    for (int r = 0; r < kGJ; ++r)
+      a[r] = (r < bj && c < bj) ? ld_split(D.R, D.R_lo, (long long)(J0 + r) * D.ldr + J0 + c) : (r == c ? 1.f : 0.f);
 #pragma unroll 1
-    for (int pb = 0; pb < 4; ++pb) {
+    for (int p = 0; p < bj; ++p) {
+      float* cf = colf + (p & 1) * kGJ;
+      if (c == p) {
 #pragma unroll
-      for (int pi = 0; pi < 32; ++pi) {
-        const int p = 32 * pb + pi;
-        if (p < bj) {
-          const int buf = (p & 1) * kGJ;
-          if (g == pb) rowp[buf + c] = a[pi];
-          if (c == p) {
+        for (int i = 0; i < kGJ; i += 4) *reinterpret_cast<float4*>(cf + i) = make_float4(a[i], a[i + 1], a[i + 2], a[i + 3]);
+      }
+      __syncthreads();
+      const float inv = 1.f / cf[0];
+      const float rp = a[0] * inv;
+      // rows 1..127 -> registers 0..126 (the textbook sweep's arithmetic); only the warp
+      // holding column p takes both paths
+      if (c == p) {
 #pragma unroll
-            for (int i = 0; i < 32; i += 4)
-              *reinterpret_cast<float4*>(colf + buf + 32 * g + i) = make_float4(a[i], a[i + 1], a[i + 2], a[i + 3]);
-          }
-          __syncthreads();
-          const float inv = 1.f / rowp[buf + p];
-          const float rp = rowp[buf + c] * inv;
+        for (int i4 = 0; i4 < kGJ; i4 += 4) {
+          const float4 f4 = *reinterpret_cast<const float4*>(cf + i4);
+          const float f[4] = {f4.x, f4.y, f4.z, f4.w};
 #pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            const float4 cf4 = *reinterpret_cast<const float4*>(colf + buf + 32 * g + i);
-            const float cf[4] = {cf4.x, cf4.y, cf4.z, cf4.w};
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              if (g == pb && i + u == pi) a[i + u] = (c == p) ? inv : rp;
-              else a[i + u] = (c == p) ? -cf[u] * inv : a[i + u] - cf[u] * rp;
-            }
-          }
+          for (int u = 0; u < 4; ++u)
+            if (i4 + u > 0) a[i4 + u - 1] = -f[u] * inv;
         }
+        a[kGJ - 1] = inv;
+      } else {
+#pragma unroll
+        for (int i4 = 0; i4 < kGJ; i4 += 4) {
+          const float4 f4 = *reinterpret_cast<const float4*>(cf + i4);
+          const float f[4] = {f4.x, f4.y, f4.z, f4.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (i4 + u > 0) a[i4 + u - 1] = a[i4 + u] - f[u] * rp;
+        }
+        a[kGJ - 1] = rp;
       }
     }
+    // row r is in register (r - bj) mod 128
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const int r = 32 * g + i;
+    for (int i = 0; i < kGJ; ++i) {
+      const int r = (i + bj) & (kGJ - 1);
       store_x(D.Dp, D.Dp_lo, (long long)r * kGJ + c, (r < bj && c < bj) ? a[i] : 0.f, 1);
     }
   } else {
-    const long long total = (long long)bj * n;
-    const long long per = (total + kGJCopy - 1) / kGJCopy;
-    const long long beg = (blockIdx.x - 1) * per, end = min(total, beg + per);
-    for (long long e = beg + threadIdx.x; e < end; e += 512) {
-      const int r = (int)(e / n), c = (int)(e - (long long)r * n);
-      const long long src = (long long)(J0 + r) * D.ldr + c, dst = (long long)r * D.ldx + c;
-      static_cast<float*>(D.E)[dst] = static_cast<const float*>(D.R)[src];
-      static_cast<float*>(D.E_lo)[dst] = static_cast<const float*>(D.R_lo)[src];
+    // rows blockIdx.x - 1, + kGJCopy, ... of E: 16-B vectors (ld and buffers are 64-element
+    // aligned), scalar tail when n % 4 != 0
+    const int n4 = n >> 2;
+    for (int r = blockIdx.x - 1; r < bj; r += kGJCopy) {
+      const float4* sh = reinterpret_cast<const float4*>(static_cast<const float*>(D.R) + (long long)(J0 + r) * D.ldr);
+      const float4* sl = reinterpret_cast<const float4*>(static_cast<const float*>(D.R_lo) + (long long)(J0 + r) * D.ldr);
+      float4* dh = reinterpret_cast<float4*>(static_cast<float*>(D.E) + (long long)r * D.ldx);
+      float4* dl = reinterpret_cast<float4*>(static_cast<float*>(D.E_lo) + (long long)r * D.ldx);
+      for (int q = threadIdx.x; q < n4; q += kGJ) {
+        const float4 h = sh[q], l = sl[q];
+        dh[q] = h;
+        dl[q] = l;
+      }
+      for (int c = 4 * n4 + threadIdx.x; c < n; c += kGJ) {
+        static_cast<float*>(D.E)[(long long)r * D.ldx + c] = static_cast<const float*>(D.R)[(long long)(J0 + r) * D.ldr + c];
+        static_cast<float*>(D.E_lo)[(long long)r * D.ldx + c] = static_cast<const float*>(D.R_lo)[(long long)(J0 + r) * D.ldr + c];
+      }
     }
   }
 }

@@ -1185,7 +1185,7 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
         KindTimer t(h, s2, 1, timed ? 4 * P->db_steps : 0);
         const int strips = (P->max_s + kGJ - 1) / kGJ;
         for (int j = 0; j < P->db_steps; ++j) {
-          PRISM_CK(launch_k(k_gj_pivot, dim3(1 + kGJCopy, B), dim3(512), kGJSmem, s2, 1, S, j));
+          PRISM_CK(launch_k(k_gj_pivot, dim3(1 + kGJCopy, B), dim3(kGJ), kGJSmem, s2, 1, S, j));
           PRISM_CK(launch_gemm(prec, g_gjT[j], s2));
           PRISM_CK(launch_gemm(prec, g_gjS[j], s2));
           PRISM_CK(launch_k(k_gj_fix, dim3(strips, B), dim3(256), kGJSmem, s2, 1, S, j));
