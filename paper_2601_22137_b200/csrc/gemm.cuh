@@ -367,6 +367,59 @@ __device__ __forceinline__ void store_row32(void* out, void* out_lo, long long o
   }
 }
 
+// fp32 / 3xTF32 32 x 32 blocks moved with coalesced 16-B accesses (each instruction covers
+// 4 rows x 128 B) through the warp's 32 x 33 staging tile tb (conflict-free both ways),
+// instead of one row per lane (32 rows, i.e. 32 lines, per instruction).
+// Load: lane l receives row r0 + l of C (+ C_lo) as 32 floats.
+template <bool SPLIT>
+__device__ __forceinline__ void warp_load_f32_block(const void* base, const void* base_lo, long long ld, int r0,
+                                                    int c0, float (&c)[32], float* tb, int lane) {
+  const int rr = lane >> 3, c4 = (lane & 7) * 4;
+  float4 h[8], l[8];
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    const long long off = (long long)(r0 + it * 4 + rr) * ld + c0 + c4;
+    h[it] = __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(base) + off));
+    if constexpr (SPLIT) l[it] = __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(base_lo) + off));
+  }
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    float* t = tb + (it * 4 + rr) * 33 + c4;
+    if constexpr (SPLIT) {
+      t[0] = h[it].x + l[it].x; t[1] = h[it].y + l[it].y; t[2] = h[it].z + l[it].z; t[3] = h[it].w + l[it].w;
+    } else {
+      t[0] = h[it].x; t[1] = h[it].y; t[2] = h[it].z; t[3] = h[it].w;
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int u = 0; u < 32; ++u) c[u] = tb[lane * 33 + u];
+  __syncwarp();
+}
+// Store the staged tile (tb[row][col] = value at (r0 + row, c0 + col)), or its transpose
+// when TR (value at (r0 + row, c0 + col) = tb[col][row]); SPLIT: tf32 hi + fp32 remainder.
+template <bool SPLIT, bool TR>
+__device__ __forceinline__ void warp_store_f32_staged(void* out, void* out_lo, long long ld, int r0, int c0,
+                                                      const float* tb, int lane) {
+  const int rr = lane >> 3, c4 = (lane & 7) * 4;
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    const int row = it * 4 + rr;
+    float v[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) v[e] = TR ? tb[(c4 + e) * 33 + row] : tb[row * 33 + c4 + e];
+    const long long off = (long long)(r0 + row) * ld + c0 + c4;
+    if constexpr (SPLIT) {
+      const float4 hi = make_float4(tf32_trunc(v[0]), tf32_trunc(v[1]), tf32_trunc(v[2]), tf32_trunc(v[3]));
+      *reinterpret_cast<float4*>(static_cast<float*>(out) + off) = hi;
+      *reinterpret_cast<float4*>(static_cast<float*>(out_lo) + off) =
+          make_float4(v[0] - hi.x, v[1] - hi.y, v[2] - hi.z, v[3] - hi.w);
+    } else {
+      *reinterpret_cast<float4*>(static_cast<float*>(out) + off) = make_float4(v[0], v[1], v[2], v[3]);
+    }
+  }
+}
+
 // Row-block partial Gram (EPI_GRAM32): out = D in plain fp32 whatever the compute
 // dtype (the partial Grams are summed across ranks), symmetric triangle + mirror.
 __device__ __forceinline__ void epi_gram32(const EpiArgs& P, int i0, int lane, int j0, const float (&d)[32],
@@ -428,6 +481,36 @@ __device__ __forceinline__ void epi_segment(const EpiArgs& P, int mode, bool sym
   const bool full_n = j0 + 32 <= P.N;
   const bool full_blk = full_n && i0 + 32 <= P.M;   // warp-uniform
   uint8_t* stg = reinterpret_cast<uint8_t*>(tb);
+  if (Cfg::KIND != 0 && full_blk && ((P.ldo & 3) == 0)) {
+    // fp32 / 3xTF32 whole block: staged once, stored coalesced (the mirror from the same tile)
+    const bool diag = sym && j0 < i0 + 32;
+    if (mode == EPI_RESID) {
+#pragma unroll
+      for (int u = 0; u < 32; ++u) {
+        if (!sym) sumsq = fmaf(v[u], v[u], sumsq);
+        else if (!diag || u > lane) sumsq = fmaf(2.f * v[u], v[u], sumsq);
+        else if (u == lane) sumsq = fmaf(v[u], v[u], sumsq);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 32; ++u) tb[lane * 33 + u] = v[u];
+    __syncwarp();
+    if (diag) {
+      // own values on / above the diagonal, transposed ones below (exact symmetry)
+      float w[32];
+#pragma unroll
+      for (int u = 0; u < 32; ++u) w[u] = tb[u * 33 + lane];
+      __syncwarp();
+#pragma unroll
+      for (int u = 0; u < 32; ++u)
+        if (u < lane) tb[lane * 33 + u] = w[u];
+      __syncwarp();
+    }
+    warp_store_f32_staged<Cfg::SPLIT, false>(P.out, P.out_lo, P.ldo, i0, j0, tb, lane);
+    if (sym && !diag) warp_store_f32_staged<Cfg::SPLIT, true>(P.out, P.out_lo, P.ldo, j0, i0, tb, lane);
+    __syncwarp();
+    return;
+  }
   if (!sym) {
     if (Cfg::KIND == 0 && full_blk) {
       warp_store_bf16_block(P.out, P.ldo, i0, j0, v, stg, lane);
@@ -1172,7 +1255,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
 #pragma unroll
           for (int u = 0; u < 32; ++u) c[u] = 0.f;
           const int j0 = tn * Cfg::BN + (c_begin + x) * 32;
-          if (needC && i < P.M && j0 < P.N) load_row32<Cfg::KIND, Cfg::SPLIT>(P.C, P.C_lo, P.ldc, i, j0, P.N, c);
+          if (needC && i0 + 32 <= P.M && j0 + 32 <= P.N && (P.ldc & 3) == 0)
+            warp_load_f32_block<Cfg::SPLIT>(P.C, P.C_lo, P.ldc, i0, j0, c, tb, lane);   // warp-uniform
+          else if (needC && i < P.M && j0 < P.N) load_row32<Cfg::KIND, Cfg::SPLIT>(P.C, P.C_lo, P.ldc, i, j0, P.N, c);
           epi_segment<Cfg>(ea, mode, sym, i0, lane, j0, coefA, coefC, d[x], c, tb, sumsq);
         }
       }
