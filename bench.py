@@ -325,12 +325,16 @@ def main():
             return P.inv_root(inputs, out=out, matrix_ids=ids, handle=h, **opts)
         if kind == "chebyshev":
             return P.chebyshev_inverse(inputs, out=out, matrix_ids=ids, handle=h, **opts)
+        # sqrt kinds: both outputs into preallocated buffers (reused every step, as a
+        # training loop would; fresh buffers would rebuild the handle's pointer-keyed plan)
         if kind == "db_newton":
-            return P.db_newton(inputs, matrix_ids=ids, handle=h, **dbo)
-        return P.sqrt_invsqrt(inputs, matrix_ids=ids, handle=h, **opts)
+            return P.db_newton(inputs, matrix_ids=ids, handle=h, out_sqrt=outs2[0], out_invsqrt=outs2[1], **dbo)
+        return P.sqrt_invsqrt(inputs, matrix_ids=ids, handle=h, out_sqrt=outs2[0], out_invsqrt=outs2[1], **opts)
 
     dbo = {k: v for k, v in opts.items() if k != "sketch_size"}
     outs = [torch.empty_like(m) for m in mats] if kind in ("polar", "sign", "inv_root", "chebyshev") else None
+    outs2 = ([torch.empty_like(m) for m in mats], [torch.empty_like(m) for m in mats]) \
+        if kind in ("sqrt", "db_newton") else (None, None)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     clocks = ClockSampler(local)
     clocks.start()                      # sampled from the timed region to the end of the GPU passes

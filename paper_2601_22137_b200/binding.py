@@ -391,10 +391,38 @@ def sqrt_invsqrt_host(mats, degree=5, max_iters=30, sketch_size=8, tol=1e-6, see
     return sq, isq, rb
 
 
+def _outputs(mats, want, given, what):
+    """Output matrices: the caller's (same shape / dtype / device as the inputs, unit column
+    stride) or fresh ones.  Reusing the same output buffers across calls keeps the handle's
+    plan (keyed by every pointer it bakes into its tables) and its CUDA graph warm."""
+    import torch
+    if not want:
+        return None
+    if given is None:
+        return [torch.empty_like(t) for t in mats]
+    given = list(given)
+    if len(given) != len(mats):
+        raise PrismError(f"{what}: {len(given)} outputs for {len(mats)} matrices")
+    for g, t in zip(given, mats):
+        if g.shape != t.shape or g.dtype != t.dtype or g.device != t.device or g.stride(1) != 1:
+            raise PrismError(f"{what}: each output must match its input's shape, dtype and device, rows contiguous")
+    return given
+
+
+def _ld_out(sq, isq, mats, what):
+    a = sq if sq is not None else isq
+    if a is None:
+        return _i64([t.shape[1] for t in mats])
+    if sq is not None and isq is not None and any(x.stride(0) != y.stride(0) for x, y in zip(sq, isq)):
+        raise PrismError(f"{what}: the two outputs of a matrix must share one row stride")
+    return _i64([t.stride(0) for t in a])
+
+
 def sqrt_invsqrt(mats, degree=5, max_iters=30, sketch_size=8, tol=1e-6, seed=42, precision=None, fit="sketched",
                  warmup_iters=0, alpha_lo=None, alpha_hi=None, want_sqrt=True, want_invsqrt=True, matrix_ids=None,
-                 stream=None, handle=None):
-    """A^{1/2}, A^{-1/2} of a batch of SPD CUDA matrices via prism_sqrt_invsqrt."""
+                 stream=None, handle=None, out_sqrt=None, out_invsqrt=None):
+    """A^{1/2}, A^{-1/2} of a batch of SPD CUDA matrices via prism_sqrt_invsqrt (outputs into
+    out_sqrt / out_invsqrt when given)."""
     import torch
     mats = list(mats)
     if not mats:
@@ -406,9 +434,9 @@ def sqrt_invsqrt(mats, degree=5, max_iters=30, sketch_size=8, tol=1e-6, seed=42,
     o = make_options(degree, max_iters, sketch_size, tol, seed, precision, fit, warmup_iters, alpha_lo, alpha_hi)
     B = len(mats)
     n = _i64([t.shape[0] for t in mats])
-    sq = [torch.empty_like(t) for t in mats] if want_sqrt else None
-    isq = [torch.empty_like(t) for t in mats] if want_invsqrt else None
-    ld_out = _i64([t.shape[1] for t in mats])
+    sq = _outputs(mats, want_sqrt, out_sqrt, "sqrt_invsqrt")
+    isq = _outputs(mats, want_invsqrt, out_invsqrt, "sqrt_invsqrt")
+    ld_out = _ld_out(sq, isq, mats, "sqrt_invsqrt")
     need = lib().prism_sqrt_workspace(h.h, B, n, ctypes.byref(o))
     if need == 0:
         raise PrismError("prism_sqrt_workspace rejected the arguments: " + lib().prism_last_error().decode())
@@ -627,9 +655,10 @@ def chebyshev_inverse_host(mats, max_iters=40, sketch_size=8, tol=1e-6, seed=42,
 
 
 def db_newton(mats, max_iters=30, tol=1e-6, precision="fp32", fit="sketched", warmup_iters=0, want_sqrt=True,
-              want_invsqrt=True, matrix_ids=None, stream=None, handle=None):
+              want_invsqrt=True, matrix_ids=None, stream=None, handle=None, out_sqrt=None, out_invsqrt=None):
     """A^{1/2}, A^{-1/2} of a batch of SPD CUDA fp32 matrices via prism_db_newton (PRISM DB
-    Newton, product form; the fit is exact and unsketched)."""
+    Newton, product form; the fit is exact and unsketched; outputs into out_sqrt /
+    out_invsqrt when given)."""
     import torch
     mats = list(mats)
     if not mats:
@@ -640,9 +669,9 @@ def db_newton(mats, max_iters=30, tol=1e-6, precision="fp32", fit="sketched", wa
     o = make_options(5, max_iters, 8, tol, 42, precision, fit, warmup_iters)
     B = len(mats)
     n = _i64([t.shape[0] for t in mats])
-    sq = [torch.empty_like(t) for t in mats] if want_sqrt else None
-    isq = [torch.empty_like(t) for t in mats] if want_invsqrt else None
-    ld_out = _i64([t.shape[1] for t in mats])
+    sq = _outputs(mats, want_sqrt, out_sqrt, "db_newton")
+    isq = _outputs(mats, want_invsqrt, out_invsqrt, "db_newton")
+    ld_out = _ld_out(sq, isq, mats, "db_newton")
     need = lib().prism_db_newton_workspace(h.h, B, n, ctypes.byref(o))
     if need == 0:
         raise PrismError("prism_db_newton_workspace rejected the arguments: " + lib().prism_last_error().decode())

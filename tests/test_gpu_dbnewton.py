@@ -91,3 +91,19 @@ def test_db_newton_zero_input_and_precision():
     assert int(rep["status"][0]) == prism.ZERO_INPUT
     with pytest.raises(P.PrismError):
         P.db_newton([torch.eye(64, device="cuda").to(torch.bfloat16)], precision="bf16")
+
+
+def test_db_newton_caller_outputs_equal_fresh_outputs():
+    sizes = [100, 260]
+    mats = [torch.tensor(W.spd_logspaced(s, 1e2, seed=800 + s)).float().cuda() for s in sizes]
+    X, Y, _ = P.db_newton(mats, tol=1e-5, max_iters=40)
+    osq = [torch.full_like(m, float("nan")) for m in mats]
+    oisq = [torch.full_like(m, float("nan")) for m in mats]
+    for _ in range(2):   # the same buffers twice: the handle's plan is reused
+        X2, Y2, _ = P.db_newton(mats, tol=1e-5, max_iters=40, out_sqrt=osq, out_invsqrt=oisq)
+    torch.cuda.synchronize()
+    assert X2[0] is osq[0] and Y2[1] is oisq[1]
+    for a, b in zip(X + Y, X2 + Y2):
+        assert torch.equal(a, b)
+    with pytest.raises(P.PrismError):
+        P.db_newton(mats, out_sqrt=osq[:1])

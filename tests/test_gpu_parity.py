@@ -268,3 +268,17 @@ def test_rowblock_two_ranks_emulated_equals_single_solve():
     assert abs(int(res[0][1]["iters"][0]) - ro.iters) <= 1
     assert _rel(Q, Qo) <= 1e-5
     assert _rel(Q, Qs[0].double().cpu().numpy()) <= 1e-5
+
+
+@pytest.mark.gpu
+def test_sqrt_caller_outputs_equal_fresh_outputs():
+    mats = [torch.tensor(W.spd_logspaced(s, 1e2, seed=900 + s)).float().cuda() for s in (96, 300)]
+    X, Y, _ = P.sqrt_invsqrt(mats, degree=5, tol=1e-5, max_iters=30, precision="fp32")
+    osq = [torch.full_like(m, float("nan")) for m in mats]
+    oisq = [torch.full_like(m, float("nan")) for m in mats]
+    X2, Y2, _ = P.sqrt_invsqrt(mats, degree=5, tol=1e-5, max_iters=30, precision="fp32", out_sqrt=osq,
+                               out_invsqrt=oisq)
+    torch.cuda.synchronize()
+    assert X2[1] is osq[1] and Y2[0] is oisq[0]
+    for a, b in zip(X + Y, X2 + Y2):
+        assert torch.equal(a, b)
