@@ -73,6 +73,48 @@ __global__ void __launch_bounds__(64, 1) tma_stream(const __grid_constant__ CUte
   if (mc > 1) cluster_sync_all();
 }
 
+// 3-D boxes {64, box_rows, kd}: one operation loads kd consecutive 64-column K blocks
+// (each a 128-B-swizzled box_rows x 128 B tile, back to back in shared memory).
+__global__ void __launch_bounds__(64, 1) tma_stream3(const __grid_constant__ CUtensorMap map, int box_rows, int kd,
+                                                     int ops, int total_rows, int STAGES, int kcols) {
+  extern __shared__ uint8_t raw[];
+  uint8_t* smem = raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);
+  const int stage_bytes = box_rows * 128 * kd;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * stage_bytes);
+  uint64_t* empty = full + STAGES;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int row0 = (blockIdx.x * box_rows) % total_rows;
+  if (threadIdx.x == 0) {
+    int stage = 0;
+    uint32_t ph = 0;
+    for (int op = 0; op < ops; ++op) {
+      mbar_wait(&empty[stage], ph ^ 1);
+      mbar_arrive_expect_tx(&full[stage], stage_bytes);
+      const int kb = (op * kd) % (kcols / 64);
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
+          ::"r"(smem_u32(smem + stage * stage_bytes)), "l"(&map), "r"(smem_u32(&full[stage])), "r"(0), "r"(row0),
+          "r"(kb) : "memory");
+      if (++stage == STAGES) { stage = 0; ph ^= 1; }
+    }
+  } else if (threadIdx.x == 32) {
+    int stage = 0;
+    uint32_t ph = 0;
+    for (int op = 0; op < ops; ++op) {
+      mbar_wait(&full[stage], ph);
+      mbar_arrive(&empty[stage]);
+      if (++stage == STAGES) { stage = 0; ph ^= 1; }
+    }
+  }
+}
+
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
                              const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -146,6 +188,42 @@ int main() {
     const double ingest = (double)kblocks * c.box * 128 / (us * 1e-6) / 1e9;
     printf("%4d %2d %4d %3d %5d%s | %8.1f  %7.1f  %6.2f  %6.2f\n", c.box, c.mc, c.grid, c.stages, kcols,
            same ? "(same)" : "", us, ingest, ingest * c.grid / 1e3, ingest * c.grid / c.mc / 1e3);
+  }
+  // 3-D: kd K blocks per operation, same bytes per stage budget
+  cudaFuncSetAttribute(tma_stream3, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  printf("3-D boxes: box_rows kd grid stages | us  per-SM-ingest GB/s  ns per op\n");
+  struct C3 { int box, kd, grid, stages; };
+  for (const C3& c : {C3{128, 1, 148, 6}, C3{128, 2, 148, 3}, C3{128, 2, 148, 6}, C3{128, 4, 148, 3},
+                      C3{256, 1, 148, 6}, C3{256, 2, 148, 3}, C3{32, 1, 148, 6}, C3{32, 4, 148, 6}, C3{32, 8, 148, 4}}) {
+    CUtensorMap map;
+    cuuint64_t dims[3] = {64, (cuuint64_t)ROWS, (cuuint64_t)(COLS / 64)};
+    cuuint64_t strides[2] = {(cuuint64_t)COLS * 2, 128};
+    cuuint32_t box[3] = {64, (cuuint32_t)c.box, (cuuint32_t)c.kd};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, buf, dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) { printf("3d encode failed %d (box %d kd %d)\n", (int)r, c.box, c.kd); continue; }
+    const int ops = 4096 / c.kd;
+    const int smem = c.stages * c.box * 128 * c.kd + 2048;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e30f;
+    for (int rep = 0; rep < 4; ++rep) {
+      cudaEventRecord(e0);
+      tma_stream3<<<c.grid, 64, smem>>>(map, c.box, c.kd, ops, ROWS, c.stages, 1024);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (rep > 0 && ms < best) best = ms;
+    }
+    cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) { printf("3d %d %d: %s\n", c.box, c.kd, cudaGetErrorString(err)); return 1; }
+    const double us = best * 1e3;
+    const double ingest = (double)ops * c.kd * c.box * 128 / (us * 1e-6) / 1e9;
+    printf("%4d %2d %4d %3d | %8.1f  %7.1f  %6.1f\n", c.box, c.kd, c.grid, c.stages, us, ingest, us * 1e3 / ops);
   }
   return 0;
 }
