@@ -493,12 +493,41 @@ __global__ void __launch_bounds__(kGJ) k_gj_pivot(SolveParams P, int j) {
   if (J0 >= n) return;
   const int bj = min(kGJ, n - J0);
   if (blockIdx.x == 0) {
+    unsigned long long* gtr = (g_chain_trace && b == P.batch - 1 && threadIdx.x == 0 && j < 64)
+                                  ? g_chain_trace + 16 * 1024 * 16 - 4096 + 4 * j : nullptr;
+    if (gtr) gtr[0] = globaltimer_ns();
     float* colf = gsm;   // [2][kGJ]
+    float(*tile)[kGJ + 1] = reinterpret_cast<float(*)[kGJ + 1]>(gsm + 2 * kGJ);
     const int c = threadIdx.x;
+    // the block through shared memory: coalesced 16-B loads (hi + lo), all in flight
+    {
+      const float* Rh = static_cast<const float*>(D.R);
+      const float* Rl = static_cast<const float*>(D.R_lo);
+#pragma unroll 8
+      for (int q = c; q < kGJ * (kGJ / 4); q += kGJ) {
+        const int r = q >> 5, c4 = (q & 31) * 4;
+        float v[4];
+        if (r < bj && c4 + 3 < bj) {
+          const long long off = (long long)(J0 + r) * D.ldr + J0 + c4;
+          const float4 h = __ldg(reinterpret_cast<const float4*>(Rh + off));
+          const float4 l = __ldg(reinterpret_cast<const float4*>(Rl + off));
+          v[0] = h.x + l.x; v[1] = h.y + l.y; v[2] = h.z + l.z; v[3] = h.w + l.w;
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int cc = c4 + e;
+            v[e] = (r < bj && cc < bj) ? ld_split(D.R, D.R_lo, (long long)(J0 + r) * D.ldr + J0 + cc) : (r == cc ? 1.f : 0.f);
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) tile[r][c4 + e] = v[e];
+      }
+    }
+    __syncthreads();
     float a[kGJ];
 #pragma unroll
-    for (int r = 0; r < kGJ; ++r)
-      a[r] = (r < bj && c < bj) ? ld_split(D.R, D.R_lo, (long long)(J0 + r) * D.ldr + J0 + c) : (r == c ? 1.f : 0.f);
+    for (int r = 0; r < kGJ; ++r) a[r] = tile[r][c];
+
 #pragma unroll 1
     for (int p = 0; p < bj; ++p) {
       float* cf = colf + (p & 1) * kGJ;
@@ -507,38 +536,34 @@ __global__ void __launch_bounds__(kGJ) k_gj_pivot(SolveParams P, int j) {
         for (int i = 0; i < kGJ; i += 4) *reinterpret_cast<float4*>(cf + i) = make_float4(a[i], a[i + 1], a[i + 2], a[i + 3]);
       }
       __syncthreads();
+      if (gtr && p == 0) gtr[1] = globaltimer_ns();
       const float inv = 1.f / cf[0];
-      const float rp = a[0] * inv;
-      // rows 1..127 -> registers 0..126 (the textbook sweep's arithmetic); only the warp
-      // holding column p takes both paths
-      if (c == p) {
+      // new row r-1 = a[r] - colf[r] * (a[p] / pivot); the pivot column's owner (its old
+      // registers already broadcast) zeroes them, so one FMA gives -colf[r] / pivot there
+      const bool own = c == p;
+      const float rr = own ? inv : a[0] * inv;
+      if (own) {
 #pragma unroll
-        for (int i4 = 0; i4 < kGJ; i4 += 4) {
-          const float4 f4 = *reinterpret_cast<const float4*>(cf + i4);
-          const float f[4] = {f4.x, f4.y, f4.z, f4.w};
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (i4 + u > 0) a[i4 + u - 1] = -f[u] * inv;
-        }
-        a[kGJ - 1] = inv;
-      } else {
-#pragma unroll
-        for (int i4 = 0; i4 < kGJ; i4 += 4) {
-          const float4 f4 = *reinterpret_cast<const float4*>(cf + i4);
-          const float f[4] = {f4.x, f4.y, f4.z, f4.w};
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (i4 + u > 0) a[i4 + u - 1] = a[i4 + u] - f[u] * rp;
-        }
-        a[kGJ - 1] = rp;
+        for (int i = 1; i < kGJ; ++i) a[i] = 0.f;
       }
+#pragma unroll
+      for (int i4 = 0; i4 < kGJ; i4 += 4) {
+        const float4 f4 = *reinterpret_cast<const float4*>(cf + i4);
+        const float f[4] = {f4.x, f4.y, f4.z, f4.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (i4 + u > 0) a[i4 + u - 1] = fmaf(-f[u], rr, a[i4 + u]);
+      }
+      a[kGJ - 1] = rr;   // the new pivot row: a[p] / pivot, and 1 / pivot on the diagonal
     }
+    if (gtr) gtr[2] = globaltimer_ns();
     // row r is in register (r - bj) mod 128
 #pragma unroll
     for (int i = 0; i < kGJ; ++i) {
       const int r = (i + bj) & (kGJ - 1);
       store_x(D.Dp, D.Dp_lo, (long long)r * kGJ + c, (r < bj && c < bj) ? a[i] : 0.f, 1);
     }
+    if (gtr) gtr[3] = globaltimer_ns();
   } else {
     // rows blockIdx.x - 1, + kGJCopy, ... of E: 16-B vectors (ld and buffers are 64-element
     // aligned), scalar tail when n % 4 != 0
