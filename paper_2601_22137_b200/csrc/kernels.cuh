@@ -610,6 +610,47 @@ __global__ void __launch_bounds__(256) k_gj_fix(SolveParams P, int j) {
     return;
   }
   float(*t)[kGJ + 1] = reinterpret_cast<float(*)[kGJ + 1]>(gsm);
+  if (bj == kGJ && w == kGJ) {
+    // whole 128 x 128 tile: 16-B loads / stores (hi + lo planes), transpose through smem
+    const float* Th = static_cast<const float*>(D.T);
+    const float* Tl = static_cast<const float*>(D.T_lo);
+    float* Rh = static_cast<float*>(D.R);
+    float* Rl = static_cast<float*>(D.R_lo);
+#pragma unroll 4
+    for (int q = threadIdx.x; q < kGJ * kGJ / 4; q += 256) {
+      const int r = q >> 5, c4 = (q & 31) * 4;
+      const long long src = (long long)r * D.ldx + c0 + c4;
+      const float4 h = __ldg(reinterpret_cast<const float4*>(Th + src));
+      const float4 l = __ldg(reinterpret_cast<const float4*>(Tl + src));
+      const float v[4] = {h.x + l.x, h.y + l.y, h.z + l.z, h.w + l.w};
+      float hv[4], lv[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        t[r][c4 + e] = v[e];
+        hv[e] = __uint_as_float(__float_as_uint(v[e]) & 0xFFFFE000u);
+        lv[e] = v[e] - hv[e];
+      }
+      const long long dst = (long long)(J0 + r) * D.ldr + c0 + c4;   // row block
+      *reinterpret_cast<float4*>(Rh + dst) = make_float4(hv[0], hv[1], hv[2], hv[3]);
+      *reinterpret_cast<float4*>(Rl + dst) = make_float4(lv[0], lv[1], lv[2], lv[3]);
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int q = threadIdx.x; q < kGJ * kGJ / 4; q += 256) {
+      const int c = q >> 5, r4 = (q & 31) * 4;
+      float hv[4], lv[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float v = t[r4 + e][c];
+        hv[e] = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+        lv[e] = v - hv[e];
+      }
+      const long long dst = (long long)(c0 + c) * D.ldr + J0 + r4;   // column block
+      *reinterpret_cast<float4*>(Rh + dst) = make_float4(hv[0], hv[1], hv[2], hv[3]);
+      *reinterpret_cast<float4*>(Rl + dst) = make_float4(lv[0], lv[1], lv[2], lv[3]);
+    }
+    return;
+  }
   for (int e = threadIdx.x; e < bj * w; e += 256) {
     const int r = e / w, c = e % w;
     const float v = ld_split(D.T, D.T_lo, (long long)r * D.ldx + c0 + c);
