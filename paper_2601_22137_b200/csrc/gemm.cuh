@@ -95,6 +95,9 @@ struct GemmProblem {
   int pad2_;
 };
 
+// ints from MatState::done to MatState::stop_iter (static_assert in kernels.cuh)
+constexpr int kStopIterOffset = 4;
+
 struct GemmLaunch {
   const GemmProblem* probs;      // problem table (even iterations)
   const GemmProblem* probs_odd;  // problem table for odd iterations (ping-pong buffers) or null
@@ -105,6 +108,11 @@ struct GemmLaunch {
   int ntiles;
   int iter_lo, iter_hi;
   int ksplit;                    // chain split-K: cluster size (the CTAs of one row tile), else 1
+  // operands final before the predecessor completes (the square GEMM after k_alpha): the
+  // producer and MMA warps run the mainloop without waiting; only the epilogue waits (for
+  // alpha).  Tiles are then skipped by stop_iter < k (final for earlier iterations; a
+  // matrix stopping at k, decided concurrently, is computed by every role alike)
+  int early;
 };
 
 // The problem fields the tile epilogue needs, held in registers for the tile: read
@@ -1001,16 +1009,29 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
     }
   }
   // wait, then let dependents launch: a launch's predecessor-of-predecessor is then always
-  // complete, which the chain kernel relies on for reads before its own wait (chaint.cuh)
-  griddep_wait();
-  griddep_launch();
+  // complete, which the chain kernel relies on for reads before its own wait (chaint.cuh).
+  // An early launch's producer / MMA warps neither wait nor trigger (its epilogue does both).
+  const bool early_role = L.early && warp < 4;
+  if (!early_role) {
+    griddep_wait();
+    griddep_launch();
+  }
   // device-side loop control (CUDA-graph WHILE body): uniform skip / parity select
   bool run = true;
+  int kcur = 0;
   if (L.iter) {
     const int k = *L.iter;
+    kcur = k;
     run = k >= L.iter_lo && k < L.iter_hi;
     if (L.probs_odd && (k & 1)) probs = L.probs_odd;
   }
+  // tiles of stopped matrices are skipped (the same decision in every role)
+  auto skip_tile = [&](int matrix) -> bool {
+    if (!L.done) return false;
+    const int* st = L.done + (size_t)matrix * L.done_stride;
+    if (L.early) return *reinterpret_cast<const volatile int*>(st + kStopIterOffset) < kcur;
+    return st[0] != 0;
+  };
 
   if (warp < 4) {
     setmaxnreg_dec<Cfg::REG_LO>();
@@ -1024,7 +1045,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
       for (int t = cid; t < L.ntiles; t += ncl) {
         const uint32_t code = L.tiles[t];
         const GemmProblem& P = probs[code >> 20];
-        if (L.done && L.done[P.matrix * L.done_stride]) continue;
+        if (skip_tile(P.matrix)) continue;
         const int tm = (code >> 10) & 1023;
         const int tn = code & 1023;
         const int kb_lo = 0, kb_hi = (P.K + Cfg::BK - 1) / Cfg::BK;
@@ -1068,7 +1089,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
       for (int t = cid; t < L.ntiles; t += ncl) {
         const uint32_t code = L.tiles[t];
         const GemmProblem& P = probs[code >> 20];
-        if (L.done && L.done[P.matrix * L.done_stride]) continue;
+        if (skip_tile(P.matrix)) continue;
         const int tn = code & 1023;
         const int kb_lo = 0, kb_hi = (P.K + Cfg::BK - 1) / Cfg::BK;
         // tf32: one TMEM accumulation chunk per PROMO_KB k-blocks, promoted to fp32
@@ -1138,7 +1159,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
     for (int t = cid; t < L.ntiles; t += ncl) {
       const uint32_t code = L.tiles[t];
       const GemmProblem& P = probs[code >> 20];
-      if (L.done && L.done[P.matrix * L.done_stride]) continue;
+      if (skip_tile(P.matrix)) continue;
       const int tm = (code >> 10) & 1023;
       const int tn = code & 1023;
       const int mode = P.mode;

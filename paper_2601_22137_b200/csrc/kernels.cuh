@@ -19,8 +19,12 @@ struct MatState {
   int iters;         // updates applied
   int status;        // PRISM_CONVERGED ...
   int incr;          // consecutive residual increases
-  int pad_;
+  int stop_iter;     // iteration k at which the matrix stopped (INT_MAX while active; -1: zero
+                     // input); GEMMs that start before k_alpha completes skip on stop_iter < k
 };
+
+static_assert(offsetof(MatState, stop_iter) - offsetof(MatState, done) == kStopIterOffset * sizeof(int),
+              "GEMM tile skipping reads stop_iter at a fixed offset from done");
 
 // Per-matrix static description (device memory).
 struct MatDesc {
@@ -395,6 +399,7 @@ __global__ void __launch_bounds__(256) k_normalize(SolveParams P) {
     S.iters = 0;
     S.incr = 0;
     S.done = (c == 0.0) ? 1 : 0;
+    S.stop_iter = (c == 0.0) ? -1 : 0x7fffffff;
     S.status = (c == 0.0) ? 4 : 1;   // ZERO_INPUT / MAX_ITERS until decided
   }
 }
@@ -1022,6 +1027,11 @@ __global__ void __launch_bounds__(256) k_alpha(SolveParams P) {
   MatState& S = P.st[b];
   if (S.done) return;
   const int s = D.s;
+  // diagnostics (scripts/trace_alpha.py): block 0's timeline of iteration k in the chain
+  // trace buffer's tail
+  unsigned long long* atr = (g_chain_trace && b == 0 && threadIdx.x == 0 && *P.iter < 32)
+                                ? g_chain_trace + 16 * 1024 * 16 - 8192 + 4 * *P.iter : nullptr;
+  if (atr) atr[0] = globaltimer_ns();
   // ||R_k||_F^2 from the Gram per-tile partials (fixed order, scheduled tiles only)
   double part = 0.0;
   const int ntile = D.tiles_m * D.tiles_n;
@@ -1046,6 +1056,7 @@ __global__ void __launch_bounds__(256) k_alpha(SolveParams P) {
     S.r_prev = r;
     S.resid = (float)(r / sqrt((double)s));
     if (stop) {
+      S.stop_iter = k;
       S.done = 1;
       S.status = status;
       S.iters = k;
@@ -1055,6 +1066,7 @@ __global__ void __launch_bounds__(256) k_alpha(SolveParams P) {
     s_stop = stop;
   }
   __syncthreads();
+  if (atr) atr[1] = globaltimer_ns();
   if (s_stop) return;
   if (threadIdx.x >= 32) return;   // warp 0 fits alpha
   double a;
@@ -1115,9 +1127,11 @@ __global__ void __launch_bounds__(256) k_alpha(SolveParams P) {
       else a = argmin_poly_warp(c, 2 * q, P.alo, P.ahi, P.ataylor);
     } else {
       double c[5] = {g[0], 2.0 * g[1], g[3] + 2.0 * g[2], 2.0 * g[4], g[5]};
+      if (atr) atr[2] = globaltimer_ns();
       a = (k < P.warmup) ? P.ahi : argmin_quartic(c, P.alo, P.ahi, P.ataylor);
     }
   }
+  if (atr) atr[3] = globaltimer_ns();
   if (threadIdx.x == 0) {
     S.alpha = a;
     P.alpha_hist[(size_t)b * P.max_iters + k] = a;

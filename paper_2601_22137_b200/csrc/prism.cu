@@ -1154,7 +1154,18 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
   const int M = r.o.max_iters;
   const GemmLaunch g_gram = make_launch(*P, P->gram[0], &P->gram[1], r.ws, 0, M + 1);
   const GemmLaunch g_apply = make_launch(*P, P->apply[0], &P->apply[1], r.ws, 0, M);
-  const GemmLaunch g_sq = make_launch(*P, P->square, nullptr, r.ws, 0, M);
+  GemmLaunch g_sq = make_launch(*P, P->square, nullptr, r.ws, 0, M);
+  // the square GEMM reads R (written by the residual step, several launches back): its
+  // mainloop can run while k_alpha finishes, only its epilogue waiting for alpha.
+  static const bool early_sq = [] { const char* e = getenv("PRISM_EARLY_SQUARE"); return !(e && e[0] == '0'); }();
+  // Used where it was measured to pay (scripts/ab_early.sh, alternating runs on one box):
+  // bf16 polar with few matrices — k_alpha then holds few SMs and the square GEMM fills
+  // the rest (4096^2: 3.69 -> 3.54 ms per step).  Not for 3xTF32 (its epilogue consumes
+  // the accumulator in K chunks during the mainloop, so a waiting epilogue stalls the
+  // MMAs: shampoo 4 % slower), large batches (k_alpha holds B SMs: GPT-2 unchanged, 1B
+  // batch 1 % slower) or the general square products of sign / Chebyshev (1-2 % slower).
+  const bool polar_kind = !r.sqrt_kind && !r.sign_kind && !r.cheb_kind && !r.inv_q && !r.db_kind;
+  if (early_sq && polar_kind && prec == PRISM_BF16 && B <= 16) g_sq.early = 1;
   const GemmLaunch g_sq2 = make_launch(*P, P->square2, nullptr, r.ws, 0, M);
   std::vector<GemmLaunch> g_gjT, g_gjS;
   for (int j = 0; j < P->db_steps; ++j) {
