@@ -1015,9 +1015,15 @@ __device__ double argmin_quartic_free(const double c[5], double a_default) {
 
 // One block (256 threads) per matrix: residual norm, stop test (R12), and
 // alpha_k from the factored sketched loss m(a) = ||V0 + a V1 + a^2 V2||^2.
-__global__ void __launch_bounds__(256) k_alpha(SolveParams P) {
-  griddep_wait();
-  griddep_launch();
+// pre_wait = 1: the residual's norm partials were written at least two launches back (a
+// sketch chain or the DB sweep runs in between), so the stop test is computed before
+// waiting for the predecessor (its state writes still follow the wait: the predecessor
+// reads the done flags); only the fit's inputs come from the predecessor.
+__global__ void __launch_bounds__(256) k_alpha(SolveParams P, int pre_wait) {
+  if (!pre_wait) {
+    griddep_wait();
+    griddep_launch();
+  }
   __shared__ double scratch[8];
   __shared__ int s_stop;
   const int k = *P.iter;
@@ -1025,7 +1031,10 @@ __global__ void __launch_bounds__(256) k_alpha(SolveParams P) {
   const int b = blockIdx.x;
   const MatDesc& D = P.mats[b];
   MatState& S = P.st[b];
-  if (S.done) return;
+  if (S.done) {
+    if (pre_wait) griddep_wait();   // (exit triggers the dependents)
+    return;
+  }
   const int s = D.s;
   // diagnostics (scripts/trace_alpha.py): block 0's timeline of iteration k in the chain
   // trace buffer's tail
@@ -1043,16 +1052,24 @@ __global__ void __launch_bounds__(256) k_alpha(SolveParams P) {
   }
   const double r2 = block_sum<double, 256>(part, scratch);
   const double r = sqrt(r2);
+  // stop test (R12) on state final since the previous iteration
+  int stop = 0, status = 1, incr = 0;
   if (threadIdx.x == 0) {
-    P.resid_hist[(size_t)b * (P.max_iters + 1) + k] = (float)(r / sqrt((double)s));
-    int stop = 0, status = 1;
     if (!isfinite(r)) { stop = 1; status = 3; }
     else if (r <= P.tol * sqrt((double)s)) { stop = 1; status = 0; }
     else {
-      S.incr = (k >= 1 && r > S.r_prev) ? S.incr + 1 : 0;
-      if (S.incr >= 5) { stop = 1; status = 2; }
+      incr = (k >= 1 && r > S.r_prev) ? S.incr + 1 : 0;
+      if (incr >= 5) { stop = 1; status = 2; }
       else if (k >= P.max_iters) { stop = 1; status = 1; }
     }
+  }
+  if (pre_wait) {
+    griddep_wait();
+    griddep_launch();
+  }
+  if (threadIdx.x == 0) {
+    P.resid_hist[(size_t)b * (P.max_iters + 1) + k] = (float)(r / sqrt((double)s));
+    if (isfinite(r) && !(r <= P.tol * sqrt((double)s))) S.incr = incr;
     S.r_prev = r;
     S.resid = (float)(r / sqrt((double)s));
     if (stop) {
@@ -1101,8 +1118,11 @@ __global__ void __launch_bounds__(256) k_alpha(SolveParams P) {
     double g[kChainG];
 #pragma unroll
     for (int j = 0; j < kChainG; ++j) g[j] = 0.0;
-    for (int t = threadIdx.x; t < D.chain_tiles; t += 32) {
-      const double* cp = D.chain_part + kChainG * t;
+    const double* __restrict__ cpart = D.chain_part;
+    const int ctiles = D.chain_tiles;
+#pragma unroll 4
+    for (int t = threadIdx.x; t < ctiles; t += 32) {   // four groups' loads in flight per lane
+      const double* cp = cpart + kChainG * t;
 #pragma unroll
       for (int j = 0; j < kChainG; ++j)
         if (j < ng) g[j] += cp[j];

@@ -1208,7 +1208,7 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
       }
       {
         KindTimer t(h, s2, 4, timed ? 1 : 0);
-        PRISM_CK(launch_k(k_alpha, dim3(B), dim3(256), 0, s2, 1, S));
+        PRISM_CK(launch_k(k_alpha, dim3(B), dim3(256), 0, s2, 1, S, 1));   // norm partials: k_db_begin
       }
       {
         KindTimer t(h, s2, 2, timed ? 2 : 0);
@@ -1236,8 +1236,10 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
       for (int j = 0; j < P->n_chain; ++j) PRISM_CK(launch_chaint(prec, chain_pass(*P, j), g_chaint[j], s2));
     }
     {
+      // norm partials from the residual step; a sketch chain in between makes them final
+      // before k_alpha's wait
       KindTimer t(h, s2, 4, timed ? 1 : 0);
-      PRISM_CK(launch_k(k_alpha, dim3(B), dim3(256), 0, s2, 1, S));
+      PRISM_CK(launch_k(k_alpha, dim3(B), dim3(256), 0, s2, 1, S, (sketched && P->n_chain > 0) ? 1 : 0));
     }
     if (P->has_square) {
       KindTimer t(h, s2, 1, timed ? (P->has_square2 ? 2 : 1) : 0);
@@ -1873,7 +1875,7 @@ prism_status prism_rowblock_update(prism_handle h, int k, const float* G, int32_
                              st));
     }
   }
-  PRISM_CK(launch_k(k_alpha, dim3(1), dim3(256), 0, st, 1, S));
+  PRISM_CK(launch_k(k_alpha, dim3(1), dim3(256), 0, st, 1, S, 0));
   if (P->has_square) PRISM_CK(launch_gemm(prec, make_launch(*P, P->square, nullptr, g_rb.ws, 0, M), st));
   PRISM_CK(launch_gemm(prec, make_launch(*P, P->apply[0], &P->apply[1], g_rb.ws, 0, M), st));
   PRISM_CK(launch_k(k_advance, dim3(1), dim3(256), 0, st, 1, S, 0, 0, all_done ? reinterpret_cast<int*>(all_done) : P->d_all_done));
