@@ -1039,7 +1039,7 @@ __global__ void __launch_bounds__(256) k_alpha(SolveParams P, int pre_wait) {
   // diagnostics (scripts/trace_alpha.py): block 0's timeline of iteration k in the chain
   // trace buffer's tail
   unsigned long long* atr = (g_chain_trace && b == 0 && threadIdx.x == 0 && *P.iter < 32)
-                                ? g_chain_trace + 16 * 1024 * 16 - 8192 + 4 * *P.iter : nullptr;
+                                ? g_chain_trace + 16 * 1024 * 16 - 8192 + 8 * *P.iter : nullptr;
   if (atr) atr[0] = globaltimer_ns();
   // ||R_k||_F^2 from the Gram per-tile partials (fixed order, scheduled tiles only)
   double part = 0.0;
@@ -1101,9 +1101,11 @@ __global__ void __launch_bounds__(256) k_alpha(SolveParams P, int pre_wait) {
 #pragma unroll
         for (int j = 0; j < 3; ++j) s3[j] += D.dbpart[3 * t + j];
 #pragma unroll
-      for (int j = 0; j < 3; ++j)
+      for (int j = 0; j < 3; ++j) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) s3[j] += __shfl_xor_sync(0xffffffffu, s3[j], o);
+        s3[j] = __shfl_sync(0xffffffffu, s3[j], 0);   // lane 0's sums everywhere (no divergence)
+      }
       const double A1 = s3[0], B1 = s3[1], C1 = s3[2];
       const double c[5] = {C1, -4.0 * C1, 2.0 * B1 + 6.0 * C1, -4.0 * B1 - 4.0 * C1, A1 + 2.0 * B1 + C1};
       a = argmin_quartic_free(c, P.ataylor);
@@ -1127,10 +1129,24 @@ __global__ void __launch_bounds__(256) k_alpha(SolveParams P, int pre_wait) {
       for (int j = 0; j < kChainG; ++j)
         if (j < ng) g[j] += cp[j];
     }
+    if (atr) {   // diagnostics: loads landed (value-dependent store orders the timer after them)
+      if (g[0] == 1.2345e300) atr[7] = 1;
+      atr[4] = globaltimer_ns();
+    }
+    if (atr) atr[6] = globaltimer_ns();
 #pragma unroll
     for (int j = 0; j < kChainG; ++j) {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) g[j] += __shfl_xor_sync(0xffffffffu, g[j], o);
+    }
+    // every lane takes lane 0's sums: the xor tree adds in a lane-dependent order, and
+    // lanes whose last bits differed took different branches of the argmin (a divergent
+    // warp ran it ~8x slower); lane 0's values are the ones whose alpha is stored
+#pragma unroll
+    for (int j = 0; j < kChainG; ++j) g[j] = __shfl_sync(0xffffffffu, g[j], 0);
+    if (atr) {
+      if (g[5] == 1.2345e300) atr[7] = 2;
+      atr[5] = globaltimer_ns();
     }
     if (P.kind_cheb) {
       // Chebyshev: m(a) = ||U - a V||^2 (R26), closed form on [1/2, 2]
@@ -1147,6 +1163,9 @@ __global__ void __launch_bounds__(256) k_alpha(SolveParams P, int pre_wait) {
       else a = argmin_poly_warp(c, 2 * q, P.alo, P.ahi, P.ataylor);
     } else {
       double c[5] = {g[0], 2.0 * g[1], g[3] + 2.0 * g[2], 2.0 * g[4], g[5]};
+      if (atr)
+        for (int j = 0; j < 5; ++j)
+          atr[-8192 + j] = (unsigned long long)__double_as_longlong(c[j]);   // diagnostics: the quartic
       if (atr) atr[2] = globaltimer_ns();
       a = (k < P.warmup) ? P.ahi : argmin_quartic(c, P.alo, P.ahi, P.ataylor);
     }

@@ -9,13 +9,13 @@
 
 using namespace prism;
 
-__global__ void probe(double* out, long long* cyc, double x0, int n) {
-  double c[5] = {0.0, -1.3, 2.1, -0.7, 0.4};
+__global__ void probe(double* out, long long* cyc, double x0, int n, double c1, double c2, double c3, double c4) {
+  double c[5] = {0.0, c1, c2, c3, c4};
   double acc = x0;
   long long t0, t1;
   // 0: full argmin
   t0 = clock64();
-  for (int i = 0; i < n; ++i) { c[1] = -1.3 + acc * 1e-300; acc += argmin_quartic(c, 0.375, 1.45, 0.375); }
+  for (int i = 0; i < n; ++i) { c[1] = c1 + acc * 1e-300; acc += argmin_quartic(c, 0.375, 1.45, 0.375); }
   t1 = clock64(); cyc[0] = (t1 - t0) / n;
   // 1: real_roots_cubic only
   double roots[3];
@@ -46,7 +46,7 @@ __global__ void probe(double* out, long long* cyc, double x0, int n) {
   t0 = clock64();
   for (int i = 0; i < n; ++i) acc = sqrt(acc + 2.0);
   t1 = clock64(); cyc[7] = (t1 - t0) / n;
-  out[0] = acc;
+  if (threadIdx.x == 0) out[0] = acc;
 }
 
 int main() {
@@ -54,13 +54,18 @@ int main() {
   long long* c;
   cudaMalloc(&d, 8);
   cudaMalloc(&c, 8 * 8);
-  probe<<<1, 1>>>(d, c, 0.1, 64);
-  cudaDeviceSynchronize();
-  probe<<<1, 1>>>(d, c, 0.1, 256);
-  cudaDeviceSynchronize();
-  long long h[8];
-  cudaMemcpy(h, c, sizeof(h), cudaMemcpyDeviceToHost);
-  const char* nm[8] = {"argmin_quartic", "real_roots_cubic", "acos", "cos", "div", "dfma", "cbrt", "sqrt"};
-  for (int i = 0; i < 8; ++i) printf("%-18s %6lld cycles per call\n", nm[i], h[i]);
+  const double Q[3][4] = {{-1.3, 2.1, -0.7, 0.4},
+                          {-48.722934571091756, -16.199242558319476, 0.023504568722528523, 0.003915087477943218},
+                          {-2971.3656000745905, -779.2859752760097, 94.5680757964538, 14.610197245665885}};
+  for (int qi = 0; qi < 3; ++qi)
+    for (int th : {1, 32}) {
+      probe<<<1, th>>>(d, c, 0.1, 64, Q[qi][0], Q[qi][1], Q[qi][2], Q[qi][3]);
+      cudaDeviceSynchronize();
+      probe<<<1, th>>>(d, c, 0.1, 256, Q[qi][0], Q[qi][1], Q[qi][2], Q[qi][3]);
+      cudaDeviceSynchronize();
+      long long h[8];
+      cudaMemcpy(h, c, sizeof(h), cudaMemcpyDeviceToHost);
+      printf("quartic %d, %2d threads: argmin %lld, real_roots_cubic %lld cycles\n", qi, th, h[0], h[1]);
+    }
   return 0;
 }

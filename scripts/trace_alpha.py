@@ -24,8 +24,12 @@ B.check(B.lib().prism_debug_trace_chain(ctypes.c_void_p(buf.data_ptr())), "trace
 P.polar(mats, handle=h, **opts)
 torch.cuda.synchronize()
 B.check(B.lib().prism_debug_trace_chain(None), "trace")
-T = buf[-8192:].view(-1, 4)[:32].cpu().numpy().astype(np.float64)
-for k, (a, b, c, d) in enumerate(T):
-    if a > 0:
-        print(f"iter {k:2d}: stop test {(b - a) / 1e3:6.2f} us  sums {(c - b) / 1e3 if c else float('nan'):6.2f} us"
-              f"  argmin {(d - c) / 1e3 if c else float('nan'):6.2f} us  total {(d - a) / 1e3 if d else float('nan'):6.2f} us")
+T = buf[-8192:].view(-1, 8)[:32].cpu().numpy().astype(np.float64)
+Cq = buf[-16384:-8192].view(-1, 8)[:32, :5].cpu().view(torch.float64).numpy()
+for k in range(3):
+    print("quartic", k, repr(list(Cq[k])))
+for k, row in enumerate(T):
+    a, b, c, d, e, f = row[:6]
+    if a > 0 and d > 0:
+        print(f"iter {k:2d}: entry->stop test done {(b - a) / 1e3:6.2f}  ->partials loaded {(e - b) / 1e3:6.2f}"
+              f"  ->reduced {(f - e) / 1e3:6.2f}  ->coeffs {(c - f) / 1e3:6.2f}  ->argmin {(d - c) / 1e3:6.2f} us")
