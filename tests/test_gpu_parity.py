@@ -282,3 +282,37 @@ def test_sqrt_caller_outputs_equal_fresh_outputs():
     assert X2[1] is osq[1] and Y2[0] is oisq[0]
     for a, b in zip(X + Y, X2 + Y2):
         assert torch.equal(a, b)
+
+
+_EARLY_SCRIPT = r"""
+import sys, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2601_22137_b200 as P
+from paper_2601_22137_b200 import workloads as W
+mats = [torch.tensor(W.gaussian(m, n, seed=7 + i)).to(torch.bfloat16).cuda()
+        for i, (m, n) in enumerate([(1024, 1024), (768, 2304), (3072, 768)])]
+Q, rep = P.polar(mats, degree=5, tol=3e-2, max_iters=20)
+torch.cuda.synchronize()
+torch.save({"Q": [q.cpu() for q in Q], "iters": rep["iters"].cpu()}, sys.argv[2])
+"""
+
+
+@pytest.mark.gpu
+def test_early_square_gemm_is_bit_identical(tmp_path):
+    """The square GEMM whose mainloop runs under k_alpha (GemmLaunch::early, bf16 polar
+    batches <= 16) computes exactly what the waiting launch computes."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "early.py"
+    script.write_text(_EARLY_SCRIPT)
+    outs = {}
+    for flag in ("0", "1"):
+        out = tmp_path / f"q{flag}.pt"
+        env = dict(os.environ, PRISM_EARLY_SQUARE=flag)
+        subprocess.run([sys.executable, str(script), root, str(out)], check=True, env=env, timeout=600)
+        outs[flag] = torch.load(out)
+    assert torch.equal(outs["0"]["iters"], outs["1"]["iters"])
+    for a, b in zip(outs["0"]["Q"], outs["1"]["Q"]):
+        assert torch.equal(a, b)
