@@ -1,11 +1,12 @@
 // Sketch-chain pass (PRISM §4.2 — the sketched-trace chain; device form DESIGN.md §4.4,
 // §4.6): D = W · Rᵀ, i.e. D[c][n] = (R W)[n][c], for every matrix of the batch.
 //
-// One tcgen05.mma costs the same ~138 cycles for any N ≤ 256 (measured, scripts/
-// mma_probe.cu), so the thin product R·W (W has 2w ≤ 32 columns) is issued with W as
-// the A operand (M = 128, of which the first 32 rows are the W rows; rows 32..127
-// read the B bytes that follow in smem and give TMEM lanes nobody reads) and 256 rows
-// of R as the B operand (N = 256).  Both operands are K-major in their natural
+// A kind::f16 tcgen05.mma (M = 128, K = 16) costs ≈ 50 cycles for N ≤ 64 and 128 for
+// N = 256 (scripts/mma_probe.cu), so the thin product R·W (W has
+// 2w ≤ 32 columns) is issued with W as the A operand (M = 128, of which the first 32
+// rows are the W rows; rows 32..127 read the B bytes that follow in smem and give TMEM
+// lanes nobody reads) and 256 rows of R as the B operand (N = 256): 32 x 256 useful
+// MACs per 128 cycles, against 128 x 32 per 50 for the untransposed form.  Both operands are K-major in their natural
 // layouts: W is stored [c][ldS] (the previous pass's output) and R row-major.
 //
 // Large matrices split K over a cluster of C = L.ksplit CTAs (the tile code's low bits
