@@ -192,10 +192,13 @@ def argmin_quartic(c: np.ndarray, lo: float, hi: float, alpha_taylor: float) -> 
 
     1. degenerate loss (max|c1..c4| = 0 or <= 1e-14 |c0|) -> Taylor a (S:209);
     2. divide c1..c4 by max|c1..c4|;
-    3. real roots of m'(a) = c1 + 2c2 a + 3c3 a^2 + 4c4 a^3, each polished by
-       two Newton steps on m';
-    4. candidates {lo, hi} U (roots in [lo, hi]); return the candidate with
-       the smallest m (ties -> smaller a).
+    3. the real roots of m''(a) = 2c2 + 6c3 a + 12c4 a^2 inside (lo, hi) cut [lo, hi]
+       into pieces on which m' is monotone, so a piece holds a root of m' where m has a
+       local minimum iff m' < 0 at its left end and m' >= 0 at its right end; that root
+       is bisected to the last bit (R16: the closed-form Cardano roots lost the moderate
+       roots when |c4| << |c3|, e.g. c4/c3 = 1e-10, and missed the minimum);
+    4. candidates {lo, hi} U those roots; return the candidate with the smallest m
+       (ties -> smaller a).
     """
     c = np.asarray(c, dtype=np.float64)
     scale = float(np.max(np.abs(c[1:])))
@@ -208,22 +211,35 @@ def argmin_quartic(c: np.ndarray, lo: float, hi: float, alpha_taylor: float) -> 
     def mprime(a):
         return ((4.0 * d4 * a + 3.0 * d3) * a + 2.0 * d2) * a + d1
 
-    def msecond(a):
-        return (12.0 * d4 * a + 6.0 * d3) * a + 2.0 * d2
-
     def m(a):  # c0 dropped: argmin-invariant
         return (((d4 * a + d3) * a + d2) * a + d1) * a
 
+    # roots of m''(a) = 12 d4 a^2 + 6 d3 a + 2 d2 (stable quadratic formula)
+    A, B, C = 12.0 * d4, 6.0 * d3, 2.0 * d2
+    crit = []
+    if A != 0.0:
+        disc = B * B - 4.0 * A * C
+        if disc >= 0.0:
+            q = -0.5 * (B + math.copysign(math.sqrt(disc), B))
+            crit.append(q / A)
+            if q != 0.0:
+                crit.append(C / q)
+    elif B != 0.0:
+        crit.append(-C / B)
+    breaks = [lo] + sorted(x for x in crit if lo < x < hi) + [hi]
     cands = [lo, hi]
-    for r in _real_roots_cubic(4.0 * d4, 3.0 * d3, 2.0 * d2, d1):
-        for _ in range(2):
-            m2 = msecond(r)
-            if m2 != 0.0:
-                nr = r - mprime(r) / m2
-                if math.isfinite(nr):
-                    r = nr
-        if math.isfinite(r) and lo <= r <= hi:
-            cands.append(r)
+    for x0, x1 in zip(breaks[:-1], breaks[1:]):
+        if not (mprime(x0) < 0.0 <= mprime(x1)):
+            continue
+        while True:   # bisection keeping m'(x0) < 0 <= m'(x1)
+            xm = 0.5 * (x0 + x1)
+            if xm <= x0 or xm >= x1:
+                break
+            if mprime(xm) < 0.0:
+                x0 = xm
+            else:
+                x1 = xm
+        cands.append(x1)
     cands.sort()
     best, best_m = cands[0], m(cands[0])
     for a in cands[1:]:

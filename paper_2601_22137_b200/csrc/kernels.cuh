@@ -856,8 +856,8 @@ __global__ void __launch_bounds__(256) k_sketch(SolveParams P) {
 }
 
 // ----------------------------------------------------------------- a5: coefficient solve
-// Robust interval argmin of the quartic (R15/R16): same written
-// procedure as the oracle, implemented independently here.
+// Real roots of a3 x^3 + a2 x^2 + a1 x + a0 (closed form; used by DB Newton's unconstrained
+// argmin, R27, whose quartic has c4 = ||E1 + E2||^2 of the order of the other terms).
 __device__ int real_roots_cubic(double a3, double a2, double a1, double a0, double* roots) {
   const double big = fmax(fabs(a2), fmax(fabs(a1), fabs(a0)));
   if (fabs(a3) <= 1e-12 * big) {
@@ -894,38 +894,68 @@ __device__ int real_roots_cubic(double a3, double a2, double a1, double a0, doub
   return 3;
 }
 
+
+// Interval argmin of the quartic m(a) = sum c_i a^i on [lo, hi] (readings R15, R16):
+// the roots of m'' (a quadratic: one sqrt) split [lo, hi] into at most three pieces on
+// which m' is monotone; a piece whose ends have m' < 0 <= m' holds exactly one local
+// minimum of m, located by Newton steps safeguarded by bisection (the bracket keeps
+// m'(x0) < 0 <= m'(x1), so the limit is that minimum to the last bits).  Candidates
+// {lo, hi} U minima, the smallest m wins (ties -> smaller a); degenerate loss -> Taylor.
+// (The closed-form Cardano roots this replaces lost the moderate roots when |c4| << |c3|
+// and missed minima; its fp64 acos / cos / cbrt also cost 9-13 us inside k_alpha.)
 __device__ double argmin_quartic(const double c[5], double lo, double hi, double aT) {
   const double scale = fmax(fmax(fabs(c[1]), fabs(c[2])), fmax(fabs(c[3]), fabs(c[4])));
   if (!isfinite(scale)) return aT;
   if (scale == 0.0 || scale <= 1e-14 * fabs(c[0])) return aT;
   const double d1 = c[1] / scale, d2 = c[2] / scale, d3 = c[3] / scale, d4 = c[4] / scale;
-  double roots[3];
-  const int nr = real_roots_cubic(4.0 * d4, 3.0 * d3, 2.0 * d2, d1, roots);
-  double cand[5];
-  int nc = 0;
-  cand[nc++] = lo;
-  cand[nc++] = hi;
-  for (int i = 0; i < nr; ++i) {
-    double r = roots[i];
-    for (int it = 0; it < 2; ++it) {
-      const double m2 = (12.0 * d4 * r + 6.0 * d3) * r + 2.0 * d2;
-      if (m2 != 0.0) {
-        const double m1 = ((4.0 * d4 * r + 3.0 * d3) * r + 2.0 * d2) * r + d1;
-        const double nr2 = r - m1 / m2;
-        if (isfinite(nr2)) r = nr2;
+  auto m = [&](double a) { return (((d4 * a + d3) * a + d2) * a + d1) * a; };
+  auto mp = [&](double a) { return ((4.0 * d4 * a + 3.0 * d3) * a + 2.0 * d2) * a + d1; };
+  auto mpp = [&](double a) { return (12.0 * d4 * a + 6.0 * d3) * a + 2.0 * d2; };
+  // breakpoints: lo, the roots of m'' inside (lo, hi), hi
+  double br[4];
+  int nb = 0;
+  br[nb++] = lo;
+  {
+    const double A = 12.0 * d4, Bq = 6.0 * d3, Cq = 2.0 * d2;
+    double r0 = NAN, r1 = NAN;
+    if (A != 0.0) {
+      const double disc = Bq * Bq - 4.0 * A * Cq;
+      if (disc >= 0.0) {
+        const double sq = sqrt(disc);
+        const double q = -0.5 * (Bq + (Bq >= 0.0 ? sq : -sq));
+        r0 = q / A;
+        r1 = q != 0.0 ? Cq / q : r0;
       }
+    } else if (Bq != 0.0) {
+      r0 = -Cq / Bq;
     }
-    if (isfinite(r) && r >= lo && r <= hi) cand[nc++] = r;
+    if (r0 > r1) { const double t = r0; r0 = r1; r1 = t; }
+    if (r0 > lo && r0 < hi) br[nb++] = r0;
+    if (r1 > lo && r1 < hi && r1 != r0) br[nb++] = r1;
   }
-  // sort ascending (insertion), pick the first strict minimum
-  for (int i = 1; i < nc; ++i)
-    for (int j = i; j > 0 && cand[j] < cand[j - 1]; --j) { double t = cand[j]; cand[j] = cand[j - 1]; cand[j - 1] = t; }
-  double best = cand[0];
-  double bm = (((d4 * best + d3) * best + d2) * best + d1) * best;
-  for (int i = 1; i < nc; ++i) {
-    const double a = cand[i];
-    const double ma = (((d4 * a + d3) * a + d2) * a + d1) * a;
-    if (ma < bm) { best = a; bm = ma; }
+  br[nb++] = hi;
+  double best = lo, bm = m(lo);
+  {
+    const double mh = m(hi);
+    if (mh < bm) { best = hi; bm = mh; }
+  }
+  for (int j = 0; j + 1 < nb; ++j) {
+    double x0 = br[j], x1 = br[j + 1];
+    if (!(mp(x0) < 0.0 && mp(x1) >= 0.0)) continue;
+    double x = 0.5 * (x0 + x1);
+    for (int it = 0; it < 100; ++it) {
+      const double f = mp(x);
+      if (f < 0.0) x0 = x; else x1 = x;
+      const double fp = mpp(x);
+      double xn = (fp != 0.0) ? x - f / fp : 0.5 * (x0 + x1);
+      if (!(xn > x0 && xn < x1)) xn = 0.5 * (x0 + x1);   // Newton left the bracket: bisect
+      if (xn == x || xn <= x0 || xn >= x1) { x = (xn > x0 && xn < x1) ? xn : x; break; }
+      x = xn;
+    }
+    // the bracket end on the non-negative side is the reported root (argmin_poly_warp rule)
+    const double r = mp(x) >= 0.0 ? x : x1;
+    const double mr = m(r);
+    if (mr < bm || (mr == bm && r < best)) { best = r; bm = mr; }
   }
   return best;
 }
@@ -1159,7 +1189,7 @@ __global__ void __launch_bounds__(256) k_alpha(SolveParams P, int pre_wait) {
       for (int i = 0; i <= q; ++i)
         for (int j = i; j <= q; ++j) c[i + j] += (i == j ? 1.0 : 2.0) * g[idx++];
       if (k < P.warmup) a = P.ahi;
-      else if (q <= 2) a = argmin_quartic(c, P.alo, P.ahi, P.ataylor);   // degree <= 4: analytic
+      else if (q <= 2) a = argmin_quartic(c, P.alo, P.ahi, P.ataylor);   // degree <= 4
       else a = argmin_poly_warp(c, 2 * q, P.alo, P.ahi, P.ataylor);
     } else {
       double c[5] = {g[0], 2.0 * g[1], g[3] + 2.0 * g[2], 2.0 * g[4], g[5]};

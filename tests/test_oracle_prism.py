@@ -437,3 +437,23 @@ def test_sign_block_matrix_gives_square_roots():
 def test_sign_zero_input():
     S, rep = prism.sign(np.zeros((8, 8)))
     assert rep.status == prism.ZERO_INPUT and not S.any()
+
+
+def test_argmin_badly_scaled_cubic_against_dense_grid():
+    """Regression pin (R16): quartics whose c4 is ~1e-10 of c3 — the closed-form Cardano
+    roots lost the moderate root and the argmin returned an interval end with a larger
+    loss.  The argmin must match a 200001-point brute-force grid."""
+    cases = [([19.544087647012184, -44.43517630092626, -114.43158552440468, 132.84099703384126,
+               1.5172433851677812e-08], 0.375, 1.45),
+             ([19.544087647012184, -44.43517630092626, -114.43158552440468, 132.84099703384126,
+               1.5172433851677812e-08], 0.5, 1.0),
+             ([3.4403680645019565e-08, 6.009257289921177e-07, -8.716852875631071, 4.452838746516632,
+               1.0848522704284619e-08], 0.375, 1.45)]
+    for c, lo, hi in cases:
+        c = np.array(c)
+        m = lambda x: c[1] * x + c[2] * x ** 2 + c[3] * x ** 3 + c[4] * x ** 4  # noqa: E731
+        xs = np.linspace(lo, hi, 200001)
+        a = prism.argmin_quartic(c, lo, hi, lo)
+        assert lo <= a <= hi
+        assert m(a) <= m(xs).min() + 1e-12 * np.max(np.abs(c[1:]))
+        assert abs(a - xs[np.argmin(m(xs))]) <= 2 * (hi - lo) / 200000
