@@ -76,6 +76,7 @@ struct SolveParams {
   double* fro_part;     // [batch * kFroParts]
   const int* tile_off;  // [batch + 1] prefix of 64x64 layout tiles (normalise: Xt; finalise: output)
   const int* out_tile_off;
+  const int* tile_mat;  // [n_tiles] matrix of each layout tile (same tiling for normalise / finalise)
   const int* fro_off;   // [batch + 1] prefix of the per-matrix ||A||_F partial counts (fro_parts)
   int n_tiles, n_out_tiles, n_fro_blocks;
   double* fro2_out;     // row-block begin: local sum of squares (else null)
@@ -337,7 +338,7 @@ __global__ void __launch_bounds__(256) k_normalize(SolveParams P) {
   griddep_launch();
   using V = Vec<PREC>;
   const int t = blockIdx.x;
-  const int b = find_matrix(P.tile_off, P.batch, t);
+  const int b = __ldg(P.tile_mat + t);   // one load (a binary search over tile_off was ~6 dependent loads)
   const MatDesc& D = P.mats[b];
   const double c = P.st[b].c;   // written by k_fro_final
   const float inv = c > 0.0 ? (float)(1.0 / c) : 0.f;
@@ -1216,7 +1217,7 @@ __global__ void __launch_bounds__(256) k_finalize(SolveParams P) {
   using V = Vec<PREC>;
   using VO = Vec<PREC == 0 ? 0 : 2>;   // user output: bf16 or plain fp32
   const int t = blockIdx.x;
-  const int b = find_matrix(P.out_tile_off, P.batch, t);
+  const int b = __ldg(P.tile_mat + t);
   const MatDesc& D = P.mats[b];
   const MatState& S = P.st[b];
   const int par = S.iters & 1;

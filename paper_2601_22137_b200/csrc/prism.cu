@@ -809,6 +809,9 @@ prism_status build_plan(const Request& r, Plan& P) {
   off += sizeof(int) * (B + 1);
   const size_t foff_off = off;
   off += sizeof(int) * (B + 1);
+  off = align_up(off, 128);
+  const size_t tmat_off = off;   // layout tile -> matrix (normalise / finalise: no search)
+  off += sizeof(int) * (size_t)toff[B];
   std::vector<LaunchDesc*> all = {&P.gram[0],   &P.gram[1],   &P.apply[0],  &P.apply[1],  &P.square,
                                   &P.chaint[0], &P.chaint[1], &P.chaint[2], &P.chaint[3], &P.chaint[4],
                                   &P.gram32[0], &P.gram32[1], &P.square2};
@@ -841,6 +844,11 @@ prism_status build_plan(const Request& r, Plan& P) {
   std::memcpy(blob + toff_off, toff.data(), sizeof(int) * (B + 1));
   std::memcpy(blob + ooff_off, ooff.data(), sizeof(int) * (B + 1));
   std::memcpy(blob + foff_off, foff.data(), sizeof(int) * (B + 1));
+  {
+    int* tm = reinterpret_cast<int*>(blob + tmat_off);
+    for (int i = 0; i < B; ++i)
+      for (int t = toff[i]; t < toff[i + 1]; ++t) tm[t] = i;
+  }
   CUtensorMap* hmaps = reinterpret_cast<CUtensorMap*>(blob + maps_off);
   for (size_t j = 0; j < maps.size(); ++j)
     if (!encode_map(&hmaps[j], maps[j])) return fail(PRISM_ERR_CUDA, "cuTensorMapEncodeTiled failed");
@@ -870,6 +878,7 @@ prism_status build_plan(const Request& r, Plan& P) {
   std::memset(&S, 0, sizeof(S));
   S.mats = reinterpret_cast<MatDesc*>(meta_dev + mats_off);
   S.tile_off = reinterpret_cast<const int*>(meta_dev + toff_off);
+  S.tile_mat = reinterpret_cast<const int*>(meta_dev + tmat_off);
   S.out_tile_off = reinterpret_cast<const int*>(meta_dev + ooff_off);
   S.fro_off = reinterpret_cast<const int*>(meta_dev + foff_off);
   S.n_fro_blocks = foff[B];
