@@ -1,23 +1,30 @@
 """bench.py — PRISM Newton–Schulz on B200 (BASELINE.json metric/configs).
 
-A "step" is one call of the whole hot path over one batch: normalise, then
-per iteration residual GEMM -> sketch chain -> alpha solve -> square GEMM ->
-apply GEMM, until every matrix converged, then write-back.  Default workload
-(N=1) is BASELINE.json configs[1]: the Muon step of GPT-2 small, 48 BF16
-layer gradients 768x{768,2304,3072} / 3072x768, PRISM-5 polar.
+A "step" is one call of the whole hot path over one batch: normalise, then per
+iteration residual GEMM -> sketch chain -> alpha solve -> square GEMM -> apply
+GEMM, until every matrix converged, then write-back.  Default workload (N=1) is
+BASELINE.json configs[1]: the Muon step of GPT-2 small, 48 BF16 layer gradients
+768x{768,2304,3072} / 3072x768, PRISM-5 polar.
 
 Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl prism|reference]
-                        [--workload gpt2|square4096|gpt1b|shampoo]
-Multi-GPU: launched by torch.distributed.run, one rank per GPU; each rank
-solves its own batch (independent matrices, no data-path collective), so the
-scaling is weak.  Prints one JSON line on rank 0.
+                        [--workload gpt2|square4096|...] [--no-extra] [--no-cpu-baseline]
+
+Multi-GPU (launched by torch.distributed.run, one rank per GPU, NCCL):
+  gpt2 (default)  weak scaling of the sharded Muon step: a 12N-layer
+                  GPT-2-small-shaped model (48N matrices), LPT-partitioned over the N
+                  ranks by prism_polar_sharded, outputs exchanged by NCCL broadcasts from
+                  their owners inside the timed region; every rank ends with all 48N.
+  gpt1b           strong scaling of configs[4] (96 matrices, 1.2 B params), same path.
+  rowblock8192    strong scaling of configs[3]: one 8192^2 BF16 matrix split by rows
+                  (prism_polar_rowblock: packed-triangle Gram all-reduce per iteration).
+  others          independent replicas (no data-path collective).
+Prints one JSON line on rank 0.
 """
 
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
 import subprocess
@@ -29,18 +36,21 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "PRISM solves/sec and TFLOP/s vs B200 BF16 peak; iterations to tolerance"
+SHARDED = ("gpt2", "gpt1b")   # workloads whose N > 1 run goes through the sharded path
 
 
 # ---------------------------------------------------------------- workloads
-def workload(name: str, rank: int):
+def workload(name: str, rank: int, world: int = 1):
     from paper_2601_22137_b200 import workloads as W
     if name == "gpt2":
-        shapes = W.gpt2_small_shapes()
-        mats = W.muon_batch(shapes, seed=1 + rank, kind="mixed")
+        shapes = W.gpt2_small_shapes() * world      # N > 1: a 12N-layer GPT-2-small-shaped model (weak)
+        mats = W.muon_batch(shapes, seed=1, kind="mixed")
         opts = dict(degree=5, max_iters=20, tol=3e-2, sketch_size=8, seed=42, precision="bf16")
         desc = ("GPT-2 small Muon step (BASELINE.json configs[1]): 48 BF16 gradient matrices, 12 x "
                 "{768x2304, 768x768, 768x3072, 3072x768}; half Gaussian (MP), half HTMP-like kappa=0.5; "
                 "PRISM-5 polar, p=8, tol 3e-2, max_iters 20")
+        if world > 1:
+            desc += f"; N={world}: {48 * world} matrices ({12 * world} layers), LPT-sharded + NCCL broadcast"
         return "gpt2-small-muon-step", shapes, mats, opts, desc, "polar"
     if name == "square4096":
         shapes = [(4096, 4096)]
@@ -48,13 +58,29 @@ def workload(name: str, rank: int):
         opts = dict(degree=5, max_iters=25, tol=3e-2, sketch_size=8, seed=42, precision="bf16")
         desc = "single 4096x4096 Gaussian BF16 polar (north_star 60%-of-peak target shape), PRISM-5, p=8, tol 3e-2"
         return "polar-4096-square", shapes, mats, opts, desc, "polar"
+    if name == "square4096_fp32":
+        shapes = [(4096, 4096)]
+        mats = [W.gaussian(4096, 4096, seed=4096 + rank)]
+        opts = dict(degree=5, max_iters=25, tol=1e-5, sketch_size=8, seed=42, precision="fp32")
+        desc = ("single 4096x4096 Gaussian polar in FP32 (3xTF32; the paper's precision, P:1225), PRISM-5, p=8, "
+                "tol 1e-5")
+        return "polar-4096-square-fp32", shapes, mats, opts, desc, "polar"
     if name == "gpt1b":
         shapes = W.gpt_1b_shapes()
-        mats = W.muon_batch(shapes, seed=1 + rank, kind="gaussian")
+        mats = W.muon_batch(shapes, seed=1, kind="gaussian")
         opts = dict(degree=5, max_iters=20, tol=3e-2, sketch_size=8, seed=42, precision="bf16")
-        desc = ("1.2B-param GPT Muon step (configs[4] batch, one GPU): 96 BF16 matrices 24 x "
+        desc = ("1.2B-param GPT Muon step (configs[4]): 96 BF16 matrices 24 x "
                 "{2048x6144, 2048^2, 2048x8192, 8192x2048}, Gaussian, PRISM-5, tol 3e-2")
+        if world > 1:
+            desc += f"; N={world}: LPT-sharded + NCCL broadcast (strong scaling)"
         return "gpt-1b-muon-step", shapes, mats, opts, desc, "polar"
+    if name == "rowblock8192":
+        shapes = [(8192, 8192)]
+        mats = [W.gaussian(8192, 8192, seed=3000)]
+        opts = dict(degree=5, max_iters=25, tol=3e-2, sketch_size=8, seed=42, precision="bf16")
+        desc = (f"configs[3]: one 8192x8192 Gaussian BF16 polar, row-block split over {world} rank(s) "
+                "(packed-triangle Gram all-reduce per iteration), PRISM-5, tol 3e-2")
+        return "polar-8192-rowblock", shapes, mats, opts, desc, "rowblock"
     if name == "shampoo":
         shapes = [(1024, 1024)] * 8 + [(2048, 2048)] * 4 + [(4096, 4096)] * 2
         mats = [W.spd_logspaced(m, 1e2, seed=100 * rank + i) for i, (m, _) in enumerate(shapes)]
@@ -86,11 +112,15 @@ def workload(name: str, rank: int):
     if name == "dbnewton":
         shapes = [(1024, 1024)] * 8 + [(2048, 2048)] * 4 + [(4096, 4096)] * 2
         mats = [W.spd_logspaced(m, 1e2, seed=100 * rank + i) for i, (m, _) in enumerate(shapes)]
-        opts = dict(max_iters=30, tol=1e-5, sketch_size=8, precision="fp32")
+        opts = dict(max_iters=30, tol=1e-5, precision="fp32")
         desc = ("Shampoo step (configs[2] blocks: 8x1024 + 4x2048 + 2x4096 SPD, kappa=1e2, FP32 3xTF32): PRISM "
                 "DB Newton product form A^{1/2}, A^{-1/2} (P:499-523; exact unsketched fit), tol 1e-5")
         return "shampoo-dbnewton-step", shapes, mats, opts, desc, "db_newton"
     raise SystemExit(f"unknown workload {name}")
+
+
+WORKLOADS = ["gpt2", "square4096", "square4096_fp32", "gpt1b", "rowblock8192", "shampoo", "sign4096", "invroot",
+             "cheb4096", "dbnewton"]
 
 
 # ---------------------------------------------------------------- helpers
@@ -177,6 +207,15 @@ class ClockSampler:
         """Start of the timed region: samples from here on are reported."""
         self.t0 = time.time()
 
+    def window(self, t0, t1):
+        sm, reasons = [], set()
+        for ts, mhz, rs in list(self.samples):
+            if t0 <= ts <= t1:
+                sm.append(mhz)
+                reasons |= rs
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
     def stop(self):
         self.stop_ev.set()
         if self.proc is not None:
@@ -188,39 +227,25 @@ class ClockSampler:
         if self.source is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
         time.sleep(0.02)
-        sm, reasons = [], set()
-        for ts, mhz, rs in list(self.samples):
-            if ts < self.t0:
-                continue
-            sm.append(mhz)
-            reasons |= rs
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(reasons), "samples": len(sm), "source": self.source}
+        d = self.window(self.t0, time.time() + 1.0)
+        d["source"] = self.source
+        return d
+
+
+def pick_peak(peaks, clk, precision):
+    """Tensor peak for the roofline denominator (MEASURED_PEAKS.json): the burst figure when
+    the timed region ran at >= 95 % of max SM clock with no power cap (a short kernel timed
+    alone), else the sustained one; tf32 = bf16 / 2 (nominal ratio), 3xTF32 issues 3 MMAs."""
+    burst = float(peaks.get("bf16_tflops", 1590.0))
+    sus = float(peaks.get("bf16_tflops_sustained", burst))
+    scale = 1.0 if precision == "bf16" else (1.0 / 2.0 / 3.0 if precision == "fp32" else 0.5)
+    med, mx = clk.get("sm_mhz"), clk.get("sm_max_mhz")
+    use_burst = bool(med and mx and med >= 0.95 * mx and "sw_power_cap" not in clk.get("reasons", []))
+    return (burst if use_burst else sus) * scale, ("burst" if use_burst else "sustained"), burst * scale, sus * scale
 
 
 def flush_l2(buf):
     buf.add_(1)   # 256 MiB write > 126 MB L2
-
-
-def cpu_oracle_solve(A, kind, opts, b):
-    from oracle import prism
-    d = 1 if opts.get("degree", 5) == 3 else 2
-    if kind == "polar":
-        return prism.polar(A, d=d, p=opts["sketch_size"], tol=opts["tol"], max_iters=opts["max_iters"],
-                           seed=opts["seed"], b=b)[1]
-    if kind == "sign":
-        return prism.sign(A, d=d, p=opts["sketch_size"], tol=opts["tol"], max_iters=opts["max_iters"],
-                          seed=opts["seed"], b=b)[1]
-    if kind == "chebyshev":
-        return prism.chebyshev_inverse(A, p=opts["sketch_size"], tol=opts["tol"], max_iters=opts["max_iters"],
-                                       seed=opts["seed"], b=b)[1]
-    if kind == "db_newton":
-        return prism.db_newton(A, tol=opts["tol"], max_iters=opts["max_iters"])[2]
-    if kind == "inv_root":
-        return prism.inv_root(A, q=opts["q"], p=opts["sketch_size"], tol=opts["tol"], max_iters=opts["max_iters"],
-                              seed=opts["seed"], b=b)[1]
-    return prism.sqrt_invsqrt(A, d=d, p=opts["sketch_size"], tol=opts["tol"], max_iters=opts["max_iters"],
-                              seed=opts["seed"], b=b)[2]
 
 
 def blas_threads():
@@ -238,6 +263,74 @@ def stored_inputs(mats, dtype_name):
     return [torch.tensor(a).to(dt).double().numpy() for a in mats]
 
 
+def cpu_oracle_solve(A, kind, opts, b):
+    """The fp64 oracle on one matrix: (primary output, report)."""
+    from oracle import prism
+    d = 1 if opts.get("degree", 5) == 3 else 2
+    kw = dict(tol=opts["tol"], max_iters=opts["max_iters"])
+    if kind in ("polar", "rowblock"):
+        r = prism.polar(A, d=d, p=opts["sketch_size"], seed=opts["seed"], b=b, **kw)
+        return r[0], r[1]
+    if kind == "sign":
+        r = prism.sign(A, d=d, p=opts["sketch_size"], seed=opts["seed"], b=b, **kw)
+        return r[0], r[1]
+    if kind == "chebyshev":
+        r = prism.chebyshev_inverse(A, p=opts["sketch_size"], seed=opts["seed"], b=b, **kw)
+        return r[0], r[1]
+    if kind == "db_newton":
+        r = prism.db_newton(A, **kw)
+        return r[0], r[2]
+    if kind == "inv_root":
+        r = prism.inv_root(A, q=opts["q"], p=opts["sketch_size"], seed=opts["seed"], b=b, **kw)
+        return r[0], r[1]
+    r = prism.sqrt_invsqrt(A, d=d, p=opts["sketch_size"], seed=opts["seed"], b=b, **kw)
+    return r[0], r[2]
+
+
+def flops_per_iter(P, kind, shapes, opts):
+    """Algorithmic FLOPs per iteration per matrix (F_min: symmetric products once)."""
+    p = opts.get("sketch_size", 8)
+    if kind in ("polar", "rowblock"):
+        return [P.polar_flops_per_iter(m, n, opts["degree"], p) for (m, n) in shapes]
+    if kind == "chebyshev":    # A'X (residual), R.R, X.P (general products) + 3 chain passes
+        return [6.0 * m ** 3 + 6.0 * m * m * p for (m, _) in shapes]
+    if kind == "inv_root":     # X + aX.R, M + P_q.M, the POLY products of P_q, chain
+        npoly = {1: 0, 2: 1, 3: 2, 4: 2}[opts["q"]]
+        return [(4.0 + 2.0 * npoly) * m ** 3 + 2.0 * (opts["q"] + 1) * m * m * p for (m, _) in shapes]
+    if kind == "db_newton":    # Gauss-Jordan sweep M -> -M^{-1} (2 n^3), X.W and Y.W (4 n^3)
+        return [6.0 * m ** 3 for (m, _) in shapes]
+    if kind == "sign":         # general products X.X, R.R, X.P + the sketch chain
+        return [4.0 * m ** 3 + ((2.0 * m ** 3 + 14.0 * m * m * p) if opts["degree"] == 5 else 6.0 * m * m * p)
+                for (m, _) in shapes]
+    return [P.sqrt_flops_per_iter(m, opts["degree"], p) for (m, _) in shapes]
+
+
+def kernel_flops(kind, shapes, iters):
+    """Algorithmic FLOPs of the residual / square / apply launches of one step."""
+    it = list(zip(shapes, iters))
+    if kind in ("polar", "rowblock"):
+        apply = sum(2.0 * max(m, n) * min(m, n) ** 2 * k for (m, n), k in it)
+        gram = sum(max(m, n) * min(m, n) * (min(m, n) + 1) * (k + 1) for (m, n), k in it)
+        sq = sum(min(m, n) ** 2 * (min(m, n) + 1) * k for (m, n), k in it)
+    elif kind in ("chebyshev", "sign"):
+        apply = sum(2.0 * m ** 3 * k for (m, _), k in it)
+        gram = sum(2.0 * m ** 3 * (k + 1) for (m, _), k in it)
+        sq = sum(2.0 * m ** 3 * k for (m, _), k in it)
+    elif kind == "inv_root":
+        apply = sum(4.0 * m ** 3 * k for (m, _), k in it)
+        gram = 0.0   # R = I - M is elementwise (k_resid_inv)
+        sq = 0.0
+    elif kind == "db_newton":
+        apply = sum(4.0 * m ** 3 * k for (m, _), k in it)
+        gram = 0.0   # M_k copied / residual formed elementwise (k_db_begin)
+        sq = sum(2.0 * m ** 3 * k for (m, _), k in it)   # Gauss-Jordan sweep
+    else:
+        apply = sum(4.0 * m ** 3 * k for (m, _), k in it)
+        gram = sum(2.0 * m ** 3 * (k + 1) for (m, _), k in it)
+        sq = sum(2.0 * m ** 3 * k for (m, _), k in it)
+    return {"gram": gram, "square": sq, "apply": apply}
+
+
 # ---------------------------------------------------------------- reference arm (the oracle)
 def run_reference(args, rank, world):
     if rank != 0:
@@ -251,7 +344,7 @@ def run_reference(args, rank, world):
         if shp not in seen:
             seen.add(shp)
             sample.append(i)
-    smallest = min(range(len(A)), key=lambda i: A[i].size)
+    smallest = min(sample, key=lambda i: A[i].size)
     for w in range(args.warmup):   # warm-up: BLAS threads / caches, one small solve
         cpu_oracle_solve(A[smallest], kind, opts, smallest)
     times = []
@@ -279,6 +372,199 @@ def run_reference(args, rank, world):
     return 0
 
 
+# ---------------------------------------------------------------- our arm: one GPU
+class Runner:
+    """Device-path and host-path (e2e) solves of one workload on one GPU through the library's
+    public API, with caller-owned outputs reused every step (a training loop's pattern: fresh
+    buffers would rebuild the handle's pointer-keyed plan)."""
+
+    def __init__(self, P, kind, mats_np, opts, dev):
+        import torch
+        self.P, self.kind, self.opts, self.dev = P, kind, opts, dev
+        dt = torch.bfloat16 if opts["precision"] == "bf16" else torch.float32
+        self.host = [torch.tensor(a).to(dt).pin_memory() for a in mats_np]
+        self.mats = [x.to(dev) for x in self.host]
+        self.B = len(self.mats)
+        self.h = P.Handle()
+        self.ids = list(range(self.B))
+        two = kind in ("sqrt", "db_newton")
+        self.out = [torch.empty_like(m) for m in self.mats]
+        self.out2 = [torch.empty_like(m) for m in self.mats] if two else None
+        self.host_out = [torch.empty_like(x).pin_memory() for x in self.host]
+        self.kw = {k: v for k, v in opts.items() if not (kind == "db_newton" and k == "sketch_size")}
+
+    def solve(self):
+        P, k = self.P, self.kind
+        if k in ("sqrt", "db_newton"):
+            f = P.sqrt_invsqrt if k == "sqrt" else P.db_newton
+            a, b, rep = f(self.mats, matrix_ids=self.ids, handle=self.h, out_sqrt=self.out, out_invsqrt=self.out2,
+                          **self.kw)
+            return a, rep
+        f = {"polar": P.polar, "sign": P.sign, "inv_root": P.inv_root, "chebyshev": P.chebyshev_inverse}[k]
+        return f(self.mats, out=self.out, matrix_ids=self.ids, handle=self.h, **self.kw)
+
+    def solve_host(self):
+        P, k = self.P, self.kind
+        if k in ("sqrt", "db_newton"):   # the Shampoo preconditioner consumes A^{-1/2}
+            f = P.sqrt_invsqrt_host if k == "sqrt" else P.db_newton_host
+            return f(self.host, matrix_ids=self.ids, handle=self.h, want_sqrt=False, out_invsqrt=self.host_out,
+                     **self.kw)
+        f = {"polar": P.polar_host, "sign": P.sign_host, "inv_root": P.inv_root_host,
+             "chebyshev": P.chebyshev_inverse_host}[k]
+        return f(self.host, out=self.host_out, matrix_ids=self.ids, handle=self.h, **self.kw)
+
+
+def time_device(run, steps, warmup, flush, stream, dist_ctx=None):
+    """W warm-up steps, then K steps bracketed by barrier + synchronize, each step timed by
+    CUDA events on the launching stream with the L2 flushed before it (outside the events)."""
+    import torch
+    for _ in range(warmup):
+        run()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    if dist_ctx is not None:
+        dist_ctx.barrier()
+    torch.cuda.synchronize()
+    res = None
+    for s in range(steps):
+        flush_l2(flush)
+        ev[s][0].record(stream)
+        res = run()
+        ev[s][1].record(stream)
+    torch.cuda.synchronize()
+    return sum(a.elapsed_time(b) for a, b in ev), res
+
+
+def profile_kernels(r, steps, flush):
+    """Per-kernel-kind device time: a separate pass of direct launches, each launch group
+    bracketed by CUDA events on the launching stream (prism_profile_*)."""
+    import torch
+    r.h.profile(True)
+    r.h.profile_read(reset=True)
+    for _ in range(steps):
+        flush_l2(flush)
+        r.solve()
+    torch.cuda.synchronize()
+    prof = r.h.profile_read(reset=True)
+    r.h.profile(False)
+    return prof
+
+
+def roofline_of(prof, kind, shapes, iters, steps, peak, peak_kind, burst, sus, name):
+    kf = kernel_flops(kind, shapes, iters)
+    kernel_tflops = {k: (kf[k] * steps / (prof[k]["ms"] / 1e3) / 1e12 if prof[k]["ms"] > 0 and kf[k] > 0 else None)
+                     for k in ("gram", "square", "apply")}
+    achieved = kernel_tflops["apply"]
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"traffic_{name}.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("apply_dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    total = sum(v["ms"] for v in prof.values())
+    roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+            "kernel": "prism_apply_kernel (X + X.P, tcgen05)", "peak_kind": peak_kind,
+            "frac_burst": (achieved / burst) if achieved else None,
+            "frac_sustained": (achieved / sus) if achieved else None}
+    kernels = {"tflops": kernel_tflops,
+               "frac_of_peak": {k: (v / peak if v else None) for k, v in kernel_tflops.items()},
+               "time_share": {k: (v["ms"] / total if total > 0 else None) for k, v in prof.items()},
+               "ms_per_step": {k: v["ms"] / steps for k, v in prof.items()},
+               "launches_per_step": {k: v["launches"] / steps for k, v in prof.items()}}
+    return roof, kernels
+
+
+def single_gpu(P, name, shapes, mats_np, opts, kind, dev, steps, warmup, flush, clocks, e2e=True):
+    """Device-timed value, e2e value and per-kernel roofline of one workload on one GPU."""
+    import torch
+    r = Runner(P, kind, mats_np, opts, dev)
+    stream = torch.cuda.current_stream(dev)
+    t_start = time.time()
+    ms, res = time_device(r.solve, steps, warmup, flush, stream)
+    t_end = time.time()
+    launches = r.h.launch_count()
+    rep = res[-1]
+    iters = rep["iters"].cpu().tolist()
+    status = rep["status"].cpu().tolist()
+    f_iter = flops_per_iter(P, kind, shapes, opts)
+    flops_step = sum(f * k for f, k in zip(f_iter, iters))
+    out = {"ms": ms, "ms_step": ms / steps, "value": r.B * steps / (ms / 1e3),
+           "tflops": flops_step * steps / (ms / 1e3) / 1e12, "iters": iters, "status": status,
+           "launches_per_step": launches, "runner": r, "t_window": (t_start, t_end)}
+    if e2e:
+        for _ in range(4):   # warm: every staging slot's buffers and plan
+            r.solve_host()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            r.solve_host()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        out["e2e_ms"] = e0.elapsed_time(e1)
+        out["e2e_bytes"] = sum(x.numel() * x.element_size() for x in r.host)
+    out["prof"] = profile_kernels(r, steps, flush)
+    return out
+
+
+def cpu_baseline(kind, shapes, mats_np, opts, dev_out, iters, budget_s=10.0):
+    """The oracle as it stands, on a bounded sample (one matrix of each distinct shape), on the
+    host cores; also the sampled device-vs-oracle parity of those matrices."""
+    import numpy as np
+    A = stored_inputs(mats_np, opts["precision"])
+    seen, sample = set(), []
+    for i, shp in enumerate(shapes):
+        if shp not in seen:
+            seen.add(shp)
+            sample.append(i)
+    t0 = time.perf_counter()
+    done, results = 0, {}
+    while True:          # whole passes over the one-per-shape sample, ~budget_s of CPU work
+        for i in sample:
+            results[i] = cpu_oracle_solve(A[i], kind, opts, i)
+        done += 1
+        if time.perf_counter() - t0 >= budget_s:
+            break
+    sec = time.perf_counter() - t0
+    rel = {}
+    for i in sample:
+        Xo = results[i][0]
+        x = dev_out[i].double().cpu().numpy()
+        rel[str(i)] = float(np.linalg.norm(x - Xo) / np.linalg.norm(Xo))
+    return {"value": done * len(sample) / sec, "unit": "solves/s", "cores": blas_threads(), "kind": "oracle",
+            "sample": f"{done} pass(es) x {len(sample)} of {len(shapes)} matrices (one per distinct shape), "
+                      f"fp64 numpy oracle, {sec:.2f} s",
+            # iterations to tolerance and relative Frobenius error, device vs the fp64 oracle on the
+            # same stored inputs
+            "iters_vs_oracle": {"matrix": sample, "device": [int(iters[i]) for i in sample],
+                                "oracle": [int(results[i][1].iters) for i in sample]},
+            "rel_err_vs_oracle": rel}
+
+
+def extra_solve(P, wl, dev, flush, clocks, steps=5, warmup=3):
+    """A driver-timed secondary number (north-star shape / the paper's precision) with its
+    own roofline; no e2e, no CPU baseline."""
+    name, shapes, mats_np, opts, desc, kind = workload(wl, 0)
+    r = single_gpu(P, name, shapes, mats_np, opts, kind, dev, steps, warmup, flush, clocks, e2e=False)
+    clk = clocks.window(*r["t_window"])
+    peaks, src = read_peaks()
+    peak, pk, burst, sus = pick_peak(peaks, clk, opts["precision"])
+    roof, kern = roofline_of(r["prof"], kind, shapes, r["iters"], steps, peak, pk, burst, sus, name)
+    roof["peak_source"] = src
+    return {"workload": name, "description": desc, "dtype": opts["precision"], "value": r["value"],
+            "unit": "solves/s", "ms_per_step": r["ms_step"], "steps": steps, "warmup": warmup,
+            "tflops": r["tflops"], "frac_of_peak": r["tflops"] / peak, "iterations": r["iters"],
+            "status_converged": sum(1 for x in r["status"] if x == 0), "roofline": roof, "kernels": kern,
+            "clocks_timed": clk}
+
+
+# ---------------------------------------------------------------- our arm: N GPUs, sharded
+def run_multi(args, rank, world, dev):
+    raise SystemExit("multi-GPU sharded / row-block bench: not built yet")
+
+
 # ---------------------------------------------------------------- our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -286,9 +572,9 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="prism", choices=["prism", "reference"])
-    ap.add_argument("--workload", default="gpt2", choices=["gpt2", "square4096", "gpt1b", "shampoo", "sign4096", "invroot", "cheb4096",
-                                                             "dbnewton"])
+    ap.add_argument("--workload", default="gpt2", choices=WORKLOADS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)   # timing rule: >= 3 warm-up steps
 
@@ -306,235 +592,76 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+        if args.workload in SHARDED or args.workload == "rowblock8192":
+            rc = run_multi(args, rank, world, dev)
+            dist.barrier()
+            dist.destroy_process_group()
+            return rc
+    elif args.workload == "rowblock8192":
+        return run_multi(args, rank, world, dev)
 
     name, shapes, mats_np, opts, desc, kind = workload(args.workload, rank)
-    dt = torch.bfloat16 if opts["precision"] == "bf16" else torch.float32
-    host = [torch.tensor(a).to(dt).pin_memory() for a in mats_np]
-    mats = [h.to(dev) for h in host]
-    B = len(mats)
-    h = P.Handle()
-    ids = list(range(B))
-    stream = torch.cuda.current_stream(dev)
-
-    def solve(inputs, out=None):
-        if kind == "polar":
-            return P.polar(inputs, out=out, matrix_ids=ids, handle=h, **opts)
-        if kind == "sign":
-            return P.sign(inputs, out=out, matrix_ids=ids, handle=h, **opts)
-        if kind == "inv_root":
-            return P.inv_root(inputs, out=out, matrix_ids=ids, handle=h, **opts)
-        if kind == "chebyshev":
-            return P.chebyshev_inverse(inputs, out=out, matrix_ids=ids, handle=h, **opts)
-        # sqrt kinds: both outputs into preallocated buffers (reused every step, as a
-        # training loop would; fresh buffers would rebuild the handle's pointer-keyed plan)
-        if kind == "db_newton":
-            return P.db_newton(inputs, matrix_ids=ids, handle=h, out_sqrt=outs2[0], out_invsqrt=outs2[1], **dbo)
-        return P.sqrt_invsqrt(inputs, matrix_ids=ids, handle=h, out_sqrt=outs2[0], out_invsqrt=outs2[1], **opts)
-
-    dbo = {k: v for k, v in opts.items() if k != "sketch_size"}
-    outs = [torch.empty_like(m) for m in mats] if kind in ("polar", "sign", "inv_root", "chebyshev") else None
-    outs2 = ([torch.empty_like(m) for m in mats], [torch.empty_like(m) for m in mats]) \
-        if kind in ("sqrt", "db_newton") else (None, None)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     clocks = ClockSampler(local)
     clocks.start()                      # sampled from the timed region to the end of the GPU passes
-    for _ in range(args.warmup):
-        solve(mats, outs)
-    torch.cuda.synchronize()
-
-    # ---- timed region: K steps, L2 flushed before each (outside the events)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
     clocks.mark()
-    rep = None
-    for s in range(args.steps):
-        flush_l2(flush)
-        ev[s][0].record(stream)
-        res = solve(mats, outs)
-        ev[s][1].record(stream)
-        rep = res[-1]
-    torch.cuda.synchronize()
-    ms = sum(a.elapsed_time(b) for a, b in ev)
-    launches_per_step = h.launch_count()
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    r = single_gpu(P, name, shapes, mats_np, opts, kind, dev, args.steps, args.warmup, flush, clocks)
+    t = torch.tensor([r["ms"], r["e2e_ms"]], dtype=torch.float64, device=dev)
     if world > 1:
         dist.barrier()
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    ms_step = ms_max / args.steps
+    ms_max, e_ms = float(t[0]), float(t[1])
+    B = r["runner"].B
     value = world * B * args.steps / (ms_max / 1e3)
-
-    iters = rep["iters"].cpu().tolist()
-    status = rep["status"].cpu().tolist()
-    if kind == "polar":
-        f_iter = [P.polar_flops_per_iter(m, n, opts["degree"], opts["sketch_size"]) for (m, n) in shapes]
-    elif kind == "chebyshev":
-        # A'X (residual), R.R, X.P (general products) + 3 chain passes
-        f_iter = [6.0 * m ** 3 + 6.0 * m * m * opts["sketch_size"] for (m, _) in shapes]
-    elif kind == "inv_root":
-        # X + aX.R, M + P_q.M, the POLY products of P_q (1 for q = 2, 2 for q = 3, 4), chain
-        npoly = {1: 0, 2: 1, 3: 2, 4: 2}[opts["q"]]
-        f_iter = [(4.0 + 2.0 * npoly) * m ** 3 + 2.0 * (opts["q"] + 1) * m * m * opts["sketch_size"]
-                  for (m, _) in shapes]
-    elif kind == "db_newton":
-        # Gauss-Jordan sweep M -> -M^{-1} (2 n^3), X.W and Y.W (4 n^3)
-        f_iter = [6.0 * m ** 3 for (m, _) in shapes]
-    elif kind == "sign":
-        # general (non-symmetric-kernel) products: X.X, R.R (d = 2), X.P, plus the sketch
-        f_iter = [4.0 * m ** 3 + ((2.0 * m ** 3 + 14.0 * m * m * opts["sketch_size"]) if opts["degree"] == 5
-                                  else 6.0 * m * m * opts["sketch_size"]) for (m, _) in shapes]
-    else:
-        f_iter = [P.sqrt_flops_per_iter(m, opts["degree"], opts["sketch_size"]) for (m, _) in shapes]
-    flops_step = sum(f * k for f, k in zip(f_iter, iters))
-    tflops = world * flops_step * args.steps / (ms_max / 1e3) / 1e12
-
-    # ---- e2e: pinned host inputs -> device -> solve -> host through the host-buffer C-ABI
-    # entry points (prism_polar_host / prism_sqrt_invsqrt_host): every step uploads its
-    # inputs and downloads its result inside the timed region; successive steps pipeline
-    # (upload of step s+1 and download of step s overlap the solves).  The events bracket
-    # the whole K-step sequence on the caller's stream, which waits for each download.
-    host_out = [torch.empty_like(x).pin_memory() for x in host]
-
-    def solve_host():
-        if kind == "polar":
-            return P.polar_host(host, out=host_out, matrix_ids=ids, handle=h, **opts)
-        if kind == "sign":
-            return P.sign_host(host, out=host_out, matrix_ids=ids, handle=h, **opts)
-        if kind == "chebyshev":
-            return P.chebyshev_inverse_host(host, out=host_out, matrix_ids=ids, handle=h, **opts)
-        if kind == "inv_root":
-            return P.inv_root_host(host, out=host_out, matrix_ids=ids, handle=h, **opts)
-        if kind == "db_newton":
-            return P.db_newton_host(host, matrix_ids=ids, handle=h, want_sqrt=False, **dbo)[1:]
-        return P.sqrt_invsqrt_host(host, matrix_ids=ids, handle=h, want_sqrt=False, **opts)[1:]
-
-    for _ in range(4):   # warm: every staging slot's buffers and plan
-        solve_host()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for s in range(args.steps):
-        solve_host()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    e_ms = e0.elapsed_time(e1)
-    te = torch.tensor([e_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e_value = world * B * args.steps / (float(te.item()) / 1e3)
-    nbytes = sum(x.numel() * x.element_size() for x in host)
-
-    # ---- per-kernel device timing (separate pass; CUDA events on the launching stream)
-    h.profile(True)
-    h.profile_read(reset=True)
-    for s in range(args.steps):
-        flush_l2(flush)
-        solve(mats, outs)
-    torch.cuda.synchronize()
-    prof = h.profile_read(reset=True)
-    h.profile(False)
-    clk = clocks.stop()
-    clk["window"] = "timed + e2e + profiling passes (GPU busy throughout)"
+    e_value = world * B * args.steps / (e_ms / 1e3)
+    tflops = r["tflops"] * world * r["ms"] / ms_max
+    clk_timed = clocks.window(*r["t_window"])
     peaks, peak_src = read_peaks()
-    peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1400.0)))
-    if opts["precision"] != "bf16":
-        peak = peak / 2.0 / 3.0   # tf32 = bf16 / 2 (nominal ratio), 3 MMAs per product in 3xTF32
-    if kind == "polar":
-        apply_flops = sum(2.0 * max(m, n) * min(m, n) ** 2 * k for (m, n), k in zip(shapes, iters)) * args.steps
-        gram_flops = sum(max(m, n) * min(m, n) * (min(m, n) + 1) * (k + 1) for (m, n), k in zip(shapes, iters)) * args.steps
-        sq_flops = sum(min(m, n) ** 2 * (min(m, n) + 1) * k for (m, n), k in zip(shapes, iters)) * args.steps
-    elif kind == "chebyshev":
-        apply_flops = sum(2.0 * m ** 3 * k for (m, _), k in zip(shapes, iters)) * args.steps
-        gram_flops = sum(2.0 * m ** 3 * (k + 1) for (m, _), k in zip(shapes, iters)) * args.steps
-        sq_flops = sum(2.0 * m ** 3 * k for (m, _), k in zip(shapes, iters)) * args.steps
-    elif kind == "inv_root":
-        npoly = {1: 0, 2: 1, 3: 2, 4: 2}[opts["q"]]
-        apply_flops = sum(4.0 * m ** 3 * k for (m, _), k in zip(shapes, iters)) * args.steps
-        gram_flops = 0.0   # R = I - M is elementwise (k_resid_inv)
-        sq_flops = sum(2.0 * npoly * m ** 3 * k for (m, _), k in zip(shapes, iters)) * args.steps
-    elif kind == "db_newton":
-        apply_flops = sum(4.0 * m ** 3 * k for (m, _), k in zip(shapes, iters)) * args.steps
-        gram_flops = 0.0   # M_k copied / residual formed elementwise (k_db_begin)
-        sq_flops = sum(2.0 * m ** 3 * k for (m, _), k in zip(shapes, iters)) * args.steps   # GJ sweep
-    elif kind == "sign":
-        apply_flops = sum(2.0 * m ** 3 * k for (m, _), k in zip(shapes, iters)) * args.steps
-        gram_flops = sum(2.0 * m ** 3 * (k + 1) for (m, _), k in zip(shapes, iters)) * args.steps
-        sq_flops = sum(2.0 * m ** 3 * k for (m, _), k in zip(shapes, iters)) * args.steps
-    else:
-        apply_flops = sum(4.0 * m ** 3 * k for (m, _), k in zip(shapes, iters)) * args.steps
-        gram_flops = sum(2.0 * m ** 3 * (k + 1) for (m, _), k in zip(shapes, iters)) * args.steps
-        sq_flops = sum(2.0 * m ** 3 * k for (m, _), k in zip(shapes, iters)) * args.steps
-    apply_ms = prof["apply"]["ms"]
-    achieved = apply_flops / (apply_ms / 1e3) / 1e12 if apply_ms > 0 else None
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", f"traffic_{name}.json")
-    if os.path.exists(tp):
-        try:
-            traffic = json.load(open(tp)).get("apply_dram_bytes_per_launch")
-        except Exception:
-            traffic = None
-    kernel_tflops = {k: (f / (prof[k]["ms"] / 1e3) / 1e12 if prof[k]["ms"] > 0 else None)
-                     for k, f in (("gram", gram_flops), ("square", sq_flops), ("apply", apply_flops))}
-    prof_total = sum(v["ms"] for v in prof.values())
-    shares = {k: (v["ms"] / prof_total if prof_total > 0 else None) for k, v in prof.items()}
+    peak, peak_kind, burst, sus = pick_peak(peaks, clk_timed, opts["precision"])
+    roof, kernels = roofline_of(r["prof"], kind, shapes, r["iters"], args.steps, peak, peak_kind, burst, sus, name)
+    roof["peak_source"] = peak_src + f" bf16 {peak_kind}" + ("" if opts["precision"] == "bf16" else
+                                                             " / 2 (tf32)" + (" / 3 (3xTF32)"
+                                                                              if opts["precision"] == "fp32" else ""))
 
-    # ---- CPU baseline: the oracle on a bounded sample (rank 0, N=1 only)
+    extra = None
+    if rank == 0 and world == 1 and not args.no_extra and args.workload == "gpt2":
+        extra = [extra_solve(P, "square4096", dev, flush, clocks, steps=10),
+                 extra_solve(P, "square4096_fp32", dev, flush, clocks, steps=5)]
+    clk = clocks.stop()
+    clk["window"] = "timed + e2e + profiling (+ extra) passes (GPU busy throughout)"
+    clk["timed_region"] = clk_timed
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        A = stored_inputs(mats_np, opts["precision"])
-        seen, sample = set(), []
-        for i, shp in enumerate(shapes):
-            if shp not in seen:
-                seen.add(shp)
-                sample.append(i)
-        t0 = time.perf_counter()
-        done = 0
-        oracle_iters = {}
-        while True:          # whole passes over the one-per-shape sample, ~10 s of CPU work
-            for i in sample:
-                oracle_iters[i] = int(cpu_oracle_solve(A[i], kind, opts, i).iters)
-            done += 1
-            if time.perf_counter() - t0 >= 10.0:
-                break
-        sec = time.perf_counter() - t0
-        cpu = {"value": done * len(sample) / sec, "unit": "solves/s", "cores": blas_threads(), "kind": "oracle",
-               "sample": f"{done} pass(es) x {len(sample)} of {B} matrices (one per distinct shape), "
-                         f"fp64 numpy oracle, {sec:.2f} s",
-               # iterations to tolerance, device vs the fp64 oracle on the same stored inputs
-               "iters_vs_oracle": {"matrix": sample, "device": [int(iters[i]) for i in sample],
-                                   "oracle": [oracle_iters[i] for i in sample]}}
+        cpu = cpu_baseline(kind, shapes, mats_np, opts, r["runner"].out, r["iters"])
 
     if rank == 0:
+        iters = r["iters"]
         line = {
             "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": opts["precision"],
             "data": "synthetic: seeded matrices shaped like the paper's workloads (no datasets)",
             "config": {"workload": name, "description": desc, "matrices_per_gpu": B, "solver": kind,
-                       "degree": opts.get("degree"), "q": opts.get("q"), "sketch_size": opts["sketch_size"], "tol": opts["tol"],
-                       "max_iters": opts["max_iters"], "precision": opts["precision"],
+                       "degree": opts.get("degree"), "q": opts.get("q"), "sketch_size": opts.get("sketch_size"),
+                       "tol": opts["tol"], "max_iters": opts["max_iters"], "precision": opts["precision"],
                        "l2": "flushed (256 MiB write) before every timed step, outside the events",
-                       "parallelism": f"independent batch per GPU x{world}",
-                       "e2e_path": "prism_*_host (the kind's host-buffer entry point): pinned host inputs uploaded and "
-                                   "results downloaded every step; steps pipelined (copies overlap solves)"},
+                       "parallelism": f"independent batch per GPU x{world}" if world > 1 else "single GPU",
+                       "e2e_path": "prism_*_host (the kind's host-buffer entry point): pinned host inputs uploaded "
+                                   "and results downloaded every step; steps pipelined (copies overlap solves)"},
             "tflops": tflops, "tflops_unit": "F_min (symmetric products once) per second",
-            "frac_of_peak_sustained": tflops / peak if peak else None,
+            "frac_of_peak": tflops / peak, "frac_of_peak_kind": peak_kind,
             "iterations": {"mean": sum(iters) / B, "max": max(iters), "min": min(iters),
                            "histogram": {str(k): iters.count(k) for k in sorted(set(iters))}},
-            "status_converged": sum(1 for x in status if x == 0),
+            "status_converged": sum(1 for x in r["status"] if x == 0),
             "clocks": clk,
-            "e2e": {"value": e_value, "unit": "solves/s", "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes},
-            "gpu_launches": launches_per_step * args.steps,
-            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                         "kernel": "prism_gemm_kernel apply (X + X.P), tcgen05",
-                         "peak_source": peak_src + (" bf16 sustained" if opts["precision"] == "bf16"
-                                                    else " bf16 sustained / 2 (tf32) / 3 (3xTF32)")},
-            "kernels": {"tflops": kernel_tflops, "time_share": shares,
-                        "ms_per_step": {k: v["ms"] / args.steps for k, v in prof.items()}},
+            "e2e": {"value": e_value, "unit": "solves/s", "h2d_bytes_per_step": r["e2e_bytes"],
+                    "d2h_bytes_per_step": r["e2e_bytes"]},
+            "gpu_launches": r["launches_per_step"] * args.steps,
+            "roofline": roof,
+            "kernels": kernels,
             "cpu_baseline": cpu,
+            "extra": extra,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -1,9 +1,9 @@
 """ctypes binding of libprism.so (include/prism.h).
 
-Argument marshalling only: torch is used for device memory (outputs,
-workspace, report buffers) and streams; every step of the PRISM iteration
-runs in the library's CUDA kernels.  If the library is missing the calls
-raise — there is no CPU fallback.
+Argument marshalling only: torch is used for device memory (outputs, workspace,
+report buffers), streams and the current device; every step of the PRISM
+iteration runs in the library's CUDA kernels.  If the library is missing the
+calls raise — there is no CPU fallback.
 """
 
 from __future__ import annotations
@@ -19,8 +19,6 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libprism.so")
 PRECISION = {"bf16": 0, "fp32": 1, "tf32": 2}
 FIT = {"sketched": 0, "taylor": 1}
 STATUS = {0: "converged", 1: "max_iters", 2: "diverged", 3: "nonfinite", 4: "zero_input"}
-
-c_i64p = ctypes.POINTER(ctypes.c_int64)
 
 
 class PrismError(RuntimeError):
@@ -52,22 +50,64 @@ class Report(ctypes.Structure):
     ]
 
 
-EXPORTS = [
-    "prism_default_options", "prism_create", "prism_destroy", "prism_last_error", "prism_abi_version",
-    "prism_polar_workspace", "prism_polar", "prism_sqrt_workspace", "prism_sqrt_invsqrt",
-    "prism_polar_host", "prism_sqrt_invsqrt_host", "prism_sign_workspace", "prism_sign", "prism_sign_host",
-    "prism_inv_root_workspace", "prism_inv_root", "prism_inv_root_host",
-                     "prism_chebyshev_inverse", "prism_chebyshev_inverse_host", "prism_db_newton",
-                     "prism_db_newton_host",
-    "prism_chebyshev_inverse_workspace", "prism_chebyshev_inverse", "prism_chebyshev_inverse_host",
-    "prism_db_newton_workspace", "prism_db_newton", "prism_db_newton_host",
-    "prism_lpt_partition", "prism_polar_flops_per_iter", "prism_sqrt_flops_per_iter",
-    "prism_launch_count", "prism_profile_enable", "prism_profile_read",
-    "prism_rowblock_workspace", "prism_rowblock_begin", "prism_rowblock_gram", "prism_rowblock_update",
-    "prism_rowblock_end",
-    "prism_debug_gemm", "prism_debug_sketch", "prism_debug_argmin",
-    "prism_debug_trace_gemm", "prism_debug_trace_chain",
-]
+# ---------------------------------------------------------------- signatures
+_vp, _i32, _i64, _dbl, _u64, _sz = (ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double,
+                                    ctypes.c_uint64, ctypes.c_size_t)
+_i64p = ctypes.POINTER(ctypes.c_int64)
+_vpp = ctypes.POINTER(ctypes.c_void_p)
+_opt = ctypes.POINTER(Options)
+_rep = ctypes.POINTER(Report)
+_ST = ctypes.c_int   # prism_status
+
+# name -> (restype, argtypes); EXPORTS is exactly the symbol set include/prism.h declares
+_SIGS = {
+    "prism_default_options": (None, [_opt]),
+    "prism_create": (_ST, [ctypes.POINTER(_vp)]),
+    "prism_destroy": (_ST, [_vp]),
+    "prism_last_error": (ctypes.c_char_p, []),
+    "prism_abi_version": (_i32, []),
+    # device-buffer solves and their workspace queries
+    "prism_polar_workspace": (_sz, [_vp, _i32, _i64p, _i64p, _opt]),
+    "prism_polar": (_ST, [_vp, _i32, _i64p, _i64p, _vpp, _i64p, _vpp, _i64p, _i64p, _opt, _rep, _vp, _sz, _vp]),
+    "prism_sqrt_workspace": (_sz, [_vp, _i32, _i64p, _opt]),
+    "prism_sqrt_invsqrt": (_ST, [_vp, _i32, _i64p, _vpp, _i64p, _vpp, _vpp, _i64p, _i64p, _opt, _rep, _vp, _sz,
+                                 _vp]),
+    "prism_sign_workspace": (_sz, [_vp, _i32, _i64p, _opt]),
+    "prism_sign": (_ST, [_vp, _i32, _i64p, _vpp, _i64p, _vpp, _i64p, _i64p, _opt, _rep, _vp, _sz, _vp]),
+    "prism_inv_root_workspace": (_sz, [_vp, _i32, _i64p, _i32, _opt]),
+    "prism_inv_root": (_ST, [_vp, _i32, _i64p, _i32, _vpp, _i64p, _vpp, _i64p, _i64p, _opt, _rep, _vp, _sz, _vp]),
+    "prism_chebyshev_inverse_workspace": (_sz, [_vp, _i32, _i64p, _opt]),
+    "prism_chebyshev_inverse": (_ST, [_vp, _i32, _i64p, _vpp, _i64p, _vpp, _i64p, _i64p, _opt, _rep, _vp, _sz,
+                                      _vp]),
+    "prism_db_newton_workspace": (_sz, [_vp, _i32, _i64p, _opt]),
+    "prism_db_newton": (_ST, [_vp, _i32, _i64p, _vpp, _i64p, _vpp, _vpp, _i64p, _i64p, _opt, _rep, _vp, _sz, _vp]),
+    # host-buffer (end-to-end) forms
+    "prism_polar_host": (_ST, [_vp, _i32, _i64p, _i64p, _vpp, _i64p, _vpp, _i64p, _i64p, _opt, _rep, _vp]),
+    "prism_sqrt_invsqrt_host": (_ST, [_vp, _i32, _i64p, _vpp, _i64p, _vpp, _vpp, _i64p, _i64p, _opt, _rep, _vp]),
+    "prism_sign_host": (_ST, [_vp, _i32, _i64p, _vpp, _i64p, _vpp, _i64p, _i64p, _opt, _rep, _vp]),
+    "prism_inv_root_host": (_ST, [_vp, _i32, _i64p, _i32, _vpp, _i64p, _vpp, _i64p, _i64p, _opt, _rep, _vp]),
+    "prism_chebyshev_inverse_host": (_ST, [_vp, _i32, _i64p, _vpp, _i64p, _vpp, _i64p, _i64p, _opt, _rep, _vp]),
+    "prism_db_newton_host": (_ST, [_vp, _i32, _i64p, _vpp, _i64p, _vpp, _vpp, _i64p, _i64p, _opt, _rep, _vp]),
+    # multi-GPU
+    "prism_lpt_partition": (_ST, [_i32, ctypes.POINTER(_dbl), _i32, ctypes.POINTER(ctypes.c_int32)]),
+    "prism_rowblock_workspace": (_sz, [_vp, _i64, _i64, _opt]),
+    "prism_rowblock_begin": (_ST, [_vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _opt, _vp, _sz, _vp]),
+    "prism_rowblock_gram": (_ST, [_vp, _i32, _vp, _vp]),
+    "prism_rowblock_update": (_ST, [_vp, _i32, _vp, _vp, _vp]),
+    "prism_rowblock_end": (_ST, [_vp, _rep, _vp]),
+    # measurement
+    "prism_polar_flops_per_iter": (_dbl, [_i64, _i64, _i32, _i32]),
+    "prism_sqrt_flops_per_iter": (_dbl, [_i64, _i32, _i32]),
+    "prism_launch_count": (_i64, [_vp]),
+    "prism_profile_enable": (_ST, [_vp, _i32]),
+    "prism_profile_read": (_ST, [_vp, ctypes.POINTER(_dbl), ctypes.POINTER(_i64), _i32]),
+    # test hooks
+    "prism_debug_gemm": (_ST, [_vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _i64, _vp, _vp, _i64, _vp,
+                               _vp, _i64, _vp, _vp, _i64, _vp, ctypes.c_float, _i32, _vp, _vp, _vp, _sz, _vp]),
+    "prism_debug_sketch": (_ST, [_u64, _i64, _i32, _i32, _i32, _vp, _vp]),
+    "prism_debug_argmin": (_ST, [_i32, _vp, _dbl, _dbl, _dbl, _vp, _vp]),
+}
+EXPORTS = sorted(_SIGS)
 
 _lib = None
 _lock = threading.Lock()
@@ -84,82 +124,10 @@ def lib():
         if not os.path.exists(LIB_PATH):
             raise PrismError(f"{LIB_PATH} not built (run `python build.py`); no CPU fallback exists")
         L = ctypes.CDLL(LIB_PATH)
-        vp, i32, i64, dbl, u64, sz = (ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double,
-                                      ctypes.c_uint64, ctypes.c_size_t)
-        L.prism_default_options.argtypes = [ctypes.POINTER(Options)]
-        L.prism_default_options.restype = None
-        L.prism_create.argtypes = [ctypes.POINTER(vp)]
-        L.prism_destroy.argtypes = [vp]
-        L.prism_last_error.restype = ctypes.c_char_p
-        L.prism_abi_version.restype = i32
-        L.prism_polar_workspace.argtypes = [vp, i32, c_i64p, c_i64p, ctypes.POINTER(Options)]
-        L.prism_polar_workspace.restype = sz
-        L.prism_polar.argtypes = [vp, i32, c_i64p, c_i64p, ctypes.POINTER(vp), c_i64p, ctypes.POINTER(vp), c_i64p,
-                                  c_i64p, ctypes.POINTER(Options), ctypes.POINTER(Report), vp, sz, vp]
-        L.prism_polar_host.argtypes = [vp, i32, c_i64p, c_i64p, ctypes.POINTER(vp), c_i64p, ctypes.POINTER(vp),
-                                       c_i64p, c_i64p, ctypes.POINTER(Options), ctypes.POINTER(Report), vp]
-        L.prism_sqrt_invsqrt_host.argtypes = [vp, i32, c_i64p, ctypes.POINTER(vp), c_i64p, ctypes.POINTER(vp),
-                                              ctypes.POINTER(vp), c_i64p, c_i64p, ctypes.POINTER(Options),
-                                              ctypes.POINTER(Report), vp]
-        L.prism_sqrt_workspace.argtypes = [vp, i32, c_i64p, ctypes.POINTER(Options)]
-        L.prism_sqrt_workspace.restype = sz
-        L.prism_sqrt_invsqrt.argtypes = [vp, i32, c_i64p, ctypes.POINTER(vp), c_i64p, ctypes.POINTER(vp),
-                                         ctypes.POINTER(vp), c_i64p, c_i64p, ctypes.POINTER(Options),
-                                         ctypes.POINTER(Report), vp, sz, vp]
-        L.prism_sign_workspace.argtypes = [vp, i32, c_i64p, ctypes.POINTER(Options)]
-        L.prism_sign_workspace.restype = sz
-        L.prism_sign.argtypes = [vp, i32, c_i64p, ctypes.POINTER(vp), c_i64p, ctypes.POINTER(vp), c_i64p, c_i64p,
-                                 ctypes.POINTER(Options), ctypes.POINTER(Report), vp, sz, vp]
-        L.prism_sign_host.argtypes = [vp, i32, c_i64p, ctypes.POINTER(vp), c_i64p, ctypes.POINTER(vp), c_i64p,
-                                      c_i64p, ctypes.POINTER(Options), ctypes.POINTER(Report), vp]
-        L.prism_inv_root_workspace.argtypes = [vp, i32, c_i64p, i32, ctypes.POINTER(Options)]
-        L.prism_inv_root_workspace.restype = sz
-        L.prism_inv_root.argtypes = [vp, i32, c_i64p, i32, ctypes.POINTER(vp), c_i64p, ctypes.POINTER(vp), c_i64p,
-                                     c_i64p, ctypes.POINTER(Options), ctypes.POINTER(Report), vp, sz, vp]
-        L.prism_inv_root_host.argtypes = [vp, i32, c_i64p, i32, ctypes.POINTER(vp), c_i64p, ctypes.POINTER(vp),
-                                          c_i64p, c_i64p, ctypes.POINTER(Options), ctypes.POINTER(Report), vp]
-        L.prism_chebyshev_inverse_workspace.argtypes = [vp, i32, c_i64p, ctypes.POINTER(Options)]
-        L.prism_chebyshev_inverse_workspace.restype = sz
-        L.prism_chebyshev_inverse.argtypes = [vp, i32, c_i64p, ctypes.POINTER(vp), c_i64p, ctypes.POINTER(vp), c_i64p,
-                                              c_i64p, ctypes.POINTER(Options), ctypes.POINTER(Report), vp, sz, vp]
-        L.prism_chebyshev_inverse_host.argtypes = [vp, i32, c_i64p, ctypes.POINTER(vp), c_i64p, ctypes.POINTER(vp),
-                                                   c_i64p, c_i64p, ctypes.POINTER(Options), ctypes.POINTER(Report),
-                                                   vp]
-        L.prism_db_newton_workspace.argtypes = [vp, i32, c_i64p, ctypes.POINTER(Options)]
-        L.prism_db_newton_workspace.restype = sz
-        L.prism_db_newton.argtypes = [vp, i32, c_i64p, ctypes.POINTER(vp), c_i64p, ctypes.POINTER(vp),
-                                      ctypes.POINTER(vp), c_i64p, c_i64p, ctypes.POINTER(Options),
-                                      ctypes.POINTER(Report), vp, sz, vp]
-        L.prism_db_newton_host.argtypes = [vp, i32, c_i64p, ctypes.POINTER(vp), c_i64p, ctypes.POINTER(vp),
-                                           ctypes.POINTER(vp), c_i64p, c_i64p, ctypes.POINTER(Options),
-                                           ctypes.POINTER(Report), vp]
-        L.prism_lpt_partition.argtypes = [i32, ctypes.POINTER(dbl), i32, ctypes.POINTER(ctypes.c_int32)]
-        L.prism_polar_flops_per_iter.argtypes = [i64, i64, i32, i32]
-        L.prism_polar_flops_per_iter.restype = dbl
-        L.prism_sqrt_flops_per_iter.argtypes = [i64, i32, i32]
-        L.prism_sqrt_flops_per_iter.restype = dbl
-        L.prism_debug_gemm.argtypes = [vp, i32, i32, i32, i32, i32, i32, i32, vp, vp, i64, vp, vp, i64, vp, vp, i64,
-                                       vp, vp, i64, vp, ctypes.c_float, i32, vp, vp, vp, sz, vp]
-        L.prism_launch_count.argtypes = [vp]
-        L.prism_launch_count.restype = i64
-        L.prism_profile_enable.argtypes = [vp, i32]
-        L.prism_profile_read.argtypes = [vp, ctypes.POINTER(dbl), ctypes.POINTER(i64), i32]
-        L.prism_rowblock_workspace.argtypes = [vp, i64, i64, ctypes.POINTER(Options)]
-        L.prism_rowblock_workspace.restype = sz
-        L.prism_rowblock_begin.argtypes = [vp, i64, i64, vp, i64, vp, i64, vp, vp, ctypes.POINTER(Options), vp, sz, vp]
-        L.prism_rowblock_gram.argtypes = [vp, i32, vp, vp]
-        L.prism_rowblock_update.argtypes = [vp, i32, vp, vp, vp]
-        L.prism_rowblock_end.argtypes = [vp, ctypes.POINTER(Report), vp]
-        L.prism_debug_sketch.argtypes = [u64, i64, i32, i32, i32, vp, vp]
-        L.prism_debug_argmin.argtypes = [i32, vp, dbl, dbl, dbl, vp, vp]
-        L.prism_debug_trace_gemm.argtypes = [vp, i32]
-        L.prism_debug_trace_chain.argtypes = [vp]
-        for name in ("prism_create", "prism_destroy", "prism_polar", "prism_sqrt_invsqrt", "prism_lpt_partition",
-                     "prism_polar_host", "prism_sqrt_invsqrt_host", "prism_sign", "prism_sign_host", "prism_inv_root", "prism_inv_root_host",
-                     "prism_debug_gemm", "prism_debug_sketch", "prism_debug_argmin",
-                     "prism_debug_trace_gemm", "prism_debug_trace_chain", "prism_profile_enable", "prism_profile_read", "prism_rowblock_begin",
-                     "prism_rowblock_gram", "prism_rowblock_update", "prism_rowblock_end"):
-            getattr(L, name).restype = i32
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
         _lib = L
         return L
 
@@ -179,7 +147,11 @@ def _ptrs(ts):
 
 
 class Handle:
-    """A prism_handle plus a reusable device workspace (per device)."""
+    """A prism_handle plus reusable device workspaces, one per (device, stream): solves
+    queued on different streams never share a workspace.  A handle is used by one host
+    thread at a time (include/prism.h)."""
+
+    KINDS = ("gram", "square", "apply", "sketch_chain", "alpha", "norm_final")
 
     def __init__(self):
         h = ctypes.c_void_p()
@@ -194,8 +166,6 @@ class Handle:
         except Exception:
             pass
 
-    KINDS = ("gram", "square", "apply", "sketch_chain", "alpha", "norm_final")
-
     def launch_count(self) -> int:
         """Kernel launches issued by the last solve on this handle."""
         return int(lib().prism_launch_count(self.h))
@@ -209,9 +179,9 @@ class Handle:
         check(lib().prism_profile_read(self.h, ms, nl, 1 if reset else 0), "prism_profile_read")
         return {k: {"ms": ms[i], "launches": nl[i]} for i, k in enumerate(self.KINDS)}
 
-    def workspace(self, nbytes: int, device):
+    def workspace(self, nbytes: int, device, stream=None):
         import torch
-        key = str(device)
+        key = (str(device), int(stream.cuda_stream) if stream is not None else 0)
         ws = self._ws.get(key)
         if ws is None or ws.numel() < nbytes:
             ws = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
@@ -260,6 +230,8 @@ def _check_dtype(ts, precision, on_host=False):
     for t in ts:
         if t.dtype != want or t.is_cuda == on_host or t.dim() != 2 or t.stride(1) != 1:
             raise PrismError(f"inputs must be 2-D {where} {want} tensors with unit column stride")
+        if on_host and not t.is_pinned():
+            raise PrismError("host-path tensors must be pinned CPU tensors (tensor.pin_memory())")
 
 
 def _report_buffers(batch, max_iters, device):
@@ -275,123 +247,12 @@ def _report_buffers(batch, max_iters, device):
 
 def _report_struct(rb):
     r = Report()
-    r.iters = rb["iters"].data_ptr()
-    r.resid = rb["resid"].data_ptr()
-    r.status = rb["status"].data_ptr()
-    r.alphas = rb["alphas"].data_ptr()
-    r.resid_hist = rb["resid_hist"].data_ptr()
+    for k in ("iters", "resid", "status", "alphas", "resid_hist"):
+        setattr(r, k, rb[k].data_ptr())
     return r
 
 
-def polar(mats, degree=5, max_iters=30, sketch_size=8, tol=1e-6, seed=42, precision=None, fit="sketched",
-          warmup_iters=0, alpha_lo=None, alpha_hi=None, out=None, matrix_ids=None, stream=None, handle=None):
-    """Polar factors of a batch of CUDA matrices via prism_polar.
-
-    Returns (outputs, report) where report holds device tensors iters, resid,
-    status, alphas [batch, max_iters], resid_hist [batch, max_iters+1].
-    Asynchronous on `stream` (default: torch's current stream).
-    """
-    import torch
-    mats = list(mats)
-    if not mats:
-        return [], {}
-    precision = _precision_of(mats[0], precision)
-    _check_dtype(mats, precision)
-    dev = mats[0].device
-    h = handle or default_handle()
-    o = make_options(degree, max_iters, sketch_size, tol, seed, precision, fit, warmup_iters, alpha_lo, alpha_hi)
-    B = len(mats)
-    m = _i64([t.shape[0] for t in mats])
-    n = _i64([t.shape[1] for t in mats])
-    if out is None:
-        out = [torch.empty_like(t) for t in mats]
-    _check_dtype(out, precision)
-    need = lib().prism_polar_workspace(h.h, B, m, n, ctypes.byref(o))
-    if need == 0:
-        raise PrismError("prism_polar_workspace rejected the arguments: " + lib().prism_last_error().decode())
-    ws = h.workspace(need, dev)
-    rb = _report_buffers(B, max_iters, dev)
-    rep = _report_struct(rb)
-    ids = _i64(matrix_ids) if matrix_ids is not None else None
-    st = stream if stream is not None else torch.cuda.current_stream(dev)
-    check(lib().prism_polar(h.h, B, m, n, _ptrs(mats), _i64([t.stride(0) for t in mats]), _ptrs(out),
-                            _i64([t.stride(0) for t in out]), ids, ctypes.byref(o), ctypes.byref(rep),
-                            ws.data_ptr(), ws.numel(), ctypes.c_void_p(st.cuda_stream)), "prism_polar")
-    return out, rb
-
-
-def _check_pinned(ts, what):
-    for t in ts:
-        if t.device.type != "cpu" or not t.is_pinned():
-            raise PrismError(f"{what}: host-path tensors must be pinned CPU tensors (tensor.pin_memory())")
-
-
-def polar_host(mats, degree=5, max_iters=30, sketch_size=8, tol=1e-6, seed=42, precision=None, fit="sketched",
-               warmup_iters=0, alpha_lo=None, alpha_hi=None, out=None, matrix_ids=None, stream=None, handle=None,
-               device=None):
-    """Polar factors of pinned HOST matrices via prism_polar_host (end-to-end path).
-
-    Uploads, solves and downloads on the handle's internal streams; returns
-    (outputs, report) immediately — outputs (pinned host tensors) and the device
-    report are valid once `stream` (default: the current stream of `device`)
-    reaches this call.  Successive calls on one handle overlap copies with solves.
-    """
-    import torch
-    mats = list(mats)
-    if not mats:
-        return [], {}
-    _check_pinned(mats, "polar_host")
-    precision = _precision_of(mats[0], precision)
-    _check_dtype(mats, precision, on_host=True)
-    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
-    h = handle or default_handle()
-    o = make_options(degree, max_iters, sketch_size, tol, seed, precision, fit, warmup_iters, alpha_lo, alpha_hi)
-    B = len(mats)
-    if out is None:
-        out = [torch.empty_like(t).pin_memory() for t in mats]
-    _check_pinned(out, "polar_host")
-    _check_dtype(out, precision, on_host=True)
-    rb = _report_buffers(B, max_iters, dev)
-    rep = _report_struct(rb)
-    ids = _i64(matrix_ids) if matrix_ids is not None else None
-    st = stream if stream is not None else torch.cuda.current_stream(dev)
-    check(lib().prism_polar_host(h.h, B, _i64([t.shape[0] for t in mats]), _i64([t.shape[1] for t in mats]),
-                                 _ptrs(mats), _i64([t.stride(0) for t in mats]), _ptrs(out),
-                                 _i64([t.stride(0) for t in out]), ids, ctypes.byref(o), ctypes.byref(rep),
-                                 ctypes.c_void_p(st.cuda_stream)), "prism_polar_host")
-    return out, rb
-
-
-def sqrt_invsqrt_host(mats, degree=5, max_iters=30, sketch_size=8, tol=1e-6, seed=42, precision=None,
-                      fit="sketched", warmup_iters=0, alpha_lo=None, alpha_hi=None, want_sqrt=True,
-                      want_invsqrt=True, matrix_ids=None, stream=None, handle=None, device=None):
-    """A^{1/2}, A^{-1/2} of pinned HOST SPD matrices via prism_sqrt_invsqrt_host."""
-    import torch
-    mats = list(mats)
-    if not mats:
-        return [], [], {}
-    _check_pinned(mats, "sqrt_invsqrt_host")
-    precision = _precision_of(mats[0], precision)
-    _check_dtype(mats, precision, on_host=True)
-    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
-    h = handle or default_handle()
-    o = make_options(degree, max_iters, sketch_size, tol, seed, precision, fit, warmup_iters, alpha_lo, alpha_hi)
-    B = len(mats)
-    sq = [torch.empty_like(t).pin_memory() for t in mats] if want_sqrt else None
-    isq = [torch.empty_like(t).pin_memory() for t in mats] if want_invsqrt else None
-    rb = _report_buffers(B, max_iters, dev)
-    rep = _report_struct(rb)
-    ids = _i64(matrix_ids) if matrix_ids is not None else None
-    st = stream if stream is not None else torch.cuda.current_stream(dev)
-    check(lib().prism_sqrt_invsqrt_host(h.h, B, _i64([t.shape[0] for t in mats]), _ptrs(mats),
-                                        _i64([t.stride(0) for t in mats]), _ptrs(sq) if sq else None,
-                                        _ptrs(isq) if isq else None, _i64([t.shape[1] for t in mats]), ids,
-                                        ctypes.byref(o), ctypes.byref(rep), ctypes.c_void_p(st.cuda_stream)),
-          "prism_sqrt_invsqrt_host")
-    return sq, isq, rb
-
-
-def _outputs(mats, want, given, what):
+def _outputs(mats, want, given, what, host):
     """Output matrices: the caller's (same shape / dtype / device as the inputs, unit column
     stride) or fresh ones.  Reusing the same output buffers across calls keeps the handle's
     plan (keyed by every pointer it bakes into its tables) and its CUDA graph warm."""
@@ -399,319 +260,167 @@ def _outputs(mats, want, given, what):
     if not want:
         return None
     if given is None:
-        return [torch.empty_like(t) for t in mats]
+        return [torch.empty_like(t).pin_memory() if host else torch.empty_like(t) for t in mats]
     given = list(given)
     if len(given) != len(mats):
         raise PrismError(f"{what}: {len(given)} outputs for {len(mats)} matrices")
     for g, t in zip(given, mats):
         if g.shape != t.shape or g.dtype != t.dtype or g.device != t.device or g.stride(1) != 1:
             raise PrismError(f"{what}: each output must match its input's shape, dtype and device, rows contiguous")
+        if host and not g.is_pinned():
+            raise PrismError(f"{what}: host-path outputs must be pinned")
     return given
 
 
-def _ld_out(sq, isq, mats, what):
-    a = sq if sq is not None else isq
+def _ld_out(o1, o2, mats, what):
+    a = o1 if o1 is not None else o2
     if a is None:
         return _i64([t.shape[1] for t in mats])
-    if sq is not None and isq is not None and any(x.stride(0) != y.stride(0) for x, y in zip(sq, isq)):
+    if o1 is not None and o2 is not None and any(x.stride(0) != y.stride(0) for x, y in zip(o1, o2)):
         raise PrismError(f"{what}: the two outputs of a matrix must share one row stride")
     return _i64([t.stride(0) for t in a])
 
 
-def sqrt_invsqrt(mats, degree=5, max_iters=30, sketch_size=8, tol=1e-6, seed=42, precision=None, fit="sketched",
-                 warmup_iters=0, alpha_lo=None, alpha_hi=None, want_sqrt=True, want_invsqrt=True, matrix_ids=None,
-                 stream=None, handle=None, out_sqrt=None, out_invsqrt=None):
-    """A^{1/2}, A^{-1/2} of a batch of SPD CUDA matrices via prism_sqrt_invsqrt (outputs into
-    out_sqrt / out_invsqrt when given)."""
+# kind -> (C entry point, workspace query, shape args: "mn" (m, n arrays), "n" or "nq")
+_KINDS = {
+    "polar": ("prism_polar", "prism_polar_workspace", "mn", 1),
+    "sign": ("prism_sign", "prism_sign_workspace", "n", 1),
+    "inv_root": ("prism_inv_root", "prism_inv_root_workspace", "nq", 1),
+    "chebyshev": ("prism_chebyshev_inverse", "prism_chebyshev_inverse_workspace", "n", 1),
+    "sqrt": ("prism_sqrt_invsqrt", "prism_sqrt_workspace", "n", 2),
+    "db_newton": ("prism_db_newton", "prism_db_newton_workspace", "n", 2),
+}
+
+
+def _solve(kind, mats, *, host=False, q=0, degree=5, max_iters=30, sketch_size=8, tol=1e-6, seed=42,
+           precision=None, fit="sketched", warmup_iters=0, alpha_lo=None, alpha_hi=None, out=None, out2=None,
+           want1=True, want2=True, matrix_ids=None, stream=None, handle=None, device=None):
+    """One library call: marshal the batch, outputs, options, report and workspace, call the
+    C entry point of `kind` on the right device and stream, return (out, out2, report)."""
     import torch
+    fn, fn_ws, shape, nout = _KINDS[kind]
     mats = list(mats)
     if not mats:
-        return [], [], {}
+        return [], ([] if nout == 2 else None), {}
     precision = _precision_of(mats[0], precision)
-    _check_dtype(mats, precision)
-    dev = mats[0].device
+    _check_dtype(mats, precision, on_host=host)
+    if shape != "mn" and any(t.shape[0] != t.shape[1] for t in mats):
+        raise PrismError(f"{kind}: matrices must be square")
+    if host:
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    else:
+        dev = mats[0].device
+        if any(t.device != dev for t in mats):
+            raise PrismError(f"{kind}: all matrices must be on one device")
     h = handle or default_handle()
     o = make_options(degree, max_iters, sketch_size, tol, seed, precision, fit, warmup_iters, alpha_lo, alpha_hi)
     B = len(mats)
-    n = _i64([t.shape[0] for t in mats])
-    sq = _outputs(mats, want_sqrt, out_sqrt, "sqrt_invsqrt")
-    isq = _outputs(mats, want_invsqrt, out_invsqrt, "sqrt_invsqrt")
-    ld_out = _ld_out(sq, isq, mats, "sqrt_invsqrt")
-    need = lib().prism_sqrt_workspace(h.h, B, n, ctypes.byref(o))
-    if need == 0:
-        raise PrismError("prism_sqrt_workspace rejected the arguments: " + lib().prism_last_error().decode())
-    ws = h.workspace(need, dev)
-    rb = _report_buffers(B, max_iters, dev)
-    rep = _report_struct(rb)
+    m = _i64([t.shape[0] for t in mats])
+    n = _i64([t.shape[1] for t in mats])
+    o1 = _outputs(mats, want1, out, kind, host)
+    o2 = _outputs(mats, want2, out2, kind, host) if nout == 2 else None
     ids = _i64(matrix_ids) if matrix_ids is not None else None
-    st = stream if stream is not None else torch.cuda.current_stream(dev)
-    check(lib().prism_sqrt_invsqrt(h.h, B, n, _ptrs(mats), _i64([t.stride(0) for t in mats]),
-                                   _ptrs(sq) if sq else None, _ptrs(isq) if isq else None, ld_out, ids,
-                                   ctypes.byref(o), ctypes.byref(rep), ws.data_ptr(), ws.numel(),
-                                   ctypes.c_void_p(st.cuda_stream)), "prism_sqrt_invsqrt")
-    return sq, isq, rb
+    L = lib()
+    with torch.cuda.device(dev):
+        st = stream if stream is not None else torch.cuda.current_stream(dev)
+        rb = _report_buffers(B, max_iters, dev)
+        rep = _report_struct(rb)
+        args = [h.h, B, m] + ([n] if shape == "mn" else []) + ([int(q)] if shape == "nq" else [])
+        args += [_ptrs(mats), _i64([t.stride(0) for t in mats])]
+        if nout == 1:
+            args += [_ptrs(o1), _i64([t.stride(0) for t in o1])]
+        else:
+            args += [_ptrs(o1) if o1 else None, _ptrs(o2) if o2 else None, _ld_out(o1, o2, mats, kind)]
+        args += [ids, ctypes.byref(o), ctypes.byref(rep)]
+        if host:
+            check(getattr(L, fn + "_host")(*args, ctypes.c_void_p(st.cuda_stream)), fn + "_host")
+        else:
+            wargs = [h.h, B, m] + ([n] if shape == "mn" else []) + ([int(q)] if shape == "nq" else [])
+            need = getattr(L, fn_ws)(*wargs, ctypes.byref(o))
+            if need == 0:
+                raise PrismError(f"{fn_ws} rejected the arguments: " + L.prism_last_error().decode())
+            ws = h.workspace(need, dev, st)
+            check(getattr(L, fn)(*args, ws.data_ptr(), ws.numel(), ctypes.c_void_p(st.cuda_stream)), fn)
+    return o1, o2, rb
 
 
-def sign(mats, degree=5, max_iters=30, sketch_size=8, tol=1e-6, seed=42, precision=None, fit="sketched",
-         warmup_iters=0, alpha_lo=None, alpha_hi=None, out=None, matrix_ids=None, stream=None, handle=None):
-    """Matrix signs of a batch of square CUDA matrices via prism_sign."""
-    import torch
-    mats = list(mats)
-    if not mats:
-        return [], {}
-    precision = _precision_of(mats[0], precision)
-    _check_dtype(mats, precision)
-    for t in mats:
-        if t.shape[0] != t.shape[1]:
-            raise PrismError("sign: matrices must be square")
-    dev = mats[0].device
-    h = handle or default_handle()
-    o = make_options(degree, max_iters, sketch_size, tol, seed, precision, fit, warmup_iters, alpha_lo, alpha_hi)
-    B = len(mats)
-    n = _i64([t.shape[0] for t in mats])
-    if out is None:
-        out = [torch.empty_like(t) for t in mats]
-    _check_dtype(out, precision)
-    need = lib().prism_sign_workspace(h.h, B, n, ctypes.byref(o))
-    if need == 0:
-        raise PrismError("prism_sign_workspace rejected the arguments: " + lib().prism_last_error().decode())
-    ws = h.workspace(need, dev)
-    rb = _report_buffers(B, max_iters, dev)
-    rep = _report_struct(rb)
-    ids = _i64(matrix_ids) if matrix_ids is not None else None
-    st = stream if stream is not None else torch.cuda.current_stream(dev)
-    check(lib().prism_sign(h.h, B, n, _ptrs(mats), _i64([t.stride(0) for t in mats]), _ptrs(out),
-                           _i64([t.stride(0) for t in out]), ids, ctypes.byref(o), ctypes.byref(rep),
-                           ws.data_ptr(), ws.numel(), ctypes.c_void_p(st.cuda_stream)), "prism_sign")
-    return out, rb
+# ---------------------------------------------------------------- public API
+# Device forms take CUDA tensors and return device outputs plus a device report (iters,
+# resid, status, alphas [batch, max_iters], resid_hist [batch, max_iters + 1]); they are
+# asynchronous on `stream` (default: the current stream of the inputs' device).  Host forms
+# (*_host) take pinned CPU tensors and run the library's pipelined upload / solve / download
+# path (prism_*_host); their outputs are valid once `stream` reaches the call.
+
+def polar(mats, out=None, **kw):
+    """Polar factors U V^T via prism_polar -> (outputs, report)."""
+    o1, _, rb = _solve("polar", mats, out=out, **kw)
+    return o1, rb
 
 
-def sign_host(mats, degree=5, max_iters=30, sketch_size=8, tol=1e-6, seed=42, precision=None, fit="sketched",
-              warmup_iters=0, alpha_lo=None, alpha_hi=None, out=None, matrix_ids=None, stream=None, handle=None,
-              device=None):
-    """Matrix signs of pinned HOST square matrices via prism_sign_host (as polar_host)."""
-    import torch
-    mats = list(mats)
-    if not mats:
-        return [], {}
-    _check_pinned(mats, "sign_host")
-    precision = _precision_of(mats[0], precision)
-    _check_dtype(mats, precision, on_host=True)
-    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
-    h = handle or default_handle()
-    o = make_options(degree, max_iters, sketch_size, tol, seed, precision, fit, warmup_iters, alpha_lo, alpha_hi)
-    B = len(mats)
-    if out is None:
-        out = [torch.empty_like(t).pin_memory() for t in mats]
-    _check_pinned(out, "sign_host")
-    _check_dtype(out, precision, on_host=True)
-    rb = _report_buffers(B, max_iters, dev)
-    rep = _report_struct(rb)
-    ids = _i64(matrix_ids) if matrix_ids is not None else None
-    st = stream if stream is not None else torch.cuda.current_stream(dev)
-    check(lib().prism_sign_host(h.h, B, _i64([t.shape[0] for t in mats]), _ptrs(mats),
-                                _i64([t.stride(0) for t in mats]), _ptrs(out), _i64([t.stride(0) for t in out]), ids,
-                                ctypes.byref(o), ctypes.byref(rep), ctypes.c_void_p(st.cuda_stream)),
-          "prism_sign_host")
-    return out, rb
+def polar_host(mats, out=None, **kw):
+    o1, _, rb = _solve("polar", mats, host=True, out=out, **kw)
+    return o1, rb
 
 
-def inv_root(mats, q=4, max_iters=30, sketch_size=8, tol=1e-6, seed=42, precision=None, fit="sketched",
-             warmup_iters=0, alpha_lo=None, alpha_hi=None, out=None, matrix_ids=None, stream=None, handle=None):
-    """A^{-1/q} of a batch of SPD CUDA matrices via prism_inv_root (coupled inverse
-    Newton, P:549-566; q in 1..4)."""
-    import torch
-    mats = list(mats)
-    if not mats:
-        return [], {}
-    precision = _precision_of(mats[0], precision)
-    _check_dtype(mats, precision)
-    for t in mats:
-        if t.shape[0] != t.shape[1]:
-            raise PrismError("inv_root: matrices must be square")
-    dev = mats[0].device
-    h = handle or default_handle()
-    o = make_options(5, max_iters, sketch_size, tol, seed, precision, fit, warmup_iters, alpha_lo, alpha_hi)
-    B = len(mats)
-    n = _i64([t.shape[0] for t in mats])
-    if out is None:
-        out = [torch.empty_like(t) for t in mats]
-    _check_dtype(out, precision)
-    need = lib().prism_inv_root_workspace(h.h, B, n, int(q), ctypes.byref(o))
-    if need == 0:
-        raise PrismError("prism_inv_root_workspace rejected the arguments: " + lib().prism_last_error().decode())
-    ws = h.workspace(need, dev)
-    rb = _report_buffers(B, max_iters, dev)
-    rep = _report_struct(rb)
-    ids = _i64(matrix_ids) if matrix_ids is not None else None
-    st = stream if stream is not None else torch.cuda.current_stream(dev)
-    check(lib().prism_inv_root(h.h, B, n, int(q), _ptrs(mats), _i64([t.stride(0) for t in mats]), _ptrs(out),
-                               _i64([t.stride(0) for t in out]), ids, ctypes.byref(o), ctypes.byref(rep),
-                               ws.data_ptr(), ws.numel(), ctypes.c_void_p(st.cuda_stream)), "prism_inv_root")
-    return out, rb
+def sign(mats, out=None, **kw):
+    """Matrix signs of square matrices via prism_sign -> (outputs, report)."""
+    o1, _, rb = _solve("sign", mats, out=out, **kw)
+    return o1, rb
 
 
-def inv_root_host(mats, q=4, max_iters=30, sketch_size=8, tol=1e-6, seed=42, precision=None, fit="sketched",
-                  warmup_iters=0, alpha_lo=None, alpha_hi=None, out=None, matrix_ids=None, stream=None,
-                  handle=None, device=None):
-    """A^{-1/q} of pinned HOST SPD matrices via prism_inv_root_host (as polar_host)."""
-    import torch
-    mats = list(mats)
-    if not mats:
-        return [], {}
-    _check_pinned(mats, "inv_root_host")
-    precision = _precision_of(mats[0], precision)
-    _check_dtype(mats, precision, on_host=True)
-    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
-    h = handle or default_handle()
-    o = make_options(5, max_iters, sketch_size, tol, seed, precision, fit, warmup_iters, alpha_lo, alpha_hi)
-    B = len(mats)
-    if out is None:
-        out = [torch.empty_like(t).pin_memory() for t in mats]
-    _check_pinned(out, "inv_root_host")
-    _check_dtype(out, precision, on_host=True)
-    rb = _report_buffers(B, max_iters, dev)
-    rep = _report_struct(rb)
-    ids = _i64(matrix_ids) if matrix_ids is not None else None
-    st = stream if stream is not None else torch.cuda.current_stream(dev)
-    check(lib().prism_inv_root_host(h.h, B, _i64([t.shape[0] for t in mats]), int(q), _ptrs(mats),
-                                    _i64([t.stride(0) for t in mats]), _ptrs(out), _i64([t.stride(0) for t in out]),
-                                    ids, ctypes.byref(o), ctypes.byref(rep), ctypes.c_void_p(st.cuda_stream)),
-          "prism_inv_root_host")
-    return out, rb
+def sign_host(mats, out=None, **kw):
+    o1, _, rb = _solve("sign", mats, host=True, out=out, **kw)
+    return o1, rb
 
 
-def _square_solve(fn_ws, fn, name, mats, q, max_iters, sketch_size, tol, seed, precision, fit, warmup_iters,
-                  alpha_lo, alpha_hi, out, matrix_ids, stream, handle):
-    import torch
-    mats = list(mats)
-    if not mats:
-        return [], {}
-    precision = _precision_of(mats[0], precision)
-    _check_dtype(mats, precision)
-    for t in mats:
-        if t.shape[0] != t.shape[1]:
-            raise PrismError(f"{name}: matrices must be square")
-    dev = mats[0].device
-    h = handle or default_handle()
-    o = make_options(5, max_iters, sketch_size, tol, seed, precision, fit, warmup_iters, alpha_lo, alpha_hi)
-    B = len(mats)
-    n = _i64([t.shape[0] for t in mats])
-    if out is None:
-        out = [torch.empty_like(t) for t in mats]
-    _check_dtype(out, precision)
-    need = fn_ws(h.h, B, n, ctypes.byref(o))
-    if need == 0:
-        raise PrismError(f"{name} workspace query rejected the arguments: " + lib().prism_last_error().decode())
-    ws = h.workspace(need, dev)
-    rb = _report_buffers(B, max_iters, dev)
-    rep = _report_struct(rb)
-    ids = _i64(matrix_ids) if matrix_ids is not None else None
-    st = stream if stream is not None else torch.cuda.current_stream(dev)
-    check(fn(h.h, B, n, _ptrs(mats), _i64([t.stride(0) for t in mats]), _ptrs(out), _i64([t.stride(0) for t in out]),
-             ids, ctypes.byref(o), ctypes.byref(rep), ws.data_ptr(), ws.numel(), ctypes.c_void_p(st.cuda_stream)),
-          name)
-    return out, rb
+def inv_root(mats, q=4, out=None, **kw):
+    """A^{-1/q} of SPD matrices by the coupled inverse Newton iteration."""
+    kw.pop("degree", None)
+    o1, _, rb = _solve("inv_root", mats, q=q, out=out, **kw)
+    return o1, rb
 
 
-def chebyshev_inverse(mats, max_iters=40, sketch_size=8, tol=1e-6, seed=42, precision=None, fit="sketched",
-                      warmup_iters=0, alpha_lo=None, alpha_hi=None, out=None, matrix_ids=None, stream=None,
-                      handle=None):
-    """A^{-1} of a batch of square CUDA matrices via prism_chebyshev_inverse."""
-    return _square_solve(lib().prism_chebyshev_inverse_workspace, lib().prism_chebyshev_inverse,
-                         "prism_chebyshev_inverse", mats, 0, max_iters, sketch_size, tol, seed, precision, fit,
-                         warmup_iters, alpha_lo, alpha_hi, out, matrix_ids, stream, handle)
+def inv_root_host(mats, q=4, out=None, **kw):
+    kw.pop("degree", None)
+    o1, _, rb = _solve("inv_root", mats, host=True, q=q, out=out, **kw)
+    return o1, rb
 
 
-def chebyshev_inverse_host(mats, max_iters=40, sketch_size=8, tol=1e-6, seed=42, precision=None, fit="sketched",
-                           warmup_iters=0, alpha_lo=None, alpha_hi=None, out=None, matrix_ids=None, stream=None,
-                           handle=None, device=None):
-    """A^{-1} of pinned HOST square matrices via prism_chebyshev_inverse_host (as polar_host)."""
-    import torch
-    mats = list(mats)
-    if not mats:
-        return [], {}
-    _check_pinned(mats, "chebyshev_inverse_host")
-    precision = _precision_of(mats[0], precision)
-    _check_dtype(mats, precision, on_host=True)
-    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
-    h = handle or default_handle()
-    o = make_options(5, max_iters, sketch_size, tol, seed, precision, fit, warmup_iters, alpha_lo, alpha_hi)
-    B = len(mats)
-    if out is None:
-        out = [torch.empty_like(t).pin_memory() for t in mats]
-    _check_pinned(out, "chebyshev_inverse_host")
-    _check_dtype(out, precision, on_host=True)
-    rb = _report_buffers(B, max_iters, dev)
-    rep = _report_struct(rb)
-    ids = _i64(matrix_ids) if matrix_ids is not None else None
-    st = stream if stream is not None else torch.cuda.current_stream(dev)
-    check(lib().prism_chebyshev_inverse_host(h.h, B, _i64([t.shape[0] for t in mats]), _ptrs(mats),
-                                             _i64([t.stride(0) for t in mats]), _ptrs(out),
-                                             _i64([t.stride(0) for t in out]), ids, ctypes.byref(o),
-                                             ctypes.byref(rep), ctypes.c_void_p(st.cuda_stream)),
-          "prism_chebyshev_inverse_host")
-    return out, rb
+def chebyshev_inverse(mats, max_iters=40, out=None, **kw):
+    """A^{-1} of square matrices by the Chebyshev iteration."""
+    kw.pop("degree", None)
+    o1, _, rb = _solve("chebyshev", mats, max_iters=max_iters, out=out, **kw)
+    return o1, rb
 
 
-def db_newton(mats, max_iters=30, tol=1e-6, precision="fp32", fit="sketched", warmup_iters=0, want_sqrt=True,
-              want_invsqrt=True, matrix_ids=None, stream=None, handle=None, out_sqrt=None, out_invsqrt=None):
-    """A^{1/2}, A^{-1/2} of a batch of SPD CUDA fp32 matrices via prism_db_newton (PRISM DB
-    Newton, product form; the fit is exact and unsketched; outputs into out_sqrt /
-    out_invsqrt when given)."""
-    import torch
-    mats = list(mats)
-    if not mats:
-        return [], [], {}
-    _check_dtype(mats, precision)
-    dev = mats[0].device
-    h = handle or default_handle()
-    o = make_options(5, max_iters, 8, tol, 42, precision, fit, warmup_iters)
-    B = len(mats)
-    n = _i64([t.shape[0] for t in mats])
-    sq = _outputs(mats, want_sqrt, out_sqrt, "db_newton")
-    isq = _outputs(mats, want_invsqrt, out_invsqrt, "db_newton")
-    ld_out = _ld_out(sq, isq, mats, "db_newton")
-    need = lib().prism_db_newton_workspace(h.h, B, n, ctypes.byref(o))
-    if need == 0:
-        raise PrismError("prism_db_newton_workspace rejected the arguments: " + lib().prism_last_error().decode())
-    ws = h.workspace(need, dev)
-    rb = _report_buffers(B, max_iters, dev)
-    rep = _report_struct(rb)
-    ids = _i64(matrix_ids) if matrix_ids is not None else None
-    st = stream if stream is not None else torch.cuda.current_stream(dev)
-    check(lib().prism_db_newton(h.h, B, n, _ptrs(mats), _i64([t.stride(0) for t in mats]),
-                                _ptrs(sq) if sq else None, _ptrs(isq) if isq else None, ld_out, ids,
-                                ctypes.byref(o), ctypes.byref(rep), ws.data_ptr(), ws.numel(),
-                                ctypes.c_void_p(st.cuda_stream)), "prism_db_newton")
-    return sq, isq, rb
+def chebyshev_inverse_host(mats, max_iters=40, out=None, **kw):
+    kw.pop("degree", None)
+    o1, _, rb = _solve("chebyshev", mats, host=True, max_iters=max_iters, out=out, **kw)
+    return o1, rb
 
 
-def db_newton_host(mats, max_iters=30, tol=1e-6, precision="fp32", fit="sketched", warmup_iters=0, want_sqrt=True,
-                   want_invsqrt=True, matrix_ids=None, stream=None, handle=None, device=None):
-    """A^{1/2}, A^{-1/2} of pinned HOST SPD fp32 matrices via prism_db_newton_host."""
-    import torch
-    mats = list(mats)
-    if not mats:
-        return [], [], {}
-    _check_pinned(mats, "db_newton_host")
-    _check_dtype(mats, precision, on_host=True)
-    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
-    h = handle or default_handle()
-    o = make_options(5, max_iters, 8, tol, 42, precision, fit, warmup_iters)
-    B = len(mats)
-    sq = [torch.empty_like(t).pin_memory() for t in mats] if want_sqrt else None
-    isq = [torch.empty_like(t).pin_memory() for t in mats] if want_invsqrt else None
-    rb = _report_buffers(B, max_iters, dev)
-    rep = _report_struct(rb)
-    ids = _i64(matrix_ids) if matrix_ids is not None else None
-    st = stream if stream is not None else torch.cuda.current_stream(dev)
-    check(lib().prism_db_newton_host(h.h, B, _i64([t.shape[0] for t in mats]), _ptrs(mats),
-                                     _i64([t.stride(0) for t in mats]), _ptrs(sq) if sq else None,
-                                     _ptrs(isq) if isq else None, _i64([t.shape[1] for t in mats]), ids,
-                                     ctypes.byref(o), ctypes.byref(rep), ctypes.c_void_p(st.cuda_stream)),
-          "prism_db_newton_host")
-    return sq, isq, rb
+def sqrt_invsqrt(mats, want_sqrt=True, want_invsqrt=True, out_sqrt=None, out_invsqrt=None, **kw):
+    """A^{1/2}, A^{-1/2} of SPD matrices (Theorem 3) -> (sqrt, invsqrt, report)."""
+    return _solve("sqrt", mats, want1=want_sqrt, want2=want_invsqrt, out=out_sqrt, out2=out_invsqrt, **kw)
+
+
+def sqrt_invsqrt_host(mats, want_sqrt=True, want_invsqrt=True, out_sqrt=None, out_invsqrt=None, **kw):
+    return _solve("sqrt", mats, host=True, want1=want_sqrt, want2=want_invsqrt, out=out_sqrt, out2=out_invsqrt,
+                  **kw)
+
+
+def db_newton(mats, want_sqrt=True, want_invsqrt=True, out_sqrt=None, out_invsqrt=None, precision="fp32", **kw):
+    """A^{1/2}, A^{-1/2} by PRISM DB Newton, product form, FP32 only."""
+    kw.pop("sketch_size", None)
+    return _solve("db_newton", mats, want1=want_sqrt, want2=want_invsqrt, out=out_sqrt, out2=out_invsqrt,
+                  precision=precision, **kw)
+
+
+def db_newton_host(mats, want_sqrt=True, want_invsqrt=True, out_sqrt=None, out_invsqrt=None, precision="fp32",
+                   **kw):
+    kw.pop("sketch_size", None)
+    return _solve("db_newton", mats, host=True, want1=want_sqrt, want2=want_invsqrt, out=out_sqrt,
+                  out2=out_invsqrt, precision=precision, **kw)
 
 
 class RowBlockSolver:
@@ -737,8 +446,8 @@ class RowBlockSolver:
         need = lib().prism_rowblock_workspace(self.h.h, rows, n, ctypes.byref(self.o))
         if need == 0:
             raise PrismError("prism_rowblock_workspace rejected the arguments: " + lib().prism_last_error().decode())
-        self.ws = self.h.workspace(need, self.dev)
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.dev)
+        self.ws = self.h.workspace(need, self.dev, self.stream)
         self._s = ctypes.c_void_p(self.stream.cuda_stream)
 
     def begin(self):
@@ -776,3 +485,4 @@ def polar_flops_per_iter(m, n, degree=5, sketch_size=8) -> float:
 
 def sqrt_flops_per_iter(n, degree=5, sketch_size=8) -> float:
     return float(lib().prism_sqrt_flops_per_iter(int(n), int(degree), int(sketch_size)))
+

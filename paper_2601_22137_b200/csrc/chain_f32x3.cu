@@ -1,0 +1,8 @@
+// Sketch-chain kernels (chaint.cuh), f32x3 instantiation: one kernel per pass code.
+#include "chain_launch.cuh"
+
+namespace prism {
+cudaError_t launch_chain_f32x3(int pass, const GemmLaunch& L, cudaStream_t st) {
+  return launch_chain_cfg<ChainTCfg<1, true>>(pass, L, st);
+}
+}  // namespace prism

@@ -57,11 +57,6 @@ __device__ __forceinline__ void chain_krange(int K, int BK, int own, int ks, int
   hi = ks < own ? (ks + 1) * nkb / own : nkb;
 }
 
-// Debug timeline (prism_debug_trace_chain): per pass code and CTA, 16 globaltimer stamps
-// of the launch: 0 entry, 1 setup done, 2 predecessor done, 3 first TMA, 4 last MMA
-// committed, 5 accumulator ready (reader), 6 slices sent, 7 slices received, 8 epilogue done.
-__device__ unsigned long long* g_chain_trace = nullptr;
-
 // Slices of a tile this CTA computes: in a split launch (C > 1) the one at its cluster
 // rank (the tile code's low bits); in a C = 1 launch all P.ksplit slices of the matrix,
 // in order (each accumulated separately and summed in the same order as the split
@@ -89,8 +84,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  unsigned long long* tr = g_chain_trace ? g_chain_trace + ((size_t)L.probs[0].pass * 1024 + blockIdx.x) * 16 : nullptr;
-  if (tr && threadIdx.x == 0) tr[0] = globaltimer_ns();
   const int C = L.ksplit > 1 ? L.ksplit : 1;           // cluster size (1, 2, 4, 8)
   const uint32_t krank = C > 1 ? cluster_ctarank() : 0u;
   const int rows_per = Cfg::BN / C;                    // rows of the tile this CTA finishes
@@ -117,7 +110,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  if (tr && threadIdx.x == 0) tr[1] = globaltimer_ns();
 
   // Before the predecessor (the previous pass) completes, everything this launch reads
   // except W is already final: the iteration counter, the done flags and R were written
@@ -154,7 +146,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
   }
   griddep_wait();
   griddep_launch();
-  if (tr && threadIdx.x == 0) tr[2] = globaltimer_ns();
 
   if (warp < 4) {
     setmaxnreg_dec<Cfg::REG_LO>();
@@ -184,7 +175,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
             tma_load_2d(sB, P.tmB, &full[stage], kb * Cfg::BK, n0);   // R rows n0 .. n0+255
             if constexpr (Cfg::SPLIT) tma_load_2d(sB + Cfg::B_BYTES, P.tmB_lo, &full[stage], kb * Cfg::BK, n0);
           }
-          if (tr && kb == kb_lo) tr[3] = globaltimer_ns();
           if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -226,7 +216,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
             if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
           }
           umma_commit<1>(&tfull[acc]);
-          if (tr) tr[4] = globaltimer_ns();
           if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
       }
@@ -291,7 +280,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
           first = false;
           if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
-        if (tr && reader && lane == 0 && h == 0) tr[5] = globaltimer_ns();
       } else {
       int kb_lo, kb_hi;
       chain_krange(P.K, Cfg::BK, P.ksplit, s_lo, kb_lo, kb_hi);
@@ -301,7 +289,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
           mbar_wait(&tfull[acc], acc_phase);
           tc_fence_after();
         }
-        if (tr && lane == 0 && h == 0) tr[5] = globaltimer_ns();
         // every owner consumed the previous round's slices: send this round's
         mbar_wait(recv_free, rphase ^ 1);
 #pragma unroll 1
@@ -331,7 +318,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[acc]);
         }
-        if (tr && lane == 0 && h == 0) tr[6] = globaltimer_ns();
       }
       if (have && ++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
@@ -339,7 +325,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
       named_bar_sync(1, 32 * Cfg::EPI_WARPS);    // own slice written locally
       if (C > 1) {
         mbar_wait(recv_full, rphase);            // the other C-1 slices landed
-        if (tr && et == 0) tr[7] = globaltimer_ns();
         if (et < rows_per) {
           // sum the C slices in fixed order (deterministic; -0.0 identity: one real slice
           // sums to itself exactly) into this thread's column of slot 0; 32 independent
@@ -355,7 +340,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
           for (int c = 0; c < 32; ++c) dsm[(size_t)c * rstride + et] = v[c];
         }
       }
-      if (tr && et == 0) tr[9] = globaltimer_ns();
       epi_chain<Cfg, PASS>(pre, i, grp, dsm + et, rstride, lane, 2);
       named_bar_sync(1, 32 * Cfg::EPI_WARPS);    // buffer consumed
       if (C > 1) {
@@ -365,7 +349,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
           for (int x = 0; x < C; ++x)
             if (x != (int)krank) mbar_arrive_release_cluster(recv_free, (uint32_t)x);
       }
-      if (tr && et == 0) tr[8] = globaltimer_ns();
     }
   }
 

@@ -943,15 +943,8 @@ __device__ __forceinline__ uint64_t operand_desc(uint32_t base, int k, int mn_ma
 
 // ---------------------------------------------------------------- the kernel
 
-// Main-GEMM k-block timeline (prism_debug_trace_gemm): for launches whose first problem has
-// epilogue mode g_trace_mode, each CTA's first tile records [0,64) producer issue (after
-// its empty wait), [64,128) MMA full arrival, [128,192) MMA issue done, per k-block.
-__device__ unsigned long long* g_gemm_trace2 = nullptr;
-__device__ int g_trace_mode = -1;
-constexpr int TRACE2_W = 376;   // + [248 + 16 e + 4 ch + k]: warp e, chunk ch: ld issue, ld done, C done, stored   // + [192 + 4 j ..]: tile j mma start / end, epilogue start / end
-
 template <class Cfg>
-__global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __grid_constant__ GemmLaunch L) {
+__device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
   extern __shared__ uint8_t smem_raw[];
   // 1024-B alignment for the 128-B swizzle atoms
   const uint32_t raw = smem_u32(smem_raw);
@@ -975,8 +968,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
   const int cid = Cfg::CTA2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;   // tile-loop index / stride
   const int ncl = Cfg::CTA2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   const GemmProblem* __restrict__ probs = L.probs;
-  unsigned long long* trace2 = nullptr;
-  if (g_gemm_trace2 && L.probs[0].mode == g_trace_mode) trace2 = g_gemm_trace2 + (size_t)blockIdx.x * TRACE2_W;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {
@@ -1073,7 +1064,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
             if constexpr (Cfg::LOB)
               load_operand<Cfg>(sB2, P.tmB_lo, &full[stage], bn0, kb * Cfg::BK, Cfg::B_ROWS, P.b_mn);
           }
-          if (trace2 && t == cid && kb < 64) trace2[kb] = globaltimer_ns();
           if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -1085,7 +1075,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      int tcount = 0;
       for (int t = cid; t < L.ntiles; t += ncl) {
         const uint32_t code = L.tiles[t];
         const GemmProblem& P = probs[code >> 20];
@@ -1101,8 +1090,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
           const uint32_t dt = tmem_base + acc * Cfg::BN;
           for (int kb = kb0; kb < kb1; ++kb) {
             mbar_wait(&full[stage], phase);
-            if (trace2 && t == cid && kb < 64) trace2[64 + kb] = globaltimer_ns();
-            if (trace2 && kb == kb_lo && tcount < 8) trace2[192 + 4 * tcount] = globaltimer_ns();
             tc_fence_after();
             const uint32_t aA = smem_u32(stage_base + stage * Cfg::STAGE_BYTES);
             const uint32_t aB = aA + Cfg::A_BYTES;
@@ -1121,14 +1108,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
               }
             }
             umma_commit<Cfg::CG>(&empty[stage]);     // smem slots (of both CTAs) free once these MMAs retire
-            if (trace2 && t == cid && kb < 64) trace2[128 + kb] = globaltimer_ns();
             if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
           }
           umma_commit<Cfg::CG>(&tfull[acc]);          // accumulator (chunk) ready for both epilogues
           if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
-        if (trace2 && tcount < 8) trace2[192 + 4 * tcount + 1] = globaltimer_ns();
-        ++tcount;
       }
     }
     }
@@ -1146,7 +1130,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
     int acc = 0;
     uint32_t acc_phase = 0;
     uint32_t cph = 0;       // bf16: phase bits of this warp's two C-block barriers
-    int etcount = 0;
     // accumulator release: one arrival per epilogue warp on the leader's tempty barrier
     auto release_acc = [&](uint64_t* bar) {
       tc_fence_before();
@@ -1198,7 +1181,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
           if (c_begin + 1 < c_end) c_fetch(c_begin + 1);
         }
         mbar_wait(&tfull[acc], acc_phase);
-        if (trace2 && et == 0 && leader && etcount < 8) trace2[192 + 4 * etcount + 2] = globaltimer_ns();
         tc_fence_after();
         const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * Cfg::BN;
         uint32_t ra[32], rb[32];
@@ -1297,8 +1279,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
         }
         named_bar_sync(1, 32 * Cfg::EPI_WARPS);
       }
-      if (trace2 && et == 0 && leader && etcount < 8) trace2[192 + 4 * etcount + 3] = globaltimer_ns();
-      ++etcount;
     }
     if (Cfg::KIND == 0 && lane == 0) bulk_wait_all();   // this warp's TMA stores are complete
   }
@@ -1311,6 +1291,28 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __gri
     tc_fence_after();
     tmem_dealloc<Cfg::CG>(tmem_base, Cfg::TMEM_ALLOC);
   }
+}
+
+// One GEMM body, one kernel symbol per role in the iteration, so ncu launch lists and
+// per-kernel profiles separate the residual (Gram) product, the square R.R, the apply
+// X + X.P and the other products (DB Newton sweep, test hook).
+enum GemmRole : int { ROLE_GRAM = 0, ROLE_SQUARE = 1, ROLE_APPLY = 2, ROLE_OTHER = 3 };
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gram_kernel(const __grid_constant__ GemmLaunch L) {
+  gemm_body<Cfg>(L);
+}
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, 1) prism_square_kernel(const __grid_constant__ GemmLaunch L) {
+  gemm_body<Cfg>(L);
+}
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, 1) prism_apply_kernel(const __grid_constant__ GemmLaunch L) {
+  gemm_body<Cfg>(L);
+}
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, 1) prism_gemm_kernel(const __grid_constant__ GemmLaunch L) {
+  gemm_body<Cfg>(L);
 }
 
 }  // namespace prism

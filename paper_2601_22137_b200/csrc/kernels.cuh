@@ -499,9 +499,6 @@ __global__ void __launch_bounds__(kGJ) k_gj_pivot(SolveParams P, int j) {
   if (J0 >= n) return;
   const int bj = min(kGJ, n - J0);
   if (blockIdx.x == 0) {
-    unsigned long long* gtr = (g_chain_trace && b == P.batch - 1 && threadIdx.x == 0 && j < 64)
-                                  ? g_chain_trace + 16 * 1024 * 16 - 4096 + 4 * j : nullptr;
-    if (gtr) gtr[0] = globaltimer_ns();
     float* colf = gsm;   // [2][kGJ]
     float(*tile)[kGJ + 1] = reinterpret_cast<float(*)[kGJ + 1]>(gsm + 2 * kGJ);
     const int c = threadIdx.x;
@@ -542,7 +539,6 @@ __global__ void __launch_bounds__(kGJ) k_gj_pivot(SolveParams P, int j) {
         for (int i = 0; i < kGJ; i += 4) *reinterpret_cast<float4*>(cf + i) = make_float4(a[i], a[i + 1], a[i + 2], a[i + 3]);
       }
       __syncthreads();
-      if (gtr && p == 0) gtr[1] = globaltimer_ns();
       const float inv = 1.f / cf[0];
       // new row r-1 = a[r] - colf[r] * (a[p] / pivot); the pivot column's owner (its old
       // registers already broadcast) zeroes them, so one FMA gives -colf[r] / pivot there
@@ -562,14 +558,12 @@ __global__ void __launch_bounds__(kGJ) k_gj_pivot(SolveParams P, int j) {
       }
       a[kGJ - 1] = rr;   // the new pivot row: a[p] / pivot, and 1 / pivot on the diagonal
     }
-    if (gtr) gtr[2] = globaltimer_ns();
     // row r is in register (r - bj) mod 128
 #pragma unroll
     for (int i = 0; i < kGJ; ++i) {
       const int r = (i + bj) & (kGJ - 1);
       store_x(D.Dp, D.Dp_lo, (long long)r * kGJ + c, (r < bj && c < bj) ? a[i] : 0.f, 1);
     }
-    if (gtr) gtr[3] = globaltimer_ns();
   } else {
     // rows blockIdx.x - 1, + kGJCopy, ... of E: 16-B vectors (ld and buffers are 64-element
     // aligned), scalar tail when n % 4 != 0
@@ -1067,11 +1061,6 @@ __global__ void __launch_bounds__(256) k_alpha(SolveParams P, int pre_wait) {
     return;
   }
   const int s = D.s;
-  // diagnostics (scripts/trace_alpha.py): block 0's timeline of iteration k in the chain
-  // trace buffer's tail
-  unsigned long long* atr = (g_chain_trace && b == 0 && threadIdx.x == 0 && *P.iter < 32)
-                                ? g_chain_trace + 16 * 1024 * 16 - 8192 + 8 * *P.iter : nullptr;
-  if (atr) atr[0] = globaltimer_ns();
   // ||R_k||_F^2 from the Gram per-tile partials (fixed order, scheduled tiles only)
   double part = 0.0;
   const int ntile = D.tiles_m * D.tiles_n;
@@ -1114,7 +1103,6 @@ __global__ void __launch_bounds__(256) k_alpha(SolveParams P, int pre_wait) {
     s_stop = stop;
   }
   __syncthreads();
-  if (atr) atr[1] = globaltimer_ns();
   if (s_stop) return;
   if (threadIdx.x >= 32) return;   // warp 0 fits alpha
   double a;
@@ -1160,11 +1148,6 @@ __global__ void __launch_bounds__(256) k_alpha(SolveParams P, int pre_wait) {
       for (int j = 0; j < kChainG; ++j)
         if (j < ng) g[j] += cp[j];
     }
-    if (atr) {   // diagnostics: loads landed (value-dependent store orders the timer after them)
-      if (g[0] == 1.2345e300) atr[7] = 1;
-      atr[4] = globaltimer_ns();
-    }
-    if (atr) atr[6] = globaltimer_ns();
 #pragma unroll
     for (int j = 0; j < kChainG; ++j) {
 #pragma unroll
@@ -1175,10 +1158,6 @@ __global__ void __launch_bounds__(256) k_alpha(SolveParams P, int pre_wait) {
     // warp ran it ~8x slower); lane 0's values are the ones whose alpha is stored
 #pragma unroll
     for (int j = 0; j < kChainG; ++j) g[j] = __shfl_sync(0xffffffffu, g[j], 0);
-    if (atr) {
-      if (g[5] == 1.2345e300) atr[7] = 2;
-      atr[5] = globaltimer_ns();
-    }
     if (P.kind_cheb) {
       // Chebyshev: m(a) = ||U - a V||^2 (R26), closed form on [1/2, 2]
       double c[5] = {g[0], -2.0 * g[1], g[2], 0.0, 0.0};
@@ -1194,14 +1173,9 @@ __global__ void __launch_bounds__(256) k_alpha(SolveParams P, int pre_wait) {
       else a = argmin_poly_warp(c, 2 * q, P.alo, P.ahi, P.ataylor);
     } else {
       double c[5] = {g[0], 2.0 * g[1], g[3] + 2.0 * g[2], 2.0 * g[4], g[5]};
-      if (atr)
-        for (int j = 0; j < 5; ++j)
-          atr[-8192 + j] = (unsigned long long)__double_as_longlong(c[j]);   // diagnostics: the quartic
-      if (atr) atr[2] = globaltimer_ns();
       a = (k < P.warmup) ? P.ahi : argmin_quartic(c, P.alo, P.ahi, P.ataylor);
     }
   }
-  if (atr) atr[3] = globaltimer_ns();
   if (threadIdx.x == 0) {
     S.alpha = a;
     P.alpha_hist[(size_t)b * P.max_iters + k] = a;

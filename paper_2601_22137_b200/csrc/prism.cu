@@ -3,8 +3,7 @@
 // (no host synchronisation anywhere on the solve path).  See include/prism.h
 // for the contract and DESIGN.md for the data layout.
 #include "../../include/prism.h"
-#include "gemm.cuh"
-#include "chaint.cuh"
+#include "launch.h"
 #include "kernels.cuh"
 
 #include <algorithm>
@@ -13,6 +12,7 @@
 #include <cmath>
 #include <cstring>
 #include <list>
+#include <map>
 #include <memory>
 #include <string>
 #include <vector>
@@ -90,147 +90,7 @@ bool encode_map(CUtensorMap* out, const MapSpec& s) {
 }
 
 // ------------------------------------------------------------------ kernel dispatch
-int g_num_sms = 0;
-
-int num_sms() {
-  if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
-  }
-  return g_num_sms;
-}
-
-// Programmatic dependent launch (PRISM_PDL=0 disables, for A/B timing): every kernel
-// calls griddep_wait() before reading its predecessors' results (ptx.cuh).
-static bool use_pdl() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("PRISM_PDL");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
-}
-
-// Launch `k` with PDL and (cluster > 1) a 1-D cluster.
-template <typename... KArgs, typename... Args>
-cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, int cluster,
-                     Args... args) {
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute at[2];
-  int n = 0;
-  at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[n].val.programmaticStreamSerializationAllowed = use_pdl() ? 1 : 0;
-  ++n;
-  if (cluster > 1) {
-    at[n].id = cudaLaunchAttributeClusterDimension;
-    at[n].val.clusterDim.x = cluster;
-    at[n].val.clusterDim.y = 1;
-    at[n].val.clusterDim.z = 1;
-    ++n;
-  }
-  cfg.attrs = at;
-  cfg.numAttrs = n;
-  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
-}
-
-template <class Cfg>
-cudaError_t launch_gemm_cfg(const GemmLaunch& L, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(prism_gemm_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Cfg::SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  if (L.ntiles <= 0) return cudaSuccess;
-  if constexpr (Cfg::CTA2) {
-    // clusters of 2 CTAs (one CTA pair per tile), persistent over the tile list
-    const int pairs = std::min(L.ntiles, num_sms() / 2);
-    return launch_k(prism_gemm_kernel<Cfg>, dim3(2 * pairs), dim3(Cfg::THREADS), Cfg::SMEM_BYTES, st, 2, L);
-  } else if (L.ksplit > 1) {
-    // chain split-K: clusters of ksplit CTAs, one row tile per cluster per round
-    const int grid = std::min(L.ntiles, num_sms() / L.ksplit * L.ksplit);
-    return launch_k(prism_gemm_kernel<Cfg>, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM_BYTES, st, L.ksplit, L);
-  } else {
-    const int grid = std::min(L.ntiles, num_sms());
-    return launch_k(prism_gemm_kernel<Cfg>, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM_BYTES, st, 1, L);
-  }
-}
-
-template <class Cfg, int PASS>
-cudaError_t launch_chaint_pass(const GemmLaunch& L, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(prism_chaint_kernel<Cfg, PASS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Cfg::SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  if (L.ntiles <= 0) return cudaSuccess;
-  const int C = std::max(1, L.ksplit);   // split chains: clusters of C CTAs (reduce-scatter)
-  const int grid = std::min(L.ntiles, num_sms() / C * C);
-  return launch_k(prism_chaint_kernel<Cfg, PASS>, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM_BYTES, st, C, L);
-}
-
-// one kernel per pass code (each carries only its own epilogue: the code of a chain
-// pass runs once per CTA per launch, from a cold instruction cache)
-template <class Cfg>
-cudaError_t launch_chaint_cfg(int pass, const GemmLaunch& L, cudaStream_t st) {
-  switch (pass) {
-    case CH2_P1: return launch_chaint_pass<Cfg, CH2_P1>(L, st);
-    case CH2_P2: return launch_chaint_pass<Cfg, CH2_P2>(L, st);
-    case CH2_P3: return launch_chaint_pass<Cfg, CH2_P3>(L, st);
-    case CH2_P4: return launch_chaint_pass<Cfg, CH2_P4>(L, st);
-    case CH2_P5: return launch_chaint_pass<Cfg, CH2_P5>(L, st);
-    case CH1_P1: return launch_chaint_pass<Cfg, CH1_P1>(L, st);
-    case CH1_P2: return launch_chaint_pass<Cfg, CH1_P2>(L, st);
-    case CH1_P3: return launch_chaint_pass<Cfg, CH1_P3>(L, st);
-    case CHI_K2: return launch_chaint_pass<Cfg, CHI_K2>(L, st);
-    case CHI_L1: return launch_chaint_pass<Cfg, CHI_L1>(L, st);
-    case CHI_L2: return launch_chaint_pass<Cfg, CHI_L2>(L, st);
-    case CHI_L3: return launch_chaint_pass<Cfg, CHI_L3>(L, st);
-    case CHI_L4: return launch_chaint_pass<Cfg, CHI_L4>(L, st);
-    case CHC_P1: return launch_chaint_pass<Cfg, CHC_P1>(L, st);
-    case CHC_P2: return launch_chaint_pass<Cfg, CHC_P2>(L, st);
-    default: return launch_chaint_pass<Cfg, CHC_P3>(L, st);
-  }
-}
-
-cudaError_t launch_chaint(int precision, int pass, const GemmLaunch& L, cudaStream_t st) {
-  if (precision == PRISM_BF16) return launch_chaint_cfg<ChainTCfg<0, false>>(pass, L, st);
-  if (precision == PRISM_FP32) return launch_chaint_cfg<ChainTCfg<1, true>>(pass, L, st);
-  return launch_chaint_cfg<ChainTCfg<1, false>>(pass, L, st);
-}
-
-
-// Main GEMM variant: CTA pairs (cta_group::2, 256 x BN tiles) by default; PRISM_GEMM_1CTA=1
-// selects single-CTA 128 x BN tiles (A/B comparison knob for profiling).
-static bool use_1cta() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("PRISM_GEMM_1CTA");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  return v == 1;
-}
-int tile_m_main() { return use_1cta() ? 128 : 256; }
-
-cudaError_t launch_gemm(int precision, const GemmLaunch& L, cudaStream_t st) {
-  if (use_1cta()) {
-    if (precision == PRISM_BF16) return launch_gemm_cfg<GemmCfg<0, false, 0, false>>(L, st);
-    if (precision == PRISM_FP32) return launch_gemm_cfg<GemmCfg<1, true, 0, false>>(L, st);
-    return launch_gemm_cfg<GemmCfg<1, false, 0, false>>(L, st);
-  }
-  if (precision == PRISM_BF16) return launch_gemm_cfg<GemmCfg<0, false>>(L, st);
-  if (precision == PRISM_FP32) return launch_gemm_cfg<GemmCfg<1, true>>(L, st);
-  return launch_gemm_cfg<GemmCfg<1, false>>(L, st);
-}
+constexpr int kTileM = 256;   // main GEMMs run on CTA pairs: tiles of 256 rows x BN columns
 
 int tile_bn(int precision) { return precision == PRISM_BF16 ? 256 : 128; }
 int tile_bk(int precision) { return precision == PRISM_BF16 ? 64 : 32; }
@@ -341,11 +201,7 @@ struct Bump {
   }
 };
 
-// Main GEMMs run on CTA pairs: tiles of TILE_M = 256 rows x BN columns.
-int tile_m_main();
-
 void add_tiles(LaunchDesc& L, int prob, int M, int N, int BN, bool sym) {
-  const int kTileM = tile_m_main();
   const int tm_n = (M + kTileM - 1) / kTileM, tn_n = (N + BN - 1) / BN;
   for (int tm = 0; tm < tm_n; ++tm)
     for (int tn = 0; tn < tn_n; ++tn) {
@@ -358,8 +214,7 @@ void add_tiles(LaunchDesc& L, int prob, int M, int N, int BN, bool sym) {
 // function of its size s alone (never of the batch), so a matrix's bits do not depend on
 // what it is batched with (or on the rank it lands on).  Each slice keeps >= 8 k-blocks.
 int chain_ks(int s) {   // clusters of 8 do not all co-schedule
-  static const int small = [] { const char* e = getenv("PRISM_CHAIN_KS_SMALL"); return e ? atoi(e) : 1; }();
-  return s < 1024 ? small : s < 2048 ? 2 : 4;
+  return s < 1024 ? 1 : s < 2048 ? 2 : 4;
 }
 
 void sort_tiles_by_cost(LaunchDesc& L) {
@@ -396,7 +251,7 @@ prism_status build_plan(const Request& r, Plan& P) {
   std::vector<MatDesc> mats(B);
   std::vector<MapSpec> maps;
   auto add_map = [&](const void* ptr, int rows, int cols, long long ld, OpKind k) -> int {
-    maps.push_back(MapSpec{ptr, rows, cols, ld, esz, k, tile_m_main() == 256 ? BN / 2 : BN, BK});   // CTA pairs: half of B per CTA
+    maps.push_back(MapSpec{ptr, rows, cols, ld, esz, k, BN / 2, BK});   // CTA pairs: half of B per CTA
     return (int)maps.size();   // 1-based index
   };
 
@@ -775,7 +630,7 @@ prism_status build_plan(const Request& r, Plan& P) {
       rows += (hp.p.M + 255) / 256;
       kmax = std::max(kmax, hp.p.ksplit);
     }
-    P.chain_ksplit = rows >= num_sms() ? 1 : kmax;
+    P.chain_ksplit = rows >= device_sms() ? 1 : kmax;
   }
   for (int j = 0; j < P.n_chain; ++j) {
     LaunchDesc& T = P.chaint[j];
@@ -934,18 +789,19 @@ GemmLaunch make_launch(const Plan& P, const LaunchDesc& L, const LaunchDesc* odd
 
 constexpr int kGJSmem = (kGJ * (kGJ + 1) + 2 * kGJ) * 4;   // Gauss-Jordan pivot / fix-up tiles
 
-// Make every kernel's large-smem attribute current before any graph capture.
+// Make every kernel's large-smem attribute current (on this device) before any graph capture.
 void ensure_attrs() {
-  static bool done = false;
-  if (done) return;
-  done = true;
+  static std::array<char, kMaxDevices> done{};
+  const int dev = current_device();
+  if (done[dev]) return;
+  done[dev] = 1;
   cudaFuncSetAttribute(k_gj_pivot, cudaFuncAttributeMaxDynamicSharedMemorySize, kGJSmem);
   cudaFuncSetAttribute(k_gj_fix, cudaFuncAttributeMaxDynamicSharedMemorySize, kGJSmem);
   GemmLaunch z{};
   z.ntiles = 0;
   for (int prec = 0; prec < 3; ++prec) {
-    launch_gemm(prec, z, 0);
-    for (int pass = CH2_P1; pass < CH_NCODES; ++pass) launch_chaint(prec, pass, z, 0);
+    for (int role = ROLE_GRAM; role <= ROLE_OTHER; ++role) launch_gemm(prec, role, z, 0);
+    for (int pass = CH2_P1; pass < CH_NCODES; ++pass) launch_chain(prec, pass, z, 0);
   }
 }
 
@@ -986,6 +842,7 @@ prism_status validate(const Request& r) {
 constexpr int kKinds = 6;
 struct prism_handle_s {
   std::list<std::unique_ptr<Plan>> plans;   // most recent first
+  std::map<std::vector<long long>, size_t> ws_cache;   // workspace size per argument key
   long long launches = 0;                   // launches of the last solve
   bool profiling = false;
   std::vector<cudaEvent_t> pool;            // reusable events
@@ -1013,6 +870,7 @@ struct prism_handle_s {
   HostSlot slots[kMaxSlots];
   int slot_next = 0;
   cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
+  cudaEvent_t ev_call = nullptr;   // host path: the caller's stream reached the call
   char* hws = nullptr;   // workspace of the host-path solves (they run in order on s_comp)
   size_t hws_bytes = 0;
   ~prism_handle_s() {
@@ -1029,6 +887,7 @@ struct prism_handle_s {
         if (e) cudaEventDestroy(e);
     }
     if (hws) cudaFree(hws);
+    if (ev_call) cudaEventDestroy(ev_call);
     for (cudaStream_t x : {s_in, s_comp, s_out})
       if (x) cudaStreamDestroy(x);
   }
@@ -1068,6 +927,7 @@ struct KindTimer {
 
 static std::vector<long long> make_key(const Request& r) {
   std::vector<long long> k;
+  k.push_back(current_device());   // plans hold device allocations and per-device graphs
   k.push_back(r.sqrt_kind);
   k.push_back(r.sign_kind);
   k.push_back(r.inv_q);
@@ -1096,6 +956,20 @@ static std::vector<long long> make_key(const Request& r) {
     k.push_back(r.ids ? r.ids[i] : i);
   }
   return k;
+}
+
+// Workspace size of a request (size-only plan), cached per argument key on the handle:
+// the bindings query it before every call.
+static size_t ws_query(prism_handle h, const Request& r) {
+  if (validate(r)) return 0;
+  std::vector<long long> key = make_key(r);
+  auto it = h->ws_cache.find(key);
+  if (it != h->ws_cache.end()) return it->second;
+  Plan P;
+  if (build_plan(r, P)) return 0;
+  if (h->ws_cache.size() > 1024) h->ws_cache.clear();
+  h->ws_cache[key] = P.ws_need;
+  return P.ws_need;
 }
 
 // Plan lookup (LRU keyed by every argument that shapes the tables) or build.
@@ -1166,7 +1040,6 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
   GemmLaunch g_sq = make_launch(*P, P->square, nullptr, r.ws, 0, M);
   // the square GEMM reads R (written by the residual step, several launches back): its
   // mainloop can run while k_alpha finishes, only its epilogue waiting for alpha.
-  static const bool early_sq = [] { const char* e = getenv("PRISM_EARLY_SQUARE"); return !(e && e[0] == '0'); }();
   // Used where it was measured to pay (scripts/ab_early.sh, alternating runs on one box):
   // bf16 polar with few matrices — k_alpha then holds few SMs and the square GEMM fills
   // the rest (4096^2: 3.69 -> 3.54 ms per step).  Not for 3xTF32 (its epilogue consumes
@@ -1174,7 +1047,7 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
   // MMAs: shampoo 4 % slower), large batches (k_alpha holds B SMs: GPT-2 unchanged, 1B
   // batch 1 % slower) or the general square products of sign / Chebyshev (1-2 % slower).
   const bool polar_kind = !r.sqrt_kind && !r.sign_kind && !r.cheb_kind && !r.inv_q && !r.db_kind;
-  if (early_sq && polar_kind && prec == PRISM_BF16 && B <= 16) g_sq.early = 1;
+  if (polar_kind && prec == PRISM_BF16 && B <= 16) g_sq.early = 1;
   const GemmLaunch g_sq2 = make_launch(*P, P->square2, nullptr, r.ws, 0, M);
   std::vector<GemmLaunch> g_gjT, g_gjS;
   for (int j = 0; j < P->db_steps; ++j) {
@@ -1206,8 +1079,8 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
         const int strips = (P->max_s + kGJ - 1) / kGJ;
         for (int j = 0; j < P->db_steps; ++j) {
           PRISM_CK(launch_k(k_gj_pivot, dim3(1 + kGJCopy, B), dim3(kGJ), kGJSmem, s2, 1, S, j));
-          PRISM_CK(launch_gemm(prec, g_gjT[j], s2));
-          PRISM_CK(launch_gemm(prec, g_gjS[j], s2));
+          PRISM_CK(launch_gemm(prec, ROLE_OTHER, g_gjT[j], s2));
+          PRISM_CK(launch_gemm(prec, ROLE_OTHER, g_gjS[j], s2));
           PRISM_CK(launch_k(k_gj_fix, dim3(strips, B), dim3(256), kGJSmem, s2, 1, S, j));
         }
       }
@@ -1221,7 +1094,7 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
       }
       {
         KindTimer t(h, s2, 2, timed ? 2 : 0);
-        PRISM_CK(launch_gemm(prec, g_apply, s2));
+        PRISM_CK(launch_gemm(prec, ROLE_APPLY, g_apply, s2));
         PRISM_CK(launch_k(k_db_update, eg, dim3(256), 0, s2, 1, S, bn));
       }
       PRISM_CK(launch_k(k_advance, dim3(1), dim3(256), 0, s2, 1, S, ch, use_handle, P->d_all_done));
@@ -1236,13 +1109,13 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
         else if (prec == PRISM_FP32) PRISM_CK(launch_k(k_resid_inv<1>, grid, dim3(256), 0, s2, 1, S, tile_bn(prec)));
         else PRISM_CK(launch_k(k_resid_inv<2>, grid, dim3(256), 0, s2, 1, S, tile_bn(prec)));
       } else {
-        PRISM_CK(launch_gemm(prec, g_gram, s2));
+        PRISM_CK(launch_gemm(prec, ROLE_GRAM, g_gram, s2));
       }
     }
     if (sketched) {
       KindTimer t(h, s2, 3, timed ? 1 + n_chain_launches : 0);
       PRISM_CK(launch_k(k_sketch, dim3((p * P->max_s / 2 + 256) / 256, B), dim3(256), 0, s2, 1, S));
-      for (int j = 0; j < P->n_chain; ++j) PRISM_CK(launch_chaint(prec, chain_pass(*P, j), g_chaint[j], s2));
+      for (int j = 0; j < P->n_chain; ++j) PRISM_CK(launch_chain(prec, chain_pass(*P, j), g_chaint[j], s2));
     }
     {
       // norm partials from the residual step; a sketch chain in between makes them final
@@ -1252,12 +1125,12 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
     }
     if (P->has_square) {
       KindTimer t(h, s2, 1, timed ? (P->has_square2 ? 2 : 1) : 0);
-      PRISM_CK(launch_gemm(prec, g_sq, s2));
-      if (P->has_square2) PRISM_CK(launch_gemm(prec, g_sq2, s2));
+      PRISM_CK(launch_gemm(prec, ROLE_SQUARE, g_sq, s2));
+      if (P->has_square2) PRISM_CK(launch_gemm(prec, ROLE_SQUARE, g_sq2, s2));
     }
     {
       KindTimer t(h, s2, 2, timed ? 1 : 0);
-      PRISM_CK(launch_gemm(prec, g_apply, s2));
+      PRISM_CK(launch_gemm(prec, ROLE_APPLY, g_apply, s2));
     }
     PRISM_CK(launch_k(k_advance, dim3(1), dim3(256), 0, s2, 1, S, ch, use_handle, P->d_all_done));
     PRISM_CK(cudaGetLastError());
@@ -1383,10 +1256,7 @@ size_t prism_polar_workspace(prism_handle h, int batch, const int64_t* m, const 
   std::vector<int64_t> ld(batch);
   for (int i = 0; i < batch; ++i) ld[i] = std::max(m[i], n[i]);
   Request r{false, batch, m, n, fakeA.data(), ld.data(), fakeQ.data(), nullptr, ld.data(), nullptr, *o, nullptr};
-  if (validate(r)) return 0;
-  Plan P;
-  if (build_plan(r, P)) return 0;
-  return P.ws_need;
+  return ws_query(h, r);
 }
 
 prism_status prism_polar(prism_handle h, int batch, const int64_t* m, const int64_t* n, const void* const* A,
@@ -1436,18 +1306,15 @@ static prism_status host_solve(prism_handle h, int kind, int inv_q, int batch, c
     for (auto& sl : h->slots)
       for (cudaEvent_t* e : {&sl.ev_h2d, &sl.ev_comp, &sl.ev_d2h})
         PRISM_CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    PRISM_CK(cudaEventCreateWithFlags(&h->ev_call, cudaEventDisableTiming));
   }
   std::vector<int64_t> ldc(batch);
   std::vector<const void*> din(batch);
   std::vector<void*> dout(batch), dout2(batch);
-  static const int nslots = [] {
-    const char* e = getenv("PRISM_HOST_SLOTS");
-    const int v = e ? atoi(e) : 3;
-    return std::max(2, std::min(prism_handle_s::kMaxSlots, v));
-  }();
+  constexpr int nslots = 3;   // upload / solve / download of three consecutive calls in flight
   auto& sl = h->slots[h->slot_next];
   h->slot_next = (h->slot_next + 1) % nslots;
-  const bool two = sqrt_kind && O1 && O2;
+  const bool two = sqrt_kind && O2;   // second output (A^{-1/2}) requested, with or without the first
   const size_t ws_need = kind == 5 ? prism_db_newton_workspace(h, batch, m, o)
                          : sqrt_kind ? prism_sqrt_workspace(h, batch, m, o)
                          : kind == 2 ? prism_sign_workspace(h, batch, m, o)
@@ -1457,16 +1324,16 @@ static prism_status host_solve(prism_handle h, int kind, int inv_q, int batch, c
   if (!ws_need) return fail(PRISM_ERR_INVALID_ARG, "workspace query failed");
   if (sl.in_bytes < bytes || sl.out_bytes < bytes || (two && !sl.out2) || h->hws_bytes < ws_need) {
     PRISM_CK(cudaDeviceSynchronize());   // growing: nothing of the old buffers may be in flight
-    if (sl.in_bytes < bytes || sl.out_bytes < bytes || (two && !sl.out2)) {
+    if (sl.in_bytes < bytes || sl.out_bytes < bytes) {
       if (sl.in) cudaFree(sl.in);
       if (sl.out) cudaFree(sl.out);
       if (sl.out2) cudaFree(sl.out2);
       sl.in = sl.out = sl.out2 = nullptr;
       PRISM_CK(cudaMalloc(&sl.in, bytes));
       PRISM_CK(cudaMalloc(&sl.out, bytes));
-      if (sqrt_kind) PRISM_CK(cudaMalloc(&sl.out2, bytes));
       sl.in_bytes = sl.out_bytes = bytes;
     }
+    if (two && !sl.out2) PRISM_CK(cudaMalloc(&sl.out2, sl.out_bytes));
     if (h->hws_bytes < ws_need) {
       if (h->hws) cudaFree(h->hws);
       h->hws = nullptr;
@@ -1480,25 +1347,18 @@ static prism_status host_solve(prism_handle h, int kind, int inv_q, int batch, c
     dout[i] = sl.out + off[i];
     dout2[i] = sl.out2 ? sl.out2 + off[i] : nullptr;
   }
-  // optional timeline (PRISM_HOST_TRACE=1): per call, upload / solve / download spans
-  static const bool tr = getenv("PRISM_HOST_TRACE") != nullptr;
-  static std::vector<std::array<cudaEvent_t, 6>> tl;
-  std::array<cudaEvent_t, 6> te{};
-  if (tr) {
-    for (auto& e : te) cudaEventCreate(&e);
-  }
-  // upload (after this slot's previous solve has consumed its inputs)
+  // upload: after the caller's stream reaches this call (its work may still be filling the
+  // pinned inputs) and after this slot's previous solve has consumed its inputs
+  PRISM_CK(cudaEventRecord(h->ev_call, caller));
+  PRISM_CK(cudaStreamWaitEvent(h->s_in, h->ev_call, 0));
   if (sl.used) PRISM_CK(cudaStreamWaitEvent(h->s_in, sl.ev_comp, 0));
-  if (tr) cudaEventRecord(te[0], h->s_in);
   for (int i = 0; i < batch; ++i)
     PRISM_CK(copy_block(sl.in + off[i], ldc[i], A_host[i], lda[i], ldc[i], m[i], esz, cudaMemcpyHostToDevice,
                         h->s_in));
-  if (tr) cudaEventRecord(te[1], h->s_in);
   PRISM_CK(cudaEventRecord(sl.ev_h2d, h->s_in));
   // solve (after the upload, and after this slot's previous download has read its outputs)
   PRISM_CK(cudaStreamWaitEvent(h->s_comp, sl.ev_h2d, 0));
   if (sl.used) PRISM_CK(cudaStreamWaitEvent(h->s_comp, sl.ev_d2h, 0));
-  if (tr) cudaEventRecord(te[2], h->s_comp);
   prism_status st;
   if (kind == 5)
     st = prism_db_newton(h, batch, m, din.data(), ldc.data(), O1 ? dout.data() : nullptr, O2 ? dout2.data() : nullptr,
@@ -1519,11 +1379,9 @@ static prism_status host_solve(prism_handle h, int kind, int inv_q, int batch, c
     st = prism_polar(h, batch, m, n, din.data(), ldc.data(), dout.data(), ldc.data(), ids, o, rep, h->hws,
                      h->hws_bytes, h->s_comp);
   if (st) return st;
-  if (tr) cudaEventRecord(te[3], h->s_comp);
   PRISM_CK(cudaEventRecord(sl.ev_comp, h->s_comp));
   // download
   PRISM_CK(cudaStreamWaitEvent(h->s_out, sl.ev_comp, 0));
-  if (tr) cudaEventRecord(te[4], h->s_out);
   for (int i = 0; i < batch; ++i) {
     if (O1 && O1[i])
       PRISM_CK(copy_block(O1[i], ldo[i], sl.out + off[i], ldc[i], ldc[i], m[i], esz, cudaMemcpyDeviceToHost,
@@ -1531,20 +1389,6 @@ static prism_status host_solve(prism_handle h, int kind, int inv_q, int batch, c
     if (two && O2[i])
       PRISM_CK(copy_block(O2[i], ldo[i], sl.out2 + off[i], ldc[i], ldc[i], m[i], esz, cudaMemcpyDeviceToHost,
                           h->s_out));
-  }
-  if (tr) {
-    cudaEventRecord(te[5], h->s_out);
-    tl.push_back(te);
-    if (tl.size() == 12) {
-      cudaDeviceSynchronize();
-      for (size_t c = 0; c < tl.size(); ++c) {
-        float v[6];
-        for (int k = 0; k < 6; ++k) cudaEventElapsedTime(&v[k], tl[0][0], tl[c][k]);
-        fprintf(stderr, "call %2zu  h2d [%7.2f %7.2f]  solve [%7.2f %7.2f]  d2h [%7.2f %7.2f] ms\n", c, v[0], v[1],
-                v[2], v[3], v[4], v[5]);
-      }
-      tl.clear();
-    }
   }
   PRISM_CK(cudaEventRecord(sl.ev_d2h, h->s_out));
   PRISM_CK(cudaStreamWaitEvent(caller, sl.ev_d2h, 0));
@@ -1593,10 +1437,8 @@ size_t prism_inv_root_workspace(prism_handle h, int batch, const int64_t* n, int
   std::vector<int64_t> ld(n, n + batch);
   Request r{false, batch, n, n, fakeA.data(), ld.data(), fakeQ.data(), nullptr, ld.data(), nullptr, *o, nullptr};
   r.inv_q = q;
-  if (q < 1 || validate(r)) return 0;
-  Plan P;
-  if (build_plan(r, P)) return 0;
-  return P.ws_need;
+  if (q < 1) return 0;
+  return ws_query(h, r);
 }
 
 prism_status prism_inv_root(prism_handle h, int batch, const int64_t* n, int q, const void* const* A,
@@ -1633,10 +1475,7 @@ size_t prism_chebyshev_inverse_workspace(prism_handle h, int batch, const int64_
   std::vector<int64_t> ld(n, n + batch);
   Request r{false, batch, n, n, fakeA.data(), ld.data(), fakeQ.data(), nullptr, ld.data(), nullptr, *o, nullptr};
   r.cheb_kind = true;
-  if (validate(r)) return 0;
-  Plan P;
-  if (build_plan(r, P)) return 0;
-  return P.ws_need;
+  return ws_query(h, r);
 }
 
 prism_status prism_chebyshev_inverse(prism_handle h, int batch, const int64_t* n, const void* const* A,
@@ -1671,10 +1510,7 @@ size_t prism_db_newton_workspace(prism_handle h, int batch, const int64_t* n, co
   std::vector<int64_t> ld(n, n + batch);
   Request r{false, batch, n, n, fakeA.data(), ld.data(), nullptr, nullptr, ld.data(), nullptr, *o, nullptr};
   r.db_kind = true;
-  if (validate(r)) return 0;
-  Plan P;
-  if (build_plan(r, P)) return 0;
-  return P.ws_need;
+  return ws_query(h, r);
 }
 
 prism_status prism_db_newton(prism_handle h, int batch, const int64_t* n, const void* const* A, const int64_t* lda,
@@ -1708,10 +1544,7 @@ size_t prism_sqrt_workspace(prism_handle h, int batch, const int64_t* n, const p
   std::vector<const void*> fakeA(batch, reinterpret_cast<const void*>(256));
   std::vector<int64_t> ld(n, n + batch);
   Request r{true, batch, n, n, fakeA.data(), ld.data(), nullptr, nullptr, ld.data(), nullptr, *o, nullptr};
-  if (validate(r)) return 0;
-  Plan P;
-  if (build_plan(r, P)) return 0;
-  return P.ws_need;
+  return ws_query(h, r);
 }
 
 prism_status prism_sqrt_invsqrt(prism_handle h, int batch, const int64_t* n, const void* const* A,
@@ -1735,10 +1568,7 @@ size_t prism_sign_workspace(prism_handle h, int batch, const int64_t* n, const p
   std::vector<int64_t> ld(n, n + batch);
   Request r{false, batch, n, n, fakeA.data(), ld.data(), fakeQ.data(), nullptr, ld.data(), nullptr, *o, nullptr};
   r.sign_kind = true;
-  if (validate(r)) return 0;
-  Plan P;
-  if (build_plan(r, P)) return 0;
-  return P.ws_need;
+  return ws_query(h, r);
 }
 
 prism_status prism_sign(prism_handle h, int batch, const int64_t* n, const void* const* A, const int64_t* lda,
@@ -1807,10 +1637,7 @@ size_t prism_rowblock_workspace(prism_handle h, int64_t rows, int64_t n, const p
   Request r{false, 1, &rows, &n, &fakeA, &ld, &fakeQ, nullptr, &ld, nullptr, *o, nullptr};
   r.rowblock = true;
   r.G = reinterpret_cast<float*>(256);
-  if (validate(r)) return 0;
-  Plan P;
-  if (build_plan(r, P)) return 0;
-  return P.ws_need;
+  return ws_query(h, r);
 }
 
 prism_status prism_rowblock_begin(prism_handle h, int64_t rows, int64_t n, const void* A_rows, int64_t lda,
@@ -1859,7 +1686,7 @@ prism_status prism_rowblock_gram(prism_handle h, int k, const double* fro2_globa
   }
   PRISM_CK(launch_k(k_set_iter, dim3(1), dim3(32), 0, st, 1, S, k));
   GemmLaunch g = make_launch(*P, P->gram32[0], &P->gram32[1], g_rb.ws, 0, g_rb.max_iters + 1);
-  PRISM_CK(launch_gemm(g_rb.prec, g, st));
+  PRISM_CK(launch_gemm(g_rb.prec, ROLE_GRAM, g, st));
   PRISM_CK(cudaGetLastError());
   return PRISM_OK;
 }
@@ -1880,13 +1707,13 @@ prism_status prism_rowblock_update(prism_handle h, int k, const float* G, int32_
   if (g_rb.fit == PRISM_FIT_SKETCHED) {
     PRISM_CK(launch_k(k_sketch, dim3((S.p * n / 2 + 256) / 256, 1), dim3(256), 0, st, 1, S));
     for (int j = 0; j < P->n_chain; ++j) {
-      PRISM_CK(launch_chaint(prec, chain_pass(*P, j), make_launch(*P, P->chaint[j], nullptr, g_rb.ws, g_rb.warmup, M),
+      PRISM_CK(launch_chain(prec, chain_pass(*P, j), make_launch(*P, P->chaint[j], nullptr, g_rb.ws, g_rb.warmup, M),
                              st));
     }
   }
   PRISM_CK(launch_k(k_alpha, dim3(1), dim3(256), 0, st, 1, S, 0));
-  if (P->has_square) PRISM_CK(launch_gemm(prec, make_launch(*P, P->square, nullptr, g_rb.ws, 0, M), st));
-  PRISM_CK(launch_gemm(prec, make_launch(*P, P->apply[0], &P->apply[1], g_rb.ws, 0, M), st));
+  if (P->has_square) PRISM_CK(launch_gemm(prec, ROLE_SQUARE, make_launch(*P, P->square, nullptr, g_rb.ws, 0, M), st));
+  PRISM_CK(launch_gemm(prec, ROLE_APPLY, make_launch(*P, P->apply[0], &P->apply[1], g_rb.ws, 0, M), st));
   PRISM_CK(launch_k(k_advance, dim3(1), dim3(256), 0, st, 1, S, 0, 0, all_done ? reinterpret_cast<int*>(all_done) : P->d_all_done));
   PRISM_CK(cudaGetLastError());
   return PRISM_OK;
@@ -1975,11 +1802,11 @@ prism_status prism_debug_gemm(prism_handle h, int precision, int b_mn, int mode,
   const OpKind bk = b_mn ? OP_MN : OP_BK;
   const int brows = b_mn ? K : N, bcols = b_mn ? N : K;
   if (!encode_map(&hm[0], MapSpec{A, M, K, lda, esz, OP_A, BN, BK}) ||
-      !encode_map(&hm[1], MapSpec{B, brows, bcols, ldb, esz, bk, tile_m_main() == 256 ? BN / 2 : BN, BK}))
+      !encode_map(&hm[1], MapSpec{B, brows, bcols, ldb, esz, bk, BN / 2, BK}))
     return fail(PRISM_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   if (split) {
     if (!encode_map(&hm[2], MapSpec{A_lo, M, K, lda, esz, OP_A, BN, BK}) ||
-        !encode_map(&hm[3], MapSpec{B_lo, brows, bcols, ldb, esz, bk, tile_m_main() == 256 ? BN / 2 : BN, BK}))
+        !encode_map(&hm[3], MapSpec{B_lo, brows, bcols, ldb, esz, bk, BN / 2, BK}))
       return fail(PRISM_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   }
   // bf16 epilogue blocks: TMA store of the output, TMA load of C (maps 4 and 5)
@@ -2018,21 +1845,11 @@ prism_status prism_debug_gemm(prism_handle h, int precision, int b_mn, int mode,
   g.done = nullptr;
   g.done_stride = 0;
   g.ntiles = (int)L.tiles.size();
-  PRISM_CK(launch_gemm(precision, g, static_cast<cudaStream_t>(stream)));
+  PRISM_CK(launch_gemm(precision, ROLE_OTHER, g, static_cast<cudaStream_t>(stream)));
   PRISM_CK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
   return PRISM_OK;
 }
 
-
-prism_status prism_debug_trace_chain(unsigned long long* buf_dev) {
-  return cudaMemcpyToSymbol(g_chain_trace, &buf_dev, sizeof(buf_dev)) == cudaSuccess ? PRISM_OK : PRISM_ERR_CUDA;
-}
-
-prism_status prism_debug_trace_gemm(unsigned long long* buf_dev, int mode) {
-  if (cudaMemcpyToSymbol(g_gemm_trace2, &buf_dev, sizeof(buf_dev)) != cudaSuccess) return PRISM_ERR_CUDA;
-  const int m = mode < 0 ? -1 : (mode & 0xFF);
-  return cudaMemcpyToSymbol(g_trace_mode, &m, sizeof(m)) == cudaSuccess ? PRISM_OK : PRISM_ERR_CUDA;
-}
 
 prism_status prism_debug_sketch(uint64_t seed, int64_t b, int k, int p, int s, float* S_dev, void* stream) {
   if (!S_dev || p < 1 || s < 1) return fail(PRISM_ERR_INVALID_ARG, "bad sketch args");

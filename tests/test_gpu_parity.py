@@ -104,7 +104,7 @@ def test_sqrt_fp32_parity(n, kappa, deg):
     assert abs(int(rep["iters"][0]) - ro.iters) <= 1
     assert _rel(X[0].double().cpu().numpy(), Xo) <= 1e-5
     # inverse root: cond(A^{-1/2}) ~ kappa^{1/2} amplifies; SURVEY §8(c) rows
-    assert _rel(Y[0].double().cpu().numpy(), Yo) <= (3e-5 if kappa <= 1e2 else 3e-4)
+    assert _rel(Y[0].double().cpu().numpy(), Yo) <= (1e-5 if kappa <= 1e2 else 3e-4)
 
 
 def test_batch_mixed_shapes_equals_single_solves():
@@ -202,25 +202,28 @@ def test_edge_cases():
     assert int(rep["status"][0]) == prism.MAX_ITERS and int(rep["iters"][0]) == 3
 
 
-def test_gpt2_batch_full_size_sampled():
-    """configs[1] at full size in the bench's launch configuration: 48 BF16
-    matrices in one call; 4 sampled matrices (one per shape) vs the oracle,
-    all 48 checked by the polar property ||Q^T Q - I|| (any size)."""
+def test_gpt2_mixed_batch_exactly_as_benchmarked():
+    """configs[1] at full size, the exact batch bench.py times (muon_batch(seed=1,
+    kind="mixed"): even members Gaussian MP, odd members HTMP-like kappa = 0.5), in one BF16
+    call with the bench's options: every one of the 48 matrices against the fp64 oracle.
+    MP members: <= 2e-2 and +-1 iteration (north_star).  HTMP members: SURVEY §8(c) gives the
+    kappa = 0.5 class no separate row; they are held to the same bar (measured 5.4e-3 -
+    9.4e-3, iterations equal) and the maximum is reported by bench.py (sampled rel_err)."""
     shapes = W.gpt2_small_shapes()
-    mats_np = W.muon_batch(shapes, seed=1, kind="gaussian")
+    mats_np = W.muon_batch(shapes, seed=1, kind="mixed")
     mats = [torch.tensor(a).to(torch.bfloat16).cuda() for a in mats_np]
-    Q, rep = P.polar(mats, degree=5, max_iters=20, tol=3e-2, seed=42, precision="bf16")
+    Q, rep = P.polar(mats, degree=5, max_iters=20, tol=3e-2, sketch_size=8, seed=42, precision="bf16",
+                     matrix_ids=list(range(48)))
     torch.cuda.synchronize()
     assert torch.all(rep["status"] == prism.CONVERGED)
+    errs = {"mp": [], "htmp": []}
     for i in range(48):
-        q = Q[i].double()
-        G = q.T @ q if q.shape[0] >= q.shape[1] else q @ q.T
-        s = G.shape[0]
-        assert float(torch.linalg.norm(G - torch.eye(s, device=G.device, dtype=G.dtype))) / s ** 0.5 <= 0.06
-    for i in (0, 1, 2, 3):
         Qo, ro = prism.polar(mats[i].double().cpu().numpy(), d=2, p=8, tol=3e-2, max_iters=20, seed=42, b=i)
-        assert abs(int(rep["iters"][i]) - ro.iters) <= 1
-        assert _rel(Q[i].double().cpu().numpy(), Qo) <= 2e-2
+        assert abs(int(rep["iters"][i]) - ro.iters) <= 1, (i, int(rep["iters"][i]), ro.iters)
+        e = _rel(Q[i].double().cpu().numpy(), Qo)
+        errs["mp" if i % 2 == 0 else "htmp"].append(e)
+        assert e <= 2e-2, (i, e)
+    print("gpt2 mixed batch: max rel err MP %.3e, HTMP %.3e" % (max(errs["mp"]), max(errs["htmp"])))
 
 
 def test_rowblock_two_ranks_emulated_equals_single_solve():
@@ -284,35 +287,18 @@ def test_sqrt_caller_outputs_equal_fresh_outputs():
         assert torch.equal(a, b)
 
 
-_EARLY_SCRIPT = r"""
-import sys, torch
-sys.path.insert(0, sys.argv[1])
-import paper_2601_22137_b200 as P
-from paper_2601_22137_b200 import workloads as W
-mats = [torch.tensor(W.gaussian(m, n, seed=7 + i)).to(torch.bfloat16).cuda()
-        for i, (m, n) in enumerate([(1024, 1024), (768, 2304), (3072, 768)])]
-Q, rep = P.polar(mats, degree=5, tol=3e-2, max_iters=20)
-torch.cuda.synchronize()
-torch.save({"Q": [q.cpu() for q in Q], "iters": rep["iters"].cpu()}, sys.argv[2])
-"""
-
-
 @pytest.mark.gpu
-def test_early_square_gemm_is_bit_identical(tmp_path):
-    """The square GEMM whose mainloop runs under k_alpha (GemmLaunch::early, bf16 polar
-    batches <= 16) computes exactly what the waiting launch computes."""
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    script = tmp_path / "early.py"
-    script.write_text(_EARLY_SCRIPT)
-    outs = {}
-    for flag in ("0", "1"):
-        out = tmp_path / f"q{flag}.pt"
-        env = dict(os.environ, PRISM_EARLY_SQUARE=flag)
-        subprocess.run([sys.executable, str(script), root, str(out)], check=True, env=env, timeout=600)
-        outs[flag] = torch.load(out)
-    assert torch.equal(outs["0"]["iters"], outs["1"]["iters"])
-    for a, b in zip(outs["0"]["Q"], outs["1"]["Q"]):
+def test_early_square_gemm_is_bit_identical():
+    """The square GEMM whose mainloop runs under k_alpha (bf16 polar batches <= 16 matrices:
+    only its epilogue waits for alpha) computes exactly what the waiting launch of a larger
+    batch computes: the same three matrices solved alone (early) and inside a batch of 17
+    (waiting) come out bit for bit equal."""
+    shapes = [(1024, 1024), (768, 2304), (3072, 768)]
+    mats = [torch.tensor(W.gaussian(m, n, seed=7 + i)).to(torch.bfloat16).cuda() for i, (m, n) in enumerate(shapes)]
+    filler = [torch.tensor(W.gaussian(256, 128, seed=50 + i)).to(torch.bfloat16).cuda() for i in range(14)]
+    Qe, re_ = P.polar(mats, degree=5, tol=3e-2, max_iters=20, matrix_ids=[0, 1, 2])
+    Qw, rw = P.polar(mats + filler, degree=5, tol=3e-2, max_iters=20, matrix_ids=list(range(17)))
+    torch.cuda.synchronize()
+    assert torch.equal(re_["iters"], rw["iters"][:3])
+    for a, b in zip(Qe, Qw[:3]):
         assert torch.equal(a, b)
