@@ -51,7 +51,8 @@ typedef enum {
   PRISM_ERR_INVALID_ARG = 1, /* null pointer, bad size/option, workspace too small */
   PRISM_ERR_UNSUPPORTED = 2, /* valid but not supported (e.g. sketch_size > 8, fit exact on device) */
   PRISM_ERR_CUDA = 3,        /* a CUDA runtime/driver call failed */
-  PRISM_ERR_INTERNAL = 4
+  PRISM_ERR_INTERNAL = 4,
+  PRISM_ERR_NCCL = 5         /* NCCL unavailable, or a collective / communicator failed */
 } prism_status;
 
 typedef enum {
@@ -76,7 +77,7 @@ typedef enum {
 typedef struct {
   int degree;          /* 3 ("PRISM-3", d=1: g = I + aR) or 5 ("PRISM-5", d=2: g = I + R/2 + aR^2) */
   int max_iters;       /* >= 1: maximum number of updates */
-  int sketch_size;     /* p, rows of the Gaussian sketch S_k, 1 <= p <= 8 ("as small as 5"); default 8 */
+  int sketch_size;     /* p, rows of the Gaussian sketch S_k; default 8; limits above */
   double tol;          /* > 0: stop before the update when ||R_k||_F <= tol * sqrt(s) (R12) */
   uint64_t seed;       /* Philox key; S_k depends only on (seed, matrix id, k) (R8) */
   int precision;       /* prism_precision */
@@ -95,7 +96,9 @@ typedef struct {
   float* resid_hist;   /* [batch * (max_iters + 1)] ||R_k||_F / sqrt(s), or NULL */
 } prism_report;
 
-/* Fill `o` with defaults: degree 5, max_iters 30, p 8, tol 1e-6, seed 42, BF16, sketched, no warmup. */
+/* Fill `o` with defaults: degree 5, max_iters 30, p 8, tol 1e-6, seed 42, BF16, sketched, no warmup.
+ * sketch_size p: 1 <= p <= min(s, 32) for polar / sqrt / sign ("as small as 5"; Theorem 2,
+ * P:229, asks for more); 1 <= p <= min(s, 8) for the inverse root and Chebyshev kinds. */
 void prism_default_options(prism_options* o);
 
 prism_status prism_create(prism_handle* h);
@@ -242,25 +245,98 @@ prism_status prism_sqrt_invsqrt_host(prism_handle h, int batch, const int64_t* n
  */
 prism_status prism_lpt_partition(int batch, const double* cost, int ranks, int32_t* owner);
 
-/*
- * Row-block split of ONE tall polar problem across ranks (C4: 8192^2 over
- * 2/4/8 GPUs).  Rank r holds rows [row0, row0 + rows) of the global m x n matrix A.
- * Per iteration k the caller all-reduces (sums) the n x n fp32 partial Gram G = X_r^T X_r
- * between prism_rowblock_gram and prism_rowblock_update (e.g. NCCL all_reduce on `stream`);
- * every rank then forms the identical R = I - G, sketch S_k (matrix id 0), alpha_k and
- * P, and updates its own rows X_r <- X_r g_d(R; alpha_k).  Sequence:
- *   begin (writes the local sum of squares to fro2_local[0]) -> all-reduce fro2 ->
- *   for k = 0..max_iters: gram(k) -> all-reduce G -> update(k) -> stop when *all_done;
- *   end (writes Q_rows and the report).  One row-block solve per host thread at a time.
- * G: n x n fp32 device buffer (ld n); all_done: device int32 (1 once converged / stopped).
+/* ---- multi-GPU: one process per GPU ----------------------------------
+ *
+ * Exchange layer.  The multi-GPU entry points move data only through a transport: the
+ * library's NCCL transport (prism_nccl_transport) or any caller-supplied one (a test
+ * harness).  Every function returns 0 on success; the operation is enqueued on `stream`
+ * (a cudaStream_t) or completed before returning.  Buffers are DEVICE memory.
  */
-size_t prism_rowblock_workspace(prism_handle h, int64_t rows, int64_t n, const prism_options* o);
-prism_status prism_rowblock_begin(prism_handle h, int64_t rows, int64_t n, const void* A_rows, int64_t lda,
-                                  void* Q_rows, int64_t ldq, float* G, double* fro2_local, const prism_options* o,
-                                  void* workspace, size_t ws_bytes, void* stream);
-prism_status prism_rowblock_gram(prism_handle h, int k, const double* fro2_global, void* stream);
-prism_status prism_rowblock_update(prism_handle h, int k, const float* G, int32_t* all_done, void* stream);
-prism_status prism_rowblock_end(prism_handle h, const prism_report* rep, void* stream);
+typedef enum { PRISM_DT_F32 = 0, PRISM_DT_F64 = 1, PRISM_DT_I32 = 2, PRISM_DT_BYTES = 3 } prism_dtype;
+typedef struct {
+  void* ctx;
+  int nranks;
+  int rank;
+  /* recv[i] = sum over ranks of send[i], i < count (send may equal recv) */
+  int (*allreduce_sum)(void* ctx, const void* send, void* recv, size_t count, int dtype, void* stream);
+  /* buf (bytes) of rank `root` copied into buf on every rank */
+  int (*broadcast)(void* ctx, void* buf, size_t bytes, int root, void* stream);
+  int (*group_start)(void* ctx);   /* bracket several collectives (may be NULL) */
+  int (*group_end)(void* ctx);
+  int (*async_error)(void* ctx);   /* non-zero once the communicator has failed (may be NULL) */
+} prism_transport;
+
+/*
+ * NCCL, resolved at run time from the libnccl.so.2 the process has loaded (torch's bundled
+ * NCCL after `import torch`; else the system one): the library does not link NCCL, so one
+ * NCCL serves the caller and the library.  `comm` is an ncclComm_t of that NCCL — from
+ * prism_nccl_comm_init, or the caller's own.  id: 128-byte ncclUniqueId (rank 0 creates it,
+ * the caller distributes it).  Errors: PRISM_ERR_NCCL (library not found, call failed).
+ */
+prism_status prism_nccl_get_unique_id(void* id);
+prism_status prism_nccl_comm_init(void** comm, int nranks, const void* id, int rank);
+prism_status prism_nccl_comm_destroy(void* comm);
+prism_status prism_nccl_transport(void* comm, prism_transport* tr);
+
+/*
+ * Sharded batch (BASELINE configs[4]; problem statement P:18): every
+ * rank passes the SAME full batch (a data-parallel step's reduced gradients).  Matrices are
+ * assigned to ranks by prism_shard_plan (LPT on F_min, deterministic), each rank solves its
+ * share with prism_polar in `nbuckets` sub-batches with the GLOBAL matrix index as sketch id
+ * (so every result is bit-identical to the single-GPU solve of the whole batch), writing
+ * straight into Q[i]; after each sub-batch the owners broadcast its outputs, so the exchange
+ * of bucket j overlaps the solve of bucket j+1.  On return every rank's Q holds all outputs
+ * once `stream` completes.  Q[i] must not alias A[i] on a non-owner (it is overwritten by the
+ * broadcast of rows m x ldq, including the padding between rows).  rep (device, [batch]
+ * layout as prism_polar, optional) receives every matrix's report on every rank.
+ * Workspace: prism_polar_sharded_workspace bytes (depends on nranks / rank).
+ */
+size_t prism_polar_sharded_workspace(prism_handle h, int nranks, int rank, int batch, const int64_t* m,
+                                     const int64_t* n, const prism_options* o, int nbuckets);
+prism_status prism_polar_sharded(prism_handle h, void* comm, int batch, const int64_t* m, const int64_t* n,
+                                 const void* const* A, const int64_t* lda, void* const* Q, const int64_t* ldq,
+                                 const prism_options* o, int nbuckets, const prism_report* rep, void* workspace,
+                                 size_t ws_bytes, void* stream);
+prism_status prism_polar_sharded_tr(prism_handle h, const prism_transport* tr, int batch, const int64_t* m,
+                                    const int64_t* n, const void* const* A, const int64_t* lda, void* const* Q,
+                                    const int64_t* ldq, const prism_options* o, int nbuckets,
+                                    const prism_report* rep, void* workspace, size_t ws_bytes, void* stream);
+/* The plan (host only): owner[i] in [0, nranks) and bucket[i] in [0, nbuckets) of matrix i. */
+prism_status prism_shard_plan(int batch, const int64_t* m, const int64_t* n, int degree, int sketch_size, int nranks,
+                              int nbuckets, int32_t* owner, int32_t* bucket);
+
+/*
+ * Row-block split of ONE polar problem too large for one GPU (BASELINE
+ * configs[3], 8192^2 over 2/4/8 GPUs; the iteration is Table 1).  Rank r holds
+ * rows [row0, row0 + rows) of the global m_global x n matrix A (rows summed over ranks =
+ * m_global).  Per iteration k every rank
+ *   1. forms its partial Gram X_r^T X_r (symmetric: upper-triangle tiles only) as fp32
+ *      panels of 256 rows, packed (panel t: rows [256t, 256t+256) x columns [256t, n)),
+ *      and all-reduces (sums) each panel group as soon as it is computed, overlapping the
+ *      rest of the Gram;
+ *   2. unpacks R = I - G, runs the sketch (matrix id 0), chain and alpha fit — identical
+ *      inputs on every rank, so alpha_k and the stop decision are identical;
+ *   3. updates its rows with no R^2 and no second collective: d = 2: Y_r = X_r R and
+ *      X_r' = (X_r + Y_r / 2) + alpha Y_r R; d = 1: X_r' = X_r + alpha X_r R
+ *      (= X_r g_d(R_k; alpha_k): 5 (rows) n^2 FLOP per rank per iteration for d = 2).
+ * The host loop stays ahead of the device: after enqueuing iteration k it waits only for
+ * iteration k's stop test (its updates still queued) before deciding to enqueue k + 1, so
+ * the call returns once the iteration count is known, with the tail enqueued on `stream`.
+ * Q_rows receives rows [row0, row0 + rows) of U V^T (may alias A_rows).  rep: [1] (device).
+ */
+size_t prism_polar_rowblock_workspace(prism_handle h, int64_t rows, int64_t n, const prism_options* o);
+prism_status prism_polar_rowblock(prism_handle h, void* comm, int64_t m_global, int64_t n, const void* A_rows,
+                                  int64_t row0, int64_t rows, int64_t lda, void* Q_rows, int64_t ldq,
+                                  const prism_options* o, const prism_report* rep, void* workspace, size_t ws_bytes,
+                                  void* stream);
+prism_status prism_polar_rowblock_tr(prism_handle h, const prism_transport* tr, int64_t m_global, int64_t n,
+                                     const void* A_rows, int64_t row0, int64_t rows, int64_t lda, void* Q_rows,
+                                     int64_t ldq, const prism_options* o, const prism_report* rep, void* workspace,
+                                     size_t ws_bytes, void* stream);
+/* Packed Gram layout (host only): panel_off[t] = float offset of panel t (t = 0..ceil(n/256)),
+ * panel_off[ceil(n/256)] = total floats; group_end[g] = first panel after group g (groups
+ * of about equal tile counts, g < ngroups). */
+prism_status prism_rowblock_layout(int64_t n, int ngroups, int64_t* panel_off, int32_t* group_end);
 
 /* Per-iteration F_min (symmetric products counted once) of a polar solve. */
 double prism_polar_flops_per_iter(int64_t m, int64_t n, int degree, int sketch_size);

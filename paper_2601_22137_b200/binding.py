@@ -50,6 +50,29 @@ class Report(ctypes.Structure):
     ]
 
 
+# prism_transport (include/prism.h): exchange callbacks of the multi-GPU entry points
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                                ctypes.c_int, ctypes.c_void_p)
+BROADCAST_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int,
+                                ctypes.c_void_p)
+GROUP_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p)
+
+
+class Transport(ctypes.Structure):
+    _fields_ = [
+        ("ctx", ctypes.c_void_p),
+        ("nranks", ctypes.c_int),
+        ("rank", ctypes.c_int),
+        ("allreduce_sum", ALLREDUCE_FN),
+        ("broadcast", BROADCAST_FN),
+        ("group_start", GROUP_FN),
+        ("group_end", GROUP_FN),
+        ("async_error", GROUP_FN),
+    ]
+
+
+DT = {"f32": 0, "f64": 1, "i32": 2, "bytes": 3}
+
 # ---------------------------------------------------------------- signatures
 _vp, _i32, _i64, _dbl, _u64, _sz = (ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double,
                                     ctypes.c_uint64, ctypes.c_size_t)
@@ -57,6 +80,8 @@ _i64p = ctypes.POINTER(ctypes.c_int64)
 _vpp = ctypes.POINTER(ctypes.c_void_p)
 _opt = ctypes.POINTER(Options)
 _rep = ctypes.POINTER(Report)
+_trp = ctypes.POINTER(Transport)
+_i32p = ctypes.POINTER(ctypes.c_int32)
 _ST = ctypes.c_int   # prism_status
 
 # name -> (restype, argtypes); EXPORTS is exactly the symbol set include/prism.h declares
@@ -90,11 +115,21 @@ _SIGS = {
     "prism_db_newton_host": (_ST, [_vp, _i32, _i64p, _vpp, _i64p, _vpp, _vpp, _i64p, _i64p, _opt, _rep, _vp]),
     # multi-GPU
     "prism_lpt_partition": (_ST, [_i32, ctypes.POINTER(_dbl), _i32, ctypes.POINTER(ctypes.c_int32)]),
-    "prism_rowblock_workspace": (_sz, [_vp, _i64, _i64, _opt]),
-    "prism_rowblock_begin": (_ST, [_vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _opt, _vp, _sz, _vp]),
-    "prism_rowblock_gram": (_ST, [_vp, _i32, _vp, _vp]),
-    "prism_rowblock_update": (_ST, [_vp, _i32, _vp, _vp, _vp]),
-    "prism_rowblock_end": (_ST, [_vp, _rep, _vp]),
+    "prism_nccl_get_unique_id": (_ST, [_vp]),
+    "prism_nccl_comm_init": (_ST, [ctypes.POINTER(_vp), _i32, _vp, _i32]),
+    "prism_nccl_comm_destroy": (_ST, [_vp]),
+    "prism_nccl_transport": (_ST, [_vp, _trp]),
+    "prism_shard_plan": (_ST, [_i32, _i64p, _i64p, _i32, _i32, _i32, _i32, _i32p, _i32p]),
+    "prism_polar_sharded_workspace": (_sz, [_vp, _i32, _i32, _i32, _i64p, _i64p, _opt, _i32]),
+    "prism_polar_sharded": (_ST, [_vp, _vp, _i32, _i64p, _i64p, _vpp, _i64p, _vpp, _i64p, _opt, _i32, _rep, _vp, _sz,
+                                  _vp]),
+    "prism_polar_sharded_tr": (_ST, [_vp, _trp, _i32, _i64p, _i64p, _vpp, _i64p, _vpp, _i64p, _opt, _i32, _rep, _vp,
+                                     _sz, _vp]),
+    "prism_polar_rowblock_workspace": (_sz, [_vp, _i64, _i64, _opt]),
+    "prism_polar_rowblock": (_ST, [_vp, _vp, _i64, _i64, _vp, _i64, _i64, _i64, _vp, _i64, _opt, _rep, _vp, _sz, _vp]),
+    "prism_polar_rowblock_tr": (_ST, [_vp, _trp, _i64, _i64, _vp, _i64, _i64, _i64, _vp, _i64, _opt, _rep, _vp, _sz,
+                                      _vp]),
+    "prism_rowblock_layout": (_ST, [_i64, _i32, _i64p, _i32p]),
     # measurement
     "prism_polar_flops_per_iter": (_dbl, [_i64, _i64, _i32, _i32]),
     "prism_sqrt_flops_per_iter": (_dbl, [_i64, _i32, _i32]),
@@ -421,53 +456,6 @@ def db_newton_host(mats, want_sqrt=True, want_invsqrt=True, out_sqrt=None, out_i
     kw.pop("sketch_size", None)
     return _solve("db_newton", mats, host=True, want1=want_sqrt, want2=want_invsqrt, out=out_sqrt,
                   out2=out_invsqrt, precision=precision, **kw)
-
-
-class RowBlockSolver:
-    """C-ABI steps of the row-block split (prism_rowblock_*): marshalling only."""
-
-    def __init__(self, A_rows, degree=5, max_iters=30, sketch_size=8, tol=1e-6, seed=42, precision=None,
-                 fit="sketched", warmup_iters=0, alpha_lo=None, alpha_hi=None, handle=None, stream=None):
-        import torch
-        precision = _precision_of(A_rows, precision)
-        _check_dtype([A_rows], precision)
-        self.A = A_rows
-        self.dev = A_rows.device
-        self.h = handle or Handle()
-        self.o = make_options(degree, max_iters, sketch_size, tol, seed, precision, fit, warmup_iters, alpha_lo,
-                              alpha_hi)
-        self.max_iters = max_iters
-        rows, n = A_rows.shape
-        self.Q = torch.empty_like(A_rows)
-        self.G = torch.empty(n, n, dtype=torch.float32, device=self.dev)
-        self.fro2 = torch.zeros(1, dtype=torch.float64, device=self.dev)
-        self.done = torch.zeros(1, dtype=torch.int32, device=self.dev)
-        self.rb = _report_buffers(1, max_iters, self.dev)
-        need = lib().prism_rowblock_workspace(self.h.h, rows, n, ctypes.byref(self.o))
-        if need == 0:
-            raise PrismError("prism_rowblock_workspace rejected the arguments: " + lib().prism_last_error().decode())
-        self.stream = stream if stream is not None else torch.cuda.current_stream(self.dev)
-        self.ws = self.h.workspace(need, self.dev, self.stream)
-        self._s = ctypes.c_void_p(self.stream.cuda_stream)
-
-    def begin(self):
-        rows, n = self.A.shape
-        check(lib().prism_rowblock_begin(self.h.h, rows, n, self.A.data_ptr(), self.A.stride(0), self.Q.data_ptr(),
-                                         self.Q.stride(0), self.G.data_ptr(), self.fro2.data_ptr(),
-                                         ctypes.byref(self.o), self.ws.data_ptr(), self.ws.numel(), self._s),
-              "prism_rowblock_begin")
-
-    def gram(self, k):
-        check(lib().prism_rowblock_gram(self.h.h, int(k), self.fro2.data_ptr(), self._s), "prism_rowblock_gram")
-
-    def update(self, k):
-        check(lib().prism_rowblock_update(self.h.h, int(k), self.G.data_ptr(), self.done.data_ptr(), self._s),
-              "prism_rowblock_update")
-
-    def end(self):
-        rep = _report_struct(self.rb)
-        check(lib().prism_rowblock_end(self.h.h, ctypes.byref(rep), self._s), "prism_rowblock_end")
-        return self.Q, self.rb
 
 
 def lpt_partition(costs, ranks: int):

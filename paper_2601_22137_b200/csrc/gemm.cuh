@@ -16,6 +16,9 @@
 //          which also builds the inverse-Newton polynomials (I + αR)^q − I, P:560-561,
 //          the DB Newton updates (1−α)X + αX·M⁻¹, and its Schur sweeps)
 //   STORE  out = D                (tests)
+//   GRAM32 out = D as fp32 packed upper-triangle panels (row-block partial Gram, summed
+//                                 across ranks)
+//   APPLY2 out = C + ½·D, out2 = D  (row-block d = 2: X_r + ½Y_r and Y_r = X_r R)
 // `sym` schedules only tiles touching the upper triangle and mirrors the
 // stores, so XᵀX and R·R cost half a dense GEMM and R, P are exactly symmetric.
 //
@@ -31,7 +34,8 @@
 
 namespace prism {
 
-enum EpiMode : int { EPI_RESID = 0, EPI_POLY = 1, EPI_APPLY = 2, EPI_STORE = 3, EPI_CHAIN = 4, EPI_GRAM32 = 5 };
+enum EpiMode : int { EPI_RESID = 0, EPI_POLY = 1, EPI_APPLY = 2, EPI_STORE = 3, EPI_CHAIN = 4, EPI_GRAM32 = 5,
+                     EPI_APPLY2 = 6 };
 
 // Sketch-chain pass codes (EPI_CHAIN).  The thin GEMM computes
 // D = R · [W_hi | W_lo] (N = 2w) and the epilogue forms out = D_hi + D_lo, then
@@ -66,8 +70,11 @@ struct GemmProblem {
   const CUtensorMap* tmB_lo;
   const CUtensorMap* tmC;   // bf16 epilogue: 32 x 32 blocks of C (TMA load) and of out (TMA store)
   const CUtensorMap* tmO;
+  const CUtensorMap* tmO2;  // EPI_APPLY2: second output (bf16 TMA store)
   void* out;
   void* out_lo;
+  void* out2;               // EPI_APPLY2: out2 = D (same leading dimension as out)
+  void* out2_lo;
   const void* C;
   const void* C_lo;
   float* norm_part;      // [tiles_m * tiles_n] per-tile Σ out² (RESID) or null
@@ -113,6 +120,7 @@ struct GemmLaunch {
   // alpha).  Tiles are then skipped by stop_iter < k (final for earlier iterations; a
   // matrix stopping at k, decided concurrently, is computed by every role alike)
   int early;
+  int max_ctas;                  // > 0: persistent grid capped (row-block Gram: SMs left to NCCL)
 };
 
 // The problem fields the tile epilogue needs, held in registers for the tile: read
@@ -124,6 +132,8 @@ struct EpiArgs {
   float* gdiag;
   long long ldo;
   int M, N;
+  void* out2;
+  void* out2_lo;
 };
 
 template <int KIND_, bool SPLIT_, int BN_ = 0, bool CTA2_ = (BN_ == 0)>
@@ -428,30 +438,65 @@ __device__ __forceinline__ void warp_store_f32_staged(void* out, void* out_lo, l
   }
 }
 
-// Row-block partial Gram (EPI_GRAM32): out = D in plain fp32 whatever the compute
-// dtype (the partial Grams are summed across ranks), symmetric triangle + mirror.
+// Row-block partial Gram (EPI_GRAM32): D in plain fp32 whatever the compute dtype (the
+// partial Grams are summed across ranks), upper triangle only, packed by 256-row panels:
+// panel t holds rows [256t, 256t + 256) x columns [256t, N), row-major with leading
+// dimension N - 256t, at float offset 256 (t N - 128 t (t - 1)) (= prism_rowblock_layout).
+__device__ __forceinline__ long long gram_panel_off(long long t, long long N) { return 256 * (t * N - 128 * t * (t - 1)); }
 __device__ __forceinline__ void epi_gram32(const EpiArgs& P, int i0, int lane, int j0, const float (&d)[32],
                                            float* tb) {
-  if (i0 >= P.M || j0 >= P.N || j0 + 31 < i0) return;   // warp-uniform
+  if (i0 >= P.M || j0 >= P.N || j0 + 31 < i0) return;   // warp-uniform: strictly lower blocks are not stored
+  const long long t = i0 >> 8, w = P.N - 256 * t;
+  float* base = static_cast<float*>(P.out) + gram_panel_off(t, P.N);
+  const int r0 = i0 - 256 * (int)t, c0 = j0 - 256 * (int)t;
+  if (j0 >= i0 + 32 && j0 + 32 <= P.N && i0 + 32 <= P.M && (w & 3) == 0) {
+    // whole block above the diagonal: staged, 16-B coalesced stores (4 rows x 128 B per instruction)
+#pragma unroll
+    for (int u = 0; u < 32; ++u) tb[lane * 33 + u] = d[u];
+    __syncwarp();
+    warp_store_f32_staged<false, false>(base, nullptr, w, r0, c0, tb, lane);
+    __syncwarp();
+    return;
+  }
   const int i = i0 + lane;
-  float* out = static_cast<float*>(P.out);
   if (i < P.M) {
 #pragma unroll
     for (int u = 0; u < 32; ++u) {
       const int j = j0 + u;
-      if (j >= i && j < P.N) out[(long long)i * P.ldo + j] = d[u];
+      if (j >= i && j < P.N) base[(long long)(r0 + lane) * w + c0 + u] = d[u];
     }
   }
+}
+
+// Row-block APPLY2, fp32 / 3xTF32 kernels: out = coefC C + coefA D and out2 = D.
+template <class Cfg>
+__device__ __forceinline__ void epi_apply2(const EpiArgs& P, int i0, int lane, int j0, float coefA, float coefC,
+                                           const float (&d)[32], const float (&c)[32], float* tb) {
+  if (i0 >= P.M || j0 >= P.N) return;
+  float v[32];
 #pragma unroll
-  for (int u = 0; u < 32; ++u) tb[lane * 33 + u] = d[u];
-  __syncwarp();
-  const int j = j0 + lane;
-  if (j < P.N) {
+  for (int u = 0; u < 32; ++u) v[u] = coefC * c[u] + coefA * d[u];
+  const int i = i0 + lane;
+  if (j0 + 32 <= P.N && i0 + 32 <= P.M && (P.ldo & 3) == 0) {
 #pragma unroll
-    for (int u = 0; u < 32; ++u)
-      if (i0 + u < j && i0 + u < P.M) out[(long long)j * P.ldo + i0 + u] = tb[u * 33 + lane];
+    for (int u = 0; u < 32; ++u) tb[lane * 33 + u] = v[u];
+    __syncwarp();
+    warp_store_f32_staged<Cfg::SPLIT, false>(P.out, P.out_lo, P.ldo, i0, j0, tb, lane);
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < 32; ++u) tb[lane * 33 + u] = d[u];
+    __syncwarp();
+    warp_store_f32_staged<Cfg::SPLIT, false>(P.out2, P.out2_lo, P.ldo, i0, j0, tb, lane);
+    __syncwarp();
+    return;
   }
-  __syncwarp();
+  if (i >= P.M) return;
+  const long long off = (long long)i * P.ldo + j0;
+  for (int u = 0; u < 32; ++u)
+    if (j0 + u < P.N) {
+      store_elem<Cfg::KIND, Cfg::SPLIT>(P.out, P.out_lo, off + u, v[u]);
+      store_elem<Cfg::KIND, Cfg::SPLIT>(P.out2, P.out2_lo, off + u, d[u]);
+    }
 }
 
 // Fused epilogue for one 32 x 32 block: rows i0 + lane (one row per lane of an
@@ -465,6 +510,7 @@ __device__ __forceinline__ void epi_segment(const EpiArgs& P, int mode, bool sym
                                             float coefA, float coefC, const float (&d)[32], const float (&c)[32],
                                             float* tb, float& sumsq) {
   if (mode == EPI_GRAM32) { epi_gram32(P, i0, lane, j0, d, tb); return; }
+  if (mode == EPI_APPLY2) { epi_apply2<Cfg>(P, i0, lane, j0, coefA, coefC, d, c, tb); return; }
   if (i0 >= P.M || j0 >= P.N) return;            // warp-uniform
   if (sym && j0 + 31 < i0) return;               // block strictly below the diagonal
   const int i = i0 + lane;
@@ -1147,20 +1193,20 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
       const int tn = code & 1023;
       const int mode = P.mode;
       const bool sym = P.sym != 0;
-      const EpiArgs ea{P.out, P.out_lo, P.gdiag, P.ldo, P.M, P.N};
+      const EpiArgs ea{P.out, P.out_lo, P.gdiag, P.ldo, P.M, P.N, P.out2, P.out2_lo};
       const void* const Cp = P.C;
       const long long ldc = P.ldc;
       const int i0 = tm * Cfg::TILE_M + (int)rank * Cfg::BM + q * 32;
       const int i = i0 + lane;                     // output row of this thread
       float coefA = 1.f, coefC = 1.f;
-      if (mode == EPI_POLY || mode == EPI_APPLY) {
+      if (mode == EPI_POLY || mode == EPI_APPLY || mode == EPI_APPLY2) {
         const double al = (P.eA | P.eC) ? *P.alpha : 1.0;
         const double pa = P.eA == 0 ? 1.0 : P.eA == 1 ? al : P.eA == 2 ? al * al : al * al * al;
         const double pc = P.eC == 0 ? 1.0 : P.eC == 1 ? al : P.eC == 2 ? al * al : al * al * al;
         coefA = static_cast<float>((double)P.kA * pa + (double)P.lA);
         coefC = static_cast<float>((double)P.c1 * pc + (double)P.lC);
       }
-      const bool needC = (mode == EPI_POLY || mode == EPI_APPLY);
+      const bool needC = (mode == EPI_POLY || mode == EPI_APPLY || mode == EPI_APPLY2);
       float sumsq = 0.f;
 
       if constexpr (Cfg::KIND == 0) {
@@ -1211,6 +1257,22 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
           if (mode == EPI_GRAM32) {
             // row-block partial Gram: plain fp32 stores (the warp's buffers as transpose scratch)
             epi_gram32(ea, i0, lane, jb + ch * 32, d, reinterpret_cast<float*>(wb));
+          } else if (mode == EPI_APPLY2) {
+            // row-block d = 2: X + Y/2 and Y = X R, both staged as bf16 blocks and TMA-stored
+            if (lane == 0) bulk_wait_read<0>();
+            __syncwarp();
+            float v[32];
+#pragma unroll
+            for (int u = 0; u < 32; ++u) v[u] = coefC * c[u] + coefA * d[u];
+            stage_row_bf16(v, wb + 4096, lane);
+            stage_row_bf16(d, wb + 6144, lane);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(tmO, wb + 4096, jb + ch * 32, i0);
+              tma_store_2d(P.tmO2, wb + 6144, jb + ch * 32, i0);
+              bulk_commit();
+            }
           } else {
             if (lane == 0) {
               if (sym) bulk_wait_read<0>();

@@ -1,0 +1,16 @@
+// Host-side hooks shared by the translation units of libprism.so (defined in prism.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "../../include/prism.h"
+
+namespace prism {
+// Record `msg` as the calling thread's last error (prism_last_error) and return `s`.
+prism_status fail_ext(prism_status s, const std::string& msg);
+// The handle's auxiliary (communication) stream on the current device, created on first use.
+cudaStream_t handle_aux_stream(prism_handle h);
+// Reusable event `idx` (< 16) of the handle on the current device (timing disabled).
+cudaEvent_t handle_event(prism_handle h, int idx);
+}  // namespace prism

@@ -50,8 +50,8 @@ struct MatDesc {
   float* keep;         // [4][s][p] kept chain columns (fp32)
   double* chain_part;  // [tiles_m][6] per-tile <Va,Vb>
   long long ldS;
-  int chain_tiles;
-  int pad2_;
+  int chain_tiles;     // <Va,Vb> partial groups: nchunk x ceil(s / 32)
+  int nchunk;          // sketch column chunks (p <= 8: 1; else ceil(p / 8), W / keep per chunk)
   // DB Newton (fp32 3xTF32 only): M_k (plain fp32, ld ldx), Gauss-Jordan sweep temporaries
   // (E = row block of W, T = D E, D = pivot inverse; hi + lo planes), W = R / R_lo,
   // per-tile (<E1,E1>, <E1,E2>, <E2,E2>) for the alpha fit
@@ -216,37 +216,49 @@ __global__ void k_set_c(SolveParams P) {
   if (threadIdx.x == 0) P.st[blockIdx.x].c = sqrt(P.fro2_in[blockIdx.x]);
 }
 
-__global__ void k_set_iter(SolveParams P, int k) {
-  griddep_wait();
-  griddep_launch();
-  if (threadIdx.x == 0) *P.iter = k;
-}
-
 __device__ __forceinline__ void store_x(void* hi, void* lo, long long idx, float v, int precision);
 
-// row-block: R = I - G from the all-reduced fp32 Gram (n x n, ld n), diag(G), and the
-// per-tile sum of R^2 in the layout the alpha kernel reads (tiles of 128 x bn, sym = 0).
+// Row-block: R = I - G from the all-reduced packed fp32 Gram (upper-triangle
+// panels, gemm.cuh epi_gram32), diag(G) in fp32, and the per-64x64-tile sum of R^2 that
+// k_alpha reads as the norm partials (tiles_m = tiles_n = ceil(n / 64), sym = 0).  The source
+// block of an R block below the diagonal is the transposed upper block, staged through smem so
+// both the packed reads and the R writes are coalesced.  grid (ceil(n/64), ceil(n/64)).
 template <int PREC>
-__global__ void __launch_bounds__(256) k_resid_from_gram(SolveParams P, const float* G, int bn) {
+__global__ void __launch_bounds__(256) k_resid_packed(SolveParams P, const float* Gp) {
   griddep_wait();
   griddep_launch();
+  __shared__ float tile[64][65];
   __shared__ double scratch[8];
   const MatDesc& D = P.mats[0];
   if (P.st[0].done) return;
   const int n = D.s;
-  const int tm = blockIdx.y, tn = blockIdx.x;
+  const int bx = blockIdx.x, by = blockIdx.y;    // R rows [64 by, +64), columns [64 bx, +64)
+  const bool upper = bx >= by;
+  const int rs = 64 * (upper ? by : bx), cs = 64 * (upper ? bx : by);   // upper source block
+  for (int e = threadIdx.x; e < 64 * 64; e += 256) {
+    const int r = e >> 6, c = e & 63;
+    const long long i = rs + r, j = cs + c;
+    float g = 0.f;
+    if (i < n && j < n && j >= i) {
+      const long long t = i >> 8;
+      g = Gp[gram_panel_off(t, n) + (i - 256 * t) * (n - 256 * t) + (j - 256 * t)];
+    }
+    tile[r][c] = g;
+  }
+  __syncthreads();
   double acc = 0.0;
-  for (int e = threadIdx.x; e < 128 * bn; e += 256) {
-    const int i = tm * 128 + e / bn, j = tn * bn + e % bn;
+  for (int e = threadIdx.x; e < 64 * 64; e += 256) {
+    const int rr = e >> 6, cc = e & 63;
+    const int i = 64 * by + rr, j = 64 * bx + cc;
     if (i >= n || j >= n) continue;
-    const float g = G[(long long)i * n + j];
-    const float r = (i == j ? 1.f : 0.f) - g;
-    store_x(D.R, D.R_lo, (long long)i * D.ldr + j, r, PREC);
+    const float g = (upper && j >= i) ? tile[rr][cc] : tile[cc][rr];
+    const float rv = (i == j ? 1.f : 0.f) - g;
+    store_x(D.R, D.R_lo, (long long)i * D.ldr + j, rv, PREC);
     if (i == j) D.gdiag[i] = g;
-    acc += (double)r * r;
+    acc += (double)rv * rv;
   }
   acc = block_sum<double, 256>(acc, scratch);
-  if (threadIdx.x == 0) D.norm_part[tm * D.tiles_n + tn] = (float)acc;
+  if (threadIdx.x == 0) D.norm_part[by * D.tiles_n + bx] = (float)acc;
 }
 
 __device__ __forceinline__ void store_x(void* hi, void* lo, long long idx, float v, int precision) {
@@ -846,7 +858,11 @@ __global__ void __launch_bounds__(256) k_sketch(SolveParams P) {
     const int row = (int)(q / s), col = (int)(q - (long long)row * s);
     const float v = __double2float_rn(z[t]);
     D.S[(long long)row * D.ldS + col] = v;
-    store_split(D.W[0], (long long)row * D.ldS + col, (long long)(p + row) * D.ldS + col, v, bf16);
+    // chain operand [S_hi; S_lo] of the row's chunk (prism.cu: chunks of 8 sketch rows)
+    const int ch = D.nchunk > 1 ? row >> 3 : 0, r = D.nchunk > 1 ? row & 7 : row;
+    const int pc = D.nchunk > 1 ? min(8, p - 8 * ch) : p, pw = D.nchunk > 1 ? 8 : p;
+    const long long base = (long long)ch * 4 * pw * D.ldS;
+    store_split(D.W[0], base + (long long)r * D.ldS + col, base + (long long)(pc + r) * D.ldS + col, v, bf16);
   }
 }
 

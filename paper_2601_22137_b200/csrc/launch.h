@@ -105,10 +105,10 @@ cudaError_t launch_gemm_cfg(int role, const GemmLaunch& L, cudaStream_t st) {
   if (L.ntiles <= 0) return cudaSuccess;
   const int sms = device_sms();
   if constexpr (Cfg::CTA2) {
-    const int pairs = std::min(L.ntiles, sms / 2);
+    const int pairs = std::min(L.ntiles, (L.max_ctas > 0 ? std::min(sms, L.max_ctas) : sms) / 2);
     return launch_k(k, dim3(2 * pairs), dim3(Cfg::THREADS), Cfg::SMEM_BYTES, st, 2, L);
   } else {
-    const int grid = std::min(L.ntiles, sms);
+    const int grid = std::min(L.ntiles, L.max_ctas > 0 ? std::min(sms, L.max_ctas) : sms);
     return launch_k(k, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM_BYTES, st, 1, L);
   }
 }

@@ -5,6 +5,7 @@
 #include "../../include/prism.h"
 #include "launch.h"
 #include "kernels.cuh"
+#include "internal.h"
 
 #include <algorithm>
 #include <array>
@@ -42,16 +43,14 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 EncodeTiledFn encode_fn() {
-  static EncodeTiledFn fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
+  static const EncodeTiledFn fn = [] {   // thread-safe one-time lookup
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(p);
-  }
+      return reinterpret_cast<EncodeTiledFn>(p);
+    return (EncodeTiledFn) nullptr;
+  }();
   return fn;
 }
 
@@ -91,6 +90,8 @@ bool encode_map(CUtensorMap* out, const MapSpec& s) {
 
 // ------------------------------------------------------------------ kernel dispatch
 constexpr int kTileM = 256;   // main GEMMs run on CTA pairs: tiles of 256 rows x BN columns
+constexpr int kChunkP = 8;    // sketch columns per chain problem (chaint.cuh: 4 x 8 W rows per MMA)
+constexpr int kMaxSketch = 64;
 
 int tile_bn(int precision) { return precision == PRISM_BF16 ? 256 : 128; }
 int tile_bk(int precision) { return precision == PRISM_BF16 ? 64 : 32; }
@@ -101,6 +102,7 @@ struct HostProblem {
   GemmProblem p;      // tm* fields hold map indices (+1; 0 = none) until serialised
   int mapA, mapB, mapA_lo, mapB_lo;
   int mapC, mapO;     // bf16 epilogue blocks (TMA load of C, TMA store of the output)
+  int mapO2;          // bf16 APPLY2 second output
 };
 
 struct LaunchDesc {
@@ -133,7 +135,15 @@ struct Plan {
   size_t meta_off = 0, meta_bytes = 0;
   std::unique_ptr<uint8_t, PinnedDeleter> blob;
   SolveParams params{};
-  LaunchDesc gram[2], square, square2, apply[2], chaint[5], gram32[2];
+  LaunchDesc gram[2], square, square2, apply[2], chaint[5];
+  // row-block split: packed partial-Gram launches per panel group, the
+  // APPLY2 launch (Y = X R, X + Y/2) of d = 2, the packed fp32 Gram, its layout
+  std::vector<LaunchDesc> rbgram[2];
+  LaunchDesc rb1[2];
+  float* Gp = nullptr;
+  double* rb_fro2 = nullptr;
+  std::vector<long long> panel_off;   // float offset of panel t, [ceil(n/256) + 1]
+  std::vector<int> group_end;         // first panel after group g
   std::vector<LaunchDesc> gjT, gjS;   // DB Newton sweep steps: T = D E, W -= E^T T
   bool db = false;
   int db_steps = 0;
@@ -158,7 +168,7 @@ struct Request {
   prism_options o;
   char* ws;   // null: size query only
   bool rowblock = false;   // row-block member of a split tall matrix: force the tall form, s = n
-  float* G = nullptr;      // row-block: fp32 partial Gram output (n x n, ld n)
+  int rb_groups = 1;       // row-block: panel groups of the packed Gram (all-reduced one by one)
   bool sign_kind = false;  // matrix sign: square path, R = I - X^2, X only (output in Q)
   int inv_q = 0;           // coupled inverse Newton A^{-1/q}: X in X[], M in Y[], R = I - M (output in Q)
   bool cheb_kind = false;  // Chebyshev inverse: A' = A/c in Y[0], R stored transposed, output X / c in Q
@@ -223,6 +233,32 @@ void sort_tiles_by_cost(LaunchDesc& L) {
   });
 }
 
+// Packed upper-triangle layout of the row-block Gram (gemm.cuh epi_gram32): panel t = rows
+// [256t, 256t + 256) x columns [256t, n), ld n - 256t; groups of panels with about equal
+// upper-triangle tile counts (each group is all-reduced as soon as its launch completes).
+void rowblock_layout(long long n, int ngroups, std::vector<long long>& off, std::vector<int>& gend) {
+  const int T = (int)((n + kTileM - 1) / kTileM);
+  off.assign(T + 1, 0);
+  std::vector<double> tiles(T);
+  double tot = 0.0;
+  for (int t = 0; t < T; ++t) {
+    const long long h = std::min<long long>(kTileM, n - (long long)kTileM * t), w = n - (long long)kTileM * t;
+    off[t + 1] = off[t] + h * w;
+    tiles[t] = (double)w;
+    tot += tiles[t];
+  }
+  ngroups = std::max(1, std::min(ngroups, T));
+  gend.assign(ngroups, T);
+  double acc = 0.0;
+  int g = 0;
+  for (int t = 0; t < T && g < ngroups - 1; ++t) {
+    acc += tiles[t];
+    if (acc >= tot * (g + 1) / ngroups) gend[g++] = t + 1;
+  }
+  for (; g < ngroups - 1; ++g) gend[g] = T;
+  for (int x = 1; x < ngroups; ++x) gend[x] = std::max(gend[x], gend[x - 1]);
+}
+
 // Build the full plan.  When r.ws == nullptr only sizes are computed.
 prism_status build_plan(const Request& r, Plan& P) {
   prism_options o = r.o;
@@ -281,30 +317,37 @@ prism_status build_plan(const Request& r, Plan& P) {
     for (int t = 0; t < 2; ++t) {
       D.X[t] = bump.take(xbytes);
       D.X_lo[t] = split ? bump.take(xbytes) : nullptr;
-      if (r.sqrt_kind || iq || db || (cheb && t == 0)) {
+      if (r.sqrt_kind || iq || db || (cheb && t == 0) || (r.rowblock && d == 2)) {   // row-block: Y, X + Y/2
         D.Y[t] = bump.take(xbytes);
         D.Y_lo[t] = split ? bump.take(xbytes) : nullptr;
       }
     }
     D.R = bump.take(rbytes);
     D.R_lo = split ? bump.take(rbytes) : nullptr;
-    void* Pm = (iq ? iq >= 2 : (d == 2 && !db)) ? bump.take(rbytes) : nullptr;   // Chebyshev: d = 2 (P^T)
+    void* Pm = (iq ? iq >= 2 : (d == 2 && !db && !r.rowblock)) ? bump.take(rbytes) : nullptr;   // Chebyshev: d = 2 (P^T)
     void* Pm_lo = (Pm && split) ? bump.take(rbytes) : nullptr;
     void* Pm2 = iq >= 3 ? bump.take(rbytes) : nullptr;
     void* Pm2_lo = (Pm2 && split) ? bump.take(rbytes) : nullptr;
     D.gdiag = reinterpret_cast<float*>(bump.take(sizeof(float) * s));
     D.tiles_m = (s + 127) / 128;
     D.tiles_n = (s + BN - 1) / BN;
+    if (r.rowblock) D.tiles_m = D.tiles_n = (s + 63) / 64;   // k_resid_packed's 64 x 64 norm tiles
     D.sym = (r.sqrt_kind || r.sign_kind || iq || cheb || db || r.rowblock) ? 0 : 1;
     D.norm_part = reinterpret_cast<float*>(bump.take(sizeof(float) * D.tiles_m * D.tiles_n));
     const long long ldS = (long long)align_up(s, 64);
     D.ldS = ldS;
+    // Sketch columns are processed in chunks of <= kChunkP (the products R^i S^T are column-
+    // separable; each chunk is its own chain problem with its own W / keep / partials, and
+    // k_alpha sums the <Va,Vb> partials of every chunk): p up to kMaxSketch.
+    const int nch = (p + kChunkP - 1) / kChunkP;
+    const int pw = nch == 1 ? p : kChunkP;   // width of a chunk region
+    D.nchunk = nch;
     D.S = reinterpret_cast<float*>(bump.take(sizeof(float) * p * ldS));
-    D.W[0] = bump.take((size_t)esz * 4 * p * ldS);
-    D.W[1] = bump.take((size_t)esz * 4 * p * ldS);
-    D.keep = reinterpret_cast<float*>(bump.take(sizeof(float) * 4 * (size_t)s * p));
-    // <Va,Vb> partials of the chain: one per 32-row group of R (chaint.cuh, epi_chain)
-    D.chain_tiles = (s + 31) / 32;
+    D.W[0] = bump.take((size_t)esz * 4 * pw * ldS * nch);
+    D.W[1] = bump.take((size_t)esz * 4 * pw * ldS * nch);
+    D.keep = reinterpret_cast<float*>(bump.take(sizeof(float) * 4 * (size_t)s * pw * nch));
+    // <Va,Vb> partials of the chain: one per 32-row group of R and chunk (chaint.cuh, epi_chain)
+    D.chain_tiles = nch * ((s + 31) / 32);
     D.chain_part = reinterpret_cast<double*>(bump.take(sizeof(double) * kChainG * D.chain_tiles));
     P.max_s = std::max(P.max_s, s);
     P.max_rows = std::max(P.max_rows, s);
@@ -326,7 +369,8 @@ prism_status build_plan(const Request& r, Plan& P) {
       h.p.c1 = 1.f;                          // out = c1 a^eC C + kA a^eA D
       h.p.kA = 1.f;
       h.p.eA = mode == EPI_POLY ? 1 : 0;
-      if (esz == 2 && (mode == EPI_RESID || mode == EPI_POLY || mode == EPI_APPLY || mode == EPI_STORE)) {
+      if (esz == 2 && (mode == EPI_RESID || mode == EPI_POLY || mode == EPI_APPLY || mode == EPI_STORE ||
+                       mode == EPI_APPLY2)) {
         maps.push_back(MapSpec{out, M, N, ldo, esz, OP_EPI, 32, 32});
         h.mapO = (int)maps.size();
         if (C) {
@@ -457,11 +501,57 @@ prism_status build_plan(const Request& r, Plan& P) {
         if (split) { am.mapA_lo = add_map(Pq_lo, nn, nn, ldr, OP_A); am.mapB_lo = add_map(D.Y_lo[t], nn, nn, ldx, OP_MN); }
         P.apply[t].probs.push_back(am);
       }
+    } else if (r.rowblock) {
+      // row-block member (rows x n of one tall polar problem): packed partial
+      // Gram X_r^T X_r (fp32 panels, one launch per panel group), then d = 2:
+      //   Y = X_r R and Xh = X_r + Y/2 (APPLY2), X_r' = Xh + a Y R (APPLY)   [= X_r g_2(R; a)]
+      // d = 1: X_r' = X_r + a X_r R.  R is stored whole (both triangles) by k_resid_packed.
+      rowblock_layout(n, r.rb_groups, P.panel_off, P.group_end);
+      P.Gp = reinterpret_cast<float*>(bump.take(sizeof(float) * (size_t)P.panel_off.back()));
+      P.rb_fro2 = reinterpret_cast<double*>(bump.take(sizeof(double)));
+      for (int t = 0; t < 2; ++t) {
+        P.rbgram[t].assign(r.rb_groups, LaunchDesc{});
+        for (int g = 0; g < r.rb_groups; ++g) {
+          HostProblem gp = mk(s, s, m, EPI_GRAM32, 1, P.Gp, nullptr, 0, nullptr, nullptr, 0);
+          gp.p.a_mn = gp.p.b_mn = 1;
+          gp.mapA = gp.mapB = add_map(D.X[t], m, n, ldx, OP_MN);
+          if (split) gp.mapA_lo = gp.mapB_lo = add_map(D.X_lo[t], m, n, ldx, OP_MN);
+          P.rbgram[t][g].probs.push_back(gp);
+        }
+        if (d == 2) {
+          HostProblem a1 = mk(m, n, s, EPI_APPLY2, 0, D.Y[1], D.Y_lo[1], ldx, D.X[t], D.X_lo[t], ldx);
+          a1.p.kA = 0.5f;   // X + D/2 (no alpha)
+          a1.p.eA = 0;
+          a1.p.out2 = D.Y[0];
+          a1.p.out2_lo = D.Y_lo[0];
+          if (esz == 2) {
+            maps.push_back(MapSpec{D.Y[0], m, n, ldx, esz, OP_EPI, 32, 32});
+            a1.mapO2 = (int)maps.size();
+          }
+          a1.mapA = add_map(D.X[t], m, n, ldx, OP_A);
+          a1.mapB = add_map(D.R, s, s, ldr, OP_BK);   // R symmetric: its rows are its columns
+          if (split) { a1.mapA_lo = add_map(D.X_lo[t], m, n, ldx, OP_A); a1.mapB_lo = add_map(D.R_lo, s, s, ldr, OP_BK); }
+          P.rb1[t].probs.push_back(a1);
+          HostProblem a2 = mk(m, n, s, EPI_APPLY, 0, D.X[1 - t], D.X_lo[1 - t], ldx, D.Y[1], D.Y_lo[1], ldx);
+          a2.p.scale_by_alpha = a2.p.eA = 1;
+          a2.mapA = add_map(D.Y[0], m, n, ldx, OP_A);
+          a2.mapB = add_map(D.R, s, s, ldr, OP_BK);
+          if (split) { a2.mapA_lo = add_map(D.Y_lo[0], m, n, ldx, OP_A); a2.mapB_lo = add_map(D.R_lo, s, s, ldr, OP_BK); }
+          P.apply[t].probs.push_back(a2);
+        } else {
+          HostProblem a = mk(m, n, s, EPI_APPLY, 0, D.X[1 - t], D.X_lo[1 - t], ldx, D.X[t], D.X_lo[t], ldx);
+          a.p.scale_by_alpha = a.p.eA = 1;
+          a.mapA = add_map(D.X[t], m, n, ldx, OP_A);
+          a.mapB = add_map(D.R, s, s, ldr, OP_BK);
+          if (split) { a.mapA_lo = add_map(D.X_lo[t], m, n, ldx, OP_A); a.mapB_lo = add_map(D.R_lo, s, s, ldr, OP_BK); }
+          P.apply[t].probs.push_back(a);
+        }
+      }
     } else if (!r.sqrt_kind && !r.sign_kind) {
       // polar: X keeps A's row-major layout (m x n).  Tall (m >= n): G = X^T X with both
       // operands MN-major, X' = X + X P (A = X K-major, B = P K-major by symmetry).
       // Wide (m < n): G = X X^T (both K-major), X' = X + P X (B = X MN-major).
-      const bool tall = r.rowblock || m >= n;
+      const bool tall = m >= n;
       for (int t = 0; t < 2; ++t) {
         HostProblem g = mk(s, s, L, EPI_RESID, 1, D.R, D.R_lo, ldr, nullptr, nullptr, 0);
         g.p.norm_part = D.norm_part;
@@ -476,17 +566,6 @@ prism_status build_plan(const Request& r, Plan& P) {
           if (split) { g.mapA_lo = add_map(D.X_lo[t], m, n, ldx, OP_A); g.mapB_lo = add_map(D.X_lo[t], m, n, ldx, OP_BK); }
         }
         P.gram[t].probs.push_back(g);
-        if (r.rowblock) {
-          // partial Gram X_r^T X_r in fp32 into the caller's buffer (summed across ranks)
-          HostProblem g32 = g;
-          g32.p.mode = EPI_GRAM32;
-          g32.p.out = r.G;
-          g32.p.out_lo = nullptr;
-          g32.p.ldo = n;
-          g32.p.norm_part = nullptr;
-          g32.p.gdiag = nullptr;
-          P.gram32[t].probs.push_back(g32);
-        }
         const void* Pa = d == 2 ? Pm : D.R;
         const void* Pa_lo = d == 2 ? Pm_lo : D.R_lo;
         HostProblem a = mk(m, n, s, EPI_APPLY, 0, D.X[1 - t], D.X_lo[1 - t], ldx, D.X[t], D.X_lo[t], ldx);
@@ -564,24 +643,27 @@ prism_status build_plan(const Request& r, Plan& P) {
                                        {CH1_P1, CH1_P2, CHI_K2, CH2_P4, CHI_L4}};
       static const int codesc[3] = {CHC_P1, CHC_P2, CHC_P3};
       const int npass = cheb ? 3 : iq ? iq + 1 : d == 2 ? 5 : 3;
+      for (int ch = 0; ch < nch; ++ch) {
+      const int pc = std::min(pw, p - ch * pw);    // sketch rows of this chunk
+      const size_t wch = (size_t)esz * 4 * pw * ldS * ch;   // byte offset of the chunk's W region
       for (int j = 0; j < npass; ++j) {
-        const int N = ((iq || cheb) ? 2 : d == 2 ? nin2[j] : nin1[j]) * p;
+        const int N = ((iq || cheb) ? 2 : d == 2 ? nin2[j] : nin1[j]) * pc;
         HostProblem c = mk(s, N, s, EPI_CHAIN, 0, nullptr, nullptr, 0, nullptr, nullptr, 0);
         c.p.pass = cheb ? codesc[j] : iq ? codesi[iq - 1][j] : d == 2 ? codes2[j] : codes1[j];
-        c.p.S = D.S;
+        c.p.S = D.S + (size_t)ch * pw * ldS;
         c.p.Rg = D.R;
         c.p.Rg_lo = D.R_lo;
         c.p.gdiag = D.gdiag;
-        c.p.Wn = D.W[(j + 1) % 2];
-        c.p.keep = D.keep;
-        c.p.chain_part = D.chain_part;
+        c.p.Wn = static_cast<char*>(D.W[(j + 1) % 2]) + wch;
+        c.p.keep = D.keep + (size_t)4 * s * pw * ch;
+        c.p.chain_part = D.chain_part + (size_t)kChainG * ((s + 31) / 32) * ch;
         c.p.ldS = D.ldS;
         c.p.ldr = ldr;
-        c.p.p = p;
+        c.p.p = pc;
         c.p.tiles_n = 1;
         c.p.ksplit = chain_ks(s);
         // A = W (rows c, K-major [c][ldS]; box 32 rows, OOB rows zero), B = R (256-row box)
-        maps.push_back(MapSpec{D.W[j % 2], N, s, D.ldS, esz, OP_BK, 32, BK});
+        maps.push_back(MapSpec{static_cast<char*>(D.W[j % 2]) + wch, N, s, D.ldS, esz, OP_BK, 32, BK});
         c.mapA = (int)maps.size();
         maps.push_back(MapSpec{D.R, s, s, ldr, esz, OP_BK, 256, BK});
         c.mapB = (int)maps.size();
@@ -591,10 +673,11 @@ prism_status build_plan(const Request& r, Plan& P) {
         }
         P.chaint[j].probs.push_back(c);
       }
+      }
     }
   }
   P.inv_q = iq;
-  P.has_square = iq ? iq >= 2 : d == 2;
+  P.has_square = r.rowblock ? false : iq ? iq >= 2 : d == 2;
   P.has_square2 = iq >= 3;
   P.n_chain = db ? 0 : cheb ? 3 : iq ? iq + 1 : (d == 2) ? 5 : 3;
   if (db) P.has_square = false;
@@ -611,7 +694,19 @@ prism_status build_plan(const Request& r, Plan& P) {
   for (int t = 0; t < 2; ++t) {
     finish(P.gram[t], !polar_k);
     finish(P.apply[t], true);
-    if (r.rowblock) finish(P.gram32[t], false);
+    if (r.rowblock) {
+      finish(P.rb1[t], true);
+      // packed Gram: group g holds the upper-triangle tiles of tile rows [group_end[g-1], group_end[g])
+      for (int g = 0; g < (int)P.rbgram[t].size(); ++g) {
+        LaunchDesc& L = P.rbgram[t][g];
+        L.tiles.clear();
+        const int t0 = g ? P.group_end[g - 1] : 0, t1 = P.group_end[g];
+        const int M = L.probs[0].p.M;
+        for (int tm = t0; tm < t1; ++tm)
+          for (int tn = 0; tn < (M + BN - 1) / BN; ++tn)
+            if (tn * BN + BN - 1 >= tm * kTileM) L.tiles.push_back(((uint32_t)tm << 10) | (uint32_t)tn);
+      }
+    }
   }
   if (P.has_square) finish(P.square, !polar_k);
   if (P.has_square2) finish(P.square2, !polar_k);
@@ -669,7 +764,9 @@ prism_status build_plan(const Request& r, Plan& P) {
   off += sizeof(int) * (size_t)toff[B];
   std::vector<LaunchDesc*> all = {&P.gram[0],   &P.gram[1],   &P.apply[0],  &P.apply[1],  &P.square,
                                   &P.chaint[0], &P.chaint[1], &P.chaint[2], &P.chaint[3], &P.chaint[4],
-                                  &P.gram32[0], &P.gram32[1], &P.square2};
+                                  &P.square2, &P.rb1[0], &P.rb1[1]};
+  for (int t = 0; t < 2; ++t)
+    for (LaunchDesc& L : P.rbgram[t]) all.push_back(&L);
   for (LaunchDesc& L : P.gjT) all.push_back(&L);
   for (LaunchDesc& L : P.gjS) all.push_back(&L);
   for (LaunchDesc* L : all) {
@@ -721,6 +818,7 @@ prism_status build_plan(const Request& r, Plan& P) {
       q.tmB_lo = mapptr(L->probs[j].mapB_lo);
       q.tmC = mapptr(L->probs[j].mapC);
       q.tmO = mapptr(L->probs[j].mapO);
+      q.tmO2 = mapptr(L->probs[j].mapO2);
       gp[j] = q;
     }
     std::memcpy(blob + L->tiles_off, L->tiles.data(), sizeof(uint32_t) * L->tiles.size());
@@ -820,7 +918,7 @@ prism_status validate(const Request& r) {
   if (o.fit != PRISM_FIT_SKETCHED && o.fit != PRISM_FIT_TAYLOR)
     return fail(PRISM_ERR_UNSUPPORTED, "fit must be SKETCHED or TAYLOR on the device");
   if (o.sketch_size < 1) return fail(PRISM_ERR_INVALID_ARG, "sketch_size must be >= 1");
-  if (o.sketch_size > 8) return fail(PRISM_ERR_UNSUPPORTED, "sketch_size > 8 not supported");
+  if (o.sketch_size > kMaxSketch) return fail(PRISM_ERR_UNSUPPORTED, "sketch_size > 64 not supported");
   if (o.warmup_iters < 0) return fail(PRISM_ERR_INVALID_ARG, "warmup_iters must be >= 0");
   const int esz = elem_size(o.precision);
   for (int i = 0; i < r.batch; ++i) {
@@ -830,7 +928,7 @@ prism_status validate(const Request& r) {
     if (r.lda[i] < n) return fail(PRISM_ERR_INVALID_ARG, "lda < n");
     if (!r.sqrt_kind && !r.db_kind && !r.Q[i]) return fail(PRISM_ERR_INVALID_ARG, "null output matrix");
     if ((r.Q || r.Q2) && r.ldq[i] < n) return fail(PRISM_ERR_INVALID_ARG, "ldq < n");
-    if (std::min(m, n) < o.sketch_size) return fail(PRISM_ERR_INVALID_ARG, "sketch_size > min(m, n)");
+    if ((r.rowblock ? n : std::min(m, n)) < o.sketch_size) return fail(PRISM_ERR_INVALID_ARG, "sketch_size > min(m, n)");
     if (reinterpret_cast<uintptr_t>(r.A[i]) % esz) return fail(PRISM_ERR_INVALID_ARG, "misaligned input");
   }
   return PRISM_OK;
@@ -871,6 +969,9 @@ struct prism_handle_s {
   int slot_next = 0;
   cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
   cudaEvent_t ev_call = nullptr;   // host path: the caller's stream reached the call
+  // multi-GPU: per-device auxiliary (communication) stream and reusable ordering events
+  std::map<int, cudaStream_t> aux;
+  std::map<int, std::array<cudaEvent_t, 16>> aux_ev;
   char* hws = nullptr;   // workspace of the host-path solves (they run in order on s_comp)
   size_t hws_bytes = 0;
   ~prism_handle_s() {
@@ -888,6 +989,10 @@ struct prism_handle_s {
     }
     if (hws) cudaFree(hws);
     if (ev_call) cudaEventDestroy(ev_call);
+    for (auto& kv : aux) cudaStreamDestroy(kv.second);
+    for (auto& kv : aux_ev)
+      for (cudaEvent_t e : kv.second)
+        if (e) cudaEventDestroy(e);
     for (cudaStream_t x : {s_in, s_comp, s_out})
       if (x) cudaStreamDestroy(x);
   }
@@ -925,6 +1030,25 @@ struct KindTimer {
   }
 };
 
+namespace prism {
+prism_status fail_ext(prism_status s, const std::string& msg) { return fail(s, msg); }
+cudaStream_t handle_aux_stream(prism_handle h) {
+  const int d = current_device();
+  auto it = h->aux.find(d);
+  if (it != h->aux.end()) return it->second;
+  cudaStream_t s = nullptr;
+  if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+  h->aux[d] = s;
+  return s;
+}
+cudaEvent_t handle_event(prism_handle h, int idx) {
+  auto& a = h->aux_ev[current_device()];
+  cudaEvent_t& e = a[idx & 15];
+  if (!e) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  return e;
+}
+}  // namespace prism
+
 static std::vector<long long> make_key(const Request& r) {
   std::vector<long long> k;
   k.push_back(current_device());   // plans hold device allocations and per-device graphs
@@ -934,7 +1058,7 @@ static std::vector<long long> make_key(const Request& r) {
   k.push_back(r.cheb_kind);
   k.push_back(r.db_kind);
   k.push_back(r.rowblock);
-  k.push_back((long long)(uintptr_t)r.G);
+  k.push_back(r.rb_groups);
   k.push_back(r.batch);
   const prism_options& o = r.o;
   long long tolbits, alo, ahi;
@@ -1622,119 +1746,146 @@ prism_status prism_profile_read(prism_handle h, double* ms, int64_t* launches, i
 }
 
 // ---------------------------------------------------------------- row-block split
-// State of the handle's current row-block solve (set by prism_rowblock_begin).
-static thread_local struct RowBlockState {
-  Plan* plan = nullptr;
-  char* ws = nullptr;
-  int prec = 0, max_iters = 0, warmup = 0, fit = 0;
-} g_rb;
+static Request rowblock_request(int64_t* rows, int64_t* n, const void** A, int64_t* lda, void** Q, int64_t* ldq,
+                                const prism_options* o, char* ws, int nranks) {
+  Request r{false, 1, rows, n, A, lda, Q, nullptr, ldq, nullptr, *o, ws};
+  r.rowblock = true;
+  r.rb_groups = nranks > 1 ? 4 : 1;   // pipelined all-reduce of the packed Gram by panel group
+  return r;
+}
 
-size_t prism_rowblock_workspace(prism_handle h, int64_t rows, int64_t n, const prism_options* o) {
+size_t prism_polar_rowblock_workspace(prism_handle h, int64_t rows, int64_t n, const prism_options* o) {
   if (!h || !o || rows < 1 || n < 1) return 0;
   const void* fakeA = reinterpret_cast<const void*>(256);
   void* fakeQ = reinterpret_cast<void*>(256);
   int64_t ld = n;
-  Request r{false, 1, &rows, &n, &fakeA, &ld, &fakeQ, nullptr, &ld, nullptr, *o, nullptr};
-  r.rowblock = true;
-  r.G = reinterpret_cast<float*>(256);
+  // the 4-group layout needs the same bytes as the 1-group one (one packed buffer)
+  Request r = rowblock_request(&rows, &n, &fakeA, &ld, &fakeQ, &ld, o, nullptr, 2);
   return ws_query(h, r);
 }
 
-prism_status prism_rowblock_begin(prism_handle h, int64_t rows, int64_t n, const void* A_rows, int64_t lda,
-                                  void* Q_rows, int64_t ldq, float* G, double* fro2_local, const prism_options* o,
-                                  void* workspace, size_t ws_bytes, void* stream) {
+prism_status prism_polar_rowblock_tr(prism_handle h, const prism_transport* tr, int64_t m_global, int64_t n,
+                                     const void* A_rows, int64_t row0, int64_t rows, int64_t lda, void* Q_rows,
+                                     int64_t ldq, const prism_options* o, const prism_report* rep, void* workspace,
+                                     size_t ws_bytes, void* stream) {
   try {
-    if (!o || !G || !fro2_local) return fail(PRISM_ERR_INVALID_ARG, "null options / G / fro2 buffer");
+    if (!h || !tr || !o || !tr->allreduce_sum) return fail(PRISM_ERR_INVALID_ARG, "null handle / transport / options");
+    if (rows < 1 || n < 1 || row0 < 0 || row0 + rows > m_global)
+      return fail(PRISM_ERR_INVALID_ARG, "row block outside the global matrix");
     const void* A = A_rows;
     void* Q = Q_rows;
-    Request r{false, 1, &rows, &n, &A, &lda, &Q, nullptr, &ldq, nullptr, *o, static_cast<char*>(workspace)};
-    r.rowblock = true;
-    r.G = G;
+    Request r = rowblock_request(&rows, &n, &A, &lda, &Q, &ldq, o, static_cast<char*>(workspace), tr->nranks);
     Plan* P = nullptr;
     prism_status gs = get_plan(h, r, ws_bytes, &P);
     if (gs) return gs;
+    ensure_attrs();
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-      SolveParams S = P->params;
-    S.fro2_out = fro2_local;
+    cudaStream_t cs = prism::handle_aux_stream(h);
+    if (!cs) return fail(PRISM_ERR_CUDA, "aux stream");
+    if (!h->h_flag) PRISM_CK(cudaMallocHost(&h->h_flag, sizeof(int)));
+    SolveParams S = P->params;
+    S.rep_iters = rep ? rep->iters : nullptr;
+    S.rep_resid = rep ? rep->resid : nullptr;
+    S.rep_status = rep ? rep->status : nullptr;
+    S.rep_alphas = rep ? rep->alphas : nullptr;
+    S.rep_resid_hist = rep ? rep->resid_hist : nullptr;
+    const int prec = o->precision, M = o->max_iters, ng = (int)P->group_end.size();
+    const bool pipelined = tr->nranks > 1 && ng > 1;
+    auto allreduce = [&](void* buf, size_t count, int dtype, cudaStream_t s2) -> prism_status {
+      if (tr->allreduce_sum(tr->ctx, buf, buf, count, dtype, s2)) return fail(PRISM_ERR_NCCL, "all-reduce failed");
+      return PRISM_OK;
+    };
+    // c = ||A||_F over all ranks: local sum of squares, all-reduced, then X_0 = A_r / c
+    S.fro2_out = P->rb_fro2;
+    PRISM_CK(cudaMemsetAsync(P->Gp, 0, sizeof(float) * (size_t)P->panel_off.back(), st));
     PRISM_CK(launch_k(k_fro_partials, dim3(S.n_fro_blocks), dim3(256), 0, st, 1, S));
     PRISM_CK(launch_k(k_fro_final, dim3(1), dim3(256), 0, st, 1, S));
+    if (prism_status e = allreduce(P->rb_fro2, 1, PRISM_DT_F64, st)) return e;
+    S.fro2_out = nullptr;
+    S.fro2_in = P->rb_fro2;
+    PRISM_CK(launch_k(k_set_c, dim3(1), dim3(32), 0, st, 1, S));
+    if (prec == PRISM_BF16) PRISM_CK(launch_k(k_normalize<0>, dim3(S.n_tiles), dim3(256), 0, st, 1, S));
+    else if (prec == PRISM_FP32) PRISM_CK(launch_k(k_normalize<1>, dim3(S.n_tiles), dim3(256), 0, st, 1, S));
+    else PRISM_CK(launch_k(k_normalize<2>, dim3(S.n_tiles), dim3(256), 0, st, 1, S));
+    const bool sketched = o->fit == PRISM_FIT_SKETCHED;
+    const int nt = (int)((n + 63) / 64);
+    cudaEvent_t ev_stop = prism::handle_event(h, 8);
+    for (int k = 0; k <= M; ++k) {
+      const int t = k & 1;
+      // 1. packed partial Gram, all-reduced panel group by panel group (on the aux stream,
+      //    overlapping the next group's launch; the Gram grid leaves SMs to the collective)
+      for (int g = 0; g < ng; ++g) {
+        GemmLaunch gl = make_launch(*P, P->rbgram[t][g], nullptr, r.ws, 0, M + 1);
+        if (pipelined) gl.max_ctas = device_sms() - 16;
+        PRISM_CK(launch_gemm(prec, ROLE_GRAM, gl, st));
+        const size_t beg = (size_t)(g ? P->panel_off[P->group_end[g - 1]] : 0);
+        const size_t end = (size_t)P->panel_off[P->group_end[g]];
+        if (end == beg) continue;
+        if (pipelined) {
+          cudaEvent_t e = prism::handle_event(h, 9 + (g & 3));
+          PRISM_CK(cudaEventRecord(e, st));
+          PRISM_CK(cudaStreamWaitEvent(cs, e, 0));
+          if (prism_status x = allreduce(P->Gp + beg, end - beg, PRISM_DT_F32, cs)) return x;
+        } else {
+          if (prism_status x = allreduce(P->Gp + beg, end - beg, PRISM_DT_F32, st)) return x;
+        }
+      }
+      if (pipelined) {
+        cudaEvent_t e = prism::handle_event(h, 13);
+        PRISM_CK(cudaEventRecord(e, cs));
+        PRISM_CK(cudaStreamWaitEvent(st, e, 0));
+      }
+      // 2. R = I - G, sketch, chain, stop test and alpha (identical on every rank)
+      if (prec == PRISM_BF16) PRISM_CK(launch_k(k_resid_packed<0>, dim3(nt, nt), dim3(256), 0, st, 1, S, (const float*)P->Gp));
+      else if (prec == PRISM_FP32) PRISM_CK(launch_k(k_resid_packed<1>, dim3(nt, nt), dim3(256), 0, st, 1, S, (const float*)P->Gp));
+      else PRISM_CK(launch_k(k_resid_packed<2>, dim3(nt, nt), dim3(256), 0, st, 1, S, (const float*)P->Gp));
+      if (sketched) {
+        PRISM_CK(launch_k(k_sketch, dim3((S.p * P->max_s / 2 + 256) / 256, 1), dim3(256), 0, st, 1, S));
+        for (int j = 0; j < P->n_chain; ++j)
+          PRISM_CK(launch_chain(prec, chain_pass(*P, j), make_launch(*P, P->chaint[j], nullptr, r.ws, o->warmup_iters, M), st));
+      }
+      PRISM_CK(launch_k(k_alpha, dim3(1), dim3(256), 0, st, 1, S, 0));
+      PRISM_CK(cudaMemcpyAsync(h->h_flag, &P->params.st[0].done, sizeof(int), cudaMemcpyDeviceToHost, st));
+      PRISM_CK(cudaEventRecord(ev_stop, st));
+      // 3. this rank's rows: X_r g_d(R; alpha) without R^2 (skipped on the device once stopped)
+      if (P->rb1[0].probs.size()) PRISM_CK(launch_gemm(prec, ROLE_APPLY, make_launch(*P, P->rb1[0], &P->rb1[1], r.ws, 0, M), st));
+      PRISM_CK(launch_gemm(prec, ROLE_APPLY, make_launch(*P, P->apply[0], &P->apply[1], r.ws, 0, M), st));
+      PRISM_CK(launch_k(k_advance, dim3(1), dim3(256), 0, st, 1, S, (cudaGraphConditionalHandle)0, 0, P->d_all_done));
+      PRISM_CK(cudaGetLastError());
+      if (tr->async_error && tr->async_error(tr->ctx)) return fail(PRISM_ERR_NCCL, "communicator error");
+      // the device keeps the updates of iteration k while the host reads its stop flag
+      PRISM_CK(cudaEventSynchronize(ev_stop));
+      if (*h->h_flag) break;
+    }
+    if (prec == PRISM_BF16) PRISM_CK(launch_k(k_finalize<0>, dim3(S.n_out_tiles), dim3(256), 0, st, 1, S));
+    else if (prec == PRISM_FP32) PRISM_CK(launch_k(k_finalize<1>, dim3(S.n_out_tiles), dim3(256), 0, st, 1, S));
+    else PRISM_CK(launch_k(k_finalize<2>, dim3(S.n_out_tiles), dim3(256), 0, st, 1, S));
+    if (rep) PRISM_CK(launch_k(k_report, dim3(1), dim3(256), 0, st, 1, S));
     PRISM_CK(cudaGetLastError());
-    g_rb.plan = P;
-    g_rb.ws = r.ws;
-    g_rb.prec = o->precision;
-    g_rb.max_iters = o->max_iters;
-    g_rb.warmup = o->warmup_iters;
-    g_rb.fit = o->fit;
     return PRISM_OK;
   } catch (...) {
-    return fail(PRISM_ERR_INTERNAL, "exception in prism_rowblock_begin");
+    return fail(PRISM_ERR_INTERNAL, "exception in prism_polar_rowblock");
   }
 }
 
-prism_status prism_rowblock_gram(prism_handle h, int k, const double* fro2_global, void* stream) {
-  if (!h || !g_rb.plan) return fail(PRISM_ERR_INVALID_ARG, "prism_rowblock_begin not called");
-  Plan* P = g_rb.plan;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  SolveParams S = P->params;
-  if (k == 0) {
-    if (!fro2_global) return fail(PRISM_ERR_INVALID_ARG, "null fro2_global at k = 0");
-    S.fro2_in = fro2_global;
-    PRISM_CK(launch_k(k_set_c, dim3(1), dim3(32), 0, st, 1, S));
-    if (g_rb.prec == PRISM_BF16) PRISM_CK(launch_k(k_normalize<0>, dim3(S.n_tiles), dim3(256), 0, st, 1, S));
-    else if (g_rb.prec == PRISM_FP32) PRISM_CK(launch_k(k_normalize<1>, dim3(S.n_tiles), dim3(256), 0, st, 1, S));
-    else PRISM_CK(launch_k(k_normalize<2>, dim3(S.n_tiles), dim3(256), 0, st, 1, S));
-  }
-  PRISM_CK(launch_k(k_set_iter, dim3(1), dim3(32), 0, st, 1, S, k));
-  GemmLaunch g = make_launch(*P, P->gram32[0], &P->gram32[1], g_rb.ws, 0, g_rb.max_iters + 1);
-  PRISM_CK(launch_gemm(g_rb.prec, ROLE_GRAM, g, st));
-  PRISM_CK(cudaGetLastError());
-  return PRISM_OK;
+prism_status prism_polar_rowblock(prism_handle h, void* comm, int64_t m_global, int64_t n, const void* A_rows,
+                                  int64_t row0, int64_t rows, int64_t lda, void* Q_rows, int64_t ldq,
+                                  const prism_options* o, const prism_report* rep, void* workspace, size_t ws_bytes,
+                                  void* stream) {
+  prism_transport tr;
+  prism_status s = prism_nccl_transport(comm, &tr);
+  if (s) return s;
+  return prism_polar_rowblock_tr(h, &tr, m_global, n, A_rows, row0, rows, lda, Q_rows, ldq, o, rep, workspace,
+                                 ws_bytes, stream);
 }
 
-prism_status prism_rowblock_update(prism_handle h, int k, const float* G, int32_t* all_done, void* stream) {
-  if (!h || !g_rb.plan) return fail(PRISM_ERR_INVALID_ARG, "prism_rowblock_begin not called");
-  if (!G) return fail(PRISM_ERR_INVALID_ARG, "null G");
-  Plan* P = g_rb.plan;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  SolveParams S = P->params;
-  const int prec = g_rb.prec, M = g_rb.max_iters;
-  const int bn = tile_bn(prec);
-  const int n = P->max_s;
-  const dim3 rg((n + bn - 1) / bn, (n + 127) / 128);
-  if (prec == PRISM_BF16) PRISM_CK(launch_k(k_resid_from_gram<0>, dim3(rg), dim3(256), 0, st, 1, S, G, bn));
-  else if (prec == PRISM_FP32) PRISM_CK(launch_k(k_resid_from_gram<1>, dim3(rg), dim3(256), 0, st, 1, S, G, bn));
-  else PRISM_CK(launch_k(k_resid_from_gram<2>, dim3(rg), dim3(256), 0, st, 1, S, G, bn));
-  if (g_rb.fit == PRISM_FIT_SKETCHED) {
-    PRISM_CK(launch_k(k_sketch, dim3((S.p * n / 2 + 256) / 256, 1), dim3(256), 0, st, 1, S));
-    for (int j = 0; j < P->n_chain; ++j) {
-      PRISM_CK(launch_chain(prec, chain_pass(*P, j), make_launch(*P, P->chaint[j], nullptr, g_rb.ws, g_rb.warmup, M),
-                             st));
-    }
-  }
-  PRISM_CK(launch_k(k_alpha, dim3(1), dim3(256), 0, st, 1, S, 0));
-  if (P->has_square) PRISM_CK(launch_gemm(prec, ROLE_SQUARE, make_launch(*P, P->square, nullptr, g_rb.ws, 0, M), st));
-  PRISM_CK(launch_gemm(prec, ROLE_APPLY, make_launch(*P, P->apply[0], &P->apply[1], g_rb.ws, 0, M), st));
-  PRISM_CK(launch_k(k_advance, dim3(1), dim3(256), 0, st, 1, S, 0, 0, all_done ? reinterpret_cast<int*>(all_done) : P->d_all_done));
-  PRISM_CK(cudaGetLastError());
-  return PRISM_OK;
-}
-
-prism_status prism_rowblock_end(prism_handle h, const prism_report* rep, void* stream) {
-  if (!h || !g_rb.plan) return fail(PRISM_ERR_INVALID_ARG, "prism_rowblock_begin not called");
-  Plan* P = g_rb.plan;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  SolveParams S = P->params;
-  S.rep_iters = rep ? rep->iters : nullptr;
-  S.rep_resid = rep ? rep->resid : nullptr;
-  S.rep_status = rep ? rep->status : nullptr;
-  S.rep_alphas = rep ? rep->alphas : nullptr;
-  S.rep_resid_hist = rep ? rep->resid_hist : nullptr;
-  if (g_rb.prec == PRISM_BF16) PRISM_CK(launch_k(k_finalize<0>, dim3(S.n_out_tiles), dim3(256), 0, st, 1, S));
-  else if (g_rb.prec == PRISM_FP32) PRISM_CK(launch_k(k_finalize<1>, dim3(S.n_out_tiles), dim3(256), 0, st, 1, S));
-  else PRISM_CK(launch_k(k_finalize<2>, dim3(S.n_out_tiles), dim3(256), 0, st, 1, S));
-  if (rep) PRISM_CK(launch_k(k_report, dim3(1), dim3(256), 0, st, 1, S));
-  PRISM_CK(cudaGetLastError());
-  g_rb.plan = nullptr;
+prism_status prism_rowblock_layout(int64_t n, int ngroups, int64_t* panel_off, int32_t* group_end) {
+  if (n < 1 || ngroups < 1 || !panel_off || !group_end) return fail(PRISM_ERR_INVALID_ARG, "bad layout args");
+  std::vector<long long> off;
+  std::vector<int> ge;
+  rowblock_layout(n, ngroups, off, ge);
+  for (size_t t = 0; t < off.size(); ++t) panel_off[t] = off[t];
+  for (int g = 0; g < ngroups; ++g) group_end[g] = g < (int)ge.size() ? ge[g] : ge.back();
   return PRISM_OK;
 }
 

@@ -1,40 +1,169 @@
-"""Multi-GPU PRISM: a Muon/Shampoo step's batch sharded across ranks.
+"""Multi-GPU PRISM: marshalling of the library's multi-GPU C ABI.
 
-One process per GPU with torch.distributed (NCCL over NVLink / NVSwitch on B200).
+One process per GPU.  Every exchange happens inside libprism through a prism_transport:
 
-* Partition: whole matrices are assigned to ranks by the native LPT
-  partitioner (prism_lpt_partition): cost = F_min(m, n) x expected iterations,
-  largest first to the least-loaded rank; identical on every rank.
-* Solve: each rank runs prism_polar / prism_sqrt_invsqrt on its matrices with
-  their *global* indices as sketch stream ids, so S_k — and therefore every
-  result bit — equals the single-GPU solve of the whole batch.
-* Exchange (the one collective on the path): every rank packs its outputs
-  into one flat buffer, the buffers are all-gathered (padded to the largest
-  rank's size, one NCCL all_gather_into_tensor), and each rank unpacks every
-  owner's matrices into place.
-
-`solve` is the CUDA library by default; the parameter exists so the
-world-size-2 gloo test on CPU can check the partition / pack / exchange /
-unpack logic without a GPU (tests/test_dist.py).
-
-Row-block split (one matrix too large for one GPU, BASELINE configs[3]):
-polar_rowblock runs the library's row-block steps with a sum all-reduce of the
-fp32 partial Gram X_r^T X_r between them every iteration (the one exchange of
-that path), so every rank forms the same R, alpha_k and P and updates its rows.
+* ``Comm``          an NCCL communicator created by the library (prism_nccl_comm_init;
+                    NCCL resolved at run time from the libnccl the process loaded, i.e.
+                    torch's) over the ranks of a torch.distributed group — the unique id
+                    travels through torch.distributed, the collectives through NCCL.
+* ``polar_sharded`` a Muon/Shampoo step's batch, LPT-sharded by matrix over the ranks
+                    (prism_polar_sharded): every rank passes the full batch, solves its
+                    share in buckets with global sketch ids (bit-identical to the
+                    single-GPU solve), and the owners broadcast each bucket's outputs while
+                    the next bucket solves; every rank returns every output.
+* ``polar_rowblock`` one matrix too large for one GPU, split by rows
+                    (prism_polar_rowblock): per iteration a packed upper-triangle fp32
+                    Gram all-reduce pipelined by panel group, then Y_r = X_r R and
+                    X_r + Y_r/2 + a Y_r R locally (no R^2, no second collective).
+* ``HostGroup`` / ``HostTransport``  a transport whose collectives run on the host
+                    (stream synchronised, device <-> host copies, a fixed-order sum):
+                    lets a test run several ranks as threads on one GPU through the real
+                    library code, with no kernel ever waiting on another rank's kernel.
 """
 
 from __future__ import annotations
 
-from typing import Callable, List, Sequence
-
-import torch
-import torch.distributed as dist
+import ctypes
+import threading
+from typing import List, Sequence
 
 from . import binding as B
 
+_cudart = None
+
+
+def _rt():
+    """cudart of the process (torch's), for the host transport's copies."""
+    global _cudart
+    if _cudart is None:
+        import os
+        import torch  # noqa: F401  (loads cudart)
+        for name in ("libcudart.so.12", "libcudart.so.13", "libcudart.so"):
+            try:
+                _cudart = ctypes.CDLL(name, mode=getattr(os, "RTLD_NOLOAD", 0) | os.RTLD_NOW)
+                break
+            except OSError:
+                continue
+        if _cudart is None:
+            raise B.PrismError("cudart not loaded")
+        _cudart.cudaMemcpy.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int]
+        _cudart.cudaStreamSynchronize.argtypes = [ctypes.c_void_p]
+    return _cudart
+
+
+# ---------------------------------------------------------------- transports
+class Comm:
+    """NCCL communicator (ncclComm_t) over the ranks of a torch.distributed group, created
+    by prism_nccl_comm_init on the current CUDA device; `transport` is its prism_transport."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        single = not (dist.is_available() and dist.is_initialized())
+        self.rank = 0 if single else dist.get_rank(group)
+        self.world = 1 if single else dist.get_world_size(group)
+        uid = ctypes.create_string_buffer(128)
+        if self.rank == 0:
+            B.check(B.lib().prism_nccl_get_unique_id(uid), "prism_nccl_get_unique_id")
+        if not single:   # rank 0's id to every rank of the group
+            obj = [uid.raw if self.rank == 0 else None]
+            src = dist.get_global_rank(group, 0) if group is not None else 0
+            dist.broadcast_object_list(obj, src=src, group=group)
+            uid = ctypes.create_string_buffer(obj[0], 128)
+        self.comm = ctypes.c_void_p()
+        B.check(B.lib().prism_nccl_comm_init(ctypes.byref(self.comm), self.world, uid, self.rank),
+                "prism_nccl_comm_init")
+        self.transport = B.Transport()
+        B.check(B.lib().prism_nccl_transport(self.comm, ctypes.byref(self.transport)), "prism_nccl_transport")
+
+    def close(self):
+        if self.comm:
+            B.check(B.lib().prism_nccl_comm_destroy(self.comm), "prism_nccl_comm_destroy")
+            self.comm = ctypes.c_void_p()
+
+
+class HostGroup:
+    """Shared state of `world` thread-ranks exchanging through the host."""
+
+    def __init__(self, world: int):
+        self.world = world
+        self.barrier = threading.Barrier(world)
+        self.slots = [None] * world
+
+
+class HostTransport:
+    """prism_transport whose collectives synchronise the stream, copy the buffer to the host,
+    exchange through a HostGroup (sum in rank order: identical bits on every rank) and copy
+    back.  Test infrastructure for emulating ranks on one GPU."""
+
+    _NP = {0: "float32", 1: "float64", 2: "int32", 3: "uint8"}
+
+    def __init__(self, group: HostGroup, rank: int):
+        self.g = group
+        self.rank = rank
+        self.calls = {"allreduce": 0, "broadcast": 0}
+        self._ar = B.ALLREDUCE_FN(self._allreduce)
+        self._bc = B.BROADCAST_FN(self._broadcast)
+        self._none = B.GROUP_FN(lambda ctx: 0)
+        self.transport = B.Transport(None, group.world, rank, self._ar, self._bc, self._none, self._none, self._none)
+
+    def _fetch(self, ptr, nbytes, dtype, stream):
+        import numpy as np
+        rt = _rt()
+        rt.cudaStreamSynchronize(ctypes.c_void_p(stream))
+        a = np.empty(nbytes // np.dtype(dtype).itemsize, dtype=dtype)
+        rt.cudaMemcpy(a.ctypes.data, ctypes.c_void_p(ptr), nbytes, 4)
+        return a
+
+    def _allreduce(self, ctx, send, recv, count, dtype, stream):
+        try:
+            import numpy as np
+            dt = np.dtype(self._NP[dtype])
+            self.calls["allreduce"] += 1
+            self.g.slots[self.rank] = self._fetch(send, count * dt.itemsize, dt, stream)
+            self.g.barrier.wait()
+            tot = self.g.slots[0].copy()
+            for r in range(1, self.g.world):
+                tot += self.g.slots[r]
+            self.g.barrier.wait()
+            _rt().cudaMemcpy(ctypes.c_void_p(recv), tot.ctypes.data, count * dt.itemsize, 4)
+            return 0
+        except Exception:   # pragma: no cover - surfaced as PRISM_ERR_NCCL
+            return 1
+
+    def _broadcast(self, ctx, buf, nbytes, root, stream):
+        try:
+            self.calls["broadcast"] += 1
+            if self.rank == root:
+                self.g.slots[root] = self._fetch(buf, nbytes, "uint8", stream)
+            else:
+                _rt().cudaStreamSynchronize(ctypes.c_void_p(stream))
+            self.g.barrier.wait()
+            if self.rank != root:
+                src = self.g.slots[root]
+                _rt().cudaMemcpy(ctypes.c_void_p(buf), src.ctypes.data, nbytes, 4)
+            self.g.barrier.wait()
+            return 0
+        except Exception:   # pragma: no cover
+            return 1
+
+
+def _transport_of(t):
+    return t.transport if hasattr(t, "transport") else t
+
+
+# ---------------------------------------------------------------- plans (host only)
+def shard_plan(shapes: Sequence[tuple], nranks: int, nbuckets: int = 2, degree: int = 5, sketch_size: int = 8):
+    """(owner, bucket) per matrix (prism_shard_plan; deterministic, identical on every rank)."""
+    n = len(shapes)
+    own = (ctypes.c_int32 * n)()
+    bk = (ctypes.c_int32 * n)()
+    B.check(B.lib().prism_shard_plan(n, B._i64([s[0] for s in shapes]), B._i64([s[1] for s in shapes]), degree,
+                                     sketch_size, nranks, nbuckets, own, bk), "prism_shard_plan")
+    return list(own), list(bk)
+
 
 def lpt_plan(shapes: Sequence[tuple], world: int, degree: int = 5, iters_est: Sequence[int] | None = None) -> List[int]:
-    """Owner rank of each matrix (deterministic; same on every rank)."""
+    """Owner rank of each matrix by LPT on F_min x expected iterations (prism_lpt_partition)."""
     costs = []
     for i, (m, n) in enumerate(shapes):
         f = B.polar_flops_per_iter(m, n, degree, 8)
@@ -42,106 +171,77 @@ def lpt_plan(shapes: Sequence[tuple], world: int, degree: int = 5, iters_est: Se
     return B.lpt_partition(costs, world)
 
 
-def _pack(ts: Sequence[torch.Tensor], numel: int, dtype, device) -> torch.Tensor:
-    buf = torch.zeros(numel, dtype=dtype, device=device)
-    off = 0
-    for t in ts:
-        n = t.numel()
-        buf[off:off + n].copy_(t.reshape(-1))
-        off += n
-    return buf
+def rowblock_layout(n: int, ngroups: int):
+    """(panel_off, group_end) of the packed row-block Gram (prism_rowblock_layout)."""
+    T = (n + 255) // 256
+    off = (ctypes.c_int64 * (T + 1))()
+    ge = (ctypes.c_int32 * ngroups)()
+    B.check(B.lib().prism_rowblock_layout(n, ngroups, off, ge), "prism_rowblock_layout")
+    return list(off), list(ge)
 
 
-def all_gather_owned(outs: List[torch.Tensor | None], owner: List[int], group=None) -> List[torch.Tensor]:
-    """Give every rank every output: owners' tensors are packed, all-gathered, unpacked.
-
-    outs[i] must be set on rank owner[i] (shape/dtype known to all ranks through
-    `outs_like`), and is filled in on the other ranks.
-    """
-    world = dist.get_world_size(group)
-    rank = dist.get_rank(group)
-    sizes = [0] * world
-    for i, t in enumerate(outs):
-        sizes[owner[i]] += t.numel()
-    width = max(sizes) if sizes else 0
-    mine = [outs[i] for i in range(len(outs)) if owner[i] == rank]
-    ref = outs[0]
-    send = _pack(mine, width, ref.dtype, ref.device)
-    recv = torch.empty(world * width, dtype=ref.dtype, device=ref.device)
-    dist.all_gather_into_tensor(recv, send, group=group)
-    cursor = [r * width for r in range(world)]
-    for i, t in enumerate(outs):
-        r = owner[i]
-        n = t.numel()
-        if r != rank:
-            t.copy_(recv[cursor[r]:cursor[r] + n].view_as(t))
-        cursor[r] += n
-    return outs
-
-
-def polar_sharded(mats: Sequence[torch.Tensor], group=None, iters_est=None,
-                  solve: Callable | None = None, **opts) -> List[torch.Tensor]:
-    """Polar factors of the whole batch on every rank; each rank solves its LPT share.
-
-    `mats` is the full batch (replicated on every rank, as the gradients of a
-    data-parallel step after their all-reduce).  Returns outputs for all matrices.
-    """
-    world = dist.get_world_size(group)
-    rank = dist.get_rank(group)
-    shapes = [tuple(t.shape) for t in mats]
-    owner = lpt_plan(shapes, world, opts.get("degree", 5), iters_est)
-    idx = [i for i in range(len(mats)) if owner[i] == rank]
-    outs: List[torch.Tensor] = [torch.empty_like(t) for t in mats]
-    if idx:
-        if solve is None:
-            mine, _ = B.polar([mats[i] for i in idx], matrix_ids=idx, **opts)
-        else:
-            mine = solve([mats[i] for i in idx], idx)
-        for i, q in zip(idx, mine):
-            outs[i] = q
-    return all_gather_owned(outs, owner, group)
+# ---------------------------------------------------------------- solves
+def polar_sharded(mats, comm, out=None, nbuckets: int = 2, report: bool = True, handle=None, stream=None,
+                  degree=5, max_iters=30, sketch_size=8, tol=1e-6, seed=42, precision=None, fit="sketched",
+                  warmup_iters=0, alpha_lo=None, alpha_hi=None):
+    """Polar factors of the whole batch on every rank (prism_polar_sharded_tr); `mats` is the
+    full batch, identical on every rank.  Returns (outputs, report of every matrix)."""
+    import torch
+    mats = list(mats)
+    tr = _transport_of(comm)
+    precision = B._precision_of(mats[0], precision)
+    B._check_dtype(mats, precision)
+    dev = mats[0].device
+    h = handle or B.default_handle()
+    o = B.make_options(degree, max_iters, sketch_size, tol, seed, precision, fit, warmup_iters, alpha_lo, alpha_hi)
+    n_ = len(mats)
+    m = B._i64([t.shape[0] for t in mats])
+    n = B._i64([t.shape[1] for t in mats])
+    out = B._outputs(mats, True, out, "polar_sharded", False)
+    L = B.lib()
+    with torch.cuda.device(dev):
+        st = stream if stream is not None else torch.cuda.current_stream(dev)
+        need = L.prism_polar_sharded_workspace(h.h, tr.nranks, tr.rank, n_, m, n, ctypes.byref(o), nbuckets)
+        if need == 0:
+            raise B.PrismError("prism_polar_sharded_workspace rejected the arguments: " + L.prism_last_error().decode())
+        ws = h.workspace(need, dev, st)
+        rb = B._report_buffers(n_, max_iters, dev) if report else None
+        rep = B._report_struct(rb) if report else None
+        B.check(L.prism_polar_sharded_tr(h.h, ctypes.byref(tr), n_, m, n, B._ptrs(mats),
+                                         B._i64([t.stride(0) for t in mats]), B._ptrs(out),
+                                         B._i64([t.stride(0) for t in out]), ctypes.byref(o), int(nbuckets),
+                                         ctypes.byref(rep) if report else None, ws.data_ptr(), ws.numel(),
+                                         ctypes.c_void_p(st.cuda_stream)), "prism_polar_sharded")
+    return out, rb
 
 
-def sqrt_invsqrt_sharded(mats: Sequence[torch.Tensor], group=None, iters_est=None,
-                         solve: Callable | None = None, **opts):
-    """A^{1/2}, A^{-1/2} of the whole batch on every rank (Shampoo blocks), LPT-sharded."""
-    world = dist.get_world_size(group)
-    rank = dist.get_rank(group)
-    shapes = [tuple(t.shape) for t in mats]
-    owner = lpt_plan(shapes, world, opts.get("degree", 5), iters_est)
-    idx = [i for i in range(len(mats)) if owner[i] == rank]
-    sq: List[torch.Tensor] = [torch.empty_like(t) for t in mats]
-    isq: List[torch.Tensor] = [torch.empty_like(t) for t in mats]
-    if idx:
-        if solve is None:
-            a, b, _ = B.sqrt_invsqrt([mats[i] for i in idx], matrix_ids=idx, **opts)
-        else:
-            a, b = solve([mats[i] for i in idx], idx)
-        for i, x, y in zip(idx, a, b):
-            sq[i] = x
-            isq[i] = y
-    all_gather_owned(sq, owner, group)
-    all_gather_owned(isq, owner, group)
-    return sq, isq
-
-
-def polar_rowblock(A_rows: torch.Tensor, group=None, allreduce: Callable | None = None, steps=None, **opts):
-    """Polar factor of a tall matrix split by rows across ranks; returns (Q_rows, report).
-
-    Per iteration: partial Gram -> all-reduce(sum) -> identical R / alpha / P on
-    every rank -> local update.  The host checks the device stop flag after each
-    iteration (one 4-byte read; the exchange already synchronises the ranks).
-    """
-    if allreduce is None:
-        def allreduce(t):
-            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
-    st = steps if steps is not None else B.RowBlockSolver(A_rows, **opts)
-    st.begin()
-    allreduce(st.fro2)
-    for k in range(st.max_iters + 1):
-        st.gram(k)
-        allreduce(st.G)
-        st.update(k)
-        if int(st.done.item()):
-            break
-    return st.end()
+def polar_rowblock(A_rows, comm, m_global: int, row0: int, out=None, handle=None, stream=None, degree=5,
+                   max_iters=30, sketch_size=8, tol=1e-6, seed=42, precision=None, fit="sketched", warmup_iters=0,
+                   alpha_lo=None, alpha_hi=None):
+    """Rows [row0, row0 + rows) of the polar factor of the m_global x n matrix whose row block
+    A_rows this rank holds (prism_polar_rowblock_tr).  Returns (Q_rows, report).  The call
+    returns once the iteration count is decided (the host follows the device's stop flag)."""
+    import torch
+    tr = _transport_of(comm)
+    precision = B._precision_of(A_rows, precision)
+    B._check_dtype([A_rows], precision)
+    dev = A_rows.device
+    h = handle or B.Handle()
+    o = B.make_options(degree, max_iters, sketch_size, tol, seed, precision, fit, warmup_iters, alpha_lo, alpha_hi)
+    rows, n = A_rows.shape
+    Q = B._outputs([A_rows], True, [out] if out is not None else None, "polar_rowblock", False)[0]
+    L = B.lib()
+    with torch.cuda.device(dev):
+        st = stream if stream is not None else torch.cuda.current_stream(dev)
+        need = L.prism_polar_rowblock_workspace(h.h, rows, n, ctypes.byref(o))
+        if need == 0:
+            raise B.PrismError("prism_polar_rowblock_workspace rejected the arguments: " +
+                               L.prism_last_error().decode())
+        ws = h.workspace(need, dev, st)
+        rb = B._report_buffers(1, max_iters, dev)
+        rep = B._report_struct(rb)
+        B.check(L.prism_polar_rowblock_tr(h.h, ctypes.byref(tr), int(m_global), n, A_rows.data_ptr(), int(row0), rows,
+                                          A_rows.stride(0), Q.data_ptr(), Q.stride(0), ctypes.byref(o),
+                                          ctypes.byref(rep), ws.data_ptr(), ws.numel(),
+                                          ctypes.c_void_p(st.cuda_stream)), "prism_polar_rowblock")
+    return Q, rb

@@ -46,7 +46,7 @@ def test_workspace_query_and_validation():
     assert lib.prism_polar_workspace(h.h, 2, m, n, ctypes.byref(o_fp32)) > ws
     bad = B.make_options(degree=4)
     assert lib.prism_polar_workspace(h.h, 2, m, n, ctypes.byref(bad)) == 0
-    bad = B.make_options(sketch_size=9)
+    bad = B.make_options(sketch_size=65)
     assert lib.prism_polar_workspace(h.h, 2, m, n, ctypes.byref(bad)) == 0
     nn = (ctypes.c_int64 * 1)(1024)
     assert lib.prism_sqrt_workspace(h.h, 1, nn, ctypes.byref(o_fp32)) > 4 * 1024 * 1024 * 4 * 2

@@ -4,7 +4,7 @@ otherwise through properties that hold at any size.
 
   configs[0]  64 x 32, PRISM-5, p = 8, <= 15 iterations            -> oracle parity (FP32)
   configs[2]  Shampoo SPD blocks 1024-4096, kappa up to 1e6, FP32    -> oracle parity / properties
-  configs[3]  8192 x 8192 BF16, row-block split (2 ranks emulated)   -> properties, vs 1-GPU solve
+  configs[3]  8192 x 8192 BF16, row-block split                      -> tests/test_gpu_multigpu.py
   configs[4]  1.2B-param GPT Muon batch (96 matrices) BF16           -> sampled oracle + properties
   north star  4096 x 4096 BF16 (bench --workload square4096)         -> full oracle parity
 """
@@ -73,54 +73,6 @@ def test_config2_shampoo_4096_kappa1e6_properties():
     assert float(torch.linalg.norm(x @ x - a) / torch.linalg.norm(a)) <= 1e-3
     eye = torch.eye(n, device=a.device, dtype=a.dtype)
     assert float(torch.linalg.norm(x @ y - eye)) / n ** 0.5 <= 1e-3
-
-
-def test_config3_8192_rowblock_two_ranks_properties():
-    """configs[3] at full size: 8192^2 BF16 split by rows over 2 emulated ranks (host
-    threads; the Gram all-reduce is a host-synchronised sum, no kernel waits on another)."""
-    import threading
-    from paper_2601_22137_b200 import dist as PD
-    from paper_2601_22137_b200.binding import RowBlockSolver
-    m = n = 8192
-    A = torch.tensor(W.gaussian(m, n, seed=3000)).to(torch.bfloat16).cuda()
-    parts = [A[: m // 2].contiguous(), A[m // 2:].contiguous()]
-    bar = threading.Barrier(2)
-    slot = [None, None]
-    res = [None, None]
-
-    def allreduce_factory(rank):
-        def ar(t):
-            torch.cuda.synchronize()
-            slot[rank] = t.clone()
-            bar.wait()
-            total = slot[0] + slot[1]
-            bar.wait()
-            t.copy_(total)
-            torch.cuda.synchronize()
-        return ar
-
-    def run(rank):
-        st = RowBlockSolver(parts[rank], degree=5, tol=3e-2, max_iters=25, precision="bf16",
-                            stream=torch.cuda.Stream())
-        with torch.cuda.stream(st.stream):
-            res[rank] = PD.polar_rowblock(parts[rank], allreduce=allreduce_factory(rank), steps=st)
-        torch.cuda.synchronize()
-
-    th = [threading.Thread(target=run, args=(r,)) for r in range(2)]
-    for t in th:
-        t.start()
-    for t in th:
-        t.join()
-    it = [int(res[r][1]["iters"][0]) for r in range(2)]
-    assert it[0] == it[1]
-    Q = torch.cat([res[0][0], res[1][0]])
-    assert _orth_err(Q) <= 0.06
-    Qs, rs = P.polar([A], degree=5, tol=3e-2, max_iters=25, precision="bf16")
-    torch.cuda.synchronize()
-    assert int(rs["status"][0]) == prism.CONVERGED and abs(int(rs["iters"][0]) - it[0]) <= 1
-    assert _orth_err(Qs[0]) <= 0.06
-    d = (Q.double() - Qs[0].double())
-    assert float(torch.linalg.norm(d) / torch.linalg.norm(Qs[0].double())) <= 2e-2
 
 
 def test_config4_gpt1b_batch_sampled():

@@ -226,53 +226,6 @@ def test_gpt2_mixed_batch_exactly_as_benchmarked():
     print("gpt2 mixed batch: max rel err MP %.3e, HTMP %.3e" % (max(errs["mp"]), max(errs["htmp"])))
 
 
-def test_rowblock_two_ranks_emulated_equals_single_solve():
-    """Row-block split (configs[3] path) with 2 ranks emulated by 2 host threads on one
-    GPU: the all-reduce is a host-synchronised sum of the two partial Grams (no kernel
-    waits on another), so the ranks' kernels never depend on each other in flight."""
-    import threading
-    from paper_2601_22137_b200 import dist as PD
-    from paper_2601_22137_b200.binding import RowBlockSolver
-    m, n = 1024, 384
-    A = torch.tensor(W.gaussian(m, n, seed=21)).float().cuda()
-    parts = [A[:640].contiguous(), A[640:].contiguous()]
-    bar = threading.Barrier(2)
-    slot = [None, None]
-    res = [None, None]
-
-    def allreduce_factory(rank):
-        def ar(t):
-            torch.cuda.synchronize()
-            slot[rank] = t.clone()
-            bar.wait()
-            total = slot[0] + slot[1]          # same order on both ranks -> identical bits
-            bar.wait()
-            t.copy_(total)
-            torch.cuda.synchronize()
-        return ar
-
-    def run(rank):
-        st = RowBlockSolver(parts[rank], degree=5, tol=1e-5, max_iters=30, precision="fp32",
-                            stream=torch.cuda.Stream())
-        with torch.cuda.stream(st.stream):
-            res[rank] = PD.polar_rowblock(parts[rank], allreduce=allreduce_factory(rank), steps=st)
-        torch.cuda.synchronize()
-
-    th = [threading.Thread(target=run, args=(r,)) for r in range(2)]
-    for t in th:
-        t.start()
-    for t in th:
-        t.join()
-    Q = torch.cat([res[0][0], res[1][0]]).double().cpu().numpy()
-    Qs, rs = P.polar([A], degree=5, tol=1e-5, max_iters=30, precision="fp32", matrix_ids=[0])
-    torch.cuda.synchronize()
-    Qo, ro = prism.polar(A.double().cpu().numpy(), d=2, p=8, tol=1e-5, max_iters=30, seed=42, b=0)
-    assert int(res[0][1]["iters"][0]) == int(res[1][1]["iters"][0])
-    assert abs(int(res[0][1]["iters"][0]) - ro.iters) <= 1
-    assert _rel(Q, Qo) <= 1e-5
-    assert _rel(Q, Qs[0].double().cpu().numpy()) <= 1e-5
-
-
 @pytest.mark.gpu
 def test_sqrt_caller_outputs_equal_fresh_outputs():
     mats = [torch.tensor(W.spd_logspaced(s, 1e2, seed=900 + s)).float().cuda() for s in (96, 300)]
@@ -302,3 +255,39 @@ def test_early_square_gemm_is_bit_identical():
     assert torch.equal(re_["iters"], rw["iters"][:3])
     for a, b in zip(Qe, Qw[:3]):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("p", [5, 16, 32])
+@pytest.mark.parametrize("deg", [3, 5])
+def test_polar_sketch_sizes_beyond_8(p, deg):
+    """Sketch sizes other than the default 8 ("as small as 5"; Theorem 2, asks
+    for more): p > 8 runs the chain in column chunks of 8 whose <Va, Vb> partials k_alpha sums
+    — the same quartic as one wide chain (the products R^i S^T are column-separable)."""
+    A = W.gaussian(600, 300, seed=40 + p)
+    At, Aq = _dev(A, "fp32")
+    Q, rep = P.polar([At], degree=deg, max_iters=30, tol=1e-5, seed=42, precision="fp32", sketch_size=p)
+    torch.cuda.synchronize()
+    Qo, ro = prism.polar(Aq, d=1 if deg == 3 else 2, p=p, tol=1e-5, max_iters=30, seed=42)
+    assert int(rep["status"][0]) == prism.CONVERGED
+    assert abs(int(rep["iters"][0]) - ro.iters) <= 1
+    assert _rel(Q[0].double().cpu().numpy(), Qo) <= 1e-5
+    n = min(len(ro.alphas), int(rep["iters"][0]))
+    assert np.max(np.abs(rep["alphas"][0, :n].cpu().numpy() - np.array(ro.alphas[:n]))) <= 1e-3
+
+
+@pytest.mark.parametrize("p", [16, 32])
+def test_sqrt_and_bf16_sketch_16_32(p):
+    A = W.spd_logspaced(384, 1e2, seed=p)
+    At, Aq = _dev(A, "fp32")
+    X, Y, rep = P.sqrt_invsqrt([At], degree=5, max_iters=40, tol=1e-5, seed=42, precision="fp32", sketch_size=p)
+    torch.cuda.synchronize()
+    Xo, Yo, ro = prism.sqrt_invsqrt(Aq, d=2, p=p, tol=1e-5, max_iters=40, seed=42)
+    assert abs(int(rep["iters"][0]) - ro.iters) <= 1
+    assert _rel(X[0].double().cpu().numpy(), Xo) <= 1e-5 and _rel(Y[0].double().cpu().numpy(), Yo) <= 1e-5
+    G = W.gaussian(768, 2304, seed=p)
+    Gt, Gq = _dev(G, "bf16")
+    Q, rq = P.polar([Gt], degree=5, max_iters=20, tol=3e-2, seed=42, precision="bf16", sketch_size=p)
+    torch.cuda.synchronize()
+    Qo, ro = prism.polar(Gq, d=2, p=p, tol=3e-2, max_iters=20, seed=42)
+    assert abs(int(rq["iters"][0]) - ro.iters) <= 1
+    assert _rel(Q[0].double().cpu().numpy(), Qo) <= 2e-2
