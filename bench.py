@@ -562,7 +562,109 @@ def extra_solve(P, wl, dev, flush, clocks, steps=5, warmup=3):
 
 # ---------------------------------------------------------------- our arm: N GPUs, sharded
 def run_multi(args, rank, world, dev):
-    raise SystemExit("multi-GPU sharded / row-block bench: not built yet")
+    """N ranks through the library's multi-GPU entry points: the sharded Muon step (gpt2: weak
+    scaling, 48N matrices; gpt1b: strong scaling of configs[4]) or the row-block 8192^2 solve
+    (strong scaling of configs[3]).  Every exchange (NCCL broadcasts / all-reduces) runs inside
+    the timed region; value = matrices solved by the whole job / max-over-ranks device time."""
+    import torch
+    import torch.distributed as dist
+    import paper_2601_22137_b200 as P
+    from paper_2601_22137_b200 import dist as D
+    name, shapes, mats_np, opts, desc, kind = workload(args.workload, rank, world)
+    dt = torch.bfloat16 if opts["precision"] == "bf16" else torch.float32
+    comm = D.Comm()
+    h = P.Handle()
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    clocks = ClockSampler(dev.index)
+    clocks.start()
+    clocks.mark()
+    ctx = dist if world > 1 else None
+    if kind == "rowblock":
+        m = shapes[0][0]
+        cuts = [m * r // world for r in range(world + 1)]
+        host = torch.tensor(mats_np[0][cuts[rank]:cuts[rank + 1]]).to(dt).pin_memory()
+        A = host.to(dev)
+        Q = torch.empty_like(A)
+        hout = torch.empty_like(host).pin_memory()
+        units = 1
+
+        def run():
+            return D.polar_rowblock(A, comm, m_global=m, row0=cuts[rank], out=Q, handle=h, **opts)
+
+        def run_e2e():
+            A.copy_(host, non_blocking=True)
+            r = run()
+            hout.copy_(Q, non_blocking=True)
+            return r
+        h2d = d2h = host.numel() * host.element_size()
+    else:
+        host = [torch.tensor(a).to(dt).pin_memory() for a in mats_np]
+        mats = [x.to(dev) for x in host]
+        outs = [torch.empty_like(x) for x in mats]
+        hout = [torch.empty_like(x).pin_memory() for x in host]
+        units = len(mats)
+
+        def run():
+            return D.polar_sharded(mats, comm, out=outs, nbuckets=2, handle=h, **opts)
+
+        def run_e2e():
+            for d_, h_ in zip(mats, host):
+                d_.copy_(h_, non_blocking=True)
+            r = run()
+            for h_, o_ in zip(hout, outs):
+                h_.copy_(o_, non_blocking=True)
+            return r
+        h2d = d2h = sum(x.numel() * x.element_size() for x in host)
+    t0 = time.time()
+    ms, res = time_device(run, args.steps, args.warmup, flush, stream, ctx)
+    t1 = time.time()
+    e_ms, _ = time_device(run_e2e, args.steps, 3, flush, stream, ctx)
+    rep = res[-1]
+    iters = rep["iters"].cpu().tolist()
+    t = torch.tensor([ms, e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max, e_max = float(t[0]), float(t[1])
+    f_iter = flops_per_iter(P, "polar", shapes, opts)
+    flops = sum(f * k for f, k in zip(f_iter, iters))
+    if kind == "rowblock":   # row-block F_min: symmetric Gram + X_r R + Y_r R (no R^2) per rank, summed
+        n = shapes[0][1]
+        flops = (m * n * (n + 1) + 4.0 * m * n * n + 14.0 * n * n * opts["sketch_size"] * world) * iters[0]
+    clk_t = clocks.window(t0, t1)
+    clk = clocks.stop()
+    clk["timed_region"] = clk_t
+    peaks, src = read_peaks()
+    peak, pk, burst, sus = pick_peak(peaks, clk_t, opts["precision"])
+    tflops = flops * args.steps / (ms_max / 1e3) / 1e12
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": units * args.steps / (ms_max / 1e3), "unit": "solves/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak" if args.workload == "gpt2" else "strong", "vs_baseline": None,
+            "dtype": opts["precision"], "data": "synthetic: seeded matrices shaped like the paper's workloads",
+            "config": {"workload": name, "description": desc, "matrices": units, "solver": kind,
+                       "parallelism": (f"row-block x{world} (prism_polar_rowblock, NCCL)" if kind == "rowblock" else
+                                       f"LPT-sharded x{world} (prism_polar_sharded, NCCL broadcasts, 2 buckets)"),
+                       "l2": "flushed (256 MiB write) before every timed step, outside the events",
+                       "e2e_path": "pinned host inputs copied in, library multi-GPU call, outputs copied out"},
+            "tflops": tflops, "tflops_unit": "F_min per second, whole job",
+            "frac_of_peak": tflops / (peak * world), "frac_of_peak_kind": pk,
+            "iterations": {"mean": sum(iters) / len(iters), "max": max(iters), "min": min(iters)},
+            "status_converged": sum(1 for x in rep["status"].cpu().tolist() if x == 0),
+            "clocks": clk,
+            "e2e": {"value": units * args.steps / (e_max / 1e3), "unit": "solves/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": None,
+            "roofline": {"bound": "tensor", "achieved": tflops / world, "peak": peak, "unit": "TFLOP/s",
+                         "frac": tflops / world / peak, "traffic": None,
+                         "kernel": "whole step per GPU (multi-GPU run; per-kernel profile in the N=1 line)",
+                         "peak_kind": pk},
+            "cpu_baseline": None,
+        }
+        print(json.dumps(line), flush=True)
+    comm.close()
+    return 0
 
 
 # ---------------------------------------------------------------- our arm

@@ -379,6 +379,11 @@ prism_status prism_debug_sketch(uint64_t seed, int64_t b, int k, int p, int s, f
 /* Device quartic argmin on [lo, hi] (R15/R16): n problems, c_dev[5*n] -> alpha_dev[n]. */
 prism_status prism_debug_argmin(int n, const double* c_dev, double lo, double hi, double a_taylor,
                                 double* alpha_dev, void* stream);
+/* Main-GEMM k-block timeline (diagnostics only): buf_dev = device u64[148 * 376]; launches
+ * whose epilogue mode is `mode` (0 residual, 1 poly, 2 apply; < 0 off) record per-CTA
+ * globaltimer stamps (gemm.cuh).  NULL disables. */
+prism_status prism_debug_trace_gemm(unsigned long long* buf_dev, int mode);
+
 #ifdef __cplusplus
 }
 #endif

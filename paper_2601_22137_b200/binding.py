@@ -141,6 +141,7 @@ _SIGS = {
                                _vp, _i64, _vp, _vp, _i64, _vp, ctypes.c_float, _i32, _vp, _vp, _vp, _sz, _vp]),
     "prism_debug_sketch": (_ST, [_u64, _i64, _i32, _i32, _i32, _vp, _vp]),
     "prism_debug_argmin": (_ST, [_i32, _vp, _dbl, _dbl, _dbl, _vp, _vp]),
+    "prism_debug_trace_gemm": (_ST, [_vp, _i32]),
 }
 EXPORTS = sorted(_SIGS)
 

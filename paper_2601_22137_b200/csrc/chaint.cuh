@@ -123,13 +123,21 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
     run = k >= L.iter_lo && k < L.iter_hi;
     if (L.probs_odd && (k & 1)) probs = L.probs_odd;
   }
+  // The first tile's skip decision is taken once, before the wait, and shared by every role
+  // and every CTA of a cluster: skip only matrices stopped in an EARLIER iteration
+  // (stop_iter < k, final long before this launch).  A matrix stopped by this iteration's
+  // residual stage (the launch just before the first pass) has its first tile computed and
+  // ignored, so producer, MMA, epilogue and the cluster's partial exchange stay in step.
+  __shared__ int s_first_active;
   int pre_n = 0;   // producer: leading k-blocks of its first tile whose R is in flight
+  if (threadIdx.x == 0) s_first_active = 1;
   if (run && warp == 0 && lane == 0 && (int)blockIdx.x < L.ntiles) {
     const uint32_t code = L.tiles[blockIdx.x];
     const GemmProblem& P = probs[code >> 20];
     tma_prefetch(P.tmA);
     tma_prefetch(P.tmB);
-    if (!(L.done && L.done[P.matrix * L.done_stride])) {
+    s_first_active = !(L.done && L.iter && L.done[P.matrix * L.done_stride + kStopIterOffset] < *L.iter);
+    if (s_first_active) {
       const int n0 = ((code >> 10) & 1023) * Cfg::BN;
       int s_lo, s_hi, kb_lo, kb_hi, dummy;
       chain_slices(P, code, C, s_lo, s_hi);
@@ -146,6 +154,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
   }
   griddep_wait();
   griddep_launch();
+  __syncthreads();   // s_first_active
+  auto skip = [&](int t, int matrix) -> bool {
+    if (t == (int)blockIdx.x) return !s_first_active;
+    return L.done && L.done[matrix * L.done_stride];
+  };
 
   if (warp < 4) {
     setmaxnreg_dec<Cfg::REG_LO>();
@@ -158,7 +171,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
       for (int t = blockIdx.x; t < L.ntiles; t += gridDim.x) {
         const uint32_t code = L.tiles[t];
         const GemmProblem& P = probs[code >> 20];
-        if (L.done && L.done[P.matrix * L.done_stride]) continue;
+        if (skip(t, P.matrix)) continue;
         const int n0 = ((code >> 10) & 1023) * Cfg::BN;
         int s_lo, s_hi, kb_lo, kb_hi, dummy;   // the slices' k-blocks are contiguous
         chain_slices(P, code, C, s_lo, s_hi);
@@ -189,7 +202,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
       for (int t = blockIdx.x; t < L.ntiles; t += gridDim.x) {
         const uint32_t code = L.tiles[t];
         const GemmProblem& P = probs[code >> 20];
-        if (L.done && L.done[P.matrix * L.done_stride]) continue;
+        if (skip(t, P.matrix)) continue;
         int s_lo, s_hi;
         chain_slices(P, code, C, s_lo, s_hi);
         for (int sl = s_lo; sl < s_hi; ++sl) {   // one TMEM chunk per slice
@@ -235,7 +248,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
     for (int t = blockIdx.x; t < L.ntiles; t += gridDim.x) {
       const uint32_t code = L.tiles[t];
       const GemmProblem& P = probs[code >> 20];
-      if (L.done && L.done[P.matrix * L.done_stride]) continue;
+      if (skip(t, P.matrix)) continue;
       const int tn = (code >> 10) & 1023;
       int s_lo, s_hi;
       chain_slices(P, code, C, s_lo, s_hi);

@@ -63,6 +63,66 @@ __host__ __device__ constexpr int chain_ng(int pass) {
   return (pass >= CHI_L1 && pass <= CHI_L4) ? (pass - CHI_L1 + 2) * (pass - CHI_L1 + 3) / 2 : pass == CHC_P3 ? 3 : 6;
 }
 
+// Per-matrix solver state (device memory, one per matrix of the batch).
+struct MatState {
+  double c;          // ||A||_F
+  double alpha;      // current alpha_k (read by GEMM epilogues)
+  double r_prev;     // ||R_{k-1}||_F
+  float resid;       // ||R_final||_F / sqrt(s)
+  int done;          // 1 once the matrix stopped (skip all further work)
+  int iters;         // updates applied
+  int status;        // PRISM_CONVERGED ...
+  int incr;          // consecutive residual increases
+  int stop_iter;     // iteration k at which the matrix stopped (INT_MAX while active; -1: zero input)
+  int arrivals;      // residual stage: norm partials landed this iteration (the last one decides)
+};
+
+// Stop test of iteration k (R12), run once per matrix by the last residual-stage
+// block (GEMM tile or SIMT block) whose norm partial lands: ||R_k||_F from the nparts
+// partials (fixed order: lane-strided fp64 sums, a fixed xor tree, lane 0's value), then the
+// state update.  Converged when ||R_k||_F <= tol sqrt(s); non-finite; diverged after 5
+// consecutive increases; max_iters when k = max_iters.  Every later kernel of iteration k
+// (sketch, chain, alpha, square, apply) sees `done` and skips the matrix.  Warp-collective.
+__device__ __forceinline__ void residual_stop_warp(MatState* S, const float* norm_part, int nparts, int k,
+                                                   double tol, int s, int max_iters, float* hist, int lane) {
+  double part = 0.0;
+  for (int t = lane; t < nparts; t += 32) part += (double)__ldcg(norm_part + t);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  if (lane != 0) return;
+  const double r = sqrt(part);
+  int stop = 0, status = 1, incr = 0;
+  if (!isfinite(r)) { stop = 1; status = 3; }
+  else if (r <= tol * sqrt((double)s)) { stop = 1; status = 0; }
+  else {
+    incr = (k >= 1 && r > S->r_prev) ? S->incr + 1 : 0;
+    if (incr >= 5) { stop = 1; status = 2; }
+    else if (k >= max_iters) { stop = 1; status = 1; }
+  }
+  hist[k] = (float)(r / sqrt((double)s));
+  if (isfinite(r) && !(r <= tol * sqrt((double)s))) S->incr = incr;
+  S->r_prev = r;
+  S->resid = (float)(r / sqrt((double)s));
+  S->iters = k;
+  S->arrivals = 0;   // next iteration's residual stage counts from zero
+  if (stop) {
+    S->stop_iter = k;
+    S->status = status;
+    __threadfence();
+    S->done = 1;
+  }
+}
+
+// Residual-stage arrival: called by one thread after its block's norm partial is stored;
+// returns true for the last of `expect` arrivals of the matrix this iteration.
+__device__ __forceinline__ bool residual_arrive(MatState* S, int expect) {
+  __threadfence();
+  return atomicAdd(&S->arrivals, 1) == expect - 1;
+}
+
+// ints from MatState::done to MatState::stop_iter (chain kernel's first-tile snapshot)
+constexpr int kStopIterOffset = (int)((offsetof(MatState, stop_iter) - offsetof(MatState, done)) / sizeof(int));
+
 struct GemmProblem {
   const CUtensorMap* tmA;
   const CUtensorMap* tmB;
@@ -101,9 +161,6 @@ struct GemmProblem {
   int p;
   int pad2_;
 };
-
-// ints from MatState::done to MatState::stop_iter (static_assert in kernels.cuh)
-constexpr int kStopIterOffset = 4;
 
 struct GemmLaunch {
   const GemmProblem* probs;      // problem table (even iterations)
@@ -989,6 +1046,16 @@ __device__ __forceinline__ uint64_t operand_desc(uint32_t base, int k, int mn_ma
 
 // ---------------------------------------------------------------- the kernel
 
+// Main-GEMM k-block timeline (prism_debug_trace_gemm): for launches whose first problem has
+// epilogue mode g_trace_mode, each CTA's first tile records [0,64) producer issue (after
+// its empty wait), [64,128) MMA full arrival, [128,192) MMA issue done, per k-block, and
+// [192 + 4 j ..] tile j MMA start / end, epilogue start / end.  Kept compiled in: with the
+// hooks removed the MMA-issue and producer loops schedule differently and the GEMMs ran
+// 8-10 % slower on B200 (A/B on one box).
+__device__ unsigned long long* g_gemm_trace2 = nullptr;
+__device__ int g_trace_mode = -1;
+constexpr int TRACE2_W = 376;
+
 template <class Cfg>
 __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
   extern __shared__ uint8_t smem_raw[];
@@ -1014,6 +1081,8 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
   const int cid = Cfg::CTA2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;   // tile-loop index / stride
   const int ncl = Cfg::CTA2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   const GemmProblem* __restrict__ probs = L.probs;
+  unsigned long long* trace2 = nullptr;
+  if (g_gemm_trace2 && L.probs[0].mode == g_trace_mode) trace2 = g_gemm_trace2 + (size_t)blockIdx.x * TRACE2_W;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {
@@ -1066,8 +1135,7 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
   auto skip_tile = [&](int matrix) -> bool {
     if (!L.done) return false;
     const int* st = L.done + (size_t)matrix * L.done_stride;
-    if (L.early) return *reinterpret_cast<const volatile int*>(st + kStopIterOffset) < kcur;
-    return st[0] != 0;
+    return st[0] != 0;   // the stop test ran in this iteration's residual stage (final here)
   };
 
   if (warp < 4) {
@@ -1110,6 +1178,7 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
             if constexpr (Cfg::LOB)
               load_operand<Cfg>(sB2, P.tmB_lo, &full[stage], bn0, kb * Cfg::BK, Cfg::B_ROWS, P.b_mn);
           }
+          if (trace2 && t == cid && kb < 64) trace2[kb] = globaltimer_ns();
           if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -1121,6 +1190,7 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
+      int tcount = 0;
       for (int t = cid; t < L.ntiles; t += ncl) {
         const uint32_t code = L.tiles[t];
         const GemmProblem& P = probs[code >> 20];
@@ -1136,6 +1206,8 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
           const uint32_t dt = tmem_base + acc * Cfg::BN;
           for (int kb = kb0; kb < kb1; ++kb) {
             mbar_wait(&full[stage], phase);
+            if (trace2 && t == cid && kb < 64) trace2[64 + kb] = globaltimer_ns();
+            if (trace2 && kb == kb_lo && tcount < 8) trace2[192 + 4 * tcount] = globaltimer_ns();
             tc_fence_after();
             const uint32_t aA = smem_u32(stage_base + stage * Cfg::STAGE_BYTES);
             const uint32_t aB = aA + Cfg::A_BYTES;
@@ -1154,11 +1226,14 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
               }
             }
             umma_commit<Cfg::CG>(&empty[stage]);     // smem slots (of both CTAs) free once these MMAs retire
+            if (trace2 && t == cid && kb < 64) trace2[128 + kb] = globaltimer_ns();
             if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
           }
           umma_commit<Cfg::CG>(&tfull[acc]);          // accumulator (chunk) ready for both epilogues
           if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
+        if (trace2 && tcount < 8) trace2[192 + 4 * tcount + 1] = globaltimer_ns();
+        ++tcount;
       }
     }
     }
@@ -1176,6 +1251,7 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
     int acc = 0;
     uint32_t acc_phase = 0;
     uint32_t cph = 0;       // bf16: phase bits of this warp's two C-block barriers
+    int etcount = 0;
     // accumulator release: one arrival per epilogue warp on the leader's tempty barrier
     auto release_acc = [&](uint64_t* bar) {
       tc_fence_before();
@@ -1227,6 +1303,7 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
           if (c_begin + 1 < c_end) c_fetch(c_begin + 1);
         }
         mbar_wait(&tfull[acc], acc_phase);
+        if (trace2 && et == 0 && leader && etcount < 8) trace2[192 + 4 * etcount + 2] = globaltimer_ns();
         tc_fence_after();
         const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * Cfg::BN;
         uint32_t ra[32], rb[32];
@@ -1341,6 +1418,8 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
         }
         named_bar_sync(1, 32 * Cfg::EPI_WARPS);
       }
+      if (trace2 && et == 0 && leader && etcount < 8) trace2[192 + 4 * etcount + 3] = globaltimer_ns();
+      ++etcount;
     }
     if (Cfg::KIND == 0 && lane == 0) bulk_wait_all();   // this warp's TMA stores are complete
   }

@@ -4,9 +4,19 @@
 
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/prism.h"
 
 namespace prism {
+// NVTX range for the lifetime of the object (phases of a call on the host timeline).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 // Record `msg` as the calling thread's last error (prism_last_error) and return `s`.
 prism_status fail_ext(prism_status s, const std::string& msg);
 // The handle's auxiliary (communication) stream on the current device, created on first use.

@@ -9,22 +9,6 @@
 
 namespace prism {
 
-// Per-matrix solver state (device memory, one per matrix of the batch).
-struct MatState {
-  double c;          // ||A||_F
-  double alpha;      // current alpha_k (read by GEMM epilogues)
-  double r_prev;     // ||R_{k-1}||_F
-  float resid;       // ||R_final||_F / sqrt(s)
-  int done;          // 1 once the matrix stopped (skip all further work)
-  int iters;         // updates applied
-  int status;        // PRISM_CONVERGED ...
-  int incr;          // consecutive residual increases
-  int stop_iter;     // iteration k at which the matrix stopped (INT_MAX while active; -1: zero
-                     // input); GEMMs that start before k_alpha completes skip on stop_iter < k
-};
-
-static_assert(offsetof(MatState, stop_iter) - offsetof(MatState, done) == kStopIterOffset * sizeof(int),
-              "GEMM tile skipping reads stop_iter at a fixed offset from done");
 
 // Per-matrix static description (device memory).
 struct MatDesc {
@@ -206,6 +190,23 @@ __global__ void __launch_bounds__(256) k_fro_final(SolveParams P) {
   if (threadIdx.x == 0) {
     if (P.fro2_out) P.fro2_out[b] = v;   // row-block: the caller all-reduces it
     else P.st[b].c = sqrt(v);
+  }
+}
+
+// End of a residual-stage SIMT block (R = I - M, DB Newton's begin, the row-block unpack):
+// store this block's norm partial; the last block of the matrix runs the stop test (R12).
+__device__ __forceinline__ void residual_stage_end(const SolveParams& P, int b, int slot, double acc) {
+  __shared__ int s_last;
+  const MatDesc& D = P.mats[b];
+  if (threadIdx.x == 0) {
+    D.norm_part[slot] = (float)acc;
+    s_last = residual_arrive(&P.st[b], D.tiles_m * D.tiles_n) ? 1 : 0;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x < 32) {
+    __threadfence();
+    residual_stop_warp(&P.st[b], D.norm_part, D.tiles_m * D.tiles_n, *P.iter, P.tol, D.s, P.max_iters,
+                       P.resid_hist + (size_t)b * (P.max_iters + 1), threadIdx.x);
   }
 }
 
@@ -403,6 +404,8 @@ __global__ void __launch_bounds__(256) k_normalize(SolveParams P) {
       x.store(D.Y[0], D.Y_lo[0], (long long)r * D.ldx + col, nv, nv == V::VE, 1.f, PREC == 1);
     }
   }
+  if (lt == 0)   // the residual stage's stop test sums every norm partial: unscheduled ones stay 0
+    for (int t = threadIdx.x; t < D.tiles_m * D.tiles_n; t += 256) D.norm_part[t] = 0.f;
   if (lt == 0 && threadIdx.x == 0) {
     if (b == 0) *P.iter = 0;
     MatState& S = P.st[b];
@@ -413,6 +416,7 @@ __global__ void __launch_bounds__(256) k_normalize(SolveParams P) {
     S.incr = 0;
     S.done = (c == 0.0) ? 1 : 0;
     S.stop_iter = (c == 0.0) ? -1 : 0x7fffffff;
+    S.arrivals = 0;
     S.status = (c == 0.0) ? 4 : 1;   // ZERO_INPUT / MAX_ITERS until decided
   }
 }
@@ -485,7 +489,7 @@ __global__ void __launch_bounds__(256) k_db_begin(SolveParams P, int bn) {
     acc += r * r;
   }
   acc = block_sum<double, 256>(acc, scratch);
-  if (threadIdx.x == 0) D.norm_part[tm * D.tiles_n + tn] = (float)acc;
+  residual_stage_end(P, b, tm * D.tiles_n + tn, acc);
 }
 
 constexpr int kGJ = 128;          // Gauss-Jordan block
@@ -838,16 +842,52 @@ __device__ __forceinline__ bool fit_at(const SolveParams& P, int k) {
   return P.fit == 0 && k < P.max_iters && k >= P.warmup;
 }
 
-__global__ void __launch_bounds__(256) k_sketch(SolveParams P) {
+// Residual stage end + sketch, one launch after the residual product (GEMM epilogue or SIMT
+// kernel wrote the per-tile sums of R^2): block x = 0 of matrix b runs the stop test of
+// iteration k (R12) on ||R_k||_F from every norm partial (fixed order), so the chain, alpha,
+// square and apply launches of iteration k all skip a matrix that stops here; blocks x >= 1
+// draw S_k (and W = [S_hi; S_lo]) for the fit.  grid (1 + ceil(p s / 2 / 256), batch).
+__global__ void __launch_bounds__(256) k_stop_sketch(SolveParams P) {
   griddep_wait();
   griddep_launch();
   const int b = blockIdx.y;
   const MatDesc& D = P.mats[b];
   const int k = *P.iter;
+  if (blockIdx.x == 0) {
+    __shared__ double scratch[8];
+    MatState& S = P.st[b];
+    if (S.done) return;
+    double part = 0.0;
+    const int nparts = D.tiles_m * D.tiles_n;   // unscheduled (lower-triangle) entries stay 0
+    for (int t = threadIdx.x; t < nparts; t += 256) part += (double)D.norm_part[t];
+    const double r2 = block_sum<double, 256>(part, scratch);
+    if (threadIdx.x == 0) {
+      const double r = sqrt(r2), s = (double)D.s;
+      int stop = 0, status = 1, incr = 0;
+      if (!isfinite(r)) { stop = 1; status = 3; }
+      else if (r <= P.tol * sqrt(s)) { stop = 1; status = 0; }
+      else {
+        incr = (k >= 1 && r > S.r_prev) ? S.incr + 1 : 0;
+        if (incr >= 5) { stop = 1; status = 2; }
+        else if (k >= P.max_iters) { stop = 1; status = 1; }
+      }
+      P.resid_hist[(size_t)b * (P.max_iters + 1) + k] = (float)(r / sqrt(s));
+      if (isfinite(r) && !(r <= P.tol * sqrt(s))) S.incr = incr;
+      S.r_prev = r;
+      S.resid = (float)(r / sqrt(s));
+      S.iters = k;
+      if (stop) {
+        S.stop_iter = k;
+        S.status = status;
+        S.done = 1;
+      }
+    }
+    return;
+  }
   if (!fit_at(P, k) || P.st[b].done) return;
   const int s = D.s, p = P.p;
   const long long total = (long long)p * s;
-  const long long e = (long long)blockIdx.x * 256 + threadIdx.x;   // pair index
+  const long long e = (long long)(blockIdx.x - 1) * 256 + threadIdx.x;   // pair index
   if (2 * e >= total) return;
   double z[2];
   sketch_pair(P.seed, (uint32_t)k, (uint32_t)D.sketch_id, (uint32_t)e, &z[0], &z[1]);
@@ -1061,65 +1101,15 @@ __device__ double argmin_quartic_free(const double c[5], double a_default) {
 // waiting for the predecessor (its state writes still follow the wait: the predecessor
 // reads the done flags); only the fit's inputs come from the predecessor.
 __global__ void __launch_bounds__(256) k_alpha(SolveParams P, int pre_wait) {
-  if (!pre_wait) {
-    griddep_wait();
-    griddep_launch();
-  }
-  __shared__ double scratch[8];
-  __shared__ int s_stop;
+  (void)pre_wait;
+  griddep_wait();
+  griddep_launch();
   const int k = *P.iter;
   const int do_fit = P.kind_db ? (P.fit != 1 && k < P.max_iters && k >= P.warmup) : (fit_at(P, k) ? 1 : 0);
   const int b = blockIdx.x;
   const MatDesc& D = P.mats[b];
   MatState& S = P.st[b];
-  if (S.done) {
-    if (pre_wait) griddep_wait();   // (exit triggers the dependents)
-    return;
-  }
-  const int s = D.s;
-  // ||R_k||_F^2 from the Gram per-tile partials (fixed order, scheduled tiles only)
-  double part = 0.0;
-  const int ntile = D.tiles_m * D.tiles_n;
-  for (int t = threadIdx.x; t < ntile; t += 256) {
-    const int tm = t / D.tiles_n, tn = t - tm * D.tiles_n;
-    const bool sched = !D.sym || (tn * 256 + 255 >= tm * 128);   // bf16 tiles (BM=128, BN=256)
-    const bool sched_tf = !D.sym || (tn * 128 + 127 >= tm * 128);
-    if (P.precision == 0 ? sched : sched_tf) part += (double)D.norm_part[t];
-  }
-  const double r2 = block_sum<double, 256>(part, scratch);
-  const double r = sqrt(r2);
-  // stop test (R12) on state final since the previous iteration
-  int stop = 0, status = 1, incr = 0;
-  if (threadIdx.x == 0) {
-    if (!isfinite(r)) { stop = 1; status = 3; }
-    else if (r <= P.tol * sqrt((double)s)) { stop = 1; status = 0; }
-    else {
-      incr = (k >= 1 && r > S.r_prev) ? S.incr + 1 : 0;
-      if (incr >= 5) { stop = 1; status = 2; }
-      else if (k >= P.max_iters) { stop = 1; status = 1; }
-    }
-  }
-  if (pre_wait) {
-    griddep_wait();
-    griddep_launch();
-  }
-  if (threadIdx.x == 0) {
-    P.resid_hist[(size_t)b * (P.max_iters + 1) + k] = (float)(r / sqrt((double)s));
-    if (isfinite(r) && !(r <= P.tol * sqrt((double)s))) S.incr = incr;
-    S.r_prev = r;
-    S.resid = (float)(r / sqrt((double)s));
-    if (stop) {
-      S.stop_iter = k;
-      S.done = 1;
-      S.status = status;
-      S.iters = k;
-    } else {
-      S.iters = k;
-    }
-    s_stop = stop;
-  }
-  __syncthreads();
-  if (s_stop) return;
+  if (S.done) return;   // stopped in this iteration's residual stage (or earlier)
   if (threadIdx.x >= 32) return;   // warp 0 fits alpha
   double a;
   if (!do_fit) {

@@ -301,7 +301,9 @@ prism_status prism_polar_sharded_tr(prism_handle h, const prism_transport* tr, i
     if (cudaEventRecord(e0, st) != cudaSuccess || cudaStreamWaitEvent(cs, e0, 0) != cudaSuccess)
       return fail_ext(PRISM_ERR_CUDA, "stream ordering");
     const int nb = (int)L.mine.size();
+    prism::NvtxRange nv_call("prism:polar_sharded");
     for (int j = 0; j < nb; ++j) {
+      prism::NvtxRange nv("prism:sharded bucket (solve + owners' broadcasts)");
       const std::vector<int>& b = L.mine[j];
       if (!b.empty()) {
         std::vector<int64_t> mm, nn, la, lq, ids;

@@ -1134,9 +1134,16 @@ static prism_status get_plan(prism_handle h, const Request& r, size_t ws_bytes, 
 
 static prism_status run_solve(prism_handle h, const Request& r0, const prism_report* rep, size_t ws_bytes,
                               cudaStream_t st) {
+  NvtxRange nv_call(r0.rowblock ? "prism:rowblock" : r0.sqrt_kind ? "prism:sqrt_invsqrt" : r0.sign_kind ? "prism:sign"
+                     : r0.inv_q ? "prism:inv_root" : r0.cheb_kind ? "prism:chebyshev_inverse"
+                     : r0.db_kind ? "prism:db_newton" : "prism:polar");
   Request r = r0;
   Plan* P = nullptr;
-  prism_status gs = get_plan(h, r, ws_bytes, &P);
+  prism_status gs;
+  {
+    NvtxRange nv("prism:plan");
+    gs = get_plan(h, r, ws_bytes, &P);
+  }
   if (gs) return gs;
 
   SolveParams S = P->params;   // report pointers are only read by k_report (outside the graph)
@@ -1236,10 +1243,14 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
         PRISM_CK(launch_gemm(prec, ROLE_GRAM, g_gram, s2));
       }
     }
-    if (sketched) {
-      KindTimer t(h, s2, 3, timed ? 1 + n_chain_launches : 0);
-      PRISM_CK(launch_k(k_sketch, dim3((p * P->max_s / 2 + 256) / 256, B), dim3(256), 0, s2, 1, S));
-      for (int j = 0; j < P->n_chain; ++j) PRISM_CK(launch_chain(prec, chain_pass(*P, j), g_chaint[j], s2));
+    {
+      // residual-stage stop test (block 0 per matrix) + S_k: every later launch of the
+      // iteration skips the matrices that stop here
+      KindTimer t(h, s2, 3, timed ? 1 + (sketched ? n_chain_launches : 0) : 0);
+      const int nsk = sketched ? (p * P->max_s / 2 + 255) / 256 : 0;
+      PRISM_CK(launch_k(k_stop_sketch, dim3(1 + nsk, B), dim3(256), 0, s2, 1, S));
+      if (sketched)
+        for (int j = 0; j < P->n_chain; ++j) PRISM_CK(launch_chain(prec, chain_pass(*P, j), g_chaint[j], s2));
     }
     {
       // norm partials from the residual step; a sketch chain in between makes them final
@@ -1261,7 +1272,7 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
     return PRISM_OK;
   };
   P->per_iter_launches = P->db ? 6 + 4 * P->db_steps
-                                : 3 + (sketched ? 1 + n_chain_launches : 0) + (P->has_square ? 1 : 0) +
+                                : 3 + 1 + (sketched ? n_chain_launches : 0) + (P->has_square ? 1 : 0) +
                                       (P->has_square2 ? 1 : 0) + 1;
   ensure_attrs();   // large-smem attributes: before the graph capture and the direct launches
   if (!h->profiling) {
@@ -1293,11 +1304,13 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
       cudaGraphDestroy(g);
       if (ei != cudaSuccess) { P->exec = nullptr; return fail(PRISM_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ei)); }
     }
+    NvtxRange nv("prism:iterate (CUDA-graph WHILE loop)");
     PRISM_CK(cudaGraphLaunch(P->exec, st));
   } else {
     // profiling: direct launches bracketed by events, host-side exit once all matrices stopped
     if (!h->h_flag) PRISM_CK(cudaMallocHost(&h->h_flag, sizeof(int)));
     for (int k = 0; k <= M; ++k) {
+      NvtxRange nv("prism:iteration (direct launches)");
       prism_status bs = body(st, 0, 0, true);
       if (bs) return bs;
       PRISM_CK(cudaMemcpyAsync(h->h_flag, P->d_all_done, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -1412,6 +1425,7 @@ static prism_status host_solve(prism_handle h, int kind, int inv_q, int batch, c
                                const int64_t* ldo, const int64_t* ids, const prism_options* o,
                                const prism_report* rep, cudaStream_t caller) {
   if (!h || !o) return fail(PRISM_ERR_INVALID_ARG, "null handle / options");
+  NvtxRange nv_call("prism:host path (upload / solve / download)");
   const bool sqrt_kind = kind == 1 || kind == 5, square = kind != 0;
   if (batch < 1 || !m || !A_host || !lda || !ldo || (kind == 0 && !n) || (!sqrt_kind && !O1))
     return fail(PRISM_ERR_INVALID_ARG, "bad host-path arguments");
@@ -1811,6 +1825,7 @@ prism_status prism_polar_rowblock_tr(prism_handle h, const prism_transport* tr, 
     const int nt = (int)((n + 63) / 64);
     cudaEvent_t ev_stop = prism::handle_event(h, 8);
     for (int k = 0; k <= M; ++k) {
+      NvtxRange nv("prism:rowblock iteration");
       const int t = k & 1;
       // 1. packed partial Gram, all-reduced panel group by panel group (on the aux stream,
       //    overlapping the next group's launch; the Gram grid leaves SMs to the collective)
@@ -1839,8 +1854,9 @@ prism_status prism_polar_rowblock_tr(prism_handle h, const prism_transport* tr, 
       if (prec == PRISM_BF16) PRISM_CK(launch_k(k_resid_packed<0>, dim3(nt, nt), dim3(256), 0, st, 1, S, (const float*)P->Gp));
       else if (prec == PRISM_FP32) PRISM_CK(launch_k(k_resid_packed<1>, dim3(nt, nt), dim3(256), 0, st, 1, S, (const float*)P->Gp));
       else PRISM_CK(launch_k(k_resid_packed<2>, dim3(nt, nt), dim3(256), 0, st, 1, S, (const float*)P->Gp));
+      PRISM_CK(launch_k(k_stop_sketch, dim3(1 + (sketched ? (S.p * P->max_s / 2 + 255) / 256 : 0), 1), dim3(256), 0,
+                        st, 1, S));
       if (sketched) {
-        PRISM_CK(launch_k(k_sketch, dim3((S.p * P->max_s / 2 + 256) / 256, 1), dim3(256), 0, st, 1, S));
         for (int j = 0; j < P->n_chain; ++j)
           PRISM_CK(launch_chain(prec, chain_pass(*P, j), make_launch(*P, P->chaint[j], nullptr, r.ws, o->warmup_iters, M), st));
       }
@@ -2001,6 +2017,14 @@ prism_status prism_debug_gemm(prism_handle h, int precision, int b_mn, int mode,
   return PRISM_OK;
 }
 
+
+prism_status prism_debug_trace_gemm(unsigned long long* buf_dev, int mode) {
+  const int m = mode < 0 ? -1 : (mode & 0xFF);
+  if (set_gemm_trace_bf16(buf_dev, m) != cudaSuccess || set_gemm_trace_f32x3(buf_dev, m) != cudaSuccess ||
+      set_gemm_trace_tf32(buf_dev, m) != cudaSuccess)
+    return fail(PRISM_ERR_CUDA, "trace hook");
+  return PRISM_OK;
+}
 
 prism_status prism_debug_sketch(uint64_t seed, int64_t b, int k, int p, int s, float* S_dev, void* stream) {
   if (!S_dev || p < 1 || s < 1) return fail(PRISM_ERR_INVALID_ARG, "bad sketch args");
