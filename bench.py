@@ -677,6 +677,8 @@ def main():
     ap.add_argument("--workload", default="gpt2", choices=WORKLOADS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="N = 1: run gpt2 / gpt1b through the multi-GPU entry point (1-rank NCCL communicator)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)   # timing rule: >= 3 warm-up steps
 
@@ -699,7 +701,7 @@ def main():
             dist.barrier()
             dist.destroy_process_group()
             return rc
-    elif args.workload == "rowblock8192":
+    elif args.workload == "rowblock8192" or (args.sharded and args.workload in SHARDED):
         return run_multi(args, rank, world, dev)
 
     name, shapes, mats_np, opts, desc, kind = workload(args.workload, rank)

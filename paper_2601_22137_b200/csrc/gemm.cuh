@@ -66,6 +66,8 @@ __host__ __device__ constexpr int chain_ng(int pass) {
 // Per-matrix solver state (device memory, one per matrix of the batch).
 struct MatState {
   double c;          // ||A||_F
+  double inv_c;      // 1 / c   (folded normalisation: iteration 0 reads A itself)
+  double inv_c2;     // 1 / c^2
   double alpha;      // current alpha_k (read by GEMM epilogues)
   double r_prev;     // ||R_{k-1}||_F
   float resid;       // ||R_final||_F / sqrt(s)
@@ -165,6 +167,7 @@ struct GemmProblem {
 struct GemmLaunch {
   const GemmProblem* probs;      // problem table (even iterations)
   const GemmProblem* probs_odd;  // problem table for odd iterations (ping-pong buffers) or null
+  const GemmProblem* probs_k0;   // problem table of iteration 0 (folded normalisation) or null
   const uint32_t* tiles;         // (problem << 20) | (tm << 10) | tn
   const int* done;               // per matrix (stride done_stride ints): 1 = stopped, skip its tiles
   const int* iter;               // device iteration counter k (or null): run only if iter_lo <= k < iter_hi
@@ -578,11 +581,11 @@ __device__ __forceinline__ void epi_segment(const EpiArgs& P, int mode, bool sym
     for (int u = 0; u < 32; ++u) v[u] = coefC * c[u] + coefA * d[u];
   } else if (mode == EPI_RESID) {
 #pragma unroll
-    for (int u = 0; u < 32; ++u) v[u] = ((j0 + u == i) ? 1.f : 0.f) - d[u];
+    for (int u = 0; u < 32; ++u) v[u] = ((j0 + u == i) ? 1.f : 0.f) - coefA * d[u];
     if (P.gdiag && row_ok && i >= j0 && i < j0 + 32) {
 #pragma unroll
       for (int u = 0; u < 32; ++u)
-        if (j0 + u == i) P.gdiag[i] = d[u];
+        if (j0 + u == i) P.gdiag[i] = coefA * d[u];
     }
   } else {
 #pragma unroll
@@ -760,11 +763,11 @@ __device__ __forceinline__ void epi_block_tma(const EpiArgs& P, const CUtensorMa
     for (int u = 0; u < 32; ++u) v[u] = coefC * c[u] + coefA * d[u];
   } else if (mode == EPI_RESID) {
 #pragma unroll
-    for (int u = 0; u < 32; ++u) v[u] = ((j0 + u == i) ? 1.f : 0.f) - d[u];
+    for (int u = 0; u < 32; ++u) v[u] = ((j0 + u == i) ? 1.f : 0.f) - coefA * d[u];
     if (P.gdiag && row_ok && i >= j0 && i < j0 + 32) {
 #pragma unroll
       for (int u = 0; u < 32; ++u)
-        if (j0 + u == i) P.gdiag[i] = d[u];
+        if (j0 + u == i) P.gdiag[i] = coefA * d[u];
     }
   } else {
 #pragma unroll
@@ -1130,6 +1133,7 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
     kcur = k;
     run = k >= L.iter_lo && k < L.iter_hi;
     if (L.probs_odd && (k & 1)) probs = L.probs_odd;
+    if (L.probs_k0 && k == 0) probs = L.probs_k0;
   }
   // tiles of stopped matrices are skipped (the same decision in every role)
   auto skip_tile = [&](int matrix) -> bool {
@@ -1275,7 +1279,8 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
       const int i0 = tm * Cfg::TILE_M + (int)rank * Cfg::BM + q * 32;
       const int i = i0 + lane;                     // output row of this thread
       float coefA = 1.f, coefC = 1.f;
-      if (mode == EPI_POLY || mode == EPI_APPLY || mode == EPI_APPLY2) {
+      // (RESID: coefA = 1, or 1/c^2 through `alpha` in a folded iteration 0: R = I - D/c^2)
+      if (mode == EPI_POLY || mode == EPI_APPLY || mode == EPI_APPLY2 || mode == EPI_RESID) {
         const double al = (P.eA | P.eC) ? *P.alpha : 1.0;
         const double pa = P.eA == 0 ? 1.0 : P.eA == 1 ? al : P.eA == 2 ? al * al : al * al * al;
         const double pc = P.eC == 0 ? 1.0 : P.eC == 1 ? al : P.eC == 2 ? al * al : al * al * al;

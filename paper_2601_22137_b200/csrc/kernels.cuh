@@ -16,6 +16,9 @@ struct MatDesc {
   void* Q;             // polar output / sqrt output
   void* Q2;            // inv-sqrt output (sqrt path) or null
   long long lda, ldq;
+  long long ldx0;      // leading dimension of X[0] (= ldq when X[0] is the caller's output Q)
+  int fold;            // folded normalisation for this matrix (BF16 / TF32 polar, TMA-legal A, Q)
+  int pad0_;
   int m, n;            // user shape
   int s, L;            // small side / large side (polar); n, n (sqrt)
   int trans;           // polar: 1 if the compute layout Xt (s x L) is A^T (tall A)
@@ -132,25 +135,35 @@ __global__ void __launch_bounds__(256) k_fro_partials(SolveParams P) {
   const bool vok = ((D.lda * esz) % 16 == 0) && ((reinterpret_cast<uintptr_t>(D.A) & 15) == 0);
   const long long nv = vok ? D.n / vec : 0;       // 16-B vectors per row
   // block jp sums a fixed contiguous share of the flattened (row, vector) index space,
-  // four independent 16-B loads in flight per thread (fixed assignment: deterministic)
+  // eight independent 16-B loads in flight per thread (fixed assignment: deterministic)
   const long long total = (long long)D.m * nv;
   const long long per = (total + parts - 1) / parts;
   const long long beg = jp * per, end = min(total, beg + per);
   const char* A = static_cast<const char*>(D.A);
   double acc = 0.0;
-  for (long long base = beg + threadIdx.x; base < end; base += 4 * 256) {
-    uint4 w[4];
+  // (row, vector) of the thread's first index; later indices advance by 256 vectors with an
+  // incremental carry instead of a 64-bit division per load
+  long long jr = 0, jc = 0;
+  if (nv > 0) {
+    const long long j0 = beg + threadIdx.x;
+    jr = j0 / nv;
+    jc = j0 - jr * nv;
+  }
+  for (long long base = beg + threadIdx.x; base < end; base += 8 * 256) {
+    uint4 w[8];
+    long long r = jr, c = jc;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < 8; ++u) {
       const long long j = base + (long long)u * 256;
       w[u] = make_uint4(0, 0, 0, 0);
-      if (j < end) {
-        const long long r = j / nv, c = j - r * nv;
-        w[u] = __ldg(reinterpret_cast<const uint4*>(A + r * D.lda * esz) + c);
-      }
+      if (j < end) w[u] = __ldg(reinterpret_cast<const uint4*>(A + r * D.lda * esz) + c);
+      c += 256;
+      while (c >= nv && nv > 0) { c -= nv; ++r; }
     }
+    jr = r;
+    jc = c;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < 8; ++u) {
       if (bf16) {
         const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w[u]);
 #pragma unroll
@@ -188,8 +201,14 @@ __global__ void __launch_bounds__(256) k_fro_final(SolveParams P) {
   double v = (threadIdx.x < parts) ? P.fro_part[b * kFroParts + threadIdx.x] : 0.0;
   v = block_sum<double, 256>(v, scratch);
   if (threadIdx.x == 0) {
-    if (P.fro2_out) P.fro2_out[b] = v;   // row-block: the caller all-reduces it
-    else P.st[b].c = sqrt(v);
+    if (P.fro2_out) {
+      P.fro2_out[b] = v;   // row-block: the caller all-reduces it
+    } else {
+      const double c = sqrt(v);
+      P.st[b].c = c;
+      P.st[b].inv_c = c > 0.0 ? 1.0 / c : 0.0;
+      P.st[b].inv_c2 = c > 0.0 ? 1.0 / v : 0.0;
+    }
   }
 }
 
@@ -214,7 +233,12 @@ __device__ __forceinline__ void residual_stage_end(const SolveParams& P, int b, 
 __global__ void k_set_c(SolveParams P) {
   griddep_wait();
   griddep_launch();
-  if (threadIdx.x == 0) P.st[blockIdx.x].c = sqrt(P.fro2_in[blockIdx.x]);
+  if (threadIdx.x == 0) {
+    const double v = P.fro2_in[blockIdx.x], c = sqrt(v);
+    P.st[blockIdx.x].c = c;
+    P.st[blockIdx.x].inv_c = c > 0.0 ? 1.0 / c : 0.0;
+    P.st[blockIdx.x].inv_c2 = c > 0.0 ? 1.0 / v : 0.0;
+  }
 }
 
 __device__ __forceinline__ void store_x(void* hi, void* lo, long long idx, float v, int precision);
@@ -277,11 +301,61 @@ __device__ __forceinline__ void store_x(void* hi, void* lo, long long idx, float
 // Layout tiles (normalise / finalise): 32 rows x 32 16-byte vectors, one block
 // (256 threads, 4 vectors each, a warp = one 512-B row segment) per tile over a
 // batch-wide flat list.  X keeps A's row-major layout, so both are scaled copies.
+// One 16-byte vector of a layout tile as raw bits (4 registers; + the lo plane in 3xTF32):
+// the memory kernels issue every load of a thread before decoding / storing, without the
+// register cost of decoded floats (occupancy is what hides the HBM latency here).
+template <int PREC>
+struct Raw {
+  uint4 h, l;
+};
+template <int PREC>
+__device__ __forceinline__ Raw<PREC> load_raw(const void* base, const void* lo, long long idx, int n_valid, bool vec) {
+  constexpr int ESZ = PREC == 0 ? 2 : 4, VE = 16 / ESZ;
+  Raw<PREC> r;
+  r.l = make_uint4(0, 0, 0, 0);
+  const char* p = static_cast<const char*>(base) + idx * ESZ;
+  const char* q = (PREC == 1 && lo) ? static_cast<const char*>(lo) + idx * ESZ : nullptr;
+  if (vec) {
+    r.h = __ldg(reinterpret_cast<const uint4*>(p));
+    if (q) r.l = __ldg(reinterpret_cast<const uint4*>(q));
+  } else {
+    uint32_t w[4] = {0, 0, 0, 0}, wl[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int e = 0; e < VE; ++e) {
+      if (e >= n_valid) continue;
+      if (PREC == 0) {
+        const uint32_t b = *reinterpret_cast<const unsigned short*>(p + 2 * e);
+        w[e >> 1] |= b << (16 * (e & 1));
+      } else {
+        w[e] = *reinterpret_cast<const uint32_t*>(p + 4 * e);
+        if (q) wl[e] = *reinterpret_cast<const uint32_t*>(q + 4 * e);
+      }
+    }
+    r.h = make_uint4(w[0], w[1], w[2], w[3]);
+    r.l = make_uint4(wl[0], wl[1], wl[2], wl[3]);
+  }
+  return r;
+}
+
 template <int PREC>   // 0 bf16, 1 fp32 hi+lo (3xTF32 split), 2 fp32
 struct Vec {
   static constexpr int ESZ = PREC == 0 ? 2 : 4;
   static constexpr int VE = 16 / ESZ;
   float v[VE];
+  __device__ __forceinline__ void from_raw(const Raw<PREC>& r) {
+    if (PREC == 0) {
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r.h);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) { const float2 f = __bfloat1622float2(h[e]); v[2 * e] = f.x; v[2 * e + 1] = f.y; }
+    } else {
+      v[0] = __uint_as_float(r.h.x); v[1] = __uint_as_float(r.h.y);
+      v[2] = __uint_as_float(r.h.z); v[3] = __uint_as_float(r.h.w);
+      if (PREC == 1) {
+        v[0] += __uint_as_float(r.l.x); v[1] += __uint_as_float(r.l.y);
+        v[2] += __uint_as_float(r.l.z); v[3] += __uint_as_float(r.l.w);
+      }
+    }
+  }
   __device__ __forceinline__ void load(const void* base, const void* lo, long long idx, int n_valid, bool vec) {
     if (PREC == 0) {
       const __nv_bfloat16* p = static_cast<const __nv_bfloat16*>(base) + idx;
@@ -353,60 +427,81 @@ __global__ void __launch_bounds__(256) k_normalize(SolveParams P) {
   const int t = blockIdx.x;
   const int b = __ldg(P.tile_mat + t);   // one load (a binary search over tile_off was ~6 dependent loads)
   const MatDesc& D = P.mats[b];
+  if (D.fold) return;   // iteration 0 reads A itself (k_init_state did the rest)
+  // the descriptor's fields in registers: read through the reference they would be reloaded
+  // from global memory after every store (possible aliasing), a dependent load per vector
+  const int Dm = D.m, Dn = D.n;
+  const long long Dlda = D.lda, Dldx = D.ldx;
+  const void* const DA = D.A;
+  void* const X0 = D.X[0];
+  void* const X0l = D.X_lo[0];
+  void* const Y0 = D.Y[0];
+  void* const Y0l = D.Y_lo[0];
   const double c = P.st[b].c;   // written by k_fro_final
   const float inv = c > 0.0 ? (float)(1.0 / c) : 0.f;
   const int TW = 32 * V::VE;
-  const int tcn = (D.n + TW - 1) / TW;
+  const int tcn = (Dn + TW - 1) / TW;
   const int lt = t - P.tile_off[b];
   const int r0 = (lt / tcn) * 32, c0 = (lt % tcn) * TW;
-  const bool src_vec = ((D.lda * V::ESZ) % 16 == 0) && ((reinterpret_cast<uintptr_t>(D.A) & 15) == 0);
+  const bool src_vec = ((Dlda * V::ESZ) % 16 == 0) && ((reinterpret_cast<uintptr_t>(DA) & 15) == 0);
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int slot = threadIdx.x + 256 * j;
     const int r = r0 + slot / 32, col = c0 + (slot % 32) * V::VE;
-    if (r >= D.m || col >= D.n) continue;
-    const int nv = min(V::VE, D.n - col);
+    if (r >= Dm || col >= Dn) continue;
+    const int nv = min(V::VE, Dn - col);
     V x;
-    x.load(D.A, nullptr, (long long)r * D.lda + col, nv, src_vec && nv == V::VE);
+    x.load(DA, nullptr, (long long)r * Dlda + col, nv, src_vec && nv == V::VE);
     if (P.kind_db) {
       // DB Newton: X_0 = M_0 = A, Y_0 = I (no scaling, R28)
-      x.store(D.X[0], D.X_lo[0], (long long)r * D.ldx + col, nv, nv == V::VE, 1.f, PREC == 1);
+      x.store(X0, X0l, (long long)r * Dldx + col, nv, nv == V::VE, 1.f, PREC == 1);
 #pragma unroll
       for (int e = 0; e < V::VE; ++e)
-        if (e < nv) D.Mst[(long long)r * D.ldx + col + e] = x.v[e];
+        if (e < nv) D.Mst[(long long)r * Dldx + col + e] = x.v[e];
 #pragma unroll
       for (int e = 0; e < V::VE; ++e) x.v[e] = (col + e == r) ? 1.f : 0.f;
-      x.store(D.Y[0], D.Y_lo[0], (long long)r * D.ldx + col, nv, nv == V::VE, 1.f, PREC == 1);
+      x.store(Y0, Y0l, (long long)r * Dldx + col, nv, nv == V::VE, 1.f, PREC == 1);
       continue;
     }
     if (P.kind_cheb) {
       // A' = A/c (row-major, Y[0]) and X_0 = A'^T: transposed scalar stores
-      x.store(D.Y[0], D.Y_lo[0], (long long)r * D.ldx + col, nv, nv == V::VE, inv, PREC == 1);
+      x.store(Y0, Y0l, (long long)r * Dldx + col, nv, nv == V::VE, inv, PREC == 1);
 #pragma unroll
       for (int e = 0; e < V::VE; ++e)
-        if (e < nv) store_x(D.X[0], D.X_lo[0], (long long)(col + e) * D.ldx + r, x.v[e] * inv, PREC);
+        if (e < nv) store_x(X0, X0l, (long long)(col + e) * Dldx + r, x.v[e] * inv, PREC);
       continue;
     }
     if (P.inv_q) {
       const double cq = 2.0 * c / (P.inv_q + 1);
-      x.store(D.Y[0], D.Y_lo[0], (long long)r * D.ldx + col, nv, nv == V::VE, c > 0.0 ? (float)(1.0 / cq) : 0.f,
+      x.store(Y0, Y0l, (long long)r * Dldx + col, nv, nv == V::VE, c > 0.0 ? (float)(1.0 / cq) : 0.f,
               PREC == 1);
 #pragma unroll
       for (int e = 0; e < V::VE; ++e) x.v[e] = (col + e == r) ? 1.f : 0.f;
-      x.store(D.X[0], D.X_lo[0], (long long)r * D.ldx + col, nv, nv == V::VE,
+      x.store(X0, X0l, (long long)r * Dldx + col, nv, nv == V::VE,
               c > 0.0 ? (float)pow(cq, -1.0 / P.inv_q) : 0.f, PREC == 1);
       continue;
     }
-    x.store(D.X[0], D.X_lo[0], (long long)r * D.ldx + col, nv, nv == V::VE, inv, PREC == 1);
+    x.store(X0, X0l, (long long)r * Dldx + col, nv, nv == V::VE, inv, PREC == 1);
     if (P.kind_sqrt) {
 #pragma unroll
       for (int e = 0; e < V::VE; ++e) x.v[e] = (col + e == r) ? 1.f : 0.f;
-      x.store(D.Y[0], D.Y_lo[0], (long long)r * D.ldx + col, nv, nv == V::VE, 1.f, PREC == 1);
+      x.store(Y0, Y0l, (long long)r * Dldx + col, nv, nv == V::VE, 1.f, PREC == 1);
     }
   }
-  if (lt == 0)   // the residual stage's stop test sums every norm partial: unscheduled ones stay 0
-    for (int t = threadIdx.x; t < D.tiles_m * D.tiles_n; t += 256) D.norm_part[t] = 0.f;
-  if (lt == 0 && threadIdx.x == 0) {
+
+}
+
+// Solver state of every matrix at the start of a solve (after ||A||_F): alpha, residual
+// history bookkeeping, done / status (zero input), and the norm partials zeroed (the stop
+// test sums every entry; unscheduled ones stay 0).  grid (batch).
+__global__ void k_init_state(SolveParams P) {
+  griddep_wait();
+  griddep_launch();
+  const int b = blockIdx.x;
+  const MatDesc& D = P.mats[b];
+  for (int t = threadIdx.x; t < D.tiles_m * D.tiles_n; t += blockDim.x) D.norm_part[t] = 0.f;
+  if (threadIdx.x == 0) {
+    const double c = P.st[b].c;
     if (b == 0) *P.iter = 0;
     MatState& S = P.st[b];
     S.alpha = P.ataylor;
@@ -417,7 +512,7 @@ __global__ void __launch_bounds__(256) k_normalize(SolveParams P) {
     S.done = (c == 0.0) ? 1 : 0;
     S.stop_iter = (c == 0.0) ? -1 : 0x7fffffff;
     S.arrivals = 0;
-    S.status = (c == 0.0) ? 4 : 1;   // ZERO_INPUT / MAX_ITERS until decided
+    S.status = (c == 0.0) ? 4 : 1;
   }
 }
 
@@ -1100,62 +1195,60 @@ __device__ double argmin_quartic_free(const double c[5], double a_default) {
 // sketch chain or the DB sweep runs in between), so the stop test is computed before
 // waiting for the predecessor (its state writes still follow the wait: the predecessor
 // reads the done flags); only the fit's inputs come from the predecessor.
-__global__ void __launch_bounds__(256) k_alpha(SolveParams P, int pre_wait) {
-  (void)pre_wait;
+// alpha_k of every active matrix: one warp per matrix, fp64.  Instantiated per kind so each
+// launch carries only its own fit (a kernel holding every kind's argmin stalled on
+// instruction fetch: ncu stall_no_inst 50 %): AK 0 polar / sqrt / sign (quartic of the
+// factored loss), 1 Chebyshev (quadratic), 2 inverse Newton (degree 2q), 3 DB Newton (free quartic).
+template <int AK>
+__global__ void __launch_bounds__(32) k_alpha(SolveParams P, int) {
   griddep_wait();
   griddep_launch();
   const int k = *P.iter;
-  const int do_fit = P.kind_db ? (P.fit != 1 && k < P.max_iters && k >= P.warmup) : (fit_at(P, k) ? 1 : 0);
+  const int do_fit = AK == 3 ? (P.fit != 1 && k < P.max_iters && k >= P.warmup) : (fit_at(P, k) ? 1 : 0);
   const int b = blockIdx.x;
   const MatDesc& D = P.mats[b];
   MatState& S = P.st[b];
   if (S.done) return;   // stopped in this iteration's residual stage (or earlier)
-  if (threadIdx.x >= 32) return;   // warp 0 fits alpha
   double a;
   if (!do_fit) {
     a = (k < P.warmup) ? P.ahi : P.ataylor;
+  } else if constexpr (AK == 3) {
+    // <E1,E1>, <E1,E2>, <E2,E2> over the tiles (fixed order) -> the exact quartic
+    // m(a) = a^4 <E1,E1> + 2 a^2 (1-a)^2 <E1,E2> + (1-a)^4 <E2,E2>  (R27)
+    double s3[3] = {0.0, 0.0, 0.0};
+    const int nt = D.tiles_m * D.tiles_n;
+    for (int t = threadIdx.x; t < nt; t += 32)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) s3[j] += D.dbpart[3 * t + j];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s3[j] += __shfl_xor_sync(0xffffffffu, s3[j], o);
+      s3[j] = __shfl_sync(0xffffffffu, s3[j], 0);   // lane 0's sums everywhere (no divergence)
+    }
+    const double A1 = s3[0], B1 = s3[1], C1 = s3[2];
+    const double c[5] = {C1, -4.0 * C1, 2.0 * B1 + 6.0 * C1, -4.0 * B1 - 4.0 * C1, A1 + 2.0 * B1 + C1};
+    a = argmin_quartic_free(c, P.ataylor);
   } else {
     // <Va, Vb> from the chain's per-32-row-group partials (R17): lane l
     // sums groups l, l+32, ... in order, then a fixed xor tree — reproducible bit for bit
-    if (P.kind_db) {
-      // <E1,E1>, <E1,E2>, <E2,E2> over the tiles (fixed order) -> the exact quartic
-      // m(a) = a^4 <E1,E1> + 2 a^2 (1-a)^2 <E1,E2> + (1-a)^4 <E2,E2>  (R27)
-      double s3[3] = {0.0, 0.0, 0.0};
-      const int nt = D.tiles_m * D.tiles_n;
-      for (int t = threadIdx.x; t < nt; t += 32)
-#pragma unroll
-        for (int j = 0; j < 3; ++j) s3[j] += D.dbpart[3 * t + j];
-#pragma unroll
-      for (int j = 0; j < 3; ++j) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s3[j] += __shfl_xor_sync(0xffffffffu, s3[j], o);
-        s3[j] = __shfl_sync(0xffffffffu, s3[j], 0);   // lane 0's sums everywhere (no divergence)
-      }
-      const double A1 = s3[0], B1 = s3[1], C1 = s3[2];
-      const double c[5] = {C1, -4.0 * C1, 2.0 * B1 + 6.0 * C1, -4.0 * B1 - 4.0 * C1, A1 + 2.0 * B1 + C1};
-      a = argmin_quartic_free(c, P.ataylor);
-      if (threadIdx.x == 0) {
-        S.alpha = a;
-        P.alpha_hist[(size_t)b * P.max_iters + k] = a;
-      }
-      return;
-    }
+    constexpr int NGMAX = AK == 0 ? 6 : AK == 1 ? 3 : kChainG;
     const int q = P.inv_q;
-    const int ng = q ? (q + 1) * (q + 2) / 2 : P.kind_cheb ? 3 : 6;
-    double g[kChainG];
+    const int ng = AK == 2 ? (q + 1) * (q + 2) / 2 : NGMAX;
+    double g[NGMAX];
 #pragma unroll
-    for (int j = 0; j < kChainG; ++j) g[j] = 0.0;
+    for (int j = 0; j < NGMAX; ++j) g[j] = 0.0;
     const double* __restrict__ cpart = D.chain_part;
     const int ctiles = D.chain_tiles;
 #pragma unroll 4
     for (int t = threadIdx.x; t < ctiles; t += 32) {   // four groups' loads in flight per lane
       const double* cp = cpart + kChainG * t;
 #pragma unroll
-      for (int j = 0; j < kChainG; ++j)
+      for (int j = 0; j < NGMAX; ++j)
         if (j < ng) g[j] += cp[j];
     }
 #pragma unroll
-    for (int j = 0; j < kChainG; ++j) {
+    for (int j = 0; j < NGMAX; ++j) {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) g[j] += __shfl_xor_sync(0xffffffffu, g[j], o);
     }
@@ -1163,12 +1256,12 @@ __global__ void __launch_bounds__(256) k_alpha(SolveParams P, int pre_wait) {
     // lanes whose last bits differed took different branches of the argmin (a divergent
     // warp ran it ~8x slower); lane 0's values are the ones whose alpha is stored
 #pragma unroll
-    for (int j = 0; j < kChainG; ++j) g[j] = __shfl_sync(0xffffffffu, g[j], 0);
-    if (P.kind_cheb) {
+    for (int j = 0; j < NGMAX; ++j) g[j] = __shfl_sync(0xffffffffu, g[j], 0);
+    if constexpr (AK == 1) {
       // Chebyshev: m(a) = ||U - a V||^2 (R26), closed form on [1/2, 2]
       double c[5] = {g[0], -2.0 * g[1], g[2], 0.0, 0.0};
       a = (k < P.warmup) ? P.ahi : argmin_quartic(c, P.alo, P.ahi, P.ataylor);
-    } else if (q) {
+    } else if constexpr (AK == 2) {
       // inverse Newton: m(a) = ||sum_i a^i V_i||^2 -> c_{i+j} += (2 - [i == j]) <V_i, V_j>
       double c[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
       int idx = 0;
@@ -1199,41 +1292,65 @@ __global__ void __launch_bounds__(256) k_finalize(SolveParams P) {
   const int t = blockIdx.x;
   const int b = __ldg(P.tile_mat + t);
   const MatDesc& D = P.mats[b];
+  const int Dm = D.m, Dn = D.n;
+  const long long Dldx = D.ldx, Dldq = D.ldq;
+  void* const DQ = D.Q;
+  void* const DQ2 = D.Q2;
   const MatState& S = P.st[b];
   const int par = S.iters & 1;
+  const bool zero = S.status == 4;   // ZERO_INPUT: output 0 (X may be an unwritten buffer)
+  // folded plans: X[0] is the caller's output itself (nothing to copy after an even number of
+  // updates), and X_0 = A/||A||_F was never written (a solve that stops at k = 0 writes it here)
+  const bool from_a = D.fold && S.iters == 0 && !zero;
+  if (D.fold && par == 0 && !zero && !from_a) return;
+  const void* const Xp = D.X[par];
+  const void* const Xpl = D.X_lo[par];
+  const void* const Yp = D.Y[par];
+  const void* const Ypl = D.Y_lo[par];
   const int TW = 32 * V::VE;
-  const int tcn = (D.n + TW - 1) / TW;
+  const int tcn = (Dn + TW - 1) / TW;
   const int lt = t - P.out_tile_off[b];
   const int r0 = (lt / tcn) * 32, c0 = (lt % tcn) * TW;
   const float fs = P.kind_sqrt ? (float)sqrt(S.c) : 1.f;
   const float fi = (P.kind_sqrt && S.c > 0.0) ? (float)(1.0 / sqrt(S.c)) : 0.f;
-  const bool q_vec = ((D.ldq * V::ESZ) % 16 == 0);
+  const bool q_vec = ((Dldq * V::ESZ) % 16 == 0);
+  const bool two = (P.kind_sqrt || P.kind_db) && DQ2;
+  const float sq = P.kind_db ? 1.f : P.kind_cheb ? (S.c > 0.0 ? (float)(1.0 / S.c) : 0.f)
+                               : (P.kind_sqrt && S.c > 0.0) ? fs : (P.kind_sqrt ? 0.f : 1.f);
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int slot = threadIdx.x + 256 * j;
     const int r = r0 + slot / 32, col = c0 + (slot % 32) * V::VE;
-    if (r >= D.m || col >= D.n) continue;
-    const int nv = min(V::VE, D.n - col);
-    const long long xi = (long long)r * D.ldx + col, qi = (long long)r * D.ldq + col;
-    if (D.Q) {
+    if (r >= Dm || col >= Dn) continue;
+    const int nv = min(V::VE, Dn - col);
+    const long long xi = (long long)r * (par ? Dldx : D.ldx0) + col, qi = (long long)r * Dldq + col;
+    const long long yi = (long long)r * Dldx + col;
+    if (DQ) {
       V x;
-      x.load(D.X[par], D.X_lo[par], xi, nv, nv == V::VE);
+      if (zero) {
+#pragma unroll
+        for (int e = 0; e < V::VE; ++e) x.v[e] = 0.f;
+      } else if (from_a) {
+        x.load(D.A, nullptr, (long long)r * D.lda + col, nv, false);
+#pragma unroll
+        for (int e = 0; e < V::VE; ++e) x.v[e] *= (float)S.inv_c;
+      } else {
+        x.load(Xp, Xpl, xi, nv, nv == V::VE);
+      }
       VO o;
 #pragma unroll
       for (int e = 0; e < V::VE; ++e) o.v[e] = x.v[e];
-      const bool vq = q_vec && nv == V::VE && ((reinterpret_cast<uintptr_t>(D.Q) & 15) == 0);
-      const float sq = P.kind_db ? 1.f : P.kind_cheb ? (S.c > 0.0 ? (float)(1.0 / S.c) : 0.f)
-                                   : (P.kind_sqrt && S.c > 0.0) ? fs : (P.kind_sqrt ? 0.f : 1.f);
-      o.store(D.Q, nullptr, qi, nv, vq, sq, false);
+      const bool vq = q_vec && nv == V::VE && ((reinterpret_cast<uintptr_t>(DQ) & 15) == 0);
+      o.store(DQ, nullptr, qi, nv, vq, sq, false);
     }
-    if ((P.kind_sqrt || P.kind_db) && D.Q2) {
+    if (two) {
       V y;
-      y.load(D.Y[par], D.Y_lo[par], xi, nv, nv == V::VE);
+      y.load(Yp, Ypl, yi, nv, nv == V::VE);
       VO o;
 #pragma unroll
       for (int e = 0; e < V::VE; ++e) o.v[e] = y.v[e];
-      const bool vq = q_vec && nv == V::VE && ((reinterpret_cast<uintptr_t>(D.Q2) & 15) == 0);
-      o.store(D.Q2, nullptr, qi, nv, vq, P.kind_db ? 1.f : fi, false);
+      const bool vq = q_vec && nv == V::VE && ((reinterpret_cast<uintptr_t>(DQ2) & 15) == 0);
+      o.store(DQ2, nullptr, qi, nv, vq, P.kind_db ? 1.f : fi, false);
     }
   }
 }

@@ -136,6 +136,9 @@ struct Plan {
   std::unique_ptr<uint8_t, PinnedDeleter> blob;
   SolveParams params{};
   LaunchDesc gram[2], square, square2, apply[2], chaint[5];
+  LaunchDesc gram0, apply0;   // folded normalisation: iteration 0 reads A (scaled by 1/c) instead of X_0
+  bool fold = false;          // some matrix folds (iteration-0 tables present)
+  bool unfolded = true;       // some matrix needs k_normalize
   // row-block split: packed partial-Gram launches per panel group, the
   // APPLY2 launch (Y = X R, X + Y/2) of d = 2, the packed fp32 Gram, its layout
   std::vector<LaunchDesc> rbgram[2];
@@ -292,6 +295,25 @@ prism_status build_plan(const Request& r, Plan& P) {
   };
 
   P.max_s = P.max_rows = P.max_cols = P.max_m = P.max_n = 0;
+  // Folded normalisation (BF16 / TF32 polar): iteration 0's Gram and apply read A itself with
+  // 1/c^2 and 1/c in their epilogues, and X[0] is the caller's output Q, so no pass writes
+  // X_0 = A/||A||_F and a solve ending on an even iteration needs no final copy.  Needs
+  // TMA-legal A and Q (16-B aligned base and leading dimension); 3xTF32 needs split operands.
+  // Per matrix (a matrix's bits never depend on what it is batched with); the plan carries
+  // iteration-0 tables whenever any matrix folds (the others read their X_0 there).
+  const bool fold_kind = !r.sqrt_kind && !r.sign_kind && !iq && !cheb && !db && !r.rowblock && prec != PRISM_FP32 &&
+                         d == 2 && r.Q;
+  auto fold_ok = [&](int i) {
+    return fold_kind && ((uintptr_t)r.A[i] % 16 == 0) && ((r.lda[i] * esz) % 16 == 0) && r.Q[i] &&
+           ((uintptr_t)r.Q[i] % 16 == 0) && ((r.ldq[i] * esz) % 16 == 0);
+  };
+  bool fold = false, unfolded = false;
+  for (int i = 0; i < B; ++i) {
+    fold = fold || fold_ok(i);
+    unfolded = unfolded || !fold_ok(i);
+  }
+  P.fold = fold;
+  P.unfolded = unfolded;
   for (int i = 0; i < B; ++i) {
     MatDesc& D = mats[i];
     std::memset(&D, 0, sizeof(D));
@@ -314,14 +336,21 @@ prism_status build_plan(const Request& r, Plan& P) {
     D.ldx = ldx;
     D.ldr = ldr;
     const size_t xbytes = (size_t)m * ldx * esz, rbytes = (size_t)s * ldr * esz;
+    D.ldx0 = ldx;
     for (int t = 0; t < 2; ++t) {
-      D.X[t] = bump.take(xbytes);
+      D.X[t] = bump.take(xbytes);   // (taken even when X[0] is Q: the size must not depend on pointers)
       D.X_lo[t] = split ? bump.take(xbytes) : nullptr;
       if (r.sqrt_kind || iq || db || (cheb && t == 0) || (r.rowblock && d == 2)) {   // row-block: Y, X + Y/2
         D.Y[t] = bump.take(xbytes);
         D.Y_lo[t] = split ? bump.take(xbytes) : nullptr;
       }
     }
+    D.fold = fold_ok(i) ? 1 : 0;
+    if (D.fold) {
+      D.X[0] = r.Q[i];
+      D.ldx0 = r.ldq[i];
+    }
+    const long long ldxs[2] = {D.ldx0, ldx};
     D.R = bump.take(rbytes);
     D.R_lo = split ? bump.take(rbytes) : nullptr;
     void* Pm = (iq ? iq >= 2 : (d == 2 && !db && !r.rowblock)) ? bump.take(rbytes) : nullptr;   // Chebyshev: d = 2 (P^T)
@@ -552,35 +581,49 @@ prism_status build_plan(const Request& r, Plan& P) {
       // operands MN-major, X' = X + X P (A = X K-major, B = P K-major by symmetry).
       // Wide (m < n): G = X X^T (both K-major), X' = X + P X (B = X MN-major).
       const bool tall = m >= n;
-      for (int t = 0; t < 2; ++t) {
+      // t = 0, 1: X[t] -> X[1-t]; t = 2 (folded plans): iteration 0, A (lda) -> X[1] with 1/c
+      for (int t = 0; t < (fold ? 3 : 2); ++t) {
+        const bool from_a = t == 2 && D.fold;   // iteration 0 of a folded matrix: A, scaled by 1/c
+        const void* Xi = from_a ? r.A[i] : D.X[t & 1 ? 1 : 0];
+        const void* Xil = from_a ? nullptr : D.X_lo[t & 1 ? 1 : 0];
+        const long long ldi = from_a ? r.lda[i] : ldxs[t & 1 ? 1 : 0];
+        const int to = t < 2 ? 1 - t : 1;
         HostProblem g = mk(s, s, L, EPI_RESID, 1, D.R, D.R_lo, ldr, nullptr, nullptr, 0);
         g.p.norm_part = D.norm_part;
         g.p.gdiag = D.gdiag;
         if (tall) {
           g.p.a_mn = g.p.b_mn = 1;
-          g.mapA = g.mapB = add_map(D.X[t], m, n, ldx, OP_MN);
-          if (split) g.mapA_lo = g.mapB_lo = add_map(D.X_lo[t], m, n, ldx, OP_MN);
+          g.mapA = g.mapB = add_map(Xi, m, n, ldi, OP_MN);
+          if (split) g.mapA_lo = g.mapB_lo = add_map(Xil, m, n, ldi, OP_MN);
         } else {
-          g.mapA = add_map(D.X[t], m, n, ldx, OP_A);
-          g.mapB = add_map(D.X[t], m, n, ldx, OP_BK);
-          if (split) { g.mapA_lo = add_map(D.X_lo[t], m, n, ldx, OP_A); g.mapB_lo = add_map(D.X_lo[t], m, n, ldx, OP_BK); }
+          g.mapA = add_map(Xi, m, n, ldi, OP_A);
+          g.mapB = add_map(Xi, m, n, ldi, OP_BK);
+          if (split) { g.mapA_lo = add_map(Xil, m, n, ldi, OP_A); g.mapB_lo = add_map(Xil, m, n, ldi, OP_BK); }
         }
-        P.gram[t].probs.push_back(g);
+        if (from_a) {   // R_0 = I - A^T A / c^2: the scale through the alpha operand of the epilogue
+          g.p.alpha = &d_st[i].inv_c2;
+          g.p.eA = 1;
+        }
+        (t < 2 ? P.gram[t] : P.gram0).probs.push_back(g);
         const void* Pa = d == 2 ? Pm : D.R;
         const void* Pa_lo = d == 2 ? Pm_lo : D.R_lo;
-        HostProblem a = mk(m, n, s, EPI_APPLY, 0, D.X[1 - t], D.X_lo[1 - t], ldx, D.X[t], D.X_lo[t], ldx);
+        HostProblem a = mk(m, n, s, EPI_APPLY, 0, D.X[to], D.X_lo[to], ldxs[to], Xi, Xil, ldi);
         a.p.scale_by_alpha = a.p.eA = d == 1;
         if (tall) {
-          a.mapA = add_map(D.X[t], m, n, ldx, OP_A);
+          a.mapA = add_map(Xi, m, n, ldi, OP_A);
           a.mapB = add_map(Pa, s, s, ldr, OP_BK);
-          if (split) { a.mapA_lo = add_map(D.X_lo[t], m, n, ldx, OP_A); a.mapB_lo = add_map(Pa_lo, s, s, ldr, OP_BK); }
+          if (split) { a.mapA_lo = add_map(Xil, m, n, ldi, OP_A); a.mapB_lo = add_map(Pa_lo, s, s, ldr, OP_BK); }
         } else {
           a.p.b_mn = 1;
           a.mapA = add_map(Pa, s, s, ldr, OP_A);
-          a.mapB = add_map(D.X[t], m, n, ldx, OP_MN);
-          if (split) { a.mapA_lo = add_map(Pa_lo, s, s, ldr, OP_A); a.mapB_lo = add_map(D.X_lo[t], m, n, ldx, OP_MN); }
+          a.mapB = add_map(Xi, m, n, ldi, OP_MN);
+          if (split) { a.mapA_lo = add_map(Pa_lo, s, s, ldr, OP_A); a.mapB_lo = add_map(Xil, m, n, ldi, OP_MN); }
         }
-        P.apply[t].probs.push_back(a);
+        if (from_a) {   // X_1 = A/c + (A/c) P: both epilogue coefficients scaled by 1/c (d = 2: P fixed)
+          a.p.alpha = &d_st[i].inv_c;
+          a.p.eA = a.p.eC = 1;
+        }
+        (t < 2 ? P.apply[t] : P.apply0).probs.push_back(a);
       }
       if (d == 2) {
         HostProblem q = mk(s, s, s, EPI_POLY, 1, Pm, Pm_lo, ldr, D.R, D.R_lo, ldr);
@@ -691,6 +734,10 @@ prism_status build_plan(const Request& r, Plan& P) {
     sort_tiles_by_cost(L);
   };
   const bool polar_k = !r.sqrt_kind;
+  if (P.fold) {
+    finish(P.gram0, false);
+    finish(P.apply0, true);
+  }
   for (int t = 0; t < 2; ++t) {
     finish(P.gram[t], !polar_k);
     finish(P.apply[t], true);
@@ -764,7 +811,7 @@ prism_status build_plan(const Request& r, Plan& P) {
   off += sizeof(int) * (size_t)toff[B];
   std::vector<LaunchDesc*> all = {&P.gram[0],   &P.gram[1],   &P.apply[0],  &P.apply[1],  &P.square,
                                   &P.chaint[0], &P.chaint[1], &P.chaint[2], &P.chaint[3], &P.chaint[4],
-                                  &P.square2, &P.rb1[0], &P.rb1[1]};
+                                  &P.square2, &P.rb1[0], &P.rb1[1], &P.gram0, &P.apply0};
   for (int t = 0; t < 2; ++t)
     for (LaunchDesc& L : P.rbgram[t]) all.push_back(&L);
   for (LaunchDesc& L : P.gjT) all.push_back(&L);
@@ -868,13 +915,15 @@ int chain_pass(const Plan& P, int j) {
   return P.chaint[j].probs.empty() ? CH2_P1 : P.chaint[j].probs[0].p.pass;
 }
 
-GemmLaunch make_launch(const Plan& P, const LaunchDesc& L, const LaunchDesc* odd, char* ws, int lo, int hi) {
+GemmLaunch make_launch(const Plan& P, const LaunchDesc& L, const LaunchDesc* odd, char* ws, int lo, int hi,
+                       const LaunchDesc* k0 = nullptr) {
   GemmLaunch g{};
   g.ksplit = (!L.probs.empty() && L.probs[0].p.mode == EPI_CHAIN) ? P.chain_ksplit : 1;
   (void)ws;
   char* meta = P.meta_dev;
   g.probs = reinterpret_cast<const GemmProblem*>(meta + L.probs_off);
   g.probs_odd = odd ? reinterpret_cast<const GemmProblem*>(meta + odd->probs_off) : nullptr;
+  g.probs_k0 = k0 ? reinterpret_cast<const GemmProblem*>(meta + k0->probs_off) : nullptr;
   g.tiles = reinterpret_cast<const uint32_t*>(meta + L.tiles_off);
   g.done = &P.params.st[0].done;
   g.done_stride = sizeof(MatState) / sizeof(int);
@@ -1157,17 +1206,19 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
 
   h->launches = 0;
   {
-    KindTimer t(h, st, 5, 3);
+    KindTimer t(h, st, 5, P->unfolded ? 4 : 3);
     PRISM_CK(launch_k(k_fro_partials, dim3(S.n_fro_blocks), dim3(256), 0, st, 1, S));
     PRISM_CK(launch_k(k_fro_final, dim3(B), dim3(256), 0, st, 1, S));
-    if (prec == PRISM_BF16) PRISM_CK(launch_k(k_normalize<0>, dim3(S.n_tiles), dim3(256), 0, st, 1, S));
+    PRISM_CK(launch_k(k_init_state, dim3(B), dim3(256), 0, st, 1, S));
+    if (!P->unfolded) {
+    } else if (prec == PRISM_BF16) PRISM_CK(launch_k(k_normalize<0>, dim3(S.n_tiles), dim3(256), 0, st, 1, S));
     else if (prec == PRISM_FP32) PRISM_CK(launch_k(k_normalize<1>, dim3(S.n_tiles), dim3(256), 0, st, 1, S));
     else PRISM_CK(launch_k(k_normalize<2>, dim3(S.n_tiles), dim3(256), 0, st, 1, S));
   }
   PRISM_CK(cudaGetLastError());
   const int M = r.o.max_iters;
-  const GemmLaunch g_gram = make_launch(*P, P->gram[0], &P->gram[1], r.ws, 0, M + 1);
-  const GemmLaunch g_apply = make_launch(*P, P->apply[0], &P->apply[1], r.ws, 0, M);
+  const GemmLaunch g_gram = make_launch(*P, P->gram[0], &P->gram[1], r.ws, 0, M + 1, P->fold ? &P->gram0 : nullptr);
+  const GemmLaunch g_apply = make_launch(*P, P->apply[0], &P->apply[1], r.ws, 0, M, P->fold ? &P->apply0 : nullptr);
   GemmLaunch g_sq = make_launch(*P, P->square, nullptr, r.ws, 0, M);
   // the square GEMM reads R (written by the residual step, several launches back): its
   // mainloop can run while k_alpha finishes, only its epilogue waiting for alpha.
@@ -1221,7 +1272,7 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
       }
       {
         KindTimer t(h, s2, 4, timed ? 1 : 0);
-        PRISM_CK(launch_k(k_alpha, dim3(B), dim3(256), 0, s2, 1, S, 1));   // norm partials: k_db_begin
+        PRISM_CK(launch_k(k_alpha<3>, dim3(B), dim3(32), 0, s2, 1, S, 1));
       }
       {
         KindTimer t(h, s2, 2, timed ? 2 : 0);
@@ -1256,7 +1307,9 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
       // norm partials from the residual step; a sketch chain in between makes them final
       // before k_alpha's wait
       KindTimer t(h, s2, 4, timed ? 1 : 0);
-      PRISM_CK(launch_k(k_alpha, dim3(B), dim3(256), 0, s2, 1, S, (sketched && P->n_chain > 0) ? 1 : 0));
+      if (P->inv_q) PRISM_CK(launch_k(k_alpha<2>, dim3(B), dim3(32), 0, s2, 1, S, 0));
+      else if (r.cheb_kind) PRISM_CK(launch_k(k_alpha<1>, dim3(B), dim3(32), 0, s2, 1, S, 0));
+      else PRISM_CK(launch_k(k_alpha<0>, dim3(B), dim3(32), 0, s2, 1, S, 0));
     }
     if (P->has_square) {
       KindTimer t(h, s2, 1, timed ? (P->has_square2 ? 2 : 1) : 0);
@@ -1326,7 +1379,7 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
   }
   if (rep) PRISM_CK(launch_k(k_report, dim3(std::max(1, std::min(64, (B * (M + 1) + 255) / 256))), dim3(256), 0, st, 1, S));
   h->last_iter = P->d_iter;
-  h->last_fixed = 4 + (rep ? 1 : 0);
+  h->last_fixed = 4 + (P->unfolded ? 1 : 0) + (rep ? 1 : 0);
   h->last_per_iter = P->per_iter_launches;
   PRISM_CK(cudaGetLastError());
   return PRISM_OK;
@@ -1818,6 +1871,7 @@ prism_status prism_polar_rowblock_tr(prism_handle h, const prism_transport* tr, 
     S.fro2_out = nullptr;
     S.fro2_in = P->rb_fro2;
     PRISM_CK(launch_k(k_set_c, dim3(1), dim3(32), 0, st, 1, S));
+    PRISM_CK(launch_k(k_init_state, dim3(1), dim3(256), 0, st, 1, S));
     if (prec == PRISM_BF16) PRISM_CK(launch_k(k_normalize<0>, dim3(S.n_tiles), dim3(256), 0, st, 1, S));
     else if (prec == PRISM_FP32) PRISM_CK(launch_k(k_normalize<1>, dim3(S.n_tiles), dim3(256), 0, st, 1, S));
     else PRISM_CK(launch_k(k_normalize<2>, dim3(S.n_tiles), dim3(256), 0, st, 1, S));
@@ -1860,7 +1914,7 @@ prism_status prism_polar_rowblock_tr(prism_handle h, const prism_transport* tr, 
         for (int j = 0; j < P->n_chain; ++j)
           PRISM_CK(launch_chain(prec, chain_pass(*P, j), make_launch(*P, P->chaint[j], nullptr, r.ws, o->warmup_iters, M), st));
       }
-      PRISM_CK(launch_k(k_alpha, dim3(1), dim3(256), 0, st, 1, S, 0));
+      PRISM_CK(launch_k(k_alpha<0>, dim3(1), dim3(32), 0, st, 1, S, 0));
       PRISM_CK(cudaMemcpyAsync(h->h_flag, &P->params.st[0].done, sizeof(int), cudaMemcpyDeviceToHost, st));
       PRISM_CK(cudaEventRecord(ev_stop, st));
       // 3. this rank's rows: X_r g_d(R; alpha) without R^2 (skipped on the device once stopped)
@@ -1994,7 +2048,7 @@ prism_status prism_debug_gemm(prism_handle h, int precision, int b_mn, int mode,
   gp->tiles_n = (N + BN - 1) / BN;
   gp->c1 = mode == EPI_POLY ? c1 : 1.f;
   gp->kA = 1.f;
-  gp->eA = (mode == EPI_POLY || scale_by_alpha) ? 1 : 0;
+  gp->eA = (mode == EPI_POLY || (mode == EPI_APPLY && scale_by_alpha)) ? 1 : 0;
   gp->eC = 0;
   gp->lA = gp->lC = 0.f;
   gp->a_mn = 0; gp->b_mn = b_mn ? 1 : 0;

@@ -20,7 +20,8 @@ for d in data:
     name = d["Kernel Name"]
     m = re.search(r"GemmCfg<\(int\)(\d+), \(bool\)(\d), \(bool\)(\d), \(int\)(\d+)>", name) or \
         re.search(r"GemmCfg<(\d+), (\w+), (\w+), (\d+)>", name)
-    k = ("gemm kind=%s split=%s bmn=%s bn=%s" % m.groups()) if m else name.split("(")[0][:60]
+    fn = re.search(r"(prism_\w+_kernel)", name)
+    k = ("%s kind=%s split=%s" % (fn.group(1) if fn else "gemm", m.group(1), m.group(2))) if m else name.split("(")[0][:60]
     v = float(d["Metric Value"].replace(",", ""))
     scale = 1e-3 if d.get("Metric Unit", "ns") == "ns" else (1.0 if d.get("Metric Unit") == "us" else 1e3)
     agg[k][0] += 1

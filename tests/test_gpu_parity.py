@@ -291,3 +291,51 @@ def test_sqrt_and_bf16_sketch_16_32(p):
     Qo, ro = prism.polar(Gq, d=2, p=p, tol=3e-2, max_iters=20, seed=42)
     assert abs(int(rq["iters"][0]) - ro.iters) <= 1
     assert _rel(Q[0].double().cpu().numpy(), Qo) <= 2e-2
+
+
+def test_folded_normalisation_edge_cases():
+    """BF16 / TF32 polar fold the normalisation X_0 = A/||A||_F into iteration 0's Gram and
+    apply when A and Q are TMA-legal, with X[0] = Q.  Checked here: a batch
+    mixing folded and unfolded matrices (misaligned leading dimension) against the oracle and
+    against single solves bit for bit; in place (Q = A); a solve that stops at k = 0 (one
+    column: X_0 is already orthonormal); a zero matrix into a non-zeroed output."""
+    # mixed: 300 columns bf16 with lda 300 (600 B: not a 16-B multiple -> unfolded) + aligned
+    base = torch.tensor(W.gaussian(256, 300, seed=91)).to(torch.bfloat16).cuda()
+    aligned = [torch.tensor(W.gaussian(m, n, seed=92 + i)).to(torch.bfloat16).cuda()
+               for i, (m, n) in enumerate([(512, 256), (256, 640)])]
+    mats = [base] + aligned
+    Q, rep = P.polar(mats, degree=5, tol=3e-2, max_iters=20, precision="bf16")
+    torch.cuda.synchronize()
+    for i, t in enumerate(mats):
+        Qs, rs = P.polar([t], degree=5, tol=3e-2, max_iters=20, precision="bf16", matrix_ids=[i])
+        torch.cuda.synchronize()
+        assert torch.equal(Qs[0], Q[i]) and int(rs["iters"][0]) == int(rep["iters"][i])
+        Qo, ro = prism.polar(t.double().cpu().numpy(), d=2, p=8, tol=3e-2, max_iters=20, seed=42, b=i)
+        assert abs(int(rep["iters"][i]) - ro.iters) <= 1 and _rel(Q[i].double().cpu().numpy(), Qo) <= 2e-2
+    # in place: Q aliases A
+    A = torch.tensor(W.gaussian(768, 384, seed=95)).to(torch.bfloat16).cuda()
+    A0 = A.clone()
+    Qn, rn = P.polar([A0], degree=5, tol=3e-2, max_iters=20, precision="bf16")
+    Qi, ri = P.polar([A], out=[A], degree=5, tol=3e-2, max_iters=20, precision="bf16")
+    torch.cuda.synchronize()
+    assert Qi[0] is A and torch.equal(A, Qn[0])
+    # stop at k = 0: one column (lda 8 elements = 16 B through a strided view) and a zero matrix
+    buf = torch.zeros(40, 8, dtype=torch.bfloat16, device="cuda")
+    buf[:, 0] = torch.tensor(W.gaussian(40, 1, seed=96)[:, 0]).to(torch.bfloat16)
+    col = buf[:, :1]
+    obuf = torch.full((40, 8), float("nan"), dtype=torch.bfloat16, device="cuda")
+    zero = torch.zeros(64, 32, dtype=torch.bfloat16, device="cuda")
+    ozero = torch.full((64, 32), float("nan"), dtype=torch.bfloat16, device="cuda")
+    Qc, rc = P.polar([col, zero], out=[obuf[:, :1], ozero], degree=5, tol=3e-2, max_iters=20, precision="bf16",
+                     sketch_size=1)
+    torch.cuda.synchronize()
+    assert int(rc["iters"][0]) == 0 and int(rc["status"][0]) == prism.CONVERGED
+    v = col.double().cpu().numpy()
+    assert _rel(Qc[0].double().cpu().numpy(), v / np.linalg.norm(v)) <= 1e-2
+    assert int(rc["status"][1]) == prism.ZERO_INPUT and torch.all(Qc[1] == 0)
+    # TF32 folds too
+    T = torch.tensor(W.gaussian(300, 200, seed=97)).float().cuda()
+    Qt, rt = P.polar([T], degree=5, tol=1e-2, max_iters=30, precision="tf32")
+    torch.cuda.synchronize()
+    Qo, ro = prism.polar(T.double().cpu().numpy(), d=2, p=8, tol=1e-2, max_iters=30, seed=42)
+    assert abs(int(rt["iters"][0]) - ro.iters) <= 1 and _rel(Qt[0].double().cpu().numpy(), Qo) <= 5e-3
