@@ -49,7 +49,7 @@ typedef struct prism_handle_s* prism_handle;
 typedef enum {
   PRISM_OK = 0,
   PRISM_ERR_INVALID_ARG = 1, /* null pointer, bad size/option, workspace too small */
-  PRISM_ERR_UNSUPPORTED = 2, /* valid but not supported (e.g. sketch_size > 8, fit exact on device) */
+  PRISM_ERR_UNSUPPORTED = 2, /* valid but not supported (e.g. sketch_size > 64, DB Newton outside FP32) */
   PRISM_ERR_CUDA = 3,        /* a CUDA runtime/driver call failed */
   PRISM_ERR_INTERNAL = 4,
   PRISM_ERR_NCCL = 5         /* NCCL unavailable, or a collective / communicator failed */
@@ -301,6 +301,22 @@ prism_status prism_polar_sharded_tr(prism_handle h, const prism_transport* tr, i
                                     const int64_t* n, const void* const* A, const int64_t* lda, void* const* Q,
                                     const int64_t* ldq, const prism_options* o, int nbuckets,
                                     const prism_report* rep, void* workspace, size_t ws_bytes, void* stream);
+/*
+ * Sharded coupled A^{1/2}, A^{-1/2} (Shampoo blocks shard like the Muon batch):
+ * the same protocol as prism_polar_sharded over prism_sqrt_invsqrt, both outputs broadcast
+ * from their owners (either output array may be NULL; ld_out as prism_sqrt_invsqrt).
+ */
+size_t prism_sqrt_invsqrt_sharded_workspace(prism_handle h, int nranks, int rank, int batch, const int64_t* n,
+                                            const prism_options* o, int nbuckets);
+prism_status prism_sqrt_invsqrt_sharded(prism_handle h, void* comm, int batch, const int64_t* n, const void* const* A,
+                                        const int64_t* lda, void* const* Asqrt, void* const* Ainvsqrt,
+                                        const int64_t* ld_out, const prism_options* o, int nbuckets,
+                                        const prism_report* rep, void* workspace, size_t ws_bytes, void* stream);
+prism_status prism_sqrt_invsqrt_sharded_tr(prism_handle h, const prism_transport* tr, int batch, const int64_t* n,
+                                           const void* const* A, const int64_t* lda, void* const* Asqrt,
+                                           void* const* Ainvsqrt, const int64_t* ld_out, const prism_options* o,
+                                           int nbuckets, const prism_report* rep, void* workspace, size_t ws_bytes,
+                                           void* stream);
 /* The plan (host only): owner[i] in [0, nranks) and bucket[i] in [0, nbuckets) of matrix i. */
 prism_status prism_shard_plan(int batch, const int64_t* m, const int64_t* n, int degree, int sketch_size, int nranks,
                               int nbuckets, int32_t* owner, int32_t* bucket);

@@ -125,6 +125,11 @@ _SIGS = {
                                   _vp]),
     "prism_polar_sharded_tr": (_ST, [_vp, _trp, _i32, _i64p, _i64p, _vpp, _i64p, _vpp, _i64p, _opt, _i32, _rep, _vp,
                                      _sz, _vp]),
+    "prism_sqrt_invsqrt_sharded_workspace": (_sz, [_vp, _i32, _i32, _i32, _i64p, _opt, _i32]),
+    "prism_sqrt_invsqrt_sharded": (_ST, [_vp, _vp, _i32, _i64p, _vpp, _i64p, _vpp, _vpp, _i64p, _opt, _i32, _rep, _vp,
+                                         _sz, _vp]),
+    "prism_sqrt_invsqrt_sharded_tr": (_ST, [_vp, _trp, _i32, _i64p, _vpp, _i64p, _vpp, _vpp, _i64p, _opt, _i32, _rep,
+                                            _vp, _sz, _vp]),
     "prism_polar_rowblock_workspace": (_sz, [_vp, _i64, _i64, _opt]),
     "prism_polar_rowblock": (_ST, [_vp, _vp, _i64, _i64, _vp, _i64, _i64, _i64, _vp, _i64, _opt, _rep, _vp, _sz, _vp]),
     "prism_polar_rowblock_tr": (_ST, [_vp, _trp, _i64, _i64, _vp, _i64, _i64, _i64, _vp, _i64, _opt, _rep, _vp, _sz,

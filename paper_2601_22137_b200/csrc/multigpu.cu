@@ -157,7 +157,8 @@ RepView rep_view(char* base, int cnt, int M) {
   return v;
 }
 
-prism_status shard_layout(prism_handle h, int nranks, int rank, int batch, const int64_t* m, const int64_t* n,
+// kind 0: polar (m x n), 1: coupled sqrt / inverse sqrt (n x n, m == n)
+prism_status shard_layout(prism_handle h, int kind, int nranks, int rank, int batch, const int64_t* m, const int64_t* n,
                           const prism_options* o, int nbuckets, ShardLayout& L) {
   if (!o || !m || !n || batch < 1 || nranks < 1 || rank < 0 || rank >= nranks || nbuckets < 1)
     return fail_ext(PRISM_ERR_INVALID_ARG, "bad sharded-batch arguments");
@@ -180,7 +181,8 @@ prism_status shard_layout(prism_handle h, int nranks, int rank, int batch, const
       mm.push_back(m[i]);
       nn.push_back(n[i]);
     }
-    const size_t w = prism_polar_workspace(h, (int)b.size(), mm.data(), nn.data(), o);
+    const size_t w = kind == 0 ? prism_polar_workspace(h, (int)b.size(), mm.data(), nn.data(), o)
+                               : prism_sqrt_workspace(h, (int)b.size(), nn.data(), o);
     if (!w) return fail_ext(PRISM_ERR_INVALID_ARG, std::string("bucket workspace query failed: ") + prism_last_error());
     L.solve_ws = std::max(L.solve_ws, w);
   }
@@ -268,23 +270,30 @@ size_t prism_polar_sharded_workspace(prism_handle h, int nranks, int rank, int b
                                      const int64_t* n, const prism_options* o, int nbuckets) {
   if (!h) return 0;
   ShardLayout L;
-  if (shard_layout(h, nranks, rank, batch, m, n, o, nbuckets, L)) return 0;
+  if (shard_layout(h, 0, nranks, rank, batch, m, n, o, nbuckets, L)) return 0;
   return L.total;
 }
 
-prism_status prism_polar_sharded_tr(prism_handle h, const prism_transport* tr, int batch, const int64_t* m,
-                                    const int64_t* n, const void* const* A, const int64_t* lda, void* const* Q,
-                                    const int64_t* ldq, const prism_options* o, int nbuckets,
-                                    const prism_report* rep, void* workspace, size_t ws_bytes, void* stream) {
+}  // extern "C"
+
+namespace {
+// The sharded batch of either kind (include/prism.h): plan, bucketed solves with global sketch
+// ids straight into the outputs, owners' broadcasts of each bucket (Q and, for sqrt, Q2) on the
+// aux stream, report all-reduce.
+prism_status sharded_impl(prism_handle h, const prism_transport* tr, int kind, int batch, const int64_t* m,
+                          const int64_t* n, const void* const* A, const int64_t* lda, void* const* Q, void* const* Q2,
+                          const int64_t* ldq, const prism_options* o, int nbuckets, const prism_report* rep,
+                          void* workspace, size_t ws_bytes, void* stream) {
   try {
     if (!h || !tr || !tr->broadcast || !tr->allreduce_sum) return fail_ext(PRISM_ERR_INVALID_ARG, "bad transport");
-    if (!A || !lda || !Q || !ldq) return fail_ext(PRISM_ERR_INVALID_ARG, "null matrix arrays");
+    if (!A || !lda || (!Q && !Q2) || !ldq) return fail_ext(PRISM_ERR_INVALID_ARG, "null matrix arrays");
     ShardLayout L;
-    prism_status s = shard_layout(h, tr->nranks, tr->rank, batch, m, n, o, nbuckets, L);
+    prism_status s = shard_layout(h, kind, tr->nranks, tr->rank, batch, m, n, o, nbuckets, L);
     if (s) return s;
     if (!workspace || ws_bytes < L.total) return fail_ext(PRISM_ERR_INVALID_ARG, "workspace too small");
     for (int i = 0; i < batch; ++i)
-      if (!A[i] || !Q[i] || ldq[i] < n[i]) return fail_ext(PRISM_ERR_INVALID_ARG, "bad output / input matrix");
+      if (!A[i] || (Q && !Q[i]) || (Q2 && !Q2[i]) || ldq[i] < n[i])
+        return fail_ext(PRISM_ERR_INVALID_ARG, "bad output / input matrix");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     cudaStream_t cs = prism::handle_aux_stream(h);
     if (!cs) return fail_ext(PRISM_ERR_CUDA, "aux stream");
@@ -301,14 +310,14 @@ prism_status prism_polar_sharded_tr(prism_handle h, const prism_transport* tr, i
     if (cudaEventRecord(e0, st) != cudaSuccess || cudaStreamWaitEvent(cs, e0, 0) != cudaSuccess)
       return fail_ext(PRISM_ERR_CUDA, "stream ordering");
     const int nb = (int)L.mine.size();
-    prism::NvtxRange nv_call("prism:polar_sharded");
+    prism::NvtxRange nv_call(kind == 0 ? "prism:polar_sharded" : "prism:sqrt_invsqrt_sharded");
     for (int j = 0; j < nb; ++j) {
       prism::NvtxRange nv("prism:sharded bucket (solve + owners' broadcasts)");
       const std::vector<int>& b = L.mine[j];
       if (!b.empty()) {
         std::vector<int64_t> mm, nn, la, lq, ids;
         std::vector<const void*> a;
-        std::vector<void*> q;
+        std::vector<void*> q, q2;
         for (int i : b) {
           mm.push_back(m[i]);
           nn.push_back(n[i]);
@@ -316,11 +325,17 @@ prism_status prism_polar_sharded_tr(prism_handle h, const prism_transport* tr, i
           lq.push_back(ldq[i]);
           ids.push_back(i);
           a.push_back(A[i]);
-          q.push_back(Q[i]);
+          if (Q) q.push_back(Q[i]);
+          if (Q2) q2.push_back(Q2[i]);
         }
         prism_report lr{lv.iters, lv.resid, lv.status, lv.alphas, lv.hist};
-        s = prism_polar(h, (int)b.size(), mm.data(), nn.data(), a.data(), la.data(), q.data(), lq.data(), ids.data(),
-                        o, rep ? &lr : nullptr, sws, L.solve_ws, stream);
+        if (kind == 0)
+          s = prism_polar(h, (int)b.size(), mm.data(), nn.data(), a.data(), la.data(), q.data(), lq.data(),
+                          ids.data(), o, rep ? &lr : nullptr, sws, L.solve_ws, stream);
+        else
+          s = prism_sqrt_invsqrt(h, (int)b.size(), nn.data(), a.data(), la.data(), Q ? q.data() : nullptr,
+                                 Q2 ? q2.data() : nullptr, lq.data(), ids.data(), o, rep ? &lr : nullptr, sws,
+                                 L.solve_ws, stream);
         if (s) return s;
         if (rep) {
           ScatterIdx ix;
@@ -340,7 +355,8 @@ prism_status prism_polar_sharded_tr(prism_handle h, const prism_transport* tr, i
       for (int i = 0; i < batch; ++i) {
         if (L.bucket[i] != j) continue;
         const size_t bytes = ((size_t)(m[i] - 1) * ldq[i] + n[i]) * esz;
-        if (tr->broadcast(tr->ctx, Q[i], bytes, L.owner[i], cs)) return fail_ext(PRISM_ERR_NCCL, "broadcast");
+        if (Q && tr->broadcast(tr->ctx, Q[i], bytes, L.owner[i], cs)) return fail_ext(PRISM_ERR_NCCL, "broadcast");
+        if (Q2 && tr->broadcast(tr->ctx, Q2[i], bytes, L.owner[i], cs)) return fail_ext(PRISM_ERR_NCCL, "broadcast");
       }
       if (tr->group_end && tr->group_end(tr->ctx)) return fail_ext(PRISM_ERR_NCCL, "group end");
     }
@@ -366,8 +382,47 @@ prism_status prism_polar_sharded_tr(prism_handle h, const prism_transport* tr, i
     if (tr->async_error && tr->async_error(tr->ctx)) return fail_ext(PRISM_ERR_NCCL, "communicator error");
     return PRISM_OK;
   } catch (...) {
-    return fail_ext(PRISM_ERR_INTERNAL, "exception in prism_polar_sharded");
+    return fail_ext(PRISM_ERR_INTERNAL, "exception in the sharded batch");
   }
+}
+}  // namespace
+
+extern "C" {
+
+prism_status prism_polar_sharded_tr(prism_handle h, const prism_transport* tr, int batch, const int64_t* m,
+                                    const int64_t* n, const void* const* A, const int64_t* lda, void* const* Q,
+                                    const int64_t* ldq, const prism_options* o, int nbuckets,
+                                    const prism_report* rep, void* workspace, size_t ws_bytes, void* stream) {
+  if (!Q) return fail_ext(PRISM_ERR_INVALID_ARG, "null outputs");
+  return sharded_impl(h, tr, 0, batch, m, n, A, lda, Q, nullptr, ldq, o, nbuckets, rep, workspace, ws_bytes, stream);
+}
+
+prism_status prism_sqrt_invsqrt_sharded_tr(prism_handle h, const prism_transport* tr, int batch, const int64_t* n,
+                                           const void* const* A, const int64_t* lda, void* const* Asqrt,
+                                           void* const* Ainvsqrt, const int64_t* ld_out, const prism_options* o,
+                                           int nbuckets, const prism_report* rep, void* workspace, size_t ws_bytes,
+                                           void* stream) {
+  return sharded_impl(h, tr, 1, batch, n, n, A, lda, Asqrt, Ainvsqrt, ld_out, o, nbuckets, rep, workspace, ws_bytes,
+                      stream);
+}
+
+size_t prism_sqrt_invsqrt_sharded_workspace(prism_handle h, int nranks, int rank, int batch, const int64_t* n,
+                                            const prism_options* o, int nbuckets) {
+  if (!h) return 0;
+  ShardLayout L;
+  if (shard_layout(h, 1, nranks, rank, batch, n, n, o, nbuckets, L)) return 0;
+  return L.total;
+}
+
+prism_status prism_sqrt_invsqrt_sharded(prism_handle h, void* comm, int batch, const int64_t* n, const void* const* A,
+                                        const int64_t* lda, void* const* Asqrt, void* const* Ainvsqrt,
+                                        const int64_t* ld_out, const prism_options* o, int nbuckets,
+                                        const prism_report* rep, void* workspace, size_t ws_bytes, void* stream) {
+  prism_transport tr;
+  prism_status s = prism_nccl_transport(comm, &tr);
+  if (s) return s;
+  return prism_sqrt_invsqrt_sharded_tr(h, &tr, batch, n, A, lda, Asqrt, Ainvsqrt, ld_out, o, nbuckets, rep, workspace,
+                                       ws_bytes, stream);
 }
 
 prism_status prism_polar_sharded(prism_handle h, void* comm, int batch, const int64_t* m, const int64_t* n,

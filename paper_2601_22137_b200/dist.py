@@ -11,6 +11,8 @@ One process per GPU.  Every exchange happens inside libprism through a prism_tra
                     share in buckets with global sketch ids (bit-identical to the
                     single-GPU solve), and the owners broadcast each bucket's outputs while
                     the next bucket solves; every rank returns every output.
+* ``sqrt_invsqrt_sharded`` the same for Shampoo's A^{1/2}, A^{-1/2} batch
+                    (prism_sqrt_invsqrt_sharded).
 * ``polar_rowblock`` one matrix too large for one GPU, split by rows
                     (prism_polar_rowblock): per iteration a packed upper-triangle fp32
                     Gram all-reduce pipelined by panel group, then Y_r = X_r R and
@@ -213,6 +215,46 @@ def polar_sharded(mats, comm, out=None, nbuckets: int = 2, report: bool = True, 
                                          ctypes.byref(rep) if report else None, ws.data_ptr(), ws.numel(),
                                          ctypes.c_void_p(st.cuda_stream)), "prism_polar_sharded")
     return out, rb
+
+
+def sqrt_invsqrt_sharded(mats, comm, want_sqrt=True, want_invsqrt=True, out_sqrt=None, out_invsqrt=None,
+                         nbuckets: int = 2, report: bool = True, handle=None, stream=None, degree=5, max_iters=30,
+                         sketch_size=8, tol=1e-6, seed=42, precision=None, fit="sketched", warmup_iters=0,
+                         alpha_lo=None, alpha_hi=None):
+    """A^{1/2}, A^{-1/2} of the whole SPD batch on every rank (prism_sqrt_invsqrt_sharded_tr):
+    the Shampoo-preconditioner form of polar_sharded.  Returns (sqrt, invsqrt, report)."""
+    import torch
+    mats = list(mats)
+    if any(t.shape[0] != t.shape[1] for t in mats):
+        raise B.PrismError("sqrt_invsqrt_sharded: matrices must be square")
+    tr = _transport_of(comm)
+    precision = B._precision_of(mats[0], precision)
+    B._check_dtype(mats, precision)
+    dev = mats[0].device
+    h = handle or B.default_handle()
+    o = B.make_options(degree, max_iters, sketch_size, tol, seed, precision, fit, warmup_iters, alpha_lo, alpha_hi)
+    n_ = len(mats)
+    n = B._i64([t.shape[1] for t in mats])
+    o1 = B._outputs(mats, want_sqrt, out_sqrt, "sqrt_invsqrt_sharded", False)
+    o2 = B._outputs(mats, want_invsqrt, out_invsqrt, "sqrt_invsqrt_sharded", False)
+    L = B.lib()
+    with torch.cuda.device(dev):
+        st = stream if stream is not None else torch.cuda.current_stream(dev)
+        need = L.prism_sqrt_invsqrt_sharded_workspace(h.h, tr.nranks, tr.rank, n_, n, ctypes.byref(o), nbuckets)
+        if need == 0:
+            raise B.PrismError("prism_sqrt_invsqrt_sharded_workspace rejected the arguments: " +
+                               L.prism_last_error().decode())
+        ws = h.workspace(need, dev, st)
+        rb = B._report_buffers(n_, max_iters, dev) if report else None
+        rep = B._report_struct(rb) if report else None
+        B.check(L.prism_sqrt_invsqrt_sharded_tr(h.h, ctypes.byref(tr), n_, n, B._ptrs(mats),
+                                                B._i64([t.stride(0) for t in mats]),
+                                                B._ptrs(o1) if o1 else None, B._ptrs(o2) if o2 else None,
+                                                B._ld_out(o1, o2, mats, "sqrt_invsqrt_sharded"), ctypes.byref(o),
+                                                int(nbuckets), ctypes.byref(rep) if report else None, ws.data_ptr(),
+                                                ws.numel(), ctypes.c_void_p(st.cuda_stream)),
+                "prism_sqrt_invsqrt_sharded")
+    return o1, o2, rb
 
 
 def polar_rowblock(A_rows, comm, m_global: int, row0: int, out=None, handle=None, stream=None, degree=5,

@@ -89,6 +89,64 @@ def test_sharded_three_thread_ranks_equal_batch_and_oracle():
         assert _rel(res[1][0][i].double().cpu().numpy(), Qo) <= 1e-5
 
 
+SPD_SIZES = [200, 96, 384, 256, 130, 512]
+
+
+def _spd_batch():
+    return [torch.tensor(W.spd_logspaced(n, 1e2, seed=70 + i)).float().cuda() for i, n in enumerate(SPD_SIZES)]
+
+
+def test_sqrt_sharded_nccl_one_rank_equals_batch():
+    mats = _spd_batch()
+    rs, ri, rref = P.sqrt_invsqrt(mats, degree=5, tol=1e-5, precision="fp32", matrix_ids=list(range(len(mats))))
+    comm = D.Comm()
+    try:
+        s, si, rep = D.sqrt_invsqrt_sharded(mats, comm, nbuckets=2, degree=5, tol=1e-5, precision="fp32")
+        # one output only: the other array is NULL through the C ABI
+        _, si2, _ = D.sqrt_invsqrt_sharded(mats, comm, want_sqrt=False, nbuckets=3, degree=5, tol=1e-5,
+                                           precision="fp32")
+        torch.cuda.synchronize()
+    finally:
+        comm.close()
+    for a, b, c, d, e in zip(s, rs, si, ri, si2):
+        assert torch.equal(a, b) and torch.equal(c, d) and torch.equal(e, d)
+    for k in ("iters", "status", "resid"):
+        assert torch.equal(rep[k], rref[k])
+
+
+def test_sqrt_sharded_two_thread_ranks_equal_batch_and_oracle():
+    world = 2
+    base = _spd_batch()
+    rs, ri, rref = P.sqrt_invsqrt(base, degree=5, tol=1e-5, precision="fp32", matrix_ids=list(range(len(base))))
+    torch.cuda.synchronize()
+    g = D.HostGroup(world)
+    res = [None] * world
+
+    def run(r):
+        torch.cuda.set_device(0)
+        mats = [t.clone() for t in base]
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            res[r] = D.sqrt_invsqrt_sharded(mats, D.HostTransport(g, r), nbuckets=2, handle=P.Handle(), stream=st,
+                                            degree=5, tol=1e-5, precision="fp32")
+        st.synchronize()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for r in range(world):
+        s, si, rep = res[r]
+        for a, b, c, d in zip(s, rs, si, ri):
+            assert torch.equal(a, b) and torch.equal(c, d)
+        assert torch.equal(rep["iters"], rref["iters"])
+    for i in (0, 2):
+        Xo, Yo, ro = prism.sqrt_invsqrt(base[i].double().cpu().numpy(), d=2, p=8, tol=1e-5, seed=42, b=i)
+        assert _rel(res[1][0][i].double().cpu().numpy(), Xo) <= 1e-5
+        assert _rel(res[0][1][i].double().cpu().numpy(), Yo) <= 1e-5
+
+
 @pytest.mark.parametrize("shape,prec,tol,bound", [((1000, 384), "fp32", 1e-5, 1e-5), ((1536, 768), "bf16", 3e-2, 2e-2),
                                                   ((600, 300), "tf32", 1e-2, 5e-3)])
 @pytest.mark.parametrize("deg", [3, 5])
