@@ -399,6 +399,10 @@ prism_status prism_debug_argmin(int n, const double* c_dev, double lo, double hi
  * whose epilogue mode is `mode` (0 residual, 1 poly, 2 apply; < 0 off) record per-CTA
  * globaltimer stamps (gemm.cuh).  NULL disables. */
 prism_status prism_debug_trace_gemm(unsigned long long* buf_dev, int mode);
+/* Sketch-chain timeline hook: buf_dev (16 iterations x 32 pass codes x 160 CTAs x 4 u64,
+ * zeroed by the caller) receives per CTA globaltimer ns at entry, after the PDL wait, when the
+ * first tile's accumulator is ready and when its epilogue ends; NULL turns it off. */
+prism_status prism_debug_trace_chain(unsigned long long* buf_dev);
 
 #ifdef __cplusplus
 }

@@ -147,6 +147,7 @@ _SIGS = {
     "prism_debug_sketch": (_ST, [_u64, _i64, _i32, _i32, _i32, _vp, _vp]),
     "prism_debug_argmin": (_ST, [_i32, _vp, _dbl, _dbl, _dbl, _vp, _vp]),
     "prism_debug_trace_gemm": (_ST, [_vp, _i32]),
+    "prism_debug_trace_chain": (_ST, [_vp]),
 }
 EXPORTS = sorted(_SIGS)
 

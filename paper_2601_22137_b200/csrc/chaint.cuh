@@ -66,6 +66,11 @@ __device__ __forceinline__ void chain_slices(const GemmProblem& P, uint32_t code
   s_hi = C > 1 ? s_lo + 1 : (P.ksplit > 1 ? P.ksplit : 1);
 }
 
+// Pass timeline (prism_debug_trace_chain, scripts/trace_chain.py): per iteration k < 16, pass
+// code and CTA, globaltimer at entry, after the PDL wait, when the first tile's accumulator is
+// ready and when its epilogue ends.  Null (the default): no recording.
+__device__ unsigned long long* g_chain_trace = nullptr;
+
 template <class Cfg, int PASS>
 __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __grid_constant__ GemmLaunch L) {
   extern __shared__ uint8_t smem_raw[];
@@ -118,6 +123,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
   // producer therefore stages the R half of its first stages now and adds W after the wait.
   const GemmProblem* __restrict__ probs = L.probs;
   bool run = true;
+  unsigned long long* tr = nullptr;
+  if (g_chain_trace && L.iter && *L.iter < 16)
+    tr = g_chain_trace + ((size_t)(*L.iter * 32 + PASS) * 160 + blockIdx.x) * 4;
+  if (tr && threadIdx.x == 0) tr[0] = globaltimer_ns();
   if (L.iter) {
     const int k = *L.iter;
     run = k >= L.iter_lo && k < L.iter_hi;
@@ -155,6 +164,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
   griddep_wait();
   griddep_launch();
   __syncthreads();   // s_first_active
+  if (tr && threadIdx.x == 0) tr[1] = globaltimer_ns();
   auto skip = [&](int t, int matrix) -> bool {
     if (t == (int)blockIdx.x) return !s_first_active;
     return L.done && L.done[matrix * L.done_stride];
@@ -271,6 +281,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
           if (reader) {
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
+            if (tr && t == (int)blockIdx.x && et == 0) tr[2] = globaltimer_ns();
 #pragma unroll 1
             for (int x = 0; x < 4; ++x) {
               const int col = h * 128 + x * 32;
@@ -301,6 +312,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
         if (have) {
           mbar_wait(&tfull[acc], acc_phase);
           tc_fence_after();
+          if (tr && t == (int)blockIdx.x && et == 0) tr[2] = globaltimer_ns();
         }
         // every owner consumed the previous round's slices: send this round's
         mbar_wait(recv_free, rphase ^ 1);
@@ -355,6 +367,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
       }
       epi_chain<Cfg, PASS>(pre, i, grp, dsm + et, rstride, lane, 2);
       named_bar_sync(1, 32 * Cfg::EPI_WARPS);    // buffer consumed
+      if (tr && t == (int)blockIdx.x && et == 0) tr[3] = globaltimer_ns();
       if (C > 1) {
         rphase ^= 1;
         // hand the slots back (gates only a later round's sends: off the critical path)

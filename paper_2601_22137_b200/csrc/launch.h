@@ -76,6 +76,9 @@ cudaError_t launch_gemm_bf16(int role, const GemmLaunch& L, cudaStream_t st);
 cudaError_t launch_gemm_f32x3(int role, const GemmLaunch& L, cudaStream_t st);
 cudaError_t launch_gemm_tf32(int role, const GemmLaunch& L, cudaStream_t st);
 cudaError_t set_gemm_trace_bf16(unsigned long long* buf, int mode);
+cudaError_t set_chain_trace_bf16(unsigned long long* buf);
+cudaError_t set_chain_trace_f32x3(unsigned long long* buf);
+cudaError_t set_chain_trace_tf32(unsigned long long* buf);
 cudaError_t set_gemm_trace_f32x3(unsigned long long* buf, int mode);
 cudaError_t set_gemm_trace_tf32(unsigned long long* buf, int mode);
 cudaError_t launch_chain_bf16(int pass, const GemmLaunch& L, cudaStream_t st);

@@ -2080,6 +2080,13 @@ prism_status prism_debug_trace_gemm(unsigned long long* buf_dev, int mode) {
   return PRISM_OK;
 }
 
+prism_status prism_debug_trace_chain(unsigned long long* buf_dev) {
+  if (set_chain_trace_bf16(buf_dev) != cudaSuccess || set_chain_trace_f32x3(buf_dev) != cudaSuccess ||
+      set_chain_trace_tf32(buf_dev) != cudaSuccess)
+    return fail(PRISM_ERR_CUDA, "trace hook");
+  return PRISM_OK;
+}
+
 prism_status prism_debug_sketch(uint64_t seed, int64_t b, int k, int p, int s, float* S_dev, void* stream) {
   if (!S_dev || p < 1 || s < 1) return fail(PRISM_ERR_INVALID_ARG, "bad sketch args");
   const long long pairs = ((long long)p * s + 1) / 2;
