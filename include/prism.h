@@ -399,6 +399,8 @@ prism_status prism_debug_argmin(int n, const double* c_dev, double lo, double hi
  * whose epilogue mode is `mode` (0 residual, 1 poly, 2 apply; < 0 off) record per-CTA
  * globaltimer stamps (gemm.cuh).  NULL disables. */
 prism_status prism_debug_trace_gemm(unsigned long long* buf_dev, int mode);
+/* Diagnostics: persistent-grid cap (CTAs) of the next prism_debug_gemm launches (0: all SMs). */
+prism_status prism_debug_gemm_max_ctas(int max_ctas);
 /* Sketch-chain timeline hook: buf_dev (16 iterations x 32 pass codes x 160 CTAs x 4 u64,
  * zeroed by the caller) receives per CTA globaltimer ns at entry, after the PDL wait, when the
  * first tile's accumulator is ready and when its epilogue ends; NULL turns it off. */

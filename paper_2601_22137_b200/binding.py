@@ -148,6 +148,7 @@ _SIGS = {
     "prism_debug_argmin": (_ST, [_i32, _vp, _dbl, _dbl, _dbl, _vp, _vp]),
     "prism_debug_trace_gemm": (_ST, [_vp, _i32]),
     "prism_debug_trace_chain": (_ST, [_vp]),
+    "prism_debug_gemm_max_ctas": (_ST, [_i32]),
 }
 EXPORTS = sorted(_SIGS)
 

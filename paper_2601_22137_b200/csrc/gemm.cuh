@@ -765,9 +765,10 @@ __device__ __forceinline__ void epi_block_tma(const EpiArgs& P, const CUtensorMa
 #pragma unroll
     for (int u = 0; u < 32; ++u) v[u] = ((j0 + u == i) ? 1.f : 0.f) - coefA * d[u];
     if (P.gdiag && row_ok && i >= j0 && i < j0 + 32) {
+      float g = 0.f;   // this lane's diagonal entry, by selects (no divergent branch per column)
 #pragma unroll
-      for (int u = 0; u < 32; ++u)
-        if (j0 + u == i) P.gdiag[i] = coefA * d[u];
+      for (int u = 0; u < 32; ++u) g = (j0 + u == i) ? d[u] : g;
+      P.gdiag[i] = coefA * g;
     }
   } else {
 #pragma unroll
@@ -775,16 +776,19 @@ __device__ __forceinline__ void epi_block_tma(const EpiArgs& P, const CUtensorMa
   }
   const bool diag = sym && j0 < i0 + 32;         // 32-aligned: the diagonal block (j0 == i0)
   if (mode == EPI_RESID && row_ok) {
-    // ||R||_F^2: every element once (symmetric: each strictly-upper element twice)
+    // ||R||_F^2: every element once (symmetric: each strictly-upper element twice).  Weights
+    // and the inclusion test by selects: the lane-dependent branches of the first form
+    // diverged on every element and cost ~1.5 us per 32 x 32 block (scripts/trace_gemm.py)
+    float ss = 0.f;
+    const float wfull = sym ? 2.f : 1.f;
 #pragma unroll
     for (int u = 0; u < 32; ++u) {
-      const int j = j0 + u;
-      if (j < P.N) {
-        if (!sym) sumsq = fmaf(v[u], v[u], sumsq);
-        else if (!diag || u > lane) sumsq = fmaf(2.f * v[u], v[u], sumsq);
-        else if (u == lane) sumsq = fmaf(v[u], v[u], sumsq);
-      }
+      const bool inc = j0 + u < P.N && (!sym || !diag || u >= lane);
+      const float w = (sym && diag && u == lane) ? 1.f : wfull;
+      const float t = fmaf(w * v[u], v[u], ss);
+      ss = inc ? t : ss;
     }
+    sumsq += ss;
   }
   stage_row_bf16(v, ob, lane);
   __syncwarp();
@@ -1356,13 +1360,17 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
               bulk_commit();
             }
           } else {
+            // output blocks: non-symmetric ones alternate O0 / O1; symmetric ones need a block
+            // and its mirror — without C (the Gram) they alternate the pairs (C0, C1) and
+            // (O0, O1), so a chunk never waits for the previous chunk's stores to drain
+            const bool pairs2 = sym && !needC;
             if (lane == 0) {
-              if (sym) bulk_wait_read<0>();
+              if (sym && !pairs2) bulk_wait_read<0>();
               else bulk_wait_read<1>();
             }
             __syncwarp();
-            uint8_t* ob = wb + 4096 + (sym ? 0 : b * 2048);
-            epi_block_tma<Cfg>(ea, tmO, mode, sym, i0, lane, jb + ch * 32, coefA, coefC, d, c, ob, wb + 6144, sumsq);
+            uint8_t* ob = pairs2 ? wb + b * 4096 : wb + 4096 + (sym ? 0 : b * 2048);
+            epi_block_tma<Cfg>(ea, tmO, mode, sym, i0, lane, jb + ch * 32, coefA, coefC, d, c, ob, ob + 2048, sumsq);
           }
           if (more) tmem_ld_wait_dep(rn);
         };

@@ -1991,6 +1991,12 @@ double prism_sqrt_flops_per_iter(int64_t n, int degree, int sketch_size) {
   return f;
 }
 
+static int g_debug_gemm_max_ctas = 0;
+prism_status prism_debug_gemm_max_ctas(int max_ctas) {
+  g_debug_gemm_max_ctas = max_ctas < 0 ? 0 : max_ctas;
+  return PRISM_OK;
+}
+
 prism_status prism_debug_gemm(prism_handle h, int precision, int b_mn, int mode, int sym, int M, int N, int K,
                               const void* A, const void* A_lo, int64_t lda, const void* B, const void* B_lo,
                               int64_t ldb, const void* C, const void* C_lo, int64_t ldc, void* out, void* out_lo,
@@ -2066,6 +2072,7 @@ prism_status prism_debug_gemm(prism_handle h, int precision, int b_mn, int mode,
   g.done = nullptr;
   g.done_stride = 0;
   g.ntiles = (int)L.tiles.size();
+  g.max_ctas = g_debug_gemm_max_ctas;
   PRISM_CK(launch_gemm(precision, ROLE_OTHER, g, static_cast<cudaStream_t>(stream)));
   PRISM_CK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
   return PRISM_OK;
