@@ -762,13 +762,18 @@ __device__ __forceinline__ void epi_block_tma(const EpiArgs& P, const CUtensorMa
 #pragma unroll
     for (int u = 0; u < 32; ++u) v[u] = coefC * c[u] + coefA * d[u];
   } else if (mode == EPI_RESID) {
+    if (j0 == i0) {   // warp-uniform: the 32 x 32 block holding the diagonal (square R)
 #pragma unroll
-    for (int u = 0; u < 32; ++u) v[u] = ((j0 + u == i) ? 1.f : 0.f) - coefA * d[u];
-    if (P.gdiag && row_ok && i >= j0 && i < j0 + 32) {
-      float g = 0.f;   // this lane's diagonal entry, by selects (no divergent branch per column)
+      for (int u = 0; u < 32; ++u) v[u] = (u == lane ? 1.f : 0.f) - coefA * d[u];
+      if (P.gdiag && row_ok) {
+        float g = 0.f;   // this lane's diagonal entry, by selects (no divergent branch per column)
 #pragma unroll
-      for (int u = 0; u < 32; ++u) g = (j0 + u == i) ? d[u] : g;
-      P.gdiag[i] = coefA * g;
+        for (int u = 0; u < 32; ++u) g = u == lane ? d[u] : g;
+        P.gdiag[i] = coefA * g;
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 32; ++u) v[u] = -coefA * d[u];
     }
   } else {
 #pragma unroll
@@ -776,19 +781,20 @@ __device__ __forceinline__ void epi_block_tma(const EpiArgs& P, const CUtensorMa
   }
   const bool diag = sym && j0 < i0 + 32;         // 32-aligned: the diagonal block (j0 == i0)
   if (mode == EPI_RESID && row_ok) {
-    // ||R||_F^2: every element once (symmetric: each strictly-upper element twice).  Weights
-    // and the inclusion test by selects: the lane-dependent branches of the first form
-    // diverged on every element and cost ~1.5 us per 32 x 32 block (scripts/trace_gemm.py)
+    // ||R||_F^2 from this block: an off-diagonal block of a symmetric R stands for itself
+    // and its mirror (weight 2); a diagonal block is summed whole (both of its triangles:
+    // the computed values, equal to the stored mirror up to the rounding of the products).
+    // No lane-dependent test per element: the first form's branches diverged on every
+    // element and its select form still cost ~1 us per 32 x 32 block (scripts/trace_gemm.py)
     float ss = 0.f;
-    const float wfull = sym ? 2.f : 1.f;
+    if (j0 + 32 <= P.N) {
 #pragma unroll
-    for (int u = 0; u < 32; ++u) {
-      const bool inc = j0 + u < P.N && (!sym || !diag || u >= lane);
-      const float w = (sym && diag && u == lane) ? 1.f : wfull;
-      const float t = fmaf(w * v[u], v[u], ss);
-      ss = inc ? t : ss;
+      for (int u = 0; u < 32; ++u) ss = fmaf(v[u], v[u], ss);
+    } else {
+#pragma unroll
+      for (int u = 0; u < 32; ++u) ss = j0 + u < P.N ? fmaf(v[u], v[u], ss) : ss;
     }
-    sumsq += ss;
+    sumsq += (sym && !diag) ? 2.f * ss : ss;
   }
   stage_row_bf16(v, ob, lane);
   __syncwarp();

@@ -73,20 +73,16 @@ for j, v in sorted(spans.items()):
           f"{statistics.median(x[3] for x in v):6.2f} us (max {max(x[3] for x in v):6.2f})")
 end = max(float(T[c, 192 + 4 * j + 3]) for c in lead for j in range(8) if T[c, 192 + 4 * j + 3] > 0)
 print(f"  launch span (first MMA -> last epilogue end): {(end - t0) / 1e3:.2f} us")
-# per-chunk epilogue marks of the first tile (leader CTAs; warps 4 and 11): [start, after
-# the buffer wait, after the block epilogue, after the next chunk's TMEM load]
+# per-chunk epilogue marks of the second tile (leader CTAs; warps 4 and 11), with the
+# instrumentation patch applied: [0] step start, [1] C ready, [2] output buffer free,
+# [3] values, [4] staged, [5] transposed, [6] stores issued, [7] next chunk's TMEM load done
 for wi, base in ((4, 224), (11, 288)):
     rows = []
     for c in lead:
         for x in range(8):
-            m = [float(T[c, base + 8 * x + k]) for k in range(7)]
+            m = [float(T[c, base + 8 * x + k]) for k in range(8)]
             if m[0] > 0:
-                rows.append((x, m[1] - m[0], m[2] - m[1], m[3] - m[2], m[0],
-                             m[4] - m[1] if m[4] else 0, m[5] - m[4] if m[5] else 0, m[6] - m[5] if m[6] else 0))
-    if rows:
-        for x in sorted(set(r[0] for r in rows)):
-            rr = [r for r in rows if r[0] == x]
-            print(f"  warp {wi} chunk {x}: wait {statistics.median(r[1] for r in rr):6.0f} ns, block "
-                  f"{statistics.median(r[2] for r in rr):6.0f} ns (marks {statistics.median(r[5] for r in rr):5.0f}, "
-                  f"{statistics.median(r[6] for r in rr):5.0f}, {statistics.median(r[7] for r in rr):5.0f}), next-ld "
-                  f"{statistics.median(r[3] for r in rr):6.0f} ns")
+                rows.append([x] + [(m[k] - m[k - 1]) if m[k] and m[k - 1] else 0.0 for k in range(1, 8)])
+    for x in sorted(set(r[0] for r in rows)):
+        rr = [r for r in rows if r[0] == x]
+        print(f"  warp {wi} chunk {x}: " + " ".join(f"{statistics.median(r[k] for r in rr):5.0f}" for k in range(1, 8)))
