@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
   bool run = true;
   unsigned long long* tr = nullptr;
   if (g_chain_trace && L.iter && *L.iter < 16)
-    tr = g_chain_trace + ((size_t)(*L.iter * 32 + PASS) * 160 + blockIdx.x) * 4;
+    tr = g_chain_trace + ((size_t)(*L.iter * 32 + PASS) * 160 + blockIdx.x) * 8;
   if (tr && threadIdx.x == 0) tr[0] = globaltimer_ns();
   if (L.iter) {
     const int k = *L.iter;
@@ -283,23 +283,27 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
             tc_fence_after();
             if (tr && t == (int)blockIdx.x && et == 0) tr[2] = globaltimer_ns();
 #pragma unroll 1
-            for (int x = 0; x < 4; ++x) {
-              const int col = h * 128 + x * 32;
-              uint32_t r[32];
-              tmem_ld32(tmem_base + acc * Cfg::BN + col, r);
+            for (int x0 = 0; x0 < 4; x0 += 2) {   // two 32-column loads in flight per wait
+              uint32_t r[2][32];
+              tmem_ld32(tmem_base + acc * Cfg::BN + h * 128 + x0 * 32, r[0]);
+              tmem_ld32(tmem_base + acc * Cfg::BN + h * 128 + (x0 + 1) * 32, r[1]);
               tmem_ld_wait();
-              float* dst = dsm + (size_t)lane * rstride + col;
-              if (first) {
 #pragma unroll
-                for (int u = 0; u < 32; ++u) dst[u] = __uint_as_float(r[u]);
-              } else {
+              for (int x = 0; x < 2; ++x) {
+                float* dst = dsm + (size_t)lane * rstride + h * 128 + (x0 + x) * 32;
+                if (first) {
 #pragma unroll
-                for (int u = 0; u < 32; ++u) dst[u] += __uint_as_float(r[u]);
+                  for (int u = 0; u < 32; ++u) dst[u] = __uint_as_float(r[x][u]);
+                } else {
+#pragma unroll
+                  for (int u = 0; u < 32; ++u) dst[u] += __uint_as_float(r[x][u]);
+                }
               }
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (tr && t == (int)blockIdx.x && et == 0) tr[4] = globaltimer_ns();
           }
           first = false;
           if (++acc == 2) { acc = 0; acc_phase ^= 1; }
@@ -343,11 +347,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[acc]);
         }
+        if (tr && t == (int)blockIdx.x && et == 0) tr[4] = globaltimer_ns();
       }
       if (have && ++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
       if (C > 1 && et == 0) mbar_arrive_expect_tx(recv_full, (uint32_t)(C - 1) * 32 * rows_per * 4);
       named_bar_sync(1, 32 * Cfg::EPI_WARPS);    // own slice written locally
+      if (tr && t == (int)blockIdx.x && et == 0) tr[5] = globaltimer_ns();
       if (C > 1) {
         mbar_wait(recv_full, rphase);            // the other C-1 slices landed
         if (et < rows_per) {
@@ -365,7 +371,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
           for (int c = 0; c < 32; ++c) dsm[(size_t)c * rstride + et] = v[c];
         }
       }
+      if (tr && t == (int)blockIdx.x && et == 0) tr[6] = globaltimer_ns();
       epi_chain<Cfg, PASS>(pre, i, grp, dsm + et, rstride, lane, 2);
+      if (tr && t == (int)blockIdx.x && et == 0) tr[7] = globaltimer_ns();
       named_bar_sync(1, 32 * Cfg::EPI_WARPS);    // buffer consumed
       if (tr && t == (int)blockIdx.x && et == 0) tr[3] = globaltimer_ns();
       if (C > 1) {

@@ -883,11 +883,38 @@ __device__ __forceinline__ void chain_prefetch(const GemmProblem& Pin, int i, in
   } else if constexpr (chain_is_last(PASS)) {
     const int ns = chain_last_slots(PASS);
     const long long M = P.M;
+    if (p == 8 && c0 == 0 && c1 == 8) {   // full chunk: two 16-B loads per kept row
 #pragma unroll
-    for (int sl = 0; sl < 4; ++sl)
+      for (int sl = 0; sl < 4; ++sl) {
+        if (sl < ns) {
+          const float4* q = reinterpret_cast<const float4*>(P.keep + ((long long)sl * M + i) * 8);
+          const float4 a = __ldcg(q), b = __ldcg(q + 1);
+          pre.v[sl * 8 + 0] = a.x; pre.v[sl * 8 + 1] = a.y; pre.v[sl * 8 + 2] = a.z; pre.v[sl * 8 + 3] = a.w;
+          pre.v[sl * 8 + 4] = b.x; pre.v[sl * 8 + 5] = b.y; pre.v[sl * 8 + 6] = b.z; pre.v[sl * 8 + 7] = b.w;
+        }
+      }
+    } else {
 #pragma unroll
-      for (int c = 0; c < 8; ++c)
-        pre.v[sl * 8 + c] = (sl < ns && c >= c0 && c < c1) ? __ldcg(P.keep + ((long long)sl * M + i) * p + c) : 0.f;
+      for (int sl = 0; sl < 4; ++sl)
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          pre.v[sl * 8 + c] = (sl < ns && c >= c0 && c < c1) ? __ldcg(P.keep + ((long long)sl * M + i) * p + c) : 0.f;
+    }
+  }
+}
+
+// Kept chain columns of row i: p consecutive floats ([slot][M][p]); a full chunk (p = 8,
+// 32-B aligned rows) as two 16-B stores — eight scalar stores per row made each warp
+// instruction touch 32 sectors, and the row epilogue of a pass took up to 2.8 us
+__device__ __forceinline__ void keep_row(float* dst, const float (&v)[8], int p) {
+  if (p == 8) {
+    float4* d4 = reinterpret_cast<float4*>(dst);
+    d4[0] = make_float4(v[0], v[1], v[2], v[3]);
+    d4[1] = make_float4(v[4], v[5], v[6], v[7]);
+  } else {
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      if (c < p) dst[c] = v[c];
   }
 }
 
@@ -929,41 +956,42 @@ __device__ __forceinline__ void epi_chain(const ChainPre& pre, int i, int grp, c
           store_w<Cfg>(P, c, 2 * p, i, o[c]);
           store_w<Cfg>(P, p + c, 2 * p, i, qv);
         } else {
-          keep[i * p + c] = o[c];
           store_w<Cfg>(P, c, p, i, qv);
         }
       }
+      if constexpr (pass == CH1_P1)
+        if (h == 2) keep_row(keep + (long long)i * p, o, p);
     } else if constexpr (pass == CH2_P2) {
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         if (c < c0 || c >= c1) continue;
-        keep[i * p + c] = o[c];
         store_w<Cfg>(P, c, 2 * p, i, o[c]);
         store_w<Cfg>(P, p + c, 2 * p, i, op[c]);
       }
+      keep_row(keep + (long long)i * p, o, p);
     } else if constexpr (pass == CH2_P3) {
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         if (c < c0 || c >= c1) continue;
-        keep[(M + i) * p + c] = o[c];
-        keep[(2 * M + i) * p + c] = op[c];
         store_w<Cfg>(P, c, p, i, op[c]);
       }
+      keep_row(keep + (M + i) * p, o, p);
+      keep_row(keep + (2 * M + i) * p, op, p);
     } else if constexpr (pass == CH2_P4 || pass == CH1_P2 || pass == CHI_K2) {
       constexpr long long slot = pass == CH2_P4 ? 3 : pass == CHI_K2 ? 2 : 1;
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         if (c < c0 || c >= c1) continue;
-        keep[(slot * M + i) * p + c] = o[c];
         store_w<Cfg>(P, c, p, i, o[c]);
       }
+      keep_row(keep + (slot * M + i) * p, o, p);
     } else if constexpr (pass == CHC_P1 || pass == CHC_P2) {
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         if (c < c0 || c >= c1) continue;
-        if constexpr (pass == CHC_P2) keep[i * p + c] = o[c];
         store_w<Cfg>(P, c, p, i, o[c]);
       }
+      if constexpr (pass == CHC_P2) keep_row(keep + (long long)i * p, o, p);
     } else if constexpr (pass == CHC_P3) {
       const float(&kv)[4][8] = *reinterpret_cast<const float(*)[4][8]>(pre.v);
 #pragma unroll

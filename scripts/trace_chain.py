@@ -31,12 +31,12 @@ h = P.Handle()
 for _ in range(3):
     P.polar(mats, out=outs, handle=h, **opts)
 torch.cuda.synchronize()
-buf = torch.zeros(16 * 32 * 160 * 4, dtype=torch.int64, device="cuda")
+buf = torch.zeros(16 * 32 * 160 * 8, dtype=torch.int64, device="cuda")
 B.check(B.lib().prism_debug_trace_chain(ctypes.c_void_p(buf.data_ptr())), "trace")
 P.polar(mats, out=outs, handle=h, **opts)
 torch.cuda.synchronize()
 B.check(B.lib().prism_debug_trace_chain(None), "trace off")
-T = buf.view(16, 32, 160, 4).cpu().double()
+T = buf.view(16, 32, 160, 8).cpu().double()
 for k in range(a.iters):
     rows = []
     for ps in range(32):
@@ -63,6 +63,12 @@ for k in range(a.iters):
             line += f"  epi-end max {us(float(epi.max())):7.2f}"
         if prev_end is not None:
             line += f"  | gap {us(float(t[:, 1].min())) - prev_end:6.2f}"
+        ok = (t[:, 2] > 0) & (t[:, 4] > 0) & (t[:, 5] > 0) & (t[:, 6] > 0) & (t[:, 7] > 0)
+        if bool(ok.any()):
+            q = t[ok]
+            med = lambda a, b: float((q[:, b] - q[:, a]).median()) / 1e3  # noqa: E731
+            line += (f"\n           epilogue: staged {med(2, 4):5.2f}  barrier {med(4, 5):5.2f}  reduce {med(5, 6):5.2f}"
+                     f"  rows {med(6, 7):5.2f}  end-barrier {med(7, 3):5.2f} us")
         if epi.numel():
             prev_end = us(float(epi.max()))
         print(line)
