@@ -401,10 +401,12 @@ prism_status prism_debug_argmin(int n, const double* c_dev, double lo, double hi
 prism_status prism_debug_trace_gemm(unsigned long long* buf_dev, int mode);
 /* Diagnostics: persistent-grid cap (CTAs) of the next prism_debug_gemm launches (0: all SMs). */
 prism_status prism_debug_gemm_max_ctas(int max_ctas);
-/* Sketch-chain timeline hook: buf_dev (16 iterations x 32 pass codes x 160 CTAs x 8 u64,
+/* Sketch-chain timeline hook: buf_dev (16 iterations x 32 pass codes x 160 CTAs x 32 u64,
  * zeroed by the caller) receives per CTA globaltimer ns at entry, after the PDL wait, when the
  * first tile's accumulator is ready, when its epilogue ends, and the epilogue's inner marks
- * (staged, barrier, reduced, row epilogue done); NULL turns it off. */
+ * (staged, barrier, reduced, row epilogue done), [8, 24) the MMA's full-barrier arrival of the
+ * first tile's first 16 k-blocks and [24, 32) the producer's W issue of its first 8; NULL
+ * turns it off. */
 prism_status prism_debug_trace_chain(unsigned long long* buf_dev);
 
 #ifdef __cplusplus

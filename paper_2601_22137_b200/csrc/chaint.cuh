@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
   bool run = true;
   unsigned long long* tr = nullptr;
   if (g_chain_trace && L.iter && *L.iter < 16)
-    tr = g_chain_trace + ((size_t)(*L.iter * 32 + PASS) * 160 + blockIdx.x) * 8;
+    tr = g_chain_trace + ((size_t)(*L.iter * 32 + PASS) * 160 + blockIdx.x) * 32;
   if (tr && threadIdx.x == 0) tr[0] = globaltimer_ns();
   if (L.iter) {
     const int k = *L.iter;
@@ -194,6 +194,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
           const bool staged = t == (int)blockIdx.x && kb - kb_lo < pre_n;   // R already in flight
           if (!staged) mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
           tma_load_2d(sA, P.tmA, &full[stage], kb * Cfg::BK, 0);    // W rows 0..31 (OOB rows zero)
+          if (tr && t == (int)blockIdx.x && kb - kb_lo < 8) tr[24 + kb - kb_lo] = globaltimer_ns();
           if (!staged) {
             tma_load_2d(sB, P.tmB, &full[stage], kb * Cfg::BK, n0);   // R rows n0 .. n0+255
             if constexpr (Cfg::SPLIT) tma_load_2d(sB + Cfg::B_BYTES, P.tmB_lo, &full[stage], kb * Cfg::BK, n0);
@@ -224,6 +225,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
           const uint32_t dt = tmem_base + acc * Cfg::BN;
           for (int kb = kb0; kb < kb1; ++kb) {
             mbar_wait(&full[stage], phase);
+            if (tr && t == (int)blockIdx.x && kb - kb0 < 16 && sl == s_lo) tr[8 + kb - kb0] = globaltimer_ns();
             tc_fence_after();
             const uint32_t aA = smem_u32(stage_base + stage * Cfg::STAGE_BYTES);
             const uint32_t aB = aA + Cfg::A_BYTES;

@@ -1199,13 +1199,19 @@ __device__ double argmin_quartic_free(const double c[5], double a_default) {
 // launch carries only its own fit (a kernel holding every kind's argmin stalled on
 // instruction fetch: ncu stall_no_inst 50 %): AK 0 polar / sqrt / sign (quartic of the
 // factored loss), 1 Chebyshev (quadratic), 2 inverse Newton (degree 2q), 3 DB Newton (free quartic).
+// One warp per matrix, kAlphaWarps matrices per block: the fit occupies ceil(B / 8) SMs,
+// not B (a block on an SM keeps a GEMM CTA — which needs the whole register file — off it;
+// the early square GEMM runs its mainloop on the others, prism.cu).
+constexpr int kAlphaWarps = 8;
 template <int AK>
-__global__ void __launch_bounds__(32) k_alpha(SolveParams P, int) {
+__global__ void __launch_bounds__(32 * kAlphaWarps) k_alpha(SolveParams P, int) {
   griddep_wait();
   griddep_launch();
   const int k = *P.iter;
   const int do_fit = AK == 3 ? (P.fit != 1 && k < P.max_iters && k >= P.warmup) : (fit_at(P, k) ? 1 : 0);
-  const int b = blockIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (b >= P.batch) return;
   const MatDesc& D = P.mats[b];
   MatState& S = P.st[b];
   if (S.done) return;   // stopped in this iteration's residual stage (or earlier)
@@ -1217,7 +1223,7 @@ __global__ void __launch_bounds__(32) k_alpha(SolveParams P, int) {
     // m(a) = a^4 <E1,E1> + 2 a^2 (1-a)^2 <E1,E2> + (1-a)^4 <E2,E2>  (R27)
     double s3[3] = {0.0, 0.0, 0.0};
     const int nt = D.tiles_m * D.tiles_n;
-    for (int t = threadIdx.x; t < nt; t += 32)
+    for (int t = lane; t < nt; t += 32)
 #pragma unroll
       for (int j = 0; j < 3; ++j) s3[j] += D.dbpart[3 * t + j];
 #pragma unroll
@@ -1241,7 +1247,7 @@ __global__ void __launch_bounds__(32) k_alpha(SolveParams P, int) {
     const double* __restrict__ cpart = D.chain_part;
     const int ctiles = D.chain_tiles;
 #pragma unroll 4
-    for (int t = threadIdx.x; t < ctiles; t += 32) {   // four groups' loads in flight per lane
+    for (int t = lane; t < ctiles; t += 32) {   // four groups' loads in flight per lane
       const double* cp = cpart + kChainG * t;
 #pragma unroll
       for (int j = 0; j < NGMAX; ++j)
@@ -1275,7 +1281,7 @@ __global__ void __launch_bounds__(32) k_alpha(SolveParams P, int) {
       a = (k < P.warmup) ? P.ahi : argmin_quartic(c, P.alo, P.ahi, P.ataylor);
     }
   }
-  if (threadIdx.x == 0) {
+  if (lane == 0) {
     S.alpha = a;
     P.alpha_hist[(size_t)b * P.max_iters + k] = a;
   }

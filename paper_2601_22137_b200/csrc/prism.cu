@@ -1229,6 +1229,10 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
   // MMAs: shampoo 4 % slower), large batches (k_alpha holds B SMs: GPT-2 unchanged, 1B
   // batch 1 % slower) or the general square products of sign / Chebyshev (1-2 % slower).
   const bool polar_kind = !r.sqrt_kind && !r.sign_kind && !r.cheb_kind && !r.inv_q && !r.db_kind;
+  // k_alpha: one warp per matrix, kAlphaWarps per block (it holds ceil(B / 8) SMs)
+  const dim3 alpha_grid((B + kAlphaWarps - 1) / kAlphaWarps), alpha_block(32 * std::min(B, kAlphaWarps));
+  // (with k_alpha packed on ceil(B / 8) SMs and the square grid capped to leave them, the
+  // GPT-2 batch measured the same step time: the early square stays at B <= 16)
   if (polar_kind && prec == PRISM_BF16 && B <= 16) g_sq.early = 1;
   const GemmLaunch g_sq2 = make_launch(*P, P->square2, nullptr, r.ws, 0, M);
   std::vector<GemmLaunch> g_gjT, g_gjS;
@@ -1272,7 +1276,7 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
       }
       {
         KindTimer t(h, s2, 4, timed ? 1 : 0);
-        PRISM_CK(launch_k(k_alpha<3>, dim3(B), dim3(32), 0, s2, 1, S, 1));
+        PRISM_CK(launch_k(k_alpha<3>, alpha_grid, alpha_block, 0, s2, 1, S, 1));
       }
       {
         KindTimer t(h, s2, 2, timed ? 2 : 0);
@@ -1307,9 +1311,9 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
       // norm partials from the residual step; a sketch chain in between makes them final
       // before k_alpha's wait
       KindTimer t(h, s2, 4, timed ? 1 : 0);
-      if (P->inv_q) PRISM_CK(launch_k(k_alpha<2>, dim3(B), dim3(32), 0, s2, 1, S, 0));
-      else if (r.cheb_kind) PRISM_CK(launch_k(k_alpha<1>, dim3(B), dim3(32), 0, s2, 1, S, 0));
-      else PRISM_CK(launch_k(k_alpha<0>, dim3(B), dim3(32), 0, s2, 1, S, 0));
+      if (P->inv_q) PRISM_CK(launch_k(k_alpha<2>, alpha_grid, alpha_block, 0, s2, 1, S, 0));
+      else if (r.cheb_kind) PRISM_CK(launch_k(k_alpha<1>, alpha_grid, alpha_block, 0, s2, 1, S, 0));
+      else PRISM_CK(launch_k(k_alpha<0>, alpha_grid, alpha_block, 0, s2, 1, S, 0));
     }
     if (P->has_square) {
       KindTimer t(h, s2, 1, timed ? (P->has_square2 ? 2 : 1) : 0);
@@ -1914,7 +1918,7 @@ prism_status prism_polar_rowblock_tr(prism_handle h, const prism_transport* tr, 
         for (int j = 0; j < P->n_chain; ++j)
           PRISM_CK(launch_chain(prec, chain_pass(*P, j), make_launch(*P, P->chaint[j], nullptr, r.ws, o->warmup_iters, M), st));
       }
-      PRISM_CK(launch_k(k_alpha<0>, dim3(1), dim3(32), 0, st, 1, S, 0));
+      PRISM_CK(launch_k(k_alpha<0>, dim3(1), dim3(32), 0, st, 1, S, 0));   // one matrix: one warp
       PRISM_CK(cudaMemcpyAsync(h->h_flag, &P->params.st[0].done, sizeof(int), cudaMemcpyDeviceToHost, st));
       PRISM_CK(cudaEventRecord(ev_stop, st));
       // 3. this rank's rows: X_r g_d(R; alpha) without R^2 (skipped on the device once stopped)

@@ -31,12 +31,12 @@ h = P.Handle()
 for _ in range(3):
     P.polar(mats, out=outs, handle=h, **opts)
 torch.cuda.synchronize()
-buf = torch.zeros(16 * 32 * 160 * 8, dtype=torch.int64, device="cuda")
+buf = torch.zeros(16 * 32 * 160 * 32, dtype=torch.int64, device="cuda")
 B.check(B.lib().prism_debug_trace_chain(ctypes.c_void_p(buf.data_ptr())), "trace")
 P.polar(mats, out=outs, handle=h, **opts)
 torch.cuda.synchronize()
 B.check(B.lib().prism_debug_trace_chain(None), "trace off")
-T = buf.view(16, 32, 160, 8).cpu().double()
+T = buf.view(16, 32, 160, 32).cpu().double()
 for k in range(a.iters):
     rows = []
     for ps in range(32):
@@ -69,6 +69,13 @@ for k in range(a.iters):
             med = lambda a, b: float((q[:, b] - q[:, a]).median()) / 1e3  # noqa: E731
             line += (f"\n           epilogue: staged {med(2, 4):5.2f}  barrier {med(4, 5):5.2f}  reduce {med(5, 6):5.2f}"
                      f"  rows {med(6, 7):5.2f}  end-barrier {med(7, 3):5.2f} us")
+        kbt = t[:, 8:24]
+        okk = (kbt[:, 0] > 0) & (t[:, 1] > 0)
+        if bool(okk.any()):
+            q = kbt[okk]
+            w = t[okk, 1]
+            arr = [float((q[:, k] - w).median()) / 1e3 for k in range(16) if bool((q[:, k] > 0).all())]
+            line += "\n           k-block ready after the PDL wait (us): " + " ".join(f"{x:.2f}" for x in arr)
         if epi.numel():
             prev_end = us(float(epi.max()))
         print(line)
