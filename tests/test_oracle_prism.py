@@ -457,3 +457,27 @@ def test_argmin_badly_scaled_cubic_against_dense_grid():
         assert lo <= a <= hi
         assert m(a) <= m(xs).min() + 1e-12 * np.max(np.abs(c[1:]))
         assert abs(a - xs[np.argmin(m(xs))]) <= 2 * (hi - lo) / 200000
+
+
+def test_argmin_against_companion_roots():
+    """Pin of argmin_quartic (R16) by an independent method: the critical points as
+    the eigenvalues of the companion matrix of m'(a) (numpy.roots), the interval ends, and
+    the smallest loss among them.  The oracle's argmin splits [lo, hi] at the roots of m''
+    and bisects m' (the same design as the device's), so this shares nothing with it; the
+    two must reach the same minimal loss (the minimiser itself may differ on flat ties)."""
+    g = np.random.default_rng(7)
+    for lo, hi in ((0.375, 1.45), (0.5, 1.0)):
+        for _ in range(3000):
+            c = g.standard_normal(5) * 10.0 ** g.uniform(-8, 3, 5)
+            if g.random() < 0.6:
+                c[4] = abs(c[4])
+            scale = float(np.max(np.abs(c[1:])))
+            m = lambda x: c[1] * x + c[2] * x ** 2 + c[3] * x ** 3 + c[4] * x ** 4  # noqa: E731
+            cands = [lo, hi]
+            for r in np.roots([4.0 * c[4], 3.0 * c[3], 2.0 * c[2], c[1]]):
+                if abs(r.imag) <= 1e-7 * (1.0 + abs(r.real)) and lo <= r.real <= hi:
+                    cands.append(float(r.real))
+            best = min(m(x) for x in cands)
+            a = prism.argmin_quartic(c, lo, hi, lo)
+            assert lo <= a <= hi
+            assert m(a) <= best + 1e-11 * scale, (c.tolist(), lo, hi, a, m(a), best)
