@@ -130,7 +130,8 @@ prism_status prism_polar(prism_handle h, int batch, const int64_t* m, const int6
  * handle-owned device staging slots, the solve, and the download into Q, then returns;
  * `stream` is made to wait for the download, so a sync of `stream` (or later work on it)
  * observes Q.  Successive calls on one handle pipeline: the upload of call k+1 and the
- * download of call k overlap the solves.  Staging and workspace are device memory owned by
+ * download of call k overlap the solves.  The upload starts when the call is made (it is
+ * not ordered after work queued earlier on `stream`): A must hold its values at the call.  Staging and workspace are device memory owned by
  * the handle (grown on demand, which synchronises the device).  rep: optional DEVICE
  * report, written in call order (read it once no later call is in flight).
  */
