@@ -142,10 +142,19 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
   if (threadIdx.x == 0) s_first_active = 1;
   if (run && warp == 0 && lane == 0 && (int)blockIdx.x < L.ntiles) {
     const uint32_t code = L.tiles[blockIdx.x];
-    const GemmProblem& P = probs[code >> 20];
+    const int q = (int)(code >> 20);
+    // the matrix from the problem index (matrix-major, probs_per_matrix each), so its stop
+    // iteration loads together with the problem's fields instead of after them (a late CTA's
+    // prologue is on the pass's critical path)
+    const int* stop_p = (L.done && L.iter)
+                            ? L.done + (size_t)(L.probs_per_matrix ? q / L.probs_per_matrix : probs[q].matrix) *
+                                           L.done_stride + kStopIterOffset
+                            : nullptr;
+    const int stop_it = stop_p ? *stop_p : 0x7fffffff;
+    const GemmProblem& P = probs[q];
     tma_prefetch(P.tmA);
     tma_prefetch(P.tmB);
-    s_first_active = !(L.done && L.iter && L.done[P.matrix * L.done_stride + kStopIterOffset] < *L.iter);
+    s_first_active = !(stop_p && stop_it < *L.iter);
     if (s_first_active) {
       const int n0 = ((code >> 10) & 1023) * Cfg::BN;
       int s_lo, s_hi, kb_lo, kb_hi, dummy;

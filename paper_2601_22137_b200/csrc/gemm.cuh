@@ -181,6 +181,7 @@ struct GemmLaunch {
   // matrix stopping at k, decided concurrently, is computed by every role alike)
   int early;
   int max_ctas;                  // > 0: persistent grid capped (row-block Gram: SMs left to NCCL)
+  int probs_per_matrix;          // chain: problems per matrix (sketch chunks, matrix-major order), else 0
 };
 
 // The problem fields the tile epilogue needs, held in registers for the tile: read

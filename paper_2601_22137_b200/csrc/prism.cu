@@ -918,7 +918,10 @@ int chain_pass(const Plan& P, int j) {
 GemmLaunch make_launch(const Plan& P, const LaunchDesc& L, const LaunchDesc* odd, char* ws, int lo, int hi,
                        const LaunchDesc* k0 = nullptr) {
   GemmLaunch g{};
-  g.ksplit = (!L.probs.empty() && L.probs[0].p.mode == EPI_CHAIN) ? P.chain_ksplit : 1;
+  const bool chain = !L.probs.empty() && L.probs[0].p.mode == EPI_CHAIN;
+  g.ksplit = chain ? P.chain_ksplit : 1;
+  // chain problems are matrix-major, one per sketch chunk (build_plan)
+  g.probs_per_matrix = chain ? (int)L.probs.size() / P.params.batch : 0;
   (void)ws;
   char* meta = P.meta_dev;
   g.probs = reinterpret_cast<const GemmProblem*>(meta + L.probs_off);
