@@ -400,6 +400,16 @@ prism_status prism_debug_argmin(int n, const double* c_dev, double lo, double hi
  * whose epilogue mode is `mode` (0 residual, 1 poly, 2 apply; < 0 off) record per-CTA
  * globaltimer stamps (gemm.cuh).  NULL disables. */
 prism_status prism_debug_trace_gemm(unsigned long long* buf_dev, int mode);
+/* Diagnostics (the pool refuses compute-sanitizer): with guards enabled, plans built from then
+ * on follow every workspace sub-buffer with a 256-B band no kernel may touch (plans are keyed
+ * by the switch; the workspace query grows accordingly).  _fill sets the bands of the last plan
+ * used on `h` to 0xA5 (on `stream`); _check synchronises `stream` and counts the changed bytes
+ * over all bands (bad_bytes) and the bands (guards). */
+prism_status prism_debug_workspace_guards(int enable);
+prism_status prism_debug_guards_fill(prism_handle h, void* stream);
+prism_status prism_debug_guards_check(prism_handle h, int64_t* bad_bytes, int64_t* guards, void* stream);
+/* Positive control of the checker: clears the first byte of guard band idx of the last plan. */
+prism_status prism_debug_guards_poke(prism_handle h, int64_t idx, void* stream);
 /* Diagnostics: persistent-grid cap (CTAs) of the next prism_debug_gemm launches (0: all SMs). */
 prism_status prism_debug_gemm_max_ctas(int max_ctas);
 /* Sketch-chain timeline hook: buf_dev (16 iterations x 32 pass codes x 160 CTAs x 32 u64,

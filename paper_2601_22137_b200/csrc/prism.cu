@@ -8,6 +8,7 @@
 #include "internal.h"
 
 #include <algorithm>
+#include <atomic>
 #include <array>
 #include <cstdio>
 #include <cmath>
@@ -151,6 +152,7 @@ struct Plan {
   bool db = false;
   int db_steps = 0;
   int n_chain = 0;
+  std::vector<std::pair<size_t, size_t>> guards;   // workspace guard bands (diagnostics)
   int chain_ksplit = 1;   // cluster size of the chain launches (split-K; 1, 2 or 4)
   bool has_square = false, has_square2 = false;
   int inv_q = 0;                    // inverse Newton root order (0: other kinds)
@@ -203,13 +205,26 @@ void resolve_interval(prism_options& o, double& lo, double& hi, double& aT, int&
   hi = std::isnan(o.alpha_hi) ? dhi : o.alpha_hi;
 }
 
+// Workspace guard bands (diagnostics, prism_debug_workspace_guards): with the switch on,
+// every workspace sub-buffer is followed by kGuardBytes that no kernel may touch; the
+// plan records them and prism_debug_guards_fill / _check test them around a solve (the
+// pool refuses compute-sanitizer).
+constexpr size_t kGuardBytes = 256;
+static std::atomic<int> g_guard_ws{0};
+
 struct Bump {
   char* base;
+  std::vector<std::pair<size_t, size_t>>* guards = nullptr;   // (offset, bytes) when guarded
   size_t off = 0;
   char* take(size_t bytes, size_t align = 256) {
     off = align_up(off, align);
     char* p = base + off;
     off += bytes;
+    if (guards) {
+      off = align_up(off, 16);
+      guards->push_back({off, kGuardBytes});
+      off += kGuardBytes;
+    }
     return p;
   }
 };
@@ -279,6 +294,8 @@ prism_status build_plan(const Request& r, Plan& P) {
   const int p = o.sketch_size;
   const int B = r.batch;
   Bump bump{r.ws};
+  P.guards.clear();
+  if (g_guard_ws.load()) bump.guards = &P.guards;
 
   // state region
   MatState* d_st = reinterpret_cast<MatState*>(bump.take(sizeof(MatState) * B));
@@ -992,6 +1009,8 @@ prism_status validate(const Request& r) {
 constexpr int kKinds = 6;
 struct prism_handle_s {
   std::list<std::unique_ptr<Plan>> plans;   // most recent first
+  std::vector<std::pair<size_t, size_t>> last_guards;   // guard bands of the last plan (diagnostics)
+  char* last_ws = nullptr;
   std::map<std::vector<long long>, size_t> ws_cache;   // workspace size per argument key
   long long launches = 0;                   // launches of the last solve
   bool profiling = false;
@@ -1102,6 +1121,7 @@ cudaEvent_t handle_event(prism_handle h, int idx) {
 static std::vector<long long> make_key(const Request& r) {
   std::vector<long long> k;
   k.push_back(current_device());   // plans hold device allocations and per-device graphs
+  k.push_back(g_guard_ws.load());  // guarded workspaces lay the buffers out differently
   k.push_back(r.sqrt_kind);
   k.push_back(r.sign_kind);
   k.push_back(r.inv_q);
@@ -1178,6 +1198,8 @@ static prism_status get_plan(prism_handle h, const Request& r, size_t ws_bytes, 
     P = h->plans.front().get();
   }
   if (ws_bytes < P->ws_need) return fail(PRISM_ERR_INVALID_ARG, "workspace too small");
+  h->last_guards = P->guards;   // diagnostics: the guard bands of the last plan used
+  h->last_ws = static_cast<char*>(r.ws);
   *out = P;
   return PRISM_OK;
 }
@@ -2089,6 +2111,40 @@ prism_status prism_debug_trace_gemm(unsigned long long* buf_dev, int mode) {
   if (set_gemm_trace_bf16(buf_dev, m) != cudaSuccess || set_gemm_trace_f32x3(buf_dev, m) != cudaSuccess ||
       set_gemm_trace_tf32(buf_dev, m) != cudaSuccess)
     return fail(PRISM_ERR_CUDA, "trace hook");
+  return PRISM_OK;
+}
+
+prism_status prism_debug_workspace_guards(int enable) {
+  g_guard_ws.store(enable ? 1 : 0);
+  return PRISM_OK;
+}
+
+prism_status prism_debug_guards_fill(prism_handle h, void* stream) {
+  if (!h || !h->last_ws) return fail(PRISM_ERR_INVALID_ARG, "no guarded solve on this handle");
+  for (const auto& g : h->last_guards)
+    PRISM_CK(cudaMemsetAsync(h->last_ws + g.first, 0xA5, g.second, static_cast<cudaStream_t>(stream)));
+  return PRISM_OK;
+}
+
+prism_status prism_debug_guards_poke(prism_handle h, int64_t idx, void* stream) {
+  if (!h || !h->last_ws || idx < 0 || idx >= (int64_t)h->last_guards.size())
+    return fail(PRISM_ERR_INVALID_ARG, "no such guard band");
+  PRISM_CK(cudaMemsetAsync(h->last_ws + h->last_guards[idx].first, 0, 1, static_cast<cudaStream_t>(stream)));
+  return PRISM_OK;
+}
+
+prism_status prism_debug_guards_check(prism_handle h, int64_t* bad_bytes, int64_t* guards, void* stream) {
+  if (!h || !bad_bytes || !guards) return fail(PRISM_ERR_INVALID_ARG, "null argument");
+  std::vector<unsigned char> buf;
+  int64_t bad = 0;
+  PRISM_CK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  for (const auto& g : h->last_guards) {
+    buf.resize(g.second);
+    PRISM_CK(cudaMemcpy(buf.data(), h->last_ws + g.first, g.second, cudaMemcpyDeviceToHost));
+    for (unsigned char c : buf) bad += c != 0xA5;
+  }
+  *bad_bytes = bad;
+  *guards = (int64_t)h->last_guards.size();
   return PRISM_OK;
 }
 
