@@ -15,6 +15,8 @@ Multi-GPU (launched by torch.distributed.run, one rank per GPU, NCCL):
                   ranks by prism_polar_sharded, outputs exchanged by NCCL broadcasts from
                   their owners inside the timed region; every rank ends with all 48N.
   gpt1b           strong scaling of configs[4] (96 matrices, 1.2 B params), same path.
+  shampoo         strong scaling of the Shampoo step's SPD blocks through
+                  prism_sqrt_invsqrt_sharded (both outputs broadcast).
   rowblock8192    strong scaling of configs[3]: one 8192^2 BF16 matrix split by rows
                   (prism_polar_rowblock: packed-triangle Gram all-reduce per iteration).
   others          independent replicas (no data-path collective).
@@ -36,7 +38,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "PRISM solves/sec and TFLOP/s vs B200 BF16 peak; iterations to tolerance"
-SHARDED = ("gpt2", "gpt1b")   # workloads whose N > 1 run goes through the sharded path
+SHARDED = ("gpt2", "gpt1b", "shampoo")   # workloads whose N > 1 run goes through the sharded path
 
 
 # ---------------------------------------------------------------- workloads
@@ -602,17 +604,24 @@ def run_multi(args, rank, world, dev):
         host = [torch.tensor(a).to(dt).pin_memory() for a in mats_np]
         mats = [x.to(dev) for x in host]
         outs = [torch.empty_like(x) for x in mats]
+        outs2 = [torch.empty_like(x) for x in mats]
         hout = [torch.empty_like(x).pin_memory() for x in host]
         units = len(mats)
 
-        def run():
-            return D.polar_sharded(mats, comm, out=outs, nbuckets=2, handle=h, **opts)
+        if kind == "sqrt":   # Shampoo blocks: A^{1/2}, A^{-1/2} sharded (prism_sqrt_invsqrt_sharded)
+            def run():
+                _, _, rep_ = D.sqrt_invsqrt_sharded(mats, comm, out_sqrt=outs, out_invsqrt=outs2, nbuckets=2,
+                                                    handle=h, **opts)
+                return outs, rep_
+        else:
+            def run():
+                return D.polar_sharded(mats, comm, out=outs, nbuckets=2, handle=h, **opts)
 
         def run_e2e():
             for d_, h_ in zip(mats, host):
                 d_.copy_(h_, non_blocking=True)
             r = run()
-            for h_, o_ in zip(hout, outs):
+            for h_, o_ in zip(hout, outs2 if kind == "sqrt" else outs):   # Shampoo consumes A^{-1/2}
                 h_.copy_(o_, non_blocking=True)
             return r
         h2d = d2h = sum(x.numel() * x.element_size() for x in host)
@@ -626,7 +635,7 @@ def run_multi(args, rank, world, dev):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max, e_max = float(t[0]), float(t[1])
-    f_iter = flops_per_iter(P, "polar", shapes, opts)
+    f_iter = flops_per_iter(P, "sqrt" if kind == "sqrt" else "polar", shapes, opts)
     flops = sum(f * k for f, k in zip(f_iter, iters))
     if kind == "rowblock":   # row-block F_min: symmetric Gram + X_r R + Y_r R (no R^2) per rank, summed
         n = shapes[0][1]
@@ -645,7 +654,8 @@ def run_multi(args, rank, world, dev):
             "dtype": opts["precision"], "data": "synthetic: seeded matrices shaped like the paper's workloads",
             "config": {"workload": name, "description": desc, "matrices": units, "solver": kind,
                        "parallelism": (f"row-block x{world} (prism_polar_rowblock, NCCL)" if kind == "rowblock" else
-                                       f"LPT-sharded x{world} (prism_polar_sharded, NCCL broadcasts, 2 buckets)"),
+                                       f"LPT-sharded x{world} ({'prism_sqrt_invsqrt_sharded' if kind == 'sqrt' else 'prism_polar_sharded'}, "
+                                       f"NCCL broadcasts, 2 buckets)"),
                        "l2": "flushed (256 MiB write) before every timed step, outside the events",
                        "e2e_path": "pinned host inputs copied in, library multi-GPU call, outputs copied out"},
             "tflops": tflops, "tflops_unit": "F_min per second, whole job",
