@@ -23,19 +23,21 @@
 
 namespace prism {
 
-template <int KIND_, bool SPLIT_>
+template <int KIND_, bool SPLIT_, int BN_ = 256>
 struct ChainTCfg {
   static constexpr int KIND = KIND_;
   static constexpr bool SPLIT = SPLIT_;   // 3xTF32: B carries R_hi and R_lo (W holds its own hi/lo rows)
   static constexpr int ESZ = KIND == 0 ? 2 : 4;
   static constexpr int BK = 128 / ESZ;      // one 128-B swizzle row of K
   static constexpr int UK = 32 / ESZ;       // K per tcgen05.mma
-  static constexpr int BN = 256;            // rows of R per tile (MMA N)
+  // rows of R per tile (MMA N): 256, or 128 for launches with few row tiles (a 4096^2
+  // matrix: 32 x 4 split CTAs instead of 16 x 4 — half the MMA time and epilogue rows each)
+  static constexpr int BN = BN_;
   static constexpr int WROWS = 32;          // W rows loaded per stage (MMA M = 128)
   static constexpr int A_BYTES = WROWS * 128;
   static constexpr int B_BYTES = BN * 128;
   static constexpr int STAGE_BYTES = A_BYTES + (SPLIT ? 2 : 1) * B_BYTES;
-  // receive / staging buffer: [C sources][32 c][256/C + 4] fp32 (padded rows: conflict-free)
+  // receive / staging buffer: [C sources][32 c][BN/C + 4] fp32 (padded rows: conflict-free)
   static constexpr int recv_bytes(int C) { return C * 32 * (BN / C + 4) * 4; }
   static constexpr int DSM_BYTES = recv_bytes(4) > recv_bytes(1) ? recv_bytes(4) : recv_bytes(1);
   static constexpr int STAGES_RAW = (227 * 1024 - 2048 - DSM_BYTES) / STAGE_BYTES;
@@ -274,7 +276,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
       int s_lo, s_hi;
       chain_slices(P, code, C, s_lo, s_hi);
       // this thread's row of the pass output, and its operands loaded ahead (chain_prefetch)
-      const bool mine = C == 1 || et < rows_per;   // whole warps (rows_per is a multiple of 32)
+      const bool mine = et < rows_per;   // whole warps (rows_per = BN / C, a multiple of 32)
       const int i = !mine ? P.M : tn * Cfg::BN + (C == 1 ? 0 : (int)krank * rows_per) + et;   // P.M: no row
       const int row0 = tn * Cfg::BN + (C == 1 ? 0 : (int)krank * rows_per) + (et & ~31);
       const int grp = (mine && row0 < P.M) ? row0 >> 5 : -1;   // this warp's 32-row group
@@ -294,14 +296,14 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
             tc_fence_after();
             if (tr && t == (int)blockIdx.x && et == 0) tr[2] = globaltimer_ns();
 #pragma unroll 1
-            for (int x0 = 0; x0 < 4; x0 += 2) {   // two 32-column loads in flight per wait
+            for (int x0 = 0; x0 < Cfg::BN / 64; x0 += 2) {   // two 32-column loads in flight per wait
               uint32_t r[2][32];
-              tmem_ld32(tmem_base + acc * Cfg::BN + h * 128 + x0 * 32, r[0]);
-              tmem_ld32(tmem_base + acc * Cfg::BN + h * 128 + (x0 + 1) * 32, r[1]);
+              tmem_ld32(tmem_base + acc * Cfg::BN + h * (Cfg::BN / 2) + x0 * 32, r[0]);
+              tmem_ld32(tmem_base + acc * Cfg::BN + h * (Cfg::BN / 2) + (x0 + 1) * 32, r[1]);
               tmem_ld_wait();
 #pragma unroll
               for (int x = 0; x < 2; ++x) {
-                float* dst = dsm + (size_t)lane * rstride + h * 128 + (x0 + x) * 32;
+                float* dst = dsm + (size_t)lane * rstride + h * (Cfg::BN / 2) + (x0 + x) * 32;
                 if (first) {
 #pragma unroll
                   for (int u = 0; u < 32; ++u) dst[u] = __uint_as_float(r[x][u]);
@@ -332,8 +334,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
         // every owner consumed the previous round's slices: send this round's
         mbar_wait(recv_free, rphase ^ 1);
 #pragma unroll 1
-        for (int x = 0; x < 4; ++x) {
-          const int col = h * 128 + x * 32;          // 32 rows n of the tile
+        for (int x = 0; x < Cfg::BN / 64; ++x) {
+          const int col = h * (Cfg::BN / 2) + x * 32;   // 32 rows n of the tile
           uint32_t r[32];
           if (have) {
             tmem_ld32(tmem_base + acc * Cfg::BN + col, r);

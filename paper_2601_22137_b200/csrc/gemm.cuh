@@ -182,6 +182,7 @@ struct GemmLaunch {
   int early;
   int max_ctas;                  // > 0: persistent grid capped (row-block Gram: SMs left to NCCL)
   int probs_per_matrix;          // chain: problems per matrix (sketch chunks, matrix-major order), else 0
+  int chain_bn;                  // chain: rows of R per tile (256, or 128 for launches with few row tiles)
 };
 
 // The problem fields the tile epilogue needs, held in registers for the tile: read

@@ -154,6 +154,7 @@ struct Plan {
   int n_chain = 0;
   std::vector<std::pair<size_t, size_t>> guards;   // workspace guard bands (diagnostics)
   int chain_ksplit = 1;   // cluster size of the chain launches (split-K; 1, 2 or 4)
+  int chain_bn = 256;     // rows of R per chain tile (128 when the 128-row tiles still fit the SMs)
   bool has_square = false, has_square2 = false;
   int inv_q = 0;                    // inverse Newton root order (0: other kinds)
   int max_s = 0, max_rows = 0, max_cols = 0, max_m = 0, max_n = 0;
@@ -776,26 +777,40 @@ prism_status build_plan(const Request& r, Plan& P) {
   if (P.has_square2) finish(P.square2, !polar_k);
   for (LaunchDesc& L : P.gjT) finish(L, false);
   for (LaunchDesc& L : P.gjS) finish(L, false);
-  // chain tiles (chaint.cuh): 256-row tiles of R, each split over a cluster of C CTAs,
+  // chain tiles (chaint.cuh): 256- (or 128-) row tiles of R, each split over a cluster of C CTAs,
   // C = the largest factor of the launch's matrices (smaller factors: empty slices).
   // Tiles of one row tile are contiguous and C-aligned, so slice == cluster rank.
   // A launch whose unsplit row tiles already fill the SMs runs every matrix's slices
   // in one CTA, in order (same bits, no exchange); otherwise each slice gets a CTA.
   P.chain_ksplit = 1;
+  P.chain_bn = 256;
   if (P.n_chain) {
-    long long rows = 0;
+    long long rows = 0, rows128 = 0;
     int kmax = 1;
     for (const HostProblem& hp : P.chaint[0].probs) {
       rows += (hp.p.M + 255) / 256;
+      rows128 += (hp.p.M + 127) / 128;
       kmax = std::max(kmax, hp.p.ksplit);
     }
     P.chain_ksplit = rows >= device_sms() ? 1 : kmax;
+    // 3xTF32: 128-row tiles when they still give one CTA per SM.  Its stages carry R_hi and
+    // R_lo (68 KB with 256-row tiles: two stages, latency-bound); 128-row tiles give five
+    // (4096^2 fp32 chain 3.65 -> 2.4-2.8 ms per step).  bf16 / tf32 keep 256 rows: their
+    // 128-row tiles stayed TMA-bound at the same k-block rate and the larger grid started
+    // more CTAs late (4096^2 bf16 chain 0.84 -> 0.90 ms).
+    if (prec == PRISM_FP32 && rows128 * P.chain_ksplit <= device_sms()) P.chain_bn = 128;
+    // the chain's R maps were made with 256-row boxes: match the tile height
+    for (int j = 0; j < P.n_chain; ++j)
+      for (const HostProblem& hp : P.chaint[j].probs) {
+        if (hp.mapB) maps[hp.mapB - 1].BN = P.chain_bn;
+        if (hp.mapB_lo) maps[hp.mapB_lo - 1].BN = P.chain_bn;
+      }
   }
   for (int j = 0; j < P.n_chain; ++j) {
     LaunchDesc& T = P.chaint[j];
     T.tiles.clear();
     for (int q = 0; q < (int)T.probs.size(); ++q)
-      for (int tn = 0; tn < (T.probs[q].p.M + 255) / 256; ++tn)
+      for (int tn = 0; tn < (T.probs[q].p.M + P.chain_bn - 1) / P.chain_bn; ++tn)
         for (int ks = 0; ks < P.chain_ksplit; ++ks)
           T.tiles.push_back(((uint32_t)q << 20) | ((uint32_t)tn << 10) | (uint32_t)ks);
     sort_tiles_by_cost(T);
@@ -939,6 +954,7 @@ GemmLaunch make_launch(const Plan& P, const LaunchDesc& L, const LaunchDesc* odd
   g.ksplit = chain ? P.chain_ksplit : 1;
   // chain problems are matrix-major, one per sketch chunk (build_plan)
   g.probs_per_matrix = chain ? (int)L.probs.size() / P.params.batch : 0;
+  g.chain_bn = P.chain_bn;
   (void)ws;
   char* meta = P.meta_dev;
   g.probs = reinterpret_cast<const GemmProblem*>(meta + L.probs_off);
