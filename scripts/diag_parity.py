@@ -1,6 +1,7 @@
 """Parity diagnostics (round 2): measured device-vs-oracle errors for the cases the
 round-1 verdict asked to tighten.  Prints one JSON line per case.
 
+  * FP32 polar (north_star bar 1e-5)
   * coupled sqrt / inv-sqrt FP32 at kappa <= 1e2 (north_star bar 1e-5 on both outputs)
   * DB Newton A^{-1/2} FP32
   * the exact mixed GPT-2 batch bench.py times (all 48 matrices vs the oracle)
@@ -56,6 +57,17 @@ def sqrt_cases(which):
                           "oracle_resid_hist": [float(v) for v in np.asarray(ohist)[: oit + 1]]}), flush=True)
 
 
+def polar_fp32():
+    for (m, n) in [(300, 200), (200, 520), (256, 256), (640, 384), (1024, 1024)]:
+        A = W.gaussian(m, n, seed=m + n)
+        At = torch.tensor(A).float().cuda()
+        Q, rep = P.polar([At], degree=5, max_iters=40, tol=1e-5, seed=42, precision="fp32")
+        torch.cuda.synchronize()
+        Qo, ro = prism.polar(At.double().cpu().numpy(), d=2, p=8, tol=1e-5, max_iters=40, seed=42)
+        print(json.dumps({"case": "polar_fp32", "shape": [m, n], "iters": int(rep["iters"][0]),
+                          "oracle_iters": ro.iters, "rel_oracle": rel(Q[0].double().cpu().numpy(), Qo)}), flush=True)
+
+
 def gpt2_mixed():
     shapes = W.gpt2_small_shapes()
     mats_np = W.muon_batch(shapes, seed=1, kind="mixed")
@@ -73,7 +85,9 @@ def gpt2_mixed():
 
 
 if __name__ == "__main__":
-    what = sys.argv[1:] or ["sqrt", "db", "gpt2"]
+    what = sys.argv[1:] or ["polar32", "sqrt", "db", "gpt2"]
+    if "polar32" in what:
+        polar_fp32()
     if "sqrt" in what:
         sqrt_cases("sqrt")
     if "db" in what:
