@@ -149,6 +149,34 @@ __global__ void __launch_bounds__(256) k_fro_partials(SolveParams P) {
     jr = j0 / nv;
     jc = j0 - jr * nv;
   }
+  if (nv > 0 && D.lda * esz == nv * 16) {
+    // dense rows (lda = n, n a whole number of vectors): the block's share is one contiguous
+    // range of memory — plain strided vector loads, no (row, column) bookkeeping
+    const uint4* q = reinterpret_cast<const uint4*>(A);
+    for (long long base = beg + threadIdx.x; base < end; base += 8 * 256) {
+      uint4 w[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const long long j = base + (long long)u * 256;
+        w[u] = j < end ? __ldg(q + j) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (bf16) {
+          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w[u]);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __bfloat1622float2(h[e]);
+            acc += (double)f.x * f.x + (double)f.y * f.y;
+          }
+        } else {
+          const float* f = reinterpret_cast<const float*>(&w[u]);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc += (double)f[e] * f[e];
+        }
+      }
+    }
+  } else
   for (long long base = beg + threadIdx.x; base < end; base += 8 * 256) {
     uint4 w[8];
     long long r = jr, c = jc;
