@@ -203,6 +203,55 @@ def test_rowblock_two_thread_ranks_fp32_parity(deg):
     assert _rel(Q, Qo) <= 1e-5
 
 
+@pytest.mark.parametrize("prec,tol,bound", [("bf16", 3e-2, 2e-2), ("tf32", 1e-2, 5e-3)])
+def test_rowblock_four_thread_ranks_ragged(prec, tol, bound):
+    # four ranks, ragged cuts (one rank holds fewer rows than a 256-row tile), n = 768:
+    # three panels, pipelined panel groups, every rank's alphas bit-identical
+    dt = torch.bfloat16 if prec == "bf16" else torch.float32
+    A = torch.tensor(W.gaussian(1100, 768, seed=23)).to(dt).cuda()
+    cuts = [0, 300, 555, 700, 1100]
+    res = _rowblock_threads(A, cuts, degree=5, tol=tol, max_iters=30, precision=prec)
+    it = [int(res[r][1]["iters"][0]) for r in range(4)]
+    assert len(set(it)) == 1
+    for r in range(1, 4):
+        assert torch.equal(res[r][1]["alphas"][0, :it[0]], res[0][1]["alphas"][0, :it[0]])
+    Q = torch.cat([res[r][0] for r in range(4)]).double().cpu().numpy()
+    Qo, ro = prism.polar(A.double().cpu().numpy(), d=2, p=8, tol=tol, max_iters=30, seed=42, b=0)
+    assert abs(it[0] - ro.iters) <= 1
+    assert _rel(Q, Qo) <= bound
+
+
+def test_sharded_four_thread_ranks_three_buckets_reports():
+    world = 4
+    base = _batch("bf16")
+    ref, rref = P.polar(base, degree=5, tol=3e-2, precision="bf16", matrix_ids=list(range(len(base))))
+    torch.cuda.synchronize()
+    g = D.HostGroup(world)
+    res = [None] * world
+
+    def run(r):
+        torch.cuda.set_device(0)
+        mats = [t.clone() for t in base]
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            res[r] = D.polar_sharded(mats, D.HostTransport(g, r), nbuckets=3, handle=P.Handle(), stream=st,
+                                     degree=5, tol=3e-2, precision="bf16")
+        st.synchronize()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for r in range(world):
+        out, rep = res[r]
+        for a, b in zip(out, ref):
+            assert torch.equal(a, b)
+        for k in ("iters", "status", "resid"):
+            assert torch.equal(rep[k], rref[k])
+        assert torch.equal(torch.nan_to_num(rep["alphas"]), torch.nan_to_num(rref["alphas"]))
+
+
 @pytest.mark.slow
 def test_config3_8192_rowblock_two_ranks_vs_oracle():
     """configs[3] at full size: 8192^2 BF16 split by rows over 2 emulated ranks, against one
