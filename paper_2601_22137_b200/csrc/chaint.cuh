@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) prism_chaint_kernel(const __g
   int pre_n = 0;   // producer: leading k-blocks of its first tile whose R is in flight
   if (threadIdx.x == 0) s_first_active = 1;
   if (run && warp == 0 && lane == 0 && (int)blockIdx.x < L.ntiles) {
-    const uint32_t code = L.tiles[blockIdx.x];
+    const uint32_t code = (int)blockIdx.x < kFirstCodes ? L.first_code[blockIdx.x] : L.tiles[blockIdx.x];
     const int q = (int)(code >> 20);
     // the matrix from the problem index (matrix-major, probs_per_matrix each), so its stop
     // iteration loads together with the problem's fields instead of after them (a late CTA's

@@ -164,6 +164,7 @@ struct GemmProblem {
   int pad2_;
 };
 
+constexpr int kFirstCodes = 160;
 struct GemmLaunch {
   const GemmProblem* probs;      // problem table (even iterations)
   const GemmProblem* probs_odd;  // problem table for odd iterations (ping-pong buffers) or null
@@ -183,6 +184,9 @@ struct GemmLaunch {
   int max_ctas;                  // > 0: persistent grid capped (row-block Gram: SMs left to NCCL)
   int probs_per_matrix;          // chain: problems per matrix (sketch chunks, matrix-major order), else 0
   int chain_bn;                  // chain: rows of R per tile (256, or 128 for launches with few row tiles)
+  // chain: the first tile code of CTA b (b < kFirstCodes) as a kernel parameter, so a CTA
+  // that starts late needs no dependent load of the tile list before staging its R
+  uint32_t first_code[kFirstCodes];
 };
 
 // The problem fields the tile epilogue needs, held in registers for the tile: read

@@ -955,6 +955,8 @@ GemmLaunch make_launch(const Plan& P, const LaunchDesc& L, const LaunchDesc* odd
   // chain problems are matrix-major, one per sketch chunk (build_plan)
   g.probs_per_matrix = chain ? (int)L.probs.size() / P.params.batch : 0;
   g.chain_bn = P.chain_bn;
+  if (chain)
+    for (int b = 0; b < kFirstCodes && b < (int)L.tiles.size(); ++b) g.first_code[b] = L.tiles[b];
   (void)ws;
   char* meta = P.meta_dev;
   g.probs = reinterpret_cast<const GemmProblem*>(meta + L.probs_off);
