@@ -83,6 +83,13 @@ def workload(name: str, rank: int, world: int = 1):
         desc = (f"configs[3]: one 8192x8192 Gaussian BF16 polar, row-block split over {world} rank(s) "
                 "(packed-triangle Gram all-reduce per iteration), PRISM-5, tol 3e-2")
         return "polar-8192-rowblock", shapes, mats, opts, desc, "rowblock"
+    if name == "square8192":
+        shapes = [(8192, 8192)]
+        mats = [W.gaussian(8192, 8192, seed=3000)]
+        opts = dict(degree=5, max_iters=25, tol=3e-2, sketch_size=8, seed=42, precision="bf16")
+        desc = ("configs[3]'s matrix on one GPU: one 8192x8192 Gaussian BF16 polar through prism_polar "
+                "(the single-GPU reference for the row-block path), PRISM-5, tol 3e-2")
+        return "polar-8192-square", shapes, mats, opts, desc, "polar"
     if name == "shampoo":
         shapes = [(1024, 1024)] * 8 + [(2048, 2048)] * 4 + [(4096, 4096)] * 2
         mats = [W.spd_logspaced(m, 1e2, seed=100 * rank + i) for i, (m, _) in enumerate(shapes)]
@@ -121,7 +128,7 @@ def workload(name: str, rank: int, world: int = 1):
     raise SystemExit(f"unknown workload {name}")
 
 
-WORKLOADS = ["gpt2", "square4096", "square4096_fp32", "gpt1b", "rowblock8192", "shampoo", "sign4096", "invroot",
+WORKLOADS = ["gpt2", "square4096", "square4096_fp32", "square8192", "gpt1b", "rowblock8192", "shampoo", "sign4096", "invroot",
              "cheb4096", "dbnewton"]
 
 
