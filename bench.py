@@ -747,7 +747,8 @@ def main():
     extra = None
     if rank == 0 and world == 1 and not args.no_extra and args.workload == "gpt2":
         extra = [extra_solve(P, "square4096", dev, flush, clocks, steps=10),
-                 extra_solve(P, "square4096_fp32", dev, flush, clocks, steps=5)]
+                 extra_solve(P, "square4096_fp32", dev, flush, clocks, steps=5),
+                 extra_solve(P, "square8192", dev, flush, clocks, steps=5)]
     clk = clocks.stop()
     clk["window"] = "timed + e2e + profiling (+ extra) passes (GPU busy throughout)"
     clk["timed_region"] = clk_timed
