@@ -100,3 +100,28 @@ def test_north_star_4096_bf16_full_parity():
     assert int(rep["status"][0]) == prism.CONVERGED
     assert abs(int(rep["iters"][0]) - ro.iters) <= 1
     assert _rel(Q[0].double().cpu().numpy(), Qo) <= 2e-2
+
+
+@pytest.mark.slow
+def test_polar_4096_fp32_full_parity():
+    """The extra block's second workload (the paper's precision): 4096^2 FP32
+    (3xTF32, 128-row chain tiles) against the fp64 oracle at tol 1e-5."""
+    A = torch.tensor(W.gaussian(4096, 4096, seed=4096)).float().cuda()
+    Q, rep = P.polar([A], degree=5, max_iters=25, tol=1e-5, seed=42, precision="fp32")
+    torch.cuda.synchronize()
+    Qo, ro = prism.polar(A.double().cpu().numpy(), d=2, p=8, tol=1e-5, max_iters=25, seed=42)
+    assert int(rep["status"][0]) == prism.CONVERGED
+    assert abs(int(rep["iters"][0]) - ro.iters) <= 1
+    assert _rel(Q[0].double().cpu().numpy(), Qo) <= 1e-5
+
+
+@pytest.mark.slow
+def test_polar_8192_bf16_single_gpu_parity():
+    """configs[3]'s matrix through the single-GPU path (the extra block's third workload)."""
+    A = torch.tensor(W.gaussian(8192, 8192, seed=3000)).to(torch.bfloat16).cuda()
+    Q, rep = P.polar([A], degree=5, max_iters=25, tol=3e-2, seed=42, precision="bf16")
+    torch.cuda.synchronize()
+    Qo, ro = prism.polar(A.double().cpu().numpy(), d=2, p=8, tol=3e-2, max_iters=25, seed=42)
+    assert int(rep["status"][0]) == prism.CONVERGED
+    assert abs(int(rep["iters"][0]) - ro.iters) <= 1
+    assert _rel(Q[0].double().cpu().numpy(), Qo) <= 2e-2
