@@ -277,8 +277,9 @@ def _check_dtype(ts, precision, on_host=False):
     where = "pinned host" if on_host else "CUDA"
     # set comprehensions: one attribute read per tensor and property (a per-tensor chain of
     # checks cost ~20 us on a 48-matrix batch)
+    T = torch.Tensor
     if ({t.dtype for t in ts} != {want} or {t.is_cuda for t in ts} != {not on_host}
-            or {t.dim() for t in ts} != {2} or {t.stride(1) for t in ts} != {1}):
+            or set(map(T.dim, ts)) != {2} or {st[1] for st in map(T.stride, ts)} != {1}):
         raise PrismError(f"inputs must be 2-D {where} {want} tensors with unit column stride")
     if on_host and not all(t.is_pinned() for t in ts):
         raise PrismError("host-path tensors must be pinned CPU tensors (tensor.pin_memory())")
@@ -320,8 +321,10 @@ def _outputs(mats, want, given, what, host):
     given = list(given)
     if len(given) != len(mats):
         raise PrismError(f"{what}: {len(given)} outputs for {len(mats)} matrices")
-    if ([g.shape for g in given] != [t.shape for t in mats] or {g.dtype for g in given} != {mats[0].dtype}
-            or {g.get_device() for g in given} != {mats[0].get_device()} or {g.stride(1) for g in given} != {1}):
+    T = torch.Tensor
+    if (list(map(T.size, given)) != list(map(T.size, mats)) or {g.dtype for g in given} != {mats[0].dtype}
+            or set(map(T.get_device, given)) != {mats[0].get_device()}
+            or {st[1] for st in map(T.stride, given)} != {1}):
         raise PrismError(f"{what}: each output must match its input's shape, dtype and device, rows contiguous")
     if host and not all(g.is_pinned() for g in given):
         raise PrismError(f"{what}: host-path outputs must be pinned")
@@ -376,10 +379,10 @@ def _solve(kind, mats, *, host=False, q=0, degree=5, max_iters=30, sketch_size=8
     # the ctypes argument arrays of this batch (sizes, pointers, leading dimensions, ids),
     # cached on the handle by everything they encode: building them for a 48-matrix batch
     # cost ~100 us per call, more than the whole host side of the library call
-    dp = torch.Tensor.data_ptr
-    key = (kind, tuple(map(dp, mats)), tuple(t.shape for t in mats), tuple(t.stride(0) for t in mats),
-           tuple(map(dp, o1)) if o1 else None, tuple(t.stride(0) for t in o1) if o1 else None,
-           tuple(map(dp, o2)) if o2 else None, tuple(t.stride(0) for t in o2) if o2 else None,
+    T = torch.Tensor
+    key = (kind, tuple(map(T.data_ptr, mats)), tuple(map(T.size, mats)), tuple(map(T.stride, mats)),
+           tuple(map(T.data_ptr, o1)) if o1 else None, tuple(map(T.stride, o1)) if o1 else None,
+           tuple(map(T.data_ptr, o2)) if o2 else None, tuple(map(T.stride, o2)) if o2 else None,
            tuple(matrix_ids) if matrix_ids is not None else None)
     arrs = h._marshal.get(key)
     if arrs is None:
