@@ -165,6 +165,9 @@ struct GemmProblem {
 };
 
 constexpr int kFirstCodes = 160;
+// tile code bit 9: a BN/2-column tile (bf16 applies only: the last, partial wave of a launch
+// is split in N so it runs on twice the CTA pairs; prism.cu).  tn then counts BN/2 columns.
+constexpr uint32_t kHalfTile = 512;
 struct GemmLaunch {
   const GemmProblem* probs;      // problem table (even iterations)
   const GemmProblem* probs_odd;  // problem table for odd iterations (ping-pong buffers) or null
@@ -1200,7 +1203,8 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
         const GemmProblem& P = probs[code >> 20];
         if (skip_tile(P.matrix)) continue;
         const int tm = (code >> 10) & 1023;
-        const int tn = code & 1023;
+        const int tn = code & 511;
+        const bool half = (code & kHalfTile) != 0;   // BN/2-column tile (last wave of an apply)
         const int kb_lo = 0, kb_hi = (P.K + Cfg::BK - 1) / Cfg::BK;
         // warm the TMA descriptor cache with this tile's maps (they live in global memory)
         tma_prefetch(P.tmA);
@@ -1210,7 +1214,8 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
           if constexpr (Cfg::LOB) tma_prefetch(P.tmB_lo);
         }
         const int am0 = tm * Cfg::TILE_M + (int)rank * Cfg::BM;      // this CTA's rows of A
-        const int bn0 = tn * Cfg::BN + (int)rank * Cfg::B_ROWS;      // this CTA's half of B
+        // this CTA's half of B (a half tile: the first B_ROWS/2 rows of the box are used)
+        const int bn0 = half ? tn * (Cfg::BN / 2) + (int)rank * (Cfg::B_ROWS / 2) : tn * Cfg::BN + (int)rank * Cfg::B_ROWS;
         for (int kb = kb_lo; kb < kb_hi; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sA = stage_base + stage * Cfg::STAGE_BYTES;
@@ -1243,7 +1248,7 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
         const uint32_t code = L.tiles[t];
         const GemmProblem& P = probs[code >> 20];
         if (skip_tile(P.matrix)) continue;
-        const int tn = code & 1023;
+        const bool half = (code & kHalfTile) != 0;
         const int kb_lo = 0, kb_hi = (P.K + Cfg::BK - 1) / Cfg::BK;
         // tf32: one TMEM accumulation chunk per PROMO_KB k-blocks, promoted to fp32
         // registers by the epilogue (bounds the truncation of the MMA accumulator add)
@@ -1259,7 +1264,8 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
             tc_fence_after();
             const uint32_t aA = smem_u32(stage_base + stage * Cfg::STAGE_BYTES);
             const uint32_t aB = aA + Cfg::A_BYTES;
-            const uint32_t idesc = Cfg::IDESC | ((uint32_t)P.a_mn << 15) | ((uint32_t)P.b_mn << 16);
+            uint32_t idesc = Cfg::IDESC | ((uint32_t)P.a_mn << 15) | ((uint32_t)P.b_mn << 16);
+            if (half) idesc = (idesc & ~(0x3Fu << 17)) | ((uint32_t)(Cfg::BN / 2 / 8) << 17);   // N = BN/2
 #pragma unroll
             for (int k = 0; k < Cfg::BK / Cfg::UK; ++k) {
               const uint64_t da = operand_desc<Cfg>(aA, k, P.a_mn);
@@ -1293,8 +1299,8 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
     const int e = warp - 4;                 // 0..7
     const int h = e >> 2;                   // column half of the tile owned by this warp
     const int et = threadIdx.x - 128;       // 0..255
-    const int c_begin = h * Cfg::CH_PER;
-    const int c_end = min(Cfg::NCH, c_begin + Cfg::CH_PER);
+    const int c_begin0 = h * Cfg::CH_PER;
+    const int c_end0 = min(Cfg::NCH, c_begin0 + Cfg::CH_PER);
     float* tb = tbuf + e * 32 * 33;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -1314,7 +1320,8 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
       const GemmProblem& P = probs[code >> 20];
       if (skip_tile(P.matrix)) continue;
       const int tm = (code >> 10) & 1023;
-      const int tn = code & 1023;
+      const int tn = code & 511;
+      const bool half = (code & kHalfTile) != 0;
       const int mode = P.mode;
       const bool sym = P.sym != 0;
       const EpiArgs ea{P.out, P.out_lo, P.gdiag, P.ldo, P.M, P.N, P.out2, P.out2_lo};
@@ -1339,7 +1346,10 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
         // chunks ahead, per-warp buffers C0/C1), next chunk's tcgen05.ld in flight
         // (ping-pong registers), output block staged and TMA-stored (O0/O1 alternate)
         uint8_t* wb = ebuf + e * 8192;
-        const int jb = tn * Cfg::BN;
+        // a half tile: BN/2 columns, half the chunks per warp
+        const int c_begin = half ? h * (Cfg::CH_PER / 2) : c_begin0;
+        const int c_end = half ? c_begin + Cfg::CH_PER / 2 : c_end0;
+        const int jb = half ? tn * (Cfg::BN / 2) : tn * Cfg::BN;
         const CUtensorMap* tmC = P.tmC;
         const CUtensorMap* tmO = P.tmO;
         auto c_fetch = [&](int ch) {   // lane 0
@@ -1436,7 +1446,7 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
 #pragma unroll
           for (int x = 0; x < Cfg::CH_PER; ++x) {
             uint32_t r[32];
-            tmem_ld32(tbase + (c_begin + x) * 32, r);
+            tmem_ld32(tbase + (c_begin0 + x) * 32, r);
             tmem_ld_wait();
 #pragma unroll
             for (int u = 0; u < 32; ++u) d[x][u] += __uint_as_float(r[u]);
@@ -1449,7 +1459,7 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
           float c[32];
 #pragma unroll
           for (int u = 0; u < 32; ++u) c[u] = 0.f;
-          const int j0 = tn * Cfg::BN + (c_begin + x) * 32;
+          const int j0 = tn * Cfg::BN + (c_begin0 + x) * 32;
           if (needC && i0 + 32 <= P.M && j0 + 32 <= P.N && (P.ldc & 3) == 0)
             warp_load_f32_block<Cfg::SPLIT>(P.C, P.C_lo, P.ldc, i0, j0, c, tb, lane);   // warp-uniform
           else if (needC && i < P.M && j0 < P.N) load_row32<Cfg::KIND, Cfg::SPLIT>(P.C, P.C_lo, P.ldc, i, j0, P.N, c);

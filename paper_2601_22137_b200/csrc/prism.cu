@@ -745,11 +745,30 @@ prism_status build_plan(const Request& r, Plan& P) {
   P.db = db;
   P.db_steps = db_steps;
   // tile lists (problem index within its launch)
-  auto finish = [&](LaunchDesc& L, bool) {
+  auto finish = [&](LaunchDesc& L, bool apply) {
     L.tiles.clear();
     for (int j = 0; j < (int)L.probs.size(); ++j)
       add_tiles(L, j, L.probs[j].p.M, L.probs[j].p.N, BN, L.probs[j].p.sym != 0);
     sort_tiles_by_cost(L);
+    // bf16 applies: the last, partial wave of the persistent launch (tiles t >= R - R % pairs
+    // run one per CTA pair while the other pairs idle) is split in N into BN/2-column tiles,
+    // so it takes about half a tile time (4096^2: 34 of 256 tiles -> 68 half tiles on 74 pairs).
+    // The per-element accumulation is the same for any N, so a matrix's bits do not depend on
+    // the split (GPU test: batch vs single solves).
+    bool all_apply = apply && prec == PRISM_BF16 && !L.probs.empty();
+    for (const HostProblem& hp : L.probs) all_apply = all_apply && hp.p.mode == EPI_APPLY && hp.p.sym == 0;
+    const int pairs = device_sms() / 2, nt = (int)L.tiles.size(), rem = nt % pairs;
+    if (all_apply && rem > 0 && 2 * rem <= pairs) {
+      std::vector<uint32_t> last(L.tiles.end() - rem, L.tiles.end());
+      L.tiles.resize(nt - rem);
+      for (uint32_t code : last) {
+        const uint32_t q = code >> 20, tm = (code >> 10) & 1023, tn = code & 1023;
+        const int N = L.probs[q].p.N;
+        for (uint32_t hh = 0; hh < 2; ++hh)
+          if ((int)((2 * tn + hh) * (BN / 2)) < N)
+            L.tiles.push_back((q << 20) | (tm << 10) | kHalfTile | (2 * tn + hh));
+      }
+    }
   };
   const bool polar_k = !r.sqrt_kind;
   if (P.fold) {
