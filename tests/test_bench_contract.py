@@ -35,3 +35,25 @@ def test_reference_arm_prints_one_contract_line():
 def test_reference_arm_other_ranks_print_nothing():
     lines = _run(["--impl", "reference", "--steps", "1", "--warmup", "0"], env={"RANK": "1", "WORLD_SIZE": "2"})
     assert lines == []
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.gpu
+def test_gpu_arm_contract_line():
+    """The GPU arm's line (short run, no CPU baseline / extra): the driver's keys plus the
+    roofline, clocks, e2e and launch-count blocks this repo reports."""
+    lines = _run(["--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-extra"])
+    d = json.loads([ln for ln in lines if ln.startswith("{")][-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "roofline", "clocks", "e2e", "gpu_launches"):
+        assert k in d, k
+    assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] >= 3 and d["value"] > 0
+    assert d["config"]["workload"] == "gpt2-small-muon-step" and d["dtype"] == "bf16"
+    rf = d["roofline"]
+    assert rf["bound"] == "tensor" and rf["unit"] == "TFLOP/s" and 0 < rf["frac"] < 1
+    assert abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-9
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    assert d["gpu_launches"] > 0
+    assert d["clocks"]["sm_mhz"] > 0 and "reasons" in d["clocks"]
