@@ -339,3 +339,24 @@ def test_folded_normalisation_edge_cases():
     torch.cuda.synchronize()
     Qo, ro = prism.polar(T.double().cpu().numpy(), d=2, p=8, tol=1e-2, max_iters=30, seed=42)
     assert abs(int(rt["iters"][0]) - ro.iters) <= 1 and _rel(Qt[0].double().cpu().numpy(), Qo) <= 5e-3
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["sqrt", "db_newton"])
+def test_single_output_requests_device_and_host(kind):
+    """Either output of the coupled kinds may be omitted (NULL in the C-ABI): the requested one
+    must equal the two-output solve bit for bit, through the device and the host entry points."""
+    mats = [torch.tensor(W.spd_logspaced(s, 1e2, seed=950 + s)).float().cuda() for s in (96, 260)]
+    host = [m.cpu().pin_memory() for m in mats]
+    dev_f, host_f = (P.sqrt_invsqrt, P.sqrt_invsqrt_host) if kind == "sqrt" else (P.db_newton, P.db_newton_host)
+    kw = dict(tol=1e-5, max_iters=40)
+    X, Y, _ = dev_f(mats, **kw)
+    X1, Y1, _ = dev_f(mats, want_invsqrt=False, **kw)
+    X2, Y2, _ = dev_f(mats, want_sqrt=False, **kw)
+    Xh1, Yh1, _ = host_f(host, want_invsqrt=False, **kw)
+    Xh2, Yh2, _ = host_f(host, want_sqrt=False, **kw)
+    torch.cuda.synchronize()
+    assert not Y1 and not X2 and not Yh1 and not Xh2
+    for i in range(len(mats)):
+        assert torch.equal(X1[i], X[i]) and torch.equal(Y2[i], Y[i])
+        assert torch.equal(Xh1[i], X[i].cpu()) and torch.equal(Yh2[i], Y[i].cpu())
