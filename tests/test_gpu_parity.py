@@ -360,3 +360,24 @@ def test_single_output_requests_device_and_host(kind):
     for i in range(len(mats)):
         assert torch.equal(X1[i], X[i]) and torch.equal(Y2[i], Y[i])
         assert torch.equal(Xh1[i], X[i].cpu()) and torch.equal(Yh2[i], Y[i].cpu())
+
+
+@pytest.mark.gpu
+def test_sqrt_divergence_status_and_residual_history():
+    """DIVERGED on the device (5 consecutive increases of ||R_k||_F): PRISM-3 with the
+    Taylor coefficient on a 64 x 64 diagonal with a negative eigenvalue, whose iterates are a
+    scalar recurrence per eigenvalue (tests/test_oracle_prism.py pins the same case): the
+    residuals fall, then grow from k = 5, and the solve stops at k = 9."""
+    lam = [1.0, 0.5, -0.03, 0.2] * 16
+    c = float(np.sqrt(np.sum(np.square(lam))))
+    x, y = np.array(lam) / c, np.ones(64)
+    hist = []
+    for _ in range(10):
+        r = 1.0 - y * x
+        hist.append(float(np.linalg.norm(r)) / 8.0)
+        x, y = x * (1.0 + 0.5 * r), (1.0 + 0.5 * r) * y
+    A = torch.diag(torch.tensor(lam, dtype=torch.float32)).cuda()
+    X, Y, rep = P.sqrt_invsqrt([A], degree=3, fit="taylor", tol=1e-6, max_iters=40, precision="fp32")
+    torch.cuda.synchronize()
+    assert int(rep["status"][0]) == prism.DIVERGED and int(rep["iters"][0]) == 9
+    np.testing.assert_allclose(rep["resid_hist"][0, :10].double().cpu().numpy(), hist, rtol=1e-3)

@@ -359,10 +359,51 @@ def test_warmup_and_status_codes():
     assert rep.status == prism.MAX_ITERS and rep.iters == 2 and len(rep.resid) == 3
 
 
-def test_sqrt_non_spd_does_not_converge():
-    A = np.diag([1.0, 0.5, -0.3, 0.2])
-    _, _, rep = prism.sqrt_invsqrt(A, d=2, tol=1e-10, max_iters=40)
-    assert rep.status in (prism.DIVERGED, prism.NONFINITE, prism.MAX_ITERS)
+def test_sqrt_non_spd_diverges_exactly_as_the_scalar_recurrence():
+    # A diagonal A keeps every iterate diagonal, so the Taylor-mode coupled iteration is one
+    # scalar recurrence per eigenvalue (P:246-250 with g_2(r) = 1 + r/2 + 3/8 r^2):
+    # x_0 = lambda / ||A||_F, y_0 = 1, r = 1 - y x, x <- x g(r), y <- g(r) y.  The negative
+    # eigenvalue makes ||R_k||_F grow at every step, so the DIVERGED rule (5 consecutive
+    # increases) stops it at k = 5, with the residual history of the recurrence.
+    lam = [1.0, 0.5, -0.3, 0.2]
+    A = np.diag(lam)
+    c = math.sqrt(sum(v * v for v in lam))
+    x, y = [v / c for v in lam], [1.0] * 4
+    hist = []
+    for _ in range(6):
+        r = [1.0 - yi * xi for xi, yi in zip(x, y)]
+        hist.append(math.sqrt(sum(v * v for v in r)) / 2.0)      # ||R||_F / sqrt(s), s = 4
+        g = [1.0 + 0.5 * v + 0.375 * v * v for v in r]
+        x = [xi * gi for xi, gi in zip(x, g)]
+        y = [gi * yi for gi, yi in zip(g, y)]
+    assert all(b > a for a, b in zip(hist, hist[1:]))
+    for fit in ("taylor", "sketched"):
+        _, _, rep = prism.sqrt_invsqrt(A, d=2, tol=1e-10, max_iters=40, fit=fit)
+        assert rep.status == prism.DIVERGED and rep.iters == 5, fit
+        np.testing.assert_allclose(rep.resid, hist, rtol=1e-12)
+    # PRISM-3 (d = 1, g_1(r) = 1 + r/2) on a 64 x 64 diagonal: ||R_k|| first falls, then
+    # grows five times in a row from k = 5, staying finite in fp32 (the device test's case)
+    lam64 = [1.0, 0.5, -0.03, 0.2] * 16
+    c = math.sqrt(sum(v * v for v in lam64))
+    x, y = [v / c for v in lam64], [1.0] * 64
+    hist = []
+    for _ in range(10):
+        r = [1.0 - yi * xi for xi, yi in zip(x, y)]
+        hist.append(math.sqrt(sum(v * v for v in r)) / 8.0)
+        x = [xi * (1.0 + 0.5 * v) for xi, v in zip(x, r)]
+        y = [(1.0 + 0.5 * v) * yi for v, yi in zip(r, y)]
+    assert hist[5] > hist[4] and all(b > a for a, b in zip(hist[4:], hist[5:]))
+    _, _, rep = prism.sqrt_invsqrt(np.diag(lam64), d=1, tol=1e-10, max_iters=40, fit="taylor")
+    assert rep.status == prism.DIVERGED and rep.iters == 9
+    np.testing.assert_allclose(rep.resid, hist, rtol=1e-12)
+    # the counter restarts after a decrease: 4 increases, a drop, 4 increases never diverge
+    rep, incr, r_prev = prism.Report(), 0, math.inf
+    for k, r in enumerate([1, 2, 3, 4, 5, 0.5, 1, 2, 3, 4]):
+        stop, incr = prism._status_update(rep, k, float(r), r_prev, 1, 1e-12, 40, incr)
+        r_prev = float(r)
+        assert not stop, k
+    stop, incr = prism._status_update(rep, 10, 5.0, r_prev, 1, 1e-12, 40, incr)
+    assert stop and rep.status == prism.DIVERGED
 
 
 def test_sqrt_iterates_commute():
