@@ -77,6 +77,8 @@ struct MatState {
   int incr;          // consecutive residual increases
   int stop_iter;     // iteration k at which the matrix stopped (INT_MAX while active; -1: zero input)
   int arrivals;      // residual stage: norm partials landed this iteration (the last one decides)
+  int flip;          // folded polar, this solve: the caller's Q holds the odd iterates X_1, X_3, ...
+                     // (else the even ones); chosen by k_init_state
 };
 
 // Stop test of iteration k (R12), run once per matrix by the last residual-stage

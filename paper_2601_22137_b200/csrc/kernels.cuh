@@ -18,6 +18,7 @@ struct MatDesc {
   long long lda, ldq;
   long long ldx0;      // leading dimension of X[0] (= ldq when X[0] is the caller's output Q)
   int fold;            // folded normalisation for this matrix (BF16 / TF32 polar, TMA-legal A, Q)
+  int flip_ok;         // folded and Q does not overlap A: Q may hold the odd iterates (MatState.flip)
   int pad0_;
   int m, n;            // user shape
   int s, L;            // small side / large side (polar); n, n (sqrt)
@@ -72,6 +73,11 @@ struct SolveParams {
   int inv_q;            // coupled inverse Newton root order (0: polar / sqrt / sign)
   int kind_cheb;        // Chebyshev inverse (A' in Y[0], X_0 = A'^T, output X / c)
   int kind_db;          // DB Newton (M_k in Mst, W = R: M_k then -M_k^{-1}; output X, Y unscaled)
+  int* parity;          // [batch] (plan-owned): final parity of each matrix's last solve (k_finalize)
+  int* flip_cur;        // [batch] (plan-owned): parity the ping-pong tables hold for each matrix
+  // folded polar: the tables whose entry b (matrix b) is swapped to flip matrix b's parity:
+  // gram[0] <-> gram[1], apply[0] <-> apply[1], apply0 <-> apply0f
+  GemmProblem* flip_tab[6];
   double tol, alo, ahi, ataylor;
   unsigned long long seed;
 };
@@ -525,10 +531,18 @@ __global__ void __launch_bounds__(256) k_normalize(SolveParams P) {
 __global__ void k_init_state(SolveParams P) {
   griddep_wait();
   griddep_launch();
+  __shared__ int s_swap;
   const int b = blockIdx.x;
   const MatDesc& D = P.mats[b];
   for (int t = threadIdx.x; t < D.tiles_m * D.tiles_n; t += blockDim.x) D.norm_part[t] = 0.f;
   if (threadIdx.x == 0) {
+    // folded polar: store the odd iterates in Q when the last solve ended after an odd
+    // number of updates, so that a repeat needs no final copy (any choice is correct: it
+    // only decides which buffer holds which iterate); the tables are flipped in place
+    const int want = (D.flip_ok && P.parity) ? P.parity[b] : 0;
+    s_swap = (P.flip_cur && want != P.flip_cur[b]) ? 1 : 0;
+    if (s_swap) P.flip_cur[b] = want;
+    P.st[b].flip = want;
     const double c = P.st[b].c;
     if (b == 0) *P.iter = 0;
     MatState& S = P.st[b];
@@ -541,6 +555,19 @@ __global__ void k_init_state(SolveParams P) {
     S.stop_iter = (c == 0.0) ? -1 : 0x7fffffff;
     S.arrivals = 0;
     S.status = (c == 0.0) ? 4 : 1;
+  }
+  __syncthreads();
+  if (s_swap) {
+    constexpr int W = (int)(sizeof(GemmProblem) / 4);
+    for (int j = 0; j < 3; ++j) {
+      uint32_t* x = reinterpret_cast<uint32_t*>(P.flip_tab[2 * j] + b);
+      uint32_t* y = reinterpret_cast<uint32_t*>(P.flip_tab[2 * j + 1] + b);
+      for (int w = threadIdx.x; w < W; w += blockDim.x) {
+        const uint32_t u = x[w];
+        x[w] = y[w];
+        y[w] = u;
+      }
+    }
   }
 }
 
@@ -1333,12 +1360,15 @@ __global__ void __launch_bounds__(256) k_finalize(SolveParams P) {
   const MatState& S = P.st[b];
   const int par = S.iters & 1;
   const bool zero = S.status == 4;   // ZERO_INPUT: output 0 (X may be an unwritten buffer)
-  // folded plans: X[0] is the caller's output itself (nothing to copy after an even number of
-  // updates), and X_0 = A/||A||_F was never written (a solve that stops at k = 0 writes it here)
+  if (D.fold && P.parity && t == P.out_tile_off[b] && threadIdx.x == 0) P.parity[b] = par;   // next solve's flip
+  // folded plans: X[0] is the caller's output itself, holding the even iterates (odd ones with
+  // S.flip): nothing to copy when the last one landed there; X[1] (workspace) holds the
+  // others.  X_0 = A/||A||_F was never written (a solve that stops at k = 0 writes it here).
   const bool from_a = D.fold && S.iters == 0 && !zero;
-  if (D.fold && par == 0 && !zero && !from_a) return;
-  const void* const Xp = D.X[par];
-  const void* const Xpl = D.X_lo[par];
+  if (D.fold && (par ^ S.flip) == 0 && !zero && !from_a) return;
+  const int src = D.fold ? 1 : par;
+  const void* const Xp = D.X[src];
+  const void* const Xpl = D.X_lo[src];
   const void* const Yp = D.Y[par];
   const void* const Ypl = D.Y_lo[par];
   const int TW = 32 * V::VE;
@@ -1357,7 +1387,7 @@ __global__ void __launch_bounds__(256) k_finalize(SolveParams P) {
     const int r = r0 + slot / 32, col = c0 + (slot % 32) * V::VE;
     if (r >= Dm || col >= Dn) continue;
     const int nv = min(V::VE, Dn - col);
-    const long long xi = (long long)r * (par ? Dldx : D.ldx0) + col, qi = (long long)r * Dldq + col;
+    const long long xi = (long long)r * (src ? Dldx : D.ldx0) + col, qi = (long long)r * Dldq + col;
     const long long yi = (long long)r * Dldx + col;
     if (DQ) {
       V x;

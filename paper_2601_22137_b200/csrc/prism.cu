@@ -138,6 +138,7 @@ struct Plan {
   SolveParams params{};
   LaunchDesc gram[2], square, square2, apply[2], chaint[5];
   LaunchDesc gram0, apply0;   // folded normalisation: iteration 0 reads A (scaled by 1/c) instead of X_0
+  LaunchDesc apply0f;         // ... and writes X_1 into Q (matrices whose Q holds the odd iterates)
   bool fold = false;          // some matrix folds (iteration-0 tables present)
   bool unfolded = true;       // some matrix needs k_normalize
   // row-block split: packed partial-Gram launches per panel group, the
@@ -332,6 +333,21 @@ prism_status build_plan(const Request& r, Plan& P) {
   }
   P.fold = fold;
   P.unfolded = unfolded;
+  // Q may take the odd iterates (iteration 0's apply writes X_1 there while the same launch
+  // still reads the inputs) only when it overlaps no input of the batch
+  auto span = [&](const void* p, long long ld, int i) {
+    const uintptr_t b = (uintptr_t)p;
+    return std::make_pair(b, b + (uintptr_t)(((long long)(r.m[i] - 1) * ld + r.n[i]) * esz));
+  };
+  auto flip_ok = [&](int i) {
+    if (!fold_ok(i)) return false;
+    const auto q = span(r.Q[i], r.ldq[i], i);
+    for (int j = 0; j < B; ++j) {
+      const auto a = span(r.A[j], r.lda[j], j);
+      if (a.first < q.second && q.first < a.second) return false;
+    }
+    return true;
+  };
   for (int i = 0; i < B; ++i) {
     MatDesc& D = mats[i];
     std::memset(&D, 0, sizeof(D));
@@ -364,6 +380,7 @@ prism_status build_plan(const Request& r, Plan& P) {
       }
     }
     D.fold = fold_ok(i) ? 1 : 0;
+    D.flip_ok = flip_ok(i) ? 1 : 0;
     if (D.fold) {
       D.X[0] = r.Q[i];
       D.ldx0 = r.ldq[i];
@@ -599,13 +616,16 @@ prism_status build_plan(const Request& r, Plan& P) {
       // operands MN-major, X' = X + X P (A = X K-major, B = P K-major by symmetry).
       // Wide (m < n): G = X X^T (both K-major), X' = X + P X (B = X MN-major).
       const bool tall = m >= n;
-      // t = 0, 1: X[t] -> X[1-t]; t = 2 (folded plans): iteration 0, A (lda) -> X[1] with 1/c
-      for (int t = 0; t < (fold ? 3 : 2); ++t) {
-        const bool from_a = t == 2 && D.fold;   // iteration 0 of a folded matrix: A, scaled by 1/c
-        const void* Xi = from_a ? r.A[i] : D.X[t & 1 ? 1 : 0];
-        const void* Xil = from_a ? nullptr : D.X_lo[t & 1 ? 1 : 0];
-        const long long ldi = from_a ? r.lda[i] : ldxs[t & 1 ? 1 : 0];
-        const int to = t < 2 ? 1 - t : 1;
+      // t = 0, 1: X[t] -> X[1-t]; t = 2 (folded plans): iteration 0, A (lda) -> X[1] with 1/c;
+      // t = 3: iteration 0's apply writing X_1 into Q = X[0] (flipped parity, MatState.flip)
+      for (int t = 0; t < (fold ? 4 : 2); ++t) {
+        const bool from_a = t >= 2 && D.fold;   // iteration 0 of a folded matrix: A, scaled by 1/c
+        const int src = t == 1 ? 1 : 0;
+        const void* Xi = from_a ? r.A[i] : D.X[src];
+        const void* Xil = from_a ? nullptr : D.X_lo[src];
+        const long long ldi = from_a ? r.lda[i] : ldxs[src];
+        const int to = t < 2 ? 1 - t : (t == 3 && D.flip_ok) ? 0 : 1;
+        if (t < 3) {
         HostProblem g = mk(s, s, L, EPI_RESID, 1, D.R, D.R_lo, ldr, nullptr, nullptr, 0);
         g.p.norm_part = D.norm_part;
         g.p.gdiag = D.gdiag;
@@ -623,6 +643,7 @@ prism_status build_plan(const Request& r, Plan& P) {
           g.p.eA = 1;
         }
         (t < 2 ? P.gram[t] : P.gram0).probs.push_back(g);
+        }
         const void* Pa = d == 2 ? Pm : D.R;
         const void* Pa_lo = d == 2 ? Pm_lo : D.R_lo;
         HostProblem a = mk(m, n, s, EPI_APPLY, 0, D.X[to], D.X_lo[to], ldxs[to], Xi, Xil, ldi);
@@ -641,7 +662,7 @@ prism_status build_plan(const Request& r, Plan& P) {
           a.p.alpha = &d_st[i].inv_c;
           a.p.eA = a.p.eC = 1;
         }
-        (t < 2 ? P.apply[t] : P.apply0).probs.push_back(a);
+        (t < 2 ? P.apply[t] : t == 2 ? P.apply0 : P.apply0f).probs.push_back(a);
       }
       if (d == 2) {
         HostProblem q = mk(s, s, s, EPI_POLY, 1, Pm, Pm_lo, ldr, D.R, D.R_lo, ldr);
@@ -860,9 +881,13 @@ prism_status build_plan(const Request& r, Plan& P) {
   off = align_up(off, 128);
   const size_t tmat_off = off;   // layout tile -> matrix (normalise / finalise: no search)
   off += sizeof(int) * (size_t)toff[B];
+  off = align_up(off, 128);
+  const size_t parity_off = off;   // [B] final parity of each matrix's last solve (k_finalize),
+  off += 2 * sizeof(int) * (size_t)B;   // [B] the parity the ping-pong tables currently hold
   std::vector<LaunchDesc*> all = {&P.gram[0],   &P.gram[1],   &P.apply[0],  &P.apply[1],  &P.square,
                                   &P.chaint[0], &P.chaint[1], &P.chaint[2], &P.chaint[3], &P.chaint[4],
-                                  &P.square2, &P.rb1[0], &P.rb1[1], &P.gram0, &P.apply0};
+                                  &P.square2, &P.rb1[0], &P.rb1[1], &P.gram0, &P.apply0,
+                                  &P.apply0f};
   for (int t = 0; t < 2; ++t)
     for (LaunchDesc& L : P.rbgram[t]) all.push_back(&L);
   for (LaunchDesc& L : P.gjT) all.push_back(&L);
@@ -894,6 +919,10 @@ prism_status build_plan(const Request& r, Plan& P) {
   std::memcpy(blob + toff_off, toff.data(), sizeof(int) * (B + 1));
   std::memcpy(blob + ooff_off, ooff.data(), sizeof(int) * (B + 1));
   std::memcpy(blob + foff_off, foff.data(), sizeof(int) * (B + 1));
+  {
+    int* par = reinterpret_cast<int*>(blob + parity_off);   // first solve: Q takes the odd iterates
+    for (int i = 0; i < B; ++i) par[i] = 1, par[B + i] = 0;
+  }
   {
     int* tm = reinterpret_cast<int*>(blob + tmat_off);
     for (int i = 0; i < B; ++i)
@@ -931,6 +960,17 @@ prism_status build_plan(const Request& r, Plan& P) {
   S.tile_off = reinterpret_cast<const int*>(meta_dev + toff_off);
   S.tile_mat = reinterpret_cast<const int*>(meta_dev + tmat_off);
   S.out_tile_off = reinterpret_cast<const int*>(meta_dev + ooff_off);
+  // folded polar: k_init_state swaps a matrix's entries of the ping-pong tables (entry b of
+  // each is matrix b) when the parity it predicts for Q differs from the tables' current one
+  S.parity = P.fold ? reinterpret_cast<int*>(meta_dev + parity_off) : nullptr;
+  S.flip_cur = P.fold ? reinterpret_cast<int*>(meta_dev + parity_off) + B : nullptr;
+  if (P.fold) {
+    const LaunchDesc* tabs[6] = {&P.gram[0], &P.gram[1], &P.apply[0], &P.apply[1], &P.apply0, &P.apply0f};
+    for (int j = 0; j < 6; ++j) {
+      if ((int)tabs[j]->probs.size() != B) return fail(PRISM_ERR_INTERNAL, "parity tables: one entry per matrix");
+      S.flip_tab[j] = reinterpret_cast<GemmProblem*>(meta_dev + tabs[j]->probs_off);
+    }
+  }
   S.fro_off = reinterpret_cast<const int*>(meta_dev + foff_off);
   S.n_fro_blocks = foff[B];
   S.n_tiles = toff[B];

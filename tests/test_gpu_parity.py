@@ -381,3 +381,42 @@ def test_sqrt_divergence_status_and_residual_history():
     torch.cuda.synchronize()
     assert int(rep["status"][0]) == prism.DIVERGED and int(rep["iters"][0]) == 9
     np.testing.assert_allclose(rep["resid_hist"][0, :10].double().cpu().numpy(), hist, rtol=1e-3)
+
+
+@pytest.mark.gpu
+def test_folded_parity_flip_across_solves():
+    """Folded BF16 polar: the caller's Q holds the even iterates on a plan's first solve and,
+    per matrix, the odd ones once a solve ended after an odd number of updates (k_init_state
+    flips the ping-pong tables).  Repeats, flips back and mispredictions (new
+    values in the same buffers) must all give the bits of a fresh solve."""
+    shapes = [(300, 200), (200, 520), (768, 768), (130, 66), (256, 640)]
+    mats = [torch.tensor(W.gaussian(m, n, seed=70 + i)).to(torch.bfloat16).cuda() for i, (m, n) in enumerate(shapes)]
+    outs = [torch.empty_like(t) for t in mats]
+    kw = dict(degree=5, tol=3e-2, max_iters=20, precision="bf16", matrix_ids=list(range(len(shapes))))
+    h = P.Handle()
+
+    def fresh():
+        Q, rep = P.polar(mats, handle=P.Handle(), **kw)
+        torch.cuda.synchronize()
+        return [q.clone() for q in Q], rep["iters"].cpu().tolist()
+
+    seen = set()
+    for spectrum in range(3):
+        if spectrum:
+            for i, t in enumerate(mats):   # new values in the same buffers: the same plan, other counts
+                m, n = shapes[i]
+                a = W.logspaced(m, n, 10.0 ** (-2 * spectrum), seed=170 + 10 * spectrum + i)
+                t.copy_(torch.tensor(a).to(torch.bfloat16))
+        ref, iters = fresh()
+        seen |= {k & 1 for k in iters}
+        for _ in range(3):
+            Q, rep = P.polar(mats, out=outs, handle=h, **kw)
+            torch.cuda.synchronize()
+            assert rep["iters"].cpu().tolist() == iters
+            for q, r in zip(Q, ref):
+                assert torch.equal(q, r)
+        if spectrum == 0:   # Gaussian inputs: the oracle agrees (bf16 bar of the GPT-2 shapes)
+            for i in (1, 2):
+                Qo, _ = prism.polar(mats[i].double().cpu().numpy(), d=2, p=8, tol=3e-2, max_iters=20, seed=42, b=i)
+                assert _rel(outs[i].double().cpu().numpy(), Qo) <= 2e-2
+    assert seen == {0, 1}
