@@ -110,8 +110,11 @@ int prism_abi_version(void);
 
 /*
  * Polar factor.  For matrix i of the batch: A_i is m[i] x n[i] (row-major, lda[i]),
- * Q_i receives U V^T with the same shape (ldq[i]; Q may alias A).  Wide inputs
- * (m < n) are handled as A^T (P:456 assumes m >= n; R14).
+ * Q_i receives U V^T with the same shape (ldq[i]; Q_i may alias A_i exactly; no other
+ * overlap of an output with an input of the batch is allowed).  BF16 / TF32 solves use Q_i
+ * as one of the two iterate buffers, so it holds intermediate values
+ * until the call's work on `stream` completes.  Wide inputs (m < n) are handled as A^T
+ * (P:456 assumes m >= n; R14).
  * matrix_ids: optional HOST array of global matrix indices used as the sketch
  * stream id (so a batch split across GPUs draws the same S_k); NULL -> 0..batch-1.
  * Workspace: at least prism_polar_workspace(...) bytes of device memory, 256-B aligned.
