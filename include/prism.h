@@ -413,7 +413,8 @@ prism_status prism_debug_guards_fill(prism_handle h, void* stream);
 prism_status prism_debug_guards_check(prism_handle h, int64_t* bad_bytes, int64_t* guards, void* stream);
 /* Positive control of the checker: clears the first byte of guard band idx of the last plan. */
 prism_status prism_debug_guards_poke(prism_handle h, int64_t idx, void* stream);
-/* Diagnostics: persistent-grid cap (CTAs) of the next prism_debug_gemm launches (0: all SMs). */
+/* Diagnostics: persistent-grid cap (CTAs) of prism_debug_gemm launches and of the GEMMs of
+ * solve plans built afterwards (0: all SMs; the row-block pipelined Gram keeps its own cap). */
 prism_status prism_debug_gemm_max_ctas(int max_ctas);
 /* Sketch-chain timeline hook: buf_dev (16 iterations x 32 pass codes x 160 CTAs x 32 u64,
  * zeroed by the caller) receives per CTA globaltimer ns at entry, after the PDL wait, when the

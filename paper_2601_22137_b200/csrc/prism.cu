@@ -1006,6 +1006,8 @@ int chain_pass(const Plan& P, int j) {
   return P.chaint[j].probs.empty() ? CH2_P1 : P.chaint[j].probs[0].p.pass;
 }
 
+static int g_debug_gemm_max_ctas = 0;   // prism_debug_gemm_max_ctas: persistent GEMM grids capped
+
 GemmLaunch make_launch(const Plan& P, const LaunchDesc& L, const LaunchDesc* odd, char* ws, int lo, int hi,
                        const LaunchDesc* k0 = nullptr) {
   GemmLaunch g{};
@@ -1028,6 +1030,7 @@ GemmLaunch make_launch(const Plan& P, const LaunchDesc& L, const LaunchDesc* odd
   g.iter = P.params.iter;
   g.iter_lo = lo;
   g.iter_hi = hi;
+  if (!chain) g.max_ctas = g_debug_gemm_max_ctas;
   return g;
 }
 
@@ -2095,7 +2098,6 @@ double prism_sqrt_flops_per_iter(int64_t n, int degree, int sketch_size) {
   return f;
 }
 
-static int g_debug_gemm_max_ctas = 0;
 prism_status prism_debug_gemm_max_ctas(int max_ctas) {
   g_debug_gemm_max_ctas = max_ctas < 0 ? 0 : max_ctas;
   return PRISM_OK;
