@@ -416,6 +416,9 @@ prism_status prism_debug_guards_poke(prism_handle h, int64_t idx, void* stream);
 /* Diagnostics: persistent-grid cap (CTAs) of prism_debug_gemm launches and of the GEMMs of
  * solve plans built afterwards (0: all SMs; the row-block pipelined Gram keeps its own cap). */
 prism_status prism_debug_gemm_max_ctas(int max_ctas);
+/* Diagnostics: GEMM tile order of plans built afterwards — within a matrix, groups of `rows`
+ * tile rows walked column by column (default 8; 1: row-major).  Never changes results. */
+prism_status prism_debug_raster_rows(int rows);
 /* Sketch-chain timeline hook: buf_dev (16 iterations x 32 pass codes x 160 CTAs x 32 u64,
  * zeroed by the caller) receives per CTA globaltimer ns at entry, after the PDL wait, when the
  * first tile's accumulator is ready, when its epilogue ends, and the epilogue's inner marks

@@ -149,6 +149,7 @@ _SIGS = {
     "prism_debug_trace_gemm": (_ST, [_vp, _i32]),
     "prism_debug_trace_chain": (_ST, [_vp]),
     "prism_debug_gemm_max_ctas": (_ST, [_i32]),
+    "prism_debug_raster_rows": (_ST, [_i32]),
     "prism_debug_workspace_guards": (_ST, [_i32]),
     "prism_debug_guards_fill": (_ST, [_vp, _vp]),
     "prism_debug_guards_check": (_ST, [_vp, _i64p, _i64p, _vp]),

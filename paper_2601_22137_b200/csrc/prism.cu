@@ -247,10 +247,28 @@ int chain_ks(int s) {   // clusters of 8 do not all co-schedule
   return s < 1024 ? 1 : s < 2048 ? 2 : 4;
 }
 
-void sort_tiles_by_cost(LaunchDesc& L) {
+// GEMM tile order within a matrix: groups of 8 tile rows walked column by column, so that a
+// wave of 74 pair tiles reads ~8 A and ~9 B panels instead of ~2 and all of them: matrices
+// larger than L2 re-read fewer operand panels from HBM (8192^2 polar 23.6-25.3 -> 22.7-23.0 ms;
+// smaller ones unchanged; scripts/probe_raster.py).  prism_debug_raster_rows overrides it.
+static uint32_t g_raster_rows = 8;
+void sort_tiles_by_cost(LaunchDesc& L, bool raster = false) {
   std::stable_sort(L.tiles.begin(), L.tiles.end(), [&](uint32_t a, uint32_t b) {
     return L.probs[a >> 20].p.K > L.probs[b >> 20].p.K;
   });
+  if (!raster || g_raster_rows <= 1) return;
+  size_t i = 0;
+  while (i < L.tiles.size()) {
+    size_t j = i;
+    while (j < L.tiles.size() && (L.tiles[j] >> 20) == (L.tiles[i] >> 20)) ++j;
+    std::stable_sort(L.tiles.begin() + i, L.tiles.begin() + j, [&](uint32_t a, uint32_t b) {
+      const uint32_t ga = ((a >> 10) & 1023) / g_raster_rows, gb = ((b >> 10) & 1023) / g_raster_rows;
+      if (ga != gb) return ga < gb;
+      if ((a & 1023) != (b & 1023)) return (a & 1023) < (b & 1023);
+      return ((a >> 10) & 1023) < ((b >> 10) & 1023);
+    });
+    i = j;
+  }
 }
 
 // Packed upper-triangle layout of the row-block Gram (gemm.cuh epi_gram32): panel t = rows
@@ -770,7 +788,7 @@ prism_status build_plan(const Request& r, Plan& P) {
     L.tiles.clear();
     for (int j = 0; j < (int)L.probs.size(); ++j)
       add_tiles(L, j, L.probs[j].p.M, L.probs[j].p.N, BN, L.probs[j].p.sym != 0);
-    sort_tiles_by_cost(L);
+    sort_tiles_by_cost(L, true);
     // bf16 applies: the last, partial wave of the persistent launch (tiles t >= R - R % pairs
     // run one per CTA pair while the other pairs idle) is split in N into BN/2-column tiles,
     // so it takes about half a tile time (4096^2: 34 of 256 tiles -> 68 half tiles on 74 pairs).
@@ -2096,6 +2114,11 @@ double prism_sqrt_flops_per_iter(int64_t n, int degree, int sketch_size) {
   if (degree == 5) f += 2.0 * x * x * x + 14.0 * x * x * p;
   else f += 6.0 * x * x * p;
   return f;
+}
+
+prism_status prism_debug_raster_rows(int rows) {
+  g_raster_rows = rows < 1 ? 1u : (uint32_t)rows;
+  return PRISM_OK;
 }
 
 prism_status prism_debug_gemm_max_ctas(int max_ctas) {
