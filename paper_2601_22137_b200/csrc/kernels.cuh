@@ -1099,8 +1099,9 @@ __device__ int real_roots_cubic(double a3, double a2, double a1, double a0, doub
 // Interval argmin of the quartic m(a) = sum c_i a^i on [lo, hi] (readings R15, R16):
 // the roots of m'' (a quadratic: one sqrt) split [lo, hi] into at most three pieces on
 // which m' is monotone; a piece whose ends have m' < 0 <= m' holds exactly one local
-// minimum of m, located by Newton steps safeguarded by bisection (the bracket keeps
-// m'(x0) < 0 <= m'(x1), so the limit is that minimum to the last bits).  Candidates
+// minimum of m, bracketed to 1/32 of the piece by the warp's 32 samples of m', then located
+// by Newton steps safeguarded by bisection (the bracket keeps m'(x0) < 0 <= m'(x1), so the
+// limit is that minimum to the last bits).  Warp-collective: every lane passes the same c.  Candidates
 // {lo, hi} U minima, the smallest m wins (ties -> smaller a); degenerate loss -> Taylor.
 // (The closed-form Cardano roots this replaces lost the moderate roots when |c4| << |c3|
 // and missed minima; its fp64 acos / cos / cbrt also cost 9-13 us inside k_alpha.)
@@ -1140,9 +1141,21 @@ __device__ double argmin_quartic(const double c[5], double lo, double hi, double
     const double mh = m(hi);
     if (mh < bm) { best = hi; bm = mh; }
   }
+  const int lane = threadIdx.x & 31;
   for (int j = 0; j + 1 < nb; ++j) {
     double x0 = br[j], x1 = br[j + 1];
     if (!(mp(x0) < 0.0 && mp(x1) >= 0.0)) continue;
+    {
+      // m' increases through the piece: the warp samples it at 32 points and the first
+      // lane with m' >= 0 narrows the bracket 32-fold, so Newton starts next to the root
+      const double xl = lane == 31 ? x1 : x0 + (x1 - x0) * (double)(lane + 1) * (1.0 / 32.0);
+      const unsigned pos = __ballot_sync(0xffffffffu, mp(xl) >= 0.0) | 0x80000000u;
+      const int f = __ffs(pos) - 1;
+      const double b1 = __shfl_sync(0xffffffffu, xl, f);
+      const double b0 = __shfl_sync(0xffffffffu, xl, f > 0 ? f - 1 : 0);
+      if (f > 0) x0 = b0;
+      x1 = b1;
+    }
     double x = 0.5 * (x0 + x1);
     for (int it = 0; it < 100; ++it) {
       const double f = mp(x);

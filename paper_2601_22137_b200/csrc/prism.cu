@@ -1522,8 +1522,10 @@ __global__ void k_sketch_debug(unsigned long long seed, int b, int k, int p, int
   if (2 * e + 1 < total) S[2 * e + 1] = __double2float_rn(z1);
 }
 __global__ void k_argmin_debug(int n, const double* c, double lo, double hi, double aT, double* out) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = argmin_quartic(c + 5 * i, lo, hi, aT);
+  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);   // one warp per quartic
+  if (i >= n) return;
+  const double a = argmin_quartic(c + 5 * i, lo, hi, aT);
+  if ((threadIdx.x & 31) == 0) out[i] = a;
 }
 }  // namespace prism
 
@@ -2269,7 +2271,7 @@ prism_status prism_debug_sketch(uint64_t seed, int64_t b, int k, int p, int s, f
 prism_status prism_debug_argmin(int n, const double* c_dev, double lo, double hi, double a_taylor,
                                 double* alpha_dev, void* stream) {
   if (n < 1 || !c_dev || !alpha_dev) return fail(PRISM_ERR_INVALID_ARG, "bad argmin args");
-  k_argmin_debug<<<(n + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(n, c_dev, lo, hi, a_taylor,
+  k_argmin_debug<<<(n + 3) / 4, 128, 0, static_cast<cudaStream_t>(stream)>>>(n, c_dev, lo, hi, a_taylor,
                                                                                  alpha_dev);
   PRISM_CK(cudaGetLastError());
   return PRISM_OK;
