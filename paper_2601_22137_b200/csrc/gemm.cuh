@@ -175,6 +175,11 @@ struct GemmLaunch {
   const GemmProblem* probs_odd;  // problem table for odd iterations (ping-pong buffers) or null
   const GemmProblem* probs_k0;   // problem table of iteration 0 (folded normalisation) or null
   const uint32_t* tiles;         // (problem << 20) | (tm << 10) | tn
+  // per-iteration compacted tile list (tiles of matrices still active, plan order; written by
+  // k_alpha's last block) and its length, used from iteration c_from on; null: `tiles` only
+  const uint32_t* ctiles;
+  const int* ccount;
+  int c_from;
   const int* done;               // per matrix (stride done_stride ints): 1 = stopped, skip its tiles
   const int* iter;               // device iteration counter k (or null): run only if iter_lo <= k < iter_hi
   int done_stride;
@@ -1184,6 +1189,15 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
     if (L.probs_odd && (k & 1)) probs = L.probs_odd;
     if (L.probs_k0 && k == 0) probs = L.probs_k0;
   }
+  // this iteration's tile list: the compacted one once it exists (read after the wait)
+  const uint32_t* __restrict__ tiles = L.tiles;
+  int ntiles = L.ntiles;
+  if constexpr (Cfg::KIND == 0) {   // bf16 plans only (prism.cu)
+    if (L.ctiles && !L.early && L.iter && kcur >= L.c_from) {
+      tiles = L.ctiles;
+      ntiles = *L.ccount;
+    }
+  }
   // tiles of stopped matrices are skipped (the same decision in every role)
   auto skip_tile = [&](int matrix) -> bool {
     if (!L.done) return false;
@@ -1200,8 +1214,8 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = cid; t < L.ntiles; t += ncl) {
-        const uint32_t code = L.tiles[t];
+      for (int t = cid; t < ntiles; t += ncl) {
+        const uint32_t code = tiles[t];
         const GemmProblem& P = probs[code >> 20];
         if (skip_tile(P.matrix)) continue;
         const int tm = (code >> 10) & 1023;
@@ -1246,8 +1260,8 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
       int acc = 0;
       uint32_t acc_phase = 0;
       int tcount = 0;
-      for (int t = cid; t < L.ntiles; t += ncl) {
-        const uint32_t code = L.tiles[t];
+      for (int t = cid; t < ntiles; t += ncl) {
+        const uint32_t code = tiles[t];
         const GemmProblem& P = probs[code >> 20];
         if (skip_tile(P.matrix)) continue;
         const bool half = (code & kHalfTile) != 0;
@@ -1317,8 +1331,8 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
         else mbar_arrive(bar);
       }
     };
-    for (int t = cid; t < L.ntiles; t += ncl) {
-      const uint32_t code = L.tiles[t];
+    for (int t = cid; t < ntiles; t += ncl) {
+      const uint32_t code = tiles[t];
       const GemmProblem& P = probs[code >> 20];
       if (skip_tile(P.matrix)) continue;
       const int tm = (code >> 10) & 1023;

@@ -50,6 +50,17 @@ struct MatDesc {
   double* dbpart;
 };
 
+// Tile list compacted per iteration to the matrices still active (plan order kept): the plan
+// describes the list as runs of consecutive tiles of one matrix (start, length, matrix).
+struct CompactList {
+  const int* runs;        // [nruns][3] (plan constants)
+  int nruns;
+  const uint32_t* src;    // the launch's full tile list
+  uint32_t* dst;          // compacted list (plan memory)
+  int* count;             // its length
+};
+constexpr int kMaxCompactRuns = 1024;
+
 struct SolveParams {
   MatDesc* mats;
   MatState* st;
@@ -78,6 +89,9 @@ struct SolveParams {
   // folded polar: the tables whose entry b (matrix b) is swapped to flip matrix b's parity:
   // gram[0] <-> gram[1], apply[0] <-> apply[1], apply0 <-> apply0f
   GemmProblem* flip_tab[6];
+  // tile lists of the Gram / square / apply launches compacted by k_alpha's last block
+  int ncompact;
+  CompactList clist[3];
   double tol, alo, ahi, ataylor;
   unsigned long long seed;
 };
@@ -1271,10 +1285,78 @@ __device__ double argmin_quartic_free(const double c[5], double a_default) {
 // not B (a block on an SM keeps a GEMM CTA — which needs the whole register file — off it;
 // the early square GEMM runs its mainloop on the others, prism.cu).
 constexpr int kAlphaWarps = 8;
+
+// k_alpha's extra blocks (kCompactBlocks, after the fit blocks): after this iteration's stop
+// test (several launches back), the square and apply of this iteration and the next Gram
+// need only the tiles of matrices still active; each list keeps its plan order with the runs
+// of stopped matrices dropped, and the GEMMs stride over the active tiles alone (tail
+// iterations: no pair holds several of the few remaining tiles while others idle).  Any
+// order computes the same bits (per-element arithmetic never depends on the tile schedule).
+// Every block derives the run prefix sums (runs in shared memory), then writes its share of
+// the compacted lists, each element found by a binary search over the run prefixes.
+constexpr int kCompactBlocks = 8;
+__device__ void compact_tile_lists(const SolveParams& P, int cb) {
+  __shared__ int s_pre[3][kMaxCompactRuns + 1];   // prefix of the active lengths (inactive: 0)
+  __shared__ int s_src[3][kMaxCompactRuns];       // first source index of each run
+  const int T = blockDim.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = T >> 5;
+  const int nl = P.ncompact;
+  int tot = 0;
+  for (int l = 0; l < nl; ++l) tot += P.clist[l].nruns;
+  // run lengths (0 for stopped matrices) and starts, all lists at once
+  for (int x = threadIdx.x; x < tot; x += T) {
+    int l = 0, r = x;
+    while (r >= P.clist[l].nruns) r -= P.clist[l].nruns, ++l;
+    const int* run = P.clist[l].runs + 3 * r;
+    const int st = run[0], len = run[1], mat = run[2];
+    s_src[l][r] = st;
+    s_pre[l][r + 1] = P.st[mat].done ? 0 : len;
+  }
+  __syncthreads();
+  for (int l = warp; l < nl; l += nw) {   // one warp per list: in-place inclusive scan
+    const int n = P.clist[l].nruns;
+    int carry = 0;
+    if (lane == 0) s_pre[l][0] = 0;
+    for (int r0 = 0; r0 < n; r0 += 32) {
+      const int r = r0 + lane;
+      int v = r < n ? s_pre[l][r + 1] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
+      }
+      if (r < n) s_pre[l][r + 1] = carry + v;
+      carry += __shfl_sync(0xffffffffu, v, 31);
+    }
+  }
+  __syncthreads();
+  for (int l = 0; l < nl; ++l) {
+    const CompactList& C = P.clist[l];
+    const int n = C.nruns, total = s_pre[l][n];
+    const int per = (total + kCompactBlocks - 1) / kCompactBlocks;
+    const int lo = cb * per, hi = min(total, lo + per);
+    for (int d = lo + threadIdx.x; d < hi; d += T) {
+      int a = 0, b = n;   // last run r with s_pre[r] <= d (zero-length runs precede their successor)
+      while (b - a > 1) {
+        const int m = (a + b) >> 1;
+        if (s_pre[l][m] <= d) a = m; else b = m;
+      }
+      C.dst[d] = C.src[s_src[l][a] + d - s_pre[l][a]];
+    }
+    if (cb == 0 && threadIdx.x == 0) *C.count = total;
+  }
+}
+
 template <int AK>
 __global__ void __launch_bounds__(32 * kAlphaWarps) k_alpha(SolveParams P, int) {
   griddep_wait();
   griddep_launch();
+  if constexpr (AK != 3) {
+    const int cb = (int)blockIdx.x - (int)(gridDim.x - (P.ncompact ? kCompactBlocks : 0));
+    if (cb >= 0) {
+      compact_tile_lists(P, cb);
+      return;
+    }
+  }
   const int k = *P.iter;
   const int do_fit = AK == 3 ? (P.fit != 1 && k < P.max_iters && k >= P.warmup) : (fit_at(P, k) ? 1 : 0);
   const int lane = threadIdx.x & 31;

@@ -139,6 +139,14 @@ struct Plan {
   LaunchDesc gram[2], square, square2, apply[2], chaint[5];
   LaunchDesc gram0, apply0;   // folded normalisation: iteration 0 reads A (scaled by 1/c) instead of X_0
   LaunchDesc apply0f;         // ... and writes X_1 into Q (matrices whose Q holds the odd iterates)
+  bool square_early = false;  // the square GEMM's mainloop runs under k_alpha (run_solve)
+  // per-iteration compacted tile lists (k_alpha's last block): 0 Gram, 1 square, 2 apply
+  struct Compact {
+    bool on = false;
+    int c_from = 0;
+    std::vector<int> runs;   // (start, length, matrix) per run of one matrix's tiles
+    size_t runs_off = 0, dst_off = 0, count_off = 0;
+  } compact[3];
   bool fold = false;          // some matrix folds (iteration-0 tables present)
   bool unfolded = true;       // some matrix needs k_normalize
   // row-block split: packed partial-Gram launches per panel group, the
@@ -874,6 +882,30 @@ prism_status build_plan(const Request& r, Plan& P) {
     sort_tiles_by_cost(T);
   }
   if ((int)P.apply[0].probs.size() >= 4096) return fail(PRISM_ERR_UNSUPPORTED, "batch too large (max 2047 sqrt / 4095 polar)");
+  // the square GEMM of bf16 polar batches <= 16 runs its mainloop under k_alpha (it reads
+  // its tile list before the wait, so it keeps the full list); see run_solve
+  P.square_early = !r.sqrt_kind && !r.sign_kind && !cheb && !iq && !db && !r.rowblock && prec == PRISM_BF16 && B <= 16;
+  {
+    const LaunchDesc* cl[3] = {&P.gram[0], &P.square, &P.apply[0]};
+    const bool want[3] = {!r.rowblock && !db && !iq, P.has_square && !P.square_early && !r.rowblock && !db,
+                          !r.rowblock && !db};
+    for (int l = 0; l < 3; ++l) {
+      Plan::Compact& C = P.compact[l];
+      C = Plan::Compact{};
+      if (!want[l] || prec != PRISM_BF16 || cl[l]->tiles.empty()) continue;   // (the tf32 GEMMs would spill)
+      const std::vector<uint32_t>& T = cl[l]->tiles;
+      for (size_t t = 0; t < T.size();) {
+        size_t u = t;
+        while (u < T.size() && (T[u] >> 20) == (T[t] >> 20)) ++u;
+        C.runs.push_back((int)t);
+        C.runs.push_back((int)(u - t));
+        C.runs.push_back(cl[l]->probs[T[t] >> 20].p.matrix);
+        t = u;
+      }
+      C.on = (int)C.runs.size() / 3 <= kMaxCompactRuns;
+      C.c_from = l == 0 ? 1 : 0;   // iteration 0's Gram runs before any stop test
+    }
+  }
 
   // flat 64x64 tile prefixes for the layout kernels (normalise over Xt, finalise over the output)
   std::vector<int> toff(B + 1, 0), ooff(B + 1, 0), foff(B + 1, 0);
@@ -902,6 +934,20 @@ prism_status build_plan(const Request& r, Plan& P) {
   off = align_up(off, 128);
   const size_t parity_off = off;   // [B] final parity of each matrix's last solve (k_finalize),
   off += 2 * sizeof(int) * (size_t)B;   // [B] the parity the ping-pong tables currently hold
+  const LaunchDesc* clists[3] = {&P.gram[0], &P.square, &P.apply[0]};
+  for (int l = 0; l < 3; ++l) {
+    Plan::Compact& C = P.compact[l];
+    if (!C.on) continue;
+    off = align_up(off, 128);
+    C.runs_off = off;
+    off += sizeof(int) * C.runs.size();
+    off = align_up(off, 128);
+    C.dst_off = off;
+    off += sizeof(uint32_t) * clists[l]->tiles.size();
+    off = align_up(off, 128);
+    C.count_off = off;
+    off += sizeof(int);
+  }
   std::vector<LaunchDesc*> all = {&P.gram[0],   &P.gram[1],   &P.apply[0],  &P.apply[1],  &P.square,
                                   &P.chaint[0], &P.chaint[1], &P.chaint[2], &P.chaint[3], &P.chaint[4],
                                   &P.square2, &P.rb1[0], &P.rb1[1], &P.gram0, &P.apply0,
@@ -937,6 +983,9 @@ prism_status build_plan(const Request& r, Plan& P) {
   std::memcpy(blob + toff_off, toff.data(), sizeof(int) * (B + 1));
   std::memcpy(blob + ooff_off, ooff.data(), sizeof(int) * (B + 1));
   std::memcpy(blob + foff_off, foff.data(), sizeof(int) * (B + 1));
+  for (int l = 0; l < 3; ++l)
+    if (P.compact[l].on)
+      std::memcpy(blob + P.compact[l].runs_off, P.compact[l].runs.data(), sizeof(int) * P.compact[l].runs.size());
   {
     int* par = reinterpret_cast<int*>(blob + parity_off);   // first solve: Q takes the odd iterates
     for (int i = 0; i < B; ++i) par[i] = 1, par[B + i] = 0;
@@ -988,6 +1037,17 @@ prism_status build_plan(const Request& r, Plan& P) {
       if ((int)tabs[j]->probs.size() != B) return fail(PRISM_ERR_INTERNAL, "parity tables: one entry per matrix");
       S.flip_tab[j] = reinterpret_cast<GemmProblem*>(meta_dev + tabs[j]->probs_off);
     }
+  }
+  S.ncompact = 0;
+  for (int l = 0; l < 3; ++l) {
+    const Plan::Compact& C = P.compact[l];
+    if (!C.on) continue;
+    CompactList& D = S.clist[S.ncompact++];
+    D.runs = reinterpret_cast<const int*>(meta_dev + C.runs_off);
+    D.nruns = (int)C.runs.size() / 3;
+    D.src = reinterpret_cast<const uint32_t*>(meta_dev + clists[l]->tiles_off);
+    D.dst = reinterpret_cast<uint32_t*>(meta_dev + C.dst_off);
+    D.count = reinterpret_cast<int*>(meta_dev + C.count_off);
   }
   S.fro_off = reinterpret_cast<const int*>(meta_dev + foff_off);
   S.n_fro_blocks = foff[B];
@@ -1338,8 +1398,8 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
   }
   PRISM_CK(cudaGetLastError());
   const int M = r.o.max_iters;
-  const GemmLaunch g_gram = make_launch(*P, P->gram[0], &P->gram[1], r.ws, 0, M + 1, P->fold ? &P->gram0 : nullptr);
-  const GemmLaunch g_apply = make_launch(*P, P->apply[0], &P->apply[1], r.ws, 0, M, P->fold ? &P->apply0 : nullptr);
+  GemmLaunch g_gram = make_launch(*P, P->gram[0], &P->gram[1], r.ws, 0, M + 1, P->fold ? &P->gram0 : nullptr);
+  GemmLaunch g_apply = make_launch(*P, P->apply[0], &P->apply[1], r.ws, 0, M, P->fold ? &P->apply0 : nullptr);
   GemmLaunch g_sq = make_launch(*P, P->square, nullptr, r.ws, 0, M);
   // the square GEMM reads R (written by the residual step, several launches back): its
   // mainloop can run while k_alpha finishes, only its epilogue waiting for alpha.
@@ -1351,10 +1411,23 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
   // batch 1 % slower) or the general square products of sign / Chebyshev (1-2 % slower).
   const bool polar_kind = !r.sqrt_kind && !r.sign_kind && !r.cheb_kind && !r.inv_q && !r.db_kind;
   // k_alpha: one warp per matrix, kAlphaWarps per block (it holds ceil(B / 8) SMs)
-  const dim3 alpha_grid((B + kAlphaWarps - 1) / kAlphaWarps), alpha_block(32 * std::min(B, kAlphaWarps));
+  const dim3 alpha_grid((B + kAlphaWarps - 1) / kAlphaWarps + (S.ncompact ? kCompactBlocks : 0)),
+      alpha_block(32 * std::min(B, kAlphaWarps));
   // (with k_alpha packed on ceil(B / 8) SMs and the square grid capped to leave them, the
   // GPT-2 batch measured the same step time: the early square stays at B <= 16)
-  if (polar_kind && prec == PRISM_BF16 && B <= 16) g_sq.early = 1;
+  if (P->square_early) g_sq.early = 1;
+  (void)polar_kind;
+  // per-iteration compacted tile lists (written by k_alpha's last block)
+  {
+    GemmLaunch* gl[3] = {&g_gram, &g_sq, &g_apply};
+    for (int l = 0; l < 3; ++l) {
+      const Plan::Compact& C = P->compact[l];
+      if (!C.on) continue;
+      gl[l]->ctiles = reinterpret_cast<const uint32_t*>(P->meta_dev + C.dst_off);
+      gl[l]->ccount = reinterpret_cast<const int*>(P->meta_dev + C.count_off);
+      gl[l]->c_from = C.c_from;
+    }
+  }
   const GemmLaunch g_sq2 = make_launch(*P, P->square2, nullptr, r.ws, 0, M);
   std::vector<GemmLaunch> g_gjT, g_gjS;
   for (int j = 0; j < P->db_steps; ++j) {
