@@ -176,7 +176,7 @@ struct GemmLaunch {
   const GemmProblem* probs_k0;   // problem table of iteration 0 (folded normalisation) or null
   const uint32_t* tiles;         // (problem << 20) | (tm << 10) | tn
   // per-iteration compacted tile list (tiles of matrices still active, plan order; written by
-  // k_alpha's last block) and its length, used from iteration c_from on; null: `tiles` only
+  // k_alpha's compaction blocks) and its length, used from iteration c_from on; null: `tiles` only
   const uint32_t* ctiles;
   const int* ccount;
   int c_from;

@@ -89,7 +89,7 @@ struct SolveParams {
   // folded polar: the tables whose entry b (matrix b) is swapped to flip matrix b's parity:
   // gram[0] <-> gram[1], apply[0] <-> apply[1], apply0 <-> apply0f
   GemmProblem* flip_tab[6];
-  // tile lists of the Gram / square / apply launches compacted by k_alpha's last block
+  // tile lists of the Gram / square / apply launches compacted by k_alpha's compaction blocks
   int ncompact;
   CompactList clist[3];
   double tol, alo, ahi, ataylor;

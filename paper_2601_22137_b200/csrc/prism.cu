@@ -140,7 +140,7 @@ struct Plan {
   LaunchDesc gram0, apply0;   // folded normalisation: iteration 0 reads A (scaled by 1/c) instead of X_0
   LaunchDesc apply0f;         // ... and writes X_1 into Q (matrices whose Q holds the odd iterates)
   bool square_early = false;  // the square GEMM's mainloop runs under k_alpha (run_solve)
-  // per-iteration compacted tile lists (k_alpha's last block): 0 Gram, 1 square, 2 apply
+  // per-iteration compacted tile lists (k_alpha's compaction blocks): 0 Gram, 1 square, 2 apply
   struct Compact {
     bool on = false;
     int c_from = 0;
@@ -1417,7 +1417,7 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
   // GPT-2 batch measured the same step time: the early square stays at B <= 16)
   if (P->square_early) g_sq.early = 1;
   (void)polar_kind;
-  // per-iteration compacted tile lists (written by k_alpha's last block)
+  // per-iteration compacted tile lists (written by k_alpha's compaction blocks)
   {
     GemmLaunch* gl[3] = {&g_gram, &g_sq, &g_apply};
     for (int l = 0; l < 3; ++l) {
