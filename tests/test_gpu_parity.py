@@ -420,3 +420,28 @@ def test_folded_parity_flip_across_solves():
                 Qo, _ = prism.polar(mats[i].double().cpu().numpy(), d=2, p=8, tol=3e-2, max_iters=20, seed=42, b=i)
                 assert _rel(outs[i].double().cpu().numpy(), Qo) <= 2e-2
     assert seen == {0, 1}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("B", [300, 1100])
+def test_large_bf16_batches_equal_single_solves(B):
+    """Large BF16 batches of small matrices with spread-out iteration counts: the per-iteration
+    tile compaction (k_alpha's compaction blocks; lists of more than 1024 runs keep the full
+    list) must not change any matrix's bits, iterations or status against its single solve."""
+    g = np.random.default_rng(B)
+    shapes = [(int(g.integers(16, 160)), int(g.integers(16, 160))) for _ in range(B)]
+    mats = []
+    for i, (m, n) in enumerate(shapes):   # a third ill-conditioned: more iterations, later stops
+        a = W.logspaced(m, n, 1e-3, seed=5000 + i) if i % 3 == 0 else W.gaussian(m, n, seed=5000 + i)
+        mats.append(torch.tensor(a).to(torch.bfloat16).cuda())
+    kw = dict(degree=5, tol=3e-2, max_iters=25, precision="bf16")
+    Qb, rb = P.polar(mats, matrix_ids=list(range(B)), **kw)
+    torch.cuda.synchronize()
+    iters = rb["iters"].cpu().tolist()
+    assert len(set(iters)) >= 3
+    assert all(int(s) == prism.CONVERGED for s in rb["status"].cpu().tolist())
+    for i in list(range(0, B, max(1, B // 12))) + [B - 1]:
+        Qs, rs = P.polar([mats[i]], matrix_ids=[i], **kw)
+        torch.cuda.synchronize()
+        assert torch.equal(Qs[0], Qb[i]), i
+        assert int(rs["iters"][0]) == iters[i]
