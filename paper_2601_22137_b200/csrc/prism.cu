@@ -892,7 +892,9 @@ prism_status build_plan(const Request& r, Plan& P) {
     for (int l = 0; l < 3; ++l) {
       Plan::Compact& C = P.compact[l];
       C = Plan::Compact{};
-      if (!want[l] || prec != PRISM_BF16 || cl[l]->tiles.empty()) continue;   // (the tf32 GEMMs would spill)
+      // bf16 only (the tf32 GEMMs would spill); batches of >= 8 matrices (a lone matrix gains
+      // nothing and k_alpha's extra blocks cost ~1.5 us per iteration: sign / Chebyshev 4096^2)
+      if (!want[l] || prec != PRISM_BF16 || B < 8 || cl[l]->tiles.empty()) continue;
       const std::vector<uint32_t>& T = cl[l]->tiles;
       for (size_t t = 0; t < T.size();) {
         size_t u = t;
