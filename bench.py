@@ -423,13 +423,16 @@ class Runner:
         return f(self.host, out=self.host_out, matrix_ids=self.ids, handle=self.h, **self.kw)
 
 
-def time_device(run, steps, warmup, flush, stream, dist_ctx=None):
+def time_device(run, steps, warmup, flush, stream, dist_ctx=None, before_timed=None):
     """W warm-up steps, then K steps bracketed by barrier + synchronize, each step timed by
-    CUDA events on the launching stream with the L2 flushed before it (outside the events)."""
+    CUDA events on the launching stream with the L2 flushed before it (outside the events).
+    `before_timed` runs once between the warm-up and the timed steps (launch-ledger reset)."""
     import torch
     for _ in range(warmup):
         run()
     torch.cuda.synchronize()
+    if before_timed is not None:
+        before_timed()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     if dist_ctx is not None:
         dist_ctx.barrier()
@@ -491,9 +494,9 @@ def single_gpu(P, name, shapes, mats_np, opts, kind, dev, steps, warmup, flush, 
     r = Runner(P, kind, mats_np, opts, dev)
     stream = torch.cuda.current_stream(dev)
     t_start = time.time()
-    ms, res = time_device(r.solve, steps, warmup, flush, stream)
+    ms, res = time_device(r.solve, steps, warmup, flush, stream, before_timed=r.h.launch_count)
     t_end = time.time()
-    launches = r.h.launch_count()
+    launches = r.h.launch_count()   # every library launch of the K timed steps (launch ledger)
     rep = res[-1]
     iters = rep["iters"].cpu().tolist()
     status = rep["status"].cpu().tolist()
@@ -501,7 +504,7 @@ def single_gpu(P, name, shapes, mats_np, opts, kind, dev, steps, warmup, flush, 
     flops_step = sum(f * k for f, k in zip(f_iter, iters))
     out = {"ms": ms, "ms_step": ms / steps, "value": r.B * steps / (ms / 1e3),
            "tflops": flops_step * steps / (ms / 1e3) / 1e12, "iters": iters, "status": status,
-           "launches_per_step": launches, "runner": r, "t_window": (t_start, t_end)}
+           "launches": launches, "runner": r, "t_window": (t_start, t_end)}
     if e2e:
         for _ in range(4):   # warm: every staging slot's buffers and plan
             r.solve_host()
@@ -633,14 +636,17 @@ def run_multi(args, rank, world, dev):
             return r
         h2d = d2h = sum(x.numel() * x.element_size() for x in host)
     t0 = time.time()
-    ms, res = time_device(run, args.steps, args.warmup, flush, stream, ctx)
+    ms, res = time_device(run, args.steps, args.warmup, flush, stream, ctx, before_timed=h.launch_count)
     t1 = time.time()
+    launches = h.launch_count()   # this rank's library launches in the timed steps
     e_ms, _ = time_device(run_e2e, args.steps, 3, flush, stream, ctx)
     rep = res[-1]
     iters = rep["iters"].cpu().tolist()
     t = torch.tensor([ms, e_ms], dtype=torch.float64, device=dev)
+    nl = torch.tensor([launches], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(nl, op=dist.ReduceOp.SUM)   # every rank's launches: the whole job
     ms_max, e_max = float(t[0]), float(t[1])
     f_iter = flops_per_iter(P, "sqrt" if kind == "sqrt" else "polar", shapes, opts)
     flops = sum(f * k for f, k in zip(f_iter, iters))
@@ -672,7 +678,7 @@ def run_multi(args, rank, world, dev):
             "clocks": clk,
             "e2e": {"value": units * args.steps / (e_max / 1e3), "unit": "solves/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
-            "gpu_launches": None,
+            "gpu_launches": int(nl[0]),
             "roofline": {"bound": "tensor", "achieved": tflops / world, "peak": peak, "unit": "TFLOP/s",
                          "frac": tflops / world / peak, "traffic": None,
                          "kernel": "whole step per GPU (multi-GPU run; per-kernel profile in the N=1 line)",
@@ -779,7 +785,7 @@ def main():
             "clocks": clk,
             "e2e": {"value": e_value, "unit": "solves/s", "h2d_bytes_per_step": r["e2e_bytes"],
                     "d2h_bytes_per_step": r["e2e_bytes"]},
-            "gpu_launches": r["launches_per_step"] * args.steps,
+            "gpu_launches": r["launches"] * world if world > 1 else r["launches"],
             "roofline": roof,
             "kernels": kernels,
             "cpu_baseline": cpu,

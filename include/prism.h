@@ -365,7 +365,10 @@ double prism_sqrt_flops_per_iter(int64_t n, int degree, int sketch_size);
 
 /* ---- measurement (bench.py) ---------------------------------------------------- */
 
-/* Kernel launches issued by the most recent prism_polar / prism_sqrt_invsqrt on h. */
+/* Kernel launches of the library issued by the calls on h since the previous
+ * prism_launch_count (which it resets): per graph solve, the launches outside its loop plus
+ * the launches per iteration times the iterations of that plan's most recent solve; per
+ * row-block call, the launches it issued.  Synchronises the device. */
 int64_t prism_launch_count(prism_handle h);
 /*
  * Per-kernel-kind device timing.  When enabled, every launch group is bracketed

@@ -1181,8 +1181,14 @@ struct prism_handle_s {
   double acc_ms[kKinds] = {0};
   long long acc_launches[kKinds] = {0};
   cudaStream_t cap = nullptr;               // private stream for graph capture
-  int* last_iter = nullptr;                 // device iteration counter of the last solve
-  int last_fixed = 0, last_per_iter = 0;
+  // launch ledger since the last prism_launch_count: per solve (device iteration counter of its
+  // plan, launches outside the loop, launches per iteration); direct-launch loops record their
+  // host-counted total with a null counter
+  struct LedgerEntry {
+    const int* iter;
+    long long fixed, per_iter;
+  };
+  std::vector<LedgerEntry> ledger;
   int* h_flag = nullptr;                    // pinned host flag (profiling path)
   // host-buffer path (prism_polar_host / prism_sqrt_invsqrt_host): device staging
   // slots, upload / solve / download on three internal streams, ordered by events, so
@@ -1578,9 +1584,8 @@ static prism_status run_solve(prism_handle h, const Request& r0, const prism_rep
     else PRISM_CK(launch_k(k_finalize<2>, dim3(S.n_out_tiles), dim3(256), 0, st, 1, S));
   }
   if (rep) PRISM_CK(launch_k(k_report, dim3(std::max(1, std::min(64, (B * (M + 1) + 255) / 256))), dim3(256), 0, st, 1, S));
-  h->last_iter = P->d_iter;
-  h->last_fixed = 4 + (P->unfolded ? 1 : 0) + (rep ? 1 : 0);
-  h->last_per_iter = P->per_iter_launches;
+  if (h->ledger.size() < (1u << 16))
+    h->ledger.push_back({P->d_iter, 4 + (P->unfolded ? 1 : 0) + (rep ? 1 : 0), P->per_iter_launches});
   PRISM_CK(cudaGetLastError());
   return PRISM_OK;
 }
@@ -1978,13 +1983,27 @@ prism_status prism_sign(prism_handle h, int batch, const int64_t* n, const void*
 }
 
 int64_t prism_launch_count(prism_handle h) {
-  // fixed launches + per-iteration launches x iterations executed (reads the device
-  // counter of the last solve: synchronises the device)
+  // per ledger entry: fixed launches + per-iteration launches x iterations executed (the
+  // device counter of that plan's most recent solve: synchronises the device)
   if (!h) return -1;
-  if (!h->last_iter) return 0;
-  int k = 0;
-  if (cudaMemcpy(&k, h->last_iter, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
-  return (int64_t)h->last_fixed + (int64_t)h->last_per_iter * k;
+  if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+  std::map<const int*, int> iters;
+  int64_t total = 0;
+  for (const auto& e : h->ledger) {
+    int k = 0;
+    if (e.iter) {
+      auto it = iters.find(e.iter);
+      if (it == iters.end()) {
+        if (cudaMemcpy(&k, e.iter, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+        iters[e.iter] = k;
+      } else {
+        k = it->second;
+      }
+    }
+    total += e.fixed + e.per_iter * (int64_t)k;
+  }
+  h->ledger.clear();
+  return total;
 }
 
 prism_status prism_profile_enable(prism_handle h, int enable) {
@@ -2080,8 +2099,10 @@ prism_status prism_polar_rowblock_tr(prism_handle h, const prism_transport* tr, 
     const bool sketched = o->fit == PRISM_FIT_SKETCHED;
     const int nt = (int)((n + 63) / 64);
     cudaEvent_t ev_stop = prism::handle_event(h, 8);
+    long long nl = 5;   // launches of this call (the launch ledger, prism_launch_count)
     for (int k = 0; k <= M; ++k) {
       NvtxRange nv("prism:rowblock iteration");
+      nl += ng + 5 + (sketched ? P->n_chain : 0) + (P->rb1[0].probs.size() ? 1 : 0);
       const int t = k & 1;
       // 1. packed partial Gram, all-reduced panel group by panel group (on the aux stream,
       //    overlapping the next group's launch; the Gram grid leaves SMs to the collective)
@@ -2134,6 +2155,8 @@ prism_status prism_polar_rowblock_tr(prism_handle h, const prism_transport* tr, 
     else PRISM_CK(launch_k(k_finalize<2>, dim3(S.n_out_tiles), dim3(256), 0, st, 1, S));
     if (rep) PRISM_CK(launch_k(k_report, dim3(1), dim3(256), 0, st, 1, S));
     PRISM_CK(cudaGetLastError());
+    nl += 1 + (rep ? 1 : 0);
+    if (h->ledger.size() < (1u << 16)) h->ledger.push_back({nullptr, nl, 0});
     return PRISM_OK;
   } catch (...) {
     return fail(PRISM_ERR_INTERNAL, "exception in prism_polar_rowblock");
