@@ -445,3 +445,31 @@ def test_large_bf16_batches_equal_single_solves(B):
         torch.cuda.synchronize()
         assert torch.equal(Qs[0], Qb[i]), i
         assert int(rs["iters"][0]) == iters[i]
+
+
+@pytest.mark.gpu
+def test_flip_compaction_early_square_together():
+    """A 12-matrix BF16 batch takes every scheduling path at once: folded parity flip (repeat
+    solves), per-iteration tile compaction (>= 8 matrices) and the early square (<= 16):
+    three repeats must give the bits and iteration counts of the single solves."""
+    shapes = [(256, 192), (192, 640), (512, 512), (130, 66), (320, 320), (96, 400)] * 2
+    mats = []
+    for i, (m, n) in enumerate(shapes):
+        a = W.logspaced(m, n, 1e-3, seed=880 + i) if i % 2 else W.gaussian(m, n, seed=880 + i)
+        mats.append(torch.tensor(a).to(torch.bfloat16).cuda())
+    kw = dict(degree=5, tol=3e-2, max_iters=25, precision="bf16")
+    ids = list(range(len(mats)))
+    single = []
+    for i, t in enumerate(mats):
+        Q, rep = P.polar([t], matrix_ids=[i], **kw)
+        torch.cuda.synchronize()
+        single.append((Q[0].clone(), int(rep["iters"][0])))
+    assert len({k for _, k in single}) >= 2
+    h = P.Handle()
+    outs = [torch.empty_like(t) for t in mats]
+    for _ in range(3):
+        Q, rep = P.polar(mats, out=outs, matrix_ids=ids, handle=h, **kw)
+        torch.cuda.synchronize()
+        for i, (q, k) in enumerate(single):
+            assert torch.equal(Q[i], q), i
+            assert int(rep["iters"][i]) == k
