@@ -473,3 +473,17 @@ def test_flip_compaction_early_square_together():
         for i, (q, k) in enumerate(single):
             assert torch.equal(Q[i], q), i
             assert int(rep["iters"][i]) == k
+
+
+@pytest.mark.gpu
+def test_launch_ledger_counts_every_solve_since_the_last_read():
+    mats = [torch.tensor(W.gaussian(300, 200, seed=960)).to(torch.bfloat16).cuda()]
+    kw = dict(degree=5, tol=3e-2, max_iters=20, precision="bf16")
+    h = P.Handle()
+    P.polar(mats, handle=h, **kw)
+    one = h.launch_count()
+    assert one > 10
+    assert h.launch_count() == 0                       # the read resets the ledger
+    for _ in range(3):
+        P.polar(mats, handle=h, **kw)
+    assert h.launch_count() == 3 * one                 # same plan, same iterations
