@@ -47,7 +47,7 @@ enum EpiMode : int { EPI_RESID = 0, EPI_POLY = 1, EPI_APPLY = 2, EPI_STORE = 3, 
 //        j < q, and CHI_L<q> for j = q: <V_i, V_j>, V_0 = K1, V_i = -C(q,i) Z_i
 //   Chebyshev inverse (R stored transposed, so a pass gives the rows of W R):
 //        CHC_P1 S R -> next;  CHC_P2 S R^2 keep -> next;  CHC_P3 S R^3: U = S R^2,
-//        V = U - S R^3, <U,U>, <U,V>, <V,V>
+//        V = U - S R^3 = U G (G = I - R) by the diagonal trick, <U,U>, <U,V>, <V,V>
 enum ChainPassCode : int { CH2_P1 = 0, CH2_P2, CH2_P3, CH2_P4, CH2_P5, CH1_P1, CH1_P2, CH1_P3,
                            CHI_K2, CHI_L1, CHI_L2, CHI_L3, CHI_L4, CHC_P1, CHC_P2, CHC_P3, CH_NCODES };
 constexpr int kChainG = 15;   // doubles per 32-row group in chain_part (<V_i,V_j>, i <= j <= 4)
@@ -159,6 +159,7 @@ struct GemmProblem {
   const void* Rg;        // R (for R_ii), compute dtype (+ R_lo in 3xTF32)
   const void* Rg_lo;
   void* Wn;              // next pass B operand: [2w'][ldS] hi rows then lo rows, compute dtype
+  const void* Wi;        // this pass's input W (same layout; CHC_P3 reads the values the MMA used)
   float* keep;           // [4][M][p] fp32 kept chain columns
   double* chain_part;    // [row groups][kChainG] per-group <Va,Vb> partials
   long long ldS, ldr;
@@ -873,8 +874,9 @@ __device__ __forceinline__ void store_w(const GemmProblem& P, int c, int wn, int
 // read through a reference every field would be reloaded after each store.
 struct ChainPre {
   GemmProblem P;
-  float rii, gii;     // pass 1: R_ii and G_ii
+  float rii, gii;     // pass 1 (and CHC_P3): R_ii and G_ii
   float v[32];        // pass 1: S[c][i] (c < 8); last pass: kept columns kv[slot][c]
+                      // (CHC_P3: kv[0] = U, v[8 + c] / v[16 + c] = the input's hi / lo W[c][i])
 };
 
 template <class Cfg, int PASS>
@@ -889,11 +891,13 @@ __device__ __forceinline__ void chain_prefetch(const GemmProblem& Pin, int i, in
   for (int u = 0; u < 32; ++u) pre.v[u] = 0.f;
   pre.rii = pre.gii = 0.f;
   if (!valid) return;
-  if constexpr (PASS == CH2_P1 || PASS == CH1_P1) {
+  if constexpr (PASS == CH2_P1 || PASS == CH1_P1 || PASS == CHC_P3) {
     if constexpr (Cfg::KIND == 0) pre.rii = __bfloat162float(static_cast<const __nv_bfloat16*>(P.Rg)[(long long)i * P.ldr + i]);
     else pre.rii = static_cast<const float*>(P.Rg)[(long long)i * P.ldr + i] +
                    (P.Rg_lo ? static_cast<const float*>(P.Rg_lo)[(long long)i * P.ldr + i] : 0.f);
     pre.gii = P.gdiag[i];
+  }
+  if constexpr (PASS == CH2_P1 || PASS == CH1_P1) {
 #pragma unroll
     for (int c = 0; c < 8; ++c) pre.v[c] = (c >= c0 && c < c1) ? __ldg(P.S + (long long)c * P.ldS + i) : 0.f;
   } else if constexpr (chain_is_last(PASS)) {
@@ -915,6 +919,21 @@ __device__ __forceinline__ void chain_prefetch(const GemmProblem& Pin, int i, in
 #pragma unroll
         for (int c = 0; c < 8; ++c)
           pre.v[sl * 8 + c] = (sl < ns && c >= c0 && c < c1) ? __ldcg(P.keep + ((long long)sl * M + i) * p + c) : 0.f;
+    }
+    if constexpr (PASS == CHC_P3) {   // the hi / lo input rows the MMA multiplied (written by CHC_P2)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        if (c < c0 || c >= c1 || c >= p) continue;
+        if constexpr (Cfg::KIND == 0) {
+          const __nv_bfloat16* w = static_cast<const __nv_bfloat16*>(P.Wi);
+          pre.v[8 + c] = __bfloat162float(w[(long long)c * P.ldS + i]);
+          pre.v[16 + c] = __bfloat162float(w[(long long)(p + c) * P.ldS + i]);
+        } else {
+          const float* w = static_cast<const float*>(P.Wi);
+          pre.v[8 + c] = __ldcg(w + (long long)c * P.ldS + i);
+          pre.v[16 + c] = __ldcg(w + (long long)(p + c) * P.ldS + i);
+        }
+      }
     }
   }
 }
@@ -1009,12 +1028,19 @@ __device__ __forceinline__ void epi_chain(const ChainPre& pre, int i, int grp, c
       }
       if constexpr (pass == CHC_P2) keep_row(keep + (long long)i * p, o, p);
     } else if constexpr (pass == CHC_P3) {
+      // V = U - U R = U G with G = I - R: R ~ I in the compute dtype loses G_ii, so the
+      // diagonal term is replaced exactly as for Q in pass 1: V_i = G_ii U_i - (UR_i - R_ii U_i),
+      // per hi / lo half (the products the MMA formed are exact in fp32, so subtracting them
+      // leaves the off-diagonal sum)
       const float(&kv)[4][8] = *reinterpret_cast<const float(*)[4][8]>(pre.v);
+      const float rii = pre.rii, gii = pre.gii;
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         if (c < c0 || c >= c1) continue;
+        const float uh = pre.v[8 + c], ul = pre.v[16 + c];
+        const float off = (col[c * cs] - uh * rii) + (col[(w + c) * cs] - ul * rii);
         const double u = (double)kv[0][c];
-        const double v = u - (double)o[c];
+        const double v = (double)gii * ((double)uh + (double)ul) - (double)off;
         g[0] += u * u; g[1] += u * v; g[2] += v * v;
       }
     } else if constexpr (pass >= CHI_L1 && pass <= CHI_L4) {

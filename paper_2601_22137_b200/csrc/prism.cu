@@ -763,6 +763,7 @@ prism_status build_plan(const Request& r, Plan& P) {
         c.p.Rg_lo = D.R_lo;
         c.p.gdiag = D.gdiag;
         c.p.Wn = static_cast<char*>(D.W[(j + 1) % 2]) + wch;
+        c.p.Wi = static_cast<char*>(D.W[j % 2]) + wch;
         c.p.keep = D.keep + (size_t)4 * s * pw * ch;
         c.p.chain_part = D.chain_part + (size_t)kChainG * ((s + 31) / 32) * ch;
         c.p.ldS = D.ldS;
