@@ -487,3 +487,24 @@ def test_launch_ledger_counts_every_solve_since_the_last_read():
     for _ in range(3):
         P.polar(mats, handle=h, **kw)
     assert h.launch_count() == 3 * one                 # same plan, same iterations
+
+
+@pytest.mark.gpu
+def test_gpt2_batch_host_path_equals_device_path():
+    """The e2e entry point on the benchmarked GPT-2 batch (48 matrices: tile compaction, parity
+    flip, three staging slots in rotation): every call's outputs equal the device path's bits."""
+    shapes = W.gpt2_small_shapes()
+    mats_np = W.muon_batch(shapes, seed=1, kind="mixed")
+    host = [torch.tensor(a).to(torch.bfloat16).pin_memory() for a in mats_np]
+    kw = dict(degree=5, tol=3e-2, max_iters=20, precision="bf16", matrix_ids=list(range(len(host))))
+    ref, _ = P.polar([t.cuda() for t in host], **kw)
+    torch.cuda.synchronize()
+    ref = [r.cpu() for r in ref]
+    h = P.Handle()
+    outs = [[torch.empty_like(t).pin_memory() for t in host] for _ in range(4)]
+    for o in outs:
+        P.polar_host(host, out=o, handle=h, **kw)
+    torch.cuda.synchronize()
+    for o in outs:
+        for x, y in zip(o, ref):
+            assert torch.equal(x, y)
